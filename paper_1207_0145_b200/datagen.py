@@ -1,0 +1,92 @@
+"""Seeded input generators for the join benchmark configurations.
+
+These are the synthetic stand-ins for the paper's datasets (PAPER.md
+290-310; the paper's data is synthetic, so nothing is missing).  All draw
+from numpy's PCG64, seeded explicitly, so identical arguments give
+bit-identical relations:
+
+* ``gen_fk``        -- BASELINE.json configs 1-3 and 5: R keys a
+  seeded permutation of 1..|R|, S keys iid uniform in [1, |R|], payloads
+  uniform in [0, 2^32).  R draws from PCG64(2*seed), S from PCG64(2*seed+1),
+  the reference harness's seed convention (bench.py:142-144).
+* ``gen_skewed_8020`` -- restates the reference generator
+  (datagen.py:65-84): 80 % of the keys uniform in the hot 20 % tail of the
+  domain (high or low end), the rest uniform in the remainder.  Config 4 uses
+  R = low, S = high.  tests/test_host_logic.py checks it reproduces the
+  reference's arrays bit for bit (fingerprints in tests/golden/golden.json).
+* ``gen_uniform`` / ``gen_location_skew`` -- datagen.py:58-62, 87-105.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .core import ConfigurationError, KeyDomain, Relation
+
+PAYLOAD_UPPER = 1 << 32
+
+
+def _rng(seed) -> np.random.Generator:
+    return np.random.Generator(np.random.PCG64(seed))
+
+
+def gen_fk(n_r: int, n_s: int, seed: int = 0) -> tuple:
+    """Foreign-key join inputs: (R, S, KeyDomain(1, n_r + 1))."""
+    rr = _rng(2 * seed)
+    r_keys = rr.permutation(n_r).astype(np.uint64)
+    r_keys += np.uint64(1)
+    r_pays = rr.integers(0, PAYLOAD_UPPER, n_r, dtype=np.uint64)
+    rs = _rng(2 * seed + 1)
+    s_keys = rs.integers(1, n_r + 1, n_s, dtype=np.uint64)
+    s_pays = rs.integers(0, PAYLOAD_UPPER, n_s, dtype=np.uint64)
+    return Relation(r_keys, r_pays), Relation(s_keys, s_pays), KeyDomain(1, n_r + 1)
+
+
+def gen_uniform(n: int, dom: KeyDomain, seed: int = 0) -> Relation:
+    rng = _rng(seed)
+    keys = rng.integers(dom.lower, dom.upper, n, dtype=np.uint64)
+    return Relation(keys, rng.integers(0, PAYLOAD_UPPER, n, dtype=np.uint64))
+
+
+def gen_skewed_8020(n: int, dom: KeyDomain, direction: str, seed: int = 0) -> Relation:
+    """80 % of keys in the 20 % high (or low) tail, uniform within segments."""
+    if direction not in ("high", "low"):
+        raise ConfigurationError("direction must be 'high' or 'low'")
+    rng = _rng(seed)
+    cut = dom.lower + (dom.width * 4) // 5
+    hot = rng.random(n) < 0.8
+    n_hot = int(np.count_nonzero(hot))
+    keys = np.empty(n, np.uint64)
+    if direction == "high":
+        keys[hot] = rng.integers(cut, dom.upper, n_hot, dtype=np.uint64)
+        keys[~hot] = rng.integers(dom.lower, cut, n - n_hot, dtype=np.uint64)
+    else:
+        edge = dom.lower + dom.width - (dom.width * 4) // 5
+        keys[hot] = rng.integers(dom.lower, edge, n_hot, dtype=np.uint64)
+        keys[~hot] = rng.integers(edge, dom.upper, n - n_hot, dtype=np.uint64)
+    return Relation(keys, rng.integers(0, PAYLOAD_UPPER, n, dtype=np.uint64))
+
+
+def gen_location_skew(rel: Relation, t: int, seed: int = 0) -> Relation:
+    """Chunk i of t holds the i-th key quantile, shuffled inside the chunk."""
+    if t < 1:
+        raise ConfigurationError("t must be >= 1")
+    order = np.argsort(rel.keys, kind="stable")
+    keys = rel.keys[order].copy()
+    pays = rel.payloads[order].copy()
+    rng = _rng([seed, 0x10C])
+    n = rel.cardinality
+    base, rem = divmod(n, t)
+    start = 0
+    for i in range(t):
+        size = base + (1 if i < rem else 0)
+        perm = rng.permutation(size)
+        keys[start:start + size] = keys[start:start + size][perm]
+        pays[start:start + size] = pays[start:start + size][perm]
+        start += size
+    return Relation(keys, pays)
+
+
+def gen_negcorr(n_r: int, n_s: int, dom: KeyDomain, seed: int = 0) -> tuple:
+    """Config 4: R skewed low, S skewed high (negatively correlated)."""
+    return gen_skewed_8020(n_r, dom, "low", seed=2 * seed), gen_skewed_8020(n_s, dom, "high", seed=2 * seed + 1)
