@@ -1,0 +1,168 @@
+/*
+ * mpsm_b200.h -- C ABI of the B200-native MPSM join path.
+ *
+ * This is the drop-in boundary: plain pointers, sizes and status codes, no
+ * torch or CUDA runtime types in the signatures (streams travel as void*,
+ * they are cudaStream_t).  Every pointer argument named d_* or documented as
+ * "device" is device memory owned by the caller; workspace is caller-
+ * allocated after a *_workspace_bytes() query (two-phase, CUB style).
+ * All compute calls are stream-ordered and asynchronous unless stated.
+ *
+ * Each entry point replaces one operator of the reference package
+ * /root/reference/pkg/src/mpsm (cited per function).  The reference operator
+ * layer is its numba kernel module (_kernels.py); its "FFI" is numba's
+ * njit call boundary: 1-D contiguous uint64 arrays + scalar u64/int64 args,
+ * results as ints/tuples and in-place mutation of output arrays
+ * (SURVEY.md 8(b)).  INTEGRATION.md shows the ctypes binding
+ * (paper_1207_0145_b200/_lib.py) a maintainer adds on the reference side.
+ */
+#ifndef MPSM_B200_H
+#define MPSM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (map to the reference's exceptions, core.py:26-49) ---- */
+#define MPSM_OK 0
+#define MPSM_ERR_DOMAIN (-1)   /* DomainError                                   */
+#define MPSM_ERR_INTERNAL (-2) /* InternalConsistencyError                      */
+#define MPSM_ERR_CONFIG (-3)   /* ConfigurationError                            */
+#define MPSM_ERR_CUDA (-4)     /* RuntimeError (CUDA / NCCL failure)            */
+#define MPSM_ERR_CAP (-5)      /* MaterializeCapExceeded                        */
+#define MPSM_ERR_ARG (-6)      /* ValueError (bad argument)                     */
+
+/* query modes (core.py:23) */
+#define MPSM_MODE_AGGREGATE_MAX 0
+#define MPSM_MODE_COUNT 1
+#define MPSM_MODE_MATERIALIZE 2
+
+/* per (private run, public run) result record written by mpsm_join_pairs,
+ * MPSM_PAIR_FIELDS uint64 words each */
+#define MPSM_PAIR_COUNT 0    /* matched pairs                                  */
+#define MPSM_PAIR_BEST 1     /* max(r_pay + s_pay) mod 2^64, valid iff count>0 */
+#define MPSM_PAIR_CHECKSUM 2 /* sum splitmix64(r_pay ^ rotl(s_pay,17))         */
+#define MPSM_PAIR_START 3    /* lower bound of the private run's first key     */
+#define MPSM_PAIR_PROBES 4   /* interpolation-search positions read            */
+#define MPSM_PAIR_END 5      /* upper bound of the private run's last key      */
+#define MPSM_PAIR_EXAMINED 6 /* distinct public positions the merge scan reads */
+#define MPSM_PAIR_EMITTED 7  /* pairs written (materialize)                    */
+#define MPSM_PAIR_FIELDS 8
+
+/* a sorted run or a relation chunk in device memory */
+typedef struct {
+    const uint64_t* keys;
+    const uint64_t* pays;
+    int64_t n;
+} mpsm_run_t;
+
+/* ------------------------------------------------------------ library ---- */
+int mpsm_version(void);
+/* last error message of the calling thread ("" if none) */
+const char* mpsm_last_error(void);
+/* select the device and check it is sm_100 (B200); returns SM count or <0 */
+int mpsm_device_init(int device);
+/* number of kernels this library launched (process-wide counter) */
+uint64_t mpsm_launch_count(void);
+/* per-kernel CUDA-event timing: enable (and reset) / read the summed device
+ * time and launch count of one kernel family ("onesweep", "upfront_hist",
+ * "scatter", "radix_histogram", "merge", "merge_partition", ...) */
+int mpsm_profile_enable(int on);
+int mpsm_profile_read(const char* name, double* total_ms, uint64_t* launches);
+
+/* ---------------------------------------------------------- run sort ----
+ * Replaces _kernels.three_phase_sort (_kernels.py:217-244) as called by
+ * sorter.sort_run_with_stats (sorter.py:91-100): sort (key, payload) pairs
+ * by key.  Reads in_*, leaves the sorted run in out_* (in may equal out);
+ * tmp_* is a ping-pong buffer of n elements.  LSD radix over the width_bits
+ * significant bits of (key - lower) (onesweep: one key-histogram sweep, then
+ * one decoupled-look-back scatter pass per digit).  Keys outside
+ * [lower, lower + span_m1] are reported through *d_bad (atomicMin of the
+ * index; initialise to UINT64_MAX) -- the reference returns -1 from the kernel
+ * and raises DomainError (sorter.py:97-98).  Stable (equal keys keep input
+ * order), which the reference does not promise. */
+int mpsm_sort_workspace_bytes(int64_t n, int width_bits, size_t* bytes);
+int mpsm_sort_pairs(const uint64_t* in_keys, const uint64_t* in_pays, int64_t n, uint64_t lower,
+                    uint64_t span_m1, int width_bits, uint64_t* out_keys, uint64_t* out_pays,
+                    uint64_t* tmp_keys, uint64_t* tmp_pays, void* workspace, size_t ws_bytes,
+                    unsigned long long* d_bad, void* stream);
+
+/* ------------------------------------------------- radix histogram ----
+ * Replaces _kernels.radix_histogram (_kernels.py:247-259) / partition.
+ * build_radix_histogram (partition.py:110-122): d_counts[(key-lower)>>shift]
+ * += 1 for nbuckets buckets (d_counts int64, accumulated, not zeroed);
+ * out-of-domain keys -> *d_bad (atomicMin of index). */
+int mpsm_radix_histogram(const uint64_t* keys, int64_t n, uint64_t lower, uint64_t span_m1, int shift,
+                         int nbuckets, int64_t* d_counts, unsigned long long* d_bad, void* stream);
+
+/* --------------------------------------------------- partition scatter ----
+ * Replaces _kernels.scatter_chunk (_kernels.py:262-284) / partition.scatter
+ * (partition.py:233-276): each tuple goes to partition d_sp[(key-lower)>>shift]
+ * at the worker's cursor for that partition (d_cursors: int64[npart] absolute
+ * arena offsets).  Order within each (worker, partition) region is the input
+ * order, i.e. the exact arena layout of the reference.  d_written (int64
+ * [npart], accumulated) receives how many tuples went to each partition so
+ * the caller can check it against the histogram (InternalConsistencyError). */
+int mpsm_scatter_workspace_bytes(int64_t n, int npart, size_t* bytes);
+int mpsm_scatter_chunk(const uint64_t* keys, const uint64_t* pays, int64_t n, uint64_t lower, int shift,
+                       const int32_t* d_sp, int nbuckets, int npart, const int64_t* d_cursors,
+                       uint64_t* arena_keys, uint64_t* arena_pays, int64_t* d_written, void* workspace,
+                       size_t ws_bytes, void* stream);
+
+/* -------------------------------------------- interpolation search ----
+ * Replaces _kernels.interp_lower_bound (_kernels.py:287-337) used by
+ * engine.interpolation_search (engine.py:124-128): for each target, the
+ * first index with key >= target and the number of positions probed (the
+ * same fp64 probe rule, so identical probe counts). */
+int mpsm_interp_lower_bound(const uint64_t* keys, int64_t n, const uint64_t* d_targets, int64_t ntargets,
+                            int64_t* d_index, int64_t* d_probes, void* stream);
+
+/* ---------------------------------------------------------- merge join ----
+ * Replaces engine._join_private_run (engine.py:228-276) over all workers,
+ * i.e. _kernels.interp_lower_bound + _kernels.merge_join_run
+ * (_kernels.py:340-408) for every (private run i, public run j) pair:
+ * window search, merge-path tiling over all pairs, merge with duplicate
+ * cross products, fused COUNT / MAX(r+s) / checksum reduction.
+ * priv / pub are HOST arrays of run descriptors pointing to device memory.
+ * d_pairs: uint64[n_priv * n_pub * MPSM_PAIR_FIELDS] (zeroed by the call).
+ * swap != 0: the private side is the reference's S (role swap, engine.py
+ * 69-78, 217-218), so pairs are oriented (public, private) for the checksum
+ * and materialized output.
+ * mode MPSM_MODE_MATERIALIZE additionally writes matched pairs as
+ * (r_pay, s_pay) rows into d_out (uint64[2*cap], row-major); call once with
+ * d_out == NULL to obtain counts, then again with an output buffer.  */
+int mpsm_join_workspace_bytes(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub,
+                              size_t* bytes);
+int mpsm_join_pairs(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub, int swap, int mode,
+                    uint64_t* d_out, int64_t cap, uint64_t* d_pairs, void* workspace, size_t ws_bytes,
+                    void* stream);
+
+/* ------------------------------------------------ splitter search ----
+ * Replaces skew._minmax_contiguous (skew.py:180-273) as used by
+ * skew.compute_splitters (skew.py:287-315): split n buckets into t
+ * contiguous ranges minimising the largest
+ *   cost(a,b) = |R_ab| log2|R_ab| + t |R_ab| + (edge_cdf[b] - edge_cdf[a])
+ * with the lexicographically smallest bounds.  Host function.
+ * prefix: int64[n+1] bucket-count prefix sums; edge_cdf: double[n+1];
+ * cand: the bound candidates computed by the caller with numpy exactly as
+ * the reference does (sorted unique batch costs when n <= 256, else the n
+ * single-bucket costs) so the floating-point values are bit-identical.
+ * out_bounds: int64[t+1].  Returns MPSM_ERR_CONFIG if t > n. */
+int mpsm_minmax_contiguous(int64_t n, int t, const int64_t* prefix, const double* edge_cdf,
+                           const double* cand, int64_t ncand, int64_t* out_bounds);
+
+/* ------------------------------------------------ multi-GPU helpers ----
+ * CUDA IPC so a rank can merge against peer ranks' public runs with NVLink
+ * peer loads (the paper's sequential remote-NUMA reads, engine.py:249-260).
+ * handle buffers are 64 bytes. */
+int mpsm_ipc_get_handle(const void* d_ptr, void* handle64);
+int mpsm_ipc_open_handle(const void* handle64, void** d_ptr);
+int mpsm_ipc_close_handle(void* d_ptr);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPSM_B200_H */

@@ -1,0 +1,125 @@
+// abi.cu -- library-level entry points of the C ABI (include/mpsm_b200.h):
+// version, error reporting, device selection, launch accounting, CUDA IPC.
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace mpsm {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+std::atomic<uint64_t>& launch_counter() {
+    static std::atomic<uint64_t> c{0};
+    return c;
+}
+
+struct ProfState {
+    std::mutex mu;
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    std::map<std::string, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> rec;
+};
+
+static ProfState& prof() {
+    static ProfState p;
+    return p;
+}
+
+bool profiling_enabled() { return prof().on; }
+
+cudaEvent_t profile_event() {
+    ProfState& p = prof();
+    std::lock_guard<std::mutex> g(p.mu);
+    if (p.used == p.pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        p.pool.push_back(e);
+    }
+    return p.pool[p.used++];
+}
+
+void profile_record(const char* name, cudaEvent_t a, cudaEvent_t b) {
+    ProfState& p = prof();
+    std::lock_guard<std::mutex> g(p.mu);
+    p.rec[name].push_back({a, b});
+}
+
+}  // namespace mpsm
+
+using namespace mpsm;
+
+extern "C" int mpsm_profile_enable(int on) {
+    ProfState& p = prof();
+    std::lock_guard<std::mutex> g(p.mu);
+    p.on = on != 0;
+    p.used = 0;
+    p.rec.clear();
+    return MPSM_OK;
+}
+
+extern "C" int mpsm_profile_read(const char* name, double* total_ms, uint64_t* launches) {
+    ProfState& p = prof();
+    std::lock_guard<std::mutex> g(p.mu);
+    double tot = 0;
+    uint64_t cnt = 0;
+    auto it = p.rec.find(name);
+    if (it != p.rec.end()) {
+        for (auto& ev : it->second) {
+            MPSM_TRY(cuda_status(cudaEventSynchronize(ev.second), "cudaEventSynchronize"));
+            float ms = 0;
+            MPSM_TRY(cuda_status(cudaEventElapsedTime(&ms, ev.first, ev.second), "cudaEventElapsedTime"));
+            tot += ms;
+            ++cnt;
+        }
+    }
+    *total_ms = tot;
+    *launches = cnt;
+    return MPSM_OK;
+}
+
+extern "C" int mpsm_version(void) { return 1; }
+
+extern "C" const char* mpsm_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" uint64_t mpsm_launch_count(void) { return launch_counter().load(); }
+
+extern "C" int mpsm_device_init(int device) {
+    MPSM_TRY(cuda_status(cudaSetDevice(device), "cudaSetDevice"));
+    cudaDeviceProp prop;
+    MPSM_TRY(cuda_status(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties"));
+    if (prop.major != 10 || prop.minor != 0) {
+        set_error(std::string("device is sm_") + std::to_string(prop.major) + std::to_string(prop.minor) +
+                  "; this library is built for sm_100a (B200) only");
+        return MPSM_ERR_CONFIG;
+    }
+    return prop.multiProcessorCount;
+}
+
+extern "C" int mpsm_ipc_get_handle(const void* d_ptr, void* handle64) {
+    cudaIpcMemHandle_t h;
+    MPSM_TRY(cuda_status(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)), "cudaIpcGetMemHandle"));
+    static_assert(sizeof(h) == 64, "IPC handle size");
+    std::memcpy(handle64, &h, 64);
+    return MPSM_OK;
+}
+
+extern "C" int mpsm_ipc_open_handle(const void* handle64, void** d_ptr) {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, 64);
+    return cuda_status(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+}
+
+extern "C" int mpsm_ipc_close_handle(void* d_ptr) {
+    return cuda_status(cudaIpcCloseMemHandle(d_ptr), "cudaIpcCloseMemHandle");
+}

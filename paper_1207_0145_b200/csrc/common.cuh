@@ -1,0 +1,147 @@
+// common.cuh -- shared helpers for the sm_100a MPSM kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdio>
+#include <string>
+
+#include "../../include/mpsm_b200.h"
+
+namespace mpsm {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+std::atomic<uint64_t>& launch_counter();
+
+inline int cuda_status(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return MPSM_OK;
+    set_error(std::string(what) + ": " + cudaGetErrorString(e));
+    return MPSM_ERR_CUDA;
+}
+
+// call after every kernel launch
+inline int check_launch(const char* name) {
+    launch_counter().fetch_add(1, std::memory_order_relaxed);
+    return cuda_status(cudaGetLastError(), name);
+}
+
+#define MPSM_TRY(expr)                 \
+    do {                               \
+        int _rc = (expr);              \
+        if (_rc != MPSM_OK) return _rc; \
+    } while (0)
+
+// optional per-kernel CUDA-event timing (mpsm_profile_enable / _read)
+bool profiling_enabled();
+void profile_record(const char* name, cudaEvent_t start, cudaEvent_t stop);
+cudaEvent_t profile_event();
+
+struct ProfScope {
+    const char* name;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ProfScope(const char* n, cudaStream_t s) : name(n), st(s) {
+        if (profiling_enabled()) {
+            a = profile_event();
+            b = profile_event();
+            cudaEventRecord(a, st);
+        }
+    }
+    ~ProfScope() {
+        if (a) {
+            cudaEventRecord(b, st);
+            profile_record(name, a, b);
+        }
+    }
+};
+
+inline int num_sms() {
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+// bump allocator over a caller-provided workspace
+struct Carve {
+    char* base;
+    size_t cap;
+    size_t off = 0;
+    bool ok = true;
+    template <class T>
+    T* take(size_t count) {
+        size_t bytes = align_up(count * sizeof(T));
+        if (off + bytes > cap) {
+            ok = false;
+            return nullptr;
+        }
+        T* p = reinterpret_cast<T*>(base + off);
+        off += bytes;
+        return p;
+    }
+};
+
+// ---------------------------------------------------------------- device
+__device__ __forceinline__ uint64_t rotl64(uint64_t x, unsigned r) { return (x << r) | (x >> (64 - r)); }
+
+// splitmix64 finalizer
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint64_t pair_hash(uint64_t r_pay, uint64_t s_pay) {
+    return mix64(r_pay ^ rotl64(s_pay, 17));
+}
+
+__device__ __forceinline__ uint64_t ld_volatile_u64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_volatile_u64(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// streaming loads/stores that do not allocate in L1
+__device__ __forceinline__ uint64_t ld_stream(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+template <class T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w > v ? w : v;
+    }
+    return v;
+}
+
+}  // namespace mpsm

@@ -1,0 +1,521 @@
+// merge_join.cu -- merge-path merge-join of sorted private runs against sorted
+// public runs with a fused COUNT / MAX(r+s) / checksum reduction (sm_100a).
+//
+// Replaces engine._join_private_run (/root/reference/pkg/src/mpsm/engine.py
+// 228-276) for all workers at once: per (private run i, public run j) the
+// interpolation search for the start (_kernels.interp_lower_bound,
+// _kernels.py:287-337) and the merge with mark/rewind over duplicate key
+// groups (_kernels.merge_join_run, _kernels.py:340-408).
+//
+// Pipeline (all stream-ordered, no host sync):
+//   k_windows    one thread per pair: S window [lb(r_first), ub(r_last)) by
+//                the reference's interpolation search (identical probe count)
+//                plus a binary search; "examined" statistic; tiles per pair
+//   k_tile_scan  exclusive scan of tiles over pairs
+//   k_partition  merge-path diagonal search for every tile boundary
+//   k_merge      persistent CTAs: load a tile of R and of the S window into
+//                shared memory, per-thread merge-path split, serial merge.
+//                For every S tuple the matching R tuples are the equal-key
+//                run that ends right before its merge position (ties merge R
+//                first), found by walking back -- the reference's
+//                cross-product of duplicate groups.  Per-thread accumulators
+//                are reduced per CTA and flushed with one atomic per pair.
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace mpsm {
+
+constexpr int MJ_THREADS = 256;
+constexpr int MJ_ITEMS = 9;  // odd: 64-bit smem accesses at stride ITEMS are conflict-free
+constexpr int MJ_TILE = MJ_THREADS * MJ_ITEMS;
+
+struct PairWin {
+    int64_t start, end;  // S window in public run j
+    int64_t tiles;       // merge tiles of this pair
+    int64_t tile_base;   // first global tile id
+};
+
+struct TileSplit {
+    int64_t i0, j0, i1, j1;  // R [i0,i1) and window-relative S [j0,j1)
+    int32_t pair;
+    int32_t pad;
+};
+
+// reference probe rule, _kernels.py:287-337 (fp64 probe position, bisect
+// after a step that fails to halve the window)
+__device__ int64_t interp_lb(const uint64_t* __restrict__ keys, int64_t n, uint64_t target, int64_t* probes_out) {
+    int64_t lo = 0, hi = n, probes = 0;
+    bool bisect_next = false;
+    while (lo < hi) {
+        int64_t width = hi - lo;
+        if (width == 1) {
+            ++probes;
+            if (keys[lo] < target) ++lo;
+            else hi = lo;
+            break;
+        }
+        uint64_t klo = keys[lo], khi = keys[hi - 1];
+        probes += 2;
+        if (klo >= target) {
+            hi = lo;
+            break;
+        }
+        if (khi < target) {
+            lo = hi;
+            break;
+        }
+        int64_t pos;
+        bool interp;
+        if (bisect_next || khi == klo) {
+            pos = lo + width / 2;
+            interp = false;
+        } else {
+            double frac = __ddiv_rn(__ull2double_rn(target - klo), __ull2double_rn(khi - klo));
+            pos = lo + (int64_t)__dmul_rn(frac, __ll2double_rn(width - 1));
+            if (pos <= lo) pos = lo + 1;
+            if (pos > hi - 1) pos = hi - 1;
+            interp = true;
+        }
+        ++probes;
+        if (keys[pos] < target) lo = pos + 1;
+        else hi = pos;
+        bisect_next = interp && (2 * (hi - lo) > width);
+    }
+    if (probes_out) *probes_out = probes;
+    return lo;
+}
+
+__device__ __forceinline__ int64_t upper_bound_u64(const uint64_t* __restrict__ keys, int64_t lo, int64_t hi,
+                                                   uint64_t target) {
+    while (lo < hi) {
+        int64_t mid = lo + ((hi - lo) >> 1);
+        if (keys[mid] <= target) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_interp_batch(const uint64_t* __restrict__ keys, int64_t n, const uint64_t* __restrict__ targets,
+                               int64_t nt, int64_t* __restrict__ idx, int64_t* __restrict__ probes) {
+    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    int64_t pr = 0;
+    int64_t r = interp_lb(keys, n, targets[t], &pr);
+    idx[t] = r;
+    if (probes) probes[t] = pr;
+}
+
+__global__ void k_windows(const mpsm_run_t* __restrict__ priv, int n_priv, const mpsm_run_t* __restrict__ pub,
+                          int n_pub, PairWin* __restrict__ win, uint64_t* __restrict__ out) {
+    int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n_priv * n_pub) return;
+    const mpsm_run_t r = priv[p / n_pub];
+    const mpsm_run_t s = pub[p % n_pub];
+    uint64_t* o = out + (size_t)p * MPSM_PAIR_FIELDS;
+    PairWin w{0, 0, 0, 0};
+    int64_t probes = 0, examined = 0;
+    if (r.n > 0 && s.n > 0) {
+        w.start = interp_lb(s.keys, s.n, r.keys[0], &probes);
+        w.end = upper_bound_u64(s.keys, w.start, s.n, r.keys[r.n - 1]);
+        // engine.py:253-260 / _kernels.py:405-407: distinct public positions
+        // read = up to the first key past the private maximum (or the end)
+        examined = (w.end < s.n - 1 ? w.end : s.n - 1) - w.start + 1;
+        if (examined < 0) examined = 0;
+        int64_t len = r.n + (w.end - w.start);
+        w.tiles = (w.end > w.start) ? (len + MJ_TILE - 1) / MJ_TILE : 0;
+    }
+    win[p] = w;
+    o[MPSM_PAIR_COUNT] = 0;
+    o[MPSM_PAIR_BEST] = 0;
+    o[MPSM_PAIR_CHECKSUM] = 0;
+    o[MPSM_PAIR_START] = (uint64_t)w.start;
+    o[MPSM_PAIR_PROBES] = (uint64_t)probes;
+    o[MPSM_PAIR_END] = (uint64_t)w.end;
+    o[MPSM_PAIR_EXAMINED] = (uint64_t)examined;
+    o[MPSM_PAIR_EMITTED] = 0;
+}
+
+__global__ void __launch_bounds__(1024) k_tile_scan(PairWin* __restrict__ win, int npairs, int64_t* __restrict__ total) {
+    __shared__ int64_t s[1024];
+    __shared__ int64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < npairs; base += 1024) {
+        int p = base + threadIdx.x;
+        int64_t v = p < npairs ? win[p].tiles : 0;
+        s[threadIdx.x] = v;
+        __syncthreads();
+        for (int off = 1; off < 1024; off <<= 1) {
+            int64_t a = threadIdx.x >= off ? s[threadIdx.x - off] : 0;
+            __syncthreads();
+            s[threadIdx.x] += a;
+            __syncthreads();
+        }
+        if (p < npairs) win[p].tile_base = carry + s[threadIdx.x] - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry += s[1023];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *total = carry;
+}
+
+// merge path: number of R elements among the first k of merge(R, W), ties R first
+__device__ __forceinline__ int64_t merge_path(const uint64_t* __restrict__ rk, int64_t nr,
+                                              const uint64_t* __restrict__ wk, int64_t nw, int64_t k) {
+    int64_t lo = k > nw ? k - nw : 0, hi = k < nr ? k : nr;
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (rk[mid] <= wk[k - 1 - mid]) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_partition(const mpsm_run_t* __restrict__ priv, const mpsm_run_t* __restrict__ pub, int n_pub,
+                            const PairWin* __restrict__ win, int npairs, const int64_t* __restrict__ total,
+                            TileSplit* __restrict__ splits) {
+    int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= *total) return;
+    // pair of this tile: last p with tile_base <= g and tiles > 0
+    int lo = 0, hi = npairs - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (win[mid].tile_base <= g) lo = mid;
+        else hi = mid - 1;
+    }
+    int p = lo;
+    while (win[p].tiles == 0 || win[p].tile_base + win[p].tiles <= g) --p;  // skip empty pairs sharing a base
+    const mpsm_run_t r = priv[p / n_pub];
+    const mpsm_run_t s = pub[p % n_pub];
+    const PairWin w = win[p];
+    const uint64_t* wk = s.keys + w.start;
+    const int64_t nw = w.end - w.start;
+    const int64_t L = r.n + nw;
+    const int64_t k0 = (g - w.tile_base) * MJ_TILE;
+    const int64_t k1 = (k0 + MJ_TILE < L) ? k0 + MJ_TILE : L;
+    TileSplit t;
+    t.i0 = merge_path(r.keys, r.n, wk, nw, k0);
+    t.j0 = k0 - t.i0;
+    t.i1 = merge_path(r.keys, r.n, wk, nw, k1);
+    t.j1 = k1 - t.i1;
+    t.pair = p;
+    t.pad = 0;
+    splits[g] = t;
+}
+
+struct MergeSmem {
+    uint64_t rk[MJ_TILE], rp[MJ_TILE];  // R part of the tile at [0, nR), W part at [nR, nR+nW)
+    uint64_t red[3][MJ_THREADS / 32];
+    TileSplit tile;
+};
+
+__device__ __forceinline__ void flush_pair(MergeSmem& sm, uint64_t* __restrict__ out, int pair, uint64_t count,
+                                           uint64_t best, uint64_t csum) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    count = warp_sum(count);
+    csum = warp_sum(csum);
+    best = warp_max_u64(best);
+    __syncthreads();
+    if (lane == 0) {
+        sm.red[0][warp] = count;
+        sm.red[1][warp] = best;
+        sm.red[2][warp] = csum;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t c = 0, b = 0, s = 0;
+        for (int w = 0; w < MJ_THREADS / 32; ++w) {
+            c += sm.red[0][w];
+            b = sm.red[1][w] > b ? sm.red[1][w] : b;
+            s += sm.red[2][w];
+        }
+        if (c) {
+            uint64_t* o = out + (size_t)pair * MPSM_PAIR_FIELDS;
+            atomicAdd((unsigned long long*)(o + MPSM_PAIR_COUNT), (unsigned long long)c);
+            atomicMax((unsigned long long*)(o + MPSM_PAIR_BEST), (unsigned long long)b);
+            atomicAdd((unsigned long long*)(o + MPSM_PAIR_CHECKSUM), (unsigned long long)s);
+        }
+    }
+}
+
+// MODE 0: aggregate into pair records; MODE 1: per-tile counts only;
+// MODE 2: emit pairs at tile_out[g] + thread offset
+template <int MODE>
+__global__ void __launch_bounds__(MJ_THREADS) k_merge(const mpsm_run_t* __restrict__ priv,
+                                                      const mpsm_run_t* __restrict__ pub, int n_pub,
+                                                      const PairWin* __restrict__ win,
+                                                      const TileSplit* __restrict__ splits,
+                                                      const int64_t* __restrict__ total, int swap,
+                                                      uint64_t* __restrict__ out_pairs,
+                                                      int64_t* __restrict__ tile_cnt, uint64_t* __restrict__ emit_out) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    MergeSmem& sm = *reinterpret_cast<MergeSmem*>(smem_raw);
+    __shared__ int64_t warp_cnt[MJ_THREADS / 32];
+    const int tid = threadIdx.x;
+    const int64_t ntiles = *total;
+    int cur_pair = -1;
+    uint64_t count = 0, best = 0, csum = 0;
+
+    for (int64_t g = blockIdx.x; g < ntiles; g += gridDim.x) {
+        __syncthreads();  // previous tile fully consumed
+        if (tid == 0) sm.tile = splits[g];
+        __syncthreads();
+        const TileSplit t = sm.tile;
+        if (MODE == 0 && t.pair != cur_pair) {
+            if (cur_pair >= 0) flush_pair(sm, out_pairs, cur_pair, count, best, csum);
+            cur_pair = t.pair;
+            count = best = csum = 0;
+        }
+        const mpsm_run_t r = priv[t.pair / n_pub];
+        const mpsm_run_t s = pub[t.pair % n_pub];
+        const int64_t wstart = win[t.pair].start;
+        const int nR = (int)(t.i1 - t.i0), nW = (int)(t.j1 - t.j0);
+        const uint64_t* __restrict__ gwk = s.keys + wstart + t.j0;
+        const uint64_t* __restrict__ gwp = s.pays + wstart + t.j0;
+        for (int x = tid; x < nR; x += MJ_THREADS) {
+            sm.rk[x] = ld_stream(r.keys + t.i0 + x);
+            sm.rp[x] = ld_stream(r.pays + t.i0 + x);
+        }
+        for (int x = tid; x < nW; x += MJ_THREADS) {
+            sm.rk[nR + x] = ld_stream(gwk + x);
+            sm.rp[nR + x] = ld_stream(gwp + x);
+        }
+        __syncthreads();
+        const uint64_t* Rk = sm.rk;
+        const uint64_t* Wk = sm.rk + nR;
+        const uint64_t* Rp = sm.rp;
+        const uint64_t* Wp = sm.rp + nR;
+        const int L = nR + nW;
+        const int k0 = min(tid * MJ_ITEMS, L);
+        const int k1 = min(k0 + MJ_ITEMS, L);
+        // per-thread split inside the tile
+        int lo = k0 > nW ? k0 - nW : 0, hi = k0 < nR ? k0 : nR;
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (Rk[mid] <= Wk[k0 - 1 - mid]) lo = mid + 1;
+            else hi = mid;
+        }
+        int ri = lo, wj = k0 - lo;
+        int64_t my_pairs = 0;
+        int64_t emit_base = 0;
+        for (int pass = (MODE == 2 ? 0 : 1); pass < 2; ++pass) {
+            // MODE 2 runs the thread's merge twice: count, then emit at its offset
+            if (MODE == 2 && pass == 1) {
+                // block exclusive scan of my_pairs
+                int64_t v = my_pairs;
+                const int lane = tid & 31, warp = tid >> 5;
+                int64_t incl = v;
+                for (int o = 1; o < 32; o <<= 1) {
+                    int64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += u;
+                }
+                if (lane == 31) warp_cnt[warp] = incl;
+                __syncthreads();
+                int64_t before = 0;
+                for (int w = 0; w < warp; ++w) before += warp_cnt[w];
+                emit_base = tile_cnt[g] + before + incl - v;  // tile_cnt holds the tile's output offset here
+                ri = lo;
+                wj = k0 - lo;
+            }
+            int64_t e = 0;
+            int ri2 = ri, wj2 = wj;
+            for (int step = k0; step < k1; ++step) {
+                if (ri2 < nR && (wj2 >= nW || Rk[ri2] <= Wk[wj2])) {
+                    ++ri2;
+                    continue;
+                }
+                const uint64_t skey = Wk[wj2];
+                const uint64_t spay = Wp[wj2];
+                int64_t gi = t.i0 + ri2 - 1;  // walk back over the equal-key R group
+                while (gi >= 0) {
+                    const bool in_tile = gi >= t.i0;
+                    const uint64_t rk = in_tile ? Rk[gi - t.i0] : r.keys[gi];
+                    if (rk != skey) break;
+                    const uint64_t rp = in_tile ? Rp[gi - t.i0] : r.pays[gi];
+                    if (MODE == 0) {
+                        const uint64_t v = rp + spay;
+                        best = v > best ? v : best;
+                        ++count;
+                        csum += swap ? pair_hash(spay, rp) : pair_hash(rp, spay);
+                    } else if (MODE == 1 || pass == 0) {
+                        ++e;
+                    } else {
+                        const int64_t o = emit_base + e;
+                        emit_out[2 * o] = swap ? spay : rp;
+                        emit_out[2 * o + 1] = swap ? rp : spay;
+                        ++e;
+                    }
+                    --gi;
+                }
+                ++wj2;
+            }
+            my_pairs = e;
+        }
+        if (MODE == 1) {
+            int64_t c = warp_sum((unsigned long long)my_pairs);
+            if ((tid & 31) == 0) warp_cnt[tid >> 5] = c;
+            __syncthreads();
+            if (tid == 0) {
+                int64_t sum = 0;
+                for (int w = 0; w < MJ_THREADS / 32; ++w) sum += warp_cnt[w];
+                tile_cnt[g] = sum;
+            }
+        }
+    }
+    if (MODE == 0 && cur_pair >= 0) flush_pair(sm, out_pairs, cur_pair, count, best, csum);
+}
+
+// per-pair emitted counts from per-tile counts; tile offsets (exclusive scan)
+__global__ void __launch_bounds__(1024) k_emit_offsets(int64_t* __restrict__ tile_cnt, const TileSplit* __restrict__ splits,
+                                                       const int64_t* __restrict__ total, uint64_t* __restrict__ out_pairs,
+                                                       int64_t* __restrict__ grand) {
+    __shared__ int64_t s[1024];
+    __shared__ int64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int64_t n = *total;
+    for (int64_t base = 0; base < n; base += 1024) {
+        int64_t g = base + threadIdx.x;
+        int64_t v = g < n ? tile_cnt[g] : 0;
+        if (g < n && v) atomicAdd((unsigned long long*)(out_pairs + (size_t)splits[g].pair * MPSM_PAIR_FIELDS + MPSM_PAIR_EMITTED), (unsigned long long)v);
+        s[threadIdx.x] = v;
+        __syncthreads();
+        for (int off = 1; off < 1024; off <<= 1) {
+            int64_t a = threadIdx.x >= off ? s[threadIdx.x - off] : 0;
+            __syncthreads();
+            s[threadIdx.x] += a;
+            __syncthreads();
+        }
+        if (g < n) tile_cnt[g] = carry + s[threadIdx.x] - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry += s[1023];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *grand = carry;
+}
+
+static int64_t max_tiles(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub) {
+    int64_t m = 0;
+    for (int i = 0; i < n_priv; ++i)
+        for (int j = 0; j < n_pub; ++j) {
+            if (priv[i].n == 0 || pub[j].n == 0) continue;
+            m += (priv[i].n + pub[j].n + MJ_TILE - 1) / MJ_TILE;
+        }
+    return std::max<int64_t>(m, 1);
+}
+
+struct JoinWs {
+    mpsm_run_t* d_priv;
+    mpsm_run_t* d_pub;
+    PairWin* win;
+    int64_t* total;
+    int64_t* grand;
+    TileSplit* splits;
+    int64_t* tile_cnt;
+};
+
+static bool carve_join(void* ws, size_t bytes, int n_priv, int n_pub, int64_t mt, JoinWs* o) {
+    Carve c{(char*)ws, bytes};
+    o->d_priv = c.take<mpsm_run_t>(std::max(n_priv, 1));
+    o->d_pub = c.take<mpsm_run_t>(std::max(n_pub, 1));
+    o->win = c.take<PairWin>((size_t)std::max(n_priv * n_pub, 1));
+    o->total = c.take<int64_t>(1);
+    o->grand = c.take<int64_t>(1);
+    o->splits = c.take<TileSplit>(mt);
+    o->tile_cnt = c.take<int64_t>(mt);
+    return c.ok;
+}
+
+static size_t join_ws_size(int n_priv, int n_pub, int64_t mt) {
+    Carve c{nullptr, (size_t)-1};
+    c.take<mpsm_run_t>(std::max(n_priv, 1));
+    c.take<mpsm_run_t>(std::max(n_pub, 1));
+    c.take<PairWin>((size_t)std::max(n_priv * n_pub, 1));
+    c.take<int64_t>(1);
+    c.take<int64_t>(1);
+    c.take<TileSplit>(mt);
+    c.take<int64_t>(mt);
+    return c.off;
+}
+
+template <int MODE>
+static int launch_merge(const JoinWs& w, int n_pub, int swap, uint64_t* d_pairs, uint64_t* emit_out, int grid,
+                        cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_merge<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)sizeof(MergeSmem)),
+                             "smem attr"));
+        attr = true;
+    }
+    ProfScope ps(MODE == 0 ? "merge" : (MODE == 1 ? "merge_count" : "merge_emit"), st);
+    k_merge<MODE><<<grid, MJ_THREADS, sizeof(MergeSmem), st>>>(w.d_priv, w.d_pub, n_pub, w.win, w.splits, w.total,
+                                                                swap, d_pairs, w.tile_cnt, emit_out);
+    return check_launch("k_merge");
+}
+
+}  // namespace mpsm
+
+using namespace mpsm;
+
+extern "C" int mpsm_interp_lower_bound(const uint64_t* keys, int64_t n, const uint64_t* d_targets, int64_t ntargets,
+                                       int64_t* d_index, int64_t* d_probes, void* stream) {
+    if (n < 0 || ntargets < 0) return MPSM_ERR_ARG;
+    if (ntargets == 0) return MPSM_OK;
+    k_interp_batch<<<(unsigned)((ntargets + 127) / 128), 128, 0, (cudaStream_t)stream>>>(keys, n, d_targets, ntargets,
+                                                                                        d_index, d_probes);
+    return check_launch("k_interp_batch");
+}
+
+extern "C" int mpsm_join_workspace_bytes(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub,
+                                         size_t* bytes) {
+    if (!bytes || n_priv < 0 || n_pub < 0) return MPSM_ERR_ARG;
+    *bytes = join_ws_size(n_priv, n_pub, max_tiles(priv, n_priv, pub, n_pub));
+    return MPSM_OK;
+}
+
+extern "C" int mpsm_join_pairs(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub, int swap,
+                               int mode, uint64_t* d_out, int64_t cap, uint64_t* d_pairs, void* workspace,
+                               size_t ws_bytes, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n_priv < 1 || n_pub < 1 || !d_pairs) return MPSM_ERR_ARG;
+    if (mode < 0 || mode > 2) return MPSM_ERR_ARG;
+    const int npairs = n_priv * n_pub;
+    const int64_t mt = max_tiles(priv, n_priv, pub, n_pub);
+    JoinWs w;
+    if (!carve_join(workspace, ws_bytes, n_priv, n_pub, mt, &w)) {
+        set_error("join workspace too small");
+        return MPSM_ERR_ARG;
+    }
+    MPSM_TRY(cuda_status(cudaMemcpyAsync(w.d_priv, priv, sizeof(mpsm_run_t) * n_priv, cudaMemcpyHostToDevice, st), "h2d"));
+    MPSM_TRY(cuda_status(cudaMemcpyAsync(w.d_pub, pub, sizeof(mpsm_run_t) * n_pub, cudaMemcpyHostToDevice, st), "h2d"));
+    k_windows<<<(npairs + 127) / 128, 128, 0, st>>>(w.d_priv, n_priv, w.d_pub, n_pub, w.win, d_pairs);
+    MPSM_TRY(check_launch("k_windows"));
+    k_tile_scan<<<1, 1024, 0, st>>>(w.win, npairs, w.total);
+    MPSM_TRY(check_launch("k_tile_scan"));
+    {
+    ProfScope ps("merge_partition", st);
+    k_partition<<<(unsigned)((mt + 255) / 256), 256, 0, st>>>(w.d_priv, w.d_pub, n_pub, w.win, npairs, w.total,
+                                                               w.splits);
+    }
+    MPSM_TRY(check_launch("k_partition"));
+    // persistent grid: a few CTAs per SM
+    int grid = (int)std::min<int64_t>((int64_t)num_sms() * 6, mt);
+    if (mode != MPSM_MODE_MATERIALIZE || d_out == nullptr) {
+        MPSM_TRY(launch_merge<0>(w, n_pub, swap, d_pairs, nullptr, grid, st));
+        return MPSM_OK;
+    }
+    // materialize: aggregates, per-tile counts, offsets, emission
+    MPSM_TRY(launch_merge<0>(w, n_pub, swap, d_pairs, nullptr, grid, st));
+    MPSM_TRY(launch_merge<1>(w, n_pub, swap, d_pairs, nullptr, grid, st));
+    k_emit_offsets<<<1, 1024, 0, st>>>(w.tile_cnt, w.splits, w.total, d_pairs, w.grand);
+    MPSM_TRY(check_launch("k_emit_offsets"));
+    (void)cap;  // the caller sized d_out from the counts of a first call
+    return launch_merge<2>(w, n_pub, swap, d_pairs, d_out, grid, st);
+}

@@ -90,3 +90,34 @@ def gen_location_skew(rel: Relation, t: int, seed: int = 0) -> Relation:
 def gen_negcorr(n_r: int, n_s: int, dom: KeyDomain, seed: int = 0) -> tuple:
     """Config 4: R skewed low, S skewed high (negatively correlated)."""
     return gen_skewed_8020(n_r, dom, "low", seed=2 * seed), gen_skewed_8020(n_s, dom, "high", seed=2 * seed + 1)
+
+
+DISTRIBUTIONS = ("uniform", "skew-80-20-high", "skew-80-20-low", "location-sorted-clusters")
+
+
+class GenSpec:
+    """Everything needed to regenerate a relation (datagen.py:33-47)."""
+
+    def __init__(self, cardinality: int, key_domain: KeyDomain, distribution: str = "uniform", seed: int = 0,
+                 location_threads: int = 4):
+        if cardinality < 0:
+            raise ConfigurationError("cardinality must be non-negative")
+        if distribution not in DISTRIBUTIONS:
+            raise ConfigurationError(f"unknown distribution {distribution!r}")
+        self.cardinality = cardinality
+        self.key_domain = key_domain
+        self.distribution = distribution
+        self.seed = seed
+        self.location_threads = location_threads
+
+
+def generate(spec: GenSpec) -> Relation:
+    """datagen.py:108-118"""
+    if spec.distribution == "uniform":
+        return gen_uniform(spec.cardinality, spec.key_domain, spec.seed)
+    if spec.distribution == "skew-80-20-high":
+        return gen_skewed_8020(spec.cardinality, spec.key_domain, "high", spec.seed)
+    if spec.distribution == "skew-80-20-low":
+        return gen_skewed_8020(spec.cardinality, spec.key_domain, "low", spec.seed)
+    base = gen_uniform(spec.cardinality, spec.key_domain, spec.seed)
+    return gen_location_skew(base, spec.location_threads, spec.seed)

@@ -1,0 +1,179 @@
+"""Device-side operators: torch tensors in, C-ABI calls out.
+
+PyTorch is only the carrier here (device memory, streams); every operator is
+a call into libmpsm_b200.so.  Buffers are uint64 torch tensors on one CUDA
+device; pointers and the current stream go through ctypes as plain integers.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import ConfigurationError
+
+U64 = torch.uint64
+I64 = torch.int64
+
+_init_lock = threading.Lock()
+_inited = {}
+
+
+def ensure_device(device: Optional[torch.device] = None) -> torch.device:
+    """Select the CUDA device and verify it is a B200 (sm_100).  Raises if none."""
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1207_0145_b200 needs a CUDA device (B200); none is visible and there is no CPU path")
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    with _init_lock:
+        if dev.index not in _inited:
+            lib = _lib.load()
+            with torch.cuda.device(dev):
+                rc = lib.mpsm_device_init(dev.index)
+            if rc < 0:
+                _lib.check(rc, "mpsm_device_init")
+            _inited[dev.index] = rc
+    return dev
+
+
+def stream_ptr(stream: Optional[torch.cuda.Stream] = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    if t is None:
+        return None
+    return int(t.data_ptr()) if t.numel() else None
+
+
+class Workspace:
+    """Grow-only scratch buffer per device (stream-ordered reuse)."""
+
+    def __init__(self, device: torch.device):
+        self.device = device
+        self.buf = torch.empty(0, dtype=torch.uint8, device=device)
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        nbytes = max(int(nbytes), 256)
+        if self.buf.numel() < nbytes:
+            self.buf = torch.empty(int(nbytes * 1.25) + 4096, dtype=torch.uint8, device=self.device)
+        return self.buf
+
+
+_ws = {}
+
+
+def workspace(device: torch.device) -> Workspace:
+    if device.index not in _ws:
+        _ws[device.index] = Workspace(device)
+    return _ws[device.index]
+
+
+def new_bad_flag(device: torch.device) -> torch.Tensor:
+    """int64[1] = -1 (all ones == UINT64_MAX: no out-of-domain key seen)."""
+    return torch.full((1,), -1, dtype=I64, device=device)
+
+
+# ---------------------------------------------------------------- operators
+
+def sort_pairs(in_k: torch.Tensor, in_p: torch.Tensor, lower: int, span_m1: int, width_bits: int,
+               out_k: torch.Tensor, out_p: torch.Tensor, tmp_k: torch.Tensor, tmp_p: torch.Tensor,
+               bad: Optional[torch.Tensor] = None) -> None:
+    n = int(in_k.numel())
+    if n == 0:
+        return
+    L = _lib.load()
+    sz = ctypes.c_size_t(0)
+    _lib.check(L.mpsm_sort_workspace_bytes(n, width_bits, ctypes.byref(sz)), "sort workspace")
+    ws = workspace(in_k.device).get(sz.value)
+    _lib.check(L.mpsm_sort_pairs(ptr(in_k), ptr(in_p), n, lower, span_m1, width_bits, ptr(out_k), ptr(out_p),
+                                 ptr(tmp_k), ptr(tmp_p), ptr(ws), ws.numel(), ptr(bad), stream_ptr()),
+               "mpsm_sort_pairs")
+
+
+def radix_histogram(keys: torch.Tensor, lower: int, span_m1: int, shift: int, nbuckets: int,
+                    counts: torch.Tensor, bad: Optional[torch.Tensor] = None) -> None:
+    n = int(keys.numel())
+    if n == 0:
+        return
+    _lib.check(_lib.load().mpsm_radix_histogram(ptr(keys), n, lower, span_m1, shift, nbuckets, ptr(counts), ptr(bad),
+                                                stream_ptr()), "mpsm_radix_histogram")
+
+
+def scatter_chunk(keys, pays, lower: int, shift: int, sp: torch.Tensor, nbuckets: int, npart: int,
+                  cursors: torch.Tensor, arena_k, arena_p, written: torch.Tensor) -> None:
+    n = int(keys.numel())
+    if n == 0:
+        return
+    L = _lib.load()
+    sz = ctypes.c_size_t(0)
+    _lib.check(L.mpsm_scatter_workspace_bytes(n, npart, ctypes.byref(sz)), "scatter workspace")
+    ws = workspace(keys.device).get(sz.value)
+    _lib.check(L.mpsm_scatter_chunk(ptr(keys), ptr(pays), n, lower, shift, ptr(sp), nbuckets, npart, ptr(cursors),
+                                    ptr(arena_k), ptr(arena_p), ptr(written), ptr(ws), ws.numel(), stream_ptr()),
+               "mpsm_scatter_chunk")
+
+
+def interp_lower_bound(keys: torch.Tensor, targets: torch.Tensor):
+    """-> (index int64 tensor, probes int64 tensor)"""
+    nt = int(targets.numel())
+    idx = torch.empty(nt, dtype=I64, device=keys.device)
+    probes = torch.empty(nt, dtype=I64, device=keys.device)
+    if nt:
+        _lib.check(_lib.load().mpsm_interp_lower_bound(ptr(keys) or 0, int(keys.numel()), ptr(targets), nt, ptr(idx),
+                                                       ptr(probes), stream_ptr()), "mpsm_interp_lower_bound")
+    return idx, probes
+
+
+def _run_descs(runs: Sequence[tuple]):
+    return _lib.runs_array((ptr(k) or 0, ptr(p) or 0, int(k.numel())) for k, p in runs)
+
+
+def join_pairs(priv: Sequence[tuple], pub: Sequence[tuple], swap: bool, mode: int,
+               out: Optional[torch.Tensor] = None, cap: int = 0) -> torch.Tensor:
+    """Merge-join every private run against every public run.
+
+    priv/pub: sequences of (keys, pays) device tensors (sorted runs).
+    Returns the uint64 [n_priv * n_pub, PAIR_FIELDS] pair-record tensor (device).
+    """
+    dev = (priv[0][0] if priv else pub[0][0]).device
+    pa, ua = _run_descs(priv), _run_descs(pub)
+    L = _lib.load()
+    sz = ctypes.c_size_t(0)
+    _lib.check(L.mpsm_join_workspace_bytes(pa, len(priv), ua, len(pub), ctypes.byref(sz)), "join workspace")
+    ws = workspace(dev).get(sz.value)
+    rec = torch.empty((len(priv) * len(pub), _lib.PAIR_FIELDS), dtype=U64, device=dev)
+    _lib.check(L.mpsm_join_pairs(pa, len(priv), ua, len(pub), int(bool(swap)), int(mode), ptr(out), int(cap),
+                                 ptr(rec), ptr(ws), ws.numel(), stream_ptr()), "mpsm_join_pairs")
+    return rec
+
+
+def minmax_contiguous(n: int, t: int, prefix: np.ndarray, edge: np.ndarray, cand: np.ndarray) -> list:
+    prefix = np.ascontiguousarray(prefix, np.int64)
+    edge = np.ascontiguousarray(edge, np.float64)
+    cand = np.ascontiguousarray(cand, np.float64)
+    out = np.zeros(t + 1, np.int64)
+    rc = _lib.load().mpsm_minmax_contiguous(n, t, prefix.ctypes.data, edge.ctypes.data, cand.ctypes.data,
+                                            cand.shape[0], out.ctypes.data)
+    if rc == _lib.ERR_CONFIG:
+        raise ConfigurationError(f"cannot split {n} buckets into {t} partitions")
+    _lib.check(rc, "mpsm_minmax_contiguous")
+    return out.tolist()
+
+
+def to_device(a, device: torch.device, non_blocking: bool = False) -> torch.Tensor:
+    """numpy uint64 / torch tensor -> contiguous uint64 tensor on device."""
+    if isinstance(a, torch.Tensor):
+        t = a if a.device == device else a.to(device, non_blocking=non_blocking)
+        return t.contiguous()
+    arr = np.ascontiguousarray(a, np.uint64)
+    if arr.shape[0] == 0:
+        return torch.empty(0, dtype=U64, device=device)
+    return torch.from_numpy(arr).to(device, non_blocking=non_blocking)

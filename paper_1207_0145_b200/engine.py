@@ -1,0 +1,436 @@
+"""GPU MPSM join engine -- the drop-in for the reference's run_join / run_pmpsm /
+run_bmpsm (/root/reference/pkg/src/mpsm/engine.py:279-466).
+
+Same signatures, phases, result semantics and statistics.  The T logical
+workers of the reference (cfg.threads) are kept: T public runs (S chunked by
+position, core.py:263-279) and, for P-MPSM, T private partitions chosen by
+the reference's CDF/histogram splitters.  One host thread issues the work of
+all workers to the GPU in barrier order (engine.py:380-419); there are no
+worker threads and no barriers to deadlock on (SURVEY.md finding 7).
+
+Per phase, device work only (csrc/):
+  sort_public   onesweep LSD radix sort of every public chunk into its run
+  histogram     per-worker 2^B bucket counts of the private chunks (+ domain)
+  splitters     host: CDF from f*T bounds per run + C++ min-max search
+  scatter       stable partition scatter into the arena (reference layout)
+  sort_private  radix sort of every partition run
+  join          merge-path merge-join of every (private, public) run pair with
+                fused COUNT / MAX / checksum (no materialisation unless asked)
+
+With T == 1 the partition phase is the identity, so the private input is
+sorted directly (the reference still copies it through its arena).
+"""
+
+from __future__ import annotations
+
+import os
+import time
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from . import device as D
+from .core import (
+    ConfigurationError,
+    DomainError,
+    InternalConsistencyError,
+    JoinConfig,
+    JoinResult,
+    KeyDomain,
+    MaterializeCapExceeded,
+    Relation,
+    Run,
+    WorkerStats,
+    chunk_bounds,
+)
+from .partition import SplitterVector, combine_counts, effective_radix_bits
+from .skew import LocalBounds, bound_positions, build_cdf, compute_splitters
+
+PhaseHook = Optional[Callable[[int, str], None]]
+MASK64 = (1 << 64) - 1
+
+
+@dataclass(frozen=True)
+class RoleAssignment:
+    """Which input plays the private (partitioned) role (engine.py:55-66)."""
+
+    private: str
+
+    @property
+    def public(self) -> str:
+        return "s" if self.private == "r" else "r"
+
+    @property
+    def swapped(self) -> bool:
+        return self.private == "s"
+
+
+def choose_roles(n_r: int, n_s: int, policy: str = "auto") -> RoleAssignment:
+    """Smaller relation private, ties keep R (engine.py:69-78)."""
+    if policy == "r-private":
+        return RoleAssignment("r")
+    if policy == "s-private":
+        return RoleAssignment("s")
+    if policy != "auto":
+        raise ConfigurationError(f"unknown role policy {policy!r}")
+    return RoleAssignment("r" if n_r <= n_s else "s")
+
+
+@dataclass(frozen=True)
+class PhaseStep:
+    name: str
+    barrier_after: bool
+
+
+@dataclass(frozen=True)
+class PhasePlan:
+    algorithm: str
+    steps: tuple
+
+    def __post_init__(self) -> None:
+        names = [s.name for s in self.steps]
+        if "join" in names and "sort_public" in names:
+            i_pub = names.index("sort_public")
+            if not self.steps[i_pub].barrier_after or names.index("join") < i_pub:
+                raise ConfigurationError("join must start after the public-sort barrier")
+
+
+def plan_phases(algorithm: str) -> PhasePlan:
+    """engine.py:100-121"""
+    if algorithm == "b-mpsm":
+        return PhasePlan(algorithm, (PhaseStep("sort_public", True), PhaseStep("sort_private", False),
+                                     PhaseStep("join", False)))
+    if algorithm == "p-mpsm":
+        return PhasePlan(algorithm, (PhaseStep("sort_public", True), PhaseStep("histogram", True),
+                                     PhaseStep("scatter", True), PhaseStep("sort_private", False),
+                                     PhaseStep("join", False)))
+    raise ConfigurationError(f"no phase plan for algorithm {algorithm!r}")
+
+
+# ------------------------------------------------------------ run helpers
+
+def _keys_of(run):
+    if isinstance(run, (Run, Relation)):
+        return run.keys, run.payloads
+    return run, None
+
+
+def interpolation_search(run, target: int) -> int:
+    """First index with key >= target (engine.py:124-128), on the GPU with the
+    reference's probe rule."""
+    keys, _ = _keys_of(run)
+    dev = D.ensure_device()
+    kd = D.to_device(keys if not isinstance(keys, (list, tuple)) else np.asarray(keys, np.uint64), dev)
+    tg = torch.from_numpy(np.array([int(target) & MASK64], np.uint64)).to(dev)
+    idx, _ = D.interp_lower_bound(kd, tg)
+    return int(idx.item())
+
+
+def merge_join(r_run: Run, s_run: Run, s_start: int, emit: Callable[[int, int], None]) -> int:
+    """emit(r_payload, s_payload) once per matching pair; returns the pair
+    count (engine.py:131-166).  The pairs are produced by the GPU merge kernel
+    (materialize mode) from s_start on and then handed to emit on the host."""
+    dev = D.ensure_device()
+    rk, rp = D.to_device(r_run.keys, dev), D.to_device(r_run.payloads, dev)
+    sk, sp = D.to_device(s_run.keys, dev), D.to_device(s_run.payloads, dev)
+    sk, sp = sk[s_start:], sp[s_start:]
+    if rk.numel() == 0 or sk.numel() == 0:
+        return 0
+    rec = D.join_pairs([(rk, rp)], [(sk, sp)], False, _lib.MODE_COUNT)
+    count = int(rec[0, _lib.PAIR_COUNT].item())
+    if count:
+        out = torch.empty(2 * count, dtype=torch.uint64, device=dev)
+        D.join_pairs([(rk, rp)], [(sk, sp)], False, _lib.MODE_MATERIALIZE, out, count)
+        pairs = out.view(count, 2).cpu().numpy()
+        for a, b in pairs.tolist():
+            emit(a, b)
+    return count
+
+
+# ----------------------------------------------------------------- engine
+
+class _Timeline:
+    """CUDA events at phase boundaries (engine.py:421-432 keys)."""
+
+    def __init__(self):
+        self.ev = {}
+
+    def mark(self, name: str) -> None:
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.ev[name] = e
+
+    def seconds(self, a: str, b: str) -> float:
+        return self.ev[a].elapsed_time(self.ev[b]) / 1e3
+
+
+def _prepare(r: Relation, s: Relation, cfg: JoinConfig):
+    roles = choose_roles(r.cardinality, s.cardinality, cfg.role_policy)
+    private, public = (r, s) if roles.private == "r" else (s, r)
+    return cfg.key_domain, roles, private, public
+
+
+def _raise_domain(flag: torch.Tensor, rel_name: str) -> None:
+    idx = int(flag.item())
+    if idx != -1:
+        raise DomainError(f"relation {rel_name} has out-of-domain keys (first at index {idx})")
+
+
+class JoinContext:
+    """Device buffers and state of one join on one GPU."""
+
+    def __init__(self, r: Relation, s: Relation, cfg: JoinConfig, phase_hook: PhaseHook):
+        self.cfg = cfg
+        self.hook = phase_hook
+        self.dev = D.ensure_device()
+        self.dom, self.roles, private, public = _prepare(r, s, cfg)
+        self.t = cfg.threads
+        self.wbits = self.dom.width_bits
+        self.span_m1 = self.dom.upper - self.dom.lower - 1
+        self.priv_k = D.to_device(private.keys, self.dev)
+        self.priv_p = D.to_device(private.payloads, self.dev)
+        self.pub_k = D.to_device(public.keys, self.dev)
+        self.pub_p = D.to_device(public.payloads, self.dev)
+        self.n_priv = int(self.priv_k.numel())
+        self.n_pub = int(self.pub_k.numel())
+        self.pub_chunks = chunk_bounds(self.n_pub, self.t)
+        self.priv_chunks = chunk_bounds(self.n_priv, self.t)
+        self.stats = [WorkerStats(i) for i in range(self.t)]
+        self.bad_pub = D.new_bad_flag(self.dev)
+        self.bad_priv = D.new_bad_flag(self.dev)
+        self.tl = _Timeline()
+
+    def _hook(self, i: int, phase: str) -> None:
+        if self.hook:
+            self.hook(i, phase)
+
+    def sort_public(self):
+        """phase 1: every public chunk -> sorted run (engine.py:389-395)."""
+        n = self.n_pub
+        self.run_k = torch.empty(n, dtype=torch.uint64, device=self.dev)
+        self.run_p = torch.empty(n, dtype=torch.uint64, device=self.dev)
+        width = max((b - a for a, b in self.pub_chunks), default=0)
+        self.tmp_k = torch.empty(width, dtype=torch.uint64, device=self.dev)
+        self.tmp_p = torch.empty(width, dtype=torch.uint64, device=self.dev)
+        self.pub_runs = []
+        for i, (a, b) in enumerate(self.pub_chunks):
+            self._hook(i, "sort_public")
+            if b > a:
+                D.sort_pairs(self.pub_k[a:b], self.pub_p[a:b], self.dom.lower, self.span_m1, self.wbits,
+                             self.run_k[a:b], self.run_p[a:b], self.tmp_k[:b - a], self.tmp_p[:b - a], self.bad_pub)
+            self.pub_runs.append((self.run_k[a:b], self.run_p[a:b]))
+            self.stats[i].tuples_sorted_public = b - a
+
+    def _ensure_tmp(self, width: int) -> None:
+        if self.tmp_k.numel() < width:
+            self.tmp_k = torch.empty(width, dtype=torch.uint64, device=self.dev)
+            self.tmp_p = torch.empty(width, dtype=torch.uint64, device=self.dev)
+
+    def sort_private_chunks(self):
+        """B-MPSM phase 2: each private chunk sorted into its own run."""
+        self.priv_run_k = torch.empty(self.n_priv, dtype=torch.uint64, device=self.dev)
+        self.priv_run_p = torch.empty(self.n_priv, dtype=torch.uint64, device=self.dev)
+        self._ensure_tmp(max((b - a for a, b in self.priv_chunks), default=0))
+        self.priv_runs = []
+        for i, (a, b) in enumerate(self.priv_chunks):
+            self._hook(i, "sort_private")
+            if b > a:
+                D.sort_pairs(self.priv_k[a:b], self.priv_p[a:b], self.dom.lower, self.span_m1, self.wbits,
+                             self.priv_run_k[a:b], self.priv_run_p[a:b], self.tmp_k[:b - a], self.tmp_p[:b - a],
+                             self.bad_priv)
+            self.priv_runs.append((self.priv_run_k[a:b], self.priv_run_p[a:b]))
+            self.stats[i].tuples_sorted_private = b - a
+
+    def partition(self):
+        """P-MPSM phase 2 (engine.py:359-374, 396-406): histograms, splitters,
+        cursors, scatter.  Returns the arena run bases."""
+        t, dom = self.t, self.dom
+        bits = effective_radix_bits(dom, self.cfg.radix_bits)
+        if (1 << bits) < t:
+            raise ConfigurationError(f"effective radix bits {bits} give fewer buckets than {t} workers")
+        nb = 1 << bits
+        shift = self.wbits - bits
+        hists = torch.zeros((t, nb), dtype=torch.int64, device=self.dev)
+        for i, (a, b) in enumerate(self.priv_chunks):
+            self._hook(i, "histogram")
+            D.radix_histogram(self.priv_k[a:b], dom.lower, self.span_m1, shift, nb, hists[i], self.bad_priv)
+        # equi-height bounds of every sorted public run (skew.py:52-62)
+        f = self.cfg.cdf_fanout
+        pos_list = []
+        for a, b in self.pub_chunks:
+            if b > a:
+                pos_list.append(torch.from_numpy(bound_positions(b - a, f, t) + a))
+        gather = torch.cat(pos_list).to(self.dev) if pos_list else None
+        bound_keys = self.run_k.view(torch.int64)[gather].view(torch.uint64) if gather is not None else None
+        # the single host synchronisation of the join: counts + bounds + flags
+        hist_h = hists.cpu().numpy()
+        bk = bound_keys.cpu().numpy() if bound_keys is not None else np.empty(0, np.uint64)
+        _raise_domain(self.bad_priv, "private")
+        _raise_domain(self.bad_pub, "public")
+        bounds, off = [], 0
+        for a, b in self.pub_chunks:
+            if b > a:
+                bounds.append(LocalBounds(bk[off:off + f * t], b - a))
+                off += f * t
+            else:
+                bounds.append(LocalBounds(np.empty(0, np.uint64), 0))
+        cdf = build_cdf(bounds, anchor_key=dom.lower)
+        ss = compute_splitters(hist_h.sum(axis=0), cdf, t, dom, bits)
+        self.splitters = ss
+        cursors = combine_counts(list(hist_h), ss.vector.sp, t)
+        cursors.verify_disjoint()
+        self.cursors = cursors
+        arena_k = torch.empty(self.n_priv, dtype=torch.uint64, device=self.dev)
+        arena_p = torch.empty(self.n_priv, dtype=torch.uint64, device=self.dev)
+        sp_dev = torch.from_numpy(ss.vector.sp.astype(np.int32)).to(self.dev)
+        cur_all = torch.from_numpy(np.stack([cursors.absolute_cursors(i)[0] for i in range(t)])).to(self.dev)
+        written = torch.zeros((t, t), dtype=torch.int64, device=self.dev)
+        self.tl.mark("hist")
+        for i, (a, b) in enumerate(self.priv_chunks):
+            self._hook(i, "scatter")
+            D.scatter_chunk(self.priv_k[a:b], self.priv_p[a:b], dom.lower, shift, sp_dev, nb, t, cur_all[i],
+                            arena_k, arena_p, written[i])
+            self.stats[i].tuples_scattered = b - a
+        self.written = written
+        self.arena = (arena_k, arena_p)
+        return cursors.run_base
+
+    def sort_partitions(self, run_base):
+        """P-MPSM phase 3 (engine.py:405-409)."""
+        arena_k, arena_p = self.arena
+        self.priv_run_k = torch.empty(self.n_priv, dtype=torch.uint64, device=self.dev)
+        self.priv_run_p = torch.empty(self.n_priv, dtype=torch.uint64, device=self.dev)
+        self._ensure_tmp(int(np.max(np.diff(run_base))) if len(run_base) > 1 else 0)
+        self.priv_runs = []
+        for i in range(self.t):
+            a, b = int(run_base[i]), int(run_base[i + 1])
+            self._hook(i, "sort_private")
+            if b > a:
+                D.sort_pairs(arena_k[a:b], arena_p[a:b], self.dom.lower, self.span_m1, self.wbits,
+                             self.priv_run_k[a:b], self.priv_run_p[a:b], self.tmp_k[:b - a], self.tmp_p[:b - a],
+                             None)
+            self.priv_runs.append((self.priv_run_k[a:b], self.priv_run_p[a:b]))
+            self.stats[i].tuples_sorted_private = b - a
+
+    def join(self):
+        """phase 4 (engine.py:228-276, 410-419) for all workers in one launch sequence."""
+        for i in range(self.t):
+            self._hook(i, "join")
+        mode = {"aggregate-max": _lib.MODE_AGGREGATE_MAX, "count": _lib.MODE_COUNT,
+                "materialize": _lib.MODE_COUNT}[self.cfg.query_mode]
+        self.rec = D.join_pairs(self.priv_runs, self.pub_runs, self.roles.swapped, mode)
+
+    def materialize(self, total: int) -> np.ndarray:
+        if total == 0:
+            return np.empty((0, 2), np.uint64)
+        out = torch.empty(2 * total, dtype=torch.uint64, device=self.dev)
+        D.join_pairs(self.priv_runs, self.pub_runs, self.roles.swapped, _lib.MODE_MATERIALIZE, out, total)
+        return out.view(total, 2).cpu().numpy()
+
+    def finalize(self, timings: dict) -> JoinResult:
+        """engine.py:195-225 plus the checksum and per-worker statistics."""
+        t = self.t
+        rec = self.rec.cpu().numpy().reshape(t, t, _lib.PAIR_FIELDS).astype(object)
+        _raise_domain(self.bad_priv, "private")
+        _raise_domain(self.bad_pub, "public")
+        count, agg, csum = 0, None, 0
+        for i in range(t):
+            st = self.stats[i]
+            ci, bi = 0, 0
+            n_priv_i = int(self.priv_runs[i][0].numel())
+            for j in range(t):
+                n_pub_j = int(self.pub_runs[j][0].numel())
+                if n_priv_i == 0 or n_pub_j == 0:
+                    continue
+                c = int(rec[i, j, _lib.PAIR_COUNT])
+                st.probe_tuples_examined += int(rec[i, j, _lib.PAIR_PROBES])
+                st.public_tuples_examined += int(rec[i, j, _lib.PAIR_PROBES]) + int(rec[i, j, _lib.PAIR_EXAMINED])
+                if c > 0:
+                    st.s_runs_with_matches += 1
+                    b = int(rec[i, j, _lib.PAIR_BEST])
+                    if ci == 0 or b > bi:
+                        bi = b
+                    ci += c
+                    csum = (csum + int(rec[i, j, _lib.PAIR_CHECKSUM])) & MASK64
+            count += ci
+            if ci > 0 and self.cfg.query_mode == "aggregate-max":
+                agg = bi if agg is None or bi > agg else agg
+        materialized = None
+        if self.cfg.query_mode == "materialize":
+            if count > self.cfg.materialize_cap:
+                raise MaterializeCapExceeded(f"join produced {count} pairs, cap is {self.cfg.materialize_cap}")
+            materialized = self.materialize(count)
+        for st in self.stats:
+            st.sort_public_seconds = timings.get("sort_public", 0.0)
+            st.sort_private_seconds = timings.get("sort_private", 0.0)
+            st.join_seconds = timings.get("join", 0.0)
+        return JoinResult(match_count=int(count), aggregate_max=agg, materialized=materialized,
+                          phase_timings=timings, worker_stats=self.stats, checksum=int(csum))
+
+
+def run_bmpsm(r: Relation, s: Relation, cfg: JoinConfig, *, phase_hook: PhaseHook = None) -> JoinResult:
+    """Basic variant: sort both inputs chunk-wise, join every private run
+    against every public run (engine.py:279-334)."""
+    ctx = JoinContext(r, s, cfg, phase_hook)
+    ctx.tl.mark("t0")
+    ctx.sort_public()
+    ctx.tl.mark("public")
+    ctx.sort_private_chunks()
+    ctx.tl.mark("sort_private")
+    ctx.join()
+    ctx.tl.mark("join")
+    torch.cuda.current_stream().synchronize()
+    tl = ctx.tl
+    timings = {"sort_public": tl.seconds("t0", "public"), "partition": 0.0,
+               "sort_private": tl.seconds("public", "sort_private"), "join": tl.seconds("sort_private", "join"),
+               "total": tl.seconds("t0", "join")}
+    return ctx.finalize(timings)
+
+
+def run_pmpsm(r: Relation, s: Relation, cfg: JoinConfig, *, phase_hook: PhaseHook = None) -> JoinResult:
+    """Range-partitioned variant (engine.py:337-433)."""
+    ctx = JoinContext(r, s, cfg, phase_hook)
+    ctx.tl.mark("t0")
+    ctx.sort_public()
+    ctx.tl.mark("public")
+    if ctx.t == 1:
+        # one partition: the histogram/scatter are the identity (the splitter
+        # search returns [0, 2^B]); sort the private input directly
+        effective_radix_bits(ctx.dom, cfg.radix_bits)
+        for ph in ("histogram", "scatter"):
+            ctx._hook(0, ph)
+        ctx.stats[0].tuples_scattered = ctx.n_priv
+        ctx.tl.mark("scatter")
+        ctx.sort_private_chunks()
+    else:
+        run_base = ctx.partition()
+        ctx.tl.mark("scatter")
+        ctx.sort_partitions(run_base)
+    ctx.tl.mark("sort_private")
+    ctx.join()
+    ctx.tl.mark("join")
+    torch.cuda.current_stream().synchronize()
+    if ctx.t > 1:
+        exp = ctx.cursors.counts
+        if not np.array_equal(ctx.written.cpu().numpy(), exp):
+            raise InternalConsistencyError("scatter wrote a different number of tuples than the histograms promised")
+    tl = ctx.tl
+    timings = {"sort_public": tl.seconds("t0", "public"), "partition": tl.seconds("public", "scatter"),
+               "sort_private": tl.seconds("scatter", "sort_private"), "join": tl.seconds("sort_private", "join"),
+               "total": tl.seconds("t0", "join")}
+    return ctx.finalize(timings)
+
+
+def run_join(r: Relation, s: Relation, cfg: JoinConfig, *, phase_hook: PhaseHook = None) -> JoinResult:
+    """Dispatch on cfg.algorithm (engine.py:456-466)."""
+    if cfg.algorithm == "b-mpsm":
+        return run_bmpsm(r, s, cfg, phase_hook=phase_hook)
+    if cfg.algorithm == "p-mpsm":
+        return run_pmpsm(r, s, cfg, phase_hook=phase_hook)
+    if cfg.algorithm == "hash-oracle":
+        raise ConfigurationError("algorithm 'hash-oracle' is the reference's CPU ground truth "
+                                 "(datagen.hash_join_oracle); this package implements the MPSM engines only")
+    raise ConfigurationError(f"unknown algorithm {cfg.algorithm!r}")
