@@ -85,6 +85,8 @@ int mpsm_profile_read(const char* name, double* total_ms, uint64_t* launches);
  * and raises DomainError (sorter.py:97-98).  Stable (equal keys keep input
  * order), which the reference does not promise. */
 int mpsm_sort_workspace_bytes(int64_t n, int width_bits, size_t* bytes);
+/* number of scatter passes (digits) the sort uses for width_bits */
+int mpsm_sort_pass_count(int width_bits);
 int mpsm_sort_pairs(const uint64_t* in_keys, const uint64_t* in_pays, int64_t n, uint64_t lower,
                     uint64_t span_m1, int width_bits, uint64_t* out_keys, uint64_t* out_pays,
                     uint64_t* tmp_keys, uint64_t* tmp_pays, void* workspace, size_t ws_bytes,

@@ -26,7 +26,7 @@ PAIR_FIELDS = 8
 EXPORTS = (
     "mpsm_version", "mpsm_last_error", "mpsm_device_init", "mpsm_launch_count",
     "mpsm_profile_enable", "mpsm_profile_read",
-    "mpsm_sort_workspace_bytes", "mpsm_sort_pairs",
+    "mpsm_sort_workspace_bytes", "mpsm_sort_pass_count", "mpsm_sort_pairs",
     "mpsm_radix_histogram",
     "mpsm_scatter_workspace_bytes", "mpsm_scatter_chunk",
     "mpsm_interp_lower_bound",
@@ -50,6 +50,7 @@ _SIGS = {
     "mpsm_profile_enable": (_int, [_int]),
     "mpsm_profile_read": (_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64)]),
     "mpsm_sort_workspace_bytes": (_int, [_i64, _int, ctypes.POINTER(_sz)]),
+    "mpsm_sort_pass_count": (_int, [_int]),
     "mpsm_sort_pairs": (_int, [_vp, _vp, _i64, _u64, _u64, _int, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp]),
     "mpsm_radix_histogram": (_int, [_vp, _i64, _u64, _u64, _int, _int, _vp, _vp, _vp]),
     "mpsm_scatter_workspace_bytes": (_int, [_i64, _int, ctypes.POINTER(_sz)]),

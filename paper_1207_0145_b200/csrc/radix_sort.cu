@@ -368,6 +368,8 @@ static int clear_status_if_wrapped(bool wrapped, uint64_t* status, int64_t n, cu
 
 using namespace mpsm;
 
+extern "C" int mpsm_sort_pass_count(int width_bits) { return plan_passes(width_bits).npasses; }
+
 extern "C" int mpsm_sort_workspace_bytes(int64_t n, int width_bits, size_t* bytes) {
     if (!bytes || n < 0 || width_bits < 0 || width_bits > 64) return MPSM_ERR_ARG;
     *bytes = sort_ws_bytes(n);
