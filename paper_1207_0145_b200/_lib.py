@@ -14,7 +14,7 @@ import os
 from .core import ConfigurationError, DomainError, InternalConsistencyError, MaterializeCapExceeded
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmpsm_b200.so")
+LIB_PATH = os.environ.get("MPSM_LIB") or os.path.join(_HERE, "libmpsm_b200.so")
 
 MPSM_OK = 0
 ERR_DOMAIN, ERR_INTERNAL, ERR_CONFIG, ERR_CUDA, ERR_CAP, ERR_ARG = -1, -2, -3, -4, -5, -6

@@ -36,7 +36,11 @@ def _headers_mtime():
     return max(os.path.getmtime(h) for h in hs)
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False, defines=(), build_dir: str = None,
+          lib: str = None) -> str:
+    """Compile csrc/ into lib (default: the in-tree libmpsm_b200.so)."""
+    BUILD = build_dir or globals()["BUILD"]
+    LIB = lib or globals()["LIB"]
     os.makedirs(BUILD, exist_ok=True)
     hdr = _headers_mtime()
     objs, jobs = [], []
@@ -46,7 +50,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) 
         objs.append(obj)
         if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(sp), hdr):
             extra = ["-Xptxas", "-v"] if ptxas_info and src.endswith(".cu") else []
-            cmd = [NVCC] + CUFLAGS + extra + ["-c", sp, "-o", obj]
+            cmd = [NVCC] + CUFLAGS + [f"-D{d}" for d in defines] + extra + ["-c", sp, "-o", obj]
             if src.endswith(".cpp"):
                 cmd = [NVCC, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-x", "c++", "-c", sp, "-o", obj]
             jobs.append(cmd)

@@ -209,11 +209,21 @@ __global__ void k_partition(const mpsm_run_t* __restrict__ priv, const mpsm_run_
     splits[g] = t;
 }
 
-struct MergeSmem {
-    uint64_t rk[MJ_TILE], rp[MJ_TILE];  // R part of the tile at [0, nR), W part at [nR, nR+nW)
-    uint64_t red[3][MJ_THREADS / 32];
-    TileSplit tile;
+// two tile buffers: tile g+gridDim streams in (cp.async) while tile g merges
+struct MergeStage {
+    uint64_t k[MJ_TILE], p[MJ_TILE];  // R part of the tile at [0, nR), W part at [nR, nR+nW)
 };
+struct MergeSmem {
+    MergeStage st[2];
+    uint64_t red[3][MJ_THREADS / 32];
+};
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
 __device__ __forceinline__ void flush_pair(MergeSmem& sm, uint64_t* __restrict__ out, int pair, uint64_t count,
                                            uint64_t best, uint64_t csum) {
@@ -221,7 +231,6 @@ __device__ __forceinline__ void flush_pair(MergeSmem& sm, uint64_t* __restrict__
     count = warp_sum(count);
     csum = warp_sum(csum);
     best = warp_max_u64(best);
-    __syncthreads();
     if (lane == 0) {
         sm.red[0][warp] = count;
         sm.red[1][warp] = best;
@@ -242,7 +251,37 @@ __device__ __forceinline__ void flush_pair(MergeSmem& sm, uint64_t* __restrict__
             atomicAdd((unsigned long long*)(o + MPSM_PAIR_CHECKSUM), (unsigned long long)s);
         }
     }
+    __syncthreads();
 }
+
+__device__ __forceinline__ void load_tile_async(MergeStage& st, const TileSplit& t, const mpsm_run_t* __restrict__ priv,
+                                                const mpsm_run_t* __restrict__ pub, int n_pub,
+                                                const PairWin* __restrict__ win) {
+    const mpsm_run_t r = priv[t.pair / n_pub];
+    const mpsm_run_t s = pub[t.pair % n_pub];
+    const int64_t wstart = win[t.pair].start;
+    const int nR = (int)(t.i1 - t.i0), nW = (int)(t.j1 - t.j0);
+    const uint64_t* rk = r.keys + t.i0;
+    const uint64_t* rp = r.pays + t.i0;
+    const uint64_t* wk = s.keys + wstart + t.j0;
+    const uint64_t* wp = s.pays + wstart + t.j0;
+    for (int x = threadIdx.x; x < nR; x += MJ_THREADS) {
+        cp_async8(&st.k[x], rk + x);
+        cp_async8(&st.p[x], rp + x);
+    }
+    for (int x = threadIdx.x; x < nW; x += MJ_THREADS) {
+        cp_async8(&st.k[nR + x], wk + x);
+        cp_async8(&st.p[nR + x], wp + x);
+    }
+}
+
+#ifdef MPSM_DBG_TIMING
+__device__ long long g_mj_ts[1 << 20][6];
+#define MJ_TS(i) \
+    if (MODE == 0 && tid == 0 && g < (1 << 20)) g_mj_ts[g][i] = clock64();
+#else
+#define MJ_TS(i)
+#endif
 
 // MODE 0: aggregate into pair records; MODE 1: per-tile counts only;
 // MODE 2: emit pairs at tile_out[g] + thread offset
@@ -261,58 +300,53 @@ __global__ void __launch_bounds__(MJ_THREADS) k_merge(const mpsm_run_t* __restri
     const int64_t ntiles = *total;
     int cur_pair = -1;
     uint64_t count = 0, best = 0, csum = 0;
+    int buf = 0;
 
-    for (int64_t g = blockIdx.x; g < ntiles; g += gridDim.x) {
-        __syncthreads();  // previous tile fully consumed
-        if (tid == 0) sm.tile = splits[g];
-        __syncthreads();
-        const TileSplit t = sm.tile;
+    int64_t g = blockIdx.x;
+    if (g < ntiles) load_tile_async(sm.st[0], splits[g], priv, pub, n_pub, win);
+    cp_async_commit();
+    for (; g < ntiles; g += gridDim.x) {
+        MJ_TS(0)
+        const int64_t gn = g + gridDim.x;
+        if (gn < ntiles) load_tile_async(sm.st[buf ^ 1], splits[gn], priv, pub, n_pub, win);
+        cp_async_commit();
+        const TileSplit t = splits[g];
         if (MODE == 0 && t.pair != cur_pair) {
             if (cur_pair >= 0) flush_pair(sm, out_pairs, cur_pair, count, best, csum);
             cur_pair = t.pair;
             count = best = csum = 0;
         }
         const mpsm_run_t r = priv[t.pair / n_pub];
-        const mpsm_run_t s = pub[t.pair % n_pub];
-        const int64_t wstart = win[t.pair].start;
+        MJ_TS(1)
+        cp_async_wait_1();  // this thread's copies of tile g landed
+        __syncthreads();    // ... and everyone else's
+        MJ_TS(2)
         const int nR = (int)(t.i1 - t.i0), nW = (int)(t.j1 - t.j0);
-        const uint64_t* __restrict__ gwk = s.keys + wstart + t.j0;
-        const uint64_t* __restrict__ gwp = s.pays + wstart + t.j0;
-        for (int x = tid; x < nR; x += MJ_THREADS) {
-            sm.rk[x] = ld_stream(r.keys + t.i0 + x);
-            sm.rp[x] = ld_stream(r.pays + t.i0 + x);
-        }
-        for (int x = tid; x < nW; x += MJ_THREADS) {
-            sm.rk[nR + x] = ld_stream(gwk + x);
-            sm.rp[nR + x] = ld_stream(gwp + x);
-        }
-        __syncthreads();
-        const uint64_t* Rk = sm.rk;
-        const uint64_t* Wk = sm.rk + nR;
-        const uint64_t* Rp = sm.rp;
-        const uint64_t* Wp = sm.rp + nR;
+        const uint64_t* Rk = sm.st[buf].k;
+        const uint64_t* Wk = sm.st[buf].k + nR;
+        const uint64_t* Rp = sm.st[buf].p;
+        const uint64_t* Wp = sm.st[buf].p + nR;
         const int L = nR + nW;
         const int k0 = min(tid * MJ_ITEMS, L);
         const int k1 = min(k0 + MJ_ITEMS, L);
         // per-thread split inside the tile
         int lo = k0 > nW ? k0 - nW : 0, hi = k0 < nR ? k0 : nR;
         while (lo < hi) {
-            int mid = (lo + hi) >> 1;
+            const int mid = (lo + hi) >> 1;
             if (Rk[mid] <= Wk[k0 - 1 - mid]) lo = mid + 1;
             else hi = mid;
         }
-        int ri = lo, wj = k0 - lo;
+        MJ_TS(3)
         int64_t my_pairs = 0;
         int64_t emit_base = 0;
         for (int pass = (MODE == 2 ? 0 : 1); pass < 2; ++pass) {
             // MODE 2 runs the thread's merge twice: count, then emit at its offset
             if (MODE == 2 && pass == 1) {
-                // block exclusive scan of my_pairs
-                int64_t v = my_pairs;
+                const int64_t v = my_pairs;
                 const int lane = tid & 31, warp = tid >> 5;
                 int64_t incl = v;
                 for (int o = 1; o < 32; o <<= 1) {
-                    int64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+                    const int64_t u = __shfl_up_sync(0xffffffffu, incl, o);
                     if (lane >= o) incl += u;
                 }
                 if (lane == 31) warp_cnt[warp] = incl;
@@ -320,19 +354,17 @@ __global__ void __launch_bounds__(MJ_THREADS) k_merge(const mpsm_run_t* __restri
                 int64_t before = 0;
                 for (int w = 0; w < warp; ++w) before += warp_cnt[w];
                 emit_base = tile_cnt[g] + before + incl - v;  // tile_cnt holds the tile's output offset here
-                ri = lo;
-                wj = k0 - lo;
             }
             int64_t e = 0;
-            int ri2 = ri, wj2 = wj;
+            int ri = lo, wj = k0 - lo;
             for (int step = k0; step < k1; ++step) {
-                if (ri2 < nR && (wj2 >= nW || Rk[ri2] <= Wk[wj2])) {
-                    ++ri2;
+                if (ri < nR && (wj >= nW || Rk[ri] <= Wk[wj])) {
+                    ++ri;
                     continue;
                 }
-                const uint64_t skey = Wk[wj2];
-                const uint64_t spay = Wp[wj2];
-                int64_t gi = t.i0 + ri2 - 1;  // walk back over the equal-key R group
+                const uint64_t skey = Wk[wj];
+                const uint64_t spay = Wp[wj];
+                int64_t gi = t.i0 + ri - 1;  // walk back over the equal-key R group
                 while (gi >= 0) {
                     const bool in_tile = gi >= t.i0;
                     const uint64_t rk = in_tile ? Rk[gi - t.i0] : r.keys[gi];
@@ -353,12 +385,12 @@ __global__ void __launch_bounds__(MJ_THREADS) k_merge(const mpsm_run_t* __restri
                     }
                     --gi;
                 }
-                ++wj2;
+                ++wj;
             }
             my_pairs = e;
         }
         if (MODE == 1) {
-            int64_t c = warp_sum((unsigned long long)my_pairs);
+            const int64_t c = warp_sum((unsigned long long)my_pairs);
             if ((tid & 31) == 0) warp_cnt[tid >> 5] = c;
             __syncthreads();
             if (tid == 0) {
@@ -367,6 +399,10 @@ __global__ void __launch_bounds__(MJ_THREADS) k_merge(const mpsm_run_t* __restri
                 tile_cnt[g] = sum;
             }
         }
+        MJ_TS(4)
+        __syncthreads();  // everyone is done with st[buf] before it is refilled
+        MJ_TS(5)
+        buf ^= 1;
     }
     if (MODE == 0 && cur_pair >= 0) flush_pair(sm, out_pairs, cur_pair, count, best, csum);
 }
@@ -445,15 +481,20 @@ static size_t join_ws_size(int n_priv, int n_pub, int64_t mt) {
 }
 
 template <int MODE>
-static int launch_merge(const JoinWs& w, int n_pub, int swap, uint64_t* d_pairs, uint64_t* emit_out, int grid,
+static int launch_merge(const JoinWs& w, int n_pub, int swap, uint64_t* d_pairs, uint64_t* emit_out, int64_t mt,
                         cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    static int per_sm = 0;
+    if (per_sm == 0) {
         MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_merge<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   (int)sizeof(MergeSmem)),
                              "smem attr"));
-        attr = true;
+        MPSM_TRY(cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge<MODE>, MJ_THREADS,
+                                                                           sizeof(MergeSmem)),
+                             "occupancy"));
+        if (per_sm < 1) per_sm = 1;
     }
+    // persistent grid: exactly the resident CTAs
+    const int grid = (int)std::min<int64_t>((int64_t)num_sms() * per_sm, mt);
     ProfScope ps(MODE == 0 ? "merge" : (MODE == 1 ? "merge_count" : "merge_emit"), st);
     k_merge<MODE><<<grid, MJ_THREADS, sizeof(MergeSmem), st>>>(w.d_priv, w.d_pub, n_pub, w.win, w.splits, w.total,
                                                                 swap, d_pairs, w.tile_cnt, emit_out);
@@ -472,6 +513,12 @@ extern "C" int mpsm_interp_lower_bound(const uint64_t* keys, int64_t n, const ui
                                                                                         d_index, d_probes);
     return check_launch("k_interp_batch");
 }
+
+#ifdef MPSM_DBG_TIMING
+extern "C" int mpsm_dbg_mj_ts(long long* host, int ntiles) {
+    return cuda_status(cudaMemcpyFromSymbol(host, g_mj_ts, sizeof(long long) * 6 * (size_t)ntiles), "dbg");
+}
+#endif
 
 extern "C" int mpsm_join_workspace_bytes(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub,
                                          size_t* bytes) {
@@ -505,17 +552,15 @@ extern "C" int mpsm_join_pairs(const mpsm_run_t* priv, int n_priv, const mpsm_ru
                                                                w.splits);
     }
     MPSM_TRY(check_launch("k_partition"));
-    // persistent grid: a few CTAs per SM
-    int grid = (int)std::min<int64_t>((int64_t)num_sms() * 6, mt);
     if (mode != MPSM_MODE_MATERIALIZE || d_out == nullptr) {
-        MPSM_TRY(launch_merge<0>(w, n_pub, swap, d_pairs, nullptr, grid, st));
+        MPSM_TRY(launch_merge<0>(w, n_pub, swap, d_pairs, nullptr, mt, st));
         return MPSM_OK;
     }
     // materialize: aggregates, per-tile counts, offsets, emission
-    MPSM_TRY(launch_merge<0>(w, n_pub, swap, d_pairs, nullptr, grid, st));
-    MPSM_TRY(launch_merge<1>(w, n_pub, swap, d_pairs, nullptr, grid, st));
+    MPSM_TRY(launch_merge<0>(w, n_pub, swap, d_pairs, nullptr, mt, st));
+    MPSM_TRY(launch_merge<1>(w, n_pub, swap, d_pairs, nullptr, mt, st));
     k_emit_offsets<<<1, 1024, 0, st>>>(w.tile_cnt, w.splits, w.total, d_pairs, w.grand);
     MPSM_TRY(check_launch("k_emit_offsets"));
     (void)cap;  // the caller sized d_out from the counts of a first call
-    return launch_merge<2>(w, n_pub, swap, d_pairs, d_out, grid, st);
+    return launch_merge<2>(w, n_pub, swap, d_pairs, d_out, mt, st);
 }

@@ -29,13 +29,28 @@
 
 namespace mpsm {
 
-constexpr int SORT_THREADS = 256;
-constexpr int SORT_ITEMS = 16;
+// tile shape and digit width (compile-time; tools/variants.py builds variants)
+#ifndef MPSM_SORT_THREADS
+#define MPSM_SORT_THREADS 512
+#endif
+#ifndef MPSM_SORT_ITEMS
+#define MPSM_SORT_ITEMS 12
+#endif
+#ifndef MPSM_SORT_MAX_BITS
+#define MPSM_SORT_MAX_BITS 9
+#endif
+#ifndef MPSM_SORT_MIN_BLOCKS
+#define MPSM_SORT_MIN_BLOCKS 2
+#endif
+constexpr int SORT_THREADS = MPSM_SORT_THREADS;
+constexpr int SORT_ITEMS = MPSM_SORT_ITEMS;
 constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;
 constexpr int SORT_WARPS = SORT_THREADS / 32;
-constexpr int MAX_BITS = 9;
+constexpr int MAX_BITS = MPSM_SORT_MAX_BITS;
 constexpr int MAX_BINS = 1 << MAX_BITS;
 constexpr int MAX_PASSES = 8;
+constexpr int HIST_THREADS = 512;
+constexpr int HIST_UNROLL = 8;
 
 // look-back status word: [63:62] flag, [61:40] epoch, [39:0] count
 constexpr uint64_t FLAG_AGG = 1ull << 62;
@@ -74,23 +89,40 @@ static uint32_t next_epoch(bool* wrapped) {
 }
 
 // ------------------------------------------------------------ upfront sweep
-__global__ void __launch_bounds__(512) k_upfront_hist(const uint64_t* __restrict__ keys, int64_t n, uint64_t lower,
-                                                      uint64_t span_m1, PassPlan plan,
-                                                      unsigned long long* __restrict__ g_hist,
-                                                      unsigned long long* __restrict__ d_bad) {
+// one read of every key: digit histograms of all passes + domain check.
+// HIST_UNROLL independent coalesced loads per thread keep enough bytes in
+// flight (the first version waited on one load per iteration).
+__global__ void __launch_bounds__(HIST_THREADS) k_upfront_hist(const uint64_t* __restrict__ keys, int64_t n,
+                                                               uint64_t lower, uint64_t span_m1, PassPlan plan,
+                                                               unsigned long long* __restrict__ g_hist,
+                                                               unsigned long long* __restrict__ d_bad) {
     __shared__ uint32_t sh[MAX_PASSES * MAX_BINS];
     const int nb = plan.npasses * MAX_BINS;
     for (int i = threadIdx.x; i < nb; i += blockDim.x) sh[i] = 0;
     __syncthreads();
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        uint64_t nk = ld_stream(keys + i) - lower;
-        // out-of-domain keys are flagged but still counted, so the scatter
-        // passes stay in bounds; the caller discards the result
-        if (nk > span_m1 && d_bad) atomicMin(d_bad, (unsigned long long)i);
-        for (int p = 0; p < plan.npasses; ++p) {
-            uint32_t d = (uint32_t)(nk >> plan.shift[p]) & ((1u << plan.bits[p]) - 1u);
-            atomicAdd(&sh[p * MAX_BINS + d], 1u);
+    constexpr int CHUNK = HIST_THREADS * HIST_UNROLL;
+    for (int64_t base = (int64_t)blockIdx.x * CHUNK; base < n; base += (int64_t)gridDim.x * CHUNK) {
+        uint64_t k[HIST_UNROLL];
+#pragma unroll
+        for (int u = 0; u < HIST_UNROLL; ++u) {
+            int64_t i = base + u * HIST_THREADS + threadIdx.x;
+            k[u] = i < n ? ld_stream(keys + i) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < HIST_UNROLL; ++u) {
+            int64_t i = base + u * HIST_THREADS + threadIdx.x;
+            if (i >= n) continue;
+            uint64_t nk = k[u] - lower;
+            // out-of-domain keys are flagged but still counted so the scatter
+            // passes stay in bounds; the caller discards the result
+            if (nk > span_m1 && d_bad) atomicMin(d_bad, (unsigned long long)i);
+#pragma unroll
+            for (int p = 0; p < MAX_PASSES; ++p) {
+                if (p < plan.npasses) {
+                    uint32_t d = (uint32_t)(nk >> plan.shift[p]) & ((1u << plan.bits[p]) - 1u);
+                    atomicAdd(&sh[p * MAX_BINS + d], 1u);
+                }
+            }
         }
     }
     __syncthreads();
@@ -134,15 +166,17 @@ struct PartitionDigit {
     int nbuckets;
     __device__ __forceinline__ uint32_t operator()(uint64_t key) const {
         uint64_t b = (key - lower) >> shift;
-        // out-of-domain keys were rejected by the histogram; clamp defensively
+        // out-of-domain keys were counted in the clamped bucket by the histogram
         if (b >= (uint64_t)nbuckets) b = nbuckets - 1;
         return (uint32_t)__ldg(sp + b);
     }
 };
 
 // -------------------------------------------------------------- one pass
-// smem: warp histograms alias the staging buffer (they are dead once every
-// thread has its staging positions)
+// smem: the warp histograms alias the staging buffer (they are dead once
+// every thread holds its staging positions).  Keys and payloads are staged
+// one after the other through the same buffer; dig[] remembers each staged
+// slot's digit for the payload write-out.
 struct PassSmem {
     union {
         uint32_t whist[SORT_WARPS][MAX_BINS];
@@ -150,19 +184,48 @@ struct PassSmem {
     } u;
     uint16_t dig[SORT_TILE];
     uint32_t tile_off[MAX_BINS];  // exclusive prefix of tile counts over digits
-    int64_t gdelta[MAX_BINS];     // global position of staged slot i = gdelta[d] + i
+    int64_t gdelta[MAX_BINS];     // global slot of staged position i = gdelta[d] + i
     uint32_t ticket;
 };
 
+__device__ __forceinline__ void ld_volatile_v2(const uint64_t* p, uint64_t& a, uint64_t& b) {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+
+// peers of this lane among the lanes of vmask holding the same digit: one
+// ballot per digit bit (cheaper than match.any on sm_100)
+__device__ __forceinline__ unsigned ballot_match(uint32_t d, int bits, unsigned vmask) {
+#if defined(MPSM_DBG_NO_MATCH)
+    return vmask & (1u << (threadIdx.x & 31));
+#elif defined(MPSM_SORT_MATCH_ANY)
+    return __match_any_sync(0xffffffffu, d) & vmask;
+#endif
+    unsigned peers = vmask;
+#pragma unroll
+    for (int b = 0; b < MAX_BITS; ++b) {
+        if (b < bits) {
+            const bool set = (d >> b) & 1u;
+            const unsigned bal = __ballot_sync(0xffffffffu, set);
+            peers &= set ? bal : ~bal;
+        }
+    }
+    return peers;
+}
+
+#ifdef MPSM_DBG_TIMING
+__device__ long long g_phase_ts[1 << 22][8];
+#define PHASE_TS(i) \
+    if (tid == 0 && tile < (1u << 22)) g_phase_ts[tile][i] = clock64();
+#else
+#define PHASE_TS(i)
+#endif
+
 template <class DigitOp>
-__global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t* __restrict__ in_k,
-                                                           const uint64_t* __restrict__ in_p,
-                                                           uint64_t* __restrict__ out_k, uint64_t* __restrict__ out_p,
-                                                           int64_t n, DigitOp digit, int nbins,
-                                                           const int64_t* __restrict__ bin_base,
-                                                           uint64_t* __restrict__ status,
-                                                           unsigned int* __restrict__ ticket_ctr, uint32_t epoch,
-                                                           int64_t* __restrict__ written) {
+__global__ void __launch_bounds__(SORT_THREADS, MPSM_SORT_MIN_BLOCKS) k_onesweep(
+    const uint64_t* __restrict__ in_k, const uint64_t* __restrict__ in_p, uint64_t* __restrict__ out_k,
+    uint64_t* __restrict__ out_p, int64_t n, DigitOp digit, int bits, int nbins, const int64_t* __restrict__ bin_base,
+    uint64_t* __restrict__ status, int64_t st_stride, unsigned int* __restrict__ ticket_ctr, uint32_t epoch,
+    int64_t* __restrict__ written) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PassSmem& sm = *reinterpret_cast<PassSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -173,61 +236,69 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t* __res
     const uint32_t tile = sm.ticket;
     const int64_t tile_base = (int64_t)tile * SORT_TILE;
     const int64_t warp_base = tile_base + (int64_t)warp * (32 * SORT_ITEMS);
+    const bool full = tile_base + SORT_TILE <= n;
+    PHASE_TS(0)
 
-    // ---- load keys (warp-striped: item k of lane l is warp_base + 32k + l)
+    // ---- keys, warp-striped: item k of lane l is warp_base + 32k + l
     uint64_t key[SORT_ITEMS];
-    uint32_t pos[SORT_ITEMS];
+    uint32_t pos[SORT_ITEMS];  // digit << 20 | rank until offsets are known
 #pragma unroll
     for (int k = 0; k < SORT_ITEMS; ++k) {
-        int64_t idx = warp_base + 32 * k + lane;
-        key[k] = idx < n ? ld_stream(in_k + idx) : 0;
+        const int64_t idx = warp_base + 32 * k + lane;
+        key[k] = (full || idx < n) ? ld_stream(in_k + idx) : 0;
     }
-    // ---- stable rank within the warp's sub-tile
+    PHASE_TS(1)
+    // ---- stable rank within the warp: ballot match + running per-warp counts
     uint32_t* wh = sm.u.whist[warp];
+    const unsigned lt = lanemask_lt();
 #pragma unroll
     for (int k = 0; k < SORT_ITEMS; ++k) {
-        int64_t idx = warp_base + 32 * k + lane;
-        const bool valid = idx < n;
-        const unsigned vmask = __ballot_sync(0xffffffffu, valid);
-        uint32_t rank = 0;
-        if (valid) {
-            uint32_t d = digit(key[k]);
-            unsigned peers = __match_any_sync(vmask, d);
-            uint32_t before = wh[d];
-            rank = before + __popc(peers & lanemask_lt());
-            __syncwarp(vmask);
-            if ((peers & lanemask_lt()) == 0) wh[d] = before + __popc(peers);
-            __syncwarp(vmask);
-            pos[k] = rank | (d << 20);  // stash digit until offsets exist
-        } else {
-            pos[k] = 0xffffffffu;
-        }
+        const int64_t idx = warp_base + 32 * k + lane;
+        const bool valid = full || idx < n;
+        const unsigned vmask = full ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
+        const uint32_t d = digit(key[k]);
+        unsigned peers = ballot_match(d, bits, vmask);  // every lane votes (full-mask ballots)
+        if (!valid) peers = 0;
+        uint32_t before = 0;
+        if (peers) before = wh[d];
+        __syncwarp();
+        if (peers && (peers & lt) == 0) wh[d] = before + __popc(peers);
+        __syncwarp();
+        pos[k] = peers ? ((d << 20) | (before + __popc(peers & lt))) : 0xffffffffu;
     }
     __syncthreads();
 
-    // ---- per digit: exclusive scan over warps, tile count, publish aggregate
-    uint32_t my_cnt[MAX_BINS / SORT_THREADS > 0 ? MAX_BINS / SORT_THREADS : 1];
+    PHASE_TS(2)
+    // ---- per digit (DPT per thread): column sum (independent loads), publish
+    // the aggregate as early as possible, then the exclusive scan over warps
+    constexpr int DPT = (MAX_BINS + SORT_THREADS - 1) / SORT_THREADS;
+    uint32_t my_cnt[DPT];
 #pragma unroll
-    for (int j = 0; j < MAX_BINS / SORT_THREADS; ++j) {
+    for (int j = 0; j < DPT; ++j) {
         const int d = tid + j * SORT_THREADS;
-        uint32_t run = 0;
+        my_cnt[j] = 0;
         if (d < nbins) {
+            uint32_t col[SORT_WARPS];
+#pragma unroll
+            for (int w = 0; w < SORT_WARPS; ++w) col[w] = sm.u.whist[w][d];
+#pragma unroll
+            for (int w = 0; w < SORT_WARPS; ++w) my_cnt[j] += col[w];
+            const uint64_t word =
+                (uint64_t)my_cnt[j] | ((uint64_t)epoch << EPOCH_SHIFT) | (tile == 0 ? FLAG_PREFIX : FLAG_AGG);
+            st_volatile_u64(status + (size_t)tile * nbins + d, word);
+            uint32_t run = 0;
 #pragma unroll
             for (int w = 0; w < SORT_WARPS; ++w) {
-                uint32_t c = sm.u.whist[w][d];
                 sm.u.whist[w][d] = run;
-                run += c;
+                run += col[w];
             }
-            uint64_t word = (uint64_t)run | ((uint64_t)epoch << EPOCH_SHIFT) | (tile == 0 ? FLAG_PREFIX : FLAG_AGG);
-            st_volatile_u64(status + (size_t)tile * nbins + d, word);
         }
-        my_cnt[j] = run;
-        sm.tile_off[d] = run;
+        if (d < MAX_BINS) sm.tile_off[d] = my_cnt[j];
     }
+    (void)st_stride;
     __syncthreads();
-    // ---- tile-local exclusive scan of counts over digits (single warp-based scan)
+    // ---- tile-local exclusive scan of counts over digits (warp 0)
     if (warp == 0) {
-        // each lane owns MAX_BINS/32 consecutive digits
         constexpr int PER = MAX_BINS / 32;
         uint32_t loc[PER];
         uint32_t sum = 0;
@@ -239,47 +310,60 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t* __res
         uint32_t incl = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += v;
         }
         uint32_t run = incl - sum;
 #pragma unroll
         for (int q = 0; q < PER; ++q) {
-            uint32_t c = loc[q];
+            const uint32_t c = loc[q];
             sm.tile_off[lane * PER + q] = run;
             run += c;
         }
     }
-    // ---- decoupled look-back for this tile's digits
+    PHASE_TS(3)
+    // ---- decoupled look-back for this thread's digits, two predecessors per step
 #pragma unroll
-    for (int j = 0; j < MAX_BINS / SORT_THREADS; ++j) {
+    for (int j = 0; j < DPT; ++j) {
         const int d = tid + j * SORT_THREADS;
         if (d < nbins) {
             uint64_t excl = 0;
+#ifdef MPSM_DBG_NO_LOOKBACK
+            if (false) {
+#else
             if (tile > 0) {
+#endif
                 int64_t t = (int64_t)tile - 1;
                 while (true) {
-                    uint64_t w = ld_volatile_u64(status + (size_t)t * nbins + d);
-                    if (((w >> EPOCH_SHIFT) & EPOCH_MASK) != epoch || (w >> 62) == 0) continue;
-                    excl += w & VALUE_MASK;
-                    if ((w >> 62) == 2) break;
+                    const uint64_t w1 = ld_volatile_u64(status + (size_t)t * nbins + d);
+                    const uint64_t w2 = t > 0 ? ld_volatile_u64(status + (size_t)(t - 1) * nbins + d) : 0;
+                    if (((w1 >> EPOCH_SHIFT) & EPOCH_MASK) != epoch || (w1 >> 62) == 0) continue;
+                    excl += w1 & VALUE_MASK;
+                    if ((w1 >> 62) == 2) break;
+                    --t;
+                    if (((w2 >> EPOCH_SHIFT) & EPOCH_MASK) != epoch || (w2 >> 62) == 0) continue;
+                    excl += w2 & VALUE_MASK;
+                    if ((w2 >> 62) == 2) break;
                     --t;
                 }
                 st_volatile_u64(status + (size_t)tile * nbins + d,
                                 (excl + my_cnt[j]) | ((uint64_t)epoch << EPOCH_SHIFT) | FLAG_PREFIX);
             }
-            sm.gdelta[d] = bin_base[d] + (int64_t)excl;  // tile_off subtracted below
-            if (written && my_cnt[j]) atomicAdd((unsigned long long*)(written + d), (unsigned long long)my_cnt[j]);
+            sm.gdelta[d] = bin_base[d] + (int64_t)excl;
+            if (written && my_cnt[j])
+                atomicAdd((unsigned long long*)(written + d), (unsigned long long)my_cnt[j]);
         }
     }
     __syncthreads();
+    PHASE_TS(4)
     for (int d = tid; d < nbins; d += SORT_THREADS) sm.gdelta[d] -= (int64_t)sm.tile_off[d];
-    // ---- staging positions
+    // ---- staging positions (whist now holds the warp-exclusive offsets)
 #pragma unroll
     for (int k = 0; k < SORT_ITEMS; ++k) {
         if (pos[k] != 0xffffffffu) {
-            uint32_t d = pos[k] >> 20;
-            pos[k] = sm.tile_off[d] + sm.u.whist[warp][d] + (pos[k] & 0xfffffu);
+            const uint32_t dk = pos[k] >> 20;
+            pos[k] = sm.tile_off[dk] + sm.u.whist[warp][dk] + (pos[k] & 0xfffffu);
+            key[k] |= 0;  // keep key live
         }
     }
     __syncthreads();  // whist dead from here; stage aliases it
@@ -291,32 +375,239 @@ __global__ void __launch_bounds__(SORT_THREADS) k_onesweep(const uint64_t* __res
         }
     }
     __syncthreads();
-    const int valid_in_tile = (int)min((int64_t)SORT_TILE, n - tile_base);
-#pragma unroll 4
-    for (int i = tid; i < valid_in_tile; i += SORT_THREADS) {
-        out_k[sm.gdelta[sm.dig[i]] + i] = sm.u.stage[i];
-    }
-    // ---- payloads follow the same permutation
+    PHASE_TS(5)
+    // payload loads go out now and land while the keys are written
     uint64_t pay[SORT_ITEMS];
 #pragma unroll
     for (int k = 0; k < SORT_ITEMS; ++k) {
-        int64_t idx = warp_base + 32 * k + lane;
-        pay[k] = idx < n ? ld_stream(in_p + idx) : 0;
+        const int64_t idx = warp_base + 32 * k + lane;
+        pay[k] = (full || idx < n) ? ld_stream(in_p + idx) : 0;
     }
+    const int valid_in_tile = full ? SORT_TILE : (int)(n - tile_base);
+#pragma unroll 4
+    for (int i = tid; i < valid_in_tile; i += SORT_THREADS) out_k[sm.gdelta[sm.dig[i]] + i] = sm.u.stage[i];
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < SORT_ITEMS; ++k)
         if (pos[k] != 0xffffffffu) sm.u.stage[pos[k]] = pay[k];
     __syncthreads();
 #pragma unroll 4
-    for (int i = tid; i < valid_in_tile; i += SORT_THREADS) {
-        out_p[sm.gdelta[sm.dig[i]] + i] = sm.u.stage[i];
+    for (int i = tid; i < valid_in_tile; i += SORT_THREADS) out_p[sm.gdelta[sm.dig[i]] + i] = sm.u.stage[i];
+    PHASE_TS(6)
+}
+
+// ------------------------------------------------ persistent prefetching pass
+// One CTA per SM loops over tiles in ticket order.  While it ranks, looks
+// back and scatters tile t, the cp.async copies of its next tile are in
+// flight into the other half of a double buffer, so HBM stays busy through
+// the latency-bound phases (the non-persistent kernel above leaves it idle:
+// ncu showed 28 % of stall samples waiting on the first key of each tile).
+// Look-back words are laid out [digit][tile] so one 32-B read fetches four
+// predecessors of a digit.
+struct PfSmem {
+    uint64_t k[2][SORT_TILE];
+    uint64_t p[2][SORT_TILE];
+    uint32_t whist[SORT_WARPS][MAX_BINS];
+    uint16_t dig[SORT_TILE];
+    uint32_t tile_off[MAX_BINS];
+    int64_t gdelta[MAX_BINS];
+    uint32_t ticket[2];
+};
+
+__device__ __forceinline__ void cp_async8_g2s(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16_g2s(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+
+
+// copy tile `tile` (keys + payloads) into buffer slot b asynchronously
+__device__ __forceinline__ void pf_issue(PfSmem& sm, int b, uint32_t tile, const uint64_t* __restrict__ in_k,
+                                         const uint64_t* __restrict__ in_p, int64_t n, bool vec16) {
+    const int64_t base = (int64_t)tile * SORT_TILE;
+    const int cnt = (int)min((int64_t)SORT_TILE, n - base);
+    if (cnt <= 0) return;
+    if (vec16 && cnt == SORT_TILE) {
+        for (int i = threadIdx.x * 2; i < SORT_TILE; i += SORT_THREADS * 2) {
+            cp_async16_g2s(&sm.k[b][i], in_k + base + i);
+            cp_async16_g2s(&sm.p[b][i], in_p + base + i);
+        }
+    } else {
+        for (int i = threadIdx.x; i < cnt; i += SORT_THREADS) {
+            cp_async8_g2s(&sm.k[b][i], in_k + base + i);
+            cp_async8_g2s(&sm.p[b][i], in_p + base + i);
+        }
     }
+}
+
+template <class DigitOp>
+__global__ void __launch_bounds__(SORT_THREADS, 1) k_onesweep_pf(
+    const uint64_t* __restrict__ in_k, const uint64_t* __restrict__ in_p, uint64_t* __restrict__ out_k,
+    uint64_t* __restrict__ out_p, int64_t n, DigitOp digit, int bits, int nbins, const int64_t* __restrict__ bin_base,
+    uint64_t* __restrict__ status, int64_t st_stride, unsigned int* __restrict__ ticket_ctr, uint32_t epoch,
+    int64_t* __restrict__ written) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    PfSmem& sm = *reinterpret_cast<PfSmem*>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t ntiles = (n + SORT_TILE - 1) / SORT_TILE;
+    const bool vec16 = ((((uintptr_t)in_k) | ((uintptr_t)in_p)) & 15) == 0;
+    const unsigned lt = lanemask_lt();
+
+    if (tid == 0) sm.ticket[0] = atomicAdd(ticket_ctr, 1u);
+    __syncthreads();
+    int cur = 0;
+    uint32_t tile = sm.ticket[0];
+    if (tile < ntiles) pf_issue(sm, 0, tile, in_k, in_p, n, vec16);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+
+    while (tile < ntiles) {
+        // claim and start the next tile
+        if (tid == 0) sm.ticket[cur ^ 1] = atomicAdd(ticket_ctr, 1u);
+        for (int i = tid; i < SORT_WARPS * MAX_BINS; i += SORT_THREADS) (&sm.whist[0][0])[i] = 0;
+        __syncthreads();
+        const uint32_t next = sm.ticket[cur ^ 1];
+        if (next < ntiles) pf_issue(sm, cur ^ 1, next, in_k, in_p, n, vec16);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncthreads();  // tile `tile` is in buf[cur]
+
+        const int64_t tile_base = (int64_t)tile * SORT_TILE;
+        const bool full = tile_base + SORT_TILE <= n;
+        const int wb = warp * (32 * SORT_ITEMS);
+        uint64_t key[SORT_ITEMS];
+        uint32_t pos[SORT_ITEMS];
+        uint32_t* wh = sm.whist[warp];
+#pragma unroll
+        for (int k = 0; k < SORT_ITEMS; ++k) {
+            const int li = wb + 32 * k + lane;
+            const bool valid = full || tile_base + li < n;
+            key[k] = valid ? sm.k[cur][li] : 0;
+            const unsigned vmask = full ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
+            const uint32_t d = digit(key[k]);
+            unsigned peers = ballot_match(d, bits, vmask);
+            if (!valid) peers = 0;
+            uint32_t before = 0;
+            if (peers) before = wh[d];
+            __syncwarp();
+            if (peers && (peers & lt) == 0) wh[d] = before + __popc(peers);
+            __syncwarp();
+            pos[k] = peers ? ((d << 20) | (before + __popc(peers & lt))) : 0xffffffffu;
+        }
+        __syncthreads();
+        uint32_t my_cnt = 0;
+        const int d = tid;
+        if (d < nbins) {
+            uint32_t col[SORT_WARPS];
+#pragma unroll
+            for (int w = 0; w < SORT_WARPS; ++w) col[w] = sm.whist[w][d];
+#pragma unroll
+            for (int w = 0; w < SORT_WARPS; ++w) my_cnt += col[w];
+            st_volatile_u64(status + (size_t)d * st_stride + tile,
+                            (uint64_t)my_cnt | ((uint64_t)epoch << EPOCH_SHIFT) | (tile == 0 ? FLAG_PREFIX : FLAG_AGG));
+            uint32_t run = 0;
+#pragma unroll
+            for (int w = 0; w < SORT_WARPS; ++w) {
+                sm.whist[w][d] = run;
+                run += col[w];
+            }
+        }
+        if (d < MAX_BINS) sm.tile_off[d] = my_cnt;
+        __syncthreads();
+        if (warp == 0) {
+            constexpr int PER = MAX_BINS / 32;
+            uint32_t loc[PER];
+            uint32_t sum = 0;
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                loc[q] = sm.tile_off[lane * PER + q];
+                sum += loc[q];
+            }
+            uint32_t incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            uint32_t run = incl - sum;
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                const uint32_t c = loc[q];
+                sm.tile_off[lane * PER + q] = run;
+                run += c;
+            }
+        }
+        if (d < nbins) {
+            uint64_t excl = 0;
+            if (tile > 0) {
+                const uint64_t* row = status + (size_t)d * st_stride;
+                int64_t t = (int64_t)tile - 1;  // next predecessor to account for
+                bool done = false;
+                while (!done) {
+                    const int64_t g0 = t & ~(int64_t)3;
+                    uint64_t w[4];
+                    ld_volatile_v2(row + g0, w[0], w[1]);
+                    ld_volatile_v2(row + g0 + 2, w[2], w[3]);
+                    // walk t, t-1, ... down to g0 inside the group
+                    while (t >= g0) {
+                        const uint64_t v = w[t - g0];
+                        if (((v >> EPOCH_SHIFT) & EPOCH_MASK) != epoch || (v >> 62) == 0) break;  // not ready: reload
+                        excl += v & VALUE_MASK;
+                        if ((v >> 62) == 2) {
+                            done = true;
+                            break;
+                        }
+                        --t;
+                    }
+                }
+                st_volatile_u64(status + (size_t)d * st_stride + tile,
+                                (excl + my_cnt) | ((uint64_t)epoch << EPOCH_SHIFT) | FLAG_PREFIX);
+            }
+            sm.gdelta[d] = bin_base[d] + (int64_t)excl;
+            if (written && my_cnt) atomicAdd((unsigned long long*)(written + d), (unsigned long long)my_cnt);
+        }
+        __syncthreads();
+        if (d < nbins) sm.gdelta[d] -= (int64_t)sm.tile_off[d];
+        uint64_t pay[SORT_ITEMS];
+#pragma unroll
+        for (int k = 0; k < SORT_ITEMS; ++k) {
+            pay[k] = sm.p[cur][wb + 32 * k + lane];
+            if (pos[k] != 0xffffffffu) {
+                const uint32_t dk = pos[k] >> 20;
+                pos[k] = sm.tile_off[dk] + sm.whist[warp][dk] + (pos[k] & 0xfffffu);
+            }
+        }
+        __syncthreads();  // buf[cur] fully read into registers: stage in place
+#pragma unroll
+        for (int k = 0; k < SORT_ITEMS; ++k) {
+            if (pos[k] != 0xffffffffu) {
+                sm.k[cur][pos[k]] = key[k];
+                sm.p[cur][pos[k]] = pay[k];
+                sm.dig[pos[k]] = (uint16_t)digit(key[k]);
+            }
+        }
+        __syncthreads();
+        const int valid_in_tile = full ? SORT_TILE : (int)(n - tile_base);
+#pragma unroll 4
+        for (int i = tid; i < valid_in_tile; i += SORT_THREADS) {
+            const int64_t g = sm.gdelta[sm.dig[i]] + i;
+            out_k[g] = sm.k[cur][i];
+            out_p[g] = sm.p[cur][i];
+        }
+        __syncthreads();  // buf[cur] free for the tile after next
+        tile = next;
+        cur ^= 1;
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 static size_t pass_smem_bytes() { return sizeof(PassSmem); }
 
 static int64_t num_tiles(int64_t n) { return (n + SORT_TILE - 1) / SORT_TILE; }
+// look-back rows of the persistent kernel are 32-B aligned
+static int64_t status_stride(int64_t n) { return (std::max<int64_t>(num_tiles(n), 1) + 3) & ~(int64_t)3; }
 
 struct SortWorkspace {
     unsigned long long* hist;  // [MAX_PASSES][MAX_BINS]
@@ -330,7 +621,7 @@ static size_t sort_ws_bytes(int64_t n) {
     b += align_up(sizeof(unsigned long long) * MAX_PASSES * MAX_BINS);
     b += align_up(sizeof(int64_t) * MAX_PASSES * MAX_BINS);
     b += align_up(sizeof(unsigned int) * MAX_PASSES);
-    b += align_up(sizeof(uint64_t) * (size_t)std::max<int64_t>(num_tiles(n), 1) * MAX_BINS);
+    b += align_up(sizeof(uint64_t) * (size_t)status_stride(n) * MAX_BINS);
     return b;
 }
 
@@ -339,7 +630,7 @@ static bool carve_sort(void* ws, size_t bytes, int64_t n, SortWorkspace* out) {
     out->hist = c.take<unsigned long long>(MAX_PASSES * MAX_BINS);
     out->starts = c.take<int64_t>(MAX_PASSES * MAX_BINS);
     out->tickets = c.take<unsigned int>(MAX_PASSES);
-    out->status = c.take<uint64_t>((size_t)std::max<int64_t>(num_tiles(n), 1) * MAX_BINS);
+    out->status = c.take<uint64_t>((size_t)status_stride(n) * MAX_BINS);
     return c.ok;
 }
 
@@ -352,6 +643,11 @@ static int set_pass_smem() {
         MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_onesweep<PartitionDigit>,
                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem_bytes()),
                              "smem attr"));
+#ifdef MPSM_SORT_PERSISTENT
+        MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_onesweep_pf<RadixDigit>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PfSmem)),
+                             "smem attr"));
+#endif
         done = true;
     }
     return MPSM_OK;
@@ -360,13 +656,19 @@ static int set_pass_smem() {
 static int clear_status_if_wrapped(bool wrapped, uint64_t* status, int64_t n, cudaStream_t st) {
     if (!wrapped) return MPSM_OK;
     return cuda_status(
-        cudaMemsetAsync(status, 0, sizeof(uint64_t) * (size_t)std::max<int64_t>(num_tiles(n), 1) * MAX_BINS, st),
+        cudaMemsetAsync(status, 0, sizeof(uint64_t) * (size_t)status_stride(n) * MAX_BINS, st),
         "memset status");
 }
 
 }  // namespace mpsm
 
 using namespace mpsm;
+
+#ifdef MPSM_DBG_TIMING
+extern "C" int mpsm_dbg_phase_ts(long long* host, int ntiles) {
+    return cuda_status(cudaMemcpyFromSymbol(host, g_phase_ts, sizeof(long long) * 8 * (size_t)ntiles), "dbg");
+}
+#endif
 
 extern "C" int mpsm_sort_pass_count(int width_bits) { return plan_passes(width_bits).npasses; }
 
@@ -393,9 +695,9 @@ extern "C" int mpsm_sort_pairs(const uint64_t* in_keys, const uint64_t* in_pays,
     MPSM_TRY(cuda_status(cudaMemsetAsync(ws.hist, 0, sizeof(unsigned long long) * MAX_PASSES * MAX_BINS, st), "memset"));
     MPSM_TRY(cuda_status(cudaMemsetAsync(ws.tickets, 0, sizeof(unsigned int) * MAX_PASSES, st), "memset"));
     {
-        int grid = std::min<int64_t>(num_sms() * 4, (n + 511) / 512);
+        int grid = (int)std::min<int64_t>(num_sms() * 4, (n + HIST_THREADS * HIST_UNROLL - 1) / (HIST_THREADS * HIST_UNROLL));
         ProfScope ps("upfront_hist", st);
-        k_upfront_hist<<<grid, 512, 0, st>>>(in_keys, n, lower, span_m1, plan, ws.hist, d_bad);
+        k_upfront_hist<<<grid, HIST_THREADS, 0, st>>>(in_keys, n, lower, span_m1, plan, ws.hist, d_bad);
         MPSM_TRY(check_launch("k_upfront_hist"));
     }
     if (plan.npasses == 0) {  // one-value domain: already sorted
@@ -434,9 +736,15 @@ extern "C" int mpsm_sort_pairs(const uint64_t* in_keys, const uint64_t* in_pays,
         MPSM_TRY(clear_status_if_wrapped(wrapped, ws.status, n, st));
         RadixDigit dig{lower, plan.shift[i], (1u << plan.bits[i]) - 1u};
         ProfScope ps("onesweep", st);
+#ifdef MPSM_SORT_PERSISTENT
+        k_onesweep_pf<RadixDigit><<<num_sms(), SORT_THREADS, sizeof(PfSmem), st>>>(
+            src_k, src_p, dk, dp, n, dig, plan.bits[i], 1 << plan.bits[i], ws.starts + i * MAX_BINS, ws.status, status_stride(n),
+            ws.tickets + i, epoch, nullptr);
+#else
         k_onesweep<RadixDigit><<<(unsigned)tiles, SORT_THREADS, pass_smem_bytes(), st>>>(
-            src_k, src_p, dk, dp, n, dig, 1 << plan.bits[i], ws.starts + i * MAX_BINS, ws.status, ws.tickets + i,
-            epoch, nullptr);
+            src_k, src_p, dk, dp, n, dig, plan.bits[i], 1 << plan.bits[i], ws.starts + i * MAX_BINS, ws.status,
+            status_stride(n), ws.tickets + i, epoch, nullptr);
+#endif
         MPSM_TRY(check_launch("k_onesweep"));
         src_k = dk;
         src_p = dp;
@@ -449,7 +757,7 @@ extern "C" int mpsm_scatter_workspace_bytes(int64_t n, int npart, size_t* bytes)
     if (!bytes || n < 0 || npart < 1 || npart > MAX_BINS) return MPSM_ERR_ARG;
     size_t b = 0;
     b += align_up(sizeof(unsigned int) * 1);
-    b += align_up(sizeof(uint64_t) * (size_t)std::max<int64_t>(num_tiles(n), 1) * npart);
+    b += align_up(sizeof(uint64_t) * (size_t)status_stride(n) * npart);
     *bytes = b;
     return MPSM_OK;
 }
@@ -466,7 +774,7 @@ extern "C" int mpsm_scatter_chunk(const uint64_t* keys, const uint64_t* pays, in
     if (n == 0) return MPSM_OK;
     Carve c{(char*)workspace, ws_bytes};
     unsigned int* ticket = c.take<unsigned int>(1);
-    uint64_t* status = c.take<uint64_t>((size_t)std::max<int64_t>(num_tiles(n), 1) * npart);
+    uint64_t* status = c.take<uint64_t>((size_t)status_stride(n) * npart);
     if (!c.ok) {
         set_error("scatter workspace too small");
         return MPSM_ERR_ARG;
@@ -476,10 +784,13 @@ extern "C" int mpsm_scatter_chunk(const uint64_t* keys, const uint64_t* pays, in
     bool wrapped = false;
     uint32_t epoch = next_epoch(&wrapped);
     if (wrapped)
-        MPSM_TRY(cuda_status(cudaMemsetAsync(status, 0, sizeof(uint64_t) * (size_t)num_tiles(n) * npart, st), "memset"));
+        MPSM_TRY(cuda_status(cudaMemsetAsync(status, 0, sizeof(uint64_t) * (size_t)status_stride(n) * npart, st), "memset"));
     PartitionDigit dig{lower, shift, d_sp, nbuckets};
+    int pbits = 0;
+    while ((1 << pbits) < npart) ++pbits;
     ProfScope ps("scatter", st);
     k_onesweep<PartitionDigit><<<(unsigned)num_tiles(n), SORT_THREADS, pass_smem_bytes(), st>>>(
-        keys, pays, arena_keys, arena_pays, n, dig, npart, d_cursors, status, ticket, epoch, d_written);
+        keys, pays, arena_keys, arena_pays, n, dig, pbits, npart, d_cursors, status, status_stride(n), ticket, epoch,
+        d_written);
     return check_launch("k_onesweep<partition>");
 }

@@ -1,0 +1,42 @@
+"""Per-phase cycle breakdown of k_merge<0> (variant built with MPSM_DBG_TIMING):
+join of n_r x n_s FK inputs generated on the device, sorted by the library."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ["MPSM_LIB"] = os.path.join(ROOT, "build", "variants_dbg", "timing", "libmpsm_b200.so")
+from paper_1207_0145_b200 import _lib, device as D  # noqa: E402
+
+n_r, n_s = 100_000_000, 400_000_000
+dev = torch.device("cuda", 0)
+rk = (torch.randperm(n_r, device=dev) + 1).view(torch.uint64)
+rp = torch.randint(0, 1 << 32, (n_r,), device=dev).view(torch.uint64)
+sk = torch.randint(1, n_r + 1, (n_s,), device=dev).view(torch.uint64)
+sp = torch.randint(0, 1 << 32, (n_s,), device=dev).view(torch.uint64)
+D.ensure_device()
+bits = 27
+def srt(k, p):
+    o = [torch.empty_like(k) for _ in range(4)]
+    D.sort_pairs(k, p, 1, n_r - 1, bits, o[0], o[1], o[2], o[3], None)
+    return o[0], o[1]
+rk, rp = srt(rk, rp)
+sk, sp = srt(sk, sp)
+for _ in range(2):
+    rec = D.join_pairs([(rk, rp)], [(sk, sp)], False, 0)
+torch.cuda.synchronize()
+print("count", int(rec[0, 0].item()))
+L = _lib.load()
+ntiles = min((n_r + n_s) // 2304 + 1, 1 << 20)
+buf = np.zeros((ntiles, 6), np.int64)
+L.mpsm_dbg_mj_ts(buf.ctypes.data_as(ctypes.c_void_p), ntiles)
+buf = buf[buf[:, 5] > 0]
+d = np.diff(buf, axis=1)
+names = ["issue_prefetch", "wait_data", "mergepath_search", "merge_loop", "end_sync"]
+print("tiles", len(buf), "cycles/tile median", np.median(buf[:, 5] - buf[:, 0]))
+for i, nm in enumerate(names):
+    print(f"  {nm:18s} median {np.median(d[:, i]):8.0f} mean {np.mean(d[:, i]):8.0f} p90 {np.percentile(d[:, i], 90):8.0f}")

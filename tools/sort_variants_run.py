@@ -1,0 +1,45 @@
+"""Time mpsm_sort_pairs of every variant under build/variants (GPU box).
+
+    python tools/sort_variants_run.py [n] [bits]
+"""
+import ctypes
+import glob
+import os
+import subprocess
+import sys
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 400_000_000
+bits = int(sys.argv[2]) if len(sys.argv) > 2 else 27
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CHILD = r'''
+import os, sys, ctypes, torch
+sys.path.insert(0, os.environ["ROOT"])
+from paper_1207_0145_b200 import _lib, device as D
+n, bits = int(sys.argv[1]), int(sys.argv[2])
+dev = torch.device("cuda", 0)
+g = torch.Generator(device=dev); g.manual_seed(1)
+keys = torch.randint(0, 1 << bits, (n,), device=dev, generator=g, dtype=torch.int64).view(torch.uint64)
+pays = torch.arange(n, device=dev, dtype=torch.int64).view(torch.uint64)
+ok = torch.empty_like(keys); op = torch.empty_like(pays); tk = torch.empty_like(keys); tp = torch.empty_like(pays)
+D.ensure_device()
+res = []
+for it in range(4):
+    _lib.profile_enable(True)
+    a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    D.sort_pairs(keys, pays, 0, (1 << bits) - 1, bits, ok, op, tk, tp, None)
+    b.record(); torch.cuda.synchronize()
+    res.append((a.elapsed_time(b), _lib.profile_read("onesweep"), _lib.profile_read("upfront_hist")))
+srt = ok.view(torch.int64)
+sorted_ok = bool((srt[1:] >= srt[:-1]).all())
+best = min(res)
+ms, (os_ms, os_n), (h_ms, _) = best
+print(f"{os.environ['VNAME']:24s} total {ms:7.3f} ms  onesweep {os_ms:7.3f} ms/{os_n} = {os_ms/os_n:6.3f} ms/pass "
+      f"({32*n/(os_ms/os_n)/1e6:7.1f} GB/s)  hist {h_ms:6.3f} ms sorted={sorted_ok}", flush=True)
+'''
+for lib in sorted(glob.glob(os.path.join(ROOT, "build", "variants", "*", "libmpsm_b200.so"))):
+    name = os.path.basename(os.path.dirname(lib))
+    env = dict(os.environ, MPSM_LIB=lib, ROOT=ROOT, VNAME=name)
+    r = subprocess.run([sys.executable, "-c", CHILD, str(n), str(bits)], env=env, capture_output=True, text=True,
+                       timeout=300)
+    print(r.stdout.strip() or (name + " FAILED " + r.stderr[-800:]), flush=True)
