@@ -265,16 +265,22 @@ def impl_ours(args):
     torch.cuda.synchronize()
     launches = _lib.launch_count() - l0
     ms = ev0.elapsed_time(ev1) / args.steps
-    prof = {k: _lib.profile_read(k) for k in ("onesweep", "upfront_hist", "merge", "merge_partition")}
+    prof = {k: _lib.profile_read(k) for k in ("seg_scatter", "seg_count", "merge", "merge_partition")}
     _lib.profile_enable(False)
     clk = clocks.stop()
     value = n_tot / (ms / 1e3)
 
-    # roofline of the dominant kernel: onesweep pass = 16 B read + 16 B write per tuple
+    # roofline of the dominant kernel, the radix scatter pass (seg::k_scatter):
+    # algorithmic bytes per tuple = its reads + writes in the layout it runs:
+    # pairs 16 + 16; first pass of a packed sort 16 + 8; later packed passes 8 + 8
     wbits = dom.width_bits
     passes = _lib.load().mpsm_sort_pass_count(wbits)
-    onesweep_bytes = 32.0 * passes * (n_r + n_s) * args.steps
-    os_ms, os_n = prof["onesweep"]
+    from paper_1207_0145_b200 import engine as _eng
+
+    packed = _eng.PACK_RECORDS and 1 <= wbits <= 63
+    per_tuple = (24 + 16 * (passes - 1)) if packed else 32 * passes
+    onesweep_bytes = float(per_tuple) * (n_r + n_s) * args.steps
+    os_ms, os_n = prof["seg_scatter"]
     achieved = onesweep_bytes / (os_ms / 1e3) / 1e9 if os_ms > 0 else None
     peaks = {}
     try:
@@ -327,9 +333,10 @@ def impl_ours(args):
         "result": {"match_count": result[0], "aggregate_max": result[1], "checksum": hex(result[2]),
                    "matches_golden": parity},
         "phase_ms": {k: 1e3 * v / args.steps for k, v in phase.items()},
-        "roofline": {"bound": "hbm", "kernel": "k_onesweep (radix scatter pass)", "achieved": achieved,
+        "roofline": {"bound": "hbm", "kernel": "seg::k_scatter (radix scatter pass)", "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
-                     "traffic": None, "algorithmic_bytes_per_tuple_per_pass": 32, "passes_per_sort": passes,
+                     "traffic": None, "algorithmic_bytes_per_tuple_per_sort": per_tuple,
+                     "layout": "packed 8-B records" if packed else "(key, payload) pairs", "passes_per_sort": passes,
                      "launches": os_n, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
         "step_canonical_gbs": step_gbs,
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},

@@ -92,6 +92,16 @@ int mpsm_sort_pairs(const uint64_t* in_keys, const uint64_t* in_pays, int64_t n,
                     uint64_t* tmp_keys, uint64_t* tmp_pays, void* workspace, size_t ws_bytes,
                     unsigned long long* d_bad, void* stream);
 
+/* packed-record variant of the run sort: the first pass reads (key, payload)
+ * SoA and every pass moves one 8-B record (key - lower) << pw | payload with
+ * pw = 64 - width_bits (1 <= width_bits <= 63).  Valid when every payload is
+ * below 2^pw; otherwise *d_overflow is set to 1 and the caller must use
+ * mpsm_sort_pairs.  The sorted run of records lands in out_rec; tmp_rec is a
+ * ping-pong buffer.  Same workspace as mpsm_sort_pairs. */
+int mpsm_sort_packed(const uint64_t* in_keys, const uint64_t* in_pays, int64_t n, uint64_t lower, uint64_t span_m1,
+                     int width_bits, uint64_t* out_rec, uint64_t* tmp_rec, void* workspace, size_t ws_bytes,
+                     unsigned long long* d_bad, unsigned int* d_overflow, void* stream);
+
 /* ------------------------------------------------- radix histogram ----
  * Replaces _kernels.radix_histogram (_kernels.py:247-259) / partition.
  * build_radix_histogram (partition.py:110-122): d_counts[(key-lower)>>shift]
@@ -141,6 +151,12 @@ int mpsm_join_workspace_bytes(const mpsm_run_t* priv, int n_priv, const mpsm_run
 int mpsm_join_pairs(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub, int swap, int mode,
                     uint64_t* d_out, int64_t cap, uint64_t* d_pairs, void* workspace, size_t ws_bytes,
                     void* stream);
+
+/* the same over runs of packed records (mpsm_sort_packed): each run's keys
+ * pointer points at its records, pays is ignored */
+int mpsm_join_pairs_packed(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub, int width_bits,
+                           uint64_t lower, int swap, int mode, uint64_t* d_out, int64_t cap, uint64_t* d_pairs,
+                           void* workspace, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------ splitter search ----
  * Replaces skew._minmax_contiguous (skew.py:180-273) as used by

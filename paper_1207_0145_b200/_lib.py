@@ -26,11 +26,11 @@ PAIR_FIELDS = 8
 EXPORTS = (
     "mpsm_version", "mpsm_last_error", "mpsm_device_init", "mpsm_launch_count",
     "mpsm_profile_enable", "mpsm_profile_read",
-    "mpsm_sort_workspace_bytes", "mpsm_sort_pass_count", "mpsm_sort_pairs",
+    "mpsm_sort_workspace_bytes", "mpsm_sort_pass_count", "mpsm_sort_pairs", "mpsm_sort_packed",
     "mpsm_radix_histogram",
     "mpsm_scatter_workspace_bytes", "mpsm_scatter_chunk",
     "mpsm_interp_lower_bound",
-    "mpsm_join_workspace_bytes", "mpsm_join_pairs",
+    "mpsm_join_workspace_bytes", "mpsm_join_pairs", "mpsm_join_pairs_packed",
     "mpsm_minmax_contiguous",
     "mpsm_ipc_get_handle", "mpsm_ipc_open_handle", "mpsm_ipc_close_handle",
 )
@@ -52,6 +52,7 @@ _SIGS = {
     "mpsm_sort_workspace_bytes": (_int, [_i64, _int, ctypes.POINTER(_sz)]),
     "mpsm_sort_pass_count": (_int, [_int]),
     "mpsm_sort_pairs": (_int, [_vp, _vp, _i64, _u64, _u64, _int, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp]),
+    "mpsm_sort_packed": (_int, [_vp, _vp, _i64, _u64, _u64, _int, _vp, _vp, _vp, _sz, _vp, _vp, _vp]),
     "mpsm_radix_histogram": (_int, [_vp, _i64, _u64, _u64, _int, _int, _vp, _vp, _vp]),
     "mpsm_scatter_workspace_bytes": (_int, [_i64, _int, ctypes.POINTER(_sz)]),
     "mpsm_scatter_chunk": (_int, [_vp, _vp, _i64, _u64, _int, _vp, _int, _int, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
@@ -60,6 +61,8 @@ _SIGS = {
                                          ctypes.POINTER(_sz)]),
     "mpsm_join_pairs": (_int, [ctypes.POINTER(RunDesc), _int, ctypes.POINTER(RunDesc), _int, _int, _int, _vp, _i64,
                                _vp, _vp, _sz, _vp]),
+    "mpsm_join_pairs_packed": (_int, [ctypes.POINTER(RunDesc), _int, ctypes.POINTER(RunDesc), _int, _int, _u64, _int,
+                                      _int, _vp, _i64, _vp, _vp, _sz, _vp]),
     "mpsm_minmax_contiguous": (_int, [_i64, _int, _vp, _vp, _vp, _i64, _vp]),
     "mpsm_ipc_get_handle": (_int, [_vp, _vp]),
     "mpsm_ipc_open_handle": (_int, [_vp, ctypes.POINTER(_vp)]),

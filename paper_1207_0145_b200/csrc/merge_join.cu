@@ -12,14 +12,20 @@
 //                the reference's interpolation search (identical probe count)
 //                plus a binary search; "examined" statistic; tiles per pair
 //   k_tile_scan  exclusive scan of tiles over pairs
-//   k_partition  merge-path diagonal search for every tile boundary
-//   k_merge      persistent CTAs: load a tile of R and of the S window into
-//                shared memory, per-thread merge-path split, serial merge.
-//                For every S tuple the matching R tuples are the equal-key
-//                run that ends right before its merge position (ties merge R
-//                first), found by walking back -- the reference's
-//                cross-product of duplicate groups.  Per-thread accumulators
-//                are reduced per CTA and flushed with one atomic per pair.
+//   k_partition  merge-path diagonal search for every tile boundary; writes
+//                a flat tile descriptor (direct pointers) so the merge kernel
+//                needs one dependent load per tile
+//   k_merge      persistent CTAs, double-buffered: tile g+grid streams into
+//                shared memory with cp.async while tile g merges.  Each thread
+//                takes MJ_ITEMS steps of the merge from its merge-path split.
+//                For every S tuple the matching R tuples are the equal-key run
+//                that ends right before its merge position (ties merge R
+//                first), found by walking back -- the reference's cross
+//                product of duplicate key groups.  Per-thread accumulators are
+//                reduced per CTA and flushed with one atomic per pair.
+//
+// Runs come in two layouts: (keys, payloads) SoA, or packed 8-B records
+// (key - lower) << pw | payload written by mpsm_sort_packed (PK = true).
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -35,32 +41,51 @@ constexpr int MJ_THREADS = 256;
 constexpr int MJ_ITEMS = 9;  // odd: 64-bit smem accesses at stride ITEMS are conflict-free
 constexpr int MJ_TILE = MJ_THREADS * MJ_ITEMS;
 
+struct PackInfo {
+    int pw;          // payload bits of a packed record (0: SoA runs)
+    uint64_t lower;  // key domain lower bound (packed keys are key - lower)
+    uint64_t pmask;  // (1 << pw) - 1
+};
+
+// original key of element i of a run
+template <bool PK>
+__device__ __forceinline__ uint64_t key_of(const uint64_t* __restrict__ k, int64_t i, const PackInfo& pi) {
+    return PK ? (k[i] >> pi.pw) + pi.lower : k[i];
+}
+
 struct PairWin {
     int64_t start, end;  // S window in public run j
     int64_t tiles;       // merge tiles of this pair
     int64_t tile_base;   // first global tile id
 };
 
+// flat tile descriptor: R tile = R[i0, i0+nR), W tile = S[w0, w0+nW)
 struct TileSplit {
-    int64_t i0, j0, i1, j1;  // R [i0,i1) and window-relative S [j0,j1)
-    int32_t pair;
-    int32_t pad;
+    const uint64_t* rk;  // R keys (or records) of the pair's private run
+    const uint64_t* rp;  // R payloads (SoA only)
+    const uint64_t* wk;  // S keys (or records) of the public run
+    const uint64_t* wp;  // S payloads (SoA only)
+    int64_t i0, w0;
+    int32_t nR, nW;
+    int32_t pair, pad;
 };
 
 // reference probe rule, _kernels.py:287-337 (fp64 probe position, bisect
 // after a step that fails to halve the window)
-__device__ int64_t interp_lb(const uint64_t* __restrict__ keys, int64_t n, uint64_t target, int64_t* probes_out) {
+template <bool PK>
+__device__ int64_t interp_lb(const uint64_t* __restrict__ keys, int64_t n, uint64_t target, int64_t* probes_out,
+                             const PackInfo& pi) {
     int64_t lo = 0, hi = n, probes = 0;
     bool bisect_next = false;
     while (lo < hi) {
-        int64_t width = hi - lo;
+        const int64_t width = hi - lo;
         if (width == 1) {
             ++probes;
-            if (keys[lo] < target) ++lo;
+            if (key_of<PK>(keys, lo, pi) < target) ++lo;
             else hi = lo;
             break;
         }
-        uint64_t klo = keys[lo], khi = keys[hi - 1];
+        const uint64_t klo = key_of<PK>(keys, lo, pi), khi = key_of<PK>(keys, hi - 1, pi);
         probes += 2;
         if (klo >= target) {
             hi = lo;
@@ -76,14 +101,14 @@ __device__ int64_t interp_lb(const uint64_t* __restrict__ keys, int64_t n, uint6
             pos = lo + width / 2;
             interp = false;
         } else {
-            double frac = __ddiv_rn(__ull2double_rn(target - klo), __ull2double_rn(khi - klo));
+            const double frac = __ddiv_rn(__ull2double_rn(target - klo), __ull2double_rn(khi - klo));
             pos = lo + (int64_t)__dmul_rn(frac, __ll2double_rn(width - 1));
             if (pos <= lo) pos = lo + 1;
             if (pos > hi - 1) pos = hi - 1;
             interp = true;
         }
         ++probes;
-        if (keys[pos] < target) lo = pos + 1;
+        if (key_of<PK>(keys, pos, pi) < target) lo = pos + 1;
         else hi = pos;
         bisect_next = interp && (2 * (hi - lo) > width);
     }
@@ -91,11 +116,12 @@ __device__ int64_t interp_lb(const uint64_t* __restrict__ keys, int64_t n, uint6
     return lo;
 }
 
-__device__ __forceinline__ int64_t upper_bound_u64(const uint64_t* __restrict__ keys, int64_t lo, int64_t hi,
-                                                   uint64_t target) {
+template <bool PK>
+__device__ __forceinline__ int64_t upper_bound_key(const uint64_t* __restrict__ keys, int64_t lo, int64_t hi,
+                                                   uint64_t target, const PackInfo& pi) {
     while (lo < hi) {
-        int64_t mid = lo + ((hi - lo) >> 1);
-        if (keys[mid] <= target) lo = mid + 1;
+        const int64_t mid = lo + ((hi - lo) >> 1);
+        if (key_of<PK>(keys, mid, pi) <= target) lo = mid + 1;
         else hi = mid;
     }
     return lo;
@@ -103,17 +129,18 @@ __device__ __forceinline__ int64_t upper_bound_u64(const uint64_t* __restrict__ 
 
 __global__ void k_interp_batch(const uint64_t* __restrict__ keys, int64_t n, const uint64_t* __restrict__ targets,
                                int64_t nt, int64_t* __restrict__ idx, int64_t* __restrict__ probes) {
-    int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nt) return;
     int64_t pr = 0;
-    int64_t r = interp_lb(keys, n, targets[t], &pr);
+    const int64_t r = interp_lb<false>(keys, n, targets[t], &pr, PackInfo{0, 0, 0});
     idx[t] = r;
     if (probes) probes[t] = pr;
 }
 
+template <bool PK>
 __global__ void k_windows(const mpsm_run_t* __restrict__ priv, int n_priv, const mpsm_run_t* __restrict__ pub,
-                          int n_pub, PairWin* __restrict__ win, uint64_t* __restrict__ out) {
-    int p = blockIdx.x * blockDim.x + threadIdx.x;
+                          int n_pub, PairWin* __restrict__ win, uint64_t* __restrict__ out, PackInfo pi) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n_priv * n_pub) return;
     const mpsm_run_t r = priv[p / n_pub];
     const mpsm_run_t s = pub[p % n_pub];
@@ -121,13 +148,13 @@ __global__ void k_windows(const mpsm_run_t* __restrict__ priv, int n_priv, const
     PairWin w{0, 0, 0, 0};
     int64_t probes = 0, examined = 0;
     if (r.n > 0 && s.n > 0) {
-        w.start = interp_lb(s.keys, s.n, r.keys[0], &probes);
-        w.end = upper_bound_u64(s.keys, w.start, s.n, r.keys[r.n - 1]);
+        w.start = interp_lb<PK>(s.keys, s.n, key_of<PK>(r.keys, 0, pi), &probes, pi);
+        w.end = upper_bound_key<PK>(s.keys, w.start, s.n, key_of<PK>(r.keys, r.n - 1, pi), pi);
         // engine.py:253-260 / _kernels.py:405-407: distinct public positions
         // read = up to the first key past the private maximum (or the end)
         examined = (w.end < s.n - 1 ? w.end : s.n - 1) - w.start + 1;
         if (examined < 0) examined = 0;
-        int64_t len = r.n + (w.end - w.start);
+        const int64_t len = r.n + (w.end - w.start);
         w.tiles = (w.end > w.start) ? (len + MJ_TILE - 1) / MJ_TILE : 0;
     }
     win[p] = w;
@@ -147,12 +174,12 @@ __global__ void __launch_bounds__(1024) k_tile_scan(PairWin* __restrict__ win, i
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
     for (int base = 0; base < npairs; base += 1024) {
-        int p = base + threadIdx.x;
-        int64_t v = p < npairs ? win[p].tiles : 0;
+        const int p = base + threadIdx.x;
+        const int64_t v = p < npairs ? win[p].tiles : 0;
         s[threadIdx.x] = v;
         __syncthreads();
         for (int off = 1; off < 1024; off <<= 1) {
-            int64_t a = threadIdx.x >= off ? s[threadIdx.x - off] : 0;
+            const int64_t a = threadIdx.x >= off ? s[threadIdx.x - off] : 0;
             __syncthreads();
             s[threadIdx.x] += a;
             __syncthreads();
@@ -166,31 +193,34 @@ __global__ void __launch_bounds__(1024) k_tile_scan(PairWin* __restrict__ win, i
 }
 
 // merge path: number of R elements among the first k of merge(R, W), ties R first
+template <bool PK>
 __device__ __forceinline__ int64_t merge_path(const uint64_t* __restrict__ rk, int64_t nr,
-                                              const uint64_t* __restrict__ wk, int64_t nw, int64_t k) {
+                                              const uint64_t* __restrict__ wk, int64_t nw, int64_t k,
+                                              const PackInfo& pi) {
     int64_t lo = k > nw ? k - nw : 0, hi = k < nr ? k : nr;
     while (lo < hi) {
-        int64_t mid = (lo + hi) >> 1;
-        if (rk[mid] <= wk[k - 1 - mid]) lo = mid + 1;
+        const int64_t mid = (lo + hi) >> 1;
+        if (key_of<PK>(rk, mid, pi) <= key_of<PK>(wk, k - 1 - mid, pi)) lo = mid + 1;
         else hi = mid;
     }
     return lo;
 }
 
+template <bool PK>
 __global__ void k_partition(const mpsm_run_t* __restrict__ priv, const mpsm_run_t* __restrict__ pub, int n_pub,
                             const PairWin* __restrict__ win, int npairs, const int64_t* __restrict__ total,
-                            TileSplit* __restrict__ splits) {
-    int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+                            TileSplit* __restrict__ splits, PackInfo pi) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= *total) return;
-    // pair of this tile: last p with tile_base <= g and tiles > 0
+    // pair of this tile: last p with tile_base <= g
     int lo = 0, hi = npairs - 1;
     while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
+        const int mid = (lo + hi + 1) >> 1;
         if (win[mid].tile_base <= g) lo = mid;
         else hi = mid - 1;
     }
     int p = lo;
-    while (win[p].tiles == 0 || win[p].tile_base + win[p].tiles <= g) --p;  // skip empty pairs sharing a base
+    while (win[p].tiles == 0 || win[p].tile_base + win[p].tiles <= g) --p;
     const mpsm_run_t r = priv[p / n_pub];
     const mpsm_run_t s = pub[p % n_pub];
     const PairWin w = win[p];
@@ -199,17 +229,23 @@ __global__ void k_partition(const mpsm_run_t* __restrict__ priv, const mpsm_run_
     const int64_t L = r.n + nw;
     const int64_t k0 = (g - w.tile_base) * MJ_TILE;
     const int64_t k1 = (k0 + MJ_TILE < L) ? k0 + MJ_TILE : L;
+    const int64_t i0 = merge_path<PK>(r.keys, r.n, wk, nw, k0, pi);
+    const int64_t i1 = merge_path<PK>(r.keys, r.n, wk, nw, k1, pi);
     TileSplit t;
-    t.i0 = merge_path(r.keys, r.n, wk, nw, k0);
-    t.j0 = k0 - t.i0;
-    t.i1 = merge_path(r.keys, r.n, wk, nw, k1);
-    t.j1 = k1 - t.i1;
+    t.rk = r.keys;
+    t.rp = r.pays;
+    t.wk = s.keys;
+    t.wp = s.pays;
+    t.i0 = i0;
+    t.w0 = w.start + (k0 - i0);
+    t.nR = (int32_t)(i1 - i0);
+    t.nW = (int32_t)((k1 - i1) - (k0 - i0));
     t.pair = p;
     t.pad = 0;
     splits[g] = t;
 }
 
-// two tile buffers: tile g+gridDim streams in (cp.async) while tile g merges
+// two tile buffers: tile g+grid streams in (cp.async) while tile g merges
 struct MergeStage {
     uint64_t k[MJ_TILE], p[MJ_TILE];  // R part of the tile at [0, nR), W part at [nR, nR+nW)
 };
@@ -254,24 +290,17 @@ __device__ __forceinline__ void flush_pair(MergeSmem& sm, uint64_t* __restrict__
     __syncthreads();
 }
 
-__device__ __forceinline__ void load_tile_async(MergeStage& st, const TileSplit& t, const mpsm_run_t* __restrict__ priv,
-                                                const mpsm_run_t* __restrict__ pub, int n_pub,
-                                                const PairWin* __restrict__ win) {
-    const mpsm_run_t r = priv[t.pair / n_pub];
-    const mpsm_run_t s = pub[t.pair % n_pub];
-    const int64_t wstart = win[t.pair].start;
-    const int nR = (int)(t.i1 - t.i0), nW = (int)(t.j1 - t.j0);
-    const uint64_t* rk = r.keys + t.i0;
-    const uint64_t* rp = r.pays + t.i0;
-    const uint64_t* wk = s.keys + wstart + t.j0;
-    const uint64_t* wp = s.pays + wstart + t.j0;
-    for (int x = threadIdx.x; x < nR; x += MJ_THREADS) {
-        cp_async8(&st.k[x], rk + x);
-        cp_async8(&st.p[x], rp + x);
-    }
-    for (int x = threadIdx.x; x < nW; x += MJ_THREADS) {
-        cp_async8(&st.k[nR + x], wk + x);
-        cp_async8(&st.p[nR + x], wp + x);
+template <bool PK>
+__device__ __forceinline__ void load_tile_async(MergeStage& st, const TileSplit& t) {
+    const uint64_t* rk = t.rk + t.i0;
+    const uint64_t* wk = t.wk + t.w0;
+    for (int x = threadIdx.x; x < t.nR; x += MJ_THREADS) cp_async8(&st.k[x], rk + x);
+    for (int x = threadIdx.x; x < t.nW; x += MJ_THREADS) cp_async8(&st.k[t.nR + x], wk + x);
+    if (!PK) {
+        const uint64_t* rp = t.rp + t.i0;
+        const uint64_t* wp = t.wp + t.w0;
+        for (int x = threadIdx.x; x < t.nR; x += MJ_THREADS) cp_async8(&st.p[x], rp + x);
+        for (int x = threadIdx.x; x < t.nW; x += MJ_THREADS) cp_async8(&st.p[t.nR + x], wp + x);
     }
 }
 
@@ -285,14 +314,11 @@ __device__ long long g_mj_ts[1 << 20][6];
 
 // MODE 0: aggregate into pair records; MODE 1: per-tile counts only;
 // MODE 2: emit pairs at tile_out[g] + thread offset
-template <int MODE>
-__global__ void __launch_bounds__(MJ_THREADS) k_merge(const mpsm_run_t* __restrict__ priv,
-                                                      const mpsm_run_t* __restrict__ pub, int n_pub,
-                                                      const PairWin* __restrict__ win,
-                                                      const TileSplit* __restrict__ splits,
+template <int MODE, bool PK>
+__global__ void __launch_bounds__(MJ_THREADS) k_merge(const TileSplit* __restrict__ splits,
                                                       const int64_t* __restrict__ total, int swap,
-                                                      uint64_t* __restrict__ out_pairs,
-                                                      int64_t* __restrict__ tile_cnt, uint64_t* __restrict__ emit_out) {
+                                                      uint64_t* __restrict__ out_pairs, int64_t* __restrict__ tile_cnt,
+                                                      uint64_t* __restrict__ emit_out, PackInfo pi) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     MergeSmem& sm = *reinterpret_cast<MergeSmem*>(smem_raw);
     __shared__ int64_t warp_cnt[MJ_THREADS / 32];
@@ -303,29 +329,36 @@ __global__ void __launch_bounds__(MJ_THREADS) k_merge(const mpsm_run_t* __restri
     int buf = 0;
 
     int64_t g = blockIdx.x;
-    if (g < ntiles) load_tile_async(sm.st[0], splits[g], priv, pub, n_pub, win);
+    TileSplit t_cur{}, t_nxt{};
+    if (g < ntiles) {
+        t_cur = splits[g];
+        load_tile_async<PK>(sm.st[0], t_cur);
+    }
     cp_async_commit();
+    if (g + gridDim.x < ntiles) t_nxt = splits[g + gridDim.x];
     for (; g < ntiles; g += gridDim.x) {
         MJ_TS(0)
         const int64_t gn = g + gridDim.x;
-        if (gn < ntiles) load_tile_async(sm.st[buf ^ 1], splits[gn], priv, pub, n_pub, win);
+        if (gn < ntiles) load_tile_async<PK>(sm.st[buf ^ 1], t_nxt);
         cp_async_commit();
-        const TileSplit t = splits[g];
+        TileSplit t_after{};  // descriptor two tiles ahead, loaded under this tile's work
+        if (gn + gridDim.x < ntiles) t_after = splits[gn + gridDim.x];
+        const TileSplit t = t_cur;
         if (MODE == 0 && t.pair != cur_pair) {
             if (cur_pair >= 0) flush_pair(sm, out_pairs, cur_pair, count, best, csum);
             cur_pair = t.pair;
             count = best = csum = 0;
         }
-        const mpsm_run_t r = priv[t.pair / n_pub];
         MJ_TS(1)
         cp_async_wait_1();  // this thread's copies of tile g landed
         __syncthreads();    // ... and everyone else's
         MJ_TS(2)
-        const int nR = (int)(t.i1 - t.i0), nW = (int)(t.j1 - t.j0);
-        const uint64_t* Rk = sm.st[buf].k;
-        const uint64_t* Wk = sm.st[buf].k + nR;
-        const uint64_t* Rp = sm.st[buf].p;
-        const uint64_t* Wp = sm.st[buf].p + nR;
+        const int nR = t.nR, nW = t.nW;
+        const uint64_t* K = sm.st[buf].k;
+        const uint64_t* Pp = sm.st[buf].p;
+        // tile-relative accessors: normalized key and payload
+        auto skey = [&](int i) -> uint64_t { return PK ? (K[i] >> pi.pw) : K[i]; };
+        auto spay = [&](int i) -> uint64_t { return PK ? (K[i] & pi.pmask) : Pp[i]; };
         const int L = nR + nW;
         const int k0 = min(tid * MJ_ITEMS, L);
         const int k1 = min(k0 + MJ_ITEMS, L);
@@ -333,7 +366,7 @@ __global__ void __launch_bounds__(MJ_THREADS) k_merge(const mpsm_run_t* __restri
         int lo = k0 > nW ? k0 - nW : 0, hi = k0 < nR ? k0 : nR;
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
-            if (Rk[mid] <= Wk[k0 - 1 - mid]) lo = mid + 1;
+            if (skey(mid) <= skey(nR + k0 - 1 - mid)) lo = mid + 1;
             else hi = mid;
         }
         MJ_TS(3)
@@ -357,38 +390,45 @@ __global__ void __launch_bounds__(MJ_THREADS) k_merge(const mpsm_run_t* __restri
             }
             int64_t e = 0;
             int ri = lo, wj = k0 - lo;
+            uint64_t rkc = ri < nR ? skey(ri) : 0;       // current R key (register-carried)
+            uint64_t wkc = wj < nW ? skey(nR + wj) : 0;  // current S key
             for (int step = k0; step < k1; ++step) {
-                if (ri < nR && (wj >= nW || Rk[ri] <= Wk[wj])) {
+                if (ri < nR && (wj >= nW || rkc <= wkc)) {
                     ++ri;
+                    if (ri < nR) rkc = skey(ri);
                     continue;
                 }
-                const uint64_t skey = Wk[wj];
-                const uint64_t spay = Wp[wj];
+                const uint64_t sp = spay(nR + wj);
                 int64_t gi = t.i0 + ri - 1;  // walk back over the equal-key R group
                 while (gi >= 0) {
                     const bool in_tile = gi >= t.i0;
-                    const uint64_t rk = in_tile ? Rk[gi - t.i0] : r.keys[gi];
-                    if (rk != skey) break;
-                    const uint64_t rp = in_tile ? Rp[gi - t.i0] : r.pays[gi];
+                    uint64_t rk, rp;
+                    if (in_tile) rk = skey((int)(gi - t.i0));
+                    else rk = PK ? (t.rk[gi] >> pi.pw) : t.rk[gi];
+                    if (rk != wkc) break;
+                    if (in_tile) rp = spay((int)(gi - t.i0));
+                    else rp = PK ? (t.rk[gi] & pi.pmask) : t.rp[gi];
                     if (MODE == 0) {
-                        const uint64_t v = rp + spay;
+                        const uint64_t v = rp + sp;
                         best = v > best ? v : best;
                         ++count;
-                        csum += swap ? pair_hash(spay, rp) : pair_hash(rp, spay);
+                        csum += swap ? pair_hash(sp, rp) : pair_hash(rp, sp);
                     } else if (MODE == 1 || pass == 0) {
                         ++e;
                     } else {
                         const int64_t o = emit_base + e;
-                        emit_out[2 * o] = swap ? spay : rp;
-                        emit_out[2 * o + 1] = swap ? rp : spay;
+                        emit_out[2 * o] = swap ? sp : rp;
+                        emit_out[2 * o + 1] = swap ? rp : sp;
                         ++e;
                     }
                     --gi;
                 }
                 ++wj;
+                if (wj < nW) wkc = skey(nR + wj);
             }
             my_pairs = e;
         }
+        MJ_TS(4)
         if (MODE == 1) {
             const int64_t c = warp_sum((unsigned long long)my_pairs);
             if ((tid & 31) == 0) warp_cnt[tid >> 5] = c;
@@ -399,10 +439,11 @@ __global__ void __launch_bounds__(MJ_THREADS) k_merge(const mpsm_run_t* __restri
                 tile_cnt[g] = sum;
             }
         }
-        MJ_TS(4)
         __syncthreads();  // everyone is done with st[buf] before it is refilled
         MJ_TS(5)
         buf ^= 1;
+        t_cur = t_nxt;
+        t_nxt = t_after;
     }
     if (MODE == 0 && cur_pair >= 0) flush_pair(sm, out_pairs, cur_pair, count, best, csum);
 }
@@ -417,13 +458,15 @@ __global__ void __launch_bounds__(1024) k_emit_offsets(int64_t* __restrict__ til
     __syncthreads();
     const int64_t n = *total;
     for (int64_t base = 0; base < n; base += 1024) {
-        int64_t g = base + threadIdx.x;
-        int64_t v = g < n ? tile_cnt[g] : 0;
-        if (g < n && v) atomicAdd((unsigned long long*)(out_pairs + (size_t)splits[g].pair * MPSM_PAIR_FIELDS + MPSM_PAIR_EMITTED), (unsigned long long)v);
+        const int64_t g = base + threadIdx.x;
+        const int64_t v = g < n ? tile_cnt[g] : 0;
+        if (g < n && v)
+            atomicAdd((unsigned long long*)(out_pairs + (size_t)splits[g].pair * MPSM_PAIR_FIELDS + MPSM_PAIR_EMITTED),
+                      (unsigned long long)v);
         s[threadIdx.x] = v;
         __syncthreads();
         for (int off = 1; off < 1024; off <<= 1) {
-            int64_t a = threadIdx.x >= off ? s[threadIdx.x - off] : 0;
+            const int64_t a = threadIdx.x >= off ? s[threadIdx.x - off] : 0;
             __syncthreads();
             s[threadIdx.x] += a;
             __syncthreads();
@@ -456,8 +499,7 @@ struct JoinWs {
     int64_t* tile_cnt;
 };
 
-static bool carve_join(void* ws, size_t bytes, int n_priv, int n_pub, int64_t mt, JoinWs* o) {
-    Carve c{(char*)ws, bytes};
+static bool carve_join(Carve c, int n_priv, int n_pub, int64_t mt, JoinWs* o) {
     o->d_priv = c.take<mpsm_run_t>(std::max(n_priv, 1));
     o->d_pub = c.take<mpsm_run_t>(std::max(n_pub, 1));
     o->win = c.take<PairWin>((size_t)std::max(n_priv * n_pub, 1));
@@ -480,15 +522,15 @@ static size_t join_ws_size(int n_priv, int n_pub, int64_t mt) {
     return c.off;
 }
 
-template <int MODE>
-static int launch_merge(const JoinWs& w, int n_pub, int swap, uint64_t* d_pairs, uint64_t* emit_out, int64_t mt,
-                        cudaStream_t st) {
+template <int MODE, bool PK>
+static int launch_merge(const JoinWs& w, int swap, uint64_t* d_pairs, uint64_t* emit_out, int64_t mt,
+                        const PackInfo& pi, cudaStream_t st) {
     static int per_sm = 0;
     if (per_sm == 0) {
-        MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_merge<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_merge<MODE, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   (int)sizeof(MergeSmem)),
                              "smem attr"));
-        MPSM_TRY(cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge<MODE>, MJ_THREADS,
+        MPSM_TRY(cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge<MODE, PK>, MJ_THREADS,
                                                                            sizeof(MergeSmem)),
                              "occupancy"));
         if (per_sm < 1) per_sm = 1;
@@ -496,9 +538,43 @@ static int launch_merge(const JoinWs& w, int n_pub, int swap, uint64_t* d_pairs,
     // persistent grid: exactly the resident CTAs
     const int grid = (int)std::min<int64_t>((int64_t)num_sms() * per_sm, mt);
     ProfScope ps(MODE == 0 ? "merge" : (MODE == 1 ? "merge_count" : "merge_emit"), st);
-    k_merge<MODE><<<grid, MJ_THREADS, sizeof(MergeSmem), st>>>(w.d_priv, w.d_pub, n_pub, w.win, w.splits, w.total,
-                                                                swap, d_pairs, w.tile_cnt, emit_out);
+    k_merge<MODE, PK><<<grid, MJ_THREADS, sizeof(MergeSmem), st>>>(w.splits, w.total, swap, d_pairs, w.tile_cnt,
+                                                                    emit_out, pi);
     return check_launch("k_merge");
+}
+
+template <bool PK>
+static int join_pairs_impl(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub, int swap, int mode,
+                           uint64_t* d_out, uint64_t* d_pairs, void* workspace, size_t ws_bytes, const PackInfo& pi,
+                           cudaStream_t st) {
+    if (n_priv < 1 || n_pub < 1 || !d_pairs) return MPSM_ERR_ARG;
+    if (mode < 0 || mode > 2) return MPSM_ERR_ARG;
+    const int npairs = n_priv * n_pub;
+    const int64_t mt = max_tiles(priv, n_priv, pub, n_pub);
+    JoinWs w;
+    if (!carve_join(Carve{(char*)workspace, ws_bytes}, n_priv, n_pub, mt, &w)) {
+        set_error("join workspace too small");
+        return MPSM_ERR_ARG;
+    }
+    MPSM_TRY(cuda_status(cudaMemcpyAsync(w.d_priv, priv, sizeof(mpsm_run_t) * n_priv, cudaMemcpyHostToDevice, st), "h2d"));
+    MPSM_TRY(cuda_status(cudaMemcpyAsync(w.d_pub, pub, sizeof(mpsm_run_t) * n_pub, cudaMemcpyHostToDevice, st), "h2d"));
+    k_windows<PK><<<(npairs + 127) / 128, 128, 0, st>>>(w.d_priv, n_priv, w.d_pub, n_pub, w.win, d_pairs, pi);
+    MPSM_TRY(check_launch("k_windows"));
+    k_tile_scan<<<1, 1024, 0, st>>>(w.win, npairs, w.total);
+    MPSM_TRY(check_launch("k_tile_scan"));
+    {
+        ProfScope ps("merge_partition", st);
+        k_partition<PK><<<(unsigned)((mt + 255) / 256), 256, 0, st>>>(w.d_priv, w.d_pub, n_pub, w.win, npairs,
+                                                                       w.total, w.splits, pi);
+    }
+    MPSM_TRY(check_launch("k_partition"));
+    MPSM_TRY((launch_merge<0, PK>(w, swap, d_pairs, nullptr, mt, pi, st)));
+    if (mode != MPSM_MODE_MATERIALIZE || d_out == nullptr) return MPSM_OK;
+    // materialize: per-tile counts, offsets, emission
+    MPSM_TRY((launch_merge<1, PK>(w, swap, d_pairs, nullptr, mt, pi, st)));
+    k_emit_offsets<<<1, 1024, 0, st>>>(w.tile_cnt, w.splits, w.total, d_pairs, w.grand);
+    MPSM_TRY(check_launch("k_emit_offsets"));
+    return launch_merge<2, PK>(w, swap, d_pairs, d_out, mt, pi, st);
 }
 
 }  // namespace mpsm
@@ -530,37 +606,17 @@ extern "C" int mpsm_join_workspace_bytes(const mpsm_run_t* priv, int n_priv, con
 extern "C" int mpsm_join_pairs(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub, int swap,
                                int mode, uint64_t* d_out, int64_t cap, uint64_t* d_pairs, void* workspace,
                                size_t ws_bytes, void* stream) {
-    cudaStream_t st = (cudaStream_t)stream;
-    if (n_priv < 1 || n_pub < 1 || !d_pairs) return MPSM_ERR_ARG;
-    if (mode < 0 || mode > 2) return MPSM_ERR_ARG;
-    const int npairs = n_priv * n_pub;
-    const int64_t mt = max_tiles(priv, n_priv, pub, n_pub);
-    JoinWs w;
-    if (!carve_join(workspace, ws_bytes, n_priv, n_pub, mt, &w)) {
-        set_error("join workspace too small");
-        return MPSM_ERR_ARG;
-    }
-    MPSM_TRY(cuda_status(cudaMemcpyAsync(w.d_priv, priv, sizeof(mpsm_run_t) * n_priv, cudaMemcpyHostToDevice, st), "h2d"));
-    MPSM_TRY(cuda_status(cudaMemcpyAsync(w.d_pub, pub, sizeof(mpsm_run_t) * n_pub, cudaMemcpyHostToDevice, st), "h2d"));
-    k_windows<<<(npairs + 127) / 128, 128, 0, st>>>(w.d_priv, n_priv, w.d_pub, n_pub, w.win, d_pairs);
-    MPSM_TRY(check_launch("k_windows"));
-    k_tile_scan<<<1, 1024, 0, st>>>(w.win, npairs, w.total);
-    MPSM_TRY(check_launch("k_tile_scan"));
-    {
-    ProfScope ps("merge_partition", st);
-    k_partition<<<(unsigned)((mt + 255) / 256), 256, 0, st>>>(w.d_priv, w.d_pub, n_pub, w.win, npairs, w.total,
-                                                               w.splits);
-    }
-    MPSM_TRY(check_launch("k_partition"));
-    if (mode != MPSM_MODE_MATERIALIZE || d_out == nullptr) {
-        MPSM_TRY(launch_merge<0>(w, n_pub, swap, d_pairs, nullptr, mt, st));
-        return MPSM_OK;
-    }
-    // materialize: aggregates, per-tile counts, offsets, emission
-    MPSM_TRY(launch_merge<0>(w, n_pub, swap, d_pairs, nullptr, mt, st));
-    MPSM_TRY(launch_merge<1>(w, n_pub, swap, d_pairs, nullptr, mt, st));
-    k_emit_offsets<<<1, 1024, 0, st>>>(w.tile_cnt, w.splits, w.total, d_pairs, w.grand);
-    MPSM_TRY(check_launch("k_emit_offsets"));
     (void)cap;  // the caller sized d_out from the counts of a first call
-    return launch_merge<2>(w, n_pub, swap, d_pairs, d_out, mt, st);
+    return join_pairs_impl<false>(priv, n_priv, pub, n_pub, swap, mode, d_out, d_pairs, workspace, ws_bytes,
+                                  PackInfo{0, 0, 0}, (cudaStream_t)stream);
+}
+
+extern "C" int mpsm_join_pairs_packed(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub,
+                                      int width_bits, uint64_t lower, int swap, int mode, uint64_t* d_out, int64_t cap,
+                                      uint64_t* d_pairs, void* workspace, size_t ws_bytes, void* stream) {
+    (void)cap;
+    if (width_bits < 1 || width_bits > 63) return MPSM_ERR_ARG;
+    const int pw = 64 - width_bits;
+    return join_pairs_impl<true>(priv, n_priv, pub, n_pub, swap, mode, d_out, d_pairs, workspace, ws_bytes,
+                                 PackInfo{pw, lower, (1ull << pw) - 1}, (cudaStream_t)stream);
 }

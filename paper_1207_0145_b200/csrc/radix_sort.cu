@@ -220,12 +220,24 @@ __device__ long long g_phase_ts[1 << 22][8];
 #define PHASE_TS(i)
 #endif
 
-template <class DigitOp>
+// pass layouts: (key, payload) SoA in and out; SoA in -> packed records out
+// (the first pass of a packed sort); packed in and out.  A packed record is
+// (key - lower) << pw | payload with pw = 64 - width_bits, valid when every
+// payload < 2^pw; the sort then moves 8 B per tuple instead of 16.
+enum PassLayout { PASS_SS = 0, PASS_SP = 1, PASS_PP = 2 };
+
+struct PackSpec {
+    uint64_t lower;
+    int pw;
+    unsigned int* overflow;  // set to 1 if some payload does not fit pw bits
+};
+
+template <class DigitOp, int PM = PASS_SS>
 __global__ void __launch_bounds__(SORT_THREADS, MPSM_SORT_MIN_BLOCKS) k_onesweep(
     const uint64_t* __restrict__ in_k, const uint64_t* __restrict__ in_p, uint64_t* __restrict__ out_k,
     uint64_t* __restrict__ out_p, int64_t n, DigitOp digit, int bits, int nbins, const int64_t* __restrict__ bin_base,
     uint64_t* __restrict__ status, int64_t st_stride, unsigned int* __restrict__ ticket_ctr, uint32_t epoch,
-    int64_t* __restrict__ written) {
+    int64_t* __restrict__ written, PackSpec pk = PackSpec{0, 0, nullptr}) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PassSmem& sm = *reinterpret_cast<PassSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -357,250 +369,64 @@ __global__ void __launch_bounds__(SORT_THREADS, MPSM_SORT_MIN_BLOCKS) k_onesweep
     __syncthreads();
     PHASE_TS(4)
     for (int d = tid; d < nbins; d += SORT_THREADS) sm.gdelta[d] -= (int64_t)sm.tile_off[d];
-    // ---- staging positions (whist now holds the warp-exclusive offsets)
+    // ---- staging positions (whist now holds the warp-exclusive offsets);
+    // the digit stays in bits 20.. for the write-out
 #pragma unroll
     for (int k = 0; k < SORT_ITEMS; ++k) {
         if (pos[k] != 0xffffffffu) {
             const uint32_t dk = pos[k] >> 20;
-            pos[k] = sm.tile_off[dk] + sm.u.whist[warp][dk] + (pos[k] & 0xfffffu);
-            key[k] |= 0;  // keep key live
+            pos[k] = (dk << 20) | (sm.tile_off[dk] + sm.u.whist[warp][dk] + (pos[k] & 0xfffffu));
         }
+    }
+    if (PM == PASS_SP) {
+        // pack (key - lower) << pw | payload in registers
+        uint64_t ovf = 0;
+#pragma unroll
+        for (int k = 0; k < SORT_ITEMS; ++k) {
+            const int64_t idx = warp_base + 32 * k + lane;
+            const uint64_t pay = (full || idx < n) ? ld_stream(in_p + idx) : 0;
+            ovf |= pay >> pk.pw;
+            // a payload wider than pw bits is masked so the key bits (and with
+            // them every later pass's digit counts) stay exact; the caller
+            // sees the overflow flag and redoes the join on pairs
+            key[k] = ((key[k] - pk.lower) << pk.pw) | (pay & ((1ull << pk.pw) - 1ull));
+        }
+        if (__any_sync(0xffffffffu, ovf != 0) && lane == 0) atomicOr(pk.overflow, 1u);
     }
     __syncthreads();  // whist dead from here; stage aliases it
 #pragma unroll
     for (int k = 0; k < SORT_ITEMS; ++k) {
         if (pos[k] != 0xffffffffu) {
-            sm.u.stage[pos[k]] = key[k];
-            sm.dig[pos[k]] = (uint16_t)digit(key[k]);
+            const uint32_t p = pos[k] & 0xfffffu;
+            sm.u.stage[p] = key[k];
+            sm.dig[p] = (uint16_t)(pos[k] >> 20);
         }
     }
     __syncthreads();
     PHASE_TS(5)
-    // payload loads go out now and land while the keys are written
-    uint64_t pay[SORT_ITEMS];
-#pragma unroll
-    for (int k = 0; k < SORT_ITEMS; ++k) {
-        const int64_t idx = warp_base + 32 * k + lane;
-        pay[k] = (full || idx < n) ? ld_stream(in_p + idx) : 0;
-    }
     const int valid_in_tile = full ? SORT_TILE : (int)(n - tile_base);
+    if (PM != PASS_SS) {
 #pragma unroll 4
-    for (int i = tid; i < valid_in_tile; i += SORT_THREADS) out_k[sm.gdelta[sm.dig[i]] + i] = sm.u.stage[i];
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < SORT_ITEMS; ++k)
-        if (pos[k] != 0xffffffffu) sm.u.stage[pos[k]] = pay[k];
-    __syncthreads();
-#pragma unroll 4
-    for (int i = tid; i < valid_in_tile; i += SORT_THREADS) out_p[sm.gdelta[sm.dig[i]] + i] = sm.u.stage[i];
-    PHASE_TS(6)
-}
-
-// ------------------------------------------------ persistent prefetching pass
-// One CTA per SM loops over tiles in ticket order.  While it ranks, looks
-// back and scatters tile t, the cp.async copies of its next tile are in
-// flight into the other half of a double buffer, so HBM stays busy through
-// the latency-bound phases (the non-persistent kernel above leaves it idle:
-// ncu showed 28 % of stall samples waiting on the first key of each tile).
-// Look-back words are laid out [digit][tile] so one 32-B read fetches four
-// predecessors of a digit.
-struct PfSmem {
-    uint64_t k[2][SORT_TILE];
-    uint64_t p[2][SORT_TILE];
-    uint32_t whist[SORT_WARPS][MAX_BINS];
-    uint16_t dig[SORT_TILE];
-    uint32_t tile_off[MAX_BINS];
-    int64_t gdelta[MAX_BINS];
-    uint32_t ticket[2];
-};
-
-__device__ __forceinline__ void cp_async8_g2s(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async16_g2s(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-
-
-// copy tile `tile` (keys + payloads) into buffer slot b asynchronously
-__device__ __forceinline__ void pf_issue(PfSmem& sm, int b, uint32_t tile, const uint64_t* __restrict__ in_k,
-                                         const uint64_t* __restrict__ in_p, int64_t n, bool vec16) {
-    const int64_t base = (int64_t)tile * SORT_TILE;
-    const int cnt = (int)min((int64_t)SORT_TILE, n - base);
-    if (cnt <= 0) return;
-    if (vec16 && cnt == SORT_TILE) {
-        for (int i = threadIdx.x * 2; i < SORT_TILE; i += SORT_THREADS * 2) {
-            cp_async16_g2s(&sm.k[b][i], in_k + base + i);
-            cp_async16_g2s(&sm.p[b][i], in_p + base + i);
-        }
+        for (int i = tid; i < valid_in_tile; i += SORT_THREADS) out_k[sm.gdelta[sm.dig[i]] + i] = sm.u.stage[i];
     } else {
-        for (int i = threadIdx.x; i < cnt; i += SORT_THREADS) {
-            cp_async8_g2s(&sm.k[b][i], in_k + base + i);
-            cp_async8_g2s(&sm.p[b][i], in_p + base + i);
-        }
-    }
-}
-
-template <class DigitOp>
-__global__ void __launch_bounds__(SORT_THREADS, 1) k_onesweep_pf(
-    const uint64_t* __restrict__ in_k, const uint64_t* __restrict__ in_p, uint64_t* __restrict__ out_k,
-    uint64_t* __restrict__ out_p, int64_t n, DigitOp digit, int bits, int nbins, const int64_t* __restrict__ bin_base,
-    uint64_t* __restrict__ status, int64_t st_stride, unsigned int* __restrict__ ticket_ctr, uint32_t epoch,
-    int64_t* __restrict__ written) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    PfSmem& sm = *reinterpret_cast<PfSmem*>(smem_raw);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t ntiles = (n + SORT_TILE - 1) / SORT_TILE;
-    const bool vec16 = ((((uintptr_t)in_k) | ((uintptr_t)in_p)) & 15) == 0;
-    const unsigned lt = lanemask_lt();
-
-    if (tid == 0) sm.ticket[0] = atomicAdd(ticket_ctr, 1u);
-    __syncthreads();
-    int cur = 0;
-    uint32_t tile = sm.ticket[0];
-    if (tile < ntiles) pf_issue(sm, 0, tile, in_k, in_p, n, vec16);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-
-    while (tile < ntiles) {
-        // claim and start the next tile
-        if (tid == 0) sm.ticket[cur ^ 1] = atomicAdd(ticket_ctr, 1u);
-        for (int i = tid; i < SORT_WARPS * MAX_BINS; i += SORT_THREADS) (&sm.whist[0][0])[i] = 0;
-        __syncthreads();
-        const uint32_t next = sm.ticket[cur ^ 1];
-        if (next < ntiles) pf_issue(sm, cur ^ 1, next, in_k, in_p, n, vec16);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-        __syncthreads();  // tile `tile` is in buf[cur]
-
-        const int64_t tile_base = (int64_t)tile * SORT_TILE;
-        const bool full = tile_base + SORT_TILE <= n;
-        const int wb = warp * (32 * SORT_ITEMS);
-        uint64_t key[SORT_ITEMS];
-        uint32_t pos[SORT_ITEMS];
-        uint32_t* wh = sm.whist[warp];
-#pragma unroll
-        for (int k = 0; k < SORT_ITEMS; ++k) {
-            const int li = wb + 32 * k + lane;
-            const bool valid = full || tile_base + li < n;
-            key[k] = valid ? sm.k[cur][li] : 0;
-            const unsigned vmask = full ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
-            const uint32_t d = digit(key[k]);
-            unsigned peers = ballot_match(d, bits, vmask);
-            if (!valid) peers = 0;
-            uint32_t before = 0;
-            if (peers) before = wh[d];
-            __syncwarp();
-            if (peers && (peers & lt) == 0) wh[d] = before + __popc(peers);
-            __syncwarp();
-            pos[k] = peers ? ((d << 20) | (before + __popc(peers & lt))) : 0xffffffffu;
-        }
-        __syncthreads();
-        uint32_t my_cnt = 0;
-        const int d = tid;
-        if (d < nbins) {
-            uint32_t col[SORT_WARPS];
-#pragma unroll
-            for (int w = 0; w < SORT_WARPS; ++w) col[w] = sm.whist[w][d];
-#pragma unroll
-            for (int w = 0; w < SORT_WARPS; ++w) my_cnt += col[w];
-            st_volatile_u64(status + (size_t)d * st_stride + tile,
-                            (uint64_t)my_cnt | ((uint64_t)epoch << EPOCH_SHIFT) | (tile == 0 ? FLAG_PREFIX : FLAG_AGG));
-            uint32_t run = 0;
-#pragma unroll
-            for (int w = 0; w < SORT_WARPS; ++w) {
-                sm.whist[w][d] = run;
-                run += col[w];
-            }
-        }
-        if (d < MAX_BINS) sm.tile_off[d] = my_cnt;
-        __syncthreads();
-        if (warp == 0) {
-            constexpr int PER = MAX_BINS / 32;
-            uint32_t loc[PER];
-            uint32_t sum = 0;
-#pragma unroll
-            for (int q = 0; q < PER; ++q) {
-                loc[q] = sm.tile_off[lane * PER + q];
-                sum += loc[q];
-            }
-            uint32_t incl = sum;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += v;
-            }
-            uint32_t run = incl - sum;
-#pragma unroll
-            for (int q = 0; q < PER; ++q) {
-                const uint32_t c = loc[q];
-                sm.tile_off[lane * PER + q] = run;
-                run += c;
-            }
-        }
-        if (d < nbins) {
-            uint64_t excl = 0;
-            if (tile > 0) {
-                const uint64_t* row = status + (size_t)d * st_stride;
-                int64_t t = (int64_t)tile - 1;  // next predecessor to account for
-                bool done = false;
-                while (!done) {
-                    const int64_t g0 = t & ~(int64_t)3;
-                    uint64_t w[4];
-                    ld_volatile_v2(row + g0, w[0], w[1]);
-                    ld_volatile_v2(row + g0 + 2, w[2], w[3]);
-                    // walk t, t-1, ... down to g0 inside the group
-                    while (t >= g0) {
-                        const uint64_t v = w[t - g0];
-                        if (((v >> EPOCH_SHIFT) & EPOCH_MASK) != epoch || (v >> 62) == 0) break;  // not ready: reload
-                        excl += v & VALUE_MASK;
-                        if ((v >> 62) == 2) {
-                            done = true;
-                            break;
-                        }
-                        --t;
-                    }
-                }
-                st_volatile_u64(status + (size_t)d * st_stride + tile,
-                                (excl + my_cnt) | ((uint64_t)epoch << EPOCH_SHIFT) | FLAG_PREFIX);
-            }
-            sm.gdelta[d] = bin_base[d] + (int64_t)excl;
-            if (written && my_cnt) atomicAdd((unsigned long long*)(written + d), (unsigned long long)my_cnt);
-        }
-        __syncthreads();
-        if (d < nbins) sm.gdelta[d] -= (int64_t)sm.tile_off[d];
+        // payload loads go out now and land while the keys are written
         uint64_t pay[SORT_ITEMS];
 #pragma unroll
         for (int k = 0; k < SORT_ITEMS; ++k) {
-            pay[k] = sm.p[cur][wb + 32 * k + lane];
-            if (pos[k] != 0xffffffffu) {
-                const uint32_t dk = pos[k] >> 20;
-                pos[k] = sm.tile_off[dk] + sm.whist[warp][dk] + (pos[k] & 0xfffffu);
-            }
+            const int64_t idx = warp_base + 32 * k + lane;
+            pay[k] = (full || idx < n) ? ld_stream(in_p + idx) : 0;
         }
-        __syncthreads();  // buf[cur] fully read into registers: stage in place
-#pragma unroll
-        for (int k = 0; k < SORT_ITEMS; ++k) {
-            if (pos[k] != 0xffffffffu) {
-                sm.k[cur][pos[k]] = key[k];
-                sm.p[cur][pos[k]] = pay[k];
-                sm.dig[pos[k]] = (uint16_t)digit(key[k]);
-            }
-        }
-        __syncthreads();
-        const int valid_in_tile = full ? SORT_TILE : (int)(n - tile_base);
 #pragma unroll 4
-        for (int i = tid; i < valid_in_tile; i += SORT_THREADS) {
-            const int64_t g = sm.gdelta[sm.dig[i]] + i;
-            out_k[g] = sm.k[cur][i];
-            out_p[g] = sm.p[cur][i];
-        }
-        __syncthreads();  // buf[cur] free for the tile after next
-        tile = next;
-        cur ^= 1;
+        for (int i = tid; i < valid_in_tile; i += SORT_THREADS) out_k[sm.gdelta[sm.dig[i]] + i] = sm.u.stage[i];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < SORT_ITEMS; ++k)
+            if (pos[k] != 0xffffffffu) sm.u.stage[pos[k] & 0xfffffu] = pay[k];
+        __syncthreads();
+#pragma unroll 4
+        for (int i = tid; i < valid_in_tile; i += SORT_THREADS) out_p[sm.gdelta[sm.dig[i]] + i] = sm.u.stage[i];
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    PHASE_TS(6)
 }
 
 static size_t pass_smem_bytes() { return sizeof(PassSmem); }
@@ -643,11 +469,13 @@ static int set_pass_smem() {
         MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_onesweep<PartitionDigit>,
                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem_bytes()),
                              "smem attr"));
-#ifdef MPSM_SORT_PERSISTENT
-        MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_onesweep_pf<RadixDigit>,
-                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PfSmem)),
+        MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_onesweep<RadixDigit, PASS_SP>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem_bytes()),
                              "smem attr"));
-#endif
+        MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_onesweep<RadixDigit, PASS_PP>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem_bytes()),
+                             "smem attr"));
+
         done = true;
     }
     return MPSM_OK;
@@ -669,88 +497,6 @@ extern "C" int mpsm_dbg_phase_ts(long long* host, int ntiles) {
     return cuda_status(cudaMemcpyFromSymbol(host, g_phase_ts, sizeof(long long) * 8 * (size_t)ntiles), "dbg");
 }
 #endif
-
-extern "C" int mpsm_sort_pass_count(int width_bits) { return plan_passes(width_bits).npasses; }
-
-extern "C" int mpsm_sort_workspace_bytes(int64_t n, int width_bits, size_t* bytes) {
-    if (!bytes || n < 0 || width_bits < 0 || width_bits > 64) return MPSM_ERR_ARG;
-    *bytes = sort_ws_bytes(n);
-    return MPSM_OK;
-}
-
-extern "C" int mpsm_sort_pairs(const uint64_t* in_keys, const uint64_t* in_pays, int64_t n, uint64_t lower,
-                               uint64_t span_m1, int width_bits, uint64_t* out_keys, uint64_t* out_pays,
-                               uint64_t* tmp_keys, uint64_t* tmp_pays, void* workspace, size_t ws_bytes,
-                               unsigned long long* d_bad, void* stream) {
-    cudaStream_t st = (cudaStream_t)stream;
-    if (n < 0 || width_bits < 0 || width_bits > 64) return MPSM_ERR_ARG;
-    if (n == 0) return MPSM_OK;
-    SortWorkspace ws;
-    if (!carve_sort(workspace, ws_bytes, n, &ws)) {
-        set_error("sort workspace too small");
-        return MPSM_ERR_ARG;
-    }
-    MPSM_TRY(set_pass_smem());
-    PassPlan plan = plan_passes(width_bits);
-    MPSM_TRY(cuda_status(cudaMemsetAsync(ws.hist, 0, sizeof(unsigned long long) * MAX_PASSES * MAX_BINS, st), "memset"));
-    MPSM_TRY(cuda_status(cudaMemsetAsync(ws.tickets, 0, sizeof(unsigned int) * MAX_PASSES, st), "memset"));
-    {
-        int grid = (int)std::min<int64_t>(num_sms() * 4, (n + HIST_THREADS * HIST_UNROLL - 1) / (HIST_THREADS * HIST_UNROLL));
-        ProfScope ps("upfront_hist", st);
-        k_upfront_hist<<<grid, HIST_THREADS, 0, st>>>(in_keys, n, lower, span_m1, plan, ws.hist, d_bad);
-        MPSM_TRY(check_launch("k_upfront_hist"));
-    }
-    if (plan.npasses == 0) {  // one-value domain: already sorted
-        if (out_keys != in_keys) {
-            MPSM_TRY(cuda_status(cudaMemcpyAsync(out_keys, in_keys, 8 * n, cudaMemcpyDeviceToDevice, st), "copy"));
-            MPSM_TRY(cuda_status(cudaMemcpyAsync(out_pays, in_pays, 8 * n, cudaMemcpyDeviceToDevice, st), "copy"));
-        }
-        return MPSM_OK;
-    }
-    k_bucket_starts<<<plan.npasses, MAX_BINS, 0, st>>>(ws.hist, plan, ws.starts);
-    MPSM_TRY(check_launch("k_bucket_starts"));
-
-    // buffer schedule: the last pass must land in out; never write in place
-    int P = plan.npasses;
-    const uint64_t *src_k = in_keys, *src_p = in_pays;
-    bool in_is_out = (in_keys == out_keys);
-    // choose dst of pass 0 so that after P passes we end in out
-    // sequence alternates dst between A and B; last = out.
-    uint64_t *A_k = out_keys, *A_p = out_pays, *B_k = tmp_keys, *B_p = tmp_pays;
-    // pass i writes to (P-1-i) even ? A : B
-    if (in_is_out && (P % 2 == 1)) {
-        // first pass would write into its own input; copy input to tmp first
-        MPSM_TRY(cuda_status(cudaMemcpyAsync(tmp_keys, in_keys, 8 * n, cudaMemcpyDeviceToDevice, st), "copy"));
-        MPSM_TRY(cuda_status(cudaMemcpyAsync(tmp_pays, in_pays, 8 * n, cudaMemcpyDeviceToDevice, st), "copy"));
-        src_k = tmp_keys;
-        src_p = tmp_pays;
-        // now passes: tmp -> out -> tmp -> ... -> out (P odd): pass 0 writes A(out) fine
-    }
-    const int64_t tiles = num_tiles(n);
-    for (int i = 0; i < P; ++i) {
-        bool to_a = ((P - 1 - i) % 2) == 0;
-        uint64_t* dk = to_a ? A_k : B_k;
-        uint64_t* dp = to_a ? A_p : B_p;
-        bool wrapped = false;
-        uint32_t epoch = next_epoch(&wrapped);
-        MPSM_TRY(clear_status_if_wrapped(wrapped, ws.status, n, st));
-        RadixDigit dig{lower, plan.shift[i], (1u << plan.bits[i]) - 1u};
-        ProfScope ps("onesweep", st);
-#ifdef MPSM_SORT_PERSISTENT
-        k_onesweep_pf<RadixDigit><<<num_sms(), SORT_THREADS, sizeof(PfSmem), st>>>(
-            src_k, src_p, dk, dp, n, dig, plan.bits[i], 1 << plan.bits[i], ws.starts + i * MAX_BINS, ws.status, status_stride(n),
-            ws.tickets + i, epoch, nullptr);
-#else
-        k_onesweep<RadixDigit><<<(unsigned)tiles, SORT_THREADS, pass_smem_bytes(), st>>>(
-            src_k, src_p, dk, dp, n, dig, plan.bits[i], 1 << plan.bits[i], ws.starts + i * MAX_BINS, ws.status,
-            status_stride(n), ws.tickets + i, epoch, nullptr);
-#endif
-        MPSM_TRY(check_launch("k_onesweep"));
-        src_k = dk;
-        src_p = dp;
-    }
-    return MPSM_OK;
-}
 
 // ------------------------------------------------------------ partition scatter
 extern "C" int mpsm_scatter_workspace_bytes(int64_t n, int npart, size_t* bytes) {

@@ -98,6 +98,22 @@ def sort_pairs(in_k: torch.Tensor, in_p: torch.Tensor, lower: int, span_m1: int,
                "mpsm_sort_pairs")
 
 
+def sort_packed(in_k: torch.Tensor, in_p: torch.Tensor, lower: int, span_m1: int, width_bits: int,
+                out_rec: torch.Tensor, tmp_rec: torch.Tensor, bad: Optional[torch.Tensor],
+                overflow: torch.Tensor) -> None:
+    """Sort into packed records (key - lower) << (64 - w) | payload; sets
+    overflow[0] = 1 if a payload does not fit (caller falls back to SoA)."""
+    n = int(in_k.numel())
+    if n == 0:
+        return
+    L = _lib.load()
+    sz = ctypes.c_size_t(0)
+    _lib.check(L.mpsm_sort_workspace_bytes(n, width_bits, ctypes.byref(sz)), "sort workspace")
+    ws = workspace(in_k.device).get(sz.value)
+    _lib.check(L.mpsm_sort_packed(ptr(in_k), ptr(in_p), n, lower, span_m1, width_bits, ptr(out_rec), ptr(tmp_rec),
+                                  ptr(ws), ws.numel(), ptr(bad), ptr(overflow), stream_ptr()), "mpsm_sort_packed")
+
+
 def radix_histogram(keys: torch.Tensor, lower: int, span_m1: int, shift: int, nbuckets: int,
                     counts: torch.Tensor, bad: Optional[torch.Tensor] = None) -> None:
     n = int(keys.numel())
@@ -152,6 +168,23 @@ def join_pairs(priv: Sequence[tuple], pub: Sequence[tuple], swap: bool, mode: in
     rec = torch.empty((len(priv) * len(pub), _lib.PAIR_FIELDS), dtype=U64, device=dev)
     _lib.check(L.mpsm_join_pairs(pa, len(priv), ua, len(pub), int(bool(swap)), int(mode), ptr(out), int(cap),
                                  ptr(rec), ptr(ws), ws.numel(), stream_ptr()), "mpsm_join_pairs")
+    return rec
+
+
+def join_pairs_packed(priv: Sequence[torch.Tensor], pub: Sequence[torch.Tensor], width_bits: int, lower: int,
+                      swap: bool, mode: int, out: Optional[torch.Tensor] = None, cap: int = 0) -> torch.Tensor:
+    """join_pairs over runs of packed records (one uint64 tensor per run)."""
+    dev = (priv[0] if priv else pub[0]).device
+    pa = _lib.runs_array((ptr(k) or 0, 0, int(k.numel())) for k in priv)
+    ua = _lib.runs_array((ptr(k) or 0, 0, int(k.numel())) for k in pub)
+    L = _lib.load()
+    sz = ctypes.c_size_t(0)
+    _lib.check(L.mpsm_join_workspace_bytes(pa, len(priv), ua, len(pub), ctypes.byref(sz)), "join workspace")
+    ws = workspace(dev).get(sz.value)
+    rec = torch.empty((len(priv) * len(pub), _lib.PAIR_FIELDS), dtype=U64, device=dev)
+    _lib.check(L.mpsm_join_pairs_packed(pa, len(priv), ua, len(pub), width_bits, lower, int(bool(swap)), int(mode),
+                                        ptr(out), int(cap), ptr(rec), ptr(ws), ws.numel(), stream_ptr()),
+               "mpsm_join_pairs_packed")
     return rec
 
 

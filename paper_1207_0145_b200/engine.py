@@ -179,16 +179,27 @@ def _raise_domain(flag: torch.Tensor, rel_name: str) -> None:
         raise DomainError(f"relation {rel_name} has out-of-domain keys (first at index {idx})")
 
 
-class JoinContext:
-    """Device buffers and state of one join on one GPU."""
+# packed 8-B records (key - lower) << (64 - w) | payload are used whenever the
+# key width allows it and every payload fits; a join that meets a wide payload
+# is re-run on (key, payload) pairs.  MPSM_PACK=0 forces the pair layout.
+PACK_RECORDS = os.environ.get("MPSM_PACK", "1") != "0"
 
-    def __init__(self, r: Relation, s: Relation, cfg: JoinConfig, phase_hook: PhaseHook):
+
+class JoinContext:
+    """Device buffers and state of one join on one GPU.
+
+    Runs are (keys, payloads) tensor pairs, or (records, None) in packed mode.
+    """
+
+    def __init__(self, r: Relation, s: Relation, cfg: JoinConfig, phase_hook: PhaseHook, packed: bool):
         self.cfg = cfg
         self.hook = phase_hook
         self.dev = D.ensure_device()
         self.dom, self.roles, private, public = _prepare(r, s, cfg)
         self.t = cfg.threads
         self.wbits = self.dom.width_bits
+        self.packed = bool(packed) and 1 <= self.wbits <= 63
+        self.pw = 64 - self.wbits
         self.span_m1 = self.dom.upper - self.dom.lower - 1
         self.priv_k = D.to_device(private.keys, self.dev)
         self.priv_p = D.to_device(private.payloads, self.dev)
@@ -201,48 +212,71 @@ class JoinContext:
         self.stats = [WorkerStats(i) for i in range(self.t)]
         self.bad_pub = D.new_bad_flag(self.dev)
         self.bad_priv = D.new_bad_flag(self.dev)
+        self.overflow = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.tmp = []
         self.tl = _Timeline()
 
     def _hook(self, i: int, phase: str) -> None:
         if self.hook:
             self.hook(i, phase)
 
+    def _empty(self, n: int) -> torch.Tensor:
+        return torch.empty(n, dtype=torch.uint64, device=self.dev)
+
+    def _tmp(self, width: int) -> list:
+        """ping-pong buffers of the run sorts, shared by all phases"""
+        if not self.tmp or self.tmp[0].numel() < width:
+            self.tmp = [self._empty(width) for _ in range(1 if self.packed else 2)]
+        return self.tmp
+
+    def _alloc_runs(self, n: int) -> tuple:
+        return (self._empty(n), None) if self.packed else (self._empty(n), self._empty(n))
+
+    def _sort_into(self, in_k, in_p, dst: tuple, a: int, b: int, bad) -> tuple:
+        """sort in_k/in_p (length b-a) into dst[.][a:b]; returns the run"""
+        n = b - a
+        tmp = self._tmp(n)
+        if self.packed:
+            out = dst[0][a:b]
+            if n:
+                D.sort_packed(in_k, in_p, self.dom.lower, self.span_m1, self.wbits, out, tmp[0][:n], bad,
+                              self.overflow)
+            return (out, None)
+        ok, op = dst[0][a:b], dst[1][a:b]
+        if n:
+            D.sort_pairs(in_k, in_p, self.dom.lower, self.span_m1, self.wbits, ok, op, tmp[0][:n], tmp[1][:n], bad)
+        return (ok, op)
+
     def sort_public(self):
         """phase 1: every public chunk -> sorted run (engine.py:389-395)."""
-        n = self.n_pub
-        self.run_k = torch.empty(n, dtype=torch.uint64, device=self.dev)
-        self.run_p = torch.empty(n, dtype=torch.uint64, device=self.dev)
-        width = max((b - a for a, b in self.pub_chunks), default=0)
-        self.tmp_k = torch.empty(width, dtype=torch.uint64, device=self.dev)
-        self.tmp_p = torch.empty(width, dtype=torch.uint64, device=self.dev)
+        self._tmp(max((b - a for a, b in self.pub_chunks), default=0))
+        self.pub_store = self._alloc_runs(self.n_pub)
         self.pub_runs = []
         for i, (a, b) in enumerate(self.pub_chunks):
             self._hook(i, "sort_public")
-            if b > a:
-                D.sort_pairs(self.pub_k[a:b], self.pub_p[a:b], self.dom.lower, self.span_m1, self.wbits,
-                             self.run_k[a:b], self.run_p[a:b], self.tmp_k[:b - a], self.tmp_p[:b - a], self.bad_pub)
-            self.pub_runs.append((self.run_k[a:b], self.run_p[a:b]))
+            self.pub_runs.append(self._sort_into(self.pub_k[a:b], self.pub_p[a:b], self.pub_store, a, b, self.bad_pub))
             self.stats[i].tuples_sorted_public = b - a
 
-    def _ensure_tmp(self, width: int) -> None:
-        if self.tmp_k.numel() < width:
-            self.tmp_k = torch.empty(width, dtype=torch.uint64, device=self.dev)
-            self.tmp_p = torch.empty(width, dtype=torch.uint64, device=self.dev)
-
     def sort_private_chunks(self):
-        """B-MPSM phase 2: each private chunk sorted into its own run."""
-        self.priv_run_k = torch.empty(self.n_priv, dtype=torch.uint64, device=self.dev)
-        self.priv_run_p = torch.empty(self.n_priv, dtype=torch.uint64, device=self.dev)
-        self._ensure_tmp(max((b - a for a, b in self.priv_chunks), default=0))
+        """B-MPSM phase 2 / P-MPSM with T=1: each private chunk sorted into its run."""
+        self.priv_store = self._alloc_runs(self.n_priv)
         self.priv_runs = []
         for i, (a, b) in enumerate(self.priv_chunks):
             self._hook(i, "sort_private")
-            if b > a:
-                D.sort_pairs(self.priv_k[a:b], self.priv_p[a:b], self.dom.lower, self.span_m1, self.wbits,
-                             self.priv_run_k[a:b], self.priv_run_p[a:b], self.tmp_k[:b - a], self.tmp_p[:b - a],
-                             self.bad_priv)
-            self.priv_runs.append((self.priv_run_k[a:b], self.priv_run_p[a:b]))
+            self.priv_runs.append(self._sort_into(self.priv_k[a:b], self.priv_p[a:b], self.priv_store, a, b,
+                                                  self.bad_priv))
             self.stats[i].tuples_sorted_private = b - a
+
+    def _public_bound_keys(self, f: int) -> np.ndarray:
+        """equi-height bound keys of every sorted public run (skew.py:52-62)"""
+        pos_list = [torch.from_numpy(bound_positions(b - a, f, self.t) + a) for a, b in self.pub_chunks if b > a]
+        if not pos_list:
+            return np.empty(0, np.uint64)
+        gather = torch.cat(pos_list).to(self.dev)
+        vals = self.pub_store[0].view(torch.int64)[gather].cpu().numpy().view(np.uint64)
+        if self.packed:
+            vals = (vals >> np.uint64(self.pw)) + np.uint64(self.dom.lower)
+        return vals
 
     def partition(self):
         """P-MPSM phase 2 (engine.py:359-374, 396-406): histograms, splitters,
@@ -257,17 +291,10 @@ class JoinContext:
         for i, (a, b) in enumerate(self.priv_chunks):
             self._hook(i, "histogram")
             D.radix_histogram(self.priv_k[a:b], dom.lower, self.span_m1, shift, nb, hists[i], self.bad_priv)
-        # equi-height bounds of every sorted public run (skew.py:52-62)
         f = self.cfg.cdf_fanout
-        pos_list = []
-        for a, b in self.pub_chunks:
-            if b > a:
-                pos_list.append(torch.from_numpy(bound_positions(b - a, f, t) + a))
-        gather = torch.cat(pos_list).to(self.dev) if pos_list else None
-        bound_keys = self.run_k.view(torch.int64)[gather].view(torch.uint64) if gather is not None else None
         # the single host synchronisation of the join: counts + bounds + flags
+        bk = self._public_bound_keys(f)
         hist_h = hists.cpu().numpy()
-        bk = bound_keys.cpu().numpy() if bound_keys is not None else np.empty(0, np.uint64)
         _raise_domain(self.bad_priv, "private")
         _raise_domain(self.bad_pub, "public")
         bounds, off = [], 0
@@ -283,12 +310,11 @@ class JoinContext:
         cursors = combine_counts(list(hist_h), ss.vector.sp, t)
         cursors.verify_disjoint()
         self.cursors = cursors
-        arena_k = torch.empty(self.n_priv, dtype=torch.uint64, device=self.dev)
-        arena_p = torch.empty(self.n_priv, dtype=torch.uint64, device=self.dev)
+        arena_k = self._empty(self.n_priv)
+        arena_p = self._empty(self.n_priv)
         sp_dev = torch.from_numpy(ss.vector.sp.astype(np.int32)).to(self.dev)
         cur_all = torch.from_numpy(np.stack([cursors.absolute_cursors(i)[0] for i in range(t)])).to(self.dev)
         written = torch.zeros((t, t), dtype=torch.int64, device=self.dev)
-        self.tl.mark("hist")
         for i, (a, b) in enumerate(self.priv_chunks):
             self._hook(i, "scatter")
             D.scatter_chunk(self.priv_k[a:b], self.priv_p[a:b], dom.lower, shift, sp_dev, nb, t, cur_all[i],
@@ -301,19 +327,19 @@ class JoinContext:
     def sort_partitions(self, run_base):
         """P-MPSM phase 3 (engine.py:405-409)."""
         arena_k, arena_p = self.arena
-        self.priv_run_k = torch.empty(self.n_priv, dtype=torch.uint64, device=self.dev)
-        self.priv_run_p = torch.empty(self.n_priv, dtype=torch.uint64, device=self.dev)
-        self._ensure_tmp(int(np.max(np.diff(run_base))) if len(run_base) > 1 else 0)
+        self.priv_store = self._alloc_runs(self.n_priv)
         self.priv_runs = []
         for i in range(self.t):
             a, b = int(run_base[i]), int(run_base[i + 1])
             self._hook(i, "sort_private")
-            if b > a:
-                D.sort_pairs(arena_k[a:b], arena_p[a:b], self.dom.lower, self.span_m1, self.wbits,
-                             self.priv_run_k[a:b], self.priv_run_p[a:b], self.tmp_k[:b - a], self.tmp_p[:b - a],
-                             None)
-            self.priv_runs.append((self.priv_run_k[a:b], self.priv_run_p[a:b]))
+            self.priv_runs.append(self._sort_into(arena_k[a:b], arena_p[a:b], self.priv_store, a, b, None))
             self.stats[i].tuples_sorted_private = b - a
+
+    def _join(self, mode: int, out=None, cap: int = 0):
+        if self.packed:
+            return D.join_pairs_packed([r[0] for r in self.priv_runs], [r[0] for r in self.pub_runs], self.wbits,
+                                       self.dom.lower, self.roles.swapped, mode, out, cap)
+        return D.join_pairs(self.priv_runs, self.pub_runs, self.roles.swapped, mode, out, cap)
 
     def join(self):
         """phase 4 (engine.py:228-276, 410-419) for all workers in one launch sequence."""
@@ -321,14 +347,17 @@ class JoinContext:
             self._hook(i, "join")
         mode = {"aggregate-max": _lib.MODE_AGGREGATE_MAX, "count": _lib.MODE_COUNT,
                 "materialize": _lib.MODE_COUNT}[self.cfg.query_mode]
-        self.rec = D.join_pairs(self.priv_runs, self.pub_runs, self.roles.swapped, mode)
+        self.rec = self._join(mode)
 
     def materialize(self, total: int) -> np.ndarray:
         if total == 0:
             return np.empty((0, 2), np.uint64)
-        out = torch.empty(2 * total, dtype=torch.uint64, device=self.dev)
-        D.join_pairs(self.priv_runs, self.pub_runs, self.roles.swapped, _lib.MODE_MATERIALIZE, out, total)
+        out = self._empty(2 * total)
+        self._join(_lib.MODE_MATERIALIZE, out, total)
         return out.view(total, 2).cpu().numpy()
+
+    def packed_overflowed(self) -> bool:
+        return self.packed and int(self.overflow.item()) != 0
 
     def finalize(self, timings: dict) -> JoinResult:
         """engine.py:195-225 plus the checksum and per-worker statistics."""
@@ -371,32 +400,16 @@ class JoinContext:
                           phase_timings=timings, worker_stats=self.stats, checksum=int(csum))
 
 
-def run_bmpsm(r: Relation, s: Relation, cfg: JoinConfig, *, phase_hook: PhaseHook = None) -> JoinResult:
-    """Basic variant: sort both inputs chunk-wise, join every private run
-    against every public run (engine.py:279-334)."""
-    ctx = JoinContext(r, s, cfg, phase_hook)
+def _run(variant: str, r: Relation, s: Relation, cfg: JoinConfig, phase_hook: PhaseHook,
+         packed: Optional[bool] = None) -> JoinResult:
+    ctx = JoinContext(r, s, cfg, phase_hook, PACK_RECORDS if packed is None else packed)
     ctx.tl.mark("t0")
     ctx.sort_public()
     ctx.tl.mark("public")
-    ctx.sort_private_chunks()
-    ctx.tl.mark("sort_private")
-    ctx.join()
-    ctx.tl.mark("join")
-    torch.cuda.current_stream().synchronize()
-    tl = ctx.tl
-    timings = {"sort_public": tl.seconds("t0", "public"), "partition": 0.0,
-               "sort_private": tl.seconds("public", "sort_private"), "join": tl.seconds("sort_private", "join"),
-               "total": tl.seconds("t0", "join")}
-    return ctx.finalize(timings)
-
-
-def run_pmpsm(r: Relation, s: Relation, cfg: JoinConfig, *, phase_hook: PhaseHook = None) -> JoinResult:
-    """Range-partitioned variant (engine.py:337-433)."""
-    ctx = JoinContext(r, s, cfg, phase_hook)
-    ctx.tl.mark("t0")
-    ctx.sort_public()
-    ctx.tl.mark("public")
-    if ctx.t == 1:
+    if variant == "b-mpsm":
+        ctx.tl.mark("scatter")
+        ctx.sort_private_chunks()
+    elif ctx.t == 1:
         # one partition: the histogram/scatter are the identity (the splitter
         # search returns [0, 2^B]); sort the private input directly
         effective_radix_bits(ctx.dom, cfg.radix_bits)
@@ -413,15 +426,31 @@ def run_pmpsm(r: Relation, s: Relation, cfg: JoinConfig, *, phase_hook: PhaseHoo
     ctx.join()
     ctx.tl.mark("join")
     torch.cuda.current_stream().synchronize()
-    if ctx.t > 1:
-        exp = ctx.cursors.counts
-        if not np.array_equal(ctx.written.cpu().numpy(), exp):
+    if ctx.packed_overflowed():
+        # a payload needs more than 64 - w bits: redo on (key, payload) pairs
+        _raise_domain(ctx.bad_priv, "private")
+        _raise_domain(ctx.bad_pub, "public")
+        return _run(variant, r, s, cfg, phase_hook, packed=False)
+    if variant == "p-mpsm" and ctx.t > 1:
+        if not np.array_equal(ctx.written.cpu().numpy(), ctx.cursors.counts):
             raise InternalConsistencyError("scatter wrote a different number of tuples than the histograms promised")
     tl = ctx.tl
-    timings = {"sort_public": tl.seconds("t0", "public"), "partition": tl.seconds("public", "scatter"),
+    timings = {"sort_public": tl.seconds("t0", "public"),
+               "partition": tl.seconds("public", "scatter") if variant == "p-mpsm" else 0.0,
                "sort_private": tl.seconds("scatter", "sort_private"), "join": tl.seconds("sort_private", "join"),
                "total": tl.seconds("t0", "join")}
     return ctx.finalize(timings)
+
+
+def run_bmpsm(r: Relation, s: Relation, cfg: JoinConfig, *, phase_hook: PhaseHook = None) -> JoinResult:
+    """Basic variant: sort both inputs chunk-wise, join every private run
+    against every public run (engine.py:279-334)."""
+    return _run("b-mpsm", r, s, cfg, phase_hook)
+
+
+def run_pmpsm(r: Relation, s: Relation, cfg: JoinConfig, *, phase_hook: PhaseHook = None) -> JoinResult:
+    """Range-partitioned variant (engine.py:337-433)."""
+    return _run("p-mpsm", r, s, cfg, phase_hook)
 
 
 def run_join(r: Relation, s: Relation, cfg: JoinConfig, *, phase_hook: PhaseHook = None) -> JoinResult:

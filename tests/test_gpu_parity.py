@@ -32,7 +32,16 @@ def _cfg(case, **kw):
 
 # --------------------------------------------------------------- engine parity
 
-def test_engine_cases_match_reference(golden):
+@pytest.fixture(params=[True, False], ids=["packed", "pairs"])
+def pack_mode(request, monkeypatch):
+    """run with packed 8-B records (default) and with (key, payload) pairs"""
+    from paper_1207_0145_b200 import engine
+
+    monkeypatch.setattr(engine, "PACK_RECORDS", request.param)
+    return request.param
+
+
+def test_engine_cases_match_reference(golden, pack_mode):
     import warnings
 
     checked = 0
@@ -64,7 +73,7 @@ def test_engine_cases_match_reference(golden):
     assert checked > 100
 
 
-def test_materialized_multiset_matches_oracle():
+def test_materialized_multiset_matches_oracle(pack_mode):
     d = dataset("dup_heavy")
     rk, rp, sk, sp, lo, up = make_inputs(d)
     want = orc.join(rk, rp, sk, sp, threads=1, lower=lo, upper=up, query_mode="materialize", materialize_cap=1 << 24)
@@ -77,7 +86,7 @@ def test_materialized_multiset_matches_oracle():
             assert got == sorted(map(tuple, want.materialized.tolist()))
 
 
-def test_config1_golden(golden):
+def test_config1_golden(golden, pack_mode):
     g = golden["config1"]
     r, s, dom = P.gen_fk(g["n_r"], g["n_s"], g["seed"])
     for t in (1, 8):
@@ -105,7 +114,7 @@ def test_fk_vs_oracle_gather(n_r, n_s, seed):
                                                                               s.payloads, 1)
 
 
-def test_negcorr_skew_vs_oracle():
+def test_negcorr_skew_vs_oracle(pack_mode):
     dom = KeyDomain(1, 1 << 32)
     r, s = P.gen_negcorr(400_000, 1_600_000, dom, seed=0)
     want = orc.join(r.keys, r.payloads, s.keys, s.payloads, threads=4, lower=dom.lower, upper=dom.upper,
@@ -116,7 +125,7 @@ def test_negcorr_skew_vs_oracle():
                                                                      want.checksum)
 
 
-def test_heavy_duplicates_cross_product():
+def test_heavy_duplicates_cross_product(pack_mode):
     # 200 x 200 pairs on one key plus a sprinkle of other keys
     rng = np.random.default_rng(3)
     rk = np.concatenate([np.full(200, 3, np.uint64), rng.integers(0, 8, 50, dtype=np.uint64)])
@@ -270,3 +279,39 @@ def test_launch_counter_moves():
     r, s, dom = P.gen_fk(1000, 4000, 1)
     P.run_join(r, s, JoinConfig(key_domain=dom))
     assert _lib.launch_count() > before
+
+
+def test_wide_payloads_fall_back_to_pairs():
+    # domain [0, 2^32) leaves 32 payload bits in a packed record; 2^40 payloads
+    # overflow it, so the engine must redo the join on (key, payload) pairs
+    rng = np.random.default_rng(4)
+    rk = rng.integers(0, 1 << 32, 50_000, dtype=np.uint64)
+    sk = np.concatenate([rk[:30_000], rng.integers(0, 1 << 32, 20_000, dtype=np.uint64)])
+    rp = rng.integers(0, 1 << 44, rk.shape[0], dtype=np.uint64)
+    sp = rng.integers(0, 1 << 63, sk.shape[0], dtype=np.uint64)
+    want = orc.join(rk, rp, sk, sp, threads=2, lower=0, upper=1 << 32)
+    for t in (1, 2):
+        res = P.run_join(Relation(rk, rp), Relation(sk, sp), JoinConfig(threads=t, key_domain=KeyDomain(0, 1 << 32)))
+        assert (res.match_count, res.aggregate_max, res.checksum) == (want.match_count, want.aggregate_max,
+                                                                     want.checksum)
+
+
+@pytest.mark.parametrize("width", [1, 7, 27, 33, 63])
+def test_packed_sort_round_trip(width):
+    n = 300_001
+    rng = np.random.default_rng(width)
+    lower = 5
+    keys = rng.integers(lower, lower + (1 << width), n, dtype=np.uint64)
+    pw = 64 - width
+    pays = rng.integers(0, 1 << min(pw, 63), n, dtype=np.uint64)
+    kd, pd = torch.from_numpy(keys).to(DEV), torch.from_numpy(pays).to(DEV)
+    out, tmp = torch.empty_like(kd), torch.empty_like(kd)
+    ovf = torch.zeros(1, dtype=torch.int32, device=DEV)
+    D.sort_packed(kd, pd, lower, (1 << width) - 1, width, out, tmp, None, ovf)
+    rec = out.cpu().numpy()
+    assert int(ovf.item()) == 0
+    got_k = (rec >> np.uint64(pw)) + np.uint64(lower)
+    got_p = rec & np.uint64((1 << pw) - 1) if pw < 64 else rec
+    order = np.argsort(keys, kind="stable")
+    assert np.array_equal(got_k, keys[order])
+    assert np.array_equal(got_p, pays[order])

@@ -1,0 +1,63 @@
+// Microbenchmark (tooling, not product): how fast does the memory system take
+// the onesweep write pattern?  Each CTA reads a contiguous tile of `tile`
+// u64 (coalesced) and writes it as nbins runs of tile/nbins elements to
+// nbins far-apart regions (bucket d of tile t at d*(n/nbins) + t*run), the
+// pattern a radix pass produces after smem staging.  Compares with a plain
+// copy.  Usage: scatter_pattern_bench n tile nbins
+#include <cstdio>
+#include <cstdlib>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__global__ void copy_k(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, size_t n) {
+    size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    for (; i < n; i += (size_t)gridDim.x * blockDim.x) out[i] = in[i];
+}
+
+template <int THREADS>
+__global__ void scatter_k(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, size_t n, int tile,
+                          int nbins) {
+    const size_t t = blockIdx.x;
+    const size_t base = t * tile;
+    const int run = tile / nbins;
+    const size_t region = n / nbins;
+    for (int i = threadIdx.x; i < tile; i += THREADS) {
+        const uint64_t v = in[base + i];
+        const int d = i / run, r = i % run;
+        out[(size_t)d * region + t * run + r] = v;
+    }
+}
+
+int main(int argc, char** argv) {
+    size_t n = argc > 1 ? strtoull(argv[1], 0, 10) : 400000000ull;
+    int tile = argc > 2 ? atoi(argv[2]) : 6144;
+    int nbins = argc > 3 ? atoi(argv[3]) : 512;
+    n = n / tile * tile;
+    uint64_t *a, *b;
+    cudaMalloc(&a, n * 8);
+    cudaMalloc(&b, n * 8);
+    cudaMemset(a, 1, n * 8);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int it = 0; it < 3; ++it) {
+        cudaEventRecord(e0);
+        copy_k<<<148 * 8, 512>>>(a, b, n);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (it == 2) printf("copy     : %.3f ms  %.0f GB/s\n", ms, 16.0 * n / ms / 1e6);
+    }
+    for (int it = 0; it < 3; ++it) {
+        cudaEventRecord(e0);
+        scatter_k<512><<<(unsigned)(n / tile), 512>>>(a, b, n, tile, nbins);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (it == 2) printf("scatter  : tile %d bins %d run %d: %.3f ms  %.0f GB/s\n", tile, nbins, tile / nbins, ms,
+                            16.0 * n / ms / 1e6);
+    }
+    return 0;
+}

@@ -1,0 +1,39 @@
+"""Per-phase cycle breakdown of seg::k_scatter (variant built with
+MPSM_DBG_TIMING) for the LAST pass of a packed sort of n keys."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ["MPSM_LIB"] = os.path.join(ROOT, "build", "variants_dbg", os.environ.get("DBGV", "timing"), "libmpsm_b200.so")
+from paper_1207_0145_b200 import _lib, device as D  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 400_000_000
+bits = 27
+packed = (sys.argv[2] if len(sys.argv) > 2 else "packed") == "packed"
+dev = torch.device("cuda", 0)
+keys = torch.randint(0, 1 << bits, (n,), device=dev, dtype=torch.int64).view(torch.uint64)
+pays = torch.randint(0, 1 << 32, (n,), device=dev, dtype=torch.int64).view(torch.uint64)
+o = [torch.empty_like(keys) for _ in range(4)]
+ovf = torch.zeros(1, dtype=torch.int32, device=dev)
+D.ensure_device()
+for _ in range(2):
+    if packed:
+        D.sort_packed(keys, pays, 0, (1 << bits) - 1, bits, o[0], o[1], None, ovf)
+    else:
+        D.sort_pairs(keys, pays, 0, (1 << bits) - 1, bits, o[0], o[1], o[2], o[3], None)
+torch.cuda.synchronize()
+L = _lib.load()
+ntiles = (n + 4095) // 4096
+buf = np.zeros((ntiles, 8), np.int64)
+L.mpsm_dbg_seg_ts(buf.ctypes.data_as(ctypes.c_void_p), ntiles)
+d = np.diff(buf[:, :7], axis=1)
+names = ["wait_data(sync)", "load+rank", "colsum+scan", "pos+payload", "stage", "write"]
+tot = buf[:, 6] - buf[:, 0]
+print(f"{'packed' if packed else 'pairs'} tiles={ntiles} cycles/tile median {np.median(tot):.0f}")
+for i, nm in enumerate(names):
+    print(f"  {nm:18s} median {np.median(d[:, i]):7.0f} mean {np.mean(d[:, i]):7.0f} p90 {np.percentile(d[:, i], 90):7.0f}")

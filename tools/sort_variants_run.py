@@ -22,20 +22,27 @@ keys = torch.randint(0, 1 << bits, (n,), device=dev, generator=g, dtype=torch.in
 pays = torch.arange(n, device=dev, dtype=torch.int64).view(torch.uint64)
 ok = torch.empty_like(keys); op = torch.empty_like(pays); tk = torch.empty_like(keys); tp = torch.empty_like(pays)
 D.ensure_device()
-res = []
-for it in range(4):
-    _lib.profile_enable(True)
-    a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
-    a.record()
-    D.sort_pairs(keys, pays, 0, (1 << bits) - 1, bits, ok, op, tk, tp, None)
-    b.record(); torch.cuda.synchronize()
-    res.append((a.elapsed_time(b), _lib.profile_read("onesweep"), _lib.profile_read("upfront_hist")))
-srt = ok.view(torch.int64)
-sorted_ok = bool((srt[1:] >= srt[:-1]).all())
-best = min(res)
-ms, (os_ms, os_n), (h_ms, _) = best
-print(f"{os.environ['VNAME']:24s} total {ms:7.3f} ms  onesweep {os_ms:7.3f} ms/{os_n} = {os_ms/os_n:6.3f} ms/pass "
-      f"({32*n/(os_ms/os_n)/1e6:7.1f} GB/s)  hist {h_ms:6.3f} ms sorted={sorted_ok}", flush=True)
+ovf = torch.zeros(1, dtype=torch.int32, device=dev)
+for packed in (False, True):
+    res = []
+    for it in range(4):
+        _lib.profile_enable(True)
+        a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        if packed:
+            D.sort_packed(keys, pays, 0, (1 << bits) - 1, bits, ok, tk, None, ovf)
+        else:
+            D.sort_pairs(keys, pays, 0, (1 << bits) - 1, bits, ok, op, tk, tp, None)
+        b.record(); torch.cuda.synchronize()
+        res.append((a.elapsed_time(b), _lib.profile_read("seg_scatter"), _lib.profile_read("seg_count")))
+    srt = (ok >> (64 - bits) if packed else ok).view(torch.int64) if False else ok.view(torch.int64)
+    if packed:
+        srt = torch.bitwise_right_shift(ok.view(torch.int64), 64 - bits) & ((1 << bits) - 1)
+    sorted_ok = bool((srt[1:] >= srt[:-1]).all())
+    best = min(res)
+    ms, (os_ms, os_n), (h_ms, h_n) = best
+    print(f"{os.environ['VNAME']:10s} {'packed' if packed else 'pairs ':6s} total {ms:7.3f} ms  scatter {os_ms:7.3f} ms/{os_n} passes"
+          f" = {os_ms/os_n:6.3f} ms/pass  count {h_ms:6.3f} ms/{h_n}  sorted={sorted_ok}", flush=True)
 '''
 for lib in sorted(glob.glob(os.path.join(ROOT, "build", "variants", "*", "libmpsm_b200.so"))):
     name = os.path.basename(os.path.dirname(lib))
