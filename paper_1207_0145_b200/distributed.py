@@ -1,0 +1,373 @@
+"""Multi-GPU MPSM join: one process per GPU, torch.distributed (NCCL) plumbing.
+
+The paper's T workers become the G ranks of the process group (SURVEY.md
+8(e)); rank i holds position-shard i of R and S (the chunk rule,
+core.py:263-279) and plays worker i of P-MPSM (engine.py:337-433):
+
+  1. sort its public shard into public run i                    (local, HBM)
+  2. histogram its private shard; all-gather the histograms and
+     the f*G equi-height bounds of every public run             (tiny collective)
+  3. every rank computes the same splitters (skew.py:287-315)
+  4. stable partition scatter of the private shard into G send
+     segments (the reference's arena layout, partition.py:233)
+  5. ONE all-to-all(v) of the private tuples over NVLink         (NCCL)
+  6. sort the received partition into private run i
+  7. merge-join private run i against every public run; the
+     G-1 remote runs are read in place through NVLink peer loads
+     (CUDA IPC mappings, the paper's remote-NUMA reads,
+     engine.py:249-260)
+  8. all-gather the G x G pair records and fold them exactly like
+     the single-GPU engine (_finalize, engine.py:195-225)
+
+Device work goes through a backend object.  The product backend is
+CudaBackend (libmpsm_b200.so); tests/test_distributed.py runs the same
+protocol under gloo with a CPU backend built on the test oracle, which is how
+the multi-rank host logic is covered without several GPUs.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import os
+import time
+from typing import Optional
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from . import device as D
+from .core import (
+    ConfigurationError,
+    DomainError,
+    JoinConfig,
+    JoinResult,
+    MaterializeCapExceeded,
+    Relation,
+    WorkerStats,
+)
+from .engine import MASK64, PACK_RECORDS, choose_roles
+from .partition import combine_counts, effective_radix_bits
+from .skew import LocalBounds, bound_positions, build_cdf, compute_splitters
+
+
+class CudaBackend:
+    """Device operations of one rank on its own GPU."""
+
+    def __init__(self, device: Optional[torch.device] = None, packed: Optional[bool] = None):
+        self.dev = D.ensure_device(device)
+        self.packed_pref = PACK_RECORDS if packed is None else packed
+        self.comm_device = self.dev
+
+    def setup(self, dom):
+        self.dom = dom
+        self.wbits = dom.width_bits
+        self.packed = self.packed_pref and 1 <= self.wbits <= 63
+        self.pw = 64 - self.wbits
+        self.span_m1 = dom.upper - dom.lower - 1
+        self.bad = D.new_bad_flag(self.dev)
+        self.overflow = torch.zeros(1, dtype=torch.int32, device=self.dev)
+
+    def to_device(self, a) -> torch.Tensor:
+        return D.to_device(a, self.dev)
+
+    def empty(self, n: int) -> torch.Tensor:
+        return torch.empty(n, dtype=torch.uint64, device=self.dev)
+
+    def sort(self, k, p):
+        n = int(k.numel())
+        if self.packed:
+            out, tmp = self.empty(n), self.empty(n)
+            D.sort_packed(k, p, self.dom.lower, self.span_m1, self.wbits, out, tmp, self.bad, self.overflow)
+            return (out, None)
+        ok, op, tk, tp = self.empty(n), self.empty(n), self.empty(n), self.empty(n)
+        D.sort_pairs(k, p, self.dom.lower, self.span_m1, self.wbits, ok, op, tk, tp, self.bad)
+        return (ok, op)
+
+    def histogram(self, keys, shift: int, nb: int) -> np.ndarray:
+        counts = torch.zeros(nb, dtype=torch.int64, device=self.dev)
+        D.radix_histogram(keys, self.dom.lower, self.span_m1, shift, nb, counts, self.bad)
+        return counts.cpu().numpy()
+
+    def bound_keys(self, run, f: int, t: int) -> np.ndarray:
+        n = int(run[0].numel())
+        if n == 0:
+            return np.empty(0, np.uint64)
+        pos = torch.from_numpy(bound_positions(n, f, t)).to(self.dev)
+        vals = run[0].view(torch.int64)[pos].cpu().numpy().view(np.uint64)
+        if self.packed:
+            vals = (vals >> np.uint64(self.pw)) + np.uint64(self.dom.lower)
+        return vals
+
+    def partition(self, k, p, shift: int, sp: np.ndarray, npart: int, starts: np.ndarray):
+        n = int(k.numel())
+        sk, spay = self.empty(n), self.empty(n)
+        written = torch.zeros(npart, dtype=torch.int64, device=self.dev)
+        D.scatter_chunk(k, p, self.dom.lower, shift, torch.from_numpy(sp.astype(np.int32)).to(self.dev), sp.shape[0],
+                        npart, torch.from_numpy(starts.astype(np.int64)).to(self.dev), sk, spay, written)
+        return sk, spay
+
+    def bad_index(self) -> int:
+        return int(self.bad.item())
+
+    def overflowed(self) -> bool:
+        return self.packed and int(self.overflow.item()) != 0
+
+    def share(self, run):
+        """CUDA IPC description of a run, for peer ranks (torch's own mechanism)."""
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        return [None if t is None else reduce_tensor(t) for t in run]
+
+    def open(self, shared):
+        return tuple(None if s is None else s[0](*s[1]) for s in shared)
+
+    def join(self, priv_runs, pub_runs, swap: bool, mode: int, out=None, cap: int = 0) -> torch.Tensor:
+        if self.packed:
+            return D.join_pairs_packed([r[0] for r in priv_runs], [r[0] for r in pub_runs], self.wbits,
+                                       self.dom.lower, swap, mode, out, cap)
+        return D.join_pairs(priv_runs, pub_runs, swap, mode, out, cap)
+
+    def materialize(self, priv_runs, pub_runs, swap: bool, total: int) -> np.ndarray:
+        if total == 0:
+            return np.empty((0, 2), np.uint64)
+        out = self.empty(2 * total)
+        self.join(priv_runs, pub_runs, swap, _lib.MODE_MATERIALIZE, out, total)
+        return out.view(total, 2).cpu().numpy()
+
+    def records(self, rec) -> np.ndarray:
+        return rec.cpu().numpy()
+
+    def sync(self):
+        torch.cuda.current_stream().synchronize()
+
+
+def _gather_obj(obj, group):
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, obj, group=group)
+    return out
+
+
+def _alltoall(be, k, p, send_counts, recv_counts, group):
+    """all-to-all(v) of the private tuples; received in source-rank order."""
+    n_recv = int(recv_counts.sum())
+    rk = torch.empty(n_recv, dtype=torch.int64, device=be.comm_device)
+    rp = torch.empty(n_recv, dtype=torch.int64, device=be.comm_device)
+    sc = [int(x) for x in send_counts]
+    rc = [int(x) for x in recv_counts]
+    dist.all_to_all_single(rk, k.view(torch.int64), rc, sc, group=group)
+    dist.all_to_all_single(rp, p.view(torch.int64), rc, sc, group=group)
+    return rk.view(torch.uint64), rp.view(torch.uint64)
+
+
+def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=None, backend=None,
+                         timings: Optional[dict] = None) -> JoinResult:
+    """P-MPSM over the ranks of `group`; r and s are this rank's shards.
+
+    Every rank returns the same JoinResult (worker i = rank i).  cfg.threads is
+    ignored: the worker count is the group size.
+    """
+    if cfg.algorithm != "p-mpsm":
+        raise ConfigurationError("the distributed engine runs p-mpsm")
+    G = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    be = backend or CudaBackend()
+    dom = cfg.key_domain
+    be.setup(dom)
+    t0 = time.perf_counter()
+    sizes = _gather_obj((r.cardinality, s.cardinality), group)
+    n_r, n_s = sum(x[0] for x in sizes), sum(x[1] for x in sizes)
+    roles = choose_roles(n_r, n_s, cfg.role_policy)
+    private, public = (r, s) if roles.private == "r" else (s, r)
+    bits = effective_radix_bits(dom, cfg.radix_bits)
+    if (1 << bits) < G:
+        raise ConfigurationError(f"effective radix bits {bits} give fewer buckets than {G} workers")
+    nb = 1 << bits
+    shift = dom.width_bits - bits
+    pk, pp = be.to_device(private.keys), be.to_device(private.payloads)
+    uk, up = be.to_device(public.keys), be.to_device(public.payloads)
+    stats = [WorkerStats(i) for i in range(G)]
+
+    # 1-2: public run, private histogram, bounds
+    pub_run = be.sort(uk, up)
+    hist = be.histogram(pk, shift, nb)
+    f = cfg.cdf_fanout
+    bk = be.bound_keys(pub_run, f, G)
+    info = _gather_obj((hist, bk, int(public.cardinality), be.bad_index()), group)
+    if any(x[3] != -1 for x in info):
+        raise DomainError("a relation shard has out-of-domain keys")
+    t_pub = time.perf_counter()
+    # 3: identical splitters on every rank
+    cdf = build_cdf([LocalBounds(x[1], x[2]) for x in info], anchor_key=dom.lower)
+    hists = [x[0] for x in info]
+    ss = compute_splitters(np.sum(hists, axis=0), cdf, G, dom, bits)
+    cursors = combine_counts(hists, ss.vector.sp, G)
+    cursors.verify_disjoint()
+    send_counts = cursors.counts[me]
+    recv_counts = cursors.counts[:, me]
+    send_starts = np.zeros(G, np.int64)
+    np.cumsum(send_counts[:-1], out=send_starts[1:])
+    # 4-5: scatter into send segments, one all-to-all
+    sk, sp = be.partition(pk, pp, shift, ss.vector.sp, G, send_starts)
+    rk, rp = _alltoall(be, sk, sp, send_counts, recv_counts, group)
+    t_part = time.perf_counter()
+    # 6: private run
+    priv_run = be.sort(rk, rp)
+    be.sync()
+    t_sort = time.perf_counter()
+    # 7: join against every public run (remote ones through peer mappings)
+    if G > 1:
+        shared = _gather_obj(be.share(pub_run), group)
+        pub_runs = [pub_run if j == me else be.open(shared[j]) for j in range(G)]
+    else:
+        pub_runs = [pub_run]
+    mode = {"aggregate-max": _lib.MODE_AGGREGATE_MAX, "count": _lib.MODE_COUNT,
+            "materialize": _lib.MODE_COUNT}[cfg.query_mode]
+    rec = be.records(be.join([priv_run], pub_runs, roles.swapped, mode))
+    overflow = be.overflowed()
+    gathered = _gather_obj((rec, int(rk.numel()), overflow), group)
+    if any(g[2] for g in gathered):
+        # a payload is wider than a packed record allows: redo on pairs
+        be2 = type(be)(packed=False) if isinstance(be, CudaBackend) else be.unpacked()
+        return run_join_distributed(r, s, cfg, group=group, backend=be2, timings=timings)
+    t_join = time.perf_counter()
+    # 8: fold, as engine.finalize with worker i = rank i
+    pub_sizes = [x[2] for x in info]
+    count, agg, csum = 0, None, 0
+    for i in range(G):
+        rec_i = gathered[i][0].reshape(G, _lib.PAIR_FIELDS).astype(object)
+        st = stats[i]
+        st.tuples_sorted_public = pub_sizes[i]
+        st.tuples_sorted_private = gathered[i][1]
+        st.tuples_scattered = int(cursors.counts[i].sum())
+        ci, bi = 0, 0
+        for j in range(G):
+            if gathered[i][1] == 0 or pub_sizes[j] == 0:
+                continue
+            c = int(rec_i[j, _lib.PAIR_COUNT])
+            st.probe_tuples_examined += int(rec_i[j, _lib.PAIR_PROBES])
+            st.public_tuples_examined += int(rec_i[j, _lib.PAIR_PROBES]) + int(rec_i[j, _lib.PAIR_EXAMINED])
+            if c > 0:
+                st.s_runs_with_matches += 1
+                b = int(rec_i[j, _lib.PAIR_BEST])
+                if ci == 0 or b > bi:
+                    bi = b
+                ci += c
+                csum = (csum + int(rec_i[j, _lib.PAIR_CHECKSUM])) & MASK64
+        count += ci
+        if ci > 0 and cfg.query_mode == "aggregate-max":
+            agg = bi if agg is None or bi > agg else agg
+    materialized = None
+    if cfg.query_mode == "materialize":
+        if count > cfg.materialize_cap:
+            raise MaterializeCapExceeded(f"join produced {count} pairs, cap is {cfg.materialize_cap}")
+        mine = int(sum(int(x) for x in rec.reshape(G, _lib.PAIR_FIELDS)[:, _lib.PAIR_COUNT]))
+        local = be.materialize([priv_run], pub_runs, roles.swapped, mine)
+        parts = _gather_obj(local, group)
+        materialized = np.concatenate(parts, axis=0) if parts else np.empty((0, 2), np.uint64)
+    tm = {"sort_public": t_pub - t0, "partition": t_part - t_pub, "sort_private": t_sort - t_part,
+          "join": t_join - t_sort, "total": t_join - t0}
+    if timings is not None:
+        timings.update(tm)
+    return JoinResult(match_count=int(count), aggregate_max=agg, materialized=materialized, phase_timings=tm,
+                      worker_stats=stats, checksum=int(csum))
+
+
+# ------------------------------------------------------------------ bench
+def fk_shard_device(n_r: int, n_s: int, rank: int, world: int, seed: int, device) -> tuple:
+    """Position-shard `rank` of a world-wide FK workload generated on the GPU.
+
+    Counter-based so a rank builds only its shard: R keys are a bijective
+    Feistel permutation of [0, n_r) (cycle walking) plus 1, S keys
+    splitmix64(seed, pos) mod n_r plus 1, payloads splitmix64 masked to 32
+    bits.  (The numpy generator of datagen.gen_fk needs the whole permutation
+    and is used at N=1.)
+    """
+    from .core import chunk_bounds
+
+    def mix(x):
+        x = x + (0x9E3779B97F4A7C15 - (1 << 64))  # int64 arithmetic wraps
+        x = (x ^ (x >> 30).bitwise_and((1 << 34) - 1)) * -4658895280553007687  # 0xBF58476D1CE4E5B9
+        x = (x ^ (x >> 27).bitwise_and((1 << 37) - 1)) * -7723592293110705685  # 0x94D049BB133111EB
+        return x ^ (x >> 31).bitwise_and((1 << 33) - 1)
+
+    ra, rb = chunk_bounds(n_r, world)[rank]
+    sa, sb = chunk_bounds(n_s, world)[rank]
+    half = max(1, math.ceil(math.log2(max(n_r, 2)) / 2))
+    mask = (1 << half) - 1
+
+    def feistel(x):
+        l, r_ = x >> half, x & mask
+        for rnd in range(4):
+            l, r_ = r_, l ^ (mix(r_ + (seed * 4 + rnd) * 0x1000193) & mask)
+        return (l << half) | r_
+
+    pos = torch.arange(ra, rb, dtype=torch.int64, device=device)
+    k = feistel(pos)
+    while True:
+        bad = k >= n_r
+        if not bool(bad.any()):
+            break
+        k = torch.where(bad, feistel(k), k)
+    r_keys = (k + 1).view(torch.uint64)
+    r_pays = (mix(pos + (2 * seed + 11) * (1 << 40)) & 0xFFFFFFFF).view(torch.uint64)
+    spos = torch.arange(sa, sb, dtype=torch.int64, device=device)
+    hs = mix(spos + (2 * seed + 1) * (1 << 41))
+    s_keys = ((hs & 0x7FFFFFFFFFFFFFFF) % n_r + 1).view(torch.uint64)
+    s_pays = (mix(spos + (2 * seed + 13) * (1 << 42)) & 0xFFFFFFFF).view(torch.uint64)
+    return Relation(r_keys, r_pays), Relation(s_keys, s_pays)
+
+
+def bench_main(args, metric, configs, make_inputs, Clocks, run_reference_sample):
+    """bench.py under torchrun: every rank holds a cfg-sized shard (weak scaling)."""
+    from .core import KeyDomain
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    G, me = dist.get_world_size(), dist.get_rank()
+    n_r1, n_s1, _ = configs[args.config]
+    n_r, n_s = n_r1 * G, n_s1 * G
+    dom = KeyDomain(1, n_r + 1)
+    r, s = fk_shard_device(n_r, n_s, me, G, 0, torch.device("cuda", local))
+    cfg = JoinConfig(threads=G, key_domain=dom)
+    be = CudaBackend()
+    for _ in range(args.warmup):
+        res = run_join_distributed(r, s, cfg, backend=be)
+    clocks = Clocks(local)
+    clocks.start()
+    dist.barrier()
+    torch.cuda.synchronize()
+    l0 = _lib.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        res = run_join_distributed(r, s, cfg, backend=be)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    dist.barrier()
+    clk = clocks.stop()
+    launches = _lib.launch_count() - l0
+    ms = float(ms.item())
+    ok = res.match_count == n_s
+    if me == 0:
+        line = {
+            "metric": metric, "value": (n_r + n_s) / (ms / 1e3), "unit": "tuples/s", "n_gpus": G,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (counter-based FK generator on device, seed 0)",
+            "config": {"workload": f"{args.config} per GPU: |R|={n_r:,} |S|={n_s:,} FK join over {G} GPUs",
+                       "algorithm": "p-mpsm", "threads": G, "parallelism": f"dp{G} (range-partitioned R, "
+                       "NCCL all-to-all, NVLink peer reads of S runs)",
+                       "l2": "inputs >> L2 (no flush needed)"},
+            "result": {"match_count": res.match_count, "aggregate_max": res.aggregate_max,
+                       "checksum": hex(res.checksum), "fk_count_ok": ok},
+            "gpu_launches": launches, "clocks": clk, "e2e": None, "roofline": None, "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()

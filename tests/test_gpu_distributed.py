@@ -1,0 +1,66 @@
+"""The distributed engine's CUDA backend on one GPU (NCCL, world size 1).
+
+With one rank the protocol still runs every device step (sort, histogram,
+partition scatter into send segments, NCCL all-to-all, join, fold)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import torch.distributed as dist  # noqa: E402
+
+from paper_1207_0145_b200.core import JoinConfig, KeyDomain, Relation  # noqa: E402
+from paper_1207_0145_b200.distributed import run_join_distributed  # noqa: E402
+import paper_1207_0145_b200 as P  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def nccl_group():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    yield
+    dist.destroy_process_group()
+
+
+def test_world_of_one_matches_golden(golden, nccl_group):
+    g = golden["config1"]
+    r, s, dom = P.gen_fk(g["n_r"], g["n_s"], g["seed"])
+    res = run_join_distributed(r, s, JoinConfig(threads=1, key_domain=dom))
+    assert (res.match_count, res.aggregate_max, res.checksum) == (g["match_count"], g["aggregate_max"],
+                                                                 g["checksum"])
+    # pairs layout and a skewed domain
+    from paper_1207_0145_b200.distributed import CudaBackend
+    from oracle import oracle as orc
+
+    d2 = KeyDomain(1, 1 << 32)
+    r2, s2 = P.gen_negcorr(200_000, 800_000, d2)
+    want = orc.join(r2.keys, r2.payloads, s2.keys, s2.payloads, threads=1, lower=1, upper=1 << 32)
+    for packed in (True, False):
+        res = run_join_distributed(r2, s2, JoinConfig(key_domain=d2), backend=CudaBackend(packed=packed))
+        assert (res.match_count, res.aggregate_max, res.checksum) == (want.match_count, want.aggregate_max,
+                                                                     want.checksum)
+
+
+def test_device_fk_shard_join(nccl_group):
+    from paper_1207_0145_b200.distributed import fk_shard_device
+
+    n_r, n_s = 2_000_000, 8_000_000
+    r, s = fk_shard_device(n_r, n_s, 0, 1, 0, torch.device("cuda", 0))
+    res = run_join_distributed(r, s, JoinConfig(key_domain=KeyDomain(1, n_r + 1)))
+    assert res.match_count == n_s
+    rk, rp = r.keys.cpu().numpy(), r.payloads.cpu().numpy()
+    sk, sp = s.keys.cpu().numpy(), s.payloads.cpu().numpy()
+    from oracle import oracle as orc
+
+    assert (res.match_count, res.aggregate_max, res.checksum) == orc.fk_gather(rk, rp, sk, sp, 1)
