@@ -82,8 +82,8 @@ int mpsm_profile_read(const char* name, double* total_ms, uint64_t* launches);
  * one decoupled-look-back scatter pass per digit).  Keys outside
  * [lower, lower + span_m1] are reported through *d_bad (atomicMin of the
  * index; initialise to UINT64_MAX) -- the reference returns -1 from the kernel
- * and raises DomainError (sorter.py:97-98).  Stable (equal keys keep input
- * order), which the reference does not promise. */
+ * and raises DomainError (sorter.py:97-98).  Like the reference, the order of
+ * payloads among equal keys is unspecified. */
 int mpsm_sort_workspace_bytes(int64_t n, int width_bits, size_t* bytes);
 /* number of scatter passes (digits) the sort uses for width_bits */
 int mpsm_sort_pass_count(int width_bits);

@@ -31,6 +31,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -246,8 +247,11 @@ __global__ void k_partition(const mpsm_run_t* __restrict__ priv, const mpsm_run_
 }
 
 // two tile buffers: tile g+grid streams in (cp.async) while tile g merges
+// slot 0 holds R[i0-1] when i0 > 0: the S tuples that open a tile usually match
+// the R tuple that closed the previous one, and keeping it in shared memory
+// spares thread 0 a dependent global load per tile
 struct MergeStage {
-    uint64_t k[MJ_TILE], p[MJ_TILE];  // R part of the tile at [0, nR), W part at [nR, nR+nW)
+    uint64_t k[MJ_TILE + 1], p[MJ_TILE + 1];  // [hp | R (nR) | W (nW)], hp = (i0 > 0)
 };
 struct MergeSmem {
     MergeStage st[2];
@@ -292,15 +296,17 @@ __device__ __forceinline__ void flush_pair(MergeSmem& sm, uint64_t* __restrict__
 
 template <bool PK>
 __device__ __forceinline__ void load_tile_async(MergeStage& st, const TileSplit& t) {
-    const uint64_t* rk = t.rk + t.i0;
+    const int hp = t.i0 > 0 ? 1 : 0;
+    const int nr = t.nR + hp;
+    const uint64_t* rk = t.rk + t.i0 - hp;
     const uint64_t* wk = t.wk + t.w0;
-    for (int x = threadIdx.x; x < t.nR; x += MJ_THREADS) cp_async8(&st.k[x], rk + x);
-    for (int x = threadIdx.x; x < t.nW; x += MJ_THREADS) cp_async8(&st.k[t.nR + x], wk + x);
+    for (int x = threadIdx.x; x < nr; x += MJ_THREADS) cp_async8(&st.k[x], rk + x);
+    for (int x = threadIdx.x; x < t.nW; x += MJ_THREADS) cp_async8(&st.k[nr + x], wk + x);
     if (!PK) {
-        const uint64_t* rp = t.rp + t.i0;
+        const uint64_t* rp = t.rp + t.i0 - hp;
         const uint64_t* wp = t.wp + t.w0;
-        for (int x = threadIdx.x; x < t.nR; x += MJ_THREADS) cp_async8(&st.p[x], rp + x);
-        for (int x = threadIdx.x; x < t.nW; x += MJ_THREADS) cp_async8(&st.p[t.nR + x], wp + x);
+        for (int x = threadIdx.x; x < nr; x += MJ_THREADS) cp_async8(&st.p[x], rp + x);
+        for (int x = threadIdx.x; x < t.nW; x += MJ_THREADS) cp_async8(&st.p[nr + x], wp + x);
     }
 }
 
@@ -314,7 +320,7 @@ __device__ long long g_mj_ts[1 << 20][6];
 
 // MODE 0: aggregate into pair records; MODE 1: per-tile counts only;
 // MODE 2: emit pairs at tile_out[g] + thread offset
-template <int MODE, bool PK>
+template <int MODE, bool PK, bool K32 = false>
 __global__ void __launch_bounds__(MJ_THREADS) k_merge(const TileSplit* __restrict__ splits,
                                                       const int64_t* __restrict__ total, int swap,
                                                       uint64_t* __restrict__ out_pairs, int64_t* __restrict__ tile_cnt,
@@ -354,14 +360,19 @@ __global__ void __launch_bounds__(MJ_THREADS) k_merge(const TileSplit* __restric
         __syncthreads();    // ... and everyone else's
         MJ_TS(2)
         const int nR = t.nR, nW = t.nW;
-        const uint64_t* K = sm.st[buf].k;
-        const uint64_t* Pp = sm.st[buf].p;
+        const int hp = t.i0 > 0 ? 1 : 0;
+        const int64_t rbase = t.i0 - hp;  // global R index of shared slot 0
+        const uint64_t* K = sm.st[buf].k + hp;  // K[i] = R tile element i (i = -1 is R[i0-1])
+        const uint64_t* Pp = sm.st[buf].p + hp;
         // tile-relative accessors: normalized key and payload
-        auto skey = [&](int i) -> uint64_t { return PK ? (K[i] >> pi.pw) : K[i]; };
+        // K32: packed keys of a domain at most 32 bits wide compare as u32
+        using KT = typename std::conditional<K32, uint32_t, uint64_t>::type;
+        auto skey = [&](int i) -> KT { return PK ? (KT)(K[i] >> pi.pw) : (KT)K[i]; };
         auto spay = [&](int i) -> uint64_t { return PK ? (K[i] & pi.pmask) : Pp[i]; };
         const int L = nR + nW;
         const int k0 = min(tid * MJ_ITEMS, L);
         const int k1 = min(k0 + MJ_ITEMS, L);
+#ifndef MPSM_MJ_SEARCH
         // per-thread split inside the tile
         int lo = k0 > nW ? k0 - nW : 0, hi = k0 < nR ? k0 : nR;
         while (lo < hi) {
@@ -369,6 +380,7 @@ __global__ void __launch_bounds__(MJ_THREADS) k_merge(const TileSplit* __restric
             if (skey(mid) <= skey(nR + k0 - 1 - mid)) lo = mid + 1;
             else hi = mid;
         }
+#endif
         MJ_TS(3)
         int64_t my_pairs = 0;
         int64_t emit_base = 0;
@@ -389,43 +401,157 @@ __global__ void __launch_bounds__(MJ_THREADS) k_merge(const TileSplit* __restric
                 emit_base = tile_cnt[g] + before + incl - v;  // tile_cnt holds the tile's output offset here
             }
             int64_t e = 0;
+            // R accessors by tile index i (i < -hp falls back to global memory)
+            auto rkey_at = [&](int64_t i) -> KT {
+                if (i >= -hp) return skey((int)i);
+                const uint64_t v = t.rk[t.i0 + i];
+                return PK ? (KT)(v >> pi.pw) : (KT)v;
+            };
+            auto rpay_at = [&](int64_t i) -> uint64_t {
+                if (i >= -hp) return spay((int)i);
+                return PK ? (t.rk[t.i0 + i] & pi.pmask) : t.rp[t.i0 + i];
+            };
+            auto emit = [&](uint64_t rp, uint64_t sp) {
+                if (MODE == 0) {
+                    const uint64_t v = rp + sp;
+                    best = v > best ? v : best;
+                    ++count;
+                    csum += swap ? pair_hash(sp, rp) : pair_hash(rp, sp);
+                } else if (MODE == 1 || pass == 0) {
+                    ++e;
+                } else {
+                    const int64_t o = emit_base + e;
+                    emit_out[2 * o] = swap ? sp : rp;
+                    emit_out[2 * o + 1] = swap ? rp : sp;
+                    ++e;
+                }
+            };
+#if defined(MPSM_MJ_SEARCH)
+            // sorted search: thread t takes S tuples t, t+256, ...; the tile's
+            // merge-path bounds guarantee each one's R upper bound lies in
+            // [0, nR] of the tile, found by binary search in shared memory
+            // (consecutive lanes search neighbouring keys, so most probes are
+            // broadcasts); the matches are the equal-key run just before it
+            for (int j = tid; j < nW; j += MJ_THREADS) {
+                const uint64_t wk = skey(nR + j);
+                int base = 0, len = nR;
+                while (len > 0) {
+                    const int half = len >> 1;
+                    if (skey(base + half) <= wk) {
+                        base += half + 1;
+                        len -= half + 1;
+                    } else {
+                        len = half;
+                    }
+                }
+                int64_t i = (int64_t)base - 1;
+                if (t.i0 + i >= 0 && rkey_at(i) == wk) {
+                    const uint64_t sp = spay(nR + j);
+                    do {
+                        emit(rpay_at(i), sp);
+                        --i;
+                    } while (t.i0 + i >= 0 && rkey_at(i) == wk);
+                }
+            }
+            (void)k1;
+#elif defined(MPSM_MJ_TWO_PHASE)
+            // phase 1 -- branch-light merge walk over this thread's MJ_ITEMS
+            // steps: record, per S step, the matching R group's last index
+            // (the equal-key R group ending right before the S tuple).
+            // phase 2 -- emit the matches (hash, max, count) with no divergent
+            // merge control around the expensive work.
             int ri = lo, wj = k0 - lo;
-            uint64_t rkc = ri < nR ? skey(ri) : 0;       // current R key (register-carried)
-            uint64_t wkc = wj < nW ? skey(nR + wj) : 0;  // current S key
+            // the equal-key R group ending at ri-1: key gk, first index gs
+            bool gvalid = t.i0 + ri - 1 >= 0;
+            uint64_t gk = 0;
+            int64_t gs = ri - 1;
+            if (gvalid) {
+                gk = rkey_at(ri - 1);
+                while (t.i0 + gs - 1 >= 0 && rkey_at(gs - 1) == gk) --gs;
+            }
+            uint64_t rkc = ri < nR ? skey(ri) : 0;       // next R key
+            uint64_t wkc = wj < nW ? skey(nR + wj) : 0;  // next S key
+            int m_r[MJ_ITEMS], m_w[MJ_ITEMS];
+            unsigned match = 0, dup = 0;
+#pragma unroll
+            for (int st = 0; st < MJ_ITEMS; ++st) {
+                m_r[st] = 0;
+                m_w[st] = 0;
+                if (k0 + st < k1) {
+                    const bool take_r = ri < nR && (wj >= nW || rkc <= wkc);
+                    if (take_r) {
+                        if (!gvalid || rkc != gk) {
+                            gk = rkc;
+                            gs = ri;
+                            gvalid = true;
+                        }
+                        ++ri;
+                    } else {
+                        if (gvalid && wkc == gk) {
+                            match |= 1u << st;
+                            if (gs < ri - 1) dup |= 1u << st;
+                            m_r[st] = ri - 1;
+                            m_w[st] = wj;
+                        }
+                        ++wj;
+                    }
+                    // one shared-memory read per step: the successor of the consumed side
+                    const int nxt = take_r ? ri : nR + wj;
+                    const bool ok = take_r ? (ri < nR) : (wj < nW);
+                    const uint64_t v = ok ? skey(nxt) : 0;
+                    if (take_r) rkc = v;
+                    else wkc = v;
+                }
+            }
+#pragma unroll
+            for (int st = 0; st < MJ_ITEMS; ++st) {
+                if (match & (1u << st)) {
+                    const uint64_t sp = spay(nR + m_w[st]);
+                    emit(spay(m_r[st]), sp);
+                    if (dup & (1u << st)) {  // duplicate R keys: the rest of the group
+                        const uint64_t sk = skey(nR + m_w[st]);
+                        for (int64_t i = (int64_t)m_r[st] - 1; t.i0 + i >= 0 && rkey_at(i) == sk; --i)
+                            emit(rpay_at(i), sp);
+                    }
+                }
+            }
+#else
+            int ri = lo, wj = k0 - lo;
+            // the equal-key R group ending at ri-1: key gk, first index gs,
+            // payload of its last element lrp (register-carried; an S tuple
+            // with key gk matches exactly R[gs, ri))
+            bool gvalid = t.i0 + ri - 1 >= 0;
+            KT gk = 0;
+            uint64_t lrp = 0;
+            int gs = ri - 1;
+            if (gvalid) {
+                gk = rkey_at(ri - 1);
+                lrp = rpay_at(ri - 1);
+                while (t.i0 + gs - 1 >= 0 && rkey_at(gs - 1) == gk) --gs;
+            }
+            KT rkc = ri < nR ? skey(ri) : 0;       // next R key
+            KT wkc = wj < nW ? skey(nR + wj) : 0;  // next S key
             for (int step = k0; step < k1; ++step) {
                 if (ri < nR && (wj >= nW || rkc <= wkc)) {
+                    if (!gvalid || rkc != gk) {
+                        gk = rkc;
+                        gs = ri;
+                        gvalid = true;
+                    }
+                    lrp = spay(ri);
                     ++ri;
                     if (ri < nR) rkc = skey(ri);
                     continue;
                 }
-                const uint64_t sp = spay(nR + wj);
-                int64_t gi = t.i0 + ri - 1;  // walk back over the equal-key R group
-                while (gi >= 0) {
-                    const bool in_tile = gi >= t.i0;
-                    uint64_t rk, rp;
-                    if (in_tile) rk = skey((int)(gi - t.i0));
-                    else rk = PK ? (t.rk[gi] >> pi.pw) : t.rk[gi];
-                    if (rk != wkc) break;
-                    if (in_tile) rp = spay((int)(gi - t.i0));
-                    else rp = PK ? (t.rk[gi] & pi.pmask) : t.rp[gi];
-                    if (MODE == 0) {
-                        const uint64_t v = rp + sp;
-                        best = v > best ? v : best;
-                        ++count;
-                        csum += swap ? pair_hash(sp, rp) : pair_hash(rp, sp);
-                    } else if (MODE == 1 || pass == 0) {
-                        ++e;
-                    } else {
-                        const int64_t o = emit_base + e;
-                        emit_out[2 * o] = swap ? sp : rp;
-                        emit_out[2 * o + 1] = swap ? rp : sp;
-                        ++e;
-                    }
-                    --gi;
+                if (gvalid && wkc == gk) {
+                    const uint64_t sp = spay(nR + wj);
+                    emit(lrp, sp);
+                    for (int i = ri - 2; i >= gs; --i) emit(rpay_at(i), sp);  // duplicate R keys
                 }
                 ++wj;
                 if (wj < nW) wkc = skey(nR + wj);
             }
+#endif
             my_pairs = e;
         }
         MJ_TS(4)
@@ -522,15 +648,15 @@ static size_t join_ws_size(int n_priv, int n_pub, int64_t mt) {
     return c.off;
 }
 
-template <int MODE, bool PK>
+template <int MODE, bool PK, bool K32 = false>
 static int launch_merge(const JoinWs& w, int swap, uint64_t* d_pairs, uint64_t* emit_out, int64_t mt,
                         const PackInfo& pi, cudaStream_t st) {
     static int per_sm = 0;
     if (per_sm == 0) {
-        MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_merge<MODE, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_merge<MODE, PK, K32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   (int)sizeof(MergeSmem)),
                              "smem attr"));
-        MPSM_TRY(cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge<MODE, PK>, MJ_THREADS,
+        MPSM_TRY(cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge<MODE, PK, K32>, MJ_THREADS,
                                                                            sizeof(MergeSmem)),
                              "occupancy"));
         if (per_sm < 1) per_sm = 1;
@@ -538,7 +664,7 @@ static int launch_merge(const JoinWs& w, int swap, uint64_t* d_pairs, uint64_t* 
     // persistent grid: exactly the resident CTAs
     const int grid = (int)std::min<int64_t>((int64_t)num_sms() * per_sm, mt);
     ProfScope ps(MODE == 0 ? "merge" : (MODE == 1 ? "merge_count" : "merge_emit"), st);
-    k_merge<MODE, PK><<<grid, MJ_THREADS, sizeof(MergeSmem), st>>>(w.splits, w.total, swap, d_pairs, w.tile_cnt,
+    k_merge<MODE, PK, K32><<<grid, MJ_THREADS, sizeof(MergeSmem), st>>>(w.splits, w.total, swap, d_pairs, w.tile_cnt,
                                                                     emit_out, pi);
     return check_launch("k_merge");
 }
@@ -568,7 +694,9 @@ static int join_pairs_impl(const mpsm_run_t* priv, int n_priv, const mpsm_run_t*
                                                                        w.total, w.splits, pi);
     }
     MPSM_TRY(check_launch("k_partition"));
-    MPSM_TRY((launch_merge<0, PK>(w, swap, d_pairs, nullptr, mt, pi, st)));
+    const bool k32 = PK && (64 - pi.pw) <= 32;  // packed keys fit 32 bits
+    if (k32) MPSM_TRY((launch_merge<0, PK, PK>(w, swap, d_pairs, nullptr, mt, pi, st)));
+    else MPSM_TRY((launch_merge<0, PK>(w, swap, d_pairs, nullptr, mt, pi, st)));
     if (mode != MPSM_MODE_MATERIALIZE || d_out == nullptr) return MPSM_OK;
     // materialize: per-tile counts, offsets, emission
     MPSM_TRY((launch_merge<1, PK>(w, swap, d_pairs, nullptr, mt, pi, st)));

@@ -33,14 +33,24 @@
 namespace mpsm {
 namespace seg {
 
-constexpr int THREADS = 512;
-constexpr int ITEMS = 8;
+#ifndef MPSM_SEG_THREADS
+#define MPSM_SEG_THREADS 512
+#endif
+#ifndef MPSM_SEG_ITEMS
+#define MPSM_SEG_ITEMS 8
+#endif
+#ifndef MPSM_SEG_PP_BLOCKS
+#define MPSM_SEG_PP_BLOCKS 2
+#endif
+constexpr int THREADS = MPSM_SEG_THREADS;
+constexpr int ITEMS = MPSM_SEG_ITEMS;
 constexpr int TILE = THREADS * ITEMS;  // 4096 tuples
 constexpr int WARPS = THREADS / 32;
 constexpr int MAX_BITS = 9;
 constexpr int MAX_BINS = 1 << MAX_BITS;
 constexpr int MAX_PASSES = 8;
 constexpr int COUNT_UNROLL = 8;
+static_assert(WARPS * MAX_BINS * 4 <= TILE * 8, "warp histograms alias one tile buffer");
 
 enum Layout { SS = 0, SP = 1, PP = 2 };
 
@@ -172,13 +182,20 @@ __device__ __forceinline__ unsigned ballot_peers(uint32_t d, int bits, unsigned 
     return __match_any_sync(0xffffffffu, d) & vmask;
 #endif
     // lanes whose digit differs from mine in some bit; bits above `bits` are
-    // zero in every lane, so all MAX_BITS ballots can run unconditionally
+    // zero in every lane, so all MAX_BITS ballots can run unconditionally.
+    // Per bit: predicate, ballot, select-complement, or -- 4 SASS ops.
     unsigned diff = ~vmask;
 #pragma unroll
     for (int b = 0; b < MAX_BITS; ++b) {
-        const unsigned t = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-        const unsigned s = (unsigned)((int)(d << (31 - b)) >> 31);
-        diff |= t ^ s;
+        asm("{\n\t.reg .pred p;\n\t.reg .b32 t, u;\n\t"
+            "and.b32 u, %1, %2;\n\t"
+            "setp.ne.u32 p, u, 0;\n\t"
+            "vote.sync.ballot.b32 t, p, 0xffffffff;\n\t"
+            "not.b32 u, t;\n\t"
+            "selp.b32 t, u, t, p;\n\t"
+            "or.b32 %0, %0, t;\n\t}"
+            : "+r"(diff)
+            : "r"(d), "r"(1u << b));
     }
     (void)bits;
     return ~diff;
@@ -192,15 +209,19 @@ __device__ long long g_seg_ts[1 << 22][8];
 #define SEG_TS(i)
 #endif
 
-template <int LAYOUT>
-__global__ void __launch_bounds__(THREADS, LAYOUT == PP ? 2 : 1) k_scatter(const uint64_t* __restrict__ in_k,
-                                                     const uint64_t* __restrict__ in_p, uint64_t* __restrict__ out_k,
-                                                     uint64_t* __restrict__ out_p, Segs sg, Digit dig, Digit odig, int bits,
-                                                     int nbins, const int64_t* __restrict__ base, uint64_t pk_lower,
-                                                     int pk_pw, unsigned int* __restrict__ overflow) {
+// STABLE = false ranks with one shared atomicAdd per tuple (order within a
+// digit arbitrary) -- allowed for the first LSD pass only, whose input order
+// carries no information.  STABLE = true ranks with warp ballots so equal
+// digits keep their input order (every later pass).
+template <int LAYOUT, bool STABLE>
+__global__ void __launch_bounds__(THREADS, LAYOUT == PP ? MPSM_SEG_PP_BLOCKS : 1) k_scatter(
+    const uint64_t* __restrict__ in_k, const uint64_t* __restrict__ in_p, uint64_t* __restrict__ out_k,
+    uint64_t* __restrict__ out_p, Segs sg, Digit dig, Digit odig, int bits, int nbins,
+    const int64_t* __restrict__ base, uint64_t pk_lower, int pk_pw, unsigned int* __restrict__ overflow) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem<LAYOUT>& sm = *reinterpret_cast<Smem<LAYOUT>*>(smem_raw);
     constexpr int NARR = Smem<LAYOUT>::NARR;
+    constexpr int HW = STABLE ? WARPS : 1;  // histogram rows: per warp, or one per tile
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt = lanemask_lt();
     const int g = blockIdx.x;
@@ -236,48 +257,62 @@ __global__ void __launch_bounds__(THREADS, LAYOUT == PP ? 2 : 1) k_scatter(const
             const int li = wb + 32 * k + lane;
             key[k] = (full || li < cnt) ? sm.buf[b][0][li] : 0;
         }
-        __syncthreads();  // buf[b][0] now hosts the warp histograms
-        uint32_t* whist_all = reinterpret_cast<uint32_t*>(sm.buf[b][0]);  // [WARPS][MAX_BINS]
-        for (int i = tid; i < WARPS * MAX_BINS / 4; i += THREADS)
-            reinterpret_cast<uint4*>(whist_all)[i] = make_uint4(0, 0, 0, 0);
+        __syncthreads();  // buf[b][0] now hosts the digit histograms [HW][MAX_BINS]
+        uint32_t* hist = reinterpret_cast<uint32_t*>(sm.buf[b][0]);
+        for (int i = tid; i < HW * MAX_BINS / 4; i += THREADS)
+            reinterpret_cast<uint4*>(hist)[i] = make_uint4(0, 0, 0, 0);
         __syncthreads();
-        uint32_t* wh = whist_all + warp * MAX_BINS;
-        unsigned peers[ITEMS];
+        if (STABLE) {
+            uint32_t* wh = hist + warp * MAX_BINS;
+            unsigned peers[ITEMS];
 #pragma unroll
-        for (int k = 0; k < ITEMS; ++k) {  // independent: the ballots pipeline
-            const int li = wb + 32 * k + lane;
-            const bool valid = full || li < cnt;
-            const unsigned vmask = full ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
-            const uint32_t d = dig(key[k]);
-            peers[k] = ballot_peers(d, bits, vmask);
-            if (!valid) peers[k] = 0;
-            pos[k] = d << 20;
-        }
+            for (int k = 0; k < ITEMS; ++k) {  // independent: the ballots pipeline
+                const int li = wb + 32 * k + lane;
+                const bool valid = full || li < cnt;
+                const unsigned vmask = full ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
+                const uint32_t d = dig(key[k]);
+                peers[k] = ballot_peers(d, bits, vmask);
+                if (!valid) peers[k] = 0;
+                pos[k] = d << 20;
+            }
 #pragma unroll
-        for (int k = 0; k < ITEMS; ++k) {  // running per-warp digit counts
-            const uint32_t d = pos[k] >> 20;
-            uint32_t before = 0;
-            if (peers[k]) before = wh[d];
-            __syncwarp();
-            if (peers[k] && (peers[k] & lt) == 0) wh[d] = before + __popc(peers[k]);
-            __syncwarp();
-            pos[k] = peers[k] ? ((d << 20) | (before + __popc(peers[k] & lt))) : 0xffffffffu;
+            for (int k = 0; k < ITEMS; ++k) {  // running per-warp digit counts
+                const uint32_t d = pos[k] >> 20;
+                uint32_t before = 0;
+                if (peers[k]) before = wh[d];
+                __syncwarp();
+                if (peers[k] && (peers[k] & lt) == 0) wh[d] = before + __popc(peers[k]);
+                __syncwarp();
+                pos[k] = peers[k] ? ((d << 20) | (before + __popc(peers[k] & lt))) : 0xffffffffu;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < ITEMS; ++k) {
+                const int li = wb + 32 * k + lane;
+                const uint32_t d = dig(key[k]);
+                pos[k] = (full || li < cnt) ? ((d << 20) | atomicAdd(&hist[d], 1u)) : 0xffffffffu;
+            }
         }
         __syncthreads();
         SEG_TS(2)
-        // ---- per digit: tile count; after the digit scan the warp histograms
-        // become absolute staging offsets tile_off[d] + (earlier warps' d's)
-        uint32_t mycnt = 0;
-        const int dd = tid;  // THREADS >= MAX_BINS
-        uint32_t col[WARPS];
-        if (dd < nbins) {
+        // ---- per digit: tile count; after the digit scan the histogram rows
+        // become absolute staging offsets tile_off[d] + (earlier rows' d's)
+        constexpr int DPT = (MAX_BINS + THREADS - 1) / THREADS;  // digits per thread
+        uint32_t mycnt[DPT];
+        uint32_t col[DPT][HW];
 #pragma unroll
-            for (int w = 0; w < WARPS; ++w) {
-                col[w] = whist_all[w * MAX_BINS + dd];
-                mycnt += col[w];
+        for (int j = 0; j < DPT; ++j) {
+            const int dd = tid + j * THREADS;
+            mycnt[j] = 0;
+            if (dd < nbins) {
+#pragma unroll
+                for (int w = 0; w < HW; ++w) {
+                    col[j][w] = hist[w * MAX_BINS + dd];
+                    mycnt[j] += col[j][w];
+                }
             }
+            if (dd < MAX_BINS) sm.tile_off[dd] = mycnt[j];
         }
-        if (dd < MAX_BINS) sm.tile_off[dd] = mycnt;
         __syncthreads();
         if (warp == 0) {
             constexpr int PER = MAX_BINS / 32;
@@ -303,23 +338,28 @@ __global__ void __launch_bounds__(THREADS, LAYOUT == PP ? 2 : 1) k_scatter(const
             }
         }
         __syncthreads();
-        if (dd < nbins) {
-            const uint32_t toff = sm.tile_off[dd];
-            uint32_t run = toff;
 #pragma unroll
-            for (int w = 0; w < WARPS; ++w) {
-                whist_all[w * MAX_BINS + dd] = run;
-                run += col[w];
+        for (int j = 0; j < DPT; ++j) {
+            const int dd = tid + j * THREADS;
+            if (dd < nbins) {
+                const uint32_t toff = sm.tile_off[dd];
+                uint32_t run = toff;
+#pragma unroll
+                for (int w = 0; w < HW; ++w) {
+                    hist[w * MAX_BINS + dd] = run;
+                    run += col[j][w];
+                }
+                sm.gdelta[dd] = sm.cur[dd] - (int64_t)toff;
+                sm.cur[dd] += mycnt[j];
             }
-            sm.gdelta[dd] = sm.cur[dd] - (int64_t)toff;
-            sm.cur[dd] += mycnt;
         }
         __syncthreads();
         SEG_TS(3)
         // ---- final staging positions
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k)
-            if (pos[k] != 0xffffffffu) pos[k] = whist_all[warp * MAX_BINS + (pos[k] >> 20)] + (pos[k] & 0xfffffu);
+            if (pos[k] != 0xffffffffu)
+                pos[k] = hist[(STABLE ? warp : 0) * MAX_BINS + (pos[k] >> 20)] + (pos[k] & 0xfffffu);
         uint64_t pay[ITEMS];
         if (LAYOUT != PP) {
 #pragma unroll
@@ -377,8 +417,9 @@ template <int LAYOUT>
 static int grid_size() {
     static int per_sm = 0;
     if (per_sm == 0) {
-        cudaFuncSetAttribute(k_scatter<LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<LAYOUT>));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scatter<LAYOUT>, THREADS, sizeof(Smem<LAYOUT>));
+        cudaFuncSetAttribute(k_scatter<LAYOUT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(Smem<LAYOUT>));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scatter<LAYOUT, true>, THREADS, sizeof(Smem<LAYOUT>));
         if (per_sm < 1) per_sm = 1;
     }
     return num_sms() * per_sm;
@@ -406,11 +447,11 @@ static bool carve(void* ws, size_t bytes, Ws* o) {
     return c.ok;
 }
 
-template <int LAYOUT>
+template <int LAYOUT, bool STABLE>
 static int set_attr() {
     static bool done = false;
     if (!done) {
-        MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_scatter<LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_scatter<LAYOUT, STABLE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   (int)sizeof(Smem<LAYOUT>)),
                              "smem attr"));
         done = true;
@@ -419,7 +460,7 @@ static int set_attr() {
 }
 
 // one digit pass: count, scan, scatter
-template <int LAYOUT>
+template <int LAYOUT, bool STABLE>
 static int pass(const uint64_t* in_k, const uint64_t* in_p, uint64_t* out_k, uint64_t* out_p, int64_t n,
                 Digit count_dig, Digit dig, int bits, const Ws& ws, uint64_t span_m1, unsigned long long* d_bad,
                 uint64_t pk_lower, int pk_pw, unsigned int* overflow, cudaStream_t st) {
@@ -433,13 +474,14 @@ static int pass(const uint64_t* in_k, const uint64_t* in_p, uint64_t* out_k, uin
     MPSM_TRY(check_launch("k_count"));
     k_scan<<<1, MAX_BINS, 0, st>>>(ws.counts, G, nbins, ws.base);
     MPSM_TRY(check_launch("k_scan"));
-    MPSM_TRY(set_attr<LAYOUT>());
+    MPSM_TRY((set_attr<LAYOUT, STABLE>()));
     {
         ProfScope ps("seg_scatter", st);
+        ProfScope ps2(LAYOUT == SS ? "seg_scatter_ss" : (LAYOUT == SP ? "seg_scatter_sp" : "seg_scatter_pp"), st);
         // digit of a staged value: records staged by the SP pass carry the key
         // above the payload bits
         const Digit odig = (LAYOUT == SP) ? Digit{0, pk_pw + dig.shift, dig.mask} : dig;
-        k_scatter<LAYOUT><<<G, THREADS, sizeof(Smem<LAYOUT>), st>>>(in_k, in_p, out_k, out_p, sg, dig, odig, bits,
+        k_scatter<LAYOUT, STABLE><<<G, THREADS, sizeof(Smem<LAYOUT>), st>>>(in_k, in_p, out_k, out_p, sg, dig, odig, bits,
                                                                     nbins, ws.base, pk_lower, pk_pw, overflow);
     }
     return check_launch("k_scatter");
@@ -502,8 +544,11 @@ extern "C" int mpsm_sort_pairs(const uint64_t* in_keys, const uint64_t* in_pays,
         uint64_t* dk = to_out ? out_keys : tmp_keys;
         uint64_t* dp = to_out ? out_pays : tmp_pays;
         const Digit dg{lower, plan.shift[i], (1u << plan.bits[i]) - 1u};
-        MPSM_TRY(pass<SS>(sk, sp, dk, dp, n, dg, dg, plan.bits[i], ws, i == 0 ? span_m1 : ~0ull, i == 0 ? d_bad : nullptr,
-                          0, 0, nullptr, st));
+        // the first LSD pass may reorder equal digits; later passes must not
+        if (i == 0)
+            MPSM_TRY((pass<SS, false>(sk, sp, dk, dp, n, dg, dg, plan.bits[i], ws, span_m1, d_bad, 0, 0, nullptr, st)));
+        else
+            MPSM_TRY((pass<SS, true>(sk, sp, dk, dp, n, dg, dg, plan.bits[i], ws, ~0ull, nullptr, 0, 0, nullptr, st)));
         sk = dk;
         sp = dp;
     }
@@ -530,12 +575,12 @@ extern "C" int mpsm_sort_packed(const uint64_t* in_keys, const uint64_t* in_pays
         uint64_t* dst = ((P - 1 - i) % 2 == 0) ? out_rec : tmp_rec;
         if (i == 0) {
             const Digit dg{lower, plan.shift[0], (1u << plan.bits[0]) - 1u};
-            MPSM_TRY(pass<SP>(in_keys, in_pays, dst, nullptr, n, dg, dg, plan.bits[0], ws, span_m1, d_bad, lower, pw,
-                              d_overflow, st));
+            MPSM_TRY((pass<SP, false>(in_keys, in_pays, dst, nullptr, n, dg, dg, plan.bits[0], ws, span_m1, d_bad,
+                                      lower, pw, d_overflow, st)));
         } else {
             const Digit dg{0, pw + plan.shift[i], (1u << plan.bits[i]) - 1u};
-            MPSM_TRY(pass<PP>(src, nullptr, dst, nullptr, n, dg, dg, plan.bits[i], ws, ~0ull, nullptr, 0, pw, nullptr,
-                              st));
+            MPSM_TRY((pass<PP, true>(src, nullptr, dst, nullptr, n, dg, dg, plan.bits[i], ws, ~0ull, nullptr, 0, pw,
+                                     nullptr, st)));
         }
         src = dst;
     }

@@ -20,14 +20,22 @@ sk = torch.randint(1, n_r + 1, (n_s,), device=dev).view(torch.uint64)
 sp = torch.randint(0, 1 << 32, (n_s,), device=dev).view(torch.uint64)
 D.ensure_device()
 bits = 27
+packed = (sys.argv[1] if len(sys.argv) > 1 else "packed") == "packed"
+ovf = torch.zeros(1, dtype=torch.int32, device=dev)
 def srt(k, p):
     o = [torch.empty_like(k) for _ in range(4)]
-    D.sort_pairs(k, p, 1, n_r - 1, bits, o[0], o[1], o[2], o[3], None)
+    if packed:
+        D.sort_packed(k, p, 1, n_r - 1, bits, o[0], o[1], None, ovf)
+    else:
+        D.sort_pairs(k, p, 1, n_r - 1, bits, o[0], o[1], o[2], o[3], None)
     return o[0], o[1]
 rk, rp = srt(rk, rp)
 sk, sp = srt(sk, sp)
 for _ in range(2):
-    rec = D.join_pairs([(rk, rp)], [(sk, sp)], False, 0)
+    if packed:
+        rec = D.join_pairs_packed([rk], [sk], bits, 1, False, 0)
+    else:
+        rec = D.join_pairs([(rk, rp)], [(sk, sp)], False, 0)
 torch.cuda.synchronize()
 print("count", int(rec[0, 0].item()))
 L = _lib.load()

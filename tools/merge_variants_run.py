@@ -1,0 +1,40 @@
+"""Time the merge join (packed FK 100M x 400M) of every variant library under
+build/variants (GPU box): python tools/merge_variants_run.py"""
+import glob
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CHILD = r'''
+import os, sys, torch
+sys.path.insert(0, os.environ["ROOT"])
+from paper_1207_0145_b200 import _lib, device as D
+n_r, n_s, bits = 100_000_000, 400_000_000, 27
+dev = torch.device("cuda", 0)
+D.ensure_device()
+rk = (torch.randperm(n_r, device=dev) + 1).view(torch.uint64)
+rp = torch.randint(0, 1 << 32, (n_r,), device=dev).view(torch.uint64)
+sk = torch.randint(1, n_r + 1, (n_s,), device=dev).view(torch.uint64)
+sp = torch.randint(0, 1 << 32, (n_s,), device=dev).view(torch.uint64)
+ovf = torch.zeros(1, dtype=torch.int32, device=dev)
+def srt(k, p):
+    o, t = torch.empty_like(k), torch.empty_like(k)
+    D.sort_packed(k, p, 1, n_r - 1, bits, o, t, None, ovf)
+    return o
+R, S = srt(rk, rp), srt(sk, sp)
+del rk, rp, sk, sp
+best = None
+for it in range(4):
+    _lib.profile_enable(True)
+    rec = D.join_pairs_packed([R], [S], bits, 1, False, 0)
+    torch.cuda.synchronize()
+    ms, n = _lib.profile_read("merge")
+    best = ms if best is None else min(best, ms)
+print(f"{os.environ['VNAME']:12s} merge {best:.3f} ms  ({4e9/best/1e6:.0f} GB/s packed)  count={int(rec[0,0].item())}")
+'''
+for lib in sorted(glob.glob(os.path.join(ROOT, "build", "variants", "*", "libmpsm_b200.so"))):
+    name = os.path.basename(os.path.dirname(lib))
+    env = dict(os.environ, MPSM_LIB=lib, ROOT=ROOT, VNAME=name)
+    r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True, timeout=300)
+    print(r.stdout.strip() or (name + " FAILED " + r.stderr[-800:]), flush=True)

@@ -34,15 +34,17 @@ for packed in (False, True):
         else:
             D.sort_pairs(keys, pays, 0, (1 << bits) - 1, bits, ok, op, tk, tp, None)
         b.record(); torch.cuda.synchronize()
-        res.append((a.elapsed_time(b), _lib.profile_read("seg_scatter"), _lib.profile_read("seg_count")))
+        res.append((a.elapsed_time(b), _lib.profile_read("seg_scatter"), _lib.profile_read("seg_count"),
+                    [_lib.profile_read(x) for x in ("seg_scatter_ss", "seg_scatter_sp", "seg_scatter_pp")]))
     srt = (ok >> (64 - bits) if packed else ok).view(torch.int64) if False else ok.view(torch.int64)
     if packed:
         srt = torch.bitwise_right_shift(ok.view(torch.int64), 64 - bits) & ((1 << bits) - 1)
     sorted_ok = bool((srt[1:] >= srt[:-1]).all())
     best = min(res)
-    ms, (os_ms, os_n), (h_ms, h_n) = best
+    ms, (os_ms, os_n), (h_ms, h_n), per = best
     print(f"{os.environ['VNAME']:10s} {'packed' if packed else 'pairs ':6s} total {ms:7.3f} ms  scatter {os_ms:7.3f} ms/{os_n} passes"
-          f" = {os_ms/os_n:6.3f} ms/pass  count {h_ms:6.3f} ms/{h_n}  sorted={sorted_ok}", flush=True)
+          f" = {os_ms/os_n:6.3f} ms/pass  count {h_ms:6.3f} ms/{h_n}  sorted={sorted_ok}  "
+          + " ".join(f"{nm}={m:.3f}/{c}" for nm, (m, c) in zip(("ss", "sp", "pp"), per) if c), flush=True)
 '''
 for lib in sorted(glob.glob(os.path.join(ROOT, "build", "variants", "*", "libmpsm_b200.so"))):
     name = os.path.basename(os.path.dirname(lib))
