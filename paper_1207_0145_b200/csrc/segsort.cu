@@ -49,8 +49,6 @@ constexpr int WARPS = THREADS / 32;
 constexpr int MAX_BITS = 9;
 constexpr int MAX_BINS = 1 << MAX_BITS;
 constexpr int MAX_PASSES = 8;
-constexpr int COUNT_UNROLL = 8;
-static_assert(WARPS * MAX_BINS * 4 <= TILE * 8, "warp histograms alias one tile buffer");
 
 enum Layout { SS = 0, SP = 1, PP = 2 };
 
@@ -91,33 +89,49 @@ struct Segs {
 };
 
 // ------------------------------------------------------------------ count
-// counts[g][d] for segment g; optional domain check (first pass)
+// counts[g][d] for segment g, and for every tile t of the segment the
+// segment-local exclusive prefix toffs[t][d] (digit d's tuples in earlier
+// tiles of the segment); optional domain check (first pass)
 __global__ void __launch_bounds__(THREADS) k_count(const uint64_t* __restrict__ in, Segs sg, Digit dig, int nbins,
-                                                   uint32_t* __restrict__ counts, uint64_t span_m1,
+                                                   uint32_t* __restrict__ counts, uint32_t* __restrict__ toffs,
+                                                   unsigned int* __restrict__ ticket, uint64_t span_m1,
                                                    unsigned long long* __restrict__ d_bad) {
-    __shared__ uint32_t h[MAX_BINS];
-    for (int i = threadIdx.x; i < MAX_BINS; i += THREADS) h[i] = 0;
+    __shared__ uint32_t h[2][MAX_BINS];  // tile k counts into h[k & 1]
+    const int tid = threadIdx.x;
+    h[0][tid] = 0;
+    h[1][tid] = 0;
+    if (blockIdx.x == 0 && tid == 0 && ticket) *ticket = 0;  // the scatter's tile dispenser
     __syncthreads();
     const int64_t b = sg.begin(blockIdx.x), e = sg.end(blockIdx.x);
-    constexpr int CHUNK = THREADS * COUNT_UNROLL;
-    for (int64_t base = b; base < e; base += CHUNK) {
-        uint64_t v[COUNT_UNROLL];
+    uint32_t run = 0;  // thread d: digit d's count in the tiles so far
+    uint64_t v[ITEMS], w[ITEMS];
+    auto load = [&](uint64_t* x, int64_t t0) {
 #pragma unroll
-        for (int u = 0; u < COUNT_UNROLL; ++u) {
-            const int64_t i = base + u * THREADS + threadIdx.x;
-            v[u] = i < e ? ld_stream(in + i) : 0;
+        for (int u = 0; u < ITEMS; ++u) {
+            const int64_t i = t0 + u * THREADS + tid;
+            x[u] = i < e ? ld_stream(in + i) : 0;
         }
+    };
+    if (b < e) load(v, b);
+    int k = 0;
+    for (int64_t t0 = b; t0 < e; t0 += TILE, k ^= 1) {
+        if (t0 + TILE < e) load(w, t0 + TILE);  // next tile in flight during this one
 #pragma unroll
-        for (int u = 0; u < COUNT_UNROLL; ++u) {
-            const int64_t i = base + u * THREADS + threadIdx.x;
+        for (int u = 0; u < ITEMS; ++u) {
+            const int64_t i = t0 + u * THREADS + tid;
             if (i < e) {
                 if (d_bad && v[u] - dig.lower > span_m1) atomicMin(d_bad, (unsigned long long)i);
-                atomicAdd(&h[dig(v[u])], 1u);
+                atomicAdd(&h[k][dig(v[u])], 1u);
             }
         }
+        __syncthreads();  // h[k] complete; the next tile counts into h[k ^ 1]
+        if (tid < nbins) toffs[(size_t)(t0 / TILE) * MAX_BINS + tid] = run;
+        run += h[k][tid];
+        h[k][tid] = 0;
+#pragma unroll
+        for (int u = 0; u < ITEMS; ++u) v[u] = w[u];
     }
-    __syncthreads();
-    for (int d = threadIdx.x; d < nbins; d += THREADS) counts[(size_t)blockIdx.x * nbins + d] = h[d];
+    if (tid < nbins) counts[(size_t)blockIdx.x * nbins + tid] = run;
 }
 
 // ------------------------------------------------------------------- scan
@@ -148,42 +162,28 @@ __global__ void __launch_bounds__(MAX_BINS) k_scan(const uint32_t* __restrict__ 
 }
 
 // ---------------------------------------------------------------- scatter
+// Shared memory of one scatter CTA.  The digit histogram of a tile keeps one
+// row per warp, two warps per 32-bit word (16-bit fields: a warp counts at
+// most 32 * ITEMS = 256 tuples per digit, a tile offset is < TILE).
 template <int LAYOUT>
 struct Smem {
     static constexpr int NARR = (LAYOUT == PP) ? 1 : 2;
-    uint64_t buf[2][NARR][TILE];  // double-buffered tile data; staging in place
-    uint32_t tile_off[MAX_BINS];
-    int64_t gdelta[MAX_BINS];
-    int64_t cur[MAX_BINS];  // running output cursor per digit of this segment
+    uint64_t buf[2][NARR][TILE + 2];     // double-buffered tile data (+1 slot of alignment shift); staging in place
+    uint32_t hist[WARPS / 2][MAX_BINS];  // [warp pair][digit]
+    int64_t gdelta[MAX_BINS];            // output index - staging index, per digit
+    uint32_t toffs[2][MAX_BINS];         // per buffer: the tile's segment-local digit prefixes
+    int64_t sbase[2][MAX_BINS];          // per buffer: its segment's digit bases
+    uint32_t wtot[WARPS];                // digit-scan carries
+    int64_t tile[2];                     // per buffer: tile index
+    uint64_t bar[2];                     // bulk-copy completion, per buffer
 };
+static_assert(THREADS == MAX_BINS, "the digit scan gives each thread one digit");
+static_assert(WARPS % 2 == 0 && WARPS <= 32 && 32 * ITEMS < 65536 && TILE < 65536, "16-bit histogram fields");
 
-__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp8(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
-}
-
-// async copy of cnt elements from g[0..cnt) into s[0..cnt)
-__device__ __forceinline__ void tile_copy(uint64_t* s, const uint64_t* g, int cnt, bool vec) {
-    if (vec) {  // g and s 16-B aligned; cnt may be odd only on the last tile
-        const int pairs = cnt >> 1;
-        for (int i = threadIdx.x; i < pairs; i += THREADS) cp16(s + 2 * i, g + 2 * i);
-        if ((cnt & 1) && threadIdx.x == 0) cp8(s + cnt - 1, g + cnt - 1);
-    } else {
-        for (int i = threadIdx.x; i < cnt; i += THREADS) cp8(s + i, g + i);
-    }
-}
-
-__device__ __forceinline__ unsigned ballot_peers(uint32_t d, int bits, unsigned vmask) {
-#ifdef MPSM_SEG_MATCH_ANY
-    return __match_any_sync(0xffffffffu, d) & vmask;
-#endif
-    // lanes whose digit differs from mine in some bit; bits above `bits` are
-    // zero in every lane, so all MAX_BITS ballots can run unconditionally.
-    // Per bit: predicate, ballot, select-complement, or -- 4 SASS ops.
+// lanes of the warp holding the same digit (fallback ranking: 9 ballots)
+__device__ __forceinline__ unsigned ballot_peers(uint32_t d, unsigned vmask) {
+    // lanes whose digit differs from mine in some bit; bits above a pass's
+    // width are zero in every lane, so all MAX_BITS ballots run unconditionally
     unsigned diff = ~vmask;
 #pragma unroll
     for (int b = 0; b < MAX_BITS; ++b) {
@@ -197,218 +197,283 @@ __device__ __forceinline__ unsigned ballot_peers(uint32_t d, int bits, unsigned 
             : "+r"(diff)
             : "r"(d), "r"(1u << b));
     }
-    (void)bits;
     return ~diff;
+}
+
+// element i of a tile of array g sits at s[off + i], off = (g / 8) & 1, so
+// that global and shared addresses agree mod 16 and the 16-B aligned body
+// moves with one bulk copy; an unaligned head/tail element is copied by the
+// issuing thread itself.  Returns the bulk bytes.
+__device__ __forceinline__ unsigned tile_plain(uint64_t* s, const uint64_t* g, int off, int cnt) {
+    const int nb = (cnt - off) >> 1;
+    if (off) s[1] = g[0];
+    if (off + 2 * nb < cnt) s[off + cnt - 1] = g[cnt - 1];
+    return 16u * nb;
+}
+__device__ __forceinline__ void tile_bulk(uint64_t* s, const uint64_t* g, int off, unsigned bytes, uint64_t* bar) {
+    if (bytes) bulk_load(s + 2 * off, g + off, bytes, bar);
 }
 
 #ifdef MPSM_DBG_TIMING
 __device__ long long g_seg_ts[1 << 22][8];
 #define SEG_TS(i) \
-    if (tid == 0) g_seg_ts[(t0 / TILE) & ((1 << 22) - 1)][i] = clock64();
+    if (tid == 0) g_seg_ts[t & ((1 << 22) - 1)][i] = clock64();
 #else
 #define SEG_TS(i)
 #endif
 
-// STABLE = false ranks with one shared atomicAdd per tuple (order within a
-// digit arbitrary) -- allowed for the first LSD pass only, whose input order
-// carries no information.  STABLE = true ranks with warp ballots so equal
-// digits keep their input order (every later pass).
-template <int LAYOUT, bool STABLE>
+// digit of a record whose key bits start at or above bit 32 (HI) -- one
+// shift of the high word
+template <bool HI>
+__device__ __forceinline__ uint32_t rec_digit(uint64_t v, const Digit& d) {
+    if (HI) return ((uint32_t)(v >> 32) >> (d.shift - 32)) & d.mask;
+    return (uint32_t)(v >> d.shift) & d.mask;
+}
+
+// One persistent CTA per segment.  Per tile, five barriers:
+//   S1 previous tile written out: thread 0 launches the bulk copy of the
+//      next tile; all wait for this tile's copy, load items into
+//      registers and rank them -- a stable rank within the warp's row
+//   S2 histograms complete: thread d scans digit d over the warp rows and
+//      the digits (block scan)
+//   S3 carries of the digit scan published
+//   S4 rows hold staging offsets: stage items in digit order in place
+//   S5 staged: clear the histogram, stream the tile out in coalesced runs
+// Ranking: lanes of a warp that add to one shared address in one atomicAdd
+// instruction receive consecutive counts in lane order (sm_100; probed once
+// per process by lane_ordered_atomics()), items of a warp go in program
+// order and warps in row order, so one ATOMS per tuple gives a stable rank.
+// Where the probe fails the peers come from ballots (ballot_peers).
+// HI: the staged records' digit lies in the high word (PP/SP with pw >= 32).
+template <int LAYOUT, bool HI>
 __global__ void __launch_bounds__(THREADS, LAYOUT == PP ? MPSM_SEG_PP_BLOCKS : 1) k_scatter(
     const uint64_t* __restrict__ in_k, const uint64_t* __restrict__ in_p, uint64_t* __restrict__ out_k,
-    uint64_t* __restrict__ out_p, Segs sg, Digit dig, Digit odig, int bits, int nbins,
-    const int64_t* __restrict__ base, uint64_t pk_lower, int pk_pw, unsigned int* __restrict__ overflow) {
+    uint64_t* __restrict__ out_p, Segs sg, Digit dig, Digit odig, int nbins, const int64_t* __restrict__ base,
+    const uint32_t* __restrict__ toffs, unsigned int* __restrict__ ticket, uint64_t pk_lower, int pk_pw,
+    unsigned int* __restrict__ overflow, bool lane_ordered) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem<LAYOUT>& sm = *reinterpret_cast<Smem<LAYOUT>*>(smem_raw);
     constexpr int NARR = Smem<LAYOUT>::NARR;
-    constexpr int HW = STABLE ? WARPS : 1;  // histogram rows: per warp, or one per tile
+    constexpr int ROWS = WARPS / 2;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt = lanemask_lt();
-    const int g = blockIdx.x;
-    const int64_t sb = sg.begin(g), se = sg.end(g);
-    if (sb >= se) return;
-    const bool vec = ((((uintptr_t)in_k) | (NARR == 2 ? (uintptr_t)in_p : 0)) & 15) == 0;  // sb is a TILE multiple
-    for (int d = tid; d < nbins; d += THREADS) sm.cur[d] = base[(size_t)g * nbins + d];
+    const int64_t T = (sg.n + TILE - 1) / TILE, tiles_per_seg = sg.seg_len / TILE;
+    if ((int64_t)blockIdx.x >= T) return;
+    const int offk = (int)(((uintptr_t)in_k >> 3) & 1), offp = NARR == 2 ? (int)(((uintptr_t)in_p >> 3) & 1) : 0;
+    const bool mine = tid < nbins;  // the digit this thread scans
+    uint32_t* hrow = sm.hist[warp >> 1];
+    const uint32_t inc = (warp & 1) ? 0x10000u : 1u;
+    const uint32_t half = (warp & 1) ? 0x4432u : 0x4410u;  // byte_perm: my 16-bit field
+    for (int i = tid; i < ROWS * MAX_BINS / 4; i += THREADS)
+        reinterpret_cast<uint4*>(&sm.hist[0][0])[i] = make_uint4(0, 0, 0, 0);
 
-    auto issue = [&](int b, int64_t t0) {
-        const int cnt = (int)min((int64_t)TILE, se - t0);
-        tile_copy(sm.buf[b][0], in_k + t0, cnt, vec);
-        if (NARR == 2) tile_copy(sm.buf[b][1], in_p + t0, cnt, vec);
+    // thread 0: one mbarrier phase brings tile t's tuples, its digit
+    // prefixes and its segment's digit bases into buffer bb
+    auto fetch = [&](int bb, int64_t t) {
+        const int64_t t0 = t * TILE;
+        const int cnt = (int)min((int64_t)TILE, sg.n - t0);
+        sm.tile[bb] = t;
+        unsigned bk = tile_plain(sm.buf[bb][0], in_k + t0, offk, cnt), bp = 0;
+        if (NARR == 2) bp = tile_plain(sm.buf[bb][NARR - 1], in_p + t0, offp, cnt);
+        const unsigned bo = MAX_BINS * 4, bs = nbins * 8;
+        mbar_arrive_expect_tx(&sm.bar[bb], bk + bp + bo + bs);
+        tile_bulk(sm.buf[bb][0], in_k + t0, offk, bk, &sm.bar[bb]);
+        if (NARR == 2) tile_bulk(sm.buf[bb][NARR - 1], in_p + t0, offp, bp, &sm.bar[bb]);
+        bulk_load(sm.toffs[bb], toffs + (size_t)t * MAX_BINS, bo, &sm.bar[bb]);
+        bulk_load(sm.sbase[bb], base + (size_t)(t / tiles_per_seg) * nbins, bs, &sm.bar[bb]);
     };
-    issue(0, sb);
-    asm volatile("cp.async.commit_group;" ::: "memory");
+    // tiles in global order: each CTA starts at tile blockIdx.x, later tiles
+    // come from a dispenser in order, so the tiles in flight at any moment
+    // are neighbours and their runs of one digit land next to each other in
+    // the output (a CTA sweeping its own contiguous segment instead halves
+    // the write bandwidth: tools/scatter_pattern_bench.cu)
+    int64_t tnext = 0;  // thread 0: the tile after the one being fetched
+    if (tid == 0) {
+        mbar_init(&sm.bar[0], 1);
+        mbar_init(&sm.bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fetch(0, blockIdx.x);
+        tnext = (int64_t)gridDim.x + atomicAdd(ticket, 1u);
+    }
+    unsigned par = 0;
     int b = 0;
-    for (int64_t t0 = sb; t0 < se; t0 += TILE) {
-        if (t0 + TILE < se) issue(b ^ 1, t0 + TILE);
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
+    for (;;) {
+        __syncthreads();  // S1
+        const int64_t t = sm.tile[b];  // set by thread 0 before S1
+        if (t >= T) break;
         SEG_TS(0)
-        __syncthreads();  // tile t0 is in buf[b]
+        if (tid == 0) {
+            if (tnext < T) {
+                fence_proxy_async_smem();  // buf[b^1] was staged through by generic stores
+                fetch(b ^ 1, tnext);
+                tnext = (int64_t)gridDim.x + atomicAdd(ticket, 1u);  // used one tile later
+            } else {
+                sm.tile[b ^ 1] = T;  // no more tiles
+            }
+        }
+        mbar_wait(&sm.bar[b], (par >> b) & 1u);
+        par ^= 1u << b;
         SEG_TS(1)
-        const int cnt = (int)min((int64_t)TILE, se - t0);
-        const bool full = cnt == TILE;
-
-        // ---- items into registers (warp-striped)
-        uint64_t key[ITEMS];
-        uint32_t pos[ITEMS];
+        const int64_t t0 = t * TILE;
+        const int cnt = (int)min((int64_t)TILE, sg.n - t0);
         const int wb = warp * (32 * ITEMS);
+        const int lim = cnt - wb - lane;  // item k is valid iff 32 * k < lim
+
+        // ---- items into registers (warp-striped) and rank
+        uint64_t key[ITEMS], pay[ITEMS];
+        uint32_t dg[ITEMS], rk[ITEMS];
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k) {
             const int li = wb + 32 * k + lane;
-            key[k] = (full || li < cnt) ? sm.buf[b][0][li] : 0;
+            key[k] = sm.buf[b][0][offk + li];
+            if (LAYOUT != PP) pay[k] = sm.buf[b][NARR - 1][offp + li];
+            dg[k] = LAYOUT == PP ? rec_digit<HI>(key[k], dig) : dig(key[k]);
         }
-        __syncthreads();  // buf[b][0] now hosts the digit histograms [HW][MAX_BINS]
-        uint32_t* hist = reinterpret_cast<uint32_t*>(sm.buf[b][0]);
-        for (int i = tid; i < HW * MAX_BINS / 4; i += THREADS)
-            reinterpret_cast<uint4*>(hist)[i] = make_uint4(0, 0, 0, 0);
-        __syncthreads();
-        if (STABLE) {
-            uint32_t* wh = hist + warp * MAX_BINS;
-            unsigned peers[ITEMS];
+        if (lane_ordered) {
+            if (cnt == TILE) {
 #pragma unroll
-            for (int k = 0; k < ITEMS; ++k) {  // independent: the ballots pipeline
-                const int li = wb + 32 * k + lane;
-                const bool valid = full || li < cnt;
-                const unsigned vmask = full ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
-                const uint32_t d = dig(key[k]);
-                peers[k] = ballot_peers(d, bits, vmask);
-                if (!valid) peers[k] = 0;
-                pos[k] = d << 20;
-            }
+                for (int k = 0; k < ITEMS; ++k) rk[k] = __byte_perm(atomicAdd(&hrow[dg[k]], inc), 0, half);
+            } else {
 #pragma unroll
-            for (int k = 0; k < ITEMS; ++k) {  // running per-warp digit counts
-                const uint32_t d = pos[k] >> 20;
-                uint32_t before = 0;
-                if (peers[k]) before = wh[d];
-                __syncwarp();
-                if (peers[k] && (peers[k] & lt) == 0) wh[d] = before + __popc(peers[k]);
-                __syncwarp();
-                pos[k] = peers[k] ? ((d << 20) | (before + __popc(peers[k] & lt))) : 0xffffffffu;
+                for (int k = 0; k < ITEMS; ++k)
+                    if (32 * k < lim) rk[k] = __byte_perm(atomicAdd(&hrow[dg[k]], inc), 0, half);
             }
         } else {
 #pragma unroll
             for (int k = 0; k < ITEMS; ++k) {
-                const int li = wb + 32 * k + lane;
-                const uint32_t d = dig(key[k]);
-                pos[k] = (full || li < cnt) ? ((d << 20) | atomicAdd(&hist[d], 1u)) : 0xffffffffu;
+                const bool valid = 32 * k < lim;
+                const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+                const unsigned peers = ballot_peers(dg[k], vmask);
+                const int leader = valid ? __ffs(peers) - 1 : lane;
+                uint32_t old = 0;
+                if (valid && leader == lane) old = atomicAdd(&hrow[dg[k]], inc * __popc(peers));
+                old = __shfl_sync(0xffffffffu, old, leader);
+                rk[k] = __byte_perm(old, 0, half) + __popc(peers & lt);
             }
         }
-        __syncthreads();
+        __syncthreads();  // S2
         SEG_TS(2)
-        // ---- per digit: tile count; after the digit scan the histogram rows
-        // become absolute staging offsets tile_off[d] + (earlier rows' d's)
-        constexpr int DPT = (MAX_BINS + THREADS - 1) / THREADS;  // digits per thread
-        uint32_t mycnt[DPT];
-        uint32_t col[DPT][HW];
+
+        // ---- digit scan: thread d sums its digit over the warp rows, then
+        // a block-wide exclusive scan over the digits
+        uint32_t col[ROWS];
+        uint32_t sum = 0;
 #pragma unroll
-        for (int j = 0; j < DPT; ++j) {
-            const int dd = tid + j * THREADS;
-            mycnt[j] = 0;
-            if (dd < nbins) {
-#pragma unroll
-                for (int w = 0; w < HW; ++w) {
-                    col[j][w] = hist[w * MAX_BINS + dd];
-                    mycnt[j] += col[j][w];
-                }
-            }
-            if (dd < MAX_BINS) sm.tile_off[dd] = mycnt[j];
+        for (int r = 0; r < ROWS; ++r) {
+            col[r] = mine ? sm.hist[r][tid] : 0;
+            sum += col[r];
         }
-        __syncthreads();
-        if (warp == 0) {
-            constexpr int PER = MAX_BINS / 32;
-            uint32_t loc[PER];
-            uint32_t sum = 0;
+        const uint32_t tot = (sum & 0xffffu) + (sum >> 16);
+        uint32_t incl = tot;
 #pragma unroll
-            for (int q = 0; q < PER; ++q) {
-                loc[q] = sm.tile_off[lane * PER + q];
-                sum += loc[q];
-            }
-            uint32_t incl = sum;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += v;
-            }
-            uint32_t run = incl - sum;
-#pragma unroll
-            for (int q = 0; q < PER; ++q) {
-                const uint32_t c = loc[q];
-                sm.tile_off[lane * PER + q] = run;
-                run += c;
-            }
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
         }
-        __syncthreads();
+        if (lane == 31) sm.wtot[warp] = incl;
+        __syncthreads();  // S3
+        const uint32_t toff = incl - tot + __reduce_add_sync(0xffffffffu, lane < warp ? sm.wtot[lane] : 0u);
+        if (mine) {
+            uint32_t run = toff;
 #pragma unroll
-        for (int j = 0; j < DPT; ++j) {
-            const int dd = tid + j * THREADS;
-            if (dd < nbins) {
-                const uint32_t toff = sm.tile_off[dd];
-                uint32_t run = toff;
-#pragma unroll
-                for (int w = 0; w < HW; ++w) {
-                    hist[w * MAX_BINS + dd] = run;
-                    run += col[j][w];
-                }
-                sm.gdelta[dd] = sm.cur[dd] - (int64_t)toff;
-                sm.cur[dd] += mycnt[j];
+            for (int r = 0; r < ROWS; ++r) {
+                // fields (run, run + lo); hi + lo = high half of col + (col << 16)
+                const uint32_t sh = col[r] << 16;
+                sm.hist[r][tid] = run * 0x10001u + sh;
+                run += (col[r] + sh) >> 16;
             }
-        }
-        __syncthreads();
-        SEG_TS(3)
-        // ---- final staging positions
-#pragma unroll
-        for (int k = 0; k < ITEMS; ++k)
-            if (pos[k] != 0xffffffffu)
-                pos[k] = hist[(STABLE ? warp : 0) * MAX_BINS + (pos[k] >> 20)] + (pos[k] & 0xfffffu);
-        uint64_t pay[ITEMS];
-        if (LAYOUT != PP) {
-#pragma unroll
-            for (int k = 0; k < ITEMS; ++k) {
-                const int li = wb + 32 * k + lane;
-                pay[k] = (full || li < cnt) ? sm.buf[b][1][li] : 0;
-            }
+            sm.gdelta[tid] = sm.sbase[b][tid] + sm.toffs[b][tid] - (int64_t)toff;
         }
         if (LAYOUT == SP) {
             uint64_t ovf = 0;
             const uint64_t pmask = (1ull << pk_pw) - 1ull;
 #pragma unroll
             for (int k = 0; k < ITEMS; ++k) {
-                ovf |= pay[k] >> pk_pw;
+                if (32 * k < lim) ovf |= pay[k] >> pk_pw;
                 // a wider payload is masked so the key bits stay exact; the
                 // caller sees *overflow and redoes the join on pairs
                 key[k] = ((key[k] - pk_lower) << pk_pw) | (pay[k] & pmask);
             }
             if (__any_sync(0xffffffffu, ovf != 0) && lane == 0) atomicOr(overflow, 1u);
         }
-        __syncthreads();  // histograms and tile reads done: stage in place
-        SEG_TS(4)
+        __syncthreads();  // S4
+        SEG_TS(3)
+
+        // ---- stage in digit order
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k) {
-            if (pos[k] != 0xffffffffu) {
-                sm.buf[b][0][pos[k]] = key[k];
-                if (LAYOUT == SS) sm.buf[b][1][pos[k]] = pay[k];
+            if (cnt == TILE || 32 * k < lim) {
+                const uint32_t p = __byte_perm(hrow[dg[k]], 0, half) + rk[k];
+                sm.buf[b][0][p] = key[k];
+                if (LAYOUT == SS) sm.buf[b][1][p] = pay[k];
             }
         }
-        __syncthreads();
-        SEG_TS(5)
+        __syncthreads();  // S5
+        SEG_TS(4)
+        for (int i = tid; i < ROWS * MAX_BINS / 4; i += THREADS)
+            reinterpret_cast<uint4*>(&sm.hist[0][0])[i] = make_uint4(0, 0, 0, 0);
 #pragma unroll 4
         for (int i = tid; i < cnt; i += THREADS) {
             const uint64_t v = sm.buf[b][0][i];
-            const int64_t o = sm.gdelta[odig(v)] + i;
+            const int64_t o = sm.gdelta[LAYOUT == SS ? odig(v) : rec_digit<HI>(v, odig)] + i;
             out_k[o] = v;
             if (LAYOUT == SS) out_p[o] = sm.buf[b][1][i];
         }
-        __syncthreads();  // buf[b] free for the tile after next
-        SEG_TS(6)
+        SEG_TS(5)
         b ^= 1;
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 // ------------------------------------------------------------------- host
+// start-up probe: do shared atomicAdds that collide within one warp
+// instruction return their counts in lane order?  (true on sm_100; if a
+// device ever says no, the stable passes fall back to ballot ranking)
+__global__ void k_probe_lane_order(int* bad) {
+    __shared__ uint32_t hs[8][32];  // one row per warp, as in k_scatter
+    const int lane = threadIdx.x & 31;
+    uint32_t* h = hs[threadIdx.x >> 5];
+    h[lane] = 0;
+    __syncthreads();
+    uint32_t x = 0x9E3779B9u * (threadIdx.x + 1) + blockIdx.x;
+    for (int it = 0; it < 64; ++it) {
+        x ^= x << 13;
+        x ^= x >> 17;
+        x ^= x << 5;
+        const uint32_t d = (x >> 7) % (1 + (it & 31));
+        const uint32_t old = atomicAdd(&h[d], 1u);
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t base = __shfl_sync(0xffffffffu, old, __ffs(peers) - 1);
+        if (old != base + __popc(peers & ((1u << lane) - 1u))) atomicAdd(bad, 1);
+        __syncthreads();
+    }
+}
+
+static bool lane_ordered_atomics() {
+    static int state = -1;
+    if (state < 0) {
+        int* d = nullptr;
+        int bad = 1;
+        if (cudaMalloc(&d, sizeof(int)) == cudaSuccess) {
+            cudaMemset(d, 0, sizeof(int));
+            k_probe_lane_order<<<148, 256>>>(d);
+            cudaMemcpy(&bad, d, sizeof(int), cudaMemcpyDeviceToHost);
+            cudaFree(d);
+        }
+        state = (bad == 0 && cudaGetLastError() == cudaSuccess) ? 1 : 0;
+#ifdef MPSM_SEG_BALLOT_RANK
+        state = 0;
+#endif
+    }
+    return state == 1;
+}
+
+extern "C" int mpsm_dbg_lane_ordered() { return lane_ordered_atomics() ? 1 : 0; }
+
 struct Ws {
     uint32_t* counts;  // [G][MAX_BINS]
     int64_t* base;     // [G][MAX_BINS]
+    uint32_t* toffs;   // [tiles][MAX_BINS]
+    unsigned int* ticket;
 };
 
 // one CTA per resident slot: the pair layouts (146 KB of shared memory) fit
@@ -434,24 +499,29 @@ static Segs make_segs(int64_t n, int G) {
     return Segs{n, seg};
 }
 
-static size_t ws_bytes() {
+static size_t ntiles(int64_t n) { return (size_t)((n + TILE - 1) / TILE); }
+
+static size_t ws_bytes(int64_t n) {
     const int G = max_grid();
-    return align_up(sizeof(uint32_t) * (size_t)G * MAX_BINS) + align_up(sizeof(int64_t) * (size_t)G * MAX_BINS);
+    return align_up(sizeof(uint32_t) * (size_t)G * MAX_BINS) + align_up(sizeof(int64_t) * (size_t)G * MAX_BINS) +
+           align_up(sizeof(uint32_t) * ntiles(n) * MAX_BINS) + align_up(sizeof(unsigned int));
 }
 
-static bool carve(void* ws, size_t bytes, Ws* o) {
+static bool carve(void* ws, size_t bytes, int64_t n, Ws* o) {
     Carve c{(char*)ws, bytes};
     const int G = max_grid();
     o->counts = c.take<uint32_t>((size_t)G * MAX_BINS);
     o->base = c.take<int64_t>((size_t)G * MAX_BINS);
+    o->toffs = c.take<uint32_t>(ntiles(n) * MAX_BINS);
+    o->ticket = c.take<unsigned int>(1);
     return c.ok;
 }
 
-template <int LAYOUT, bool STABLE>
+template <int LAYOUT, bool HI>
 static int set_attr() {
     static bool done = false;
     if (!done) {
-        MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_scatter<LAYOUT, STABLE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_scatter<LAYOUT, HI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   (int)sizeof(Smem<LAYOUT>)),
                              "smem attr"));
         done = true;
@@ -460,7 +530,7 @@ static int set_attr() {
 }
 
 // one digit pass: count, scan, scatter
-template <int LAYOUT, bool STABLE>
+template <int LAYOUT>
 static int pass(const uint64_t* in_k, const uint64_t* in_p, uint64_t* out_k, uint64_t* out_p, int64_t n,
                 Digit count_dig, Digit dig, int bits, const Ws& ws, uint64_t span_m1, unsigned long long* d_bad,
                 uint64_t pk_lower, int pk_pw, unsigned int* overflow, cudaStream_t st) {
@@ -469,20 +539,27 @@ static int pass(const uint64_t* in_k, const uint64_t* in_p, uint64_t* out_k, uin
     const int nbins = 1 << bits;
     {
         ProfScope ps("seg_count", st);
-        k_count<<<G, THREADS, 0, st>>>(in_k, sg, count_dig, nbins, ws.counts, span_m1, d_bad);
+        k_count<<<G, THREADS, 0, st>>>(in_k, sg, count_dig, nbins, ws.counts, ws.toffs, ws.ticket, span_m1,
+                                       d_bad);
     }
     MPSM_TRY(check_launch("k_count"));
     k_scan<<<1, MAX_BINS, 0, st>>>(ws.counts, G, nbins, ws.base);
     MPSM_TRY(check_launch("k_scan"));
-    MPSM_TRY((set_attr<LAYOUT, STABLE>()));
+    // digit of a staged value: records staged by the SP pass carry the key
+    // above the payload bits
+    const Digit odig = (LAYOUT == SP) ? Digit{0, pk_pw + dig.shift, dig.mask} : dig;
+    const bool hi = LAYOUT != SS && odig.shift >= 32;
+    MPSM_TRY(hi ? (set_attr<LAYOUT, true>()) : (set_attr<LAYOUT, false>()));
     {
         ProfScope ps("seg_scatter", st);
         ProfScope ps2(LAYOUT == SS ? "seg_scatter_ss" : (LAYOUT == SP ? "seg_scatter_sp" : "seg_scatter_pp"), st);
-        // digit of a staged value: records staged by the SP pass carry the key
-        // above the payload bits
-        const Digit odig = (LAYOUT == SP) ? Digit{0, pk_pw + dig.shift, dig.mask} : dig;
-        k_scatter<LAYOUT, STABLE><<<G, THREADS, sizeof(Smem<LAYOUT>), st>>>(in_k, in_p, out_k, out_p, sg, dig, odig, bits,
-                                                                    nbins, ws.base, pk_lower, pk_pw, overflow);
+        const bool lo = lane_ordered_atomics();
+        if (hi)
+            k_scatter<LAYOUT, true><<<G, THREADS, sizeof(Smem<LAYOUT>), st>>>(
+                in_k, in_p, out_k, out_p, sg, dig, odig, nbins, ws.base, ws.toffs, ws.ticket, pk_lower, pk_pw, overflow, lo);
+        else
+            k_scatter<LAYOUT, false><<<G, THREADS, sizeof(Smem<LAYOUT>), st>>>(
+                in_k, in_p, out_k, out_p, sg, dig, odig, nbins, ws.base, ws.toffs, ws.ticket, pk_lower, pk_pw, overflow, lo);
     }
     return check_launch("k_scatter");
 }
@@ -502,7 +579,7 @@ extern "C" int mpsm_sort_pass_count(int width_bits) { return seg::make_plan(widt
 
 extern "C" int mpsm_sort_workspace_bytes(int64_t n, int width_bits, size_t* bytes) {
     if (!bytes || n < 0 || width_bits < 0 || width_bits > 64) return MPSM_ERR_ARG;
-    *bytes = seg::ws_bytes();
+    *bytes = seg::ws_bytes(n);
     return MPSM_OK;
 }
 
@@ -515,14 +592,15 @@ extern "C" int mpsm_sort_pairs(const uint64_t* in_keys, const uint64_t* in_pays,
     if (n < 0 || width_bits < 0 || width_bits > 64) return MPSM_ERR_ARG;
     if (n == 0) return MPSM_OK;
     Ws ws;
-    if (!carve(workspace, ws_bytes, &ws)) {
+    if (!carve(workspace, ws_bytes, n, &ws)) {
         set_error("sort workspace too small");
         return MPSM_ERR_ARG;
     }
     const Plan plan = make_plan(width_bits);
     if (plan.npasses == 0) {  // one-value domain: check it and copy
         const int G = max_grid();
-        k_count<<<G, THREADS, 0, st>>>(in_keys, make_segs(n, G), Digit{lower, 0, 0}, 1, ws.counts, span_m1, d_bad);
+        k_count<<<G, THREADS, 0, st>>>(in_keys, make_segs(n, G), Digit{lower, 0, 0}, 1, ws.counts, ws.toffs, nullptr,
+                                       span_m1, d_bad);
         MPSM_TRY(check_launch("k_count"));
         if (out_keys != in_keys) {
             MPSM_TRY(cuda_status(cudaMemcpyAsync(out_keys, in_keys, 8 * n, cudaMemcpyDeviceToDevice, st), "copy"));
@@ -544,11 +622,8 @@ extern "C" int mpsm_sort_pairs(const uint64_t* in_keys, const uint64_t* in_pays,
         uint64_t* dk = to_out ? out_keys : tmp_keys;
         uint64_t* dp = to_out ? out_pays : tmp_pays;
         const Digit dg{lower, plan.shift[i], (1u << plan.bits[i]) - 1u};
-        // the first LSD pass may reorder equal digits; later passes must not
-        if (i == 0)
-            MPSM_TRY((pass<SS, false>(sk, sp, dk, dp, n, dg, dg, plan.bits[i], ws, span_m1, d_bad, 0, 0, nullptr, st)));
-        else
-            MPSM_TRY((pass<SS, true>(sk, sp, dk, dp, n, dg, dg, plan.bits[i], ws, ~0ull, nullptr, 0, 0, nullptr, st)));
+        MPSM_TRY(pass<SS>(sk, sp, dk, dp, n, dg, dg, plan.bits[i], ws, i == 0 ? span_m1 : ~0ull, i == 0 ? d_bad : nullptr,
+                          0, 0, nullptr, st));
         sk = dk;
         sp = dp;
     }
@@ -563,7 +638,7 @@ extern "C" int mpsm_sort_packed(const uint64_t* in_keys, const uint64_t* in_pays
     if (n < 0 || width_bits < 1 || width_bits > 63 || !d_overflow) return MPSM_ERR_ARG;
     if (n == 0) return MPSM_OK;
     Ws ws;
-    if (!carve(workspace, ws_bytes, &ws)) {
+    if (!carve(workspace, ws_bytes, n, &ws)) {
         set_error("sort workspace too small");
         return MPSM_ERR_ARG;
     }
@@ -575,12 +650,12 @@ extern "C" int mpsm_sort_packed(const uint64_t* in_keys, const uint64_t* in_pays
         uint64_t* dst = ((P - 1 - i) % 2 == 0) ? out_rec : tmp_rec;
         if (i == 0) {
             const Digit dg{lower, plan.shift[0], (1u << plan.bits[0]) - 1u};
-            MPSM_TRY((pass<SP, false>(in_keys, in_pays, dst, nullptr, n, dg, dg, plan.bits[0], ws, span_m1, d_bad,
-                                      lower, pw, d_overflow, st)));
+            MPSM_TRY(pass<SP>(in_keys, in_pays, dst, nullptr, n, dg, dg, plan.bits[0], ws, span_m1, d_bad, lower, pw,
+                              d_overflow, st));
         } else {
             const Digit dg{0, pw + plan.shift[i], (1u << plan.bits[i]) - 1u};
-            MPSM_TRY((pass<PP, true>(src, nullptr, dst, nullptr, n, dg, dg, plan.bits[i], ws, ~0ull, nullptr, 0, pw,
-                                     nullptr, st)));
+            MPSM_TRY(pass<PP>(src, nullptr, dst, nullptr, n, dg, dg, plan.bits[i], ws, ~0ull, nullptr, 0, pw, nullptr,
+                              st));
         }
         src = dst;
     }

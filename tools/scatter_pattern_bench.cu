@@ -28,6 +28,25 @@ __global__ void scatter_k(const uint64_t* __restrict__ in, uint64_t* __restrict_
     }
 }
 
+// segmented: G persistent CTAs, CTA g owns tiles [g*T/G, (g+1)*T/G); bucket d
+// of its k-th tile goes to d*region + g*(region/G) + k*run -- the pattern of
+// segsort.cu (each CTA appends to nbins private streams)
+template <int THREADS>
+__global__ void seg_k(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, size_t n, int tile, int nbins) {
+    const size_t T = n / tile, G = gridDim.x;
+    const size_t t0 = blockIdx.x * T / G, t1 = (blockIdx.x + 1) * T / G;
+    const int run = tile / nbins;
+    const size_t region = n / nbins;
+    const size_t sub = region / G;
+    for (size_t t = t0; t < t1; ++t) {
+        for (int i = threadIdx.x; i < tile; i += THREADS) {
+            const uint64_t v = in[t * tile + i];
+            const int d = i / run, r = i % run;
+            out[(size_t)d * region + blockIdx.x * sub + (t - t0) * run + r] = v;
+        }
+    }
+}
+
 int main(int argc, char** argv) {
     size_t n = argc > 1 ? strtoull(argv[1], 0, 10) : 400000000ull;
     int tile = argc > 2 ? atoi(argv[2]) : 6144;
@@ -58,6 +77,18 @@ int main(int argc, char** argv) {
         cudaEventElapsedTime(&ms, e0, e1);
         if (it == 2) printf("scatter  : tile %d bins %d run %d: %.3f ms  %.0f GB/s\n", tile, nbins, tile / nbins, ms,
                             16.0 * n / ms / 1e6);
+    }
+    for (int G : {148, 296, 592}) {
+        for (int it = 0; it < 3; ++it) {
+            cudaEventRecord(e0);
+            seg_k<512><<<G, 512>>>(a, b, n, tile, nbins);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (it == 2) printf("segmented: G %d tile %d bins %d run %d: %.3f ms  %.0f GB/s\n", G, tile, nbins, tile / nbins, ms,
+                                16.0 * n / ms / 1e6);
+        }
     }
     return 0;
 }

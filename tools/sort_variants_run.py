@@ -42,7 +42,8 @@ for packed in (False, True):
     sorted_ok = bool((srt[1:] >= srt[:-1]).all())
     best = min(res)
     ms, (os_ms, os_n), (h_ms, h_n), per = best
-    print(f"{os.environ['VNAME']:10s} {'packed' if packed else 'pairs ':6s} total {ms:7.3f} ms  scatter {os_ms:7.3f} ms/{os_n} passes"
+    lo = _lib.load().mpsm_dbg_lane_ordered()
+    print(f"lo={lo} {os.environ['VNAME']:10s} {'packed' if packed else 'pairs ':6s} total {ms:7.3f} ms  scatter {os_ms:7.3f} ms/{os_n} passes"
           f" = {os_ms/os_n:6.3f} ms/pass  count {h_ms:6.3f} ms/{h_n}  sorted={sorted_ok}  "
           + " ".join(f"{nm}={m:.3f}/{c}" for nm, (m, c) in zip(("ss", "sp", "pp"), per) if c), flush=True)
 '''
