@@ -246,26 +246,75 @@ __global__ void k_partition(const mpsm_run_t* __restrict__ priv, const mpsm_run_
     splits[g] = t;
 }
 
-// two tile buffers: tile g+grid streams in (cp.async) while tile g merges
-// slot 0 holds R[i0-1] when i0 > 0: the S tuples that open a tile usually match
-// the R tuple that closed the previous one, and keeping it in shared memory
-// spares thread 0 a dependent global load per tile
-struct MergeStage {
-    uint64_t k[MJ_TILE + 1], p[MJ_TILE + 1];  // [hp | R (nR) | W (nW)], hp = (i0 > 0)
+// Tile staging.  A stage holds the 16-B aligned superset of the tile's R
+// range (with the prior tuple R[i0-1] when i0 > 0: the S tuples that open a
+// tile usually match the R tuple that closed the previous one) followed by
+// the aligned superset of its W range; each range arrives with one bulk copy
+// (TMA).  Reading up to 8 B beyond a range stays inside its 16-B block, so
+// inside the mapped allocation.
+template <bool PK>
+struct alignas(16) MergeStage {
+    uint64_t k[MJ_TILE + 8];
+    uint64_t p[PK ? 2 : MJ_TILE + 8];  // payloads (SoA runs only)
+    TileSplit t;                       // descriptor of the staged tile
 };
+template <bool PK>
 struct MergeSmem {
-    MergeStage st[2];
+    MergeStage<PK> st[2];
+    uint64_t bar[2];
     uint64_t red[3][MJ_THREADS / 32];
+    int64_t warp_cnt[MJ_THREADS / 32];
 };
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+// a range [first, first + n) of array a as an aligned bulk copy: element
+// first sits at index off of the copy
+struct Span {
+    const uint64_t* src;
+    int off;
+    unsigned bytes;
+};
+__device__ __forceinline__ Span span_of(const uint64_t* a, int64_t first, int n) {
+    if (n <= 0) return Span{a, 0, 0u};
+    const uintptr_t lo = (uintptr_t)(a + first), hi = (uintptr_t)(a + first + n);
+    const uintptr_t a0 = lo & ~(uintptr_t)15, a1 = (hi + 15) & ~(uintptr_t)15;
+    return Span{(const uint64_t*)a0, (int)((lo - a0) >> 3), (unsigned)(a1 - a0)};
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
-__device__ __forceinline__ void flush_pair(MergeSmem& sm, uint64_t* __restrict__ out, int pair, uint64_t count,
+// where tile t's elements sit in a stage
+struct TilePlace {
+    Span rk, wk, rp, wp;
+    int hp;
+};
+template <bool PK>
+__device__ __forceinline__ TilePlace place_of(const TileSplit& t) {
+    TilePlace q;
+    q.hp = t.i0 > 0 ? 1 : 0;
+    q.rk = span_of(t.rk, t.i0 - q.hp, t.nR + q.hp);
+    q.wk = span_of(t.wk, t.w0, t.nW);
+    if (!PK) {
+        q.rp = span_of(t.rp, t.i0 - q.hp, t.nR + q.hp);
+        q.wp = span_of(t.wp, t.w0, t.nW);
+    }
+    return q;
+}
+
+template <bool PK>
+__device__ __forceinline__ void fetch_tile(MergeStage<PK>& st, uint64_t* bar, const TileSplit& t) {
+    const TilePlace q = place_of<PK>(t);
+    st.t = t;
+    unsigned tx = q.rk.bytes + q.wk.bytes;
+    if (!PK) tx += q.rp.bytes + q.wp.bytes;
+    mbar_arrive_expect_tx(bar, tx);
+    if (q.rk.bytes) bulk_load(st.k, q.rk.src, q.rk.bytes, bar);
+    if (q.wk.bytes) bulk_load(st.k + q.rk.bytes / 8, q.wk.src, q.wk.bytes, bar);
+    if (!PK) {
+        if (q.rp.bytes) bulk_load(st.p, q.rp.src, q.rp.bytes, bar);
+        if (q.wp.bytes) bulk_load(st.p + q.rp.bytes / 8, q.wp.src, q.wp.bytes, bar);
+    }
+}
+
+template <bool PK>
+__device__ __forceinline__ void flush_pair(MergeSmem<PK>& sm, uint64_t* __restrict__ out, int pair, uint64_t count,
                                            uint64_t best, uint64_t csum) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     count = warp_sum(count);
@@ -294,22 +343,6 @@ __device__ __forceinline__ void flush_pair(MergeSmem& sm, uint64_t* __restrict__
     __syncthreads();
 }
 
-template <bool PK>
-__device__ __forceinline__ void load_tile_async(MergeStage& st, const TileSplit& t) {
-    const int hp = t.i0 > 0 ? 1 : 0;
-    const int nr = t.nR + hp;
-    const uint64_t* rk = t.rk + t.i0 - hp;
-    const uint64_t* wk = t.wk + t.w0;
-    for (int x = threadIdx.x; x < nr; x += MJ_THREADS) cp_async8(&st.k[x], rk + x);
-    for (int x = threadIdx.x; x < t.nW; x += MJ_THREADS) cp_async8(&st.k[nr + x], wk + x);
-    if (!PK) {
-        const uint64_t* rp = t.rp + t.i0 - hp;
-        const uint64_t* wp = t.wp + t.w0;
-        for (int x = threadIdx.x; x < nr; x += MJ_THREADS) cp_async8(&st.p[x], rp + x);
-        for (int x = threadIdx.x; x < t.nW; x += MJ_THREADS) cp_async8(&st.p[nr + x], wp + x);
-    }
-}
-
 #ifdef MPSM_DBG_TIMING
 __device__ long long g_mj_ts[1 << 20][6];
 #define MJ_TS(i) \
@@ -320,67 +353,80 @@ __device__ long long g_mj_ts[1 << 20][6];
 
 // MODE 0: aggregate into pair records; MODE 1: per-tile counts only;
 // MODE 2: emit pairs at tile_out[g] + thread offset
+// Persistent CTAs, two stages: thread 0 launches the bulk copies of tile
+// g + grid (descriptor loaded a tile earlier) while tile g merges.  Each
+// thread takes MJ_ITEMS steps of the merge from its merge-path split; for
+// every S tuple the matching R tuples are the equal-key run that ends right
+// before its merge position (ties merge R first) -- the reference's cross
+// product of duplicate key groups.  Per-thread accumulators are reduced per
+// CTA and flushed with one atomic per (pair, CTA).
 template <int MODE, bool PK, bool K32 = false>
-__global__ void __launch_bounds__(MJ_THREADS) k_merge(const TileSplit* __restrict__ splits,
-                                                      const int64_t* __restrict__ total, int swap,
-                                                      uint64_t* __restrict__ out_pairs, int64_t* __restrict__ tile_cnt,
-                                                      uint64_t* __restrict__ emit_out, PackInfo pi) {
+__global__ void __launch_bounds__(MJ_THREADS, PK ? 4 : 2) k_merge(const TileSplit* __restrict__ splits,
+                                                                 const int64_t* __restrict__ total, int swap,
+                                                                 uint64_t* __restrict__ out_pairs,
+                                                                 int64_t* __restrict__ tile_cnt,
+                                                                 uint64_t* __restrict__ emit_out, PackInfo pi) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    MergeSmem& sm = *reinterpret_cast<MergeSmem*>(smem_raw);
-    __shared__ int64_t warp_cnt[MJ_THREADS / 32];
+    MergeSmem<PK>& sm = *reinterpret_cast<MergeSmem<PK>*>(smem_raw);
     const int tid = threadIdx.x;
     const int64_t ntiles = *total;
+    const int64_t G = gridDim.x;
+    int64_t g = blockIdx.x;
+    if (g >= ntiles) return;
     int cur_pair = -1;
     uint64_t count = 0, best = 0, csum = 0;
     int buf = 0;
-
-    int64_t g = blockIdx.x;
-    TileSplit t_cur{}, t_nxt{};
-    if (g < ntiles) {
-        t_cur = splits[g];
-        load_tile_async<PK>(sm.st[0], t_cur);
+    unsigned par = 0;
+    TileSplit t_nxt{};  // thread 0: descriptor of tile g + grid
+    if (tid == 0) {
+        mbar_init(&sm.bar[0], 1);
+        mbar_init(&sm.bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fetch_tile<PK>(sm.st[0], &sm.bar[0], splits[g]);
+        if (g + G < ntiles) t_nxt = splits[g + G];
     }
-    cp_async_commit();
-    if (g + gridDim.x < ntiles) t_nxt = splits[g + gridDim.x];
-    for (; g < ntiles; g += gridDim.x) {
+    using KT = typename std::conditional<K32, uint32_t, uint64_t>::type;
+    for (; g < ntiles; g += G) {
         MJ_TS(0)
-        const int64_t gn = g + gridDim.x;
-        if (gn < ntiles) load_tile_async<PK>(sm.st[buf ^ 1], t_nxt);
-        cp_async_commit();
-        TileSplit t_after{};  // descriptor two tiles ahead, loaded under this tile's work
-        if (gn + gridDim.x < ntiles) t_after = splits[gn + gridDim.x];
-        const TileSplit t = t_cur;
+        __syncthreads();  // stage buf^1 free, stage buf's descriptor visible
+        if (tid == 0 && g + G < ntiles) {
+            fetch_tile<PK>(sm.st[buf ^ 1], &sm.bar[buf ^ 1], t_nxt);
+            if (g + 2 * G < ntiles) t_nxt = splits[g + 2 * G];  // consumed one tile later
+        }
+        const TileSplit t = sm.st[buf].t;
         if (MODE == 0 && t.pair != cur_pair) {
-            if (cur_pair >= 0) flush_pair(sm, out_pairs, cur_pair, count, best, csum);
+            if (cur_pair >= 0) flush_pair<PK>(sm, out_pairs, cur_pair, count, best, csum);
             cur_pair = t.pair;
             count = best = csum = 0;
         }
         MJ_TS(1)
-        cp_async_wait_1();  // this thread's copies of tile g landed
-        __syncthreads();    // ... and everyone else's
+        mbar_wait(&sm.bar[buf], (par >> buf) & 1u);
+        par ^= 1u << buf;
         MJ_TS(2)
-        const int nR = t.nR, nW = t.nW;
-        const int hp = t.i0 > 0 ? 1 : 0;
-        const int64_t rbase = t.i0 - hp;  // global R index of shared slot 0
-        const uint64_t* K = sm.st[buf].k + hp;  // K[i] = R tile element i (i = -1 is R[i0-1])
-        const uint64_t* Pp = sm.st[buf].p + hp;
-        // tile-relative accessors: normalized key and payload
-        // K32: packed keys of a domain at most 32 bits wide compare as u32
-        using KT = typename std::conditional<K32, uint32_t, uint64_t>::type;
-        auto skey = [&](int i) -> KT { return PK ? (KT)(K[i] >> pi.pw) : (KT)K[i]; };
-        auto spay = [&](int i) -> uint64_t { return PK ? (K[i] & pi.pmask) : Pp[i]; };
+        const TilePlace q = place_of<PK>(t);
+        const int nR = t.nR, nW = t.nW, hp = q.hp;
+        // R tile element i (i >= -hp) and W tile element j in the stage
+        const uint64_t* RK = sm.st[buf].k + q.rk.off + hp;
+        const uint64_t* WK = sm.st[buf].k + q.rk.bytes / 8 + q.wk.off;
+        const uint64_t* RP = PK ? RK : sm.st[buf].p + q.rp.off + hp;
+        const uint64_t* WP = PK ? WK : sm.st[buf].p + q.rp.bytes / 8 + q.wp.off;
+        // normalized keys and payloads; K32: packed keys of a domain at most
+        // 32 bits wide compare as u32
+        auto nkey = [&](uint64_t v) -> KT { return PK ? (KT)(v >> pi.pw) : (KT)v; };
+        auto rkey = [&](int i) -> KT { return nkey(RK[i]); };
+        auto wkey = [&](int j) -> KT { return nkey(WK[j]); };
+        auto rpay = [&](int i) -> uint64_t { return PK ? (RP[i] & pi.pmask) : RP[i]; };
+        auto wpay = [&](int j) -> uint64_t { return PK ? (WP[j] & pi.pmask) : WP[j]; };
         const int L = nR + nW;
         const int k0 = min(tid * MJ_ITEMS, L);
         const int k1 = min(k0 + MJ_ITEMS, L);
-#ifndef MPSM_MJ_SEARCH
         // per-thread split inside the tile
         int lo = k0 > nW ? k0 - nW : 0, hi = k0 < nR ? k0 : nR;
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
-            if (skey(mid) <= skey(nR + k0 - 1 - mid)) lo = mid + 1;
+            if (rkey(mid) <= wkey(k0 - 1 - mid)) lo = mid + 1;
             else hi = mid;
         }
-#endif
         MJ_TS(3)
         int64_t my_pairs = 0;
         int64_t emit_base = 0;
@@ -394,21 +440,20 @@ __global__ void __launch_bounds__(MJ_THREADS) k_merge(const TileSplit* __restric
                     const int64_t u = __shfl_up_sync(0xffffffffu, incl, o);
                     if (lane >= o) incl += u;
                 }
-                if (lane == 31) warp_cnt[warp] = incl;
+                if (lane == 31) sm.warp_cnt[warp] = incl;
                 __syncthreads();
                 int64_t before = 0;
-                for (int w = 0; w < warp; ++w) before += warp_cnt[w];
+                for (int w = 0; w < warp; ++w) before += sm.warp_cnt[w];
                 emit_base = tile_cnt[g] + before + incl - v;  // tile_cnt holds the tile's output offset here
             }
             int64_t e = 0;
             // R accessors by tile index i (i < -hp falls back to global memory)
             auto rkey_at = [&](int64_t i) -> KT {
-                if (i >= -hp) return skey((int)i);
-                const uint64_t v = t.rk[t.i0 + i];
-                return PK ? (KT)(v >> pi.pw) : (KT)v;
+                if (i >= -hp) return rkey((int)i);
+                return nkey(t.rk[t.i0 + i]);
             };
             auto rpay_at = [&](int64_t i) -> uint64_t {
-                if (i >= -hp) return spay((int)i);
+                if (i >= -hp) return rpay((int)i);
                 return PK ? (t.rk[t.i0 + i] & pi.pmask) : t.rp[t.i0 + i];
             };
             auto emit = [&](uint64_t rp, uint64_t sp) {
@@ -426,96 +471,6 @@ __global__ void __launch_bounds__(MJ_THREADS) k_merge(const TileSplit* __restric
                     ++e;
                 }
             };
-#if defined(MPSM_MJ_SEARCH)
-            // sorted search: thread t takes S tuples t, t+256, ...; the tile's
-            // merge-path bounds guarantee each one's R upper bound lies in
-            // [0, nR] of the tile, found by binary search in shared memory
-            // (consecutive lanes search neighbouring keys, so most probes are
-            // broadcasts); the matches are the equal-key run just before it
-            for (int j = tid; j < nW; j += MJ_THREADS) {
-                const uint64_t wk = skey(nR + j);
-                int base = 0, len = nR;
-                while (len > 0) {
-                    const int half = len >> 1;
-                    if (skey(base + half) <= wk) {
-                        base += half + 1;
-                        len -= half + 1;
-                    } else {
-                        len = half;
-                    }
-                }
-                int64_t i = (int64_t)base - 1;
-                if (t.i0 + i >= 0 && rkey_at(i) == wk) {
-                    const uint64_t sp = spay(nR + j);
-                    do {
-                        emit(rpay_at(i), sp);
-                        --i;
-                    } while (t.i0 + i >= 0 && rkey_at(i) == wk);
-                }
-            }
-            (void)k1;
-#elif defined(MPSM_MJ_TWO_PHASE)
-            // phase 1 -- branch-light merge walk over this thread's MJ_ITEMS
-            // steps: record, per S step, the matching R group's last index
-            // (the equal-key R group ending right before the S tuple).
-            // phase 2 -- emit the matches (hash, max, count) with no divergent
-            // merge control around the expensive work.
-            int ri = lo, wj = k0 - lo;
-            // the equal-key R group ending at ri-1: key gk, first index gs
-            bool gvalid = t.i0 + ri - 1 >= 0;
-            uint64_t gk = 0;
-            int64_t gs = ri - 1;
-            if (gvalid) {
-                gk = rkey_at(ri - 1);
-                while (t.i0 + gs - 1 >= 0 && rkey_at(gs - 1) == gk) --gs;
-            }
-            uint64_t rkc = ri < nR ? skey(ri) : 0;       // next R key
-            uint64_t wkc = wj < nW ? skey(nR + wj) : 0;  // next S key
-            int m_r[MJ_ITEMS], m_w[MJ_ITEMS];
-            unsigned match = 0, dup = 0;
-#pragma unroll
-            for (int st = 0; st < MJ_ITEMS; ++st) {
-                m_r[st] = 0;
-                m_w[st] = 0;
-                if (k0 + st < k1) {
-                    const bool take_r = ri < nR && (wj >= nW || rkc <= wkc);
-                    if (take_r) {
-                        if (!gvalid || rkc != gk) {
-                            gk = rkc;
-                            gs = ri;
-                            gvalid = true;
-                        }
-                        ++ri;
-                    } else {
-                        if (gvalid && wkc == gk) {
-                            match |= 1u << st;
-                            if (gs < ri - 1) dup |= 1u << st;
-                            m_r[st] = ri - 1;
-                            m_w[st] = wj;
-                        }
-                        ++wj;
-                    }
-                    // one shared-memory read per step: the successor of the consumed side
-                    const int nxt = take_r ? ri : nR + wj;
-                    const bool ok = take_r ? (ri < nR) : (wj < nW);
-                    const uint64_t v = ok ? skey(nxt) : 0;
-                    if (take_r) rkc = v;
-                    else wkc = v;
-                }
-            }
-#pragma unroll
-            for (int st = 0; st < MJ_ITEMS; ++st) {
-                if (match & (1u << st)) {
-                    const uint64_t sp = spay(nR + m_w[st]);
-                    emit(spay(m_r[st]), sp);
-                    if (dup & (1u << st)) {  // duplicate R keys: the rest of the group
-                        const uint64_t sk = skey(nR + m_w[st]);
-                        for (int64_t i = (int64_t)m_r[st] - 1; t.i0 + i >= 0 && rkey_at(i) == sk; --i)
-                            emit(rpay_at(i), sp);
-                    }
-                }
-            }
-#else
             int ri = lo, wj = k0 - lo;
             // the equal-key R group ending at ri-1: key gk, first index gs,
             // payload of its last element lrp (register-carried; an S tuple
@@ -529,8 +484,8 @@ __global__ void __launch_bounds__(MJ_THREADS) k_merge(const TileSplit* __restric
                 lrp = rpay_at(ri - 1);
                 while (t.i0 + gs - 1 >= 0 && rkey_at(gs - 1) == gk) --gs;
             }
-            KT rkc = ri < nR ? skey(ri) : 0;       // next R key
-            KT wkc = wj < nW ? skey(nR + wj) : 0;  // next S key
+            KT rkc = ri < nR ? rkey(ri) : 0;  // next R key
+            KT wkc = wj < nW ? wkey(wj) : 0;  // next S key
             for (int step = k0; step < k1; ++step) {
                 if (ri < nR && (wj >= nW || rkc <= wkc)) {
                     if (!gvalid || rkc != gk) {
@@ -538,40 +493,36 @@ __global__ void __launch_bounds__(MJ_THREADS) k_merge(const TileSplit* __restric
                         gs = ri;
                         gvalid = true;
                     }
-                    lrp = spay(ri);
+                    lrp = rpay(ri);
                     ++ri;
-                    if (ri < nR) rkc = skey(ri);
+                    if (ri < nR) rkc = rkey(ri);
                     continue;
                 }
                 if (gvalid && wkc == gk) {
-                    const uint64_t sp = spay(nR + wj);
+                    const uint64_t sp = wpay(wj);
                     emit(lrp, sp);
                     for (int i = ri - 2; i >= gs; --i) emit(rpay_at(i), sp);  // duplicate R keys
                 }
                 ++wj;
-                if (wj < nW) wkc = skey(nR + wj);
+                if (wj < nW) wkc = wkey(wj);
             }
-#endif
             my_pairs = e;
         }
         MJ_TS(4)
         if (MODE == 1) {
             const int64_t c = warp_sum((unsigned long long)my_pairs);
-            if ((tid & 31) == 0) warp_cnt[tid >> 5] = c;
+            if ((tid & 31) == 0) sm.warp_cnt[tid >> 5] = c;
             __syncthreads();
             if (tid == 0) {
                 int64_t sum = 0;
-                for (int w = 0; w < MJ_THREADS / 32; ++w) sum += warp_cnt[w];
+                for (int w = 0; w < MJ_THREADS / 32; ++w) sum += sm.warp_cnt[w];
                 tile_cnt[g] = sum;
             }
         }
-        __syncthreads();  // everyone is done with st[buf] before it is refilled
         MJ_TS(5)
         buf ^= 1;
-        t_cur = t_nxt;
-        t_nxt = t_after;
     }
-    if (MODE == 0 && cur_pair >= 0) flush_pair(sm, out_pairs, cur_pair, count, best, csum);
+    if (MODE == 0 && cur_pair >= 0) flush_pair<PK>(sm, out_pairs, cur_pair, count, best, csum);
 }
 
 // per-pair emitted counts from per-tile counts; tile offsets (exclusive scan)
@@ -654,17 +605,17 @@ static int launch_merge(const JoinWs& w, int swap, uint64_t* d_pairs, uint64_t* 
     static int per_sm = 0;
     if (per_sm == 0) {
         MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_merge<MODE, PK, K32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  (int)sizeof(MergeSmem)),
+                                                  (int)sizeof(MergeSmem<PK>)),
                              "smem attr"));
         MPSM_TRY(cuda_status(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge<MODE, PK, K32>, MJ_THREADS,
-                                                                           sizeof(MergeSmem)),
+                                                                           sizeof(MergeSmem<PK>)),
                              "occupancy"));
         if (per_sm < 1) per_sm = 1;
     }
     // persistent grid: exactly the resident CTAs
     const int grid = (int)std::min<int64_t>((int64_t)num_sms() * per_sm, mt);
     ProfScope ps(MODE == 0 ? "merge" : (MODE == 1 ? "merge_count" : "merge_emit"), st);
-    k_merge<MODE, PK, K32><<<grid, MJ_THREADS, sizeof(MergeSmem), st>>>(w.splits, w.total, swap, d_pairs, w.tile_cnt,
+    k_merge<MODE, PK, K32><<<grid, MJ_THREADS, sizeof(MergeSmem<PK>), st>>>(w.splits, w.total, swap, d_pairs, w.tile_cnt,
                                                                     emit_out, pi);
     return check_launch("k_merge");
 }

@@ -39,6 +39,9 @@ namespace seg {
 #ifndef MPSM_SEG_ITEMS
 #define MPSM_SEG_ITEMS 8
 #endif
+#ifndef MPSM_SEG_COUNT_PER_SM  // count CTAs (segments) per SM
+#define MPSM_SEG_COUNT_PER_SM 2
+#endif
 #ifndef MPSM_SEG_PP_BLOCKS
 #define MPSM_SEG_PP_BLOCKS 2
 #endif
@@ -138,15 +141,17 @@ __global__ void __launch_bounds__(THREADS) k_count(const uint64_t* __restrict__ 
 // base[g][d] = start(d) + sum_{g' < g} counts[g'][d]  (single CTA)
 __global__ void __launch_bounds__(MAX_BINS) k_scan(const uint32_t* __restrict__ counts, int G, int nbins,
                                                    int64_t* __restrict__ base) {
+    constexpr int B = 16;  // rows in flight per thread
     __shared__ int64_t tot[MAX_BINS];
     const int d = threadIdx.x;
+    const bool mine = d < nbins;
     int64_t run = 0;
-    if (d < nbins) {
-        for (int g = 0; g < G; ++g) {
-            const uint32_t c = counts[(size_t)g * nbins + d];
-            base[(size_t)g * nbins + d] = run;
-            run += c;
-        }
+    for (int g0 = 0; g0 < G; g0 += B) {
+        uint32_t c[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) c[u] = (mine && g0 + u < G) ? counts[(size_t)(g0 + u) * nbins + d] : 0;
+#pragma unroll
+        for (int u = 0; u < B; ++u) run += c[u];
     }
     tot[d] = run;
     __syncthreads();
@@ -156,9 +161,17 @@ __global__ void __launch_bounds__(MAX_BINS) k_scan(const uint32_t* __restrict__ 
         tot[d] += a;
         __syncthreads();
     }
-    const int64_t start = tot[d] - run;  // exclusive
-    if (d < nbins)
-        for (int g = 0; g < G; ++g) base[(size_t)g * nbins + d] += start;
+    run = tot[d] - run;  // digit start (exclusive)
+    for (int g0 = 0; g0 < G; g0 += B) {
+        uint32_t c[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) c[u] = (mine && g0 + u < G) ? counts[(size_t)(g0 + u) * nbins + d] : 0;
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            if (mine && g0 + u < G) base[(size_t)(g0 + u) * nbins + d] = run;
+            run += c[u];
+        }
+    }
 }
 
 // ---------------------------------------------------------------- scatter
@@ -534,16 +547,19 @@ template <int LAYOUT>
 static int pass(const uint64_t* in_k, const uint64_t* in_p, uint64_t* out_k, uint64_t* out_p, int64_t n,
                 Digit count_dig, Digit dig, int bits, const Ws& ws, uint64_t span_m1, unsigned long long* d_bad,
                 uint64_t pk_lower, int pk_pw, unsigned int* overflow, cudaStream_t st) {
+    // segments (count CTAs) are independent of the scatter grid: the tile
+    // prefixes make every tile self-contained
     const int G = std::min(grid_size<LAYOUT>(), max_grid());
-    const Segs sg = make_segs(n, G);
+    const int GC = std::min(num_sms() * MPSM_SEG_COUNT_PER_SM, max_grid());
+    const Segs sg = make_segs(n, GC);
     const int nbins = 1 << bits;
     {
         ProfScope ps("seg_count", st);
-        k_count<<<G, THREADS, 0, st>>>(in_k, sg, count_dig, nbins, ws.counts, ws.toffs, ws.ticket, span_m1,
-                                       d_bad);
+        k_count<<<GC, THREADS, 0, st>>>(in_k, sg, count_dig, nbins, ws.counts, ws.toffs, ws.ticket, span_m1,
+                                        d_bad);
     }
     MPSM_TRY(check_launch("k_count"));
-    k_scan<<<1, MAX_BINS, 0, st>>>(ws.counts, G, nbins, ws.base);
+    k_scan<<<1, MAX_BINS, 0, st>>>(ws.counts, GC, nbins, ws.base);
     MPSM_TRY(check_launch("k_scan"));
     // digit of a staged value: records staged by the SP pass carry the key
     // above the payload bits
