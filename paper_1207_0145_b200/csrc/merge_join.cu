@@ -193,12 +193,14 @@ __global__ void __launch_bounds__(1024) k_tile_scan(PairWin* __restrict__ win, i
     if (threadIdx.x == 0) *total = carry;
 }
 
-// merge path: number of R elements among the first k of merge(R, W), ties R first
+// merge path: number of R elements among the first k of merge(R, W), ties R
+// first, searched among R indices [lo, hi] (a coarse bracket)
 template <bool PK>
-__device__ __forceinline__ int64_t merge_path(const uint64_t* __restrict__ rk, int64_t nr,
-                                              const uint64_t* __restrict__ wk, int64_t nw, int64_t k,
-                                              const PackInfo& pi) {
-    int64_t lo = k > nw ? k - nw : 0, hi = k < nr ? k : nr;
+__device__ __forceinline__ int64_t merge_path_in(const uint64_t* __restrict__ rk, int64_t nr,
+                                                 const uint64_t* __restrict__ wk, int64_t nw, int64_t k, int64_t lo,
+                                                 int64_t hi, const PackInfo& pi) {
+    lo = max(lo, k > nw ? k - nw : (int64_t)0);
+    hi = min(hi, k < nr ? k : nr);
     while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;
         if (key_of<PK>(rk, mid, pi) <= key_of<PK>(wk, k - 1 - mid, pi)) lo = mid + 1;
@@ -207,13 +209,8 @@ __device__ __forceinline__ int64_t merge_path(const uint64_t* __restrict__ rk, i
     return lo;
 }
 
-template <bool PK>
-__global__ void k_partition(const mpsm_run_t* __restrict__ priv, const mpsm_run_t* __restrict__ pub, int n_pub,
-                            const PairWin* __restrict__ win, int npairs, const int64_t* __restrict__ total,
-                            TileSplit* __restrict__ splits, PackInfo pi) {
-    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= *total) return;
-    // pair of this tile: last p with tile_base <= g
+// pair of global tile g: last p with tile_base <= g and tiles > 0
+__device__ __forceinline__ int pair_of_tile(const PairWin* __restrict__ win, int npairs, int64_t g) {
     int lo = 0, hi = npairs - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -222,16 +219,49 @@ __global__ void k_partition(const mpsm_run_t* __restrict__ priv, const mpsm_run_
     }
     int p = lo;
     while (win[p].tiles == 0 || win[p].tile_base + win[p].tiles <= g) --p;
+    return p;
+}
+
+// Tile boundaries in two levels: k_part_coarse places every PART_STRIDE-th
+// tile start of a pair by a full merge-path search; k_partition places each
+// tile start inside its coarse bracket (log2(PART_STRIDE * MJ_TILE) steps
+// instead of log2(|R|)); k_split_fill closes each tile at its successor's
+// start.  One search per boundary.
+constexpr int PART_STRIDE = 32;
+
+template <bool PK>
+__global__ void k_part_coarse(const mpsm_run_t* __restrict__ priv, const mpsm_run_t* __restrict__ pub, int n_pub,
+                              const PairWin* __restrict__ win, int npairs, const int64_t* __restrict__ total,
+                              int64_t* __restrict__ coarse, PackInfo pi) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= *total) return;
+    const int p = pair_of_tile(win, npairs, g);
+    const PairWin w = win[p];
+    const int64_t local = g - w.tile_base;
+    if (local % PART_STRIDE) return;
+    const mpsm_run_t r = priv[p / n_pub];
+    const mpsm_run_t s = pub[p % n_pub];
+    const int64_t nw = w.end - w.start;
+    coarse[g] = merge_path_in<PK>(r.keys, r.n, s.keys + w.start, nw, local * MJ_TILE, 0, r.n, pi);
+}
+
+template <bool PK>
+__global__ void k_partition(const mpsm_run_t* __restrict__ priv, const mpsm_run_t* __restrict__ pub, int n_pub,
+                            const PairWin* __restrict__ win, int npairs, const int64_t* __restrict__ total,
+                            const int64_t* __restrict__ coarse, TileSplit* __restrict__ splits, PackInfo pi) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= *total) return;
+    const int p = pair_of_tile(win, npairs, g);
     const mpsm_run_t r = priv[p / n_pub];
     const mpsm_run_t s = pub[p % n_pub];
     const PairWin w = win[p];
-    const uint64_t* wk = s.keys + w.start;
     const int64_t nw = w.end - w.start;
-    const int64_t L = r.n + nw;
-    const int64_t k0 = (g - w.tile_base) * MJ_TILE;
-    const int64_t k1 = (k0 + MJ_TILE < L) ? k0 + MJ_TILE : L;
-    const int64_t i0 = merge_path<PK>(r.keys, r.n, wk, nw, k0, pi);
-    const int64_t i1 = merge_path<PK>(r.keys, r.n, wk, nw, k1, pi);
+    const int64_t local = g - w.tile_base;
+    const int64_t c0 = local - local % PART_STRIDE, c1 = c0 + PART_STRIDE;
+    const int64_t lo = coarse[w.tile_base + c0];
+    const int64_t hi = c1 < w.tiles ? coarse[w.tile_base + c1] : r.n;
+    const int64_t k0 = local * MJ_TILE;
+    const int64_t i0 = (local == c0) ? lo : merge_path_in<PK>(r.keys, r.n, s.keys + w.start, nw, k0, lo, hi, pi);
     TileSplit t;
     t.rk = r.keys;
     t.rp = r.pays;
@@ -239,11 +269,28 @@ __global__ void k_partition(const mpsm_run_t* __restrict__ priv, const mpsm_run_
     t.wp = s.pays;
     t.i0 = i0;
     t.w0 = w.start + (k0 - i0);
-    t.nR = (int32_t)(i1 - i0);
-    t.nW = (int32_t)((k1 - i1) - (k0 - i0));
+    t.nR = 0;
+    t.nW = 0;
     t.pair = p;
     t.pad = 0;
     splits[g] = t;
+}
+
+__global__ void k_split_fill(const mpsm_run_t* __restrict__ priv, int n_pub, const PairWin* __restrict__ win,
+                             const int64_t* __restrict__ total, TileSplit* __restrict__ splits) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n = *total;
+    if (g >= n) return;
+    TileSplit& t = splits[g];
+    const PairWin w = win[t.pair];
+    const int64_t nr = priv[t.pair / n_pub].n;
+    const int64_t L = nr + (w.end - w.start);
+    const int64_t local = g - w.tile_base;
+    const int64_t k0 = local * MJ_TILE;
+    const int64_t k1 = min(k0 + MJ_TILE, L);
+    const int64_t i1 = (local + 1 < w.tiles) ? splits[g + 1].i0 : nr;
+    t.nR = (int32_t)(i1 - t.i0);
+    t.nW = (int32_t)((k1 - i1) - (k0 - t.i0));
 }
 
 // Tile staging.  A stage holds the 16-B aligned superset of the tile's R
@@ -641,8 +688,11 @@ static int join_pairs_impl(const mpsm_run_t* priv, int n_priv, const mpsm_run_t*
     MPSM_TRY(check_launch("k_tile_scan"));
     {
         ProfScope ps("merge_partition", st);
-        k_partition<PK><<<(unsigned)((mt + 255) / 256), 256, 0, st>>>(w.d_priv, w.d_pub, n_pub, w.win, npairs,
-                                                                       w.total, w.splits, pi);
+        const unsigned pg = (unsigned)((mt + 255) / 256);
+        k_part_coarse<PK><<<pg, 256, 0, st>>>(w.d_priv, w.d_pub, n_pub, w.win, npairs, w.total, w.tile_cnt, pi);
+        k_partition<PK><<<pg, 256, 0, st>>>(w.d_priv, w.d_pub, n_pub, w.win, npairs, w.total, w.tile_cnt, w.splits,
+                                            pi);
+        k_split_fill<<<pg, 256, 0, st>>>(w.d_priv, n_pub, w.win, w.total, w.splits);
     }
     MPSM_TRY(check_launch("k_partition"));
     const bool k32 = PK && (64 - pi.pw) <= 32;  // packed keys fit 32 bits
