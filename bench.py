@@ -323,6 +323,18 @@ def impl_ours(args):
             cpu = {"value": None, "unit": "tuples/s", "cores": cpu_threads(), "kind": "reference",
                    "sample": f"failed: {exc!r}"}
 
+    # DRAM bytes per scatter launch from the committed ncu --set full capture
+    # (tools/ncu_traffic.py over one bench step's k_scatter launches)
+    traffic = traffic_detail = None
+    tfile = os.path.join(ROOT, "profiles", "traffic_scatter.json")
+    if packed and args.config == "cfg2" and os.path.exists(tfile):
+        with open(tfile) as f:
+            tj = json.load(f)
+        traffic = tj["dram_bytes_per_launch"]
+        traffic_detail = {"unit": "bytes per launch (dram read + write)",
+                          "algorithmic_bytes_per_launch": tj["algorithmic_bytes_per_launch"],
+                          "ratio": tj["traffic_over_algorithmic"], "source": "profiles/traffic_scatter.json"}
+
     line = {
         "metric": METRIC, "value": value, "unit": "tuples/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -335,7 +347,8 @@ def impl_ours(args):
         "phase_ms": {k: 1e3 * v / args.steps for k, v in phase.items()},
         "roofline": {"bound": "hbm", "kernel": "seg::k_scatter (radix scatter pass)", "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
-                     "traffic": None, "algorithmic_bytes_per_tuple_per_sort": per_tuple,
+                     "traffic": traffic, "traffic_detail": traffic_detail,
+                     "algorithmic_bytes_per_tuple_per_sort": per_tuple,
                      "layout": "packed 8-B records" if packed else "(key, payload) pairs", "passes_per_sort": passes,
                      "launches": os_n, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
         "step_canonical_gbs": step_gbs,

@@ -38,8 +38,17 @@
 
 namespace mpsm {
 
-constexpr int MJ_THREADS = 256;
-constexpr int MJ_ITEMS = 9;  // odd: 64-bit smem accesses at stride ITEMS are conflict-free
+#ifndef MPSM_MJ_THREADS
+#define MPSM_MJ_THREADS 128
+#endif
+#ifndef MPSM_MJ_ITEMS
+#define MPSM_MJ_ITEMS 17
+#endif
+#ifndef MPSM_MJ_BLOCKS
+#define MPSM_MJ_BLOCKS 6
+#endif
+constexpr int MJ_THREADS = MPSM_MJ_THREADS;
+constexpr int MJ_ITEMS = MPSM_MJ_ITEMS;  // odd: 64-bit smem accesses at stride ITEMS are conflict-free
 constexpr int MJ_TILE = MJ_THREADS * MJ_ITEMS;
 
 struct PackInfo {
@@ -408,7 +417,7 @@ __device__ long long g_mj_ts[1 << 20][6];
 // product of duplicate key groups.  Per-thread accumulators are reduced per
 // CTA and flushed with one atomic per (pair, CTA).
 template <int MODE, bool PK, bool K32 = false>
-__global__ void __launch_bounds__(MJ_THREADS, PK ? 4 : 2) k_merge(const TileSplit* __restrict__ splits,
+__global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(const TileSplit* __restrict__ splits,
                                                                  const int64_t* __restrict__ total, int swap,
                                                                  uint64_t* __restrict__ out_pairs,
                                                                  int64_t* __restrict__ tile_cnt,

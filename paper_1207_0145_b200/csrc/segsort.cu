@@ -138,39 +138,34 @@ __global__ void __launch_bounds__(THREADS) k_count(const uint64_t* __restrict__ 
 }
 
 // ------------------------------------------------------------------- scan
-// base[g][d] = start(d) + sum_{g' < g} counts[g'][d]  (single CTA)
-__global__ void __launch_bounds__(MAX_BINS) k_scan(const uint32_t* __restrict__ counts, int G, int nbins,
-                                                   int64_t* __restrict__ base) {
-    constexpr int B = 16;  // rows in flight per thread
-    __shared__ int64_t tot[MAX_BINS];
-    const int d = threadIdx.x;
+// base[g][d] = sum_{g' < g} counts[g'][d] (segment-relative to digit d's
+// start) and dtot[d] = digit d's total.  One CTA per 32 digits; thread
+// (row group r, digit lane) sums its group of segments, the groups are
+// scanned through shared memory.
+constexpr int SCAN_GROUPS = 32;
+
+__global__ void __launch_bounds__(32 * SCAN_GROUPS) k_scan(const uint32_t* __restrict__ counts, int G, int nbins,
+                                                         int64_t* __restrict__ base, int64_t* __restrict__ dtot) {
+    __shared__ int64_t part[SCAN_GROUPS][33];
+    const int dl = threadIdx.x & 31, r = threadIdx.x >> 5;
+    const int d = blockIdx.x * 32 + dl;
+    const int rpg = (G + SCAN_GROUPS - 1) / SCAN_GROUPS;
+    const int g0 = r * rpg, g1 = min(g0 + rpg, G);
     const bool mine = d < nbins;
-    int64_t run = 0;
-    for (int g0 = 0; g0 < G; g0 += B) {
-        uint32_t c[B];
-#pragma unroll
-        for (int u = 0; u < B; ++u) c[u] = (mine && g0 + u < G) ? counts[(size_t)(g0 + u) * nbins + d] : 0;
-#pragma unroll
-        for (int u = 0; u < B; ++u) run += c[u];
-    }
-    tot[d] = run;
+    int64_t sum = 0;
+#pragma unroll 8
+    for (int g = g0; g < g1; ++g) sum += mine ? counts[(size_t)g * nbins + d] : 0;
+    part[r][dl] = sum;
     __syncthreads();
-    for (int off = 1; off < MAX_BINS; off <<= 1) {
-        const int64_t a = d >= off ? tot[d - off] : 0;
-        __syncthreads();
-        tot[d] += a;
-        __syncthreads();
-    }
-    run = tot[d] - run;  // digit start (exclusive)
-    for (int g0 = 0; g0 < G; g0 += B) {
-        uint32_t c[B];
-#pragma unroll
-        for (int u = 0; u < B; ++u) c[u] = (mine && g0 + u < G) ? counts[(size_t)(g0 + u) * nbins + d] : 0;
-#pragma unroll
-        for (int u = 0; u < B; ++u) {
-            if (mine && g0 + u < G) base[(size_t)(g0 + u) * nbins + d] = run;
-            run += c[u];
-        }
+    int64_t run = 0;
+    for (int q = 0; q < r; ++q) run += part[q][dl];
+    if (!mine) return;
+    if (r == SCAN_GROUPS - 1) dtot[d] = run + sum;
+#pragma unroll 8
+    for (int g = g0; g < g1; ++g) {  // second read hits L2
+        const uint32_t c = counts[(size_t)g * nbins + d];
+        base[(size_t)g * nbins + d] = run;
+        run += c;
     }
 }
 
@@ -262,8 +257,8 @@ template <int LAYOUT, bool HI>
 __global__ void __launch_bounds__(THREADS, LAYOUT == PP ? MPSM_SEG_PP_BLOCKS : 1) k_scatter(
     const uint64_t* __restrict__ in_k, const uint64_t* __restrict__ in_p, uint64_t* __restrict__ out_k,
     uint64_t* __restrict__ out_p, Segs sg, Digit dig, Digit odig, int nbins, const int64_t* __restrict__ base,
-    const uint32_t* __restrict__ toffs, unsigned int* __restrict__ ticket, uint64_t pk_lower, int pk_pw,
-    unsigned int* __restrict__ overflow, bool lane_ordered) {
+    const uint32_t* __restrict__ toffs, const int64_t* __restrict__ dtot, unsigned int* __restrict__ ticket,
+    uint64_t pk_lower, int pk_pw, unsigned int* __restrict__ overflow, bool lane_ordered) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem<LAYOUT>& sm = *reinterpret_cast<Smem<LAYOUT>*>(smem_raw);
     constexpr int NARR = Smem<LAYOUT>::NARR;
@@ -279,6 +274,21 @@ __global__ void __launch_bounds__(THREADS, LAYOUT == PP ? MPSM_SEG_PP_BLOCKS : 1
     const uint32_t half = (warp & 1) ? 0x4432u : 0x4410u;  // byte_perm: my 16-bit field
     for (int i = tid; i < ROWS * MAX_BINS / 4; i += THREADS)
         reinterpret_cast<uint4*>(&sm.hist[0][0])[i] = make_uint4(0, 0, 0, 0);
+    // start of my digit's output region: exclusive scan of the digit totals
+    int64_t dstart;
+    {
+        const int64_t v = mine ? dtot[tid] : 0;
+        int64_t incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        if (lane == 31) sm.gdelta[warp] = incl;  // gdelta is free until the first tile
+        __syncthreads();
+        dstart = incl - v;
+        for (int w = 0; w < warp; ++w) dstart += sm.gdelta[w];
+    }
 
     // thread 0: one mbarrier phase brings tile t's tuples, its digit
     // prefixes and its segment's digit bases into buffer bb
@@ -395,7 +405,7 @@ __global__ void __launch_bounds__(THREADS, LAYOUT == PP ? MPSM_SEG_PP_BLOCKS : 1
                 sm.hist[r][tid] = run * 0x10001u + sh;
                 run += (col[r] + sh) >> 16;
             }
-            sm.gdelta[tid] = sm.sbase[b][tid] + sm.toffs[b][tid] - (int64_t)toff;
+            sm.gdelta[tid] = dstart + sm.sbase[b][tid] + sm.toffs[b][tid] - (int64_t)toff;
         }
         if (LAYOUT == SP) {
             uint64_t ovf = 0;
@@ -486,6 +496,7 @@ struct Ws {
     uint32_t* counts;  // [G][MAX_BINS]
     int64_t* base;     // [G][MAX_BINS]
     uint32_t* toffs;   // [tiles][MAX_BINS]
+    int64_t* dtot;     // [MAX_BINS]
     unsigned int* ticket;
 };
 
@@ -517,7 +528,8 @@ static size_t ntiles(int64_t n) { return (size_t)((n + TILE - 1) / TILE); }
 static size_t ws_bytes(int64_t n) {
     const int G = max_grid();
     return align_up(sizeof(uint32_t) * (size_t)G * MAX_BINS) + align_up(sizeof(int64_t) * (size_t)G * MAX_BINS) +
-           align_up(sizeof(uint32_t) * ntiles(n) * MAX_BINS) + align_up(sizeof(unsigned int));
+           align_up(sizeof(uint32_t) * ntiles(n) * MAX_BINS) + align_up(sizeof(int64_t) * MAX_BINS) +
+           align_up(sizeof(unsigned int));
 }
 
 static bool carve(void* ws, size_t bytes, int64_t n, Ws* o) {
@@ -526,6 +538,7 @@ static bool carve(void* ws, size_t bytes, int64_t n, Ws* o) {
     o->counts = c.take<uint32_t>((size_t)G * MAX_BINS);
     o->base = c.take<int64_t>((size_t)G * MAX_BINS);
     o->toffs = c.take<uint32_t>(ntiles(n) * MAX_BINS);
+    o->dtot = c.take<int64_t>(MAX_BINS);
     o->ticket = c.take<unsigned int>(1);
     return c.ok;
 }
@@ -559,7 +572,7 @@ static int pass(const uint64_t* in_k, const uint64_t* in_p, uint64_t* out_k, uin
                                         d_bad);
     }
     MPSM_TRY(check_launch("k_count"));
-    k_scan<<<1, MAX_BINS, 0, st>>>(ws.counts, GC, nbins, ws.base);
+    k_scan<<<(nbins + 31) / 32, 32 * SCAN_GROUPS, 0, st>>>(ws.counts, GC, nbins, ws.base, ws.dtot);
     MPSM_TRY(check_launch("k_scan"));
     // digit of a staged value: records staged by the SP pass carry the key
     // above the payload bits
@@ -572,10 +585,10 @@ static int pass(const uint64_t* in_k, const uint64_t* in_p, uint64_t* out_k, uin
         const bool lo = lane_ordered_atomics();
         if (hi)
             k_scatter<LAYOUT, true><<<G, THREADS, sizeof(Smem<LAYOUT>), st>>>(
-                in_k, in_p, out_k, out_p, sg, dig, odig, nbins, ws.base, ws.toffs, ws.ticket, pk_lower, pk_pw, overflow, lo);
+                in_k, in_p, out_k, out_p, sg, dig, odig, nbins, ws.base, ws.toffs, ws.dtot, ws.ticket, pk_lower, pk_pw, overflow, lo);
         else
             k_scatter<LAYOUT, false><<<G, THREADS, sizeof(Smem<LAYOUT>), st>>>(
-                in_k, in_p, out_k, out_p, sg, dig, odig, nbins, ws.base, ws.toffs, ws.ticket, pk_lower, pk_pw, overflow, lo);
+                in_k, in_p, out_k, out_p, sg, dig, odig, nbins, ws.base, ws.toffs, ws.dtot, ws.ticket, pk_lower, pk_pw, overflow, lo);
     }
     return check_launch("k_scatter");
 }
