@@ -68,8 +68,8 @@ int mpsm_device_init(int device);
 /* number of kernels this library launched (process-wide counter) */
 uint64_t mpsm_launch_count(void);
 /* per-kernel CUDA-event timing: enable (and reset) / read the summed device
- * time and launch count of one kernel family ("onesweep", "upfront_hist",
- * "scatter", "radix_histogram", "merge", "merge_partition", ...) */
+ * time and launch count of one kernel family ("seg_scatter", "seg_count",
+ * "seg_scatter_sp", "seg_scatter_pp", "merge", "merge_partition", ...) */
 int mpsm_profile_enable(int on);
 int mpsm_profile_read(const char* name, double* total_ms, uint64_t* launches);
 
@@ -78,12 +78,15 @@ int mpsm_profile_read(const char* name, double* total_ms, uint64_t* launches);
  * sorter.sort_run_with_stats (sorter.py:91-100): sort (key, payload) pairs
  * by key.  Reads in_*, leaves the sorted run in out_* (in may equal out);
  * tmp_* is a ping-pong buffer of n elements.  LSD radix over the width_bits
- * significant bits of (key - lower) (onesweep: one key-histogram sweep, then
- * one decoupled-look-back scatter pass per digit).  Keys outside
- * [lower, lower + span_m1] are reported through *d_bad (atomicMin of the
- * index; initialise to UINT64_MAX) -- the reference returns -1 from the kernel
- * and raises DomainError (sorter.py:97-98).  Like the reference, the order of
- * payloads among equal keys is unspecified. */
+ * significant bits of (key - lower), digits of <= 9 bits; per digit a count
+ * sweep (per-tile digit prefixes) and a scatter pass that takes tiles in
+ * global order (segsort.cu).  Keys outside [lower, lower + span_m1] are
+ * reported through *d_bad (atomicMin of the index; initialise to UINT64_MAX)
+ * -- the reference returns -1 from the kernel and raises DomainError
+ * (sorter.py:97-98).  The sort is stable (equal keys keep their input
+ * order); callers must not rely on it -- the reference's order among equal
+ * keys is unspecified.  The workspace grows with n (4 B per 512 digits per
+ * 4096-tuple tile). */
 int mpsm_sort_workspace_bytes(int64_t n, int width_bits, size_t* bytes);
 /* number of scatter passes (digits) the sort uses for width_bits */
 int mpsm_sort_pass_count(int width_bits);

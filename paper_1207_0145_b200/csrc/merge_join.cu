@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
             }
             KT rkc = ri < nR ? rkey(ri) : 0;  // next R key
             KT wkc = wj < nW ? wkey(wj) : 0;  // next S key
-            for (int step = k0; step < k1; ++step) {
+            auto step = [&]() {
                 if (ri < nR && (wj >= nW || rkc <= wkc)) {
                     if (!gvalid || rkc != gk) {
                         gk = rkc;
@@ -552,7 +552,7 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                     lrp = rpay(ri);
                     ++ri;
                     if (ri < nR) rkc = rkey(ri);
-                    continue;
+                    return;
                 }
                 if (gvalid && wkc == gk) {
                     const uint64_t sp = wpay(wj);
@@ -561,7 +561,8 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                 }
                 ++wj;
                 if (wj < nW) wkc = wkey(wj);
-            }
+            };
+            for (int st = k0; st < k1; ++st) step();
             my_pairs = e;
         }
         MJ_TS(4)
