@@ -42,18 +42,34 @@ namespace seg {
 #ifndef MPSM_SEG_COUNT_PER_SM  // count CTAs (segments) per SM
 #define MPSM_SEG_COUNT_PER_SM 2
 #endif
-#ifndef MPSM_SEG_PP_BLOCKS
-#define MPSM_SEG_PP_BLOCKS 2
+#ifndef MPSM_SEG_PP_BLOCKS  // record-pass scatter CTAs per SM
+#define MPSM_SEG_PP_BLOCKS 1
+#endif
+#ifndef MPSM_SEG_PP_ITEMS  // record-pass tuples per thread per tile
+#define MPSM_SEG_PP_ITEMS 16
+#endif
+#ifndef MPSM_SEG_PP_STAGES  // record-pass tile buffers in shared memory
+#define MPSM_SEG_PP_STAGES 2
 #endif
 constexpr int THREADS = MPSM_SEG_THREADS;
 constexpr int ITEMS = MPSM_SEG_ITEMS;
-constexpr int TILE = THREADS * ITEMS;  // 4096 tuples
+constexpr int TILE = THREADS * ITEMS;  // 4096 tuples: the count chunk and the smallest scatter tile
 constexpr int WARPS = THREADS / 32;
 constexpr int MAX_BITS = 9;
 constexpr int MAX_BINS = 1 << MAX_BITS;
 constexpr int MAX_PASSES = 8;
 
 enum Layout { SS = 0, SP = 1, PP = 2 };
+
+// per-layout scatter shape: tuples per thread, tile, tile buffers, CTAs/SM
+template <int LAYOUT>
+struct LCfg {
+    static constexpr int ITEMS_L = LAYOUT == PP ? MPSM_SEG_PP_ITEMS : ITEMS;
+    static constexpr int TILE_L = THREADS * ITEMS_L;
+    static constexpr int NST = LAYOUT == PP ? MPSM_SEG_PP_STAGES : 2;
+    static constexpr int BLOCKS = LAYOUT == PP ? MPSM_SEG_PP_BLOCKS : 1;
+    static_assert(TILE_L % TILE == 0, "scatter tiles are whole count chunks");
+};
 
 struct Plan {
     int npasses;
@@ -95,11 +111,13 @@ struct Segs {
 // counts[g][d] for segment g, and for every tile t of the segment the
 // segment-local exclusive prefix toffs[t][d] (digit d's tuples in earlier
 // tiles of the segment); optional domain check (first pass)
+template <int CPT>  // count chunks (TILE tuples) per scatter tile
 __global__ void __launch_bounds__(THREADS) k_count(const uint64_t* __restrict__ in, Segs sg, Digit dig, int nbins,
                                                    uint32_t* __restrict__ counts, uint32_t* __restrict__ toffs,
                                                    unsigned int* __restrict__ ticket, uint64_t span_m1,
                                                    unsigned long long* __restrict__ d_bad) {
-    __shared__ uint32_t h[2][MAX_BINS];  // tile k counts into h[k & 1]
+    constexpr int STILE = CPT * TILE;
+    __shared__ uint32_t h[2][MAX_BINS];  // scatter tile k counts into h[k & 1]
     const int tid = threadIdx.x;
     h[0][tid] = 0;
     h[1][tid] = 0;
@@ -108,31 +126,34 @@ __global__ void __launch_bounds__(THREADS) k_count(const uint64_t* __restrict__ 
     const int64_t b = sg.begin(blockIdx.x), e = sg.end(blockIdx.x);
     uint32_t run = 0;  // thread d: digit d's count in the tiles so far
     uint64_t v[ITEMS], w[ITEMS];
-    auto load = [&](uint64_t* x, int64_t t0) {
+    auto load = [&](uint64_t* x, int64_t c0) {
 #pragma unroll
         for (int u = 0; u < ITEMS; ++u) {
-            const int64_t i = t0 + u * THREADS + tid;
+            const int64_t i = c0 + u * THREADS + tid;
             x[u] = i < e ? ld_stream(in + i) : 0;
         }
     };
     if (b < e) load(v, b);
-    int k = 0;
-    for (int64_t t0 = b; t0 < e; t0 += TILE, k ^= 1) {
-        if (t0 + TILE < e) load(w, t0 + TILE);  // next tile in flight during this one
+    int k = 0, c = 0;
+    for (int64_t c0 = b; c0 < e; c0 += TILE) {
+        if (c0 + TILE < e) load(w, c0 + TILE);  // next chunk in flight during this one
 #pragma unroll
         for (int u = 0; u < ITEMS; ++u) {
-            const int64_t i = t0 + u * THREADS + tid;
+            const int64_t i = c0 + u * THREADS + tid;
             if (i < e) {
                 if (d_bad && v[u] - dig.lower > span_m1) atomicMin(d_bad, (unsigned long long)i);
                 atomicAdd(&h[k][dig(v[u])], 1u);
             }
         }
-        __syncthreads();  // h[k] complete; the next tile counts into h[k ^ 1]
-        if (tid < nbins) toffs[(size_t)(t0 / TILE) * MAX_BINS + tid] = run;
-        run += h[k][tid];
-        h[k][tid] = 0;
 #pragma unroll
         for (int u = 0; u < ITEMS; ++u) v[u] = w[u];
+        if (++c < CPT && c0 + TILE < e) continue;
+        __syncthreads();  // h[k] complete; the next tile counts into h[k ^ 1]
+        if (tid < nbins) toffs[(size_t)((c0 - (c - 1) * TILE) / STILE) * MAX_BINS + tid] = run;
+        run += h[k][tid];
+        h[k][tid] = 0;
+        k ^= 1;
+        c = 0;
     }
     if (tid < nbins) counts[(size_t)blockIdx.x * nbins + tid] = run;
 }
@@ -176,17 +197,18 @@ __global__ void __launch_bounds__(32 * SCAN_GROUPS) k_scan(const uint32_t* __res
 template <int LAYOUT>
 struct Smem {
     static constexpr int NARR = (LAYOUT == PP) ? 1 : 2;
-    uint64_t buf[2][NARR][TILE + 2];     // double-buffered tile data (+1 slot of alignment shift); staging in place
+    static constexpr int TL = LCfg<LAYOUT>::TILE_L, NST = LCfg<LAYOUT>::NST;
+    uint64_t buf[NST][NARR][TL + 2];     // tile buffers (+1 slot of alignment shift); staging in place
     uint32_t hist[WARPS / 2][MAX_BINS];  // [warp pair][digit]
     int64_t gdelta[MAX_BINS];            // output index - staging index, per digit
-    uint32_t toffs[2][MAX_BINS];         // per buffer: the tile's segment-local digit prefixes
-    int64_t sbase[2][MAX_BINS];          // per buffer: its segment's digit bases
+    uint32_t toffs[NST][MAX_BINS];       // per buffer: the tile's segment-local digit prefixes
+    int64_t sbase[NST][MAX_BINS];        // per buffer: its segment's digit bases
     uint32_t wtot[WARPS];                // digit-scan carries
-    int64_t tile[2];                     // per buffer: tile index
-    uint64_t bar[2];                     // bulk-copy completion, per buffer
+    int64_t tile[NST];                   // per buffer: tile index
+    uint64_t bar[NST];                   // bulk-copy completion, per buffer
 };
 static_assert(THREADS == MAX_BINS, "the digit scan gives each thread one digit");
-static_assert(WARPS % 2 == 0 && WARPS <= 32 && 32 * ITEMS < 65536 && TILE < 65536, "16-bit histogram fields");
+static_assert(WARPS % 2 == 0 && WARPS <= 32, "two warps per histogram word");
 
 // lanes of the warp holding the same digit (fallback ranking: 9 ballots)
 __device__ __forceinline__ unsigned ballot_peers(uint32_t d, unsigned vmask) {
@@ -254,7 +276,7 @@ __device__ __forceinline__ uint32_t rec_digit(uint64_t v, const Digit& d) {
 // Where the probe fails the peers come from ballots (ballot_peers).
 // HI: the staged records' digit lies in the high word (PP/SP with pw >= 32).
 template <int LAYOUT, bool HI>
-__global__ void __launch_bounds__(THREADS, LAYOUT == PP ? MPSM_SEG_PP_BLOCKS : 1) k_scatter(
+__global__ void __launch_bounds__(THREADS, LCfg<LAYOUT>::BLOCKS) k_scatter(
     const uint64_t* __restrict__ in_k, const uint64_t* __restrict__ in_p, uint64_t* __restrict__ out_k,
     uint64_t* __restrict__ out_p, Segs sg, Digit dig, Digit odig, int nbins, const int64_t* __restrict__ base,
     const uint32_t* __restrict__ toffs, const int64_t* __restrict__ dtot, unsigned int* __restrict__ ticket,
@@ -263,9 +285,11 @@ __global__ void __launch_bounds__(THREADS, LAYOUT == PP ? MPSM_SEG_PP_BLOCKS : 1
     Smem<LAYOUT>& sm = *reinterpret_cast<Smem<LAYOUT>*>(smem_raw);
     constexpr int NARR = Smem<LAYOUT>::NARR;
     constexpr int ROWS = WARPS / 2;
+    constexpr int IT = LCfg<LAYOUT>::ITEMS_L, TL = LCfg<LAYOUT>::TILE_L, NST = LCfg<LAYOUT>::NST;
+    static_assert(32 * IT < 65536 && TL < 65536, "16-bit histogram fields");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt = lanemask_lt();
-    const int64_t T = (sg.n + TILE - 1) / TILE, tiles_per_seg = sg.seg_len / TILE;
+    const int64_t T = (sg.n + TL - 1) / TL, tiles_per_seg = sg.seg_len / TL;
     if ((int64_t)blockIdx.x >= T) return;
     const int offk = (int)(((uintptr_t)in_k >> 3) & 1), offp = NARR == 2 ? (int)(((uintptr_t)in_p >> 3) & 1) : 0;
     const bool mine = tid < nbins;  // the digit this thread scans
@@ -293,8 +317,8 @@ __global__ void __launch_bounds__(THREADS, LAYOUT == PP ? MPSM_SEG_PP_BLOCKS : 1
     // thread 0: one mbarrier phase brings tile t's tuples, its digit
     // prefixes and its segment's digit bases into buffer bb
     auto fetch = [&](int bb, int64_t t) {
-        const int64_t t0 = t * TILE;
-        const int cnt = (int)min((int64_t)TILE, sg.n - t0);
+        const int64_t t0 = t * TL;
+        const int cnt = (int)min((int64_t)TL, sg.n - t0);
         sm.tile[bb] = t;
         unsigned bk = tile_plain(sm.buf[bb][0], in_k + t0, offk, cnt), bp = 0;
         if (NARR == 2) bp = tile_plain(sm.buf[bb][NARR - 1], in_p + t0, offp, cnt);
@@ -310,12 +334,16 @@ __global__ void __launch_bounds__(THREADS, LAYOUT == PP ? MPSM_SEG_PP_BLOCKS : 1
     // are neighbours and their runs of one digit land next to each other in
     // the output (a CTA sweeping its own contiguous segment instead halves
     // the write bandwidth: tools/scatter_pattern_bench.cu)
-    int64_t tnext = 0;  // thread 0: the tile after the one being fetched
+    int64_t tnext = 0;  // thread 0: the next tile to fetch (ticket taken a tile earlier)
     if (tid == 0) {
-        mbar_init(&sm.bar[0], 1);
-        mbar_init(&sm.bar[1], 1);
+        for (int q = 0; q < NST; ++q) mbar_init(&sm.bar[q], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fetch(0, blockIdx.x);
+        for (int q = 1; q < NST - 1; ++q) {
+            const int64_t tq = (int64_t)gridDim.x + atomicAdd(ticket, 1u);
+            if (tq < T) fetch(q, tq);
+            else sm.tile[q] = T;
+        }
         tnext = (int64_t)gridDim.x + atomicAdd(ticket, 1u);
     }
     unsigned par = 0;
@@ -326,44 +354,45 @@ __global__ void __launch_bounds__(THREADS, LAYOUT == PP ? MPSM_SEG_PP_BLOCKS : 1
         if (t >= T) break;
         SEG_TS(0)
         if (tid == 0) {
+            const int nb = (b + NST - 1) % NST;  // the buffer of the previous tile
             if (tnext < T) {
-                fence_proxy_async_smem();  // buf[b^1] was staged through by generic stores
-                fetch(b ^ 1, tnext);
+                fence_proxy_async_smem();  // buf[nb] was staged through by generic stores
+                fetch(nb, tnext);
                 tnext = (int64_t)gridDim.x + atomicAdd(ticket, 1u);  // used one tile later
             } else {
-                sm.tile[b ^ 1] = T;  // no more tiles
+                sm.tile[nb] = T;  // no more tiles
             }
         }
         mbar_wait(&sm.bar[b], (par >> b) & 1u);
         par ^= 1u << b;
         SEG_TS(1)
-        const int64_t t0 = t * TILE;
-        const int cnt = (int)min((int64_t)TILE, sg.n - t0);
-        const int wb = warp * (32 * ITEMS);
+        const int64_t t0 = t * TL;
+        const int cnt = (int)min((int64_t)TL, sg.n - t0);
+        const int wb = warp * (32 * IT);
         const int lim = cnt - wb - lane;  // item k is valid iff 32 * k < lim
 
         // ---- items into registers (warp-striped) and rank
-        uint64_t key[ITEMS], pay[ITEMS];
-        uint32_t dg[ITEMS], rk[ITEMS];
+        uint64_t key[IT], pay[IT];
+        uint32_t dg[IT], rk[IT];
 #pragma unroll
-        for (int k = 0; k < ITEMS; ++k) {
+        for (int k = 0; k < IT; ++k) {
             const int li = wb + 32 * k + lane;
             key[k] = sm.buf[b][0][offk + li];
             if (LAYOUT != PP) pay[k] = sm.buf[b][NARR - 1][offp + li];
             dg[k] = LAYOUT == PP ? rec_digit<HI>(key[k], dig) : dig(key[k]);
         }
         if (lane_ordered) {
-            if (cnt == TILE) {
+            if (cnt == TL) {
 #pragma unroll
-                for (int k = 0; k < ITEMS; ++k) rk[k] = __byte_perm(atomicAdd(&hrow[dg[k]], inc), 0, half);
+                for (int k = 0; k < IT; ++k) rk[k] = __byte_perm(atomicAdd(&hrow[dg[k]], inc), 0, half);
             } else {
 #pragma unroll
-                for (int k = 0; k < ITEMS; ++k)
+                for (int k = 0; k < IT; ++k)
                     if (32 * k < lim) rk[k] = __byte_perm(atomicAdd(&hrow[dg[k]], inc), 0, half);
             }
         } else {
 #pragma unroll
-            for (int k = 0; k < ITEMS; ++k) {
+            for (int k = 0; k < IT; ++k) {
                 const bool valid = 32 * k < lim;
                 const unsigned vmask = __ballot_sync(0xffffffffu, valid);
                 const unsigned peers = ballot_peers(dg[k], vmask);
@@ -411,7 +440,7 @@ __global__ void __launch_bounds__(THREADS, LAYOUT == PP ? MPSM_SEG_PP_BLOCKS : 1
             uint64_t ovf = 0;
             const uint64_t pmask = (1ull << pk_pw) - 1ull;
 #pragma unroll
-            for (int k = 0; k < ITEMS; ++k) {
+            for (int k = 0; k < IT; ++k) {
                 if (32 * k < lim) ovf |= pay[k] >> pk_pw;
                 // a wider payload is masked so the key bits stay exact; the
                 // caller sees *overflow and redoes the join on pairs
@@ -424,8 +453,8 @@ __global__ void __launch_bounds__(THREADS, LAYOUT == PP ? MPSM_SEG_PP_BLOCKS : 1
 
         // ---- stage in digit order
 #pragma unroll
-        for (int k = 0; k < ITEMS; ++k) {
-            if (cnt == TILE || 32 * k < lim) {
+        for (int k = 0; k < IT; ++k) {
+            if (cnt == TL || 32 * k < lim) {
                 const uint32_t p = __byte_perm(hrow[dg[k]], 0, half) + rk[k];
                 sm.buf[b][0][p] = key[k];
                 if (LAYOUT == SS) sm.buf[b][1][p] = pay[k];
@@ -443,7 +472,7 @@ __global__ void __launch_bounds__(THREADS, LAYOUT == PP ? MPSM_SEG_PP_BLOCKS : 1
             if (LAYOUT == SS) out_p[o] = sm.buf[b][1][i];
         }
         SEG_TS(5)
-        b ^= 1;
+        b = (b + 1) % NST;
     }
 }
 
@@ -516,10 +545,11 @@ static int grid_size() {
 
 static int max_grid() { return num_sms() * 4; }
 
-static Segs make_segs(int64_t n, int G) {
+// G segments of whole scatter tiles (tile: the layout's TILE_L)
+static Segs make_segs(int64_t n, int G, int tile = TILE) {
     int64_t seg = (n + G - 1) / G;
-    seg = (seg + TILE - 1) / TILE * TILE;
-    if (seg == 0) seg = TILE;
+    seg = (seg + tile - 1) / tile * tile;
+    if (seg == 0) seg = tile;
     return Segs{n, seg};
 }
 
@@ -564,12 +594,12 @@ static int pass(const uint64_t* in_k, const uint64_t* in_p, uint64_t* out_k, uin
     // prefixes make every tile self-contained
     const int G = std::min(grid_size<LAYOUT>(), max_grid());
     const int GC = std::min(num_sms() * MPSM_SEG_COUNT_PER_SM, max_grid());
-    const Segs sg = make_segs(n, GC);
+    const Segs sg = make_segs(n, GC, LCfg<LAYOUT>::TILE_L);
     const int nbins = 1 << bits;
     {
         ProfScope ps("seg_count", st);
-        k_count<<<GC, THREADS, 0, st>>>(in_k, sg, count_dig, nbins, ws.counts, ws.toffs, ws.ticket, span_m1,
-                                        d_bad);
+        k_count<LCfg<LAYOUT>::TILE_L / TILE><<<GC, THREADS, 0, st>>>(in_k, sg, count_dig, nbins, ws.counts, ws.toffs,
+                                                                      ws.ticket, span_m1, d_bad);
     }
     MPSM_TRY(check_launch("k_count"));
     k_scan<<<(nbins + 31) / 32, 32 * SCAN_GROUPS, 0, st>>>(ws.counts, GC, nbins, ws.base, ws.dtot);
@@ -628,8 +658,8 @@ extern "C" int mpsm_sort_pairs(const uint64_t* in_keys, const uint64_t* in_pays,
     const Plan plan = make_plan(width_bits);
     if (plan.npasses == 0) {  // one-value domain: check it and copy
         const int G = max_grid();
-        k_count<<<G, THREADS, 0, st>>>(in_keys, make_segs(n, G), Digit{lower, 0, 0}, 1, ws.counts, ws.toffs, nullptr,
-                                       span_m1, d_bad);
+        k_count<1><<<G, THREADS, 0, st>>>(in_keys, make_segs(n, G), Digit{lower, 0, 0}, 1, ws.counts, ws.toffs,
+                                          nullptr, span_m1, d_bad);
         MPSM_TRY(check_launch("k_count"));
         if (out_keys != in_keys) {
             MPSM_TRY(cuda_status(cudaMemcpyAsync(out_keys, in_keys, 8 * n, cudaMemcpyDeviceToDevice, st), "copy"));

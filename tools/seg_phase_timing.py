@@ -31,9 +31,9 @@ L = _lib.load()
 ntiles = (n + 4095) // 4096
 buf = np.zeros((ntiles, 8), np.int64)
 L.mpsm_dbg_seg_ts(buf.ctypes.data_as(ctypes.c_void_p), ntiles)
-d = np.diff(buf[:, :7], axis=1)
-names = ["wait_data(sync)", "load+rank", "colsum+scan", "pos+payload", "stage", "write"]
-tot = buf[:, 6] - buf[:, 0]
+d = np.diff(buf[:, :6], axis=1)
+names = ["wait_data(mbar)", "load+rank+S2", "scan+S3+S4", "stage+S5", "write"]
+tot = buf[:, 5] - buf[:, 0]
 print(f"{'packed' if packed else 'pairs'} tiles={ntiles} cycles/tile median {np.median(tot):.0f}")
 for i, nm in enumerate(names):
     print(f"  {nm:18s} median {np.median(d[:, i]):7.0f} mean {np.mean(d[:, i]):7.0f} p90 {np.percentile(d[:, i], 90):7.0f}")
