@@ -34,6 +34,8 @@ extern "C" {
 #define MPSM_ERR_CUDA (-4)     /* RuntimeError (CUDA / NCCL failure)            */
 #define MPSM_ERR_CAP (-5)      /* MaterializeCapExceeded                        */
 #define MPSM_ERR_ARG (-6)      /* ValueError (bad argument)                     */
+#define MPSM_ERR_FORMAT (-7)   /* FormatError (malformed relation file)         */
+#define MPSM_ERR_IO (-8)       /* OSError (file could not be opened / read)     */
 
 /* query modes (core.py:23) */
 #define MPSM_MODE_AGGREGATE_MAX 0
@@ -182,6 +184,23 @@ int mpsm_minmax_contiguous(int64_t n, int t, const int64_t* prefix, const double
 int mpsm_ipc_get_handle(const void* d_ptr, void* handle64);
 int mpsm_ipc_open_handle(const void* handle64, void** d_ptr);
 int mpsm_ipc_close_handle(void* d_ptr);
+
+/* ------------------------------------------------ relation files ----
+ * The reference's relation file (bench.py:8-11, read_relation bench.py:84-102,
+ * write_relation bench.py:73-81): magic "MPSMREL1", u64 n, then n
+ * little-endian (key u64, payload u64) records.
+ * mpsm_relfile_header checks magic and exact length like read_relation and
+ * returns n; on MPSM_ERR_FORMAT *bad_offset is the byte offset the reference
+ * reports (0 for bad magic, the file size for a truncated header,
+ * min(size, 16 + 16 n) for a length mismatch).  Host functions. */
+int mpsm_relfile_header(const char* path, uint64_t* n, int64_t* bad_offset);
+/* reads the n records (16 n bytes, interleaved) into host memory dst (pinned
+ * or pageable) with `threads` parallel readers (0: all cores) */
+int mpsm_relfile_read(const char* path, uint64_t n, void* dst, int threads);
+/* writes a relation file from SoA host arrays */
+int mpsm_relfile_write(const char* path, const uint64_t* keys, const uint64_t* pays, uint64_t n);
+/* device: split n interleaved records into SoA keys / payloads */
+int mpsm_deinterleave(const uint64_t* d_records, int64_t n, uint64_t* d_keys, uint64_t* d_pays, void* stream);
 
 #ifdef __cplusplus
 }

@@ -11,13 +11,13 @@ from __future__ import annotations
 import ctypes
 import os
 
-from .core import ConfigurationError, DomainError, InternalConsistencyError, MaterializeCapExceeded
+from .core import ConfigurationError, DomainError, FormatError, InternalConsistencyError, MaterializeCapExceeded
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MPSM_LIB") or os.path.join(_HERE, "libmpsm_b200.so")
 
 MPSM_OK = 0
-ERR_DOMAIN, ERR_INTERNAL, ERR_CONFIG, ERR_CUDA, ERR_CAP, ERR_ARG = -1, -2, -3, -4, -5, -6
+ERR_DOMAIN, ERR_INTERNAL, ERR_CONFIG, ERR_CUDA, ERR_CAP, ERR_ARG, ERR_FORMAT, ERR_IO = -1, -2, -3, -4, -5, -6, -7, -8
 MODE_AGGREGATE_MAX, MODE_COUNT, MODE_MATERIALIZE = 0, 1, 2
 PAIR_COUNT, PAIR_BEST, PAIR_CHECKSUM, PAIR_START, PAIR_PROBES, PAIR_END, PAIR_EXAMINED, PAIR_EMITTED = range(8)
 PAIR_FIELDS = 8
@@ -33,6 +33,7 @@ EXPORTS = (
     "mpsm_join_workspace_bytes", "mpsm_join_pairs", "mpsm_join_pairs_packed",
     "mpsm_minmax_contiguous",
     "mpsm_ipc_get_handle", "mpsm_ipc_open_handle", "mpsm_ipc_close_handle",
+    "mpsm_relfile_header", "mpsm_relfile_read", "mpsm_relfile_write", "mpsm_deinterleave",
 )
 
 
@@ -67,6 +68,10 @@ _SIGS = {
     "mpsm_ipc_get_handle": (_int, [_vp, _vp]),
     "mpsm_ipc_open_handle": (_int, [_vp, ctypes.POINTER(_vp)]),
     "mpsm_ipc_close_handle": (_int, [_vp]),
+    "mpsm_relfile_header": (_int, [ctypes.c_char_p, ctypes.POINTER(_u64), ctypes.POINTER(_i64)]),
+    "mpsm_relfile_read": (_int, [ctypes.c_char_p, _u64, _vp, _int]),
+    "mpsm_relfile_write": (_int, [ctypes.c_char_p, _vp, _vp, _u64]),
+    "mpsm_deinterleave": (_int, [_vp, _i64, _vp, _vp, _vp]),
 }
 
 _lib = None
@@ -105,6 +110,10 @@ def check(rc: int, what: str = "") -> None:
         raise MaterializeCapExceeded(text)
     if rc == ERR_ARG:
         raise ValueError(text)
+    if rc == ERR_IO:
+        raise OSError(text)
+    if rc == ERR_FORMAT:
+        raise FormatError(text)
     raise RuntimeError(f"CUDA failure in {what}: {msg}")
 
 

@@ -121,3 +121,17 @@ def generate(spec: GenSpec) -> Relation:
         return gen_skewed_8020(spec.cardinality, spec.key_domain, "low", spec.seed)
     base = gen_uniform(spec.cardinality, spec.key_domain, spec.seed)
     return gen_location_skew(base, spec.location_threads, spec.seed)
+
+
+def gen_fk_device(n_r: int, n_s: int, seed: int = 0, device=None, rank: int = 0, world: int = 1) -> tuple:
+    """FK workload generated on the GPU (counter-based; a rank builds only its
+    position shard): -> (R, S, KeyDomain) with CUDA uint64 columns.  Not the
+    numpy stream of gen_fk -- same distribution (R keys a permutation of
+    [1, n_r], S keys uniform over them, 32-bit payloads)."""
+    import torch
+
+    from .distributed import fk_shard_device
+
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    r, s = fk_shard_device(n_r, n_s, rank, world, seed, dev)
+    return r, s, KeyDomain(1, n_r + 1)
