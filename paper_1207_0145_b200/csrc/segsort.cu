@@ -51,6 +51,9 @@ namespace seg {
 #ifndef MPSM_SEG_PP_STAGES  // record-pass tile buffers in shared memory
 #define MPSM_SEG_PP_STAGES 2
 #endif
+#ifndef MPSM_SEG_STAGES  // pair-input (SS / SP) tile buffers in shared memory
+#define MPSM_SEG_STAGES 2
+#endif
 constexpr int THREADS = MPSM_SEG_THREADS;
 constexpr int ITEMS = MPSM_SEG_ITEMS;
 constexpr int TILE = THREADS * ITEMS;  // 4096 tuples: the count chunk and the smallest scatter tile
@@ -66,7 +69,7 @@ template <int LAYOUT>
 struct LCfg {
     static constexpr int ITEMS_L = LAYOUT == PP ? MPSM_SEG_PP_ITEMS : ITEMS;
     static constexpr int TILE_L = THREADS * ITEMS_L;
-    static constexpr int NST = LAYOUT == PP ? MPSM_SEG_PP_STAGES : 2;
+    static constexpr int NST = LAYOUT == PP ? MPSM_SEG_PP_STAGES : MPSM_SEG_STAGES;
     static constexpr int BLOCKS = LAYOUT == PP ? MPSM_SEG_PP_BLOCKS : 1;
     static_assert(TILE_L % TILE == 0, "scatter tiles are whole count chunks");
 };
@@ -202,7 +205,6 @@ struct Smem {
     uint32_t hist[WARPS / 2][MAX_BINS];  // [warp pair][digit]
     int64_t gdelta[MAX_BINS];            // output index - staging index, per digit
     uint32_t toffs[NST][MAX_BINS];       // per buffer: the tile's segment-local digit prefixes
-    int64_t sbase[NST][MAX_BINS];        // per buffer: its segment's digit bases
     uint32_t wtot[WARPS];                // digit-scan carries
     int64_t tile[NST];                   // per buffer: tile index
     uint64_t bar[NST];                   // bulk-copy completion, per buffer
@@ -314,20 +316,19 @@ __global__ void __launch_bounds__(THREADS, LCfg<LAYOUT>::BLOCKS) k_scatter(
         for (int w = 0; w < warp; ++w) dstart += sm.gdelta[w];
     }
 
-    // thread 0: one mbarrier phase brings tile t's tuples, its digit
-    // prefixes and its segment's digit bases into buffer bb
+    // thread 0: one mbarrier phase brings tile t's tuples and its digit
+    // prefixes into buffer bb
     auto fetch = [&](int bb, int64_t t) {
         const int64_t t0 = t * TL;
         const int cnt = (int)min((int64_t)TL, sg.n - t0);
         sm.tile[bb] = t;
         unsigned bk = tile_plain(sm.buf[bb][0], in_k + t0, offk, cnt), bp = 0;
         if (NARR == 2) bp = tile_plain(sm.buf[bb][NARR - 1], in_p + t0, offp, cnt);
-        const unsigned bo = MAX_BINS * 4, bs = nbins * 8;
-        mbar_arrive_expect_tx(&sm.bar[bb], bk + bp + bo + bs);
+        const unsigned bo = MAX_BINS * 4;
+        mbar_arrive_expect_tx(&sm.bar[bb], bk + bp + bo);
         tile_bulk(sm.buf[bb][0], in_k + t0, offk, bk, &sm.bar[bb]);
         if (NARR == 2) tile_bulk(sm.buf[bb][NARR - 1], in_p + t0, offp, bp, &sm.bar[bb]);
         bulk_load(sm.toffs[bb], toffs + (size_t)t * MAX_BINS, bo, &sm.bar[bb]);
-        bulk_load(sm.sbase[bb], base + (size_t)(t / tiles_per_seg) * nbins, bs, &sm.bar[bb]);
     };
     // tiles in global order: each CTA starts at tile blockIdx.x, later tiles
     // come from a dispenser in order, so the tiles in flight at any moment
@@ -363,6 +364,8 @@ __global__ void __launch_bounds__(THREADS, LCfg<LAYOUT>::BLOCKS) k_scatter(
                 sm.tile[nb] = T;  // no more tiles
             }
         }
+        // my digit's segment base (L2-resident, G x 512); consumed after the rank
+        const int64_t sbase = mine ? base[(size_t)(t / tiles_per_seg) * nbins + tid] : 0;
         mbar_wait(&sm.bar[b], (par >> b) & 1u);
         par ^= 1u << b;
         SEG_TS(1)
@@ -434,7 +437,7 @@ __global__ void __launch_bounds__(THREADS, LCfg<LAYOUT>::BLOCKS) k_scatter(
                 sm.hist[r][tid] = run * 0x10001u + sh;
                 run += (col[r] + sh) >> 16;
             }
-            sm.gdelta[tid] = dstart + sm.sbase[b][tid] + sm.toffs[b][tid] - (int64_t)toff;
+            sm.gdelta[tid] = dstart + sbase + sm.toffs[b][tid] - (int64_t)toff;
         }
         if (LAYOUT == SP) {
             uint64_t ovf = 0;

@@ -13,7 +13,7 @@ os.environ["MPSM_LIB"] = os.path.join(ROOT, "build", "variants_dbg", os.environ.
 from paper_1207_0145_b200 import _lib, device as D  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 400_000_000
-bits = 27
+bits = int(sys.argv[3]) if len(sys.argv) > 3 else 27  # 9: one (SP) pass only
 packed = (sys.argv[2] if len(sys.argv) > 2 else "packed") == "packed"
 dev = torch.device("cuda", 0)
 keys = torch.randint(0, 1 << bits, (n,), device=dev, dtype=torch.int64).view(torch.uint64)
@@ -28,7 +28,7 @@ for _ in range(2):
         D.sort_pairs(keys, pays, 0, (1 << bits) - 1, bits, o[0], o[1], o[2], o[3], None)
 torch.cuda.synchronize()
 L = _lib.load()
-ntiles = (n + 4095) // 4096
+ntiles = (n + 4095) // 4096 if (bits <= 9 or not packed) else (n + 8191) // 8192
 buf = np.zeros((ntiles, 8), np.int64)
 L.mpsm_dbg_seg_ts(buf.ctypes.data_as(ctypes.c_void_p), ntiles)
 d = np.diff(buf[:, :6], axis=1)
