@@ -202,6 +202,28 @@ int mpsm_relfile_write(const char* path, const uint64_t* keys, const uint64_t* p
 /* device: split n interleaved records into SoA keys / payloads */
 int mpsm_deinterleave(const uint64_t* d_records, int64_t n, uint64_t* d_keys, uint64_t* d_pays, void* stream);
 
+/* ------------------------------------------------- packed upload ----
+ * Host (key, payload) SoA -> device packed records (key - lower) << (64 - w)
+ * | payload, the layout mpsm_sort_records sorts.  Host worker threads pack
+ * 1M-tuple chunks into pinned staging slots and each chunk is copied while
+ * later ones are packed: half the PCIe bytes of copying the columns.  Keys
+ * outside [lower, lower + span_m1]: *bad_index = first such index (else -1;
+ * the reference raises DomainError, sorter.py:97-98).  A payload >= 2^(64-w):
+ * *overflow = 1 and the records are invalid (use the column path).  The
+ * copies are ordered before later work on `stream`; returns once the host
+ * buffers have been read.  Not thread-safe (one uploader per process). */
+int mpsm_upload_records(const uint64_t* h_keys, const uint64_t* h_pays, int64_t n, uint64_t lower,
+                        uint64_t span_m1, int width_bits, uint64_t* d_rec, int threads, void* stream,
+                        int64_t* bad_index, int* overflow);
+/* host->device bytes moved by mpsm_upload_records since the last reset
+ * (8 per host-packed tuple, 16 per tuple the GPU packs from mapped memory) */
+uint64_t mpsm_upload_bytes(int reset);
+/* sort packed records (key in the top width_bits bits) by key: every pass
+ * moves 8 B (the mpsm_sort_packed passes after its packing pass).  in_rec
+ * must differ from out_rec and tmp_rec.  Same workspace as mpsm_sort_pairs. */
+int mpsm_sort_records(const uint64_t* in_rec, int64_t n, int width_bits, uint64_t* out_rec, uint64_t* tmp_rec,
+                      void* workspace, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

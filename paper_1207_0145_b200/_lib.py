@@ -34,6 +34,7 @@ EXPORTS = (
     "mpsm_minmax_contiguous",
     "mpsm_ipc_get_handle", "mpsm_ipc_open_handle", "mpsm_ipc_close_handle",
     "mpsm_relfile_header", "mpsm_relfile_read", "mpsm_relfile_write", "mpsm_deinterleave",
+    "mpsm_upload_records", "mpsm_upload_bytes", "mpsm_sort_records",
 )
 
 
@@ -72,6 +73,10 @@ _SIGS = {
     "mpsm_relfile_read": (_int, [ctypes.c_char_p, _u64, _vp, _int]),
     "mpsm_relfile_write": (_int, [ctypes.c_char_p, _vp, _vp, _u64]),
     "mpsm_deinterleave": (_int, [_vp, _i64, _vp, _vp, _vp]),
+    "mpsm_upload_records": (_int, [_vp, _vp, _i64, _u64, _u64, _int, _vp, _int, _vp, ctypes.POINTER(_i64),
+                                   ctypes.POINTER(_int)]),
+    "mpsm_sort_records": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _sz, _vp]),
+    "mpsm_upload_bytes": (_u64, [_int]),
 }
 
 _lib = None

@@ -723,3 +723,31 @@ extern "C" int mpsm_sort_packed(const uint64_t* in_keys, const uint64_t* in_pays
     }
     return MPSM_OK;
 }
+
+extern "C" int mpsm_sort_records(const uint64_t* in_rec, int64_t n, int width_bits, uint64_t* out_rec,
+                                 uint64_t* tmp_rec, void* workspace, size_t ws_bytes, void* stream) {
+    using namespace seg;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n < 0 || width_bits < 1 || width_bits > 63) return MPSM_ERR_ARG;
+    if (n == 0) return MPSM_OK;
+    if (in_rec == out_rec || in_rec == tmp_rec || out_rec == tmp_rec) {
+        set_error("mpsm_sort_records: in, out and tmp must be distinct");
+        return MPSM_ERR_ARG;
+    }
+    Ws ws;
+    if (!carve(workspace, ws_bytes, n, &ws)) {
+        set_error("sort workspace too small");
+        return MPSM_ERR_ARG;
+    }
+    const Plan plan = make_plan(width_bits);
+    const int pw = 64 - width_bits;
+    const int P = plan.npasses;
+    const uint64_t* src = in_rec;
+    for (int i = 0; i < P; ++i) {
+        uint64_t* dst = ((P - 1 - i) % 2 == 0) ? out_rec : tmp_rec;
+        const Digit dg{0, pw + plan.shift[i], (1u << plan.bits[i]) - 1u};
+        MPSM_TRY(pass<PP>(src, nullptr, dst, nullptr, n, dg, dg, plan.bits[i], ws, ~0ull, nullptr, 0, pw, nullptr, st));
+        src = dst;
+    }
+    return MPSM_OK;
+}

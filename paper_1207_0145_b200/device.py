@@ -114,6 +114,49 @@ def sort_packed(in_k: torch.Tensor, in_p: torch.Tensor, lower: int, span_m1: int
                                   ptr(ws), ws.numel(), ptr(bad), ptr(overflow), stream_ptr()), "mpsm_sort_packed")
 
 
+def sort_records(in_rec: torch.Tensor, width_bits: int, out_rec: torch.Tensor, tmp_rec: torch.Tensor) -> None:
+    """Sort packed records (key in the top width_bits bits); in, out, tmp distinct."""
+    n = int(in_rec.numel())
+    if n == 0:
+        return
+    L = _lib.load()
+    sz = ctypes.c_size_t(0)
+    _lib.check(L.mpsm_sort_workspace_bytes(n, width_bits, ctypes.byref(sz)), "sort workspace")
+    ws = workspace(in_rec.device).get(sz.value)
+    _lib.check(L.mpsm_sort_records(ptr(in_rec), n, width_bits, ptr(out_rec), ptr(tmp_rec), ptr(ws), ws.numel(),
+                                   stream_ptr()), "mpsm_sort_records")
+
+
+def host_columns(a):
+    """A host uint64 column as (keep-alive object, address), or None if `a`
+    is not host-resident."""
+    if isinstance(a, torch.Tensor):
+        if a.device.type != "cpu":
+            return None
+        t = a.contiguous()
+        if t.dtype not in (U64, torch.int64):
+            return None
+        return t, t.data_ptr()
+    arr = np.ascontiguousarray(a)
+    if arr.dtype not in (np.uint64, np.int64) or arr.ndim != 1:
+        return None
+    return arr, arr.ctypes.data
+
+
+def upload_records(keys, pays, lower: int, span_m1: int, width_bits: int, out_rec: torch.Tensor,
+                   threads: int = 0) -> tuple:
+    """Host (key, payload) columns -> packed records on the device (half the
+    PCIe bytes).  -> (first out-of-domain index or -1, payload overflow)."""
+    hk, hp = host_columns(keys), host_columns(pays)
+    n = int(out_rec.numel())
+    bad = ctypes.c_int64(-1)
+    ovf = ctypes.c_int(0)
+    _lib.check(_lib.load().mpsm_upload_records(hk[1] if n else None, hp[1] if n else None, n, lower, span_m1,
+                                               width_bits, ptr(out_rec), threads, stream_ptr(), ctypes.byref(bad),
+                                               ctypes.byref(ovf)), "mpsm_upload_records")
+    return int(bad.value), bool(ovf.value)
+
+
 def radix_histogram(keys: torch.Tensor, lower: int, span_m1: int, shift: int, nbuckets: int,
                     counts: torch.Tensor, bad: Optional[torch.Tensor] = None) -> None:
     n = int(keys.numel())

@@ -183,6 +183,14 @@ def _raise_domain(flag: torch.Tensor, rel_name: str) -> None:
 # key width allows it and every payload fits; a join that meets a wide payload
 # is re-run on (key, payload) pairs.  MPSM_PACK=0 forces the pair layout.
 PACK_RECORDS = os.environ.get("MPSM_PACK", "1") != "0"
+# host-resident inputs of a packed join cross PCIe as packed records (host
+# threads pack while earlier chunks copy: half the bytes, device.upload_records)
+# MPSM_HOST_PACK=0 copies the columns instead.
+HOST_PACK = os.environ.get("MPSM_HOST_PACK", "1") != "0"
+
+
+class _PackOverflow(Exception):
+    """a payload does not fit the packed record: rerun on (key, payload) pairs"""
 
 
 class JoinContext:
@@ -191,7 +199,8 @@ class JoinContext:
     Runs are (keys, payloads) tensor pairs, or (records, None) in packed mode.
     """
 
-    def __init__(self, r: Relation, s: Relation, cfg: JoinConfig, phase_hook: PhaseHook, packed: bool):
+    def __init__(self, r: Relation, s: Relation, cfg: JoinConfig, phase_hook: PhaseHook, packed: bool,
+                 variant: str = "p-mpsm"):
         self.cfg = cfg
         self.hook = phase_hook
         self.dev = D.ensure_device()
@@ -201,12 +210,22 @@ class JoinContext:
         self.packed = bool(packed) and 1 <= self.wbits <= 63
         self.pw = 64 - self.wbits
         self.span_m1 = self.dom.upper - self.dom.lower - 1
-        self.priv_k = D.to_device(private.keys, self.dev)
-        self.priv_p = D.to_device(private.payloads, self.dev)
-        self.pub_k = D.to_device(public.keys, self.dev)
-        self.pub_p = D.to_device(public.payloads, self.dev)
-        self.n_priv = int(self.priv_k.numel())
-        self.n_pub = int(self.pub_k.numel())
+        # the private side skips the partition (which reads key columns) in
+        # B-MPSM and with one worker
+        self.priv_rec = self._upload(private, "private", variant == "b-mpsm" or self.t == 1)
+        self.pub_rec = self._upload(public, "public", True)
+        if self.priv_rec is None:
+            self.priv_k = D.to_device(private.keys, self.dev)
+            self.priv_p = D.to_device(private.payloads, self.dev)
+            self.n_priv = int(self.priv_k.numel())
+        else:
+            self.n_priv = int(self.priv_rec.numel())
+        if self.pub_rec is None:
+            self.pub_k = D.to_device(public.keys, self.dev)
+            self.pub_p = D.to_device(public.payloads, self.dev)
+            self.n_pub = int(self.pub_k.numel())
+        else:
+            self.n_pub = int(self.pub_rec.numel())
         self.pub_chunks = chunk_bounds(self.n_pub, self.t)
         self.priv_chunks = chunk_bounds(self.n_priv, self.t)
         self.stats = [WorkerStats(i) for i in range(self.t)]
@@ -215,6 +234,21 @@ class JoinContext:
         self.overflow = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.tmp = []
         self.tl = _Timeline()
+
+    def _upload(self, rel: Relation, name: str, allowed: bool):
+        """host columns -> packed records on the device, or None (columns path)"""
+        if not (allowed and self.packed and HOST_PACK):
+            return None
+        hk, hp = D.host_columns(rel.keys), D.host_columns(rel.payloads)
+        if hk is None or hp is None or hk[0].shape[0] != hp[0].shape[0]:
+            return None
+        rec = torch.empty(int(hk[0].shape[0]), dtype=torch.uint64, device=self.dev)
+        bad, ovf = D.upload_records(hk[0], hp[0], self.dom.lower, self.span_m1, self.wbits, rec)
+        if bad >= 0:
+            raise DomainError(f"relation {name} has out-of-domain keys (first at index {bad})")
+        if ovf:
+            raise _PackOverflow()
+        return rec
 
     def _hook(self, i: int, phase: str) -> None:
         if self.hook:
@@ -233,9 +267,15 @@ class JoinContext:
         return (self._empty(n), None) if self.packed else (self._empty(n), self._empty(n))
 
     def _sort_into(self, in_k, in_p, dst: tuple, a: int, b: int, bad) -> tuple:
-        """sort in_k/in_p (length b-a) into dst[.][a:b]; returns the run"""
+        """sort in_k/in_p (length b-a; in_p None: in_k holds packed records)
+        into dst[.][a:b]; returns the run"""
         n = b - a
         tmp = self._tmp(n)
+        if in_p is None:
+            out = dst[0][a:b]
+            if n:
+                D.sort_records(in_k, self.wbits, out, tmp[0][:n])
+            return (out, None)
         if self.packed:
             out = dst[0][a:b]
             if n:
@@ -254,7 +294,11 @@ class JoinContext:
         self.pub_runs = []
         for i, (a, b) in enumerate(self.pub_chunks):
             self._hook(i, "sort_public")
-            self.pub_runs.append(self._sort_into(self.pub_k[a:b], self.pub_p[a:b], self.pub_store, a, b, self.bad_pub))
+            if self.pub_rec is not None:
+                run = self._sort_into(self.pub_rec[a:b], None, self.pub_store, a, b, self.bad_pub)
+            else:
+                run = self._sort_into(self.pub_k[a:b], self.pub_p[a:b], self.pub_store, a, b, self.bad_pub)
+            self.pub_runs.append(run)
             self.stats[i].tuples_sorted_public = b - a
 
     def sort_private_chunks(self):
@@ -263,8 +307,11 @@ class JoinContext:
         self.priv_runs = []
         for i, (a, b) in enumerate(self.priv_chunks):
             self._hook(i, "sort_private")
-            self.priv_runs.append(self._sort_into(self.priv_k[a:b], self.priv_p[a:b], self.priv_store, a, b,
-                                                  self.bad_priv))
+            if self.priv_rec is not None:
+                run = self._sort_into(self.priv_rec[a:b], None, self.priv_store, a, b, self.bad_priv)
+            else:
+                run = self._sort_into(self.priv_k[a:b], self.priv_p[a:b], self.priv_store, a, b, self.bad_priv)
+            self.priv_runs.append(run)
             self.stats[i].tuples_sorted_private = b - a
 
     def _public_bound_keys(self, f: int) -> np.ndarray:
@@ -402,7 +449,10 @@ class JoinContext:
 
 def _run(variant: str, r: Relation, s: Relation, cfg: JoinConfig, phase_hook: PhaseHook,
          packed: Optional[bool] = None) -> JoinResult:
-    ctx = JoinContext(r, s, cfg, phase_hook, PACK_RECORDS if packed is None else packed)
+    try:
+        ctx = JoinContext(r, s, cfg, phase_hook, PACK_RECORDS if packed is None else packed, variant)
+    except _PackOverflow:
+        return _run(variant, r, s, cfg, phase_hook, packed=False)
     ctx.tl.mark("t0")
     ctx.sort_public()
     ctx.tl.mark("public")

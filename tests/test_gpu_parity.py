@@ -32,13 +32,16 @@ def _cfg(case, **kw):
 
 # --------------------------------------------------------------- engine parity
 
-@pytest.fixture(params=[True, False], ids=["packed", "pairs"])
+@pytest.fixture(params=["host", "device", "pairs"], ids=["packed-host", "packed-device", "pairs"])
 def pack_mode(request, monkeypatch):
-    """run with packed 8-B records (default) and with (key, payload) pairs"""
+    """run with packed 8-B records packed on the host during the upload
+    (default for host inputs), packed by the first sort pass on the device,
+    and with (key, payload) pairs"""
     from paper_1207_0145_b200 import engine
 
-    monkeypatch.setattr(engine, "PACK_RECORDS", request.param)
-    return request.param
+    monkeypatch.setattr(engine, "PACK_RECORDS", request.param != "pairs")
+    monkeypatch.setattr(engine, "HOST_PACK", request.param == "host")
+    return request.param != "pairs"
 
 
 def test_engine_cases_match_reference(golden, pack_mode):
