@@ -206,15 +206,18 @@ int mpsm_deinterleave(const uint64_t* d_records, int64_t n, uint64_t* d_keys, ui
  * Host (key, payload) SoA -> device packed records (key - lower) << (64 - w)
  * | payload, the layout mpsm_sort_records sorts.  Host worker threads pack
  * 1M-tuple chunks into pinned staging slots and each chunk is copied while
- * later ones are packed: half the PCIe bytes of copying the columns.  Keys
+ * later ones are packed: half the PCIe bytes of copying the columns.  When
+ * the columns are pinned, every gpu_pack_every-th chunk is instead packed by
+ * the GPU reading the mapped columns (balances host memory bandwidth against
+ * PCIe; 0: the host packs all, -1: default 4, MPSM_UPLOAD_RAW_EVERY).  Keys
  * outside [lower, lower + span_m1]: *bad_index = first such index (else -1;
  * the reference raises DomainError, sorter.py:97-98).  A payload >= 2^(64-w):
  * *overflow = 1 and the records are invalid (use the column path).  The
  * copies are ordered before later work on `stream`; returns once the host
  * buffers have been read.  Not thread-safe (one uploader per process). */
 int mpsm_upload_records(const uint64_t* h_keys, const uint64_t* h_pays, int64_t n, uint64_t lower,
-                        uint64_t span_m1, int width_bits, uint64_t* d_rec, int threads, void* stream,
-                        int64_t* bad_index, int* overflow);
+                        uint64_t span_m1, int width_bits, uint64_t* d_rec, int threads, int gpu_pack_every,
+                        void* stream, int64_t* bad_index, int* overflow);
 /* host->device bytes moved by mpsm_upload_records since the last reset
  * (8 per host-packed tuple, 16 per tuple the GPU packs from mapped memory) */
 uint64_t mpsm_upload_bytes(int reset);

@@ -42,7 +42,7 @@ namespace mpsm {
 #define MPSM_MJ_THREADS 128
 #endif
 #ifndef MPSM_MJ_ITEMS
-#define MPSM_MJ_ITEMS 17
+#define MPSM_MJ_ITEMS 15
 #endif
 #ifndef MPSM_MJ_BLOCKS
 #define MPSM_MJ_BLOCKS 6
@@ -317,6 +317,7 @@ struct alignas(16) MergeStage {
 template <bool PK>
 struct MergeSmem {
     MergeStage<PK> st[2];
+    uint16_t ub[MJ_TILE];  // MODE 0: per W tuple of the tile, R tuples <= its key (tile-relative)
     uint64_t bar[2];
     uint64_t red[3][MJ_THREADS / 32];
     int64_t warp_cnt[MJ_THREADS / 32];
@@ -486,6 +487,58 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
         MJ_TS(3)
         int64_t my_pairs = 0;
         int64_t emit_base = 0;
+#ifndef MPSM_MJ_ONE_PHASE
+        if (MODE == 0) {
+            // phase 1 -- the thread's merge steps, branch-light: record for
+            // every W tuple the number of tile R tuples with key <= its key
+            {
+                int ri = lo, wj = k0 - lo;
+                KT rkc = ri < nR ? rkey(ri) : 0;
+                KT wkc = wj < nW ? wkey(wj) : 0;
+                for (int st = k0; st < k1; ++st) {
+                    const bool take_r = ri < nR && (wj >= nW || rkc <= wkc);
+                    if (!take_r) sm.ub[wj] = (uint16_t)ri;
+                    ri += take_r;
+                    wj += !take_r;
+                    if (take_r && ri < nR) rkc = rkey(ri);
+                    if (!take_r && wj < nW) wkc = wkey(wj);
+                }
+            }
+            __syncthreads();
+            // phase 2 -- W tuples dealt round-robin (balanced, no merge
+            // control flow): each matches the equal-key R group ending at
+            // tile index ub - 1 (walked back; usually one tuple)
+            const uint64_t pmask = pi.pmask;
+            auto acc = [&](uint64_t rp, uint64_t sp) {
+                const uint64_t v = rp + sp;
+                best = v > best ? v : best;
+                ++count;
+                csum += swap ? pair_hash(sp, rp) : pair_hash(rp, sp);
+            };
+            for (int j = tid; j < nW; j += MJ_THREADS) {
+                const uint64_t wv = WK[j];
+                const KT wk = nkey(wv);
+                int i = (int)sm.ub[j] - 1;
+                if (i < -hp) continue;  // no R tuple <= the key (tile at the run start)
+                uint64_t rv = RK[i];
+                if (nkey(rv) != wk) continue;
+                const uint64_t sp = PK ? (wv & pmask) : WP[j];
+                for (;;) {  // the equal-key R group, backwards; usually one tuple
+                    acc(PK ? (rv & pmask) : RP[i], sp);
+                    if (--i < -hp) {  // the group reaches back before the tile
+                        for (int64_t g = t.i0 + i; g >= 0; --g) {
+                            const uint64_t gv = t.rk[g];
+                            if (nkey(gv) != wk) break;
+                            acc(PK ? (gv & pmask) : t.rp[g], sp);
+                        }
+                        break;
+                    }
+                    rv = RK[i];
+                    if (nkey(rv) != wk) break;
+                }
+            }
+        } else
+#endif
         for (int pass = (MODE == 2 ? 0 : 1); pass < 2; ++pass) {
             // MODE 2 runs the thread's merge twice: count, then emit at its offset
             if (MODE == 2 && pass == 1) {

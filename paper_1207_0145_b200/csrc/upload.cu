@@ -166,7 +166,7 @@ struct Uploader {
     }
 
     int run(const uint64_t* k, const uint64_t* p, int64_t n_, uint64_t lo, uint64_t span, int pw_, uint64_t* d_rec,
-            cudaStream_t st, int64_t* bad_out, int* ovf_out) {
+            int gpu_every, cudaStream_t st, int64_t* bad_out, int* ovf_out) {
         // the copy stream must not overwrite a slot that a previous call's
         // copies still read: drain it first
         MPSM_TRY(cuda_status(cudaStreamSynchronize(copy), "drain"));
@@ -182,12 +182,13 @@ struct Uploader {
         next.store(0);
         // raw chunks need host columns the GPU can read (pinned / registered)
         raw_every = 0;
-        if (raw_every_default() > 0) {
+        if (gpu_every < 0) gpu_every = raw_every_default();
+        if (gpu_every > 0) {
             cudaPointerAttributes ak, ap;
             if (cudaPointerGetAttributes(&ak, k) == cudaSuccess && cudaPointerGetAttributes(&ap, p) == cudaSuccess &&
                 ak.type == cudaMemoryTypeHost && ap.type == cudaMemoryTypeHost && ak.devicePointer == k &&
                 ap.devicePointer == p)
-                raw_every = raw_every_default();
+                raw_every = gpu_every;
             cudaGetLastError();
         }
         MPSM_TRY(cuda_status(cudaMemsetAsync(d_bad, 0xff, sizeof(unsigned long long), copy), "flag"));
@@ -263,8 +264,8 @@ Uploader& uploader() {
 using namespace mpsm;
 
 extern "C" int mpsm_upload_records(const uint64_t* h_keys, const uint64_t* h_pays, int64_t n, uint64_t lower,
-                                   uint64_t span_m1, int width_bits, uint64_t* d_rec, int threads, void* stream,
-                                   int64_t* bad_index, int* overflow) {
+                                   uint64_t span_m1, int width_bits, uint64_t* d_rec, int threads, int gpu_pack_every,
+                                   void* stream, int64_t* bad_index, int* overflow) {
     if (n < 0 || width_bits < 1 || width_bits > 63 || !bad_index || !overflow) return MPSM_ERR_ARG;
     *bad_index = -1;
     *overflow = 0;
@@ -272,7 +273,8 @@ extern "C" int mpsm_upload_records(const uint64_t* h_keys, const uint64_t* h_pay
     if (!h_keys || !h_pays || !d_rec) return MPSM_ERR_ARG;
     Uploader& u = uploader();
     MPSM_TRY(u.init(threads));
-    return u.run(h_keys, h_pays, n, lower, span_m1, 64 - width_bits, d_rec, (cudaStream_t)stream, bad_index, overflow);
+    return u.run(h_keys, h_pays, n, lower, span_m1, 64 - width_bits, d_rec, gpu_pack_every, (cudaStream_t)stream,
+                 bad_index, overflow);
 }
 
 extern "C" uint64_t mpsm_upload_bytes(int reset) {

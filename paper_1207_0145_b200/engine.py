@@ -211,15 +211,13 @@ class JoinContext:
         self.pw = 64 - self.wbits
         self.span_m1 = self.dom.upper - self.dom.lower - 1
         # the private side skips the partition (which reads key columns) in
-        # B-MPSM and with one worker
-        self.priv_rec = self._upload(private, "private", variant == "b-mpsm" or self.t == 1)
+        # B-MPSM and with one worker; host inputs of it are staged after the
+        # public sort is queued, so that upload overlaps the public sort
+        self._private = private
+        self._priv_pack = variant == "b-mpsm" or self.t == 1
+        self.priv_rec = None
+        self.n_priv = int(private.keys.shape[0]) if hasattr(private.keys, "shape") else len(private.keys)
         self.pub_rec = self._upload(public, "public", True)
-        if self.priv_rec is None:
-            self.priv_k = D.to_device(private.keys, self.dev)
-            self.priv_p = D.to_device(private.payloads, self.dev)
-            self.n_priv = int(self.priv_k.numel())
-        else:
-            self.n_priv = int(self.priv_rec.numel())
         if self.pub_rec is None:
             self.pub_k = D.to_device(public.keys, self.dev)
             self.pub_p = D.to_device(public.payloads, self.dev)
@@ -235,7 +233,17 @@ class JoinContext:
         self.tmp = []
         self.tl = _Timeline()
 
-    def _upload(self, rel: Relation, name: str, allowed: bool):
+    def stage_private(self) -> None:
+        """private input -> device (packed records or columns)"""
+        private = self._private
+        # the GPU is sorting the public run: host threads pack every chunk
+        self.priv_rec = self._upload(private, "private", self._priv_pack, gpu_pack_every=0)
+        if self.priv_rec is None:
+            self.priv_k = D.to_device(private.keys, self.dev)
+            self.priv_p = D.to_device(private.payloads, self.dev)
+        self._private = None
+
+    def _upload(self, rel: Relation, name: str, allowed: bool, gpu_pack_every: int = -1):
         """host columns -> packed records on the device, or None (columns path)"""
         if not (allowed and self.packed and HOST_PACK):
             return None
@@ -243,7 +251,8 @@ class JoinContext:
         if hk is None or hp is None or hk[0].shape[0] != hp[0].shape[0]:
             return None
         rec = torch.empty(int(hk[0].shape[0]), dtype=torch.uint64, device=self.dev)
-        bad, ovf = D.upload_records(hk[0], hp[0], self.dom.lower, self.span_m1, self.wbits, rec)
+        bad, ovf = D.upload_records(hk[0], hp[0], self.dom.lower, self.span_m1, self.wbits, rec,
+                                    gpu_pack_every=gpu_pack_every)
         if bad >= 0:
             raise DomainError(f"relation {name} has out-of-domain keys (first at index {bad})")
         if ovf:
@@ -451,11 +460,14 @@ def _run(variant: str, r: Relation, s: Relation, cfg: JoinConfig, phase_hook: Ph
          packed: Optional[bool] = None) -> JoinResult:
     try:
         ctx = JoinContext(r, s, cfg, phase_hook, PACK_RECORDS if packed is None else packed, variant)
+        ctx.tl.mark("t0")
+        ctx.sort_public()
+        ctx.tl.mark("public")
+        # with host inputs the private upload runs while the GPU sorts the
+        # public run (its wait lands in the "partition" interval)
+        ctx.stage_private()
     except _PackOverflow:
         return _run(variant, r, s, cfg, phase_hook, packed=False)
-    ctx.tl.mark("t0")
-    ctx.sort_public()
-    ctx.tl.mark("public")
     if variant == "b-mpsm":
         ctx.tl.mark("scatter")
         ctx.sort_private_chunks()
