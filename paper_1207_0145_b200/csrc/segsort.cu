@@ -40,7 +40,7 @@ namespace seg {
 #define MPSM_SEG_ITEMS 8
 #endif
 #ifndef MPSM_SEG_COUNT_PER_SM  // count CTAs (segments) per SM
-#define MPSM_SEG_COUNT_PER_SM 2
+#define MPSM_SEG_COUNT_PER_SM 4
 #endif
 #ifndef MPSM_SEG_PP_BLOCKS  // record-pass scatter CTAs per SM
 #define MPSM_SEG_PP_BLOCKS 1

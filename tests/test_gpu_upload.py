@@ -111,3 +111,28 @@ def test_join_host_inputs_all_paths(monkeypatch):
     badk[12345] = dom.upper + 7
     with pytest.raises(DomainError, match="12345"):
         P.run_join(r, P.Relation(badk, np.asarray(s.payloads)), P.JoinConfig(threads=1, key_domain=dom))
+
+
+@pytest.mark.parametrize("n", [8191, 8192, 8193, 2 * 8192 + 1, 5 * 8192 - 3, 123_457])
+@pytest.mark.parametrize("w", [10, 18, 27])
+def test_sort_packed_tile_edges(n, w):
+    """the packing pass (4096-tuple tiles) and record passes (8192-tuple
+    tiles) at tile-boundary sizes; stable"""
+    import torch
+
+    from paper_1207_0145_b200 import device as D
+
+    rng = np.random.default_rng(n + 7 * w)
+    lower = 3
+    k = rng.integers(lower, lower + (1 << w), n, dtype=np.uint64)
+    p = np.arange(n, dtype=np.uint64)
+    dk, dp = torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda()
+    out = torch.empty_like(dk)
+    tmp = torch.empty_like(dk)
+    ovf = torch.zeros(1, dtype=torch.int32, device="cuda")
+    D.sort_packed(dk, dp, lower, (1 << w) - 1, w, out, tmp, None, ovf)
+    got = out.cpu().numpy()
+    order = np.argsort(k, kind="stable")
+    want = ((k[order] - np.uint64(lower)) << np.uint64(64 - w)) | p[order]
+    assert int(ovf.item()) == 0
+    assert np.array_equal(got, want)
