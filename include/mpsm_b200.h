@@ -205,11 +205,11 @@ int mpsm_deinterleave(const uint64_t* d_records, int64_t n, uint64_t* d_keys, ui
 /* ------------------------------------------------- packed upload ----
  * Host (key, payload) SoA -> device packed records (key - lower) << (64 - w)
  * | payload, the layout mpsm_sort_records sorts.  Host worker threads pack
- * 1M-tuple chunks into pinned staging slots and each chunk is copied while
+ * 128K-tuple chunks into pinned staging slots and each chunk is copied while
  * later ones are packed: half the PCIe bytes of copying the columns.  When
  * the columns are pinned, every gpu_pack_every-th chunk is instead packed by
  * the GPU reading the mapped columns (balances host memory bandwidth against
- * PCIe; 0: the host packs all, -1: default 4, MPSM_UPLOAD_RAW_EVERY).  Keys
+ * PCIe; 0: the host packs all, -1: default 0, MPSM_UPLOAD_RAW_EVERY).  Keys
  * outside [lower, lower + span_m1]: *bad_index = first such index (else -1;
  * the reference raises DomainError, sorter.py:97-98).  A payload >= 2^(64-w):
  * *overflow = 1 and the records are invalid (use the column path).  The

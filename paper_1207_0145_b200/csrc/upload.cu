@@ -5,9 +5,12 @@
 // with its own async copy while later chunks are being packed.  The domain
 // check of the first sort pass (DomainError, sorter.py:97-98) and the
 // payload-width check of the packed layout move into the packing loop.
-// Measured on the GPU box (tools/host_pack_bench.cu): plain pinned H2D of
-// 16 B/tuple 55.6 GB/s; 16 packing threads 60-78 GB/s of input; pipelined
-// pack + copy of 500M tuples 111 ms vs 144 ms for the plain copy.
+// Measured on the GPU box (tools/host_pack_bench.cu, bench.py e2e): plain
+// pinned H2D of 16 B/tuple 55.6 GB/s (144 ms for cfg2's 500M tuples);
+// 1 MB staging slots, 12 packing threads: cfg2 end to end 155 -> 101 ms.
+// Slots small enough to stay in the host's last-level cache matter: the copy
+// then reads the packed chunk from cache, and host DRAM sees little more
+// than the column reads (1M-tuple slots: 120 ms).
 
 #include <cuda_runtime.h>
 
@@ -46,17 +49,25 @@ __global__ void __launch_bounds__(256) k_pack_mapped(const uint64_t* __restrict_
 
 namespace {
 
-constexpr int64_t CHUNK = 1 << 20;  // tuples per staging slot (8 MB packed)
+// tuples per staging slot (packed: 8 B each); MPSM_UPLOAD_CHUNK overrides
+int64_t chunk_default() {
+    const char* e = getenv("MPSM_UPLOAD_CHUNK");
+    // 1 MB packed slots: packed data is still in the host's last-level cache
+    // when its copy reads it (cfg2 e2e: 1M-tuple slots 120 ms, 128K 100 ms,
+    // 64K 122 ms: per-copy overhead)
+    return e ? std::max<int64_t>(4096, atoll(e)) : (int64_t)1 << 17;
+}
 std::atomic<uint64_t> g_upload_bytes{0};  // host->device bytes moved by uploads
 
 // every raw_every-th chunk is packed by the GPU from mapped host memory
 // (0: all chunks packed by the host); MPSM_UPLOAD_RAW_EVERY overrides
 int raw_every_default() {
     const char* e = getenv("MPSM_UPLOAD_RAW_EVERY");
-    return e ? atoi(e) : 4;
+    return e ? atoi(e) : 0;  // off: with cache-sized slots the host alone keeps up
 }
 
 struct Uploader {
+    int64_t CHUNK = 0;
     int nslots = 0;
     std::vector<uint64_t*> slot;         // pinned staging
     std::vector<cudaEvent_t> slot_done;  // copy of the slot's last chunk finished
@@ -96,6 +107,7 @@ struct Uploader {
 
     int init(int threads) {
         if (copy) return MPSM_OK;
+        CHUNK = chunk_default();
         if (threads <= 0) {
             const char* e = getenv("MPSM_UPLOAD_THREADS");
             // leave the issuing thread a core
