@@ -217,7 +217,9 @@ def impl_ours(args):
     import torch
 
     ws, rank, local = dist_env()
-    if ws > 1:
+    # MPSM_BENCH_DIST=1 runs the multi-GPU path at world size 1 (a smoke
+    # test of it on a one-GPU box)
+    if ws > 1 or (os.environ.get("MPSM_BENCH_DIST") == "1" and "LOCAL_RANK" in os.environ):
         from paper_1207_0145_b200 import distributed
 
         return distributed.bench_main(args, METRIC, CONFIGS, make_inputs, Clocks, run_reference_sample)

@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(THREADS, LCfg<LAYOUT>::BLOCKS) k_scatter(
         const int64_t t = sm.tile[b];  // set by thread 0 before S1
         if (t >= T) break;
         SEG_TS(0)
-        if (tid == 0) {
+        if (NST > 1 && tid == 0) {
             const int nb = (b + NST - 1) % NST;  // the buffer of the previous tile
             if (tnext < T) {
                 fence_proxy_async_smem();  // buf[nb] was staged through by generic stores
@@ -475,6 +475,19 @@ __global__ void __launch_bounds__(THREADS, LCfg<LAYOUT>::BLOCKS) k_scatter(
             if (LAYOUT == SS) out_p[o] = sm.buf[b][1][i];
         }
         SEG_TS(5)
+        if (NST == 1) {  // one buffer: refill it once the tile is out (the
+                         // other CTA on the SM covers the load latency)
+            __syncthreads();
+            if (tid == 0) {
+                if (tnext < T) {
+                    fence_proxy_async_smem();
+                    fetch(0, tnext);
+                    tnext = (int64_t)gridDim.x + atomicAdd(ticket, 1u);
+                } else {
+                    sm.tile[0] = T;
+                }
+            }
+        }
         b = (b + 1) % NST;
     }
 }
