@@ -205,6 +205,8 @@ class JoinContext:
         self.hook = phase_hook
         self.dev = D.ensure_device()
         self.dom, self.roles, private, public = _prepare(r, s, cfg)
+        # the reference names relations r / s in its domain errors (engine.py:183-188)
+        self.rel_name = {"private": self.roles.private, "public": "s" if self.roles.private == "r" else "r"}
         self.t = cfg.threads
         self.wbits = self.dom.width_bits
         self.packed = bool(packed) and 1 <= self.wbits <= 63
@@ -254,7 +256,7 @@ class JoinContext:
         bad, ovf = D.upload_records(hk[0], hp[0], self.dom.lower, self.span_m1, self.wbits, rec,
                                     gpu_pack_every=gpu_pack_every)
         if bad >= 0:
-            raise DomainError(f"relation {name} has out-of-domain keys (first at index {bad})")
+            raise DomainError(f"relation {self.rel_name[name]} has out-of-domain keys (first at index {bad})")
         if ovf:
             raise _PackOverflow()
         return rec
@@ -351,8 +353,8 @@ class JoinContext:
         # the single host synchronisation of the join: counts + bounds + flags
         bk = self._public_bound_keys(f)
         hist_h = hists.cpu().numpy()
-        _raise_domain(self.bad_priv, "private")
-        _raise_domain(self.bad_pub, "public")
+        _raise_domain(self.bad_priv, self.rel_name["private"])
+        _raise_domain(self.bad_pub, self.rel_name["public"])
         bounds, off = [], 0
         for a, b in self.pub_chunks:
             if b > a:
@@ -419,8 +421,8 @@ class JoinContext:
         """engine.py:195-225 plus the checksum and per-worker statistics."""
         t = self.t
         rec = self.rec.cpu().numpy().reshape(t, t, _lib.PAIR_FIELDS).astype(object)
-        _raise_domain(self.bad_priv, "private")
-        _raise_domain(self.bad_pub, "public")
+        _raise_domain(self.bad_priv, self.rel_name["private"])
+        _raise_domain(self.bad_pub, self.rel_name["public"])
         count, agg, csum = 0, None, 0
         for i in range(t):
             st = self.stats[i]
@@ -490,8 +492,8 @@ def _run(variant: str, r: Relation, s: Relation, cfg: JoinConfig, phase_hook: Ph
     torch.cuda.current_stream().synchronize()
     if ctx.packed_overflowed():
         # a payload needs more than 64 - w bits: redo on (key, payload) pairs
-        _raise_domain(ctx.bad_priv, "private")
-        _raise_domain(ctx.bad_pub, "public")
+        _raise_domain(ctx.bad_priv, ctx.rel_name["private"])
+        _raise_domain(ctx.bad_pub, ctx.rel_name["public"])
         return _run(variant, r, s, cfg, phase_hook, packed=False)
     if variant == "p-mpsm" and ctx.t > 1:
         if not np.array_equal(ctx.written.cpu().numpy(), ctx.cursors.counts):
