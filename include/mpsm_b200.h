@@ -180,8 +180,11 @@ int mpsm_minmax_contiguous(int64_t n, int t, const int64_t* prefix, const double
 /* ------------------------------------------------ multi-GPU helpers ----
  * CUDA IPC so a rank can merge against peer ranks' public runs with NVLink
  * peer loads (the paper's sequential remote-NUMA reads, engine.py:249-260).
- * handle buffers are 64 bytes. */
-int mpsm_ipc_get_handle(const void* d_ptr, void* handle64);
+ * handle buffers are 64 bytes.  get_handle names the cudaMalloc block that
+ * holds d_ptr and returns d_ptr's byte offset in it; open_handle maps the
+ * block into the calling thread's current device with lazy peer access
+ * (open each block once per process; add the offset). */
+int mpsm_ipc_get_handle(const void* d_ptr, void* handle64, int64_t* offset);
 int mpsm_ipc_open_handle(const void* handle64, void** d_ptr);
 int mpsm_ipc_close_handle(void* d_ptr);
 

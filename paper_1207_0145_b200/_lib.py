@@ -66,7 +66,7 @@ _SIGS = {
     "mpsm_join_pairs_packed": (_int, [ctypes.POINTER(RunDesc), _int, ctypes.POINTER(RunDesc), _int, _int, _u64, _int,
                                       _int, _vp, _i64, _vp, _vp, _sz, _vp]),
     "mpsm_minmax_contiguous": (_int, [_i64, _int, _vp, _vp, _vp, _i64, _vp]),
-    "mpsm_ipc_get_handle": (_int, [_vp, _vp]),
+    "mpsm_ipc_get_handle": (_int, [_vp, _vp, ctypes.POINTER(_i64)]),
     "mpsm_ipc_open_handle": (_int, [_vp, ctypes.POINTER(_vp)]),
     "mpsm_ipc_close_handle": (_int, [_vp]),
     "mpsm_relfile_header": (_int, [ctypes.c_char_p, ctypes.POINTER(_u64), ctypes.POINTER(_i64)]),

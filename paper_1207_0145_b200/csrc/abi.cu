@@ -106,14 +106,47 @@ extern "C" int mpsm_device_init(int device) {
     return prop.multiProcessorCount;
 }
 
-extern "C" int mpsm_ipc_get_handle(const void* d_ptr, void* handle64) {
-    cudaIpcMemHandle_t h;
-    MPSM_TRY(cuda_status(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)), "cudaIpcGetMemHandle"));
-    static_assert(sizeof(h) == 64, "IPC handle size");
-    std::memcpy(handle64, &h, 64);
+// base of the allocation holding d_ptr (the caching allocator sub-allocates:
+// the IPC handle names the whole cudaMalloc block), through the driver's
+// cuMemGetAddressRange fetched at run time (no link-time libcuda)
+static int alloc_base(const void* d_ptr, uintptr_t* base) {
+    typedef int (*range_fn)(unsigned long long*, size_t*, unsigned long long);
+    static range_fn fn = nullptr;
+    if (!fn) {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        MPSM_TRY(cuda_status(cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q),
+                             "cudaGetDriverEntryPoint"));
+        if (!f || q != cudaDriverEntryPointSuccess) {
+            set_error("cuMemGetAddressRange unavailable");
+            return MPSM_ERR_CUDA;
+        }
+        fn = (range_fn)f;
+    }
+    unsigned long long b = 0;
+    size_t size = 0;
+    if (fn(&b, &size, (unsigned long long)(uintptr_t)d_ptr) != 0) {
+        set_error("cuMemGetAddressRange failed");
+        return MPSM_ERR_CUDA;
+    }
+    *base = (uintptr_t)b;
     return MPSM_OK;
 }
 
+extern "C" int mpsm_ipc_get_handle(const void* d_ptr, void* handle64, int64_t* offset) {
+    if (!d_ptr || !handle64 || !offset) return MPSM_ERR_ARG;
+    uintptr_t base = 0;
+    MPSM_TRY(alloc_base(d_ptr, &base));
+    cudaIpcMemHandle_t h;
+    MPSM_TRY(cuda_status(cudaIpcGetMemHandle(&h, (void*)base), "cudaIpcGetMemHandle"));
+    static_assert(sizeof(h) == 64, "IPC handle size");
+    std::memcpy(handle64, &h, 64);
+    *offset = (int64_t)((uintptr_t)d_ptr - base);
+    return MPSM_OK;
+}
+
+// maps the block into the CURRENT device's context with lazy peer access, so
+// this rank's kernels read it over NVLink
 extern "C" int mpsm_ipc_open_handle(const void* handle64, void** d_ptr) {
     cudaIpcMemHandle_t h;
     std::memcpy(&h, handle64, 64);

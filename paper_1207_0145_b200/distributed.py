@@ -53,6 +53,49 @@ from .partition import combine_counts, effective_radix_bits
 from .skew import LocalBounds, bound_positions, build_cdf, compute_splitters
 
 
+class PeerRun:
+    """A run in a peer rank's HBM, mapped into this process (read by the
+    merge kernel with NVLink peer loads): exposes what device.join_* read."""
+
+    __slots__ = ("ptr", "n", "device")
+
+    def __init__(self, ptr: int, n: int, device):
+        self.ptr, self.n, self.device = ptr, n, device
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
+    def numel(self) -> int:
+        return self.n
+
+
+_IPC_BLOCKS: dict = {}  # (device index, handle bytes) -> mapped block base, open once per process
+
+
+def ipc_share(t: torch.Tensor) -> tuple:
+    """(handle bytes, byte offset, numel) naming a device tensor for peers"""
+    import ctypes
+
+    h = (ctypes.c_char * 64)()
+    off = ctypes.c_int64(0)
+    _lib.check(_lib.load().mpsm_ipc_get_handle(t.data_ptr(), h, ctypes.byref(off)), "mpsm_ipc_get_handle")
+    return bytes(h), int(off.value), int(t.numel())
+
+
+def ipc_open(shared: tuple, device) -> PeerRun:
+    """map a peer's tensor into the current device (cached per block)"""
+    import ctypes
+
+    handle, off, n = shared
+    key = (torch.cuda.current_device(), handle)
+    if key not in _IPC_BLOCKS:
+        p = ctypes.c_void_p()
+        buf = (ctypes.c_char * 64).from_buffer_copy(handle)
+        _lib.check(_lib.load().mpsm_ipc_open_handle(buf, ctypes.byref(p)), "mpsm_ipc_open_handle")
+        _IPC_BLOCKS[key] = int(p.value)
+    return PeerRun(_IPC_BLOCKS[key] + off, n, device)
+
+
 class CudaBackend:
     """Device operations of one rank on its own GPU."""
 
@@ -116,13 +159,13 @@ class CudaBackend:
         return self.packed and int(self.overflow.item()) != 0
 
     def share(self, run):
-        """CUDA IPC description of a run, for peer ranks (torch's own mechanism)."""
-        from torch.multiprocessing.reductions import reduce_tensor
-
-        return [None if t is None else reduce_tensor(t) for t in run]
+        """CUDA IPC description of a run, for peer ranks (mpsm_ipc_get_handle)."""
+        return [None if t is None else ((b"", 0, 0) if t.numel() == 0 else ipc_share(t)) for t in run]
 
     def open(self, shared):
-        return tuple(None if s is None else s[0](*s[1]) for s in shared)
+        """a peer's run mapped into this rank's device (lazy NVLink peer access)"""
+        return tuple(None if s is None else (PeerRun(0, 0, self.dev) if s[2] == 0 else ipc_open(s, self.dev))
+                     for s in shared)
 
     def join(self, priv_runs, pub_runs, swap: bool, mode: int, out=None, cap: int = 0) -> torch.Tensor:
         if self.packed:

@@ -64,3 +64,39 @@ def test_device_fk_shard_join(nccl_group):
     from oracle import oracle as orc
 
     assert (res.match_count, res.aggregate_max, res.checksum) == orc.fk_gather(rk, rp, sk, sp, 1)
+
+
+@pytest.mark.gpu
+def test_ipc_handle_offset_roundtrip_in_child_process():
+    """mpsm_ipc_get_handle names the cudaMalloc block of a sub-allocated
+    tensor plus its byte offset; a second process maps it (lazy peer access)
+    and reads exactly the tensor's elements (what a peer rank's merge reads)."""
+    import subprocess
+    import sys
+
+    import torch
+
+    from paper_1207_0145_b200.distributed import ipc_share
+
+    big = torch.arange(1 << 20, dtype=torch.int64, device="cuda") * 7 + 3
+    x = big[12345:12345 + 5000]  # inside a caching-allocator block
+    torch.cuda.synchronize()
+    handle, off, n = ipc_share(x)
+    assert n == 5000 and off >= 12345 * 8
+    child = r"""
+import sys, torch
+sys.path.insert(0, sys.argv[1])
+from paper_1207_0145_b200.distributed import ipc_open
+torch.cuda.set_device(0)
+run = ipc_open((bytes.fromhex(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])), torch.device("cuda", 0))
+class A:
+    __cuda_array_interface__ = {"shape": (run.numel(),), "typestr": "<i8", "data": (run.data_ptr(), False), "version": 3}
+t = torch.as_tensor(A(), device="cuda")
+want = torch.arange(12345, 12345 + 5000, dtype=torch.int64, device="cuda") * 7 + 3
+print("OK" if bool((t == want).all()) else "MISMATCH")
+"""
+    root = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", child, root, handle.hex(), str(off), str(n)], capture_output=True,
+                       text=True, timeout=300)
+    assert "OK" in r.stdout, r.stdout + r.stderr
+    del big, x
