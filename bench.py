@@ -296,6 +296,23 @@ def impl_ours(args):
                  + 16 * (n_r + n_s))
     step_gbs = canonical / (ms / 1e3) / 1e9
 
+    # per-phase HBM roofline (the north star asks >= 60 % on the sort and
+    # merge-join phases): bytes the phase moves in this layout (count passes
+    # 8 B/tuple + scatter passes, merge reads every run once) and SURVEY
+    # 8(d)'s canonical bytes, over the phase's CUDA-event time
+    n_pub, n_priv = max(n_r, n_s), min(n_r, n_s)
+    sort_b = (8 * passes + per_tuple) if packed else (8 * passes + 32 * passes)
+    canon_sort = 8 + 32 * math.ceil(wbits / 8)
+    rec_b = 8 if packed else 16
+    phase_roof = {}
+    for name, nb, cb in (("sort_public", n_pub * sort_b, n_pub * canon_sort),
+                         ("sort_private", n_priv * sort_b, n_priv * canon_sort),
+                         ("join", (n_r + n_s) * rec_b, 16 * (n_r + n_s))):
+        t = phase[name] / args.steps
+        if t > 0:
+            phase_roof[name] = {"gbs": nb / t / 1e9, "frac": nb / t / 1e9 / peak,
+                                "canonical_gbs": cb / t / 1e9, "canonical_frac": cb / t / 1e9 / peak}
+
     e2e = None
     if not args.no_e2e:
         rh = Relation(torch.from_numpy(r.keys).pin_memory(), torch.from_numpy(r.payloads).pin_memory())
@@ -363,6 +380,7 @@ def impl_ours(args):
                      "layout": "packed 8-B records" if packed else "(key, payload) pairs", "passes_per_sort": passes,
                      "launches": os_n, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
         "step_canonical_gbs": step_gbs,
+        "phase_roofline": phase_roof,
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
         "gpu_launches": launches,
         "clocks": clk,

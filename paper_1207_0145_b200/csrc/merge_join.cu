@@ -505,6 +505,7 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                 }
             }
             __syncthreads();
+            MJ_TS(4)
             // phase 2 -- W tuples dealt round-robin (balanced, no merge
             // control flow): each matches the equal-key R group ending at
             // tile index ub - 1 (walked back; usually one tuple)
@@ -618,7 +619,7 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
             for (int st = k0; st < k1; ++st) step();
             my_pairs = e;
         }
-        MJ_TS(4)
+        if (MODE != 0) MJ_TS(4)
         if (MODE == 1) {
             const int64_t c = warp_sum((unsigned long long)my_pairs);
             if ((tid & 31) == 0) sm.warp_cnt[tid >> 5] = c;

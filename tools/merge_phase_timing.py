@@ -39,12 +39,12 @@ for _ in range(2):
 torch.cuda.synchronize()
 print("count", int(rec[0, 0].item()))
 L = _lib.load()
-ntiles = min((n_r + n_s) // 2176 + 1, 1 << 20)
+ntiles = min((n_r + n_s) // 1920 + 1, 1 << 20)
 buf = np.zeros((ntiles, 6), np.int64)
 L.mpsm_dbg_mj_ts(buf.ctypes.data_as(ctypes.c_void_p), ntiles)
 buf = buf[buf[:, 5] > 0]
 d = np.diff(buf, axis=1)
-names = ["S1+fetch+flush", "wait_data", "mergepath_search", "merge_loop", "tile_end"]
+names = ["S1+fetch+flush", "wait_data", "mergepath_search", "phase1+sync", "phase2"]
 print("tiles", len(buf), "cycles/tile median", np.median(buf[:, 5] - buf[:, 0]))
 for i, nm in enumerate(names):
     print(f"  {nm:18s} median {np.median(d[:, i]):8.0f} mean {np.mean(d[:, i]):8.0f} p90 {np.percentile(d[:, i], 90):8.0f}")
