@@ -129,11 +129,27 @@ __global__ void __launch_bounds__(THREADS) k_count(const uint64_t* __restrict__ 
     const int64_t b = sg.begin(blockIdx.x), e = sg.end(blockIdx.x);
     uint32_t run = 0;  // thread d: digit d's count in the tiles so far
     uint64_t v[ITEMS], w[ITEMS];
+    // element u of a thread's chunk share: pairs of neighbours moved with
+    // 16-B loads when the input is 16-B aligned (chunks start at TILE
+    // multiples), else single elements
+    const bool vec = ((uintptr_t)in & 15) == 0;
+    auto pos = [&](int64_t c0, int u) -> int64_t {
+        return vec ? c0 + 2 * ((u >> 1) * THREADS + tid) + (u & 1) : c0 + u * THREADS + tid;
+    };
     auto load = [&](uint64_t* x, int64_t c0) {
+        if (vec && c0 + TILE <= e) {
 #pragma unroll
-        for (int u = 0; u < ITEMS; ++u) {
-            const int64_t i = c0 + u * THREADS + tid;
-            x[u] = i < e ? ld_stream(in + i) : 0;
+            for (int u = 0; u < ITEMS; u += 2) {
+                const ulonglong2 q = __ldcs(reinterpret_cast<const ulonglong2*>(in + pos(c0, u)));
+                x[u] = q.x;
+                x[u + 1] = q.y;
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < ITEMS; ++u) {
+                const int64_t i = pos(c0, u);
+                x[u] = i < e ? ld_stream(in + i) : 0;
+            }
         }
     };
     if (b < e) load(v, b);
@@ -142,7 +158,7 @@ __global__ void __launch_bounds__(THREADS) k_count(const uint64_t* __restrict__ 
         if (c0 + TILE < e) load(w, c0 + TILE);  // next chunk in flight during this one
 #pragma unroll
         for (int u = 0; u < ITEMS; ++u) {
-            const int64_t i = c0 + u * THREADS + tid;
+            const int64_t i = pos(c0, u);
             if (i < e) {
                 if (d_bad && v[u] - dig.lower > span_m1) atomicMin(d_bad, (unsigned long long)i);
                 atomicAdd(&h[k][dig(v[u])], 1u);
@@ -210,6 +226,7 @@ struct Smem {
     uint64_t bar[NST];                   // bulk-copy completion, per buffer
 };
 static_assert(THREADS == MAX_BINS, "the digit scan gives each thread one digit");
+static_assert(ITEMS % 2 == 0, "count loads element pairs");
 static_assert(WARPS % 2 == 0 && WARPS <= 32, "two warps per histogram word");
 
 // lanes of the warp holding the same digit (fallback ranking: 9 ballots)
