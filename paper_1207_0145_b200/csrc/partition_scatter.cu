@@ -1,23 +1,15 @@
-// radix_sort.cu -- onesweep LSD radix sort of (u64 key, u64 payload) SoA pairs
-// and the stable partition scatter, for sm_100a.
+// partition_scatter.cu -- the private-input partition scatter for sm_100a:
+// every tuple of a worker's chunk goes to the arena region of its partition
+// (splitter-vector lookup of its radix bucket), stable, so the arena layout
+// is exactly the reference's (worker regions in input order).  Replaces
+// _kernels.scatter_chunk (/root/reference/pkg/src/mpsm/_kernels.py:262-284).
 //
-// Replaces the reference run sort _kernels.three_phase_sort
-// (/root/reference/pkg/src/mpsm/_kernels.py:217-244; MSD radix cluster +
-// introsort + insertion pass on CPU) and the private-input scatter
-// _kernels.scatter_chunk (_kernels.py:262-284).
-//
-// Sort = one upfront sweep that histograms every digit of every pass and
-// checks the key domain (8 B/tuple), then one scatter pass per digit
-// (16 B read + 16 B write per tuple).  Each pass is a single kernel: tiles
-// take a ticket in launch order, rank their keys stably per digit with warp
-// match_any, publish per-digit tile counts, resolve their global offsets with
-// a decoupled look-back over predecessor tiles, stage the tile in shared
-// memory in digit order and write it out with coalesced runs.
-//
-// The partition scatter is the same pass with digit = partition id
-// (splitter-vector lookup of the radix bucket) and per-partition base
-// offsets = the worker's write cursors, so the arena layout is exactly the
-// reference's (worker regions in input order).
+// One kernel: tiles take a ticket in launch order, rank their tuples stably
+// per partition with warp ballots, publish per-partition tile counts,
+// resolve their global offsets with a decoupled look-back over predecessor
+// tiles (few partitions: short chains), stage the tile in shared memory in
+// partition order and write it out in coalesced runs.  (This was the first
+// design of the run sort too; segsort.cu replaced it there.)
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -29,28 +21,18 @@
 
 namespace mpsm {
 
-// tile shape and digit width (compile-time; tools/variants.py builds variants)
 #ifndef MPSM_SORT_THREADS
 #define MPSM_SORT_THREADS 512
 #endif
 #ifndef MPSM_SORT_ITEMS
 #define MPSM_SORT_ITEMS 12
 #endif
-#ifndef MPSM_SORT_MAX_BITS
-#define MPSM_SORT_MAX_BITS 9
-#endif
-#ifndef MPSM_SORT_MIN_BLOCKS
-#define MPSM_SORT_MIN_BLOCKS 2
-#endif
 constexpr int SORT_THREADS = MPSM_SORT_THREADS;
 constexpr int SORT_ITEMS = MPSM_SORT_ITEMS;
 constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;
 constexpr int SORT_WARPS = SORT_THREADS / 32;
-constexpr int MAX_BITS = MPSM_SORT_MAX_BITS;
+constexpr int MAX_BITS = 9;  // at most 512 partitions
 constexpr int MAX_BINS = 1 << MAX_BITS;
-constexpr int MAX_PASSES = 8;
-constexpr int HIST_THREADS = 512;
-constexpr int HIST_UNROLL = 8;
 
 // look-back status word: [63:62] flag, [61:40] epoch, [39:0] count
 constexpr uint64_t FLAG_AGG = 1ull << 62;
@@ -59,27 +41,7 @@ constexpr uint64_t VALUE_MASK = (1ull << 40) - 1;
 constexpr int EPOCH_SHIFT = 40;
 constexpr uint64_t EPOCH_MASK = (1ull << 22) - 1;
 
-struct PassPlan {
-    int npasses;
-    int shift[MAX_PASSES];
-    int bits[MAX_PASSES];
-};
-
-static PassPlan plan_passes(int width_bits) {
-    PassPlan p{};
-    if (width_bits <= 0) return p;
-    int np = (width_bits + MAX_BITS - 1) / MAX_BITS;
-    int base = width_bits / np, rem = width_bits % np, sh = 0;
-    p.npasses = np;
-    for (int i = 0; i < np; ++i) {
-        p.bits[i] = base + (i < rem ? 1 : 0);
-        p.shift[i] = sh;
-        sh += p.bits[i];
-    }
-    return p;
-}
-
-// process-wide epoch so stale look-back words from earlier passes never match
+// process-wide epoch so stale look-back words from earlier calls never match
 static uint32_t next_epoch(bool* wrapped) {
     static std::atomic<uint32_t> epoch{0};
     uint32_t e = (epoch.fetch_add(1) + 1) & (uint32_t)EPOCH_MASK;
@@ -87,77 +49,6 @@ static uint32_t next_epoch(bool* wrapped) {
     if (e == 0) e = (epoch.fetch_add(1) + 1) & (uint32_t)EPOCH_MASK;
     return e;
 }
-
-// ------------------------------------------------------------ upfront sweep
-// one read of every key: digit histograms of all passes + domain check.
-// HIST_UNROLL independent coalesced loads per thread keep enough bytes in
-// flight (the first version waited on one load per iteration).
-__global__ void __launch_bounds__(HIST_THREADS) k_upfront_hist(const uint64_t* __restrict__ keys, int64_t n,
-                                                               uint64_t lower, uint64_t span_m1, PassPlan plan,
-                                                               unsigned long long* __restrict__ g_hist,
-                                                               unsigned long long* __restrict__ d_bad) {
-    __shared__ uint32_t sh[MAX_PASSES * MAX_BINS];
-    const int nb = plan.npasses * MAX_BINS;
-    for (int i = threadIdx.x; i < nb; i += blockDim.x) sh[i] = 0;
-    __syncthreads();
-    constexpr int CHUNK = HIST_THREADS * HIST_UNROLL;
-    for (int64_t base = (int64_t)blockIdx.x * CHUNK; base < n; base += (int64_t)gridDim.x * CHUNK) {
-        uint64_t k[HIST_UNROLL];
-#pragma unroll
-        for (int u = 0; u < HIST_UNROLL; ++u) {
-            int64_t i = base + u * HIST_THREADS + threadIdx.x;
-            k[u] = i < n ? ld_stream(keys + i) : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < HIST_UNROLL; ++u) {
-            int64_t i = base + u * HIST_THREADS + threadIdx.x;
-            if (i >= n) continue;
-            uint64_t nk = k[u] - lower;
-            // out-of-domain keys are flagged but still counted so the scatter
-            // passes stay in bounds; the caller discards the result
-            if (nk > span_m1 && d_bad) atomicMin(d_bad, (unsigned long long)i);
-#pragma unroll
-            for (int p = 0; p < MAX_PASSES; ++p) {
-                if (p < plan.npasses) {
-                    uint32_t d = (uint32_t)(nk >> plan.shift[p]) & ((1u << plan.bits[p]) - 1u);
-                    atomicAdd(&sh[p * MAX_BINS + d], 1u);
-                }
-            }
-        }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < nb; i += blockDim.x)
-        if (sh[i]) atomicAdd(&g_hist[i], (unsigned long long)sh[i]);
-}
-
-// exclusive scan of each pass's histogram -> bucket start offsets
-__global__ void __launch_bounds__(MAX_BINS) k_bucket_starts(const unsigned long long* __restrict__ g_hist,
-                                                            PassPlan plan, int64_t* __restrict__ starts) {
-    __shared__ int64_t s[MAX_BINS];
-    const int p = blockIdx.x;
-    const int nbins = 1 << plan.bits[p];
-    const int t = threadIdx.x;
-    int64_t v = (t < nbins) ? (int64_t)g_hist[p * MAX_BINS + t] : 0;
-    s[t] = v;
-    __syncthreads();
-    for (int off = 1; off < MAX_BINS; off <<= 1) {
-        int64_t add = (t >= off) ? s[t - off] : 0;
-        __syncthreads();
-        s[t] += add;
-        __syncthreads();
-    }
-    if (t < nbins) starts[p * MAX_BINS + t] = s[t] - v;
-}
-
-// ---------------------------------------------------------------- digit ops
-struct RadixDigit {
-    uint64_t lower;
-    int shift;
-    uint32_t mask;
-    __device__ __forceinline__ uint32_t operator()(uint64_t key) const {
-        return (uint32_t)((key - lower) >> shift) & mask;
-    }
-};
 
 struct PartitionDigit {
     uint64_t lower;
@@ -188,18 +79,9 @@ struct PassSmem {
     uint32_t ticket;
 };
 
-__device__ __forceinline__ void ld_volatile_v2(const uint64_t* p, uint64_t& a, uint64_t& b) {
-    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
-}
-
 // peers of this lane among the lanes of vmask holding the same digit: one
 // ballot per digit bit (cheaper than match.any on sm_100)
 __device__ __forceinline__ unsigned ballot_match(uint32_t d, int bits, unsigned vmask) {
-#if defined(MPSM_DBG_NO_MATCH)
-    return vmask & (1u << (threadIdx.x & 31));
-#elif defined(MPSM_SORT_MATCH_ANY)
-    return __match_any_sync(0xffffffffu, d) & vmask;
-#endif
     unsigned peers = vmask;
 #pragma unroll
     for (int b = 0; b < MAX_BITS; ++b) {
@@ -212,32 +94,12 @@ __device__ __forceinline__ unsigned ballot_match(uint32_t d, int bits, unsigned 
     return peers;
 }
 
-#ifdef MPSM_DBG_TIMING
-__device__ long long g_phase_ts[1 << 22][8];
-#define PHASE_TS(i) \
-    if (tid == 0 && tile < (1u << 22)) g_phase_ts[tile][i] = clock64();
-#else
-#define PHASE_TS(i)
-#endif
-
-// pass layouts: (key, payload) SoA in and out; SoA in -> packed records out
-// (the first pass of a packed sort); packed in and out.  A packed record is
-// (key - lower) << pw | payload with pw = 64 - width_bits, valid when every
-// payload < 2^pw; the sort then moves 8 B per tuple instead of 16.
-enum PassLayout { PASS_SS = 0, PASS_SP = 1, PASS_PP = 2 };
-
-struct PackSpec {
-    uint64_t lower;
-    int pw;
-    unsigned int* overflow;  // set to 1 if some payload does not fit pw bits
-};
-
-template <class DigitOp, int PM = PASS_SS>
-__global__ void __launch_bounds__(SORT_THREADS, MPSM_SORT_MIN_BLOCKS) k_onesweep(
+template <class DigitOp>
+__global__ void __launch_bounds__(SORT_THREADS, 2) k_onesweep(
     const uint64_t* __restrict__ in_k, const uint64_t* __restrict__ in_p, uint64_t* __restrict__ out_k,
     uint64_t* __restrict__ out_p, int64_t n, DigitOp digit, int bits, int nbins, const int64_t* __restrict__ bin_base,
     uint64_t* __restrict__ status, int64_t st_stride, unsigned int* __restrict__ ticket_ctr, uint32_t epoch,
-    int64_t* __restrict__ written, PackSpec pk = PackSpec{0, 0, nullptr}) {
+    int64_t* __restrict__ written) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PassSmem& sm = *reinterpret_cast<PassSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -249,7 +111,6 @@ __global__ void __launch_bounds__(SORT_THREADS, MPSM_SORT_MIN_BLOCKS) k_onesweep
     const int64_t tile_base = (int64_t)tile * SORT_TILE;
     const int64_t warp_base = tile_base + (int64_t)warp * (32 * SORT_ITEMS);
     const bool full = tile_base + SORT_TILE <= n;
-    PHASE_TS(0)
 
     // ---- keys, warp-striped: item k of lane l is warp_base + 32k + l
     uint64_t key[SORT_ITEMS];
@@ -259,7 +120,6 @@ __global__ void __launch_bounds__(SORT_THREADS, MPSM_SORT_MIN_BLOCKS) k_onesweep
         const int64_t idx = warp_base + 32 * k + lane;
         key[k] = (full || idx < n) ? ld_stream(in_k + idx) : 0;
     }
-    PHASE_TS(1)
     // ---- stable rank within the warp: ballot match + running per-warp counts
     uint32_t* wh = sm.u.whist[warp];
     const unsigned lt = lanemask_lt();
@@ -280,7 +140,6 @@ __global__ void __launch_bounds__(SORT_THREADS, MPSM_SORT_MIN_BLOCKS) k_onesweep
     }
     __syncthreads();
 
-    PHASE_TS(2)
     // ---- per digit (DPT per thread): column sum (independent loads), publish
     // the aggregate as early as possible, then the exclusive scan over warps
     constexpr int DPT = (MAX_BINS + SORT_THREADS - 1) / SORT_THREADS;
@@ -333,18 +192,13 @@ __global__ void __launch_bounds__(SORT_THREADS, MPSM_SORT_MIN_BLOCKS) k_onesweep
             run += c;
         }
     }
-    PHASE_TS(3)
     // ---- decoupled look-back for this thread's digits, two predecessors per step
 #pragma unroll
     for (int j = 0; j < DPT; ++j) {
         const int d = tid + j * SORT_THREADS;
         if (d < nbins) {
             uint64_t excl = 0;
-#ifdef MPSM_DBG_NO_LOOKBACK
-            if (false) {
-#else
             if (tile > 0) {
-#endif
                 int64_t t = (int64_t)tile - 1;
                 while (true) {
                     const uint64_t w1 = ld_volatile_u64(status + (size_t)t * nbins + d);
@@ -367,7 +221,6 @@ __global__ void __launch_bounds__(SORT_THREADS, MPSM_SORT_MIN_BLOCKS) k_onesweep
         }
     }
     __syncthreads();
-    PHASE_TS(4)
     for (int d = tid; d < nbins; d += SORT_THREADS) sm.gdelta[d] -= (int64_t)sm.tile_off[d];
     // ---- staging positions (whist now holds the warp-exclusive offsets);
     // the digit stays in bits 20.. for the write-out
@@ -377,21 +230,6 @@ __global__ void __launch_bounds__(SORT_THREADS, MPSM_SORT_MIN_BLOCKS) k_onesweep
             const uint32_t dk = pos[k] >> 20;
             pos[k] = (dk << 20) | (sm.tile_off[dk] + sm.u.whist[warp][dk] + (pos[k] & 0xfffffu));
         }
-    }
-    if (PM == PASS_SP) {
-        // pack (key - lower) << pw | payload in registers
-        uint64_t ovf = 0;
-#pragma unroll
-        for (int k = 0; k < SORT_ITEMS; ++k) {
-            const int64_t idx = warp_base + 32 * k + lane;
-            const uint64_t pay = (full || idx < n) ? ld_stream(in_p + idx) : 0;
-            ovf |= pay >> pk.pw;
-            // a payload wider than pw bits is masked so the key bits (and with
-            // them every later pass's digit counts) stay exact; the caller
-            // sees the overflow flag and redoes the join on pairs
-            key[k] = ((key[k] - pk.lower) << pk.pw) | (pay & ((1ull << pk.pw) - 1ull));
-        }
-        if (__any_sync(0xffffffffu, ovf != 0) && lane == 0) atomicOr(pk.overflow, 1u);
     }
     __syncthreads();  // whist dead from here; stage aliases it
 #pragma unroll
@@ -403,12 +241,8 @@ __global__ void __launch_bounds__(SORT_THREADS, MPSM_SORT_MIN_BLOCKS) k_onesweep
         }
     }
     __syncthreads();
-    PHASE_TS(5)
     const int valid_in_tile = full ? SORT_TILE : (int)(n - tile_base);
-    if (PM != PASS_SS) {
-#pragma unroll 4
-        for (int i = tid; i < valid_in_tile; i += SORT_THREADS) out_k[sm.gdelta[sm.dig[i]] + i] = sm.u.stage[i];
-    } else {
+    {
         // payload loads go out now and land while the keys are written
         uint64_t pay[SORT_ITEMS];
 #pragma unroll
@@ -426,77 +260,28 @@ __global__ void __launch_bounds__(SORT_THREADS, MPSM_SORT_MIN_BLOCKS) k_onesweep
 #pragma unroll 4
         for (int i = tid; i < valid_in_tile; i += SORT_THREADS) out_p[sm.gdelta[sm.dig[i]] + i] = sm.u.stage[i];
     }
-    PHASE_TS(6)
 }
 
 static size_t pass_smem_bytes() { return sizeof(PassSmem); }
 
 static int64_t num_tiles(int64_t n) { return (n + SORT_TILE - 1) / SORT_TILE; }
-// look-back rows of the persistent kernel are 32-B aligned
+// look-back rows are 32-B aligned
 static int64_t status_stride(int64_t n) { return (std::max<int64_t>(num_tiles(n), 1) + 3) & ~(int64_t)3; }
-
-struct SortWorkspace {
-    unsigned long long* hist;  // [MAX_PASSES][MAX_BINS]
-    int64_t* starts;           // [MAX_PASSES][MAX_BINS]
-    unsigned int* tickets;     // [MAX_PASSES]
-    uint64_t* status;          // [tiles][MAX_BINS]
-};
-
-static size_t sort_ws_bytes(int64_t n) {
-    size_t b = 0;
-    b += align_up(sizeof(unsigned long long) * MAX_PASSES * MAX_BINS);
-    b += align_up(sizeof(int64_t) * MAX_PASSES * MAX_BINS);
-    b += align_up(sizeof(unsigned int) * MAX_PASSES);
-    b += align_up(sizeof(uint64_t) * (size_t)status_stride(n) * MAX_BINS);
-    return b;
-}
-
-static bool carve_sort(void* ws, size_t bytes, int64_t n, SortWorkspace* out) {
-    Carve c{(char*)ws, bytes};
-    out->hist = c.take<unsigned long long>(MAX_PASSES * MAX_BINS);
-    out->starts = c.take<int64_t>(MAX_PASSES * MAX_BINS);
-    out->tickets = c.take<unsigned int>(MAX_PASSES);
-    out->status = c.take<uint64_t>((size_t)status_stride(n) * MAX_BINS);
-    return c.ok;
-}
 
 static int set_pass_smem() {
     static bool done = false;
     if (!done) {
-        MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_onesweep<RadixDigit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  (int)pass_smem_bytes()),
-                             "smem attr"));
         MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_onesweep<PartitionDigit>,
                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem_bytes()),
                              "smem attr"));
-        MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_onesweep<RadixDigit, PASS_SP>,
-                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem_bytes()),
-                             "smem attr"));
-        MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_onesweep<RadixDigit, PASS_PP>,
-                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem_bytes()),
-                             "smem attr"));
-
         done = true;
     }
     return MPSM_OK;
 }
 
-static int clear_status_if_wrapped(bool wrapped, uint64_t* status, int64_t n, cudaStream_t st) {
-    if (!wrapped) return MPSM_OK;
-    return cuda_status(
-        cudaMemsetAsync(status, 0, sizeof(uint64_t) * (size_t)status_stride(n) * MAX_BINS, st),
-        "memset status");
-}
-
 }  // namespace mpsm
 
 using namespace mpsm;
-
-#ifdef MPSM_DBG_TIMING
-extern "C" int mpsm_dbg_phase_ts(long long* host, int ntiles) {
-    return cuda_status(cudaMemcpyFromSymbol(host, g_phase_ts, sizeof(long long) * 8 * (size_t)ntiles), "dbg");
-}
-#endif
 
 // ------------------------------------------------------------ partition scatter
 extern "C" int mpsm_scatter_workspace_bytes(int64_t n, int npart, size_t* bytes) {

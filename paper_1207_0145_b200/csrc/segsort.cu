@@ -13,7 +13,8 @@
 //            while tile i is ranked (stable, warp ballots), staged in digit
 //            order and written out as coalesced runs at running per-digit
 //            cursors.  No CTA waits for another: this replaces the decoupled
-//            look-back of radix_sort.cu, whose latency chain held that kernel
+//            look-back of the first design (kept for the partition scatter,
+//            partition_scatter.cu), whose latency chain held that kernel
 //            to ~35 % of HBM bandwidth although the scatter write pattern
 //            itself runs at 6 TB/s (tools/scatter_pattern_bench.cu).
 //

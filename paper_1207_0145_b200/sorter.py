@@ -1,8 +1,8 @@
 """Run sorting on the GPU, mirroring /root/reference/pkg/src/mpsm/sorter.py.
 
 The reference sorts a run with a three-phase CPU algorithm (MSD radix pass,
-introsort, insertion pass).  Here every entry point is the onesweep LSD radix
-sort of csrc/radix_sort.cu over the width_bits significant bits of
+introsort, insertion pass).  Here every entry point is the segmented LSD radix
+sort of csrc/segsort.cu over the width_bits significant bits of
 (key - lower).  The three-phase helpers keep their names and contracts:
 ``radix_msd_pass`` clusters by the top min(8, w) bits (a stable partition
 scatter), ``introsort`` / ``insertion_pass`` sort the given range.  Sorting is
