@@ -1,27 +1,31 @@
-// segsort.cu -- segmented reduce-then-scan LSD radix sort for sm_100a.
+// segsort.cu -- reduce-then-scan LSD radix sort for sm_100a.
 //
 // The run sort of the join (replaces _kernels.three_phase_sort,
-// /root/reference/pkg/src/mpsm/_kernels.py:217-244).  Per digit pass:
+// /root/reference/pkg/src/mpsm/_kernels.py:217-244).  Digits of <= 9 bits;
+// per digit pass:
 //
-//   count    one CTA per contiguous input segment counts the segment's digits
-//            (8 B read per tuple; for the first pass this sweep also checks
-//            the key domain)
-//   scan     per (segment, digit) base offsets: digit start + counts of the
-//            same digit in earlier segments
-//   scatter  the same CTA/segment pairing streams its segment tile by tile:
-//            cp.async double buffering brings tile i+1 into shared memory
-//            while tile i is ranked (stable, warp ballots), staged in digit
-//            order and written out as coalesced runs at running per-digit
-//            cursors.  No CTA waits for another: this replaces the decoupled
-//            look-back of the first design (kept for the partition scatter,
-//            partition_scatter.cu), whose latency chain held that kernel
-//            to ~35 % of HBM bandwidth although the scatter write pattern
-//            itself runs at 6 TB/s (tools/scatter_pattern_bench.cu).
+//   count    one CTA per contiguous input segment (4 per SM) counts the
+//            digits of every scatter tile of its segment and writes each
+//            tile's segment-local digit prefixes (8 B read per tuple; the
+//            first pass also checks the key domain)
+//   scan     per (segment, digit) base offsets and digit totals
+//   scatter  persistent CTAs take tiles IN GLOBAL ORDER from an atomic tile
+//            dispenser, so tiles in flight are neighbours and their runs of
+//            one digit land next to each other (per-CTA segments halved the
+//            write bandwidth, tools/scatter_pattern_bench.cu).  Thread 0
+//            brings tile i+1 (tuples + digit prefixes) into shared memory with
+//            TMA bulk copies while tile i is ranked -- one shared atomicAdd
+//            per tuple into per-warp 16-bit histogram rows gives a stable
+//            rank (lane-ordered atomics, probed at start-up; warp-ballot
+//            fallback) -- scanned, staged in digit order in place and written
+//            out in coalesced runs.  No CTA waits for another (the decoupled
+//            look-back of the first design, kept for the partition scatter in
+//            partition_scatter.cu, held that kernel to ~35 % of HBM).
 //
 // Layouts: (key, payload) pairs throughout (SS); pairs in -> packed 8-B
 // records (key - lower) << pw | payload out (SP, first pass of a packed sort);
-// records in and out (PP).  Packed records halve the bytes of every later
-// pass and of the merge join.
+// records in and out (PP, 8192-tuple tiles).  Packed records halve the bytes
+// of every later pass and of the merge join.
 
 #include <cuda_runtime.h>
 #include <stdint.h>
