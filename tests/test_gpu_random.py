@@ -19,6 +19,7 @@ from paper_1207_0145_b200 import engine  # noqa: E402
 from paper_1207_0145_b200.core import JoinConfig, KeyDomain, Relation  # noqa: E402
 from oracle import oracle as orc  # noqa: E402
 
+CAP = 1 << 24  # materialize cap
 STATS = ("tuples_sorted_public", "tuples_sorted_private", "tuples_scattered", "public_tuples_examined",
          "probe_tuples_examined", "s_runs_with_matches")
 
@@ -55,6 +56,7 @@ for _i in range(96):
         wide=bool(_rng.random() < 0.2),  # 64-bit payloads: the packed path must fall back
         device_inputs=bool(_rng.random() < 0.4),
         pack=str(_rng.choice(["host", "device", "pairs"])),
+        mode=str(_rng.choice(["aggregate-max", "aggregate-max", "count", "materialize"])),
     ))
 
 
@@ -73,11 +75,17 @@ def test_random_join_matches_oracle(case, monkeypatch):
     upper = lower + span
     try:
         want = orc.join(rk, rp, sk, sp, threads=case["threads"], lower=lower, upper=upper, radix_bits=10,
-                        algorithm=case["algorithm"], role_policy=case["role"])
+                        algorithm=case["algorithm"], role_policy=case["role"], query_mode=case["mode"],
+                        materialize_cap=CAP)
+    except OverflowError:  # more pairs than the cap: skip the materialize comparison
+        case = dict(case, mode="count")
+        want = orc.join(rk, rp, sk, sp, threads=case["threads"], lower=lower, upper=upper, radix_bits=10,
+                        algorithm=case["algorithm"], role_policy=case["role"], query_mode="count")
     except ValueError as exc:
         if "s_span" in str(exc):
             # the reference's float artifact in its CDF (skew.py:150, DESIGN.md
             # section 2): we clamp the span; the totals are T-independent
+            case = dict(case, mode="aggregate-max")
             want = orc.join(rk, rp, sk, sp, threads=1, lower=lower, upper=upper, radix_bits=10,
                             algorithm=case["algorithm"], role_policy=case["role"])
             want.worker_stats = None
@@ -92,7 +100,8 @@ def test_random_join_matches_oracle(case, monkeypatch):
     else:
         r, s = Relation(rk, rp), Relation(sk, sp)
     cfg = JoinConfig(threads=case["threads"], algorithm=case["algorithm"], role_policy=case["role"],
-                     key_domain=KeyDomain(lower, upper), radix_bits=10)
+                     key_domain=KeyDomain(lower, upper), radix_bits=10, query_mode=case["mode"],
+                     materialize_cap=CAP)
     with warnings.catch_warnings():
         warnings.simplefilter("ignore")
         if want is None:
@@ -103,6 +112,10 @@ def test_random_join_matches_oracle(case, monkeypatch):
     assert got.match_count == want.match_count
     assert got.aggregate_max == want.aggregate_max
     assert got.checksum == want.checksum
+    if case["mode"] == "materialize":
+        g = got.materialized[np.lexsort((got.materialized[:, 1], got.materialized[:, 0]))]
+        w = want.materialized[np.lexsort((want.materialized[:, 1], want.materialized[:, 0]))]
+        assert np.array_equal(g, w)
     if want.worker_stats is None:
         return
     assert len(got.worker_stats) == len(want.worker_stats)
