@@ -221,6 +221,13 @@ int mpsm_deinterleave(const uint64_t* d_records, int64_t n, uint64_t* d_keys, ui
 int mpsm_upload_records(const uint64_t* h_keys, const uint64_t* h_pays, int64_t n, uint64_t lower,
                         uint64_t span_m1, int width_bits, uint64_t* d_rec, int threads, int gpu_pack_every,
                         void* stream, int64_t* bad_index, int* overflow);
+/* device (key, payload) columns -> packed records (before an exchange: the
+ * multi-GPU all-to-all moves 8 B per tuple).  Same domain / payload-width
+ * checks as mpsm_upload_records, reported through device flags: *d_bad =
+ * atomicMin of the first out-of-domain index, *d_overflow |= 1. */
+int mpsm_pack_records(const uint64_t* d_keys, const uint64_t* d_pays, int64_t n, uint64_t lower, uint64_t span_m1,
+                      int width_bits, uint64_t* d_rec, unsigned long long* d_bad, unsigned int* d_overflow,
+                      void* stream);
 /* host->device bytes moved by mpsm_upload_records since the last reset
  * (8 per host-packed tuple, 16 per tuple the GPU packs from mapped memory) */
 uint64_t mpsm_upload_bytes(int reset);

@@ -292,3 +292,14 @@ extern "C" int mpsm_upload_records(const uint64_t* h_keys, const uint64_t* h_pay
 extern "C" uint64_t mpsm_upload_bytes(int reset) {
     return reset ? g_upload_bytes.exchange(0) : g_upload_bytes.load();
 }
+
+extern "C" int mpsm_pack_records(const uint64_t* d_keys, const uint64_t* d_pays, int64_t n, uint64_t lower,
+                                 uint64_t span_m1, int width_bits, uint64_t* d_rec, unsigned long long* d_bad,
+                                 unsigned int* d_overflow, void* stream) {
+    if (n < 0 || width_bits < 1 || width_bits > 63 || !d_bad || !d_overflow) return MPSM_ERR_ARG;
+    if (n == 0) return MPSM_OK;
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
+    k_pack_mapped<<<grid, 256, 0, (cudaStream_t)stream>>>(d_keys, d_pays, n, 0, lower, span_m1, 64 - width_bits, d_rec,
+                                                          d_bad, d_overflow);
+    return check_launch("k_pack_mapped");
+}

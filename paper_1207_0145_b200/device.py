@@ -127,6 +127,16 @@ def sort_records(in_rec: torch.Tensor, width_bits: int, out_rec: torch.Tensor, t
                                    stream_ptr()), "mpsm_sort_records")
 
 
+def pack_records(keys: torch.Tensor, pays: torch.Tensor, lower: int, span_m1: int, width_bits: int,
+                 out_rec: torch.Tensor, bad: torch.Tensor, overflow: torch.Tensor) -> None:
+    """device columns -> packed records; domain / payload-width flags on device"""
+    n = int(keys.numel())
+    if n == 0:
+        return
+    _lib.check(_lib.load().mpsm_pack_records(ptr(keys), ptr(pays), n, lower, span_m1, width_bits, ptr(out_rec),
+                                             ptr(bad), ptr(overflow), stream_ptr()), "mpsm_pack_records")
+
+
 def host_columns(a):
     """A host uint64 column as (keep-alive object, address), or None if `a`
     is not host-resident."""

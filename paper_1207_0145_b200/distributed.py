@@ -152,6 +152,21 @@ class CudaBackend:
                         npart, torch.from_numpy(starts.astype(np.int64)).to(self.dev), sk, spay, written)
         return sk, spay
 
+    def pack(self, k, p):
+        """(key, payload) columns -> packed records for the exchange, or None
+        when the join runs on pairs"""
+        if not self.packed:
+            return None
+        rec = self.empty(int(k.numel()))
+        D.pack_records(k, p, self.dom.lower, self.span_m1, self.wbits, rec, self.bad, self.overflow)
+        return rec
+
+    def sort_records(self, rec):
+        n = int(rec.numel())
+        out, tmp = self.empty(n), self.empty(n)
+        D.sort_records(rec, self.wbits, out, tmp)
+        return (out, None)
+
     def bad_index(self) -> int:
         return int(self.bad.item())
 
@@ -205,6 +220,14 @@ def _alltoall(be, k, p, send_counts, recv_counts, group):
     return rk.view(torch.uint64), rp.view(torch.uint64)
 
 
+def _alltoall_one(be, x, send_counts, recv_counts, group):
+    """all-to-all(v) of one u64 column (packed records); source-rank order."""
+    out = torch.empty(int(recv_counts.sum()), dtype=torch.int64, device=be.comm_device)
+    dist.all_to_all_single(out, x.view(torch.int64), [int(v) for v in recv_counts], [int(v) for v in send_counts],
+                           group=group)
+    return out.view(torch.uint64)
+
+
 def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=None, backend=None,
                          timings: Optional[dict] = None) -> JoinResult:
     """P-MPSM over the ranks of `group`; r and s are this rank's shards.
@@ -254,10 +277,16 @@ def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=Non
     np.cumsum(send_counts[:-1], out=send_starts[1:])
     # 4-5: scatter into send segments, one all-to-all
     sk, sp = be.partition(pk, pp, shift, ss.vector.sp, G, send_starts)
-    rk, rp = _alltoall(be, sk, sp, send_counts, recv_counts, group)
+    rec = be.pack(sk, sp) if hasattr(be, "pack") else None
+    if rec is not None:  # packed join: one all-to-all of 8-B records
+        rr = _alltoall_one(be, rec, send_counts, recv_counts, group)
+        n_recv_priv = int(rr.numel())
+    else:
+        rk, rp = _alltoall(be, sk, sp, send_counts, recv_counts, group)
+        n_recv_priv = int(rk.numel())
     t_part = time.perf_counter()
     # 6: private run
-    priv_run = be.sort(rk, rp)
+    priv_run = be.sort_records(rr) if rec is not None else be.sort(rk, rp)
     be.sync()
     t_sort = time.perf_counter()
     # 7: join against every public run (remote ones through peer mappings)
@@ -268,9 +297,9 @@ def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=Non
         pub_runs = [pub_run]
     mode = {"aggregate-max": _lib.MODE_AGGREGATE_MAX, "count": _lib.MODE_COUNT,
             "materialize": _lib.MODE_COUNT}[cfg.query_mode]
-    rec = be.records(be.join([priv_run], pub_runs, roles.swapped, mode))
+    rec_h = be.records(be.join([priv_run], pub_runs, roles.swapped, mode))
     overflow = be.overflowed()
-    gathered = _gather_obj((rec, int(rk.numel()), overflow), group)
+    gathered = _gather_obj((rec_h, n_recv_priv, overflow), group)
     if any(g[2] for g in gathered):
         # a payload is wider than a packed record allows: redo on pairs
         be2 = type(be)(packed=False) if isinstance(be, CudaBackend) else be.unpacked()
@@ -306,7 +335,7 @@ def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=Non
     if cfg.query_mode == "materialize":
         if count > cfg.materialize_cap:
             raise MaterializeCapExceeded(f"join produced {count} pairs, cap is {cfg.materialize_cap}")
-        mine = int(sum(int(x) for x in rec.reshape(G, _lib.PAIR_FIELDS)[:, _lib.PAIR_COUNT]))
+        mine = int(sum(int(x) for x in rec_h.reshape(G, _lib.PAIR_FIELDS)[:, _lib.PAIR_COUNT]))
         local = be.materialize([priv_run], pub_runs, roles.swapped, mine)
         parts = _gather_obj(local, group)
         materialized = np.concatenate(parts, axis=0) if parts else np.empty((0, 2), np.uint64)
