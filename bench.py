@@ -87,13 +87,14 @@ def make_inputs(name: str, seed: int = 0):
 
 # ------------------------------------------------------------ clocks sampler
 class Clocks:
-    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    QUERY = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
         self.proc = None
+        self.window = None  # (t0, t1) wall-clock bounds of the timed region
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
 
     def start(self):
@@ -101,11 +102,15 @@ class Clocks:
             os.makedirs(os.path.dirname(self.path), exist_ok=True)
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.QUERY}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.fh,
+                                          "--format=csv,noheader,nounits", "-lms", "20"], stdout=self.fh,
                                          stderr=subprocess.DEVNULL)
         except Exception as exc:  # nvidia-smi missing
             log("clock sampling unavailable:", exc)
             self.proc = None
+
+    def mark(self, t0: float, t1: float) -> None:
+        """the timed region; samples outside it are dropped"""
+        self.window = (t0, t1)
 
     def stop(self) -> dict:
         if self.proc is None:
@@ -118,19 +123,30 @@ class Clocks:
         self.fh.close()
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        import datetime
+
+        rows = []
         with open(self.path) as fh:
             for line in fh:
                 f = [x.strip() for x in line.split(",")]
-                if len(f) < 9:
+                if len(f) < 10:
                     continue
                 try:
-                    sm.append(float(f[1]))
-                    mx = float(f[2])
+                    ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                    rows.append((ts, float(f[2]), float(f[3]), f[6:10]))
                 except ValueError:
                     continue
-                for nm, v in zip(names, f[5:9]):
-                    if v.lower() == "active":
-                        reasons.add(nm)
+        if self.window and rows:
+            t0, t1 = self.window
+            inside = [r for r in rows if t0 - 0.02 <= r[0] <= t1 + 0.02]
+            # a timed region shorter than the sampling period: nearest samples
+            rows = inside or sorted(rows, key=lambda r: abs(r[0] - (t0 + t1) / 2))[:2]
+        for _, smv, mxv, flags in rows:
+            sm.append(smv)
+            mx = mxv
+            for nm, v in zip(names, flags):
+                if v.lower() == "active":
+                    reasons.add(nm)
         try:
             os.remove(self.path)
         except OSError:
@@ -241,6 +257,8 @@ def impl_ours(args):
     sd = Relation(torch.from_numpy(s.keys).to(dev), torch.from_numpy(s.payloads).to(dev))
     cfg = JoinConfig(threads=1, algorithm="p-mpsm", key_domain=dom)
 
+    clocks = Clocks(local)
+    clocks.start()  # sampling runs from before the warm-up; samples are kept for the timed region only
     for _ in range(args.warmup):
         res = P.run_join(rd, sd, cfg)
     torch.cuda.synchronize()
@@ -250,11 +268,10 @@ def impl_ours(args):
     if golden is not None and not parity:
         log(f"[bench] PARITY FAILURE {result} != {golden}")
 
-    clocks = Clocks(local)
-    clocks.start()
     _lib.profile_enable(True)
     l0 = _lib.launch_count()
     torch.cuda.synchronize()
+    w0 = time.time()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record()
@@ -265,6 +282,7 @@ def impl_ours(args):
             phase[k] += res.phase_timings[k]
     ev1.record()
     torch.cuda.synchronize()
+    clocks.mark(w0, time.time())
     launches = _lib.launch_count() - l0
     ms = ev0.elapsed_time(ev1) / args.steps
     prof = {k: _lib.profile_read(k) for k in ("seg_scatter", "seg_count", "merge", "merge_partition")}

@@ -412,6 +412,7 @@ def bench_main(args, metric, configs, make_inputs, Clocks, run_reference_sample)
     clocks.start()
     dist.barrier()
     torch.cuda.synchronize()
+    w0 = time.time()
     l0 = _lib.launch_count()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -423,6 +424,7 @@ def bench_main(args, metric, configs, make_inputs, Clocks, run_reference_sample)
     ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     dist.barrier()
+    clocks.mark(w0, time.time())
     clk = clocks.stop()
     launches = _lib.launch_count() - l0
     ms = float(ms.item())
