@@ -303,8 +303,9 @@ __global__ void k_split_fill(const mpsm_run_t* __restrict__ priv, int n_pub, con
 }
 
 // Tile staging.  A stage holds the 16-B aligned superset of the tile's R
-// range (with the prior tuple R[i0-1] when i0 > 0: the S tuples that open a
-// tile usually match the R tuple that closed the previous one) followed by
+// range (with the prior tuples R[i0-2], R[i0-1] when they exist: the S tuples
+// that open a tile usually match the R tuple that closed the previous one,
+// and R[i0-2] tells whether that group reaches back further) followed by
 // the aligned superset of its W range; each range arrives with one bulk copy
 // (TMA).  Reading up to 8 B beyond a range stays inside its 16-B block, so
 // inside the mapped allocation.
@@ -318,6 +319,7 @@ template <bool PK>
 struct MergeSmem {
     MergeStage<PK> st[2];
     uint16_t ub[MJ_TILE];  // MODE 0: per W tuple of the tile, R tuples <= its key (tile-relative)
+    int tdup[2];           // MODE 0, per tile parity: some R key of the tile repeats
     uint64_t bar[2];
     uint64_t red[3][MJ_THREADS / 32];
     int64_t warp_cnt[MJ_THREADS / 32];
@@ -345,7 +347,7 @@ struct TilePlace {
 template <bool PK>
 __device__ __forceinline__ TilePlace place_of(const TileSplit& t) {
     TilePlace q;
-    q.hp = t.i0 > 0 ? 1 : 0;
+    q.hp = t.i0 >= 2 ? 2 : (int)t.i0;  // up to two prior R tuples
     q.rk = span_of(t.rk, t.i0 - q.hp, t.nR + q.hp);
     q.wk = span_of(t.wk, t.w0, t.nW);
     if (!PK) {
@@ -439,6 +441,7 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
         mbar_init(&sm.bar[0], 1);
         mbar_init(&sm.bar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        sm.tdup[0] = sm.tdup[1] = 0;
         fetch_tile<PK>(sm.st[0], &sm.bar[0], splits[g]);
         if (g + G < ntiles) t_nxt = splits[g + G];
     }
@@ -450,6 +453,7 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
             fetch_tile<PK>(sm.st[buf ^ 1], &sm.bar[buf ^ 1], t_nxt);
             if (g + 2 * G < ntiles) t_nxt = splits[g + 2 * G];  // consumed one tile later
         }
+        if (MODE == 0 && tid == 0) sm.tdup[buf ^ 1] = 0;  // last read before this tile's S1
         const TileSplit t = sm.st[buf].t;
         if (MODE == 0 && t.pair != cur_pair) {
             if (cur_pair >= 0) flush_pair<PK>(sm, out_pairs, cur_pair, count, best, csum);
@@ -491,18 +495,28 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
         if (MODE == 0) {
             // phase 1 -- the thread's merge steps, branch-light: record for
             // every W tuple the number of tile R tuples with key <= its key
+            // ... and whether two neighbouring R keys of the tile (or of its
+            // two prior tuples) are equal: then some S tuple matches an
+            // equal-key group of several R tuples
             {
                 int ri = lo, wj = k0 - lo;
                 KT rkc = ri < nR ? rkey(ri) : 0;
                 KT wkc = wj < nW ? wkey(wj) : 0;
+                bool dup = ri < nR && ri - 1 >= -hp && rkey(ri - 1) == rkc;
+                if (tid == 0 && hp == 2) dup = dup || rkey(-2) == rkey(-1);
                 for (int st = k0; st < k1; ++st) {
                     const bool take_r = ri < nR && (wj >= nW || rkc <= wkc);
                     if (!take_r) sm.ub[wj] = (uint16_t)ri;
                     ri += take_r;
                     wj += !take_r;
-                    if (take_r && ri < nR) rkc = rkey(ri);
+                    if (take_r && ri < nR) {
+                        const KT nk = rkey(ri);
+                        dup = dup || nk == rkc;
+                        rkc = nk;
+                    }
                     if (!take_r && wj < nW) wkc = wkey(wj);
                 }
+                if (dup) sm.tdup[buf] = 1;
             }
             __syncthreads();
             MJ_TS(4)
@@ -516,6 +530,15 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                 ++count;
                 csum += swap ? pair_hash(sp, rp) : pair_hash(rp, sp);
             };
+            if (!sm.tdup[buf]) {  // unique R keys: at most one match per W tuple
+                for (int j = tid; j < nW; j += MJ_THREADS) {
+                    const int i = (int)sm.ub[j] - 1;
+                    if (i < -hp) continue;  // no R tuple <= the key (tile at the run start)
+                    const uint64_t wv = WK[j], rv = RK[i];
+                    if (nkey(rv) != nkey(wv)) continue;
+                    acc(PK ? (rv & pmask) : RP[i], PK ? (wv & pmask) : WP[j]);
+                }
+            } else
             for (int j = tid; j < nW; j += MJ_THREADS) {
                 const uint64_t wv = WK[j];
                 const KT wk = nkey(wv);
