@@ -47,6 +47,11 @@ namespace mpsm {
 #ifndef MPSM_MJ_BLOCKS
 #define MPSM_MJ_BLOCKS 6
 #endif
+#ifndef MPSM_MJ_P2_UNROLL  // match-phase loop unroll (independent W tuples in flight)
+#define MPSM_MJ_P2_UNROLL 2
+#endif
+#define MPSM_PRAGMA(x) _Pragma(#x)
+#define MPSM_UNROLL(n) MPSM_PRAGMA(unroll n)
 constexpr int MJ_THREADS = MPSM_MJ_THREADS;
 constexpr int MJ_ITEMS = MPSM_MJ_ITEMS;  // odd: 64-bit smem accesses at stride ITEMS are conflict-free
 constexpr int MJ_TILE = MJ_THREADS * MJ_ITEMS;
@@ -531,6 +536,7 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                 csum += swap ? pair_hash(sp, rp) : pair_hash(rp, sp);
             };
             if (!sm.tdup[buf]) {  // unique R keys: at most one match per W tuple
+                MPSM_UNROLL(MPSM_MJ_P2_UNROLL)
                 for (int j = tid; j < nW; j += MJ_THREADS) {
                     const int i = (int)sm.ub[j] - 1;
                     if (i < -hp) continue;  // no R tuple <= the key (tile at the run start)
