@@ -23,10 +23,6 @@ from .partition import SplitterVector, bucket_lower_key
 EXACT_SEARCH_MAX_BUCKETS = 256
 
 
-def _host(a) -> np.ndarray:
-    return a.cpu().numpy() if hasattr(a, "cpu") and not isinstance(a, np.ndarray) else np.asarray(a)
-
-
 @dataclass(frozen=True)
 class LocalBounds:
     """Equi-height sample of one sorted public run (skew.py:32-49)."""
