@@ -290,14 +290,20 @@ def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=Non
     be.sync()
     t_sort = time.perf_counter()
     # 7: join against every public run (remote ones through peer mappings)
+    # rank-rotated order, own run first (engine.py:251: (i + k) % T): at any
+    # moment each rank reads a different peer, so no peer's NVLink serves
+    # all readers at once
+    order = [(me + k) % G for k in range(G)]
     if G > 1:
         shared = _gather_obj(be.share(pub_run), group)
-        pub_runs = [pub_run if j == me else be.open(shared[j]) for j in range(G)]
+        pub_runs = [pub_run if j == me else be.open(shared[j]) for j in order]
     else:
         pub_runs = [pub_run]
     mode = {"aggregate-max": _lib.MODE_AGGREGATE_MAX, "count": _lib.MODE_COUNT,
             "materialize": _lib.MODE_COUNT}[cfg.query_mode]
-    rec_h = be.records(be.join([priv_run], pub_runs, roles.swapped, mode))
+    rec_rot = np.asarray(be.records(be.join([priv_run], pub_runs, roles.swapped, mode))).reshape(G, _lib.PAIR_FIELDS)
+    rec_h = np.empty_like(rec_rot)
+    rec_h[order] = rec_rot  # back to public-run (rank) order
     overflow = be.overflowed()
     gathered = _gather_obj((rec_h, n_recv_priv, overflow), group)
     if any(g[2] for g in gathered):
