@@ -99,10 +99,13 @@ def ipc_open(shared: tuple, device) -> PeerRun:
 class CudaBackend:
     """Device operations of one rank on its own GPU."""
 
-    def __init__(self, device: Optional[torch.device] = None, packed: Optional[bool] = None):
+    def __init__(self, device: Optional[torch.device] = None, packed: Optional[bool] = None,
+                 comm_device: Optional[torch.device] = None):
         self.dev = D.ensure_device(device)
         self.packed_pref = PACK_RECORDS if packed is None else packed
-        self.comm_device = self.dev
+        # where the all-to-all buffers live: the GPU (NCCL), or the host for a
+        # CPU process group (gloo; tests run several ranks on one GPU)
+        self.comm_device = comm_device if comm_device is not None else self.dev
 
     def setup(self, dom):
         self.dom = dom
@@ -215,17 +218,17 @@ def _alltoall(be, k, p, send_counts, recv_counts, group):
     rp = torch.empty(n_recv, dtype=torch.int64, device=be.comm_device)
     sc = [int(x) for x in send_counts]
     rc = [int(x) for x in recv_counts]
-    dist.all_to_all_single(rk, k.view(torch.int64), rc, sc, group=group)
-    dist.all_to_all_single(rp, p.view(torch.int64), rc, sc, group=group)
-    return rk.view(torch.uint64), rp.view(torch.uint64)
+    dist.all_to_all_single(rk, k.view(torch.int64).to(be.comm_device), rc, sc, group=group)
+    dist.all_to_all_single(rp, p.view(torch.int64).to(be.comm_device), rc, sc, group=group)
+    return rk.view(torch.uint64).to(k.device), rp.view(torch.uint64).to(k.device)
 
 
 def _alltoall_one(be, x, send_counts, recv_counts, group):
     """all-to-all(v) of one u64 column (packed records); source-rank order."""
     out = torch.empty(int(recv_counts.sum()), dtype=torch.int64, device=be.comm_device)
-    dist.all_to_all_single(out, x.view(torch.int64), [int(v) for v in recv_counts], [int(v) for v in send_counts],
-                           group=group)
-    return out.view(torch.uint64)
+    dist.all_to_all_single(out, x.view(torch.int64).to(be.comm_device), [int(v) for v in recv_counts],
+                           [int(v) for v in send_counts], group=group)
+    return out.view(torch.uint64).to(x.device)
 
 
 def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=None, backend=None,
@@ -308,7 +311,7 @@ def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=Non
     gathered = _gather_obj((rec_h, n_recv_priv, overflow), group)
     if any(g[2] for g in gathered):
         # a payload is wider than a packed record allows: redo on pairs
-        be2 = type(be)(packed=False) if isinstance(be, CudaBackend) else be.unpacked()
+        be2 = type(be)(packed=False, comm_device=be.comm_device) if isinstance(be, CudaBackend) else be.unpacked()
         return run_join_distributed(r, s, cfg, group=group, backend=be2, timings=timings)
     t_join = time.perf_counter()
     # 8: fold, as engine.finalize with worker i = rank i

@@ -100,3 +100,77 @@ print("OK" if bool((t == want).all()) else "MISMATCH")
                        text=True, timeout=300)
     assert "OK" in r.stdout, r.stdout + r.stderr
     del big, x
+
+
+def _gloo_cuda_worker(rank, world, port, cases, packed, q):
+    import os as _os
+
+    _os.environ["MASTER_ADDR"] = "127.0.0.1"
+    _os.environ["MASTER_PORT"] = str(port)
+    import torch as _t
+    import torch.distributed as _dist
+
+    _t.cuda.set_device(0)
+    _dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1207_0145_b200.core import JoinConfig as _JC, KeyDomain as _KD, Relation as _Rel, chunk_bounds
+        from paper_1207_0145_b200.distributed import CudaBackend, run_join_distributed as _rjd
+        from tests.golden_inputs import dataset, make_inputs
+
+        out = []
+        for name, mode, role in cases:
+            rk, rp, sk, sp, lo, up = make_inputs(dataset(name))
+            ra, rb = chunk_bounds(rk.shape[0], world)[rank]
+            sa, sb = chunk_bounds(sk.shape[0], world)[rank]
+            cfg = _JC(threads=world, key_domain=_KD(lo, up), query_mode=mode, role_policy=role,
+                      materialize_cap=1 << 24)
+            be = CudaBackend(packed=packed, comm_device=_t.device("cpu"))
+            res = _rjd(_Rel(rk[ra:rb], rp[ra:rb]), _Rel(sk[sa:sb], sp[sa:sb]), cfg, backend=be)
+            mat = None if res.materialized is None else sorted(map(tuple, res.materialized.tolist()))
+            out.append((res.match_count, res.aggregate_max, res.checksum, mat,
+                        [(w.public_tuples_examined, w.probe_tuples_examined, w.s_runs_with_matches,
+                          w.tuples_sorted_private) for w in res.worker_stats]))
+        q.put((rank, out))
+    finally:
+        _dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("packed", [True, False], ids=["packed", "pairs"])
+def test_cuda_backend_two_ranks_one_gpu_match_reference(golden, packed):
+    """Two ranks of the CUDA engine (gloo for the host collectives, both on
+    cuda:0): partition, exchange, public runs mapped by CUDA IPC from the
+    other process and read by the merge kernel, rank-rotated order, fold.
+    Only correctness: the ranks' kernels never wait on one another."""
+    import torch.multiprocessing as mp
+
+    from tests.test_distributed import CASES
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    with socket.socket() as sck:
+        sck.bind(("127.0.0.1", 0))
+        port = sck.getsockname()[1]
+    procs = [ctx.Process(target=_gloo_cuda_worker, args=(r, 2, port, CASES, packed, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert results[0] == results[1]
+    from tests.golden_inputs import reference_totals
+
+    for (name, mode, role), got in zip(CASES, results[0]):
+        want = None
+        for c in golden["engine_cases"]:
+            if (c["dataset"], c["algorithm"], c["threads"], c["query_mode"], c["role_policy"]) == \
+                    (name, "p-mpsm", 2, "aggregate-max", role) and "error" not in c:
+                want = c
+        count, mx, cs = reference_totals(name)
+        assert got[0] == count and got[2] == cs, name
+        if mode == "aggregate-max":
+            assert got[1] == mx, name
+        if want is not None:
+            stats = [(w["public_tuples_examined"], w["probe_tuples_examined"], w["s_runs_with_matches"],
+                      w["tuples_sorted_private"]) for w in want["worker_stats"]]
+            assert got[4] == stats, name
