@@ -12,17 +12,24 @@
 //                the reference's interpolation search (identical probe count)
 //                plus a binary search; "examined" statistic; tiles per pair
 //   k_tile_scan  exclusive scan of tiles over pairs
-//   k_partition  merge-path diagonal search for every tile boundary; writes
-//                a flat tile descriptor (direct pointers) so the merge kernel
-//                needs one dependent load per tile
-//   k_merge      persistent CTAs, double-buffered: tile g+grid streams into
-//                shared memory with cp.async while tile g merges.  Each thread
-//                takes MJ_ITEMS steps of the merge from its merge-path split.
-//                For every S tuple the matching R tuples are the equal-key run
-//                that ends right before its merge position (ties merge R
-//                first), found by walking back -- the reference's cross
-//                product of duplicate key groups.  Per-thread accumulators are
-//                reduced per CTA and flushed with one atomic per pair.
+//   k_part_coarse / k_partition / k_split_fill
+//                merge-path tile boundaries in two levels (every 32nd tile
+//                by a full search, the rest inside their coarse bracket),
+//                written as flat tile descriptors (direct pointers)
+//   k_merge      persistent CTAs, two stages: thread 0 brings tile g+grid into
+//                shared memory with TMA bulk copies (descriptor loaded a tile
+//                earlier) while tile g merges.  MODE 0 (aggregates) runs two
+//                phases per tile: each thread walks MJ_ITEMS merge steps from
+//                its merge-path split and records, per S tuple, how many tile
+//                R tuples have key <= its key (and whether any two R keys of
+//                the tile are equal); then the S tuples are dealt
+//                round-robin and each matches the equal-key R group ending
+//                there (ties merge R first) -- the reference's cross product
+//                of duplicate key groups, with the walk-back only in tiles
+//                that have repeated R keys.  COUNT / MAX / checksum are
+//                reduced per CTA and flushed with one atomic per pair.  The
+//                materialize modes (count, then emit at scanned offsets) use
+//                the one-phase walk.
 //
 // Runs come in two layouts: (keys, payloads) SoA, or packed 8-B records
 // (key - lower) << pw | payload written by mpsm_sort_packed (PK = true).
