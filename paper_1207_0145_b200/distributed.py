@@ -48,7 +48,7 @@ from .core import (
     Relation,
     WorkerStats,
 )
-from .engine import MASK64, PACK_RECORDS, choose_roles
+from .engine import HOST_PACK, MASK64, PACK_RECORDS, choose_roles
 from .partition import combine_counts, effective_radix_bits
 from .skew import LocalBounds, bound_positions, build_cdf, compute_splitters
 
@@ -164,6 +164,23 @@ class CudaBackend:
         D.pack_records(k, p, self.dom.lower, self.span_m1, self.wbits, rec, self.bad, self.overflow)
         return rec
 
+    def upload(self, rel: Relation):
+        """host (key, payload) columns -> packed records on this GPU, or None
+        (device inputs, pair joins); domain errors flag self.bad, a too-wide
+        payload flags self.overflow (the join then reruns on pairs)"""
+        if not (self.packed and HOST_PACK):
+            return None
+        hk, hp = D.host_columns(rel.keys), D.host_columns(rel.payloads)
+        if hk is None or hp is None:
+            return None
+        rec = self.empty(int(hk[0].shape[0]))
+        bad, ovf = D.upload_records(hk[0], hp[0], self.dom.lower, self.span_m1, self.wbits, rec)
+        if bad >= 0:
+            self.bad.fill_(bad)
+        if ovf:
+            self.overflow.fill_(1)
+        return rec
+
     def sort_records(self, rec):
         n = int(rec.numel())
         out, tmp = self.empty(n), self.empty(n)
@@ -255,12 +272,16 @@ def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=Non
         raise ConfigurationError(f"effective radix bits {bits} give fewer buckets than {G} workers")
     nb = 1 << bits
     shift = dom.width_bits - bits
+    # host-resident public shards of a packed join cross PCIe as 8-B records
+    pub_rec = be.upload(public) if hasattr(be, "upload") else None
     pk, pp = be.to_device(private.keys), be.to_device(private.payloads)
-    uk, up = be.to_device(public.keys), be.to_device(public.payloads)
     stats = [WorkerStats(i) for i in range(G)]
 
     # 1-2: public run, private histogram, bounds
-    pub_run = be.sort(uk, up)
+    if pub_rec is not None:
+        pub_run = be.sort_records(pub_rec)
+    else:
+        pub_run = be.sort(be.to_device(public.keys), be.to_device(public.payloads))
     hist = be.histogram(pk, shift, nb)
     f = cfg.cdf_fanout
     bk = be.bound_keys(pub_run, f, G)
@@ -422,6 +443,7 @@ def bench_main(args, metric, configs, make_inputs, Clocks, run_reference_sample)
     dist.barrier()
     torch.cuda.synchronize()
     w0 = time.time()
+    _lib.profile_enable(True)
     l0 = _lib.launch_count()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -436,8 +458,51 @@ def bench_main(args, metric, configs, make_inputs, Clocks, run_reference_sample)
     clocks.mark(w0, time.time())
     clk = clocks.stop()
     launches = _lib.launch_count() - l0
+    sc_ms, sc_n = _lib.profile_read("seg_scatter")
+    _lib.profile_enable(False)
     ms = float(ms.item())
     ok = res.match_count == n_s
+
+    # roofline of the radix scatter on this rank: public sort (packing pass +
+    # record passes) and the record sort of the received private tuples
+    passes = _lib.load().mpsm_sort_pass_count(dom.width_bits)
+    n_recv = res.worker_stats[me].tuples_sorted_private
+    sc_bytes = args.steps * (s.cardinality * (24 + 16 * (passes - 1)) + n_recv * 16 * passes)
+    achieved = sc_bytes / (sc_ms / 1e3) / 1e9 if sc_ms > 0 else None
+    peak = 6532.2
+    try:
+        with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                               "MEASURED_PEAKS.json")) as fh:
+            peak = json.load(fh).get("hbm_gbs", peak)
+    except OSError:
+        pass
+    roof = {"bound": "hbm", "kernel": "seg::k_scatter (radix scatter pass), rank 0", "achieved": achieved,
+            "peak": peak, "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": None,
+            "launches": sc_n}
+
+    # end to end: every rank's shard from pinned host memory through the same call
+    e2e = None
+    if not getattr(args, "no_e2e", False):
+        rh = Relation(r.keys.cpu().pin_memory(), r.payloads.cpu().pin_memory())
+        sh = Relation(s.keys.cpu().pin_memory(), s.payloads.cpu().pin_memory())
+        k = max(1, min(args.steps, getattr(args, "e2e_steps", 3)))
+        run_join_distributed(rh, sh, cfg, backend=be)
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(k):
+            res_e = run_join_distributed(rh, sh, cfg, backend=be)
+        e1.record()
+        torch.cuda.synchronize()
+        e_ms = torch.tensor([e0.elapsed_time(e1) / k], device="cuda")
+        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        e_ms = float(e_ms.item())
+        e2e = {"value": (n_r + n_s) / (e_ms / 1e3), "unit": "tuples/s", "ms_per_step": e_ms, "steps": k,
+               "h2d_bytes_per_step": 8 * n_s + 16 * n_r, "d2h_bytes_per_step": 8 * _lib.PAIR_FIELDS * G * G,
+               "result_ok": (res_e.match_count, res_e.checksum) == (res.match_count, res.checksum),
+               "input_path": "pinned host shards; public side as packed 8-B records (upload_records), "
+                             "private side as columns"}
+        del rh, sh
     if me == 0:
         line = {
             "metric": metric, "value": (n_r + n_s) / (ms / 1e3), "unit": "tuples/s", "n_gpus": G,
@@ -450,7 +515,7 @@ def bench_main(args, metric, configs, make_inputs, Clocks, run_reference_sample)
                        "l2": "inputs >> L2 (no flush needed)"},
             "result": {"match_count": res.match_count, "aggregate_max": res.aggregate_max,
                        "checksum": hex(res.checksum), "fk_count_ok": ok},
-            "gpu_launches": launches, "clocks": clk, "e2e": None, "roofline": None, "cpu_baseline": None,
+            "gpu_launches": launches, "clocks": clk, "e2e": e2e, "roofline": roof, "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
