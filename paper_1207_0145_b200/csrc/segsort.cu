@@ -518,23 +518,34 @@ __global__ void __launch_bounds__(THREADS, LCfg<LAYOUT>::BLOCKS) k_scatter(
 // start-up probe: do shared atomicAdds that collide within one warp
 // instruction return their counts in lane order?  (true on sm_100; if a
 // device ever says no, the stable passes fall back to ballot ranking)
+// The probe mirrors k_scatter's use: two warps share a row of 32-bit words
+// (16-bit field per warp, increment 1 or 1 << 16), concurrent warps add to
+// the same rows, and the returned field must equal the lane's rank among
+// the lanes of its warp instruction that hit the same word, plus the field's
+// value before the instruction.
 __global__ void k_probe_lane_order(int* bad) {
-    __shared__ uint32_t hs[8][32];  // one row per warp, as in k_scatter
-    const int lane = threadIdx.x & 31;
-    uint32_t* h = hs[threadIdx.x >> 5];
-    h[lane] = 0;
+    __shared__ uint32_t hs[4][64];  // 8 warps, two per row, 64 words per row
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t* h = hs[warp >> 1];
+    const uint32_t inc = (warp & 1) ? 0x10000u : 1u;
+    const int sh = (warp & 1) * 16;
+    for (int i = threadIdx.x; i < 4 * 64; i += blockDim.x) (&hs[0][0])[i] = 0;
     __syncthreads();
     uint32_t x = 0x9E3779B9u * (threadIdx.x + 1) + blockIdx.x;
-    for (int it = 0; it < 64; ++it) {
+    for (int it = 0; it < 96; ++it) {
         x ^= x << 13;
         x ^= x >> 17;
         x ^= x << 5;
-        const uint32_t d = (x >> 7) % (1 + (it & 31));
-        const uint32_t old = atomicAdd(&h[d], 1u);
+        const uint32_t d = (x >> 7) % (1 + (it & 63));  // 1..64 distinct words: from all-equal to spread
+        const uint32_t old = (atomicAdd(&h[d], inc) >> sh) & 0xffffu;
         const unsigned peers = __match_any_sync(0xffffffffu, d);
         const uint32_t base = __shfl_sync(0xffffffffu, old, __ffs(peers) - 1);
         if (old != base + __popc(peers & ((1u << lane) - 1u))) atomicAdd(bad, 1);
-        __syncthreads();
+        if ((it & 15) == 15) {  // keep the 16-bit fields far from overflow
+            __syncthreads();
+            for (int i = threadIdx.x; i < 4 * 64; i += blockDim.x) (&hs[0][0])[i] = 0;
+            __syncthreads();
+        }
     }
 }
 
