@@ -129,6 +129,18 @@ int mpsm_scatter_chunk(const uint64_t* keys, const uint64_t* pays, int64_t n, ui
                        uint64_t* arena_keys, uint64_t* arena_pays, int64_t* d_written, void* workspace,
                        size_t ws_bytes, void* stream);
 
+/* multi-GPU partition of a private shard straight into packed records:
+ * every tuple goes to partition d_sp[min((key - lower) >> shift, nbuckets-1)]
+ * and out_rec receives the records (key - lower) << (64 - width_bits) |
+ * payload grouped by partition (stable), ready for the all-to-all -- one
+ * radix-style pass (the packing pass of mpsm_sort_packed with the partition
+ * id as its digit).  Same workspace as mpsm_sort_pairs; domain and payload-
+ * width checks as mpsm_sort_packed. */
+int mpsm_partition_records(const uint64_t* keys, const uint64_t* pays, int64_t n, uint64_t lower, uint64_t span_m1,
+                           int width_bits, int shift, const int32_t* d_sp, int nbuckets, int npart,
+                           uint64_t* out_rec, void* workspace, size_t ws_bytes, unsigned long long* d_bad,
+                           unsigned int* d_overflow, void* stream);
+
 /* -------------------------------------------- interpolation search ----
  * Replaces _kernels.interp_lower_bound (_kernels.py:287-337) used by
  * engine.interpolation_search (engine.py:124-128): for each target, the

@@ -34,7 +34,7 @@ EXPORTS = (
     "mpsm_minmax_contiguous",
     "mpsm_ipc_get_handle", "mpsm_ipc_open_handle", "mpsm_ipc_close_handle",
     "mpsm_relfile_header", "mpsm_relfile_read", "mpsm_relfile_write", "mpsm_deinterleave",
-    "mpsm_upload_records", "mpsm_upload_bytes", "mpsm_sort_records", "mpsm_pack_records",
+    "mpsm_upload_records", "mpsm_upload_bytes", "mpsm_sort_records", "mpsm_pack_records", "mpsm_partition_records",
 )
 
 
@@ -78,6 +78,8 @@ _SIGS = {
     "mpsm_sort_records": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _sz, _vp]),
     "mpsm_upload_bytes": (_u64, [_int]),
     "mpsm_pack_records": (_int, [_vp, _vp, _i64, _u64, _u64, _int, _vp, _vp, _vp, _vp]),
+    "mpsm_partition_records": (_int, [_vp, _vp, _i64, _u64, _u64, _int, _int, _vp, _int, _int, _vp, _vp, _sz, _vp,
+                                      _vp, _vp]),
 }
 
 _lib = None

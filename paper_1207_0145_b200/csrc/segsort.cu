@@ -105,7 +105,16 @@ struct Digit {
     uint64_t lower;
     int shift;
     uint32_t mask;
+    // partition passes (TABLE kernels): digit = table[min(bucket, nbuckets - 1)]
+    // with bucket = (v - lower) >> shift -- the splitter vector of P-MPSM
+    const int32_t* table = nullptr;
+    int nbuckets = 0;
     __device__ __forceinline__ uint32_t operator()(uint64_t v) const { return (uint32_t)((v - lower) >> shift) & mask; }
+    __device__ __forceinline__ uint32_t lookup(uint64_t v) const {
+        uint64_t b = (v - lower) >> shift;
+        if (b >= (uint64_t)nbuckets) b = (uint64_t)nbuckets - 1;
+        return (uint32_t)__ldg(table + b);
+    }
 };
 
 struct Segs {
@@ -119,7 +128,7 @@ struct Segs {
 // counts[g][d] for segment g, and for every tile t of the segment the
 // segment-local exclusive prefix toffs[t][d] (digit d's tuples in earlier
 // tiles of the segment); optional domain check (first pass)
-template <int CPT>  // count chunks (TILE tuples) per scatter tile
+template <int CPT, bool TABLE = false>  // count chunks (TILE tuples) per scatter tile
 __global__ void __launch_bounds__(THREADS) k_count(const uint64_t* __restrict__ in, Segs sg, Digit dig, int nbins,
                                                    uint32_t* __restrict__ counts, uint32_t* __restrict__ toffs,
                                                    unsigned int* __restrict__ ticket, uint64_t span_m1,
@@ -166,7 +175,7 @@ __global__ void __launch_bounds__(THREADS) k_count(const uint64_t* __restrict__ 
             const int64_t i = pos(c0, u);
             if (i < e) {
                 if (d_bad && v[u] - dig.lower > span_m1) atomicMin(d_bad, (unsigned long long)i);
-                atomicAdd(&h[k][dig(v[u])], 1u);
+                atomicAdd(&h[k][TABLE ? dig.lookup(v[u]) : dig(v[u])], 1u);
             }
         }
 #pragma unroll
@@ -299,7 +308,7 @@ __device__ __forceinline__ uint32_t rec_digit(uint64_t v, const Digit& d) {
 // order and warps in row order, so one ATOMS per tuple gives a stable rank.
 // Where the probe fails the peers come from ballots (ballot_peers).
 // HI: the staged records' digit lies in the high word (PP/SP with pw >= 32).
-template <int LAYOUT, bool HI>
+template <int LAYOUT, bool HI, bool TABLE = false>
 __global__ void __launch_bounds__(THREADS, LCfg<LAYOUT>::BLOCKS) k_scatter(
     const uint64_t* __restrict__ in_k, const uint64_t* __restrict__ in_p, uint64_t* __restrict__ out_k,
     uint64_t* __restrict__ out_p, Segs sg, Digit dig, Digit odig, int nbins, const int64_t* __restrict__ base,
@@ -404,7 +413,7 @@ __global__ void __launch_bounds__(THREADS, LCfg<LAYOUT>::BLOCKS) k_scatter(
             const int li = wb + 32 * k + lane;
             key[k] = sm.buf[b][0][offk + li];
             if (LAYOUT != PP) pay[k] = sm.buf[b][NARR - 1][offp + li];
-            dg[k] = LAYOUT == PP ? rec_digit<HI>(key[k], dig) : dig(key[k]);
+            dg[k] = TABLE ? dig.lookup(key[k]) : (LAYOUT == PP ? rec_digit<HI>(key[k], dig) : dig(key[k]));
         }
         if (lane_ordered) {
             if (cnt == TL) {
@@ -492,7 +501,8 @@ __global__ void __launch_bounds__(THREADS, LCfg<LAYOUT>::BLOCKS) k_scatter(
 #pragma unroll 4
         for (int i = tid; i < cnt; i += THREADS) {
             const uint64_t v = sm.buf[b][0][i];
-            const int64_t o = sm.gdelta[LAYOUT == SS ? odig(v) : rec_digit<HI>(v, odig)] + i;
+            const int64_t o =
+                sm.gdelta[TABLE ? odig.lookup(v) : (LAYOUT == SS ? odig(v) : rec_digit<HI>(v, odig))] + i;
             out_k[o] = v;
             if (LAYOUT == SS) out_p[o] = sm.buf[b][1][i];
         }
@@ -622,20 +632,20 @@ static bool carve(void* ws, size_t bytes, int64_t n, Ws* o) {
     return c.ok;
 }
 
-template <int LAYOUT, bool HI>
+template <int LAYOUT, bool HI, bool TABLE = false>
 static int set_attr() {
     static bool done = false;
     if (!done) {
-        MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_scatter<LAYOUT, HI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  (int)sizeof(Smem<LAYOUT>)),
+        MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_scatter<LAYOUT, HI, TABLE>,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem<LAYOUT>)),
                              "smem attr"));
         done = true;
     }
     return MPSM_OK;
 }
 
-// one digit pass: count, scan, scatter
-template <int LAYOUT>
+// one digit pass: count, scan, scatter (TABLE: the digit is a partition id)
+template <int LAYOUT, bool TABLE = false>
 static int pass(const uint64_t* in_k, const uint64_t* in_p, uint64_t* out_k, uint64_t* out_p, int64_t n,
                 Digit count_dig, Digit dig, int bits, const Ws& ws, uint64_t span_m1, unsigned long long* d_bad,
                 uint64_t pk_lower, int pk_pw, unsigned int* overflow, cudaStream_t st) {
@@ -647,26 +657,26 @@ static int pass(const uint64_t* in_k, const uint64_t* in_p, uint64_t* out_k, uin
     const int nbins = 1 << bits;
     {
         ProfScope ps("seg_count", st);
-        k_count<LCfg<LAYOUT>::TILE_L / TILE><<<GC, THREADS, 0, st>>>(in_k, sg, count_dig, nbins, ws.counts, ws.toffs,
-                                                                      ws.ticket, span_m1, d_bad);
+        k_count<LCfg<LAYOUT>::TILE_L / TILE, TABLE><<<GC, THREADS, 0, st>>>(in_k, sg, count_dig, nbins, ws.counts,
+                                                                             ws.toffs, ws.ticket, span_m1, d_bad);
     }
     MPSM_TRY(check_launch("k_count"));
     k_scan<<<(nbins + 31) / 32, 32 * SCAN_GROUPS, 0, st>>>(ws.counts, GC, nbins, ws.base, ws.dtot);
     MPSM_TRY(check_launch("k_scan"));
     // digit of a staged value: records staged by the SP pass carry the key
     // above the payload bits
-    const Digit odig = (LAYOUT == SP) ? Digit{0, pk_pw + dig.shift, dig.mask} : dig;
+    const Digit odig = (LAYOUT == SP) ? Digit{0, pk_pw + dig.shift, dig.mask, dig.table, dig.nbuckets} : dig;
     const bool hi = LAYOUT != SS && odig.shift >= 32;
-    MPSM_TRY(hi ? (set_attr<LAYOUT, true>()) : (set_attr<LAYOUT, false>()));
+    MPSM_TRY(hi ? (set_attr<LAYOUT, true, TABLE>()) : (set_attr<LAYOUT, false, TABLE>()));
     {
         ProfScope ps("seg_scatter", st);
         ProfScope ps2(LAYOUT == SS ? "seg_scatter_ss" : (LAYOUT == SP ? "seg_scatter_sp" : "seg_scatter_pp"), st);
         const bool lo = lane_ordered_atomics();
         if (hi)
-            k_scatter<LAYOUT, true><<<G, THREADS, sizeof(Smem<LAYOUT>), st>>>(
+            k_scatter<LAYOUT, true, TABLE><<<G, THREADS, sizeof(Smem<LAYOUT>), st>>>(
                 in_k, in_p, out_k, out_p, sg, dig, odig, nbins, ws.base, ws.toffs, ws.dtot, ws.ticket, pk_lower, pk_pw, overflow, lo);
         else
-            k_scatter<LAYOUT, false><<<G, THREADS, sizeof(Smem<LAYOUT>), st>>>(
+            k_scatter<LAYOUT, false, TABLE><<<G, THREADS, sizeof(Smem<LAYOUT>), st>>>(
                 in_k, in_p, out_k, out_p, sg, dig, odig, nbins, ws.base, ws.toffs, ws.dtot, ws.ticket, pk_lower, pk_pw, overflow, lo);
     }
     return check_launch("k_scatter");
@@ -796,4 +806,25 @@ extern "C" int mpsm_sort_records(const uint64_t* in_rec, int64_t n, int width_bi
         src = dst;
     }
     return MPSM_OK;
+}
+
+extern "C" int mpsm_partition_records(const uint64_t* keys, const uint64_t* pays, int64_t n, uint64_t lower,
+                                      uint64_t span_m1, int width_bits, int shift, const int32_t* d_sp, int nbuckets,
+                                      int npart, uint64_t* out_rec, void* workspace, size_t ws_bytes,
+                                      unsigned long long* d_bad, unsigned int* d_overflow, void* stream) {
+    using namespace seg;
+    if (n < 0 || width_bits < 1 || width_bits > 63 || npart < 1 || npart > MAX_BINS || nbuckets < 1 || shift < 0 ||
+        !d_sp || !d_overflow)
+        return MPSM_ERR_ARG;
+    if (n == 0) return MPSM_OK;
+    Ws ws;
+    if (!carve(workspace, ws_bytes, n, &ws)) {
+        set_error("partition workspace too small");
+        return MPSM_ERR_ARG;
+    }
+    int pbits = 0;
+    while ((1 << pbits) < npart) ++pbits;
+    const Digit dg{lower, shift, 0u, d_sp, nbuckets};
+    return pass<SP, true>(keys, pays, out_rec, nullptr, n, dg, dg, pbits, ws, span_m1, d_bad, lower, 64 - width_bits,
+                          d_overflow, (cudaStream_t)stream);
 }

@@ -137,6 +137,23 @@ def pack_records(keys: torch.Tensor, pays: torch.Tensor, lower: int, span_m1: in
                                              ptr(bad), ptr(overflow), stream_ptr()), "mpsm_pack_records")
 
 
+def partition_records(keys: torch.Tensor, pays: torch.Tensor, lower: int, span_m1: int, width_bits: int, shift: int,
+                      sp: torch.Tensor, npart: int, out_rec: torch.Tensor, bad: torch.Tensor,
+                      overflow: torch.Tensor) -> None:
+    """private shard -> packed records grouped by partition (stable); sp:
+    int32 splitter vector (bucket -> partition) on the device"""
+    n = int(keys.numel())
+    if n == 0:
+        return
+    L = _lib.load()
+    sz = ctypes.c_size_t(0)
+    _lib.check(L.mpsm_sort_workspace_bytes(n, width_bits, ctypes.byref(sz)), "sort workspace")
+    ws = workspace(keys.device).get(sz.value)
+    _lib.check(L.mpsm_partition_records(ptr(keys), ptr(pays), n, lower, span_m1, width_bits, shift, ptr(sp),
+                                        int(sp.numel()), npart, ptr(out_rec), ptr(ws), ws.numel(), ptr(bad),
+                                        ptr(overflow), stream_ptr()), "mpsm_partition_records")
+
+
 def host_columns(a):
     """A host uint64 column as (keep-alive object, address), or None if `a`
     is not host-resident."""

@@ -155,30 +155,15 @@ class CudaBackend:
                         npart, torch.from_numpy(starts.astype(np.int64)).to(self.dev), sk, spay, written)
         return sk, spay
 
-    def pack(self, k, p):
-        """(key, payload) columns -> packed records for the exchange, or None
-        when the join runs on pairs"""
+    def partition_records(self, k, p, shift: int, sp: np.ndarray, npart: int):
+        """packed join: the private shard straight into records grouped by
+        destination rank (one pass), or None for pair joins"""
         if not self.packed:
             return None
         rec = self.empty(int(k.numel()))
-        D.pack_records(k, p, self.dom.lower, self.span_m1, self.wbits, rec, self.bad, self.overflow)
-        return rec
-
-    def upload(self, rel: Relation):
-        """host (key, payload) columns -> packed records on this GPU, or None
-        (device inputs, pair joins); domain errors flag self.bad, a too-wide
-        payload flags self.overflow (the join then reruns on pairs)"""
-        if not (self.packed and HOST_PACK):
-            return None
-        hk, hp = D.host_columns(rel.keys), D.host_columns(rel.payloads)
-        if hk is None or hp is None:
-            return None
-        rec = self.empty(int(hk[0].shape[0]))
-        bad, ovf = D.upload_records(hk[0], hp[0], self.dom.lower, self.span_m1, self.wbits, rec)
-        if bad >= 0:
-            self.bad.fill_(bad)
-        if ovf:
-            self.overflow.fill_(1)
+        spd = torch.from_numpy(sp.astype(np.int32)).to(self.dev)
+        D.partition_records(k, p, self.dom.lower, self.span_m1, self.wbits, shift, spd, npart, rec, self.bad,
+                            self.overflow)
         return rec
 
     def sort_records(self, rec):
@@ -300,8 +285,9 @@ def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=Non
     send_starts = np.zeros(G, np.int64)
     np.cumsum(send_counts[:-1], out=send_starts[1:])
     # 4-5: scatter into send segments, one all-to-all
-    sk, sp = be.partition(pk, pp, shift, ss.vector.sp, G, send_starts)
-    rec = be.pack(sk, sp) if hasattr(be, "pack") else None
+    rec = be.partition_records(pk, pp, shift, ss.vector.sp, G) if hasattr(be, "partition_records") else None
+    if rec is None:
+        sk, sp = be.partition(pk, pp, shift, ss.vector.sp, G, send_starts)
     if rec is not None:  # packed join: one all-to-all of 8-B records
         rr = _alltoall_one(be, rec, send_counts, recv_counts, group)
         n_recv_priv = int(rr.numel())

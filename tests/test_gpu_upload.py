@@ -136,3 +136,32 @@ def test_sort_packed_tile_edges(n, w):
     want = ((k[order] - np.uint64(lower)) << np.uint64(64 - w)) | p[order]
     assert int(ovf.item()) == 0
     assert np.array_equal(got, want)
+
+
+def test_pack_records_and_partition_records_match_numpy():
+    """mpsm_pack_records (device columns -> records) and
+    mpsm_partition_records (records grouped by partition id, stable)."""
+    import torch
+
+    from paper_1207_0145_b200 import device as D
+
+    rng = np.random.default_rng(77)
+    n, w, lower = 1_000_003, 24, 9
+    k = rng.integers(lower, lower + (1 << w), n, dtype=np.uint64)
+    p = rng.integers(0, 1 << 32, n, dtype=np.uint64)
+    dk, dp = torch.from_numpy(k).cuda(), torch.from_numpy(p).cuda()
+    bad = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    ovf = torch.zeros(1, dtype=torch.int32, device="cuda")
+    rec = torch.empty_like(dk)
+    D.pack_records(dk, dp, lower, (1 << w) - 1, w, rec, bad, ovf)
+    want = _pack_np(k, p, lower, w)
+    assert np.array_equal(rec.cpu().numpy(), want) and int(bad.item()) == -1 and int(ovf.item()) == 0
+    # partition: 2^10 buckets of the top 10 key bits -> 5 partitions
+    shift = w - 10
+    cuts = np.sort(rng.choice(np.arange(1, 1 << 10), 4, replace=False))
+    sp = np.searchsorted(cuts, np.arange(1 << 10), side="right").astype(np.int32)
+    part = sp[((k - np.uint64(lower)) >> np.uint64(shift)).astype(np.int64)]
+    out = torch.empty_like(dk)
+    D.partition_records(dk, dp, lower, (1 << w) - 1, w, shift, torch.from_numpy(sp).cuda(), 5, out, bad, ovf)
+    order = np.argsort(part, kind="stable")
+    assert np.array_equal(out.cpu().numpy(), want[order])
