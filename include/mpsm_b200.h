@@ -229,10 +229,13 @@ int mpsm_deinterleave(const uint64_t* d_records, int64_t n, uint64_t* d_keys, ui
  * the reference raises DomainError, sorter.py:97-98).  A payload >= 2^(64-w):
  * *overflow = 1 and the records are invalid (use the column path).  The
  * copies are ordered before later work on `stream`; returns once the host
- * buffers have been read.  Not thread-safe (one uploader per process). */
+ * buffers have been read.  The copies start after the work queued on
+ * `stream` before `ready_event` (a cudaEvent_t recorded when d_rec was
+ * allocated; NULL: after all work queued on `stream` so far), so work queued
+ * later overlaps the upload.  Not thread-safe (one uploader per process). */
 int mpsm_upload_records(const uint64_t* h_keys, const uint64_t* h_pays, int64_t n, uint64_t lower,
                         uint64_t span_m1, int width_bits, uint64_t* d_rec, int threads, int gpu_pack_every,
-                        void* stream, int64_t* bad_index, int* overflow);
+                        void* stream, void* ready_event, int64_t* bad_index, int* overflow);
 /* device (key, payload) columns -> packed records (before an exchange: the
  * multi-GPU all-to-all moves 8 B per tuple).  Same domain / payload-width
  * checks as mpsm_upload_records, reported through device flags: *d_bad =

@@ -73,8 +73,8 @@ _SIGS = {
     "mpsm_relfile_read": (_int, [ctypes.c_char_p, _u64, _vp, _int]),
     "mpsm_relfile_write": (_int, [ctypes.c_char_p, _vp, _vp, _u64]),
     "mpsm_deinterleave": (_int, [_vp, _i64, _vp, _vp, _vp]),
-    "mpsm_upload_records": (_int, [_vp, _vp, _i64, _u64, _u64, _int, _vp, _int, _int, _vp, ctypes.POINTER(_i64),
-                                   ctypes.POINTER(_int)]),
+    "mpsm_upload_records": (_int, [_vp, _vp, _i64, _u64, _u64, _int, _vp, _int, _int, _vp, _vp,
+                                   ctypes.POINTER(_i64), ctypes.POINTER(_int)]),
     "mpsm_sort_records": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _sz, _vp]),
     "mpsm_upload_bytes": (_u64, [_int]),
     "mpsm_pack_records": (_int, [_vp, _vp, _i64, _u64, _u64, _int, _vp, _vp, _vp, _vp]),

@@ -178,7 +178,7 @@ struct Uploader {
     }
 
     int run(const uint64_t* k, const uint64_t* p, int64_t n_, uint64_t lo, uint64_t span, int pw_, uint64_t* d_rec,
-            int gpu_every, cudaStream_t st, int64_t* bad_out, int* ovf_out) {
+            int gpu_every, cudaStream_t st, cudaEvent_t ready_ev, int64_t* bad_out, int* ovf_out) {
         // the copy stream must not overwrite a slot that a previous call's
         // copies still read: drain it first
         MPSM_TRY(cuda_status(cudaStreamSynchronize(copy), "drain"));
@@ -211,9 +211,16 @@ struct Uploader {
             ready[c].store(0);
             issued[c].store(0);
         }
-        // the compute stream's earlier work (which may still read d_rec) first
-        MPSM_TRY(cuda_status(cudaEventRecord(done, st), "event"));
-        MPSM_TRY(cuda_status(cudaStreamWaitEvent(copy, done, 0), "wait"));
+        // the compute stream's earlier work (which may still use d_rec's
+        // memory) first: all of it, or what preceded the caller's `ready`
+        // event (recorded when d_rec was allocated -- later work, e.g. a sort
+        // queued meanwhile, then runs concurrently with the upload)
+        if (ready_ev) {
+            MPSM_TRY(cuda_status(cudaStreamWaitEvent(copy, ready_ev, 0), "wait"));
+        } else {
+            MPSM_TRY(cuda_status(cudaEventRecord(done, st), "event"));
+            MPSM_TRY(cuda_status(cudaStreamWaitEvent(copy, done, 0), "wait"));
+        }
         {
             std::lock_guard<std::mutex> g(mu);
             finished = 0;
@@ -277,7 +284,7 @@ using namespace mpsm;
 
 extern "C" int mpsm_upload_records(const uint64_t* h_keys, const uint64_t* h_pays, int64_t n, uint64_t lower,
                                    uint64_t span_m1, int width_bits, uint64_t* d_rec, int threads, int gpu_pack_every,
-                                   void* stream, int64_t* bad_index, int* overflow) {
+                                   void* stream, void* ready_event, int64_t* bad_index, int* overflow) {
     if (n < 0 || width_bits < 1 || width_bits > 63 || !bad_index || !overflow) return MPSM_ERR_ARG;
     *bad_index = -1;
     *overflow = 0;
@@ -286,7 +293,7 @@ extern "C" int mpsm_upload_records(const uint64_t* h_keys, const uint64_t* h_pay
     Uploader& u = uploader();
     MPSM_TRY(u.init(threads));
     return u.run(h_keys, h_pays, n, lower, span_m1, 64 - width_bits, d_rec, gpu_pack_every, (cudaStream_t)stream,
-                 bad_index, overflow);
+                 (cudaEvent_t)ready_event, bad_index, overflow);
 }
 
 extern "C" uint64_t mpsm_upload_bytes(int reset) {

@@ -171,18 +171,20 @@ def host_columns(a):
 
 
 def upload_records(keys, pays, lower: int, span_m1: int, width_bits: int, out_rec: torch.Tensor,
-                   threads: int = 0, gpu_pack_every: int = -1) -> tuple:
+                   threads: int = 0, gpu_pack_every: int = -1, ready: Optional[torch.cuda.Event] = None) -> tuple:
     """Host (key, payload) columns -> packed records on the device (half the
     PCIe bytes).  gpu_pack_every: every k-th chunk packed by the GPU from the
     mapped (pinned) columns; 0 = host only (use while the GPU is busy), -1 =
-    default.  -> (first out-of-domain index or -1, payload overflow)."""
+    default.  ready: event recorded when out_rec was allocated (the copies need
+    not wait for work queued after it).  -> (first out-of-domain index or -1,
+    payload overflow)."""
     hk, hp = host_columns(keys), host_columns(pays)
     n = int(out_rec.numel())
     bad = ctypes.c_int64(-1)
     ovf = ctypes.c_int(0)
     _lib.check(_lib.load().mpsm_upload_records(hk[1] if n else None, hp[1] if n else None, n, lower, span_m1,
                                                width_bits, ptr(out_rec), threads, gpu_pack_every, stream_ptr(),
-                                               ctypes.byref(bad),
+                                               ready.cuda_event if ready is not None else None, ctypes.byref(bad),
                                                ctypes.byref(ovf)), "mpsm_upload_records")
     return int(bad.value), bool(ovf.value)
 

@@ -219,6 +219,13 @@ class JoinContext:
         self._priv_pack = variant == "b-mpsm" or self.t == 1
         self.priv_rec = None
         self.n_priv = int(private.keys.shape[0]) if hasattr(private.keys, "shape") else len(private.keys)
+        # the private upload buffer is allocated now, before the public sort is
+        # queued: its copies then need not wait for that sort
+        self._priv_buf = self._priv_ready = None
+        if self._priv_pack and self.packed and HOST_PACK and D.host_columns(private.keys) is not None:
+            self._priv_buf = torch.empty(self.n_priv, dtype=torch.uint64, device=self.dev)
+            self._priv_ready = torch.cuda.Event()
+            self._priv_ready.record()
         self.pub_rec = self._upload(public, "public", True)
         if self.pub_rec is None:
             self.pub_k = D.to_device(public.keys, self.dev)
@@ -239,22 +246,23 @@ class JoinContext:
         """private input -> device (packed records or columns)"""
         private = self._private
         # the GPU is sorting the public run: host threads pack every chunk
-        self.priv_rec = self._upload(private, "private", self._priv_pack, gpu_pack_every=0)
+        self.priv_rec = self._upload(private, "private", self._priv_pack, gpu_pack_every=0, buf=self._priv_buf,
+                                     ready=self._priv_ready)
         if self.priv_rec is None:
             self.priv_k = D.to_device(private.keys, self.dev)
             self.priv_p = D.to_device(private.payloads, self.dev)
         self._private = None
 
-    def _upload(self, rel: Relation, name: str, allowed: bool, gpu_pack_every: int = -1):
+    def _upload(self, rel: Relation, name: str, allowed: bool, gpu_pack_every: int = -1, buf=None, ready=None):
         """host columns -> packed records on the device, or None (columns path)"""
         if not (allowed and self.packed and HOST_PACK):
             return None
         hk, hp = D.host_columns(rel.keys), D.host_columns(rel.payloads)
         if hk is None or hp is None or hk[0].shape[0] != hp[0].shape[0]:
             return None
-        rec = torch.empty(int(hk[0].shape[0]), dtype=torch.uint64, device=self.dev)
+        rec = buf if buf is not None else torch.empty(int(hk[0].shape[0]), dtype=torch.uint64, device=self.dev)
         bad, ovf = D.upload_records(hk[0], hp[0], self.dom.lower, self.span_m1, self.wbits, rec,
-                                    gpu_pack_every=gpu_pack_every)
+                                    gpu_pack_every=gpu_pack_every, ready=ready)
         if bad >= 0:
             raise DomainError(f"relation {self.rel_name[name]} has out-of-domain keys (first at index {bad})")
         if ovf:

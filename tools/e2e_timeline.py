@@ -28,6 +28,14 @@ def wrap(cls, name):
     setattr(cls, name, g)
 
 
+if os.environ.get("SYNC_AFTER_PUBLIC") == "1":  # no overlap of the private upload with the public sort
+    _sp = engine.JoinContext.sort_public
+
+    def _sp_sync(self):
+        _sp(self)
+        torch.cuda.synchronize()
+
+    engine.JoinContext.sort_public = _sp_sync
 for nm in ("_upload", "stage_private", "sort_public", "sort_private_chunks", "join", "finalize"):
     wrap(engine.JoinContext, nm)
 
@@ -43,3 +51,4 @@ for it in range(4):
     t1 = time.perf_counter()
     print(f"iter {it}: {1e3 * (t1 - t0):.1f} ms  " +
           "  ".join(f"{n}@{1e3 * (a - t0):.1f}+{1e3 * (b - a):.1f}" for n, a, b in marks), flush=True)
+
