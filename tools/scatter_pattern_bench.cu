@@ -47,6 +47,29 @@ __global__ void seg_k(const uint64_t* __restrict__ in, uint64_t* __restrict__ ou
     }
 }
 
+
+// tile in smem, then run d of the tile leaves with ONE bulk (TMA) store per
+// run, issued by thread d (runs of `run` 8-B elements, 16-B aligned here)
+template <int THREADS>
+__global__ void bulk_k(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, size_t n, int tile, int nbins) {
+    extern __shared__ __align__(16) uint64_t sm[];
+    const size_t t = blockIdx.x;
+    const size_t base = t * tile;
+    const int run = tile / nbins;
+    const size_t region = n / nbins;
+    for (int i = threadIdx.x; i < tile; i += THREADS) sm[i] = in[base + i];
+    __syncthreads();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int d = threadIdx.x; d < nbins; d += THREADS) {
+        const unsigned s = (unsigned)__cvta_generic_to_shared(sm + (size_t)d * run);
+        uint64_t* g = out + (size_t)d * region + t * run;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(g), "r"(s), "r"(run * 8)
+                     : "memory");
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
 int main(int argc, char** argv) {
     size_t n = argc > 1 ? strtoull(argv[1], 0, 10) : 400000000ull;
     int tile = argc > 2 ? atoi(argv[2]) : 6144;
@@ -77,6 +100,17 @@ int main(int argc, char** argv) {
         cudaEventElapsedTime(&ms, e0, e1);
         if (it == 2) printf("scatter  : tile %d bins %d run %d: %.3f ms  %.0f GB/s\n", tile, nbins, tile / nbins, ms,
                             16.0 * n / ms / 1e6);
+    }
+    cudaFuncSetAttribute(bulk_k<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, tile * 8);
+    for (int it = 0; it < 3; ++it) {
+        cudaEventRecord(e0);
+        bulk_k<512><<<(unsigned)(n / tile), 512, tile * 8>>>(a, b, n, tile, nbins);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (it == 2) printf("bulk     : tile %d bins %d run %d: %.3f ms  %.0f GB/s  (%s)\n", tile, nbins, tile / nbins, ms,
+                            16.0 * n / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
     }
     for (int G : {148, 296, 592}) {
         for (int it = 0; it < 3; ++it) {
