@@ -281,8 +281,11 @@ __device__ __forceinline__ void tile_bulk(uint64_t* s, const uint64_t* g, int of
 __device__ long long g_seg_ts[1 << 22][8];
 #define SEG_TS(i) \
     if (tid == 0) g_seg_ts[t & ((1 << 22) - 1)][i] = clock64();
+#define WS_TS(who, tt, i) \
+    if (tid == (who)) g_seg_ts[(tt) & ((1 << 22) - 1)][i] = clock64();
 #else
 #define SEG_TS(i)
+#define WS_TS(who, tt, i)
 #endif
 
 // digit of a record whose key bits start at or above bit 32 (HI) -- one
@@ -524,6 +527,257 @@ __global__ void __launch_bounds__(THREADS, LCfg<LAYOUT>::BLOCKS) k_scatter(
     }
 }
 
+// ------------------------------------------------ warp-specialised scatter
+// The record passes (SP, PP) with the write-out on its own warps: THREADS
+// "rankers" load, rank, scan and stage tile i while WS_WRITERS "writers"
+// stream tile i-1 out of its buffer and then refill that buffer with tile
+// i+2.  k_scatter runs the phases back to back, so the SM's stores stop
+// while it ranks and its ranking stops while it stores (tools/
+// seg_phase_timing.py: the write is ~37 % of a tile); here they overlap.
+// Three tile buffers (load / stage / write), one histogram.
+#ifndef MPSM_SEG_WS  // 0: record passes on k_scatter
+#define MPSM_SEG_WS 1
+#endif
+#ifndef MPSM_SEG_WS_WRITERS_SP  // writer threads (multiple of 32) of the SP / PP passes
+#define MPSM_SEG_WS_WRITERS_SP 96
+#endif
+#ifndef MPSM_SEG_WS_WRITERS_PP
+#define MPSM_SEG_WS_WRITERS_PP 128
+#endif
+template <int LAYOUT>
+struct WsCfg {
+    static constexpr int WRITERS = LAYOUT == PP ? MPSM_SEG_WS_WRITERS_PP : MPSM_SEG_WS_WRITERS_SP;
+    static constexpr int THREADS_ALL = THREADS + WRITERS;
+};
+constexpr int WS_NB = 3;
+// named barriers: 0 __syncthreads, 1 rankers, 2 writers, 3 + b buffer b staged
+constexpr int BAR_RANK = 1, BAR_WRITE = 2, BAR_STAGED = 3;
+
+template <int LAYOUT>
+struct WsSmem {
+    static constexpr int NARR = (LAYOUT == PP) ? 1 : 2;
+    static constexpr int TL = LCfg<LAYOUT>::TILE_L;
+    uint64_t buf[WS_NB][NARR][TL + 2];
+    uint32_t hist[WARPS / 2][MAX_BINS];
+    int64_t gdelta[WS_NB][MAX_BINS];  // per buffer: the writers read it while the next tile is ranked
+    uint32_t toffs[WS_NB][MAX_BINS];
+    uint32_t wtot[WARPS];
+    int64_t tile[WS_NB];
+    uint64_t bar[WS_NB];
+};
+
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <int LAYOUT, bool HI>
+__global__ void __launch_bounds__(WsCfg<LAYOUT>::THREADS_ALL, 1) k_scatter_ws(
+    const uint64_t* __restrict__ in_k, const uint64_t* __restrict__ in_p, uint64_t* __restrict__ out_k, Segs sg,
+    Digit dig, Digit odig, int nbins, const int64_t* __restrict__ base, const uint32_t* __restrict__ toffs,
+    const int64_t* __restrict__ dtot, unsigned int* __restrict__ ticket, uint64_t pk_lower, int pk_pw,
+    unsigned int* __restrict__ overflow, bool lane_ordered) {
+    static_assert(LAYOUT != SS, "record output only");
+    constexpr int WS_WRITERS = WsCfg<LAYOUT>::WRITERS, WS_THREADS = WsCfg<LAYOUT>::THREADS_ALL;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    WsSmem<LAYOUT>& sm = *reinterpret_cast<WsSmem<LAYOUT>*>(smem_raw);
+    constexpr int NARR = WsSmem<LAYOUT>::NARR;
+    constexpr int ROWS = WARPS / 2;
+    constexpr int IT = LCfg<LAYOUT>::ITEMS_L, TL = LCfg<LAYOUT>::TILE_L;
+    static_assert(32 * IT < 65536 && TL < 65536, "16-bit histogram fields");
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t T = (sg.n + TL - 1) / TL, tiles_per_seg = sg.seg_len / TL;
+    if ((int64_t)blockIdx.x >= T) return;
+    const int offk = (int)(((uintptr_t)in_k >> 3) & 1), offp = NARR == 2 ? (int)(((uintptr_t)in_p >> 3) & 1) : 0;
+    const bool ranker = tid < THREADS;
+    const bool mine = tid < nbins;
+
+    auto fetch = [&](int bb, int64_t t) {
+        const int64_t t0 = t * TL;
+        const int cnt = (int)min((int64_t)TL, sg.n - t0);
+        sm.tile[bb] = t;
+        unsigned bk = tile_plain(sm.buf[bb][0], in_k + t0, offk, cnt), bp = 0;
+        if (NARR == 2) bp = tile_plain(sm.buf[bb][NARR - 1], in_p + t0, offp, cnt);
+        const unsigned bo = MAX_BINS * 4;
+        mbar_arrive_expect_tx(&sm.bar[bb], bk + bp + bo);
+        tile_bulk(sm.buf[bb][0], in_k + t0, offk, bk, &sm.bar[bb]);
+        if (NARR == 2) tile_bulk(sm.buf[bb][NARR - 1], in_p + t0, offp, bp, &sm.bar[bb]);
+        bulk_load(sm.toffs[bb], toffs + (size_t)t * MAX_BINS, bo, &sm.bar[bb]);
+    };
+    auto fetch_next = [&](int bb) {  // one writer thread: the next tile (global order) into buffer bb
+        const int64_t t = (int64_t)gridDim.x + atomicAdd(ticket, 1u);
+        if (t < T) {
+            fetch(bb, t);
+        } else {
+            sm.tile[bb] = T;  // no more tiles: complete the phase without data
+            mbar_arrive_expect_tx(&sm.bar[bb], 0);
+        }
+    };
+
+    for (int i = tid; i < ROWS * MAX_BINS / 4; i += WS_THREADS)
+        reinterpret_cast<uint4*>(&sm.hist[0][0])[i] = make_uint4(0, 0, 0, 0);
+    int64_t dstart = 0;  // ranker d: start of digit d's output region
+    {
+        const int64_t v = mine ? dtot[tid] : 0;
+        int64_t incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        if (ranker && lane == 31) sm.gdelta[0][warp] = incl;
+        if (tid == THREADS) {
+            for (int q = 0; q < WS_NB; ++q) mbar_init(&sm.bar[q], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        if (ranker) {
+            dstart = incl - v;
+            for (int w = 0; w < warp; ++w) dstart += sm.gdelta[0][w];
+        }
+        __syncthreads();  // gdelta[0] is free again
+        if (tid == THREADS) {
+            fetch(0, blockIdx.x);
+            for (int q = 1; q < WS_NB; ++q) fetch_next(q);
+        }
+    }
+
+    if (!ranker) {  // ------------------------------------------ writers
+        const int wt = tid - THREADS;
+        for (int b = 0;; b = (b == WS_NB - 1) ? 0 : b + 1) {
+#ifdef MPSM_DBG_TIMING
+            const long long w0 = clock64();
+#endif
+            named_sync(BAR_STAGED + b, WS_THREADS);
+            const int64_t t = sm.tile[b];
+            if (t >= T) break;
+#ifdef MPSM_DBG_TIMING
+            if (tid == THREADS) g_seg_ts[t & ((1 << 22) - 1)][3] = w0;
+#endif
+            WS_TS(THREADS, t, 4)
+            const int cnt = (int)min((int64_t)TL, sg.n - t * TL);
+            const uint64_t* sb = sm.buf[b][0];
+            const int64_t* gd = sm.gdelta[b];
+#pragma unroll 4
+            for (int i = wt; i < cnt; i += WS_WRITERS) {
+                const uint64_t v = sb[i];
+                out_k[gd[rec_digit<HI>(v, odig)] + i] = v;
+            }
+            WS_TS(THREADS, t, 5)
+            named_sync(BAR_WRITE, WS_WRITERS);  // buffer b read by every writer
+            if (wt == 0) {
+                fence_proxy_async_smem();  // generic accesses to buf[b] before the bulk copy
+                fetch_next(b);
+            }
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------- rankers
+    uint32_t* hrow = sm.hist[warp >> 1];
+    const uint32_t inc = (warp & 1) ? 0x10000u : 1u;
+    const uint32_t half = (warp & 1) ? 0x4432u : 0x4410u;
+    const unsigned lt = lanemask_lt();
+    unsigned par = 0;
+    for (int b = 0;; b = (b == WS_NB - 1) ? 0 : b + 1) {
+#ifdef MPSM_DBG_TIMING
+        const long long r0 = clock64();
+#endif
+        mbar_wait(&sm.bar[b], (par >> b) & 1u);
+        par ^= 1u << b;
+        const int64_t t = sm.tile[b];
+        if (t >= T) {
+            named_arrive(BAR_STAGED + b, WS_THREADS);  // releases the writers
+            break;
+        }
+#ifdef MPSM_DBG_TIMING
+        if (tid == 0) g_seg_ts[t & ((1 << 22) - 1)][0] = r0;
+#endif
+        WS_TS(0, t, 1)
+        const int64_t sbase = mine ? base[(size_t)(t / tiles_per_seg) * nbins + tid] : 0;
+        const int cnt = (int)min((int64_t)TL, sg.n - t * TL);
+        const int wb = warp * (32 * IT);
+        const int lim = cnt - wb - lane;
+        uint64_t key[IT], pay[LAYOUT == SP ? IT : 1];
+        uint32_t rk[IT];
+#pragma unroll
+        for (int k = 0; k < IT; ++k) {
+            const int li = wb + 32 * k + lane;
+            key[k] = sm.buf[b][0][offk + li];
+            if (LAYOUT == SP) pay[k] = sm.buf[b][1][offp + li];
+        }
+        named_sync(BAR_RANK, THREADS);  // S1: the previous tile's histogram is cleared
+#pragma unroll
+        for (int k = 0; k < IT; ++k) {
+            const uint32_t dg = LAYOUT == PP ? rec_digit<HI>(key[k], dig) : dig(key[k]);
+            if (lane_ordered) {
+                if (cnt == TL || 32 * k < lim) rk[k] = __byte_perm(atomicAdd(&hrow[dg], inc), 0, half);
+            } else {
+                const bool valid = 32 * k < lim;
+                const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+                const unsigned peers = ballot_peers(dg, vmask);
+                const int leader = valid ? __ffs(peers) - 1 : lane;
+                uint32_t old = 0;
+                if (valid && leader == lane) old = atomicAdd(&hrow[dg], inc * __popc(peers));
+                old = __shfl_sync(0xffffffffu, old, leader);
+                rk[k] = __byte_perm(old, 0, half) + __popc(peers & lt);
+            }
+        }
+        named_sync(BAR_RANK, THREADS);  // S2
+        WS_TS(0, t, 6)
+        uint32_t col[ROWS];
+        uint32_t sum = 0;
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r) {
+            col[r] = mine ? sm.hist[r][tid] : 0;
+            sum += col[r];
+        }
+        const uint32_t tot = (sum & 0xffffu) + (sum >> 16);
+        uint32_t incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (lane == 31) sm.wtot[warp] = incl;
+        named_sync(BAR_RANK, THREADS);  // S3
+        const uint32_t toff = incl - tot + __reduce_add_sync(0xffffffffu, lane < warp ? sm.wtot[lane] : 0u);
+        if (mine) {
+            uint32_t run = toff;
+#pragma unroll
+            for (int r = 0; r < ROWS; ++r) {
+                const uint32_t sh = col[r] << 16;
+                sm.hist[r][tid] = run * 0x10001u + sh;
+                run += (col[r] + sh) >> 16;
+            }
+            sm.gdelta[b][tid] = dstart + sbase + sm.toffs[b][tid] - (int64_t)toff;
+        }
+        if (LAYOUT == SP) {
+            uint64_t ovf = 0;
+            const uint64_t pmask = (1ull << pk_pw) - 1ull;
+#pragma unroll
+            for (int k = 0; k < IT; ++k) {
+                if (32 * k < lim) ovf |= pay[k] >> pk_pw;
+                key[k] = ((key[k] - pk_lower) << pk_pw) | (pay[k] & pmask);
+            }
+            if (__any_sync(0xffffffffu, ovf != 0) && lane == 0) atomicOr(overflow, 1u);
+        }
+        named_sync(BAR_RANK, THREADS);  // S4
+#pragma unroll
+        for (int k = 0; k < IT; ++k) {
+            if (cnt == TL || 32 * k < lim) {
+                const uint32_t p = __byte_perm(hrow[rec_digit<HI>(key[k], odig)], 0, half) + rk[k];
+                sm.buf[b][0][p] = key[k];
+            }
+        }
+        named_sync(BAR_RANK, THREADS);  // S5: staged, histogram free
+        for (int i = tid; i < ROWS * MAX_BINS / 4; i += THREADS)
+            reinterpret_cast<uint4*>(&sm.hist[0][0])[i] = make_uint4(0, 0, 0, 0);
+        WS_TS(0, t, 2)
+        named_arrive(BAR_STAGED + b, WS_THREADS);
+    }
+}
+
 // ------------------------------------------------------------------- host
 // start-up probe: do shared atomicAdds that collide within one warp
 // instruction return their counts in lane order?  (true on sm_100; if a
@@ -644,6 +898,18 @@ static int set_attr() {
     return MPSM_OK;
 }
 
+template <int LAYOUT, bool HI>
+static int set_attr_ws() {
+    static bool done = false;
+    if (!done) {
+        MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_scatter_ws<LAYOUT, HI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)sizeof(WsSmem<LAYOUT>)),
+                             "smem attr"));
+        done = true;
+    }
+    return MPSM_OK;
+}
+
 // one digit pass: count, scan, scatter (TABLE: the digit is a partition id)
 template <int LAYOUT, bool TABLE = false>
 static int pass(const uint64_t* in_k, const uint64_t* in_p, uint64_t* out_k, uint64_t* out_p, int64_t n,
@@ -672,6 +938,19 @@ static int pass(const uint64_t* in_k, const uint64_t* in_p, uint64_t* out_k, uin
         ProfScope ps("seg_scatter", st);
         ProfScope ps2(LAYOUT == SS ? "seg_scatter_ss" : (LAYOUT == SP ? "seg_scatter_sp" : "seg_scatter_pp"), st);
         const bool lo = lane_ordered_atomics();
+        if constexpr (MPSM_SEG_WS && LAYOUT != SS && !TABLE) {
+            MPSM_TRY(hi ? (set_attr_ws<LAYOUT, true>()) : (set_attr_ws<LAYOUT, false>()));
+            const int GW = num_sms();
+            if (hi)
+                k_scatter_ws<LAYOUT, true><<<GW, WsCfg<LAYOUT>::THREADS_ALL, sizeof(WsSmem<LAYOUT>), st>>>(
+                    in_k, in_p, out_k, sg, dig, odig, nbins, ws.base, ws.toffs, ws.dtot, ws.ticket, pk_lower, pk_pw,
+                    overflow, lo);
+            else
+                k_scatter_ws<LAYOUT, false><<<GW, WsCfg<LAYOUT>::THREADS_ALL, sizeof(WsSmem<LAYOUT>), st>>>(
+                    in_k, in_p, out_k, sg, dig, odig, nbins, ws.base, ws.toffs, ws.dtot, ws.ticket, pk_lower, pk_pw,
+                    overflow, lo);
+            return check_launch("k_scatter_ws");
+        }
         if (hi)
             k_scatter<LAYOUT, true, TABLE><<<G, THREADS, sizeof(Smem<LAYOUT>), st>>>(
                 in_k, in_p, out_k, out_p, sg, dig, odig, nbins, ws.base, ws.toffs, ws.dtot, ws.ticket, pk_lower, pk_pw, overflow, lo);

@@ -70,6 +70,32 @@ __global__ void bulk_k(const uint64_t* __restrict__ in, uint64_t* __restrict__ o
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
+
+// persistent: `per_sm` CTAs per SM loop over tiles in global order from a
+// dispenser; each thread reads its elements of the tile and writes them to
+// the runs (no staging) -- isolates persistence + dispensing from the rest
+template <int THREADS>
+__global__ void persist_k(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, size_t n, int tile, int nbins,
+                          unsigned int* ticket) {
+    __shared__ unsigned int t_sh;
+    const size_t T = n / tile;
+    const int run = tile / nbins;
+    const size_t region = n / nbins;
+    for (;;) {
+        if (threadIdx.x == 0) t_sh = atomicAdd(ticket, 1u);
+        __syncthreads();
+        const size_t t = t_sh;
+        __syncthreads();
+        if (t >= T) break;
+        const size_t base = t * tile;
+        for (int i = threadIdx.x; i < tile; i += THREADS) {
+            const uint64_t v = in[base + i];
+            const int d = i / run, r = i % run;
+            out[(size_t)d * region + t * run + r] = v;
+        }
+    }
+}
+
 int main(int argc, char** argv) {
     size_t n = argc > 1 ? strtoull(argv[1], 0, 10) : 400000000ull;
     int tile = argc > 2 ? atoi(argv[2]) : 6144;
@@ -111,6 +137,21 @@ int main(int argc, char** argv) {
         cudaEventElapsedTime(&ms, e0, e1);
         if (it == 2) printf("bulk     : tile %d bins %d run %d: %.3f ms  %.0f GB/s  (%s)\n", tile, nbins, tile / nbins, ms,
                             16.0 * n / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
+    }
+    unsigned int* ticket;
+    cudaMalloc(&ticket, 4);
+    for (int per_sm : {1, 2, 4, 8}) {
+        for (int it = 0; it < 3; ++it) {
+            cudaMemset(ticket, 0, 4);
+            cudaEventRecord(e0);
+            persist_k<256><<<148 * per_sm, 256>>>(a, b, n, tile, nbins, ticket);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (it == 2) printf("persist256: %d CTA/SM tile %d bins %d: %.3f ms  %.0f GB/s\n", per_sm, tile, nbins, ms,
+                                16.0 * n / ms / 1e6);
+        }
     }
     for (int G : {148, 296, 592}) {
         for (int it = 0; it < 3; ++it) {

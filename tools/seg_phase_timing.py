@@ -31,6 +31,13 @@ L = _lib.load()
 ntiles = (n + 4095) // 4096 if (bits <= 9 or not packed) else (n + 8191) // 8192
 buf = np.zeros((ntiles, 8), np.int64)
 L.mpsm_dbg_seg_ts(buf.ctypes.data_as(ctypes.c_void_p), ntiles)
+if os.environ.get("WS"):  # k_scatter_ws: ranker thread 0 (cols 0,1,6,2), writer thread 0 (cols 3,4,5)
+    print(f"{'packed' if packed else 'pairs'} tiles={ntiles} (warp-specialised)")
+    for nm, a, b in (("ranker wait data", 0, 1), ("ranker load+rank", 1, 6), ("ranker scan+stage", 6, 2),
+                     ("writer wait staged", 3, 4), ("writer write", 4, 5)):
+        x = buf[:, b] - buf[:, a]
+        print(f"  {nm:20s} median {np.median(x):7.0f} mean {np.mean(x):7.0f} p90 {np.percentile(x, 90):7.0f}")
+    sys.exit(0)
 d = np.diff(buf[:, :6], axis=1)
 names = ["wait_data(mbar)", "load+rank+S2", "scan+S3+S4", "stage+S5", "write"]
 tot = buf[:, 5] - buf[:, 0]
