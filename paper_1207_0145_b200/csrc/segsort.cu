@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -825,9 +826,9 @@ static bool lane_ordered_atomics() {
             cudaFree(d);
         }
         state = (bad == 0 && cudaGetLastError() == cudaSuccess) ? 1 : 0;
-#ifdef MPSM_SEG_BALLOT_RANK
-        state = 0;
-#endif
+        // MPSM_SEG_BALLOT_RANK=1 forces the ballot ranking (tests of the fallback)
+        const char* force = getenv("MPSM_SEG_BALLOT_RANK");
+        if (force && force[0] == '1') state = 0;
     }
     return state == 1;
 }

@@ -323,3 +323,59 @@ def test_packed_sort_round_trip(width):
     assert np.array_equal(got_k, keys[order])
     a, b = np.lexsort((got_p, got_k)), np.lexsort((pays, keys))
     assert np.array_equal(got_p[a], pays[b])
+
+
+_STABLE_CHILD = r'''
+import sys
+import numpy as np
+import torch
+sys.path.insert(0, sys.argv[1])
+from paper_1207_0145_b200 import device as D
+dev = torch.device("cuda", 0)
+D.ensure_device()
+for n, width in ((1, 9), (4097, 9), (300_001, 27), (1_000_003, 33), (2_500_000, 20)):
+    rng = np.random.default_rng(n + width)
+    keys = rng.integers(0, 1 << width, n, dtype=np.uint64)
+    idx = np.arange(n, dtype=np.uint64)  # payload = input position: a stable sort keeps it increasing per key
+    order = np.argsort(keys, kind="stable")
+    kd, pd = torch.from_numpy(keys).to(dev), torch.from_numpy(idx).to(dev)
+    # packed (SP + PP record passes, k_scatter_ws)
+    out, tmp = torch.empty_like(kd), torch.empty_like(kd)
+    ovf = torch.zeros(1, dtype=torch.int32, device=dev)
+    D.sort_packed(kd, pd, 0, (1 << width) - 1, width, out, tmp, None, ovf)
+    rec = out.cpu().numpy()
+    pw = 64 - width
+    assert int(ovf.item()) == 0
+    assert np.array_equal(rec >> np.uint64(pw), keys[order]), ("packed keys", n, width)
+    assert np.array_equal(rec & np.uint64((1 << pw) - 1), idx[order]), ("packed stability", n, width)
+    # records in, records out (PP only)
+    rin_np = rec[rng.permutation(n)]
+    out2, tmp2 = torch.empty_like(kd), torch.empty_like(kd)
+    D.sort_records(torch.from_numpy(rin_np).to(dev), width, out2, tmp2)
+    want = rin_np[np.argsort(rin_np >> np.uint64(pw), kind="stable")]
+    assert np.array_equal(out2.cpu().numpy(), want), ("records", n, width)
+    # pairs (SS passes, k_scatter)
+    ok, op, tk, tp = (torch.empty_like(kd) for _ in range(4))
+    D.sort_pairs(kd, pd, 0, (1 << width) - 1, width, ok, op, tk, tp, None)
+    assert np.array_equal(ok.cpu().numpy(), keys[order]), ("pairs keys", n, width)
+    assert np.array_equal(op.cpu().numpy(), idx[order]), ("pairs stability", n, width)
+print("STABLE-OK lane_ordered=%d" % D._lib.load().mpsm_dbg_lane_ordered())
+'''
+
+
+@pytest.mark.parametrize("ballot", ["0", "1"], ids=["lane-ordered-atomics", "ballot-fallback"])
+def test_sorts_are_stable_on_both_ranking_paths(ballot):
+    """Every scatter kernel (pairs, packing, record passes) is a stable
+    pass, with the lane-ordered shared-atomic ranking and with the warp-ballot
+    fallback the library uses where the start-up probe fails
+    (MPSM_SEG_BALLOT_RANK=1 forces it; read once per process)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MPSM_SEG_BALLOT_RANK=ballot)
+    r = subprocess.run([sys.executable, "-c", _STABLE_CHILD, root], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert "STABLE-OK" in r.stdout, r.stdout + r.stderr
+    assert f"lane_ordered={1 - int(ballot)}" in r.stdout or ballot == "0", r.stdout
