@@ -572,7 +572,7 @@ __device__ __forceinline__ void named_arrive(int id, int n) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-template <int LAYOUT, bool HI>
+template <int LAYOUT, bool HI, bool TABLE = false>
 __global__ void __launch_bounds__(WsCfg<LAYOUT>::THREADS_ALL, 1) k_scatter_ws(
     const uint64_t* __restrict__ in_k, const uint64_t* __restrict__ in_p, uint64_t* __restrict__ out_k, Segs sg,
     Digit dig, Digit odig, int nbins, const int64_t* __restrict__ base, const uint32_t* __restrict__ toffs,
@@ -662,7 +662,7 @@ __global__ void __launch_bounds__(WsCfg<LAYOUT>::THREADS_ALL, 1) k_scatter_ws(
 #pragma unroll 4
             for (int i = wt; i < cnt; i += WS_WRITERS) {
                 const uint64_t v = sb[i];
-                out_k[gd[rec_digit<HI>(v, odig)] + i] = v;
+                out_k[gd[TABLE ? odig.lookup(v) : rec_digit<HI>(v, odig)] + i] = v;
             }
             WS_TS(THREADS, t, 5)
             named_sync(BAR_WRITE, WS_WRITERS);  // buffer b read by every writer
@@ -710,7 +710,8 @@ __global__ void __launch_bounds__(WsCfg<LAYOUT>::THREADS_ALL, 1) k_scatter_ws(
         named_sync(BAR_RANK, THREADS);  // S1: the previous tile's histogram is cleared
 #pragma unroll
         for (int k = 0; k < IT; ++k) {
-            const uint32_t dg = LAYOUT == PP ? rec_digit<HI>(key[k], dig) : dig(key[k]);
+            const uint32_t dg =
+                TABLE ? dig.lookup(key[k]) : (LAYOUT == PP ? rec_digit<HI>(key[k], dig) : dig(key[k]));
             if (lane_ordered) {
                 if (cnt == TL || 32 * k < lim) rk[k] = __byte_perm(atomicAdd(&hrow[dg], inc), 0, half);
             } else {
@@ -767,7 +768,8 @@ __global__ void __launch_bounds__(WsCfg<LAYOUT>::THREADS_ALL, 1) k_scatter_ws(
 #pragma unroll
         for (int k = 0; k < IT; ++k) {
             if (cnt == TL || 32 * k < lim) {
-                const uint32_t p = __byte_perm(hrow[rec_digit<HI>(key[k], odig)], 0, half) + rk[k];
+                const uint32_t d = TABLE ? odig.lookup(key[k]) : rec_digit<HI>(key[k], odig);
+                const uint32_t p = __byte_perm(hrow[d], 0, half) + rk[k];
                 sm.buf[b][0][p] = key[k];
             }
         }
@@ -899,11 +901,11 @@ static int set_attr() {
     return MPSM_OK;
 }
 
-template <int LAYOUT, bool HI>
+template <int LAYOUT, bool HI, bool TABLE>
 static int set_attr_ws() {
     static bool done = false;
     if (!done) {
-        MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_scatter_ws<LAYOUT, HI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_scatter_ws<LAYOUT, HI, TABLE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   (int)sizeof(WsSmem<LAYOUT>)),
                              "smem attr"));
         done = true;
@@ -939,15 +941,15 @@ static int pass(const uint64_t* in_k, const uint64_t* in_p, uint64_t* out_k, uin
         ProfScope ps("seg_scatter", st);
         ProfScope ps2(LAYOUT == SS ? "seg_scatter_ss" : (LAYOUT == SP ? "seg_scatter_sp" : "seg_scatter_pp"), st);
         const bool lo = lane_ordered_atomics();
-        if constexpr (MPSM_SEG_WS && LAYOUT != SS && !TABLE) {
-            MPSM_TRY(hi ? (set_attr_ws<LAYOUT, true>()) : (set_attr_ws<LAYOUT, false>()));
+        if constexpr (MPSM_SEG_WS && LAYOUT != SS) {
+            MPSM_TRY(hi ? (set_attr_ws<LAYOUT, true, TABLE>()) : (set_attr_ws<LAYOUT, false, TABLE>()));
             const int GW = num_sms();
             if (hi)
-                k_scatter_ws<LAYOUT, true><<<GW, WsCfg<LAYOUT>::THREADS_ALL, sizeof(WsSmem<LAYOUT>), st>>>(
+                k_scatter_ws<LAYOUT, true, TABLE><<<GW, WsCfg<LAYOUT>::THREADS_ALL, sizeof(WsSmem<LAYOUT>), st>>>(
                     in_k, in_p, out_k, sg, dig, odig, nbins, ws.base, ws.toffs, ws.dtot, ws.ticket, pk_lower, pk_pw,
                     overflow, lo);
             else
-                k_scatter_ws<LAYOUT, false><<<GW, WsCfg<LAYOUT>::THREADS_ALL, sizeof(WsSmem<LAYOUT>), st>>>(
+                k_scatter_ws<LAYOUT, false, TABLE><<<GW, WsCfg<LAYOUT>::THREADS_ALL, sizeof(WsSmem<LAYOUT>), st>>>(
                     in_k, in_p, out_k, sg, dig, odig, nbins, ws.base, ws.toffs, ws.dtot, ws.ticket, pk_lower, pk_pw,
                     overflow, lo);
             return check_launch("k_scatter_ws");
