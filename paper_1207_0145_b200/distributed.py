@@ -132,10 +132,14 @@ class CudaBackend:
         D.sort_pairs(k, p, self.dom.lower, self.span_m1, self.wbits, ok, op, tk, tp, self.bad)
         return (ok, op)
 
-    def histogram(self, keys, shift: int, nb: int) -> np.ndarray:
+    def histogram_async(self, keys, shift: int, nb: int) -> torch.Tensor:
+        """Queue the private histogram; read it with .cpu() later."""
         counts = torch.zeros(nb, dtype=torch.int64, device=self.dev)
         D.radix_histogram(keys, self.dom.lower, self.span_m1, shift, nb, counts, self.bad)
-        return counts.cpu().numpy()
+        return counts
+
+    def histogram(self, keys, shift: int, nb: int) -> np.ndarray:
+        return self.histogram_async(keys, shift, nb).cpu().numpy()
 
     def bound_keys(self, run, f: int, t: int) -> np.ndarray:
         n = int(run[0].numel())
@@ -207,7 +211,49 @@ class CudaBackend:
         torch.cuda.current_stream().synchronize()
 
 
+def _gather_u64(vec, group, device) -> np.ndarray:
+    """all-gather of one fixed-length u64 vector per rank -> [G, L].  One
+    tensor collective (NCCL on the GPU, gloo on the host) instead of the
+    pickling two-step all_gather_object: the protocol's host round trips are
+    on the critical path between the public sort and the partition."""
+    vec = np.ascontiguousarray(vec, dtype=np.uint64)
+    G = dist.get_world_size(group)
+    if G == 1:
+        return vec[None, :].copy()
+    t = torch.from_numpy(vec.view(np.int64).copy()).to(device)
+    outs = [torch.empty_like(t) for _ in range(G)]
+    dist.all_gather(outs, t, group=group)
+    return torch.stack(outs).cpu().numpy().view(np.uint64)
+
+
+def _enc_share(shared) -> np.ndarray:
+    """CudaBackend.share() of a run -> fixed u64 layout (per slot: present,
+    numel, offset, 64-B handle)"""
+    out = np.zeros(2 * 11, np.uint64)
+    for i, sh in enumerate(shared):
+        if sh is None:
+            continue
+        h, off, n = sh
+        out[11 * i:11 * i + 3] = (1, n, off)
+        if n:
+            out[11 * i + 3:11 * i + 11] = np.frombuffer(h, np.uint64)
+    return out
+
+
+def _dec_share(v: np.ndarray) -> list:
+    slots = []
+    for i in range(2):
+        if v[11 * i] == 0:
+            slots.append(None)
+            continue
+        n, off = int(v[11 * i + 1]), int(v[11 * i + 2])
+        slots.append((v[11 * i + 3:11 * i + 11].tobytes() if n else b"", off, n))
+    return slots
+
+
 def _gather_obj(obj, group):
+    if dist.get_world_size(group) == 1:
+        return [obj]
     out = [None] * dist.get_world_size(group)
     dist.all_gather_object(out, obj, group=group)
     return out
@@ -248,8 +294,16 @@ def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=Non
     dom = cfg.key_domain
     be.setup(dom)
     t0 = time.perf_counter()
-    sizes = _gather_obj((r.cardinality, s.cardinality), group)
-    n_r, n_s = sum(x[0] for x in sizes), sum(x[1] for x in sizes)
+    trace = [] if (timings is not None and os.environ.get("MPSM_DIST_TRACE") == "1") else None
+
+    def _tr(what):  # host timeline (tools/dist_phase_timing.py)
+        if trace is not None:
+            trace.append((what, 1e3 * (time.perf_counter() - t0)))
+
+    cdev = getattr(be, "comm_device", torch.device("cpu"))
+    sizes = _gather_u64([r.cardinality, s.cardinality], group, cdev).astype(np.int64)
+    _tr("sizes gathered")
+    n_r, n_s = int(sizes[:, 0].sum()), int(sizes[:, 1].sum())
     roles = choose_roles(n_r, n_s, cfg.role_policy)
     private, public = (r, s) if roles.private == "r" else (s, r)
     bits = effective_radix_bits(dom, cfg.radix_bits)
@@ -262,15 +316,29 @@ def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=Non
     pk, pp = be.to_device(private.keys), be.to_device(private.payloads)
     stats = [WorkerStats(i) for i in range(G)]
 
-    # 1-2: public run, private histogram, bounds
+    # 1-2: private histogram (queued first: it needs only the private
+    # shard), public run, bounds
+    h_dev = be.histogram_async(pk, shift, nb) if hasattr(be, "histogram_async") else None
     if pub_rec is not None:
         pub_run = be.sort_records(pub_rec)
     else:
         pub_run = be.sort(be.to_device(public.keys), be.to_device(public.payloads))
-    hist = be.histogram(pk, shift, nb)
+    hist = h_dev.cpu().numpy() if h_dev is not None else be.histogram(pk, shift, nb)
     f = cfg.cdf_fanout
-    bk = be.bound_keys(pub_run, f, G)
-    info = _gather_obj((hist, bk, int(public.cardinality), be.bad_index()), group)
+    bk = np.asarray(be.bound_keys(pub_run, f, G), np.uint64)
+    _tr("public sorted, hist + bounds on host")
+    # per rank: [hist (nb) | public cardinality | bad index | #bounds | f*G bounds]
+    kb = f * G
+    vec = np.zeros(nb + 3 + kb, np.uint64)
+    vec[:nb] = np.asarray(hist, np.int64).view(np.uint64)
+    vec[nb:nb + 3] = np.array([int(public.cardinality), be.bad_index(), bk.shape[0]], np.int64).view(np.uint64)
+    vec[nb + 3:nb + 3 + bk.shape[0]] = bk
+    allv = _gather_u64(vec, group, cdev)
+    info = []
+    for v in allv:
+        card, bad, nbk = (int(x) for x in v[nb:nb + 3].view(np.int64))
+        info.append((v[:nb].view(np.int64).copy(), v[nb + 3:nb + 3 + nbk].copy(), card, bad))
+    _tr("gathered")
     if any(x[3] != -1 for x in info):
         raise DomainError("a relation shard has out-of-domain keys")
     t_pub = time.perf_counter()
@@ -284,6 +352,7 @@ def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=Non
     recv_counts = cursors.counts[:, me]
     send_starts = np.zeros(G, np.int64)
     np.cumsum(send_counts[:-1], out=send_starts[1:])
+    _tr("splitters")
     # 4-5: scatter into send segments, one all-to-all
     rec = be.partition_records(pk, pp, shift, ss.vector.sp, G) if hasattr(be, "partition_records") else None
     if rec is None:
@@ -295,17 +364,22 @@ def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=Non
         rk, rp = _alltoall(be, sk, sp, send_counts, recv_counts, group)
         n_recv_priv = int(rk.numel())
     t_part = time.perf_counter()
+    _tr("partition + all-to-all issued")
     # 6: private run
     priv_run = be.sort_records(rr) if rec is not None else be.sort(rk, rp)
     be.sync()
     t_sort = time.perf_counter()
+    _tr("private sorted")
     # 7: join against every public run (remote ones through peer mappings)
     # rank-rotated order, own run first (engine.py:251: (i + k) % T): at any
     # moment each rank reads a different peer, so no peer's NVLink serves
     # all readers at once
     order = [(me + k) % G for k in range(G)]
     if G > 1:
-        shared = _gather_obj(be.share(pub_run), group)
+        if isinstance(be, CudaBackend):  # IPC handles: fixed layout, one tensor gather
+            shared = [_dec_share(v) for v in _gather_u64(_enc_share(be.share(pub_run)), group, cdev)]
+        else:
+            shared = _gather_obj(be.share(pub_run), group)
         pub_runs = [pub_run if j == me else be.open(shared[j]) for j in order]
     else:
         pub_runs = [pub_run]
@@ -315,7 +389,8 @@ def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=Non
     rec_h = np.empty_like(rec_rot)
     rec_h[order] = rec_rot  # back to public-run (rank) order
     overflow = be.overflowed()
-    gathered = _gather_obj((rec_h, n_recv_priv, overflow), group)
+    fin = np.concatenate([np.asarray(rec_h, np.uint64).ravel(), np.array([n_recv_priv, int(overflow)], np.uint64)])
+    gathered = [(v[:-2].reshape(G, _lib.PAIR_FIELDS), int(v[-2]), bool(v[-1])) for v in _gather_u64(fin, group, cdev)]
     if any(g[2] for g in gathered):
         # a payload is wider than a packed record allows: redo on pairs
         be2 = type(be)(packed=False, comm_device=be.comm_device) if isinstance(be, CudaBackend) else be.unpacked()
@@ -359,6 +434,9 @@ def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=Non
           "join": t_join - t_sort, "total": t_join - t0}
     if timings is not None:
         timings.update(tm)
+        if trace is not None:
+            _tr("folded")
+            timings["trace"] = trace
     return JoinResult(match_count=int(count), aggregate_max=agg, materialized=materialized, phase_timings=tm,
                       worker_stats=stats, checksum=int(csum))
 

@@ -161,7 +161,10 @@ def _edge_cdf(cdf: Cdf, dom: KeyDomain, radix_bits: int) -> np.ndarray:
     n = 1 << radix_bits
     sh = dom.width_bits - radix_bits
     top = (1 << 64) - 1
-    edges = np.array([min(dom.lower + (e << sh), top) for e in range(n + 1)], np.uint64)
+    if dom.lower + (n << sh) <= top:  # no edge saturates: exact in u64
+        edges = np.uint64(dom.lower) + (np.arange(n + 1, dtype=np.uint64) << np.uint64(sh))
+    else:
+        edges = np.array([min(dom.lower + (e << sh), top) for e in range(n + 1)], np.uint64)
     return cdf.eval_many(edges)
 
 

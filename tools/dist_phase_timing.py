@@ -27,6 +27,9 @@ for it in range(4):
     res = run_join_distributed(r, s, cfg, backend=be, timings=tm)
     torch.cuda.synchronize()
     if me == 0:
+        trace = tm.pop("trace", None)
         print(f"iter {it}: wall {1e3 * (time.perf_counter() - t0):.2f} ms  " +
               "  ".join(f"{k} {1e3 * v:.2f}" for k, v in tm.items()), flush=True)
+        if trace:  # MPSM_DIST_TRACE=1: host timeline of the protocol
+            print("   " + "  ".join(f"{w} @{ms:.2f}" for w, ms in trace), flush=True)
 dist.destroy_process_group()
