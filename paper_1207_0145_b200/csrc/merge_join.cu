@@ -535,22 +535,34 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
             // phase 2 -- W tuples dealt round-robin (balanced, no merge
             // control flow): each matches the equal-key R group ending at
             // tile index ub - 1 (walked back; usually one tuple)
-            const uint64_t pmask = pi.pmask;
+            // K32: the payload field covers the whole low word, so the mask
+            // touches the high word only
+            const uint64_t pmask = K32 ? (pi.pmask | 0xffffffffull) : pi.pmask;
             auto acc = [&](uint64_t rp, uint64_t sp) {
                 const uint64_t v = rp + sp;
                 best = v > best ? v : best;
                 ++count;
                 csum += swap ? pair_hash(sp, rp) : pair_hash(rp, sp);
             };
-            if (!sm.tdup[buf]) {  // unique R keys: at most one match per W tuple
+            // unique R keys: at most one match per W tuple; the orientation
+            // test is hoisted out of the loop (SW: checksum of (s, r))
+            auto unique_pass = [&](auto SW) {
                 MPSM_UNROLL(MPSM_MJ_P2_UNROLL)
                 for (int j = tid; j < nW; j += MJ_THREADS) {
                     const int i = (int)sm.ub[j] - 1;
                     if (i < -hp) continue;  // no R tuple <= the key (tile at the run start)
                     const uint64_t wv = WK[j], rv = RK[i];
                     if (nkey(rv) != nkey(wv)) continue;
-                    acc(PK ? (rv & pmask) : RP[i], PK ? (wv & pmask) : WP[j]);
+                    const uint64_t rp = PK ? (rv & pmask) : RP[i], sp = PK ? (wv & pmask) : WP[j];
+                    const uint64_t v = rp + sp;
+                    best = v > best ? v : best;
+                    ++count;
+                    csum += decltype(SW)::value ? pair_hash(sp, rp) : pair_hash(rp, sp);
                 }
+            };
+            if (!sm.tdup[buf]) {
+                if (swap) unique_pass(std::true_type{});
+                else unique_pass(std::false_type{});
             } else
             for (int j = tid; j < nW; j += MJ_THREADS) {
                 const uint64_t wv = WK[j];
