@@ -333,7 +333,8 @@ sys.path.insert(0, sys.argv[1])
 from paper_1207_0145_b200 import device as D
 dev = torch.device("cuda", 0)
 D.ensure_device()
-for n, width in ((1, 9), (4097, 9), (300_001, 27), (1_000_003, 33), (2_500_000, 20)):
+for n, width in ((1, 9), (4097, 9), (8193, 27), (300_001, 27), (1_000_003, 33), (2_500_000, 20),
+                 (5_000_000, 18), (1_300_000, 10), (70_000, 3)):
     rng = np.random.default_rng(n + width)
     keys = rng.integers(0, 1 << width, n, dtype=np.uint64)
     idx = np.arange(n, dtype=np.uint64)  # payload = input position: a stable sort keeps it increasing per key
