@@ -67,6 +67,7 @@ struct PackInfo {
     int pw;          // payload bits of a packed record (0: SoA runs)
     uint64_t lower;  // key domain lower bound (packed keys are key - lower)
     uint64_t pmask;  // (1 << pw) - 1
+    uint32_t kmask;  // pw >= 32: payload bits in a record's high word, (1 << (pw - 32)) - 1
 };
 
 // original key of element i of a run
@@ -154,7 +155,7 @@ __global__ void k_interp_batch(const uint64_t* __restrict__ keys, int64_t n, con
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nt) return;
     int64_t pr = 0;
-    const int64_t r = interp_lb<false>(keys, n, targets[t], &pr, PackInfo{0, 0, 0});
+    const int64_t r = interp_lb<false>(keys, n, targets[t], &pr, PackInfo{0, 0, 0, 0});
     idx[t] = r;
     if (probes) probes[t] = pr;
 }
@@ -484,8 +485,12 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
         const uint64_t* RP = PK ? RK : sm.st[buf].p + q.rp.off + hp;
         const uint64_t* WP = PK ? WK : sm.st[buf].p + q.rp.bytes / 8 + q.wp.off;
         // normalized keys and payloads; K32: packed keys of a domain at most
-        // 32 bits wide compare as u32
-        auto nkey = [&](uint64_t v) -> KT { return PK ? (KT)(v >> pi.pw) : (KT)v; };
+        // 32 bits wide compare as their record's high word with the payload
+        // bits in it set (same order and equality as the keys; no shift)
+        auto nkey = [&](uint64_t v) -> KT {
+            if (K32) return (KT)((uint32_t)(v >> 32) | pi.kmask);
+            return PK ? (KT)(v >> pi.pw) : (KT)v;
+        };
         auto rkey = [&](int i) -> KT { return nkey(RK[i]); };
         auto wkey = [&](int j) -> KT { return nkey(WK[j]); };
         auto rpay = [&](int i) -> uint64_t { return PK ? (RP[i] & pi.pmask) : RP[i]; };
@@ -849,7 +854,7 @@ extern "C" int mpsm_join_pairs(const mpsm_run_t* priv, int n_priv, const mpsm_ru
                                size_t ws_bytes, void* stream) {
     (void)cap;  // the caller sized d_out from the counts of a first call
     return join_pairs_impl<false>(priv, n_priv, pub, n_pub, swap, mode, d_out, d_pairs, workspace, ws_bytes,
-                                  PackInfo{0, 0, 0}, (cudaStream_t)stream);
+                                  PackInfo{0, 0, 0, 0}, (cudaStream_t)stream);
 }
 
 extern "C" int mpsm_join_pairs_packed(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub,
@@ -859,5 +864,6 @@ extern "C" int mpsm_join_pairs_packed(const mpsm_run_t* priv, int n_priv, const 
     if (width_bits < 1 || width_bits > 63) return MPSM_ERR_ARG;
     const int pw = 64 - width_bits;
     return join_pairs_impl<true>(priv, n_priv, pub, n_pub, swap, mode, d_out, d_pairs, workspace, ws_bytes,
-                                 PackInfo{pw, lower, (1ull << pw) - 1}, (cudaStream_t)stream);
+                                 PackInfo{pw, lower, (1ull << pw) - 1, pw >= 32 ? (1u << (pw - 32)) - 1u : 0u},
+                                 (cudaStream_t)stream);
 }
