@@ -18,9 +18,11 @@ Printed JSON line (rank 0):
              over ranks
   e2e        the same through run_join with pinned HOST buffers: H2D of the
              inputs and D2H of the result inside the timed region
-  roofline   onesweep radix pass (the dominant kernel): algorithmic bytes
-             (32 B per tuple per pass) / summed CUDA-event launch time inside
-             the timed region vs MEASURED_PEAKS.json hbm_gbs
+  roofline   the radix scatter pass seg::k_scatter[_ws] (the dominant kernel):
+             algorithmic bytes (packing pass 16 + 8, record passes 8 + 8 B per
+             tuple) / its summed CUDA-event launch time inside the timed region
+             vs MEASURED_PEAKS.json hbm_gbs; traffic from the committed ncu
+             capture (profiles/traffic_scatter.json)
   cpu_baseline  the reference package (oracle/_ref, numba, all host threads)
              on a bounded sample of the same workload
 ``--impl reference`` times the reference's own CPU implementation instead.
