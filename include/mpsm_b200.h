@@ -212,7 +212,10 @@ int mpsm_relfile_header(const char* path, uint64_t* n, int64_t* bad_offset);
 /* reads the n records (16 n bytes, interleaved) into host memory dst (pinned
  * or pageable) with `threads` parallel readers (0: all cores) */
 int mpsm_relfile_read(const char* path, uint64_t n, void* dst, int threads);
-/* writes a relation file from SoA host arrays */
+/* reads the n records straight into SoA host arrays keys / pays (the reading
+ * threads split the records; read_relation's columns, bench.py:100-102) */
+int mpsm_relfile_read_columns(const char* path, uint64_t n, uint64_t* keys, uint64_t* pays, int threads);
+/* writes a relation file from SoA host arrays (parallel, all cores) */
 int mpsm_relfile_write(const char* path, const uint64_t* keys, const uint64_t* pays, uint64_t n);
 /* device: split n interleaved records into SoA keys / payloads */
 int mpsm_deinterleave(const uint64_t* d_records, int64_t n, uint64_t* d_keys, uint64_t* d_pays, void* stream);

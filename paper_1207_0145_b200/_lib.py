@@ -33,7 +33,8 @@ EXPORTS = (
     "mpsm_join_workspace_bytes", "mpsm_join_pairs", "mpsm_join_pairs_packed",
     "mpsm_minmax_contiguous",
     "mpsm_ipc_get_handle", "mpsm_ipc_open_handle", "mpsm_ipc_close_handle",
-    "mpsm_relfile_header", "mpsm_relfile_read", "mpsm_relfile_write", "mpsm_deinterleave",
+    "mpsm_relfile_header", "mpsm_relfile_read", "mpsm_relfile_read_columns", "mpsm_relfile_write",
+    "mpsm_deinterleave",
     "mpsm_upload_records", "mpsm_upload_bytes", "mpsm_sort_records", "mpsm_pack_records", "mpsm_partition_records",
 )
 
@@ -71,6 +72,7 @@ _SIGS = {
     "mpsm_ipc_close_handle": (_int, [_vp]),
     "mpsm_relfile_header": (_int, [ctypes.c_char_p, ctypes.POINTER(_u64), ctypes.POINTER(_i64)]),
     "mpsm_relfile_read": (_int, [ctypes.c_char_p, _u64, _vp, _int]),
+    "mpsm_relfile_read_columns": (_int, [ctypes.c_char_p, _u64, _vp, _vp, _int]),
     "mpsm_relfile_write": (_int, [ctypes.c_char_p, _vp, _vp, _u64]),
     "mpsm_deinterleave": (_int, [_vp, _i64, _vp, _vp, _vp]),
     "mpsm_upload_records": (_int, [_vp, _vp, _i64, _u64, _u64, _int, _vp, _int, _int, _vp, _vp,

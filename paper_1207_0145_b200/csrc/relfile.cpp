@@ -2,7 +2,9 @@
 // (magic "MPSMREL1", u64 n, n interleaved little-endian (key, payload) u64
 // records; /root/reference/pkg/src/mpsm/bench.py:8-11,73-102).  Reading is
 // parallel pread into the caller's (ideally pinned) buffer, so a file moves
-// to the GPU as one H2D copy plus mpsm_deinterleave.
+// to the GPU as one H2D copy plus mpsm_deinterleave; host columns are split
+// by the reading threads themselves, and writing is parallel pwrite of
+// interleaved blocks (tools/relfile_bench.py).
 
 #include <fcntl.h>
 #include <sys/stat.h>
@@ -53,6 +55,39 @@ bool write_all(int fd, const char* src, size_t bytes) {
     }
     return true;
 }
+
+bool pwrite_all(int fd, const char* src, size_t bytes, off_t off) {
+    while (bytes) {
+        const ssize_t r = ::pwrite(fd, src, bytes, off);
+        if (r <= 0) return false;
+        src += r;
+        off += r;
+        bytes -= (size_t)r;
+    }
+    return true;
+}
+
+// records [0, n) split over `threads` workers in contiguous ranges; fn(a, b)
+// returns false on an I/O error
+template <class F>
+bool parallel_ranges(uint64_t n, int threads, F fn) {
+    if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+    const uint64_t per = std::max<uint64_t>((uint64_t)1 << 20, (n + threads - 1) / threads);
+    std::vector<std::thread> pool;
+    std::vector<char> ok;
+    for (uint64_t a = 0; a < n; a += per) ok.push_back(1);
+    size_t i = 0;
+    for (uint64_t a = 0; a < n; a += per, ++i) {
+        const uint64_t b = std::min(n, a + per);
+        pool.emplace_back([&, a, b, i] { ok[i] = fn(a, b) ? 1 : 0; });
+    }
+    for (auto& t : pool) t.join();
+    for (char c : ok)
+        if (!c) return false;
+    return true;
+}
+
+constexpr uint64_t kBlock = 1 << 16;  // records per thread-local block (1 MB)
 
 }  // namespace
 
@@ -126,6 +161,32 @@ extern "C" int mpsm_relfile_read(const char* path, uint64_t n, void* dst, int th
     return MPSM_OK;
 }
 
+extern "C" int mpsm_relfile_read_columns(const char* path, uint64_t n, uint64_t* keys, uint64_t* pays, int threads) {
+    if (!path || (n && (!keys || !pays))) return MPSM_ERR_ARG;
+    Fd f(path, O_RDONLY);
+    if (f.fd < 0) {
+        mpsm::set_error(std::string("cannot open ") + path + ": " + std::strerror(errno));
+        return MPSM_ERR_IO;
+    }
+    const bool ok = parallel_ranges(n, threads, [&](uint64_t a, uint64_t b) {
+        std::vector<uint64_t> buf(2 * kBlock);
+        for (uint64_t i = a; i < b; i += kBlock) {
+            const size_t m = (size_t)std::min<uint64_t>(kBlock, b - i);
+            if (!pread_all(f.fd, (char*)buf.data(), 16 * m, (off_t)(16 + 16 * i))) return false;
+            for (size_t j = 0; j < m; ++j) {
+                keys[i + j] = buf[2 * j];
+                pays[i + j] = buf[2 * j + 1];
+            }
+        }
+        return true;
+    });
+    if (!ok) {
+        mpsm::set_error(std::string("short read from ") + path);
+        return MPSM_ERR_IO;
+    }
+    return MPSM_OK;
+}
+
 extern "C" int mpsm_relfile_write(const char* path, const uint64_t* keys, const uint64_t* pays, uint64_t n) {
     if (!path || (n && (!keys || !pays))) return MPSM_ERR_ARG;
     Fd f(path, O_WRONLY | O_CREAT | O_TRUNC);
@@ -137,18 +198,22 @@ extern "C" int mpsm_relfile_write(const char* path, const uint64_t* keys, const 
     std::memcpy(hdr, kMagic, 8);
     std::memcpy(hdr + 8, &n, 8);
     if (!write_all(f.fd, hdr, 16)) return MPSM_ERR_IO;
-    constexpr size_t B = 1 << 16;  // records per block
-    std::vector<uint64_t> buf(2 * B);
-    for (uint64_t i = 0; i < n; i += B) {
-        const size_t m = (size_t)std::min<uint64_t>(B, n - i);
-        for (size_t j = 0; j < m; ++j) {
-            buf[2 * j] = keys[i + j];
-            buf[2 * j + 1] = pays[i + j];
+    // interleaved blocks written at their offsets by parallel workers
+    const bool ok = parallel_ranges(n, 0, [&](uint64_t a, uint64_t b) {
+        std::vector<uint64_t> buf(2 * kBlock);
+        for (uint64_t i = a; i < b; i += kBlock) {
+            const size_t m = (size_t)std::min<uint64_t>(kBlock, b - i);
+            for (size_t j = 0; j < m; ++j) {
+                buf[2 * j] = keys[i + j];
+                buf[2 * j + 1] = pays[i + j];
+            }
+            if (!pwrite_all(f.fd, (const char*)buf.data(), 16 * m, (off_t)(16 + 16 * i))) return false;
         }
-        if (!write_all(f.fd, (const char*)buf.data(), 16 * m)) {
-            mpsm::set_error(std::string("short write to ") + path);
-            return MPSM_ERR_IO;
-        }
+        return true;
+    });
+    if (!ok) {
+        mpsm::set_error(std::string("short write to ") + path);
+        return MPSM_ERR_IO;
     }
     return MPSM_OK;
 }

@@ -44,13 +44,16 @@ def _read_records(path, n: int, dst_ptr: int, threads: int = 0) -> None:
     _lib.check(_lib.load().mpsm_relfile_read(_path(path), n, dst_ptr, threads), "mpsm_relfile_read")
 
 
-def read_relation(path) -> Relation:
-    """Load a relation into host memory (numpy), checking magic and length."""
+def read_relation(path, threads: int = 0) -> Relation:
+    """Load a relation into host memory (numpy), checking magic and length;
+    the reading threads split the records into the two columns."""
     n = read_header(path)
-    rec = np.empty(2 * n, dtype="<u8")
+    keys = np.empty(n, dtype="<u8")
+    pays = np.empty(n, dtype="<u8")
     if n:
-        _read_records(path, n, rec.ctypes.data)
-    return Relation(rec[0::2].copy(), rec[1::2].copy())
+        _lib.check(_lib.load().mpsm_relfile_read_columns(_path(path), n, keys.ctypes.data, pays.ctypes.data, threads),
+                   "mpsm_relfile_read_columns")
+    return Relation(keys, pays)
 
 
 def write_relation(rel: Relation, path) -> None:
