@@ -380,3 +380,59 @@ def test_sorts_are_stable_on_both_ranking_paths(ballot):
                        timeout=600)
     assert "STABLE-OK" in r.stdout, r.stdout + r.stderr
     assert f"lane_ordered={1 - int(ballot)}" in r.stdout or ballot == "0", r.stdout
+
+
+# ------------------------------------------------------- unaligned buffers
+
+@pytest.mark.parametrize("off_r,off_s", [(1, 0), (0, 1), (1, 3), (3, 1)])
+def test_unaligned_device_views_match_oracle(off_r, off_s, pack_mode):
+    """Inputs that are views at an 8-B (not 16-B) offset: the sorts' bulk
+    tile copies move the aligned body and copy the head/tail elements
+    themselves (segsort.cu tile_plain), the merge stages aligned supersets."""
+    r, s, dom = P.gen_fk(300_001, 1_200_007, 11)
+    want = orc.fk_gather(r.keys, r.payloads, s.keys, s.payloads, 1)
+
+    def view(a, off):
+        buf = torch.empty(a.shape[0] + off, dtype=torch.uint64, device=DEV)
+        buf[off:] = torch.from_numpy(a).to(DEV)
+        return buf[off:]
+
+    rd = Relation(view(r.keys, off_r), view(r.payloads, off_s))
+    sd = Relation(view(s.keys, off_s), view(s.payloads, off_r))
+    assert rd.keys.data_ptr() % 16 == 8 * (off_r % 2)
+    for t in (1, 3):
+        res = P.run_join(rd, sd, JoinConfig(threads=t, key_domain=dom))
+        assert (res.match_count, res.aggregate_max, res.checksum) == want
+
+
+@pytest.mark.parametrize("off", [1, 3])
+def test_sorts_into_unaligned_outputs(off):
+    """every sort entry with input, output and scratch buffers at 8-B offsets"""
+    n, width = 70_001, 27
+    rng = np.random.default_rng(off)
+    keys = rng.integers(0, 1 << width, n, dtype=np.uint64)
+    idx = np.arange(n, dtype=np.uint64)
+    order = np.argsort(keys, kind="stable")
+
+    def buf(src=None):
+        b = torch.empty(n + off, dtype=torch.uint64, device=DEV)[off:]
+        if src is not None:
+            b.copy_(torch.from_numpy(src).to(DEV))
+        return b
+
+    kd, pd = buf(keys), buf(idx)
+    out, tmp = buf(), buf()
+    ovf = torch.zeros(1, dtype=torch.int32, device=DEV)
+    D.sort_packed(kd, pd, 0, (1 << width) - 1, width, out, tmp, None, ovf)
+    rec = out.cpu().numpy()
+    pw = 64 - width
+    assert np.array_equal(rec >> np.uint64(pw), keys[order])
+    assert np.array_equal(rec & np.uint64((1 << pw) - 1), idx[order])
+    out2, tmp2 = buf(), buf()
+    shuffled = rec[rng.permutation(n)]
+    D.sort_records(buf(shuffled), width, out2, tmp2)
+    assert np.array_equal(out2.cpu().numpy(), shuffled[np.argsort(shuffled >> np.uint64(pw), kind="stable")])
+    ok, op, tk, tp = buf(), buf(), buf(), buf()
+    D.sort_pairs(kd, pd, 0, (1 << width) - 1, width, ok, op, tk, tp, None)
+    assert np.array_equal(ok.cpu().numpy(), keys[order])
+    assert np.array_equal(op.cpu().numpy(), idx[order])
