@@ -547,8 +547,13 @@ def bench_main(args, metric, configs, make_inputs, Clocks, run_reference_sample)
     # end to end: every rank's shard from pinned host memory through the same call
     e2e = None
     if not getattr(args, "no_e2e", False):
-        rh = Relation(r.keys.cpu().pin_memory(), r.payloads.cpu().pin_memory())
-        sh = Relation(s.keys.cpu().pin_memory(), s.payloads.cpu().pin_memory())
+        def pinned(t):  # device -> pinned host directly (no pageable copy: N ranks share the host RAM)
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t)
+            return h
+
+        rh = Relation(pinned(r.keys), pinned(r.payloads))
+        sh = Relation(pinned(s.keys), pinned(s.payloads))
         k = max(1, min(args.steps, getattr(args, "e2e_steps", 3)))
         run_join_distributed(rh, sh, cfg, backend=be)
         dist.barrier()
