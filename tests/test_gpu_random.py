@@ -41,9 +41,13 @@ def _keys(rng, n, lower, span, kind):
     return (k + np.uint64(lower)).astype(np.uint64)
 
 
+# MPSM_RANDOM_SEED / MPSM_RANDOM_CASES draw a different / larger sweep
+# (tools/random_sweep.sh); the default is the committed 96-case sweep
+import os  # noqa: E402
+
 CASES = []
-_rng = np.random.default_rng(20261019)
-for _i in range(96):
+_rng = np.random.default_rng(int(os.environ.get("MPSM_RANDOM_SEED", "20261019")))
+for _i in range(int(os.environ.get("MPSM_RANDOM_CASES", "96"))):
     CASES.append(dict(
         seed=int(_rng.integers(1 << 30)),
         n_r=int(_rng.choice([0, 1, 4095, 8193, 20_000, 150_001])),
