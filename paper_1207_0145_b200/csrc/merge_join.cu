@@ -516,24 +516,41 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
             // two prior tuples) are equal: then some S tuple matches an
             // equal-key group of several R tuples
             {
+                // K32: also whether a record of the tile carries payload
+                // bits above bit 31 (in its high word: hi & kmask); if none
+                // does, the match phase works on the low words alone
+                uint32_t wide = 0;
+                auto hi_of = [&](uint64_t v) -> uint32_t { return (uint32_t)(v >> 32); };
+                auto rk_w = [&](int i) -> KT {
+                    if (K32) wide |= hi_of(RK[i]);
+                    return rkey(i);
+                };
+                auto wk_w = [&](int j) -> KT {
+                    if (K32) wide |= hi_of(WK[j]);
+                    return wkey(j);
+                };
                 int ri = lo, wj = k0 - lo;
-                KT rkc = ri < nR ? rkey(ri) : 0;
-                KT wkc = wj < nW ? wkey(wj) : 0;
+                KT rkc = ri < nR ? rk_w(ri) : 0;
+                KT wkc = wj < nW ? wk_w(wj) : 0;
                 bool dup = ri < nR && ri - 1 >= -hp && rkey(ri - 1) == rkc;
-                if (tid == 0 && hp == 2) dup = dup || rkey(-2) == rkey(-1);
+                if (tid == 0) {
+                    if (hp == 2) dup = dup || rk_w(-2) == rk_w(-1);
+                    else if (hp == 1) rk_w(-1);
+                }
                 for (int st = k0; st < k1; ++st) {
                     const bool take_r = ri < nR && (wj >= nW || rkc <= wkc);
                     if (!take_r) sm.ub[wj] = (uint16_t)ri;
                     ri += take_r;
                     wj += !take_r;
                     if (take_r && ri < nR) {
-                        const KT nk = rkey(ri);
+                        const KT nk = rk_w(ri);
                         dup = dup || nk == rkc;
                         rkc = nk;
                     }
-                    if (!take_r && wj < nW) wkc = wkey(wj);
+                    if (!take_r && wj < nW) wkc = wk_w(wj);
                 }
-                if (dup) sm.tdup[buf] = 1;
+                const int fl = (dup ? 1 : 0) | ((K32 && (wide & pi.kmask)) ? 2 : 0);
+                if (fl) atomicOr(&sm.tdup[buf], fl);
             }
             __syncthreads();
             MJ_TS(4)
@@ -565,7 +582,29 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                     csum += decltype(SW)::value ? pair_hash(sp, rp) : pair_hash(rp, sp);
                 }
             };
-            if (!sm.tdup[buf]) {
+            // K32 and every payload of the tile below 2^32: keys compare as
+            // the high words outside the payload bits, payloads are the low
+            // words, and rotl64(s, 17) of a 32-bit s is a plain shift
+            auto unique_pass32 = [&](auto SW) {
+                MPSM_UNROLL(MPSM_MJ_P2_UNROLL)
+                for (int j = tid; j < nW; j += MJ_THREADS) {
+                    const int i = (int)sm.ub[j] - 1;
+                    if (i < -hp) continue;
+                    const uint64_t wv = WK[j], rv = RK[i];
+                    if (((uint32_t)(wv >> 32) ^ (uint32_t)(rv >> 32)) & ~pi.kmask) continue;
+                    const uint32_t rp = (uint32_t)rv, sp = (uint32_t)wv;
+                    const uint64_t v = (uint64_t)rp + sp;
+                    best = v > best ? v : best;
+                    ++count;
+                    const uint32_t a = decltype(SW)::value ? sp : rp, b = decltype(SW)::value ? rp : sp;
+                    csum += mix64((uint64_t)a ^ ((uint64_t)b << 17));
+                }
+            };
+            const int tfl = sm.tdup[buf];
+            if (K32 && tfl == 0) {
+                if (swap) unique_pass32(std::true_type{});
+                else unique_pass32(std::false_type{});
+            } else if (!(tfl & 1)) {
                 if (swap) unique_pass(std::true_type{});
                 else unique_pass(std::false_type{});
             } else

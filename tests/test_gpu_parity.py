@@ -436,3 +436,22 @@ def test_sorts_into_unaligned_outputs(off):
     D.sort_pairs(kd, pd, 0, (1 << width) - 1, width, ok, op, tk, tp, None)
     assert np.array_equal(ok.cpu().numpy(), keys[order])
     assert np.array_equal(op.cpu().numpy(), idx[order])
+
+
+@pytest.mark.parametrize("frac_wide", [0.0, 0.001, 1.0])
+def test_payloads_above_32_bits_in_packed_records(frac_wide, pack_mode):
+    """w = 27 leaves 37 payload bits in a packed record: payloads of 33-37
+    bits stay on the packed path; merge tiles holding one switch from the
+    low-word match phase to the full-record one (k_merge's per-tile flag)."""
+    n_r, n_s = 200_000, 800_000
+    r, s, _ = P.gen_fk(n_r, n_s, 3)
+    dom = KeyDomain(1, (1 << 27) + 1)  # w = 27
+    rng = np.random.default_rng(4)
+    for rel in (r, s):
+        n = rel.payloads.shape[0]
+        big = rng.random(n) < frac_wide
+        rel.payloads[big] = rng.integers(1 << 32, 1 << 37, int(big.sum()), dtype=np.uint64)
+    want = orc.fk_gather(r.keys, r.payloads, s.keys, s.payloads, 1)
+    for t in (1, 2):
+        res = P.run_join(r, s, JoinConfig(threads=t, key_domain=dom))
+        assert (res.match_count, res.aggregate_max, res.checksum) == want
