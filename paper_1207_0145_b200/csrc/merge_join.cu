@@ -487,8 +487,9 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
         // normalized keys and payloads; K32: packed keys of a domain at most
         // 32 bits wide compare as their record's high word with the payload
         // bits in it set (same order and equality as the keys; no shift)
+        const uint32_t kmask = pi.kmask;  // in a register, not re-read from the parameter bank per key
         auto nkey = [&](uint64_t v) -> KT {
-            if (K32) return (KT)((uint32_t)(v >> 32) | pi.kmask);
+            if (K32) return (KT)((uint32_t)(v >> 32) | kmask);
             return PK ? (KT)(v >> pi.pw) : (KT)v;
         };
         auto rkey = [&](int i) -> KT { return nkey(RK[i]); };
@@ -537,6 +538,7 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                     if (hp == 2) dup = dup || rk_w(-2) == rk_w(-1);
                     else if (hp == 1) rk_w(-1);
                 }
+                KT dmin = dup ? (KT)0 : (KT)1;  // 0 iff two neighbouring R keys are equal (one min per step)
                 for (int st = k0; st < k1; ++st) {
                     const bool take_r = ri < nR && (wj >= nW || rkc <= wkc);
                     if (!take_r) sm.ub[wj] = (uint16_t)ri;
@@ -544,12 +546,13 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                     wj += !take_r;
                     if (take_r && ri < nR) {
                         const KT nk = rk_w(ri);
-                        dup = dup || nk == rkc;
+                        dmin = min(dmin, (KT)(nk ^ rkc));
                         rkc = nk;
                     }
                     if (!take_r && wj < nW) wkc = wk_w(wj);
                 }
-                const int fl = (dup ? 1 : 0) | ((K32 && (wide & pi.kmask)) ? 2 : 0);
+                dup = dmin == 0;
+                const int fl = (dup ? 1 : 0) | ((K32 && (wide & kmask)) ? 2 : 0);
                 if (fl) atomicOr(&sm.tdup[buf], fl);
             }
             __syncthreads();
