@@ -333,6 +333,7 @@ struct MergeSmem {
     MergeStage<PK> st[2];
     uint16_t ub[MJ_TILE];  // MODE 0: per W tuple of the tile, R tuples <= its key (tile-relative)
     int tdup[2];           // MODE 0, per tile parity: some R key of the tile repeats
+    uint32_t kmask;        // PackInfo::kmask, read back with a volatile load (see k_merge)
     uint64_t bar[2];
     uint64_t red[3][MJ_THREADS / 32];
     int64_t warp_cnt[MJ_THREADS / 32];
@@ -455,6 +456,7 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
         mbar_init(&sm.bar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         sm.tdup[0] = sm.tdup[1] = 0;
+        sm.kmask = pi.kmask;
         fetch_tile<PK>(sm.st[0], &sm.bar[0], splits[g]);
         if (g + G < ntiles) t_nxt = splits[g + G];
     }
@@ -487,7 +489,11 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
         // normalized keys and payloads; K32: packed keys of a domain at most
         // 32 bits wide compare as their record's high word with the payload
         // bits in it set (same order and equality as the keys; no shift)
-        const uint32_t kmask = pi.kmask;  // in a register, not re-read from the parameter bank per key
+        // kept in a register: a value from a volatile shared load cannot be
+        // re-read from the parameter bank (ptxas otherwise trades the
+        // register for an LDC per key)
+        uint32_t kmask;
+        asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(kmask) : "r"(smem_addr(&sm.kmask)));
         auto nkey = [&](uint64_t v) -> KT {
             if (K32) return (KT)((uint32_t)(v >> 32) | kmask);
             return PK ? (KT)(v >> pi.pw) : (KT)v;
