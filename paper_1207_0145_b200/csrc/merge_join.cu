@@ -327,6 +327,7 @@ struct alignas(16) MergeStage {
     uint64_t k[MJ_TILE + 8];
     uint64_t p[PK ? 2 : MJ_TILE + 8];  // payloads (SoA runs only)
     TileSplit t;                       // descriptor of the staged tile
+    int r0, w0, rp0, wp0, hp;          // where R tile element 0 / W element 0 sit in k[] (p[]); prior R tuples
 };
 template <bool PK>
 struct MergeSmem {
@@ -375,6 +376,14 @@ template <bool PK>
 __device__ __forceinline__ void fetch_tile(MergeStage<PK>& st, uint64_t* bar, const TileSplit& t) {
     const TilePlace q = place_of<PK>(t);
     st.t = t;
+    // the placement, computed once here for every thread of the CTA
+    st.hp = q.hp;
+    st.r0 = q.rk.off + q.hp;
+    st.w0 = (int)(q.rk.bytes / 8) + q.wk.off;
+    if (!PK) {
+        st.rp0 = q.rp.off + q.hp;
+        st.wp0 = (int)(q.rp.bytes / 8) + q.wp.off;
+    }
     unsigned tx = q.rk.bytes + q.wk.bytes;
     if (!PK) tx += q.rp.bytes + q.wp.bytes;
     mbar_arrive_expect_tx(bar, tx);
@@ -479,13 +488,12 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
         mbar_wait(&sm.bar[buf], (par >> buf) & 1u);
         par ^= 1u << buf;
         MJ_TS(2)
-        const TilePlace q = place_of<PK>(t);
-        const int nR = t.nR, nW = t.nW, hp = q.hp;
+        const int nR = t.nR, nW = t.nW, hp = sm.st[buf].hp;
         // R tile element i (i >= -hp) and W tile element j in the stage
-        const uint64_t* RK = sm.st[buf].k + q.rk.off + hp;
-        const uint64_t* WK = sm.st[buf].k + q.rk.bytes / 8 + q.wk.off;
-        const uint64_t* RP = PK ? RK : sm.st[buf].p + q.rp.off + hp;
-        const uint64_t* WP = PK ? WK : sm.st[buf].p + q.rp.bytes / 8 + q.wp.off;
+        const uint64_t* RK = sm.st[buf].k + sm.st[buf].r0;
+        const uint64_t* WK = sm.st[buf].k + sm.st[buf].w0;
+        const uint64_t* RP = PK ? RK : sm.st[buf].p + sm.st[buf].rp0;
+        const uint64_t* WP = PK ? WK : sm.st[buf].p + sm.st[buf].wp0;
         // normalized keys and payloads; K32: packed keys of a domain at most
         // 32 bits wide compare as their record's high word with the payload
         // bits in it set (same order and equality as the keys; no shift)
@@ -600,7 +608,7 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                     const int i = (int)sm.ub[j] - 1;
                     if (i < -hp) continue;
                     const uint64_t wv = WK[j], rv = RK[i];
-                    if (((uint32_t)(wv >> 32) ^ (uint32_t)(rv >> 32)) & ~pi.kmask) continue;
+                    if (((uint32_t)(wv >> 32) ^ (uint32_t)(rv >> 32)) & ~pi.kmask) continue;  // a uniform-register operand
                     const uint32_t rp = (uint32_t)rv, sp = (uint32_t)wv;
                     const uint64_t v = (uint64_t)rp + sp;
                     best = v > best ? v : best;
