@@ -602,11 +602,13 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
             // K32 and every payload of the tile below 2^32: keys compare as
             // the high words outside the payload bits, payloads are the low
             // words, and rotl64(s, 17) of a 32-bit s is a plain shift
-            auto unique_pass32 = [&](auto SW) {
+            // CHK: only a pair's first tile (no prior R tuple, hp == 0) can
+            // hold a W tuple with no R tuple <= its key
+            auto unique_pass32 = [&](auto SW, auto CHK) {
                 MPSM_UNROLL(MPSM_MJ_P2_UNROLL)
                 for (int j = tid; j < nW; j += MJ_THREADS) {
                     const int i = (int)sm.ub[j] - 1;
-                    if (i < -hp) continue;
+                    if (decltype(CHK)::value && i < -hp) continue;
                     const uint64_t wv = WK[j], rv = RK[i];
                     if (((uint32_t)(wv >> 32) ^ (uint32_t)(rv >> 32)) & ~pi.kmask) continue;  // a uniform-register operand
                     const uint32_t rp = (uint32_t)rv, sp = (uint32_t)wv;
@@ -619,8 +621,13 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
             };
             const int tfl = sm.tdup[buf];
             if (K32 && tfl == 0) {
-                if (swap) unique_pass32(std::true_type{});
-                else unique_pass32(std::false_type{});
+                if (hp == 0) {
+                    if (swap) unique_pass32(std::true_type{}, std::true_type{});
+                    else unique_pass32(std::false_type{}, std::true_type{});
+                } else {
+                    if (swap) unique_pass32(std::true_type{}, std::false_type{});
+                    else unique_pass32(std::false_type{}, std::false_type{});
+                }
             } else if (!(tfl & 1)) {
                 if (swap) unique_pass(std::true_type{});
                 else unique_pass(std::false_type{});
