@@ -3,19 +3,24 @@
 (|R|+|S|) and achieved HBM GB/s fraction).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config cfg2] [--no-cpu-baseline] [--no-e2e]
+                    [--config cfg2] [--threads T] [--no-cpu-baseline] [--no-e2e]
 
 One step = one complete P-MPSM join through the public API ``run_join``
 (sort S into runs, partition/sort R, merge-join with fused COUNT / MAX /
 checksum, result read back to the host) over the configuration's synthetic
 inputs.  At N=1 the workload is BASELINE.json configs[1] (cfg2: |R|=100M,
-|S|=400M FK join, 8 GB of 16-B tuples), which fits one B200.  Under torchrun
-(N>1) every rank holds a cfg2-sized shard (weak scaling) and the ranks run the
-distributed engine (NCCL all-to-all of R + NVLink peer reads of S runs).
+|S|=400M FK join, 8 GB of 16-B tuples), which fits one B200; ``--config``
+selects any other single-GPU config (cfg1, cfg3m1..m16, cfg4).  Under
+torchrun (N>1) the ranks run the distributed engine (NCCL all-to-all of R +
+NVLink peer reads of S runs) on BASELINE configs[4] (cfg5, strong scaling)
+or configs[3] (cfg4), see distributed.bench_main.
 
 Printed JSON line (rank 0):
   value      whole-job tuples/s, inputs resident in HBM, CUDA-event timed, max
              over ranks
+  result     (count, MAX, checksum) of the join, checked against the committed
+             golden (the reference's own results) or the independent torch
+             checker (tests/torch_check.py) on the same arrays
   e2e        the same through run_join with pinned HOST buffers: H2D of the
              inputs and D2H of the result inside the timed region
   roofline   the radix scatter pass seg::k_scatter[_ws] (the dominant kernel):
@@ -23,16 +28,17 @@ Printed JSON line (rank 0):
              tuple) / its summed CUDA-event launch time inside the timed region
              vs MEASURED_PEAKS.json hbm_gbs; traffic from the committed ncu
              capture (profiles/traffic_scatter.json)
+  phase_roofline / step_roofline  bytes each phase actually moves / its time
   cpu_baseline  the reference package (oracle/_ref, numba, all host threads)
-             on a bounded sample of the same workload
-``--impl reference`` times the reference's own CPU implementation instead.
+             on the SAME arrays (the full workload), median of 3 joins
+``--impl reference`` times the reference's own CPU run_join on the full
+workload instead (one join per step).
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -61,7 +67,6 @@ GOLDEN = {
     "cfg1": (4_000_000, 8_587_739_465, 0x7CDED1377072045D),
     "cfg2": (400_000_000, 8_589_753_492, 0xAA48801BE88FA31B),
 }
-CPU_SAMPLE = (10_000_000, 40_000_000)  # bounded sample of cfg2 for the CPU legs
 
 
 def log(*a):
@@ -166,71 +171,126 @@ def cpu_threads() -> int:
         return os.cpu_count() or 1
 
 
-def run_reference_sample(reps: int = 2):
-    """Time the reference (oracle/_ref, numba) or, if absent, the C oracle
-    port on a bounded sample of cfg2.  Returns (tuples/s, kind, cores, sample, result)."""
-    from paper_1207_0145_b200 import datagen
+class ReferenceCPU:
+    """The reference's own CPU path on the host cores: the unmodified package
+    installed into oracle/_ref (numba, run_join p-mpsm with threads = all host
+    cores, tight KeyDomain), or the C oracle port if it is absent.  Runs on
+    the SAME numpy arrays the GPU arm consumes."""
 
-    n_r, n_s = CPU_SAMPLE
-    r, s, dom = datagen.gen_fk(n_r, n_s, 0)
-    t = cpu_threads()
-    ref_dir = os.path.join(ROOT, "oracle", "_ref")
+    def __init__(self, r, s, dom):
+        self.t = cpu_threads()
+        self.n = r.cardinality + s.cardinality
+        ref_dir = os.path.join(ROOT, "oracle", "_ref")
+        if os.path.isdir(os.path.join(ref_dir, "mpsm")):
+            sys.path.insert(0, ref_dir)
+            import mpsm  # the reference package, unmodified
+
+            self.kind = "reference"
+            mpsm.warmup()
+            rr, ss = mpsm.Relation(r.keys, r.payloads), mpsm.Relation(s.keys, s.payloads)
+            cfg = mpsm.JoinConfig(threads=self.t, algorithm="p-mpsm", key_domain=mpsm.KeyDomain(dom.lower, dom.upper))
+            self._call = lambda: mpsm.run_join(rr, ss, cfg)
+        else:
+            from oracle import oracle as orc
+
+            self.kind = "port"
+            self._call = lambda: orc.join(r.keys, r.payloads, s.keys, s.payloads, threads=self.t, lower=dom.lower,
+                                          upper=dom.upper, parallel=True)
+
+    def step(self):
+        """one wall-clock-timed join -> (seconds, (count, max))"""
+        t0 = time.perf_counter()
+        out = self._call()
+        return time.perf_counter() - t0, (out.match_count, out.aggregate_max)
+
+    def describe(self, what: str) -> dict:
+        return {"kind": self.kind, "cores": self.t,
+                "sample": f"the full workload (the GPU arm's arrays): p-mpsm run_join, threads={self.t}, {what}"}
+
+
+def cpu_baseline(r, s, dom, reps: int = 3) -> dict:
+    ref = ReferenceCPU(r, s, dom)
+    ref.step()  # JIT cache / page-in
     times, res = [], None
-    if os.path.isdir(os.path.join(ref_dir, "mpsm")):
-        sys.path.insert(0, ref_dir)
-        import mpsm  # the reference package, unmodified
-
-        kind = "reference"
-        mpsm.warmup()
-        rr, ss = mpsm.Relation(r.keys, r.payloads), mpsm.Relation(s.keys, s.payloads)
-        cfg = mpsm.JoinConfig(threads=t, algorithm="p-mpsm", key_domain=mpsm.KeyDomain(dom.lower, dom.upper))
-        mpsm.run_join(rr, ss, cfg)  # first run: JIT cache / page-in
-        for _ in range(reps):
-            t0 = time.perf_counter()
-            out = mpsm.run_join(rr, ss, cfg)
-            times.append(time.perf_counter() - t0)
-        res = (out.match_count, out.aggregate_max, None)
-    else:
-        from oracle import oracle as orc
-
-        kind = "port"
-        for _ in range(reps):
-            t0 = time.perf_counter()
-            out = orc.join(r.keys, r.payloads, s.keys, s.payloads, threads=t, lower=dom.lower, upper=dom.upper,
-                           parallel=True)
-            times.append(time.perf_counter() - t0)
-        res = (out.match_count, out.aggregate_max, out.checksum)
+    for _ in range(reps):
+        dt, res = ref.step()
+        times.append(dt)
     med = statistics.median(times)
-    sample = (f"|R|={n_r:,} |S|={n_s:,} FK (cfg2 generator at 1/10 scale), p-mpsm T={t}, "
-              f"median of {reps} wall-clock runs of run_join after warm-up")
-    return (n_r + n_s) / med, kind, t, sample, res
+    d = ref.describe(f"median of {reps} wall-clock runs after one warm-up run")
+    d.update({"value": ref.n / med, "unit": "tuples/s", "ms_per_step": 1e3 * med,
+              "result": {"match_count": res[0], "aggregate_max": res[1]}})
+    return d
+
+
+def config_of(name: str, dom) -> dict:
+    """the workload description shared by both arms (same arrays, same join)"""
+    n_r, n_s, kind = CONFIGS[name]
+    what = "FK equi-join" if kind == "fk" else "negatively correlated 80-20 skew join, 32-bit keys"
+    return {"workload": f"{name}: |R|={n_r:,} |S|={n_s:,} {what}, 16-B (u64,u64) tuples",
+            "algorithm": "p-mpsm", "key_domain": [dom.lower, dom.upper],
+            "generator": "numpy PCG64 seed 0 (datagen.gen_fk / gen_negcorr)",
+            "l2": f"inputs {16 * (n_r + n_s) / 1e9:.1f} GB >> 126 MB L2 (no flush needed)"}
 
 
 def impl_reference(args):
+    """--impl reference: the reference's CPU run_join on the full workload,
+    one join per step, on rank 0 (other ranks exit without work)."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    steps = []
-    val = kind = cores = sample = None
-    for i in range(args.warmup + args.steps):
-        v, kind, cores, sample, _ = run_reference_sample(reps=1)
-        if i >= args.warmup:
-            steps.append(v)
-    val = statistics.median(steps)
-    n = CPU_SAMPLE[0] + CPU_SAMPLE[1]
+    t_gen = time.perf_counter()
+    r, s, dom = make_inputs(args.config)
+    log(f"[bench-ref] generated {args.config} in {time.perf_counter() - t_gen:.1f}s")
+    ref = ReferenceCPU(r, s, dom)
+    res = None
+    for _ in range(args.warmup):
+        _, res = ref.step()
+    times = []
+    for _ in range(args.steps):
+        dt, res = ref.step()
+        times.append(dt)
+    total = sum(times)
+    val = args.steps * ref.n / total
+    golden = GOLDEN.get(args.config)
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "tuples/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * n / val, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic (FK generator, PCG64 seed 0)",
-        "config": {"workload": "cfg2 sample: |R|=10M, |S|=40M FK join (CPU-bounded sample of configs[1])",
-                   "algorithm": "p-mpsm", "threads": cores},
-        "cpu_baseline": {"value": val, "unit": "tuples/s", "cores": cores, "kind": kind, "sample": sample},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic (numpy PCG64 seed 0)",
+        "config": config_of(args.config, dom),
+        "engine": {"impl": f"reference run_join ({ref.kind}, CPU)", "threads": ref.t},
+        "result": {"match_count": res[0], "aggregate_max": res[1],
+                   "matches_golden": None if golden is None else tuple(res) == golden[:2]},
+        "cpu_baseline": dict(ref.describe(f"{args.steps} timed joins after {args.warmup} warm-up joins"),
+                             value=val, unit="tuples/s"),
         "e2e": {"value": val, "unit": "tuples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------- ours
+def expected_result(name: str, rd, sd):
+    """(count, max, checksum) the join must produce, and where it comes from:
+    the committed golden (the reference's own count/max) when there is one,
+    else the independent torch checker (tests/torch_check.py) on the same
+    device arrays -- never this package's kernels."""
+    import torch
+
+    golden = GOLDEN.get(name)
+    if golden is not None:
+        return golden, "golden: the reference's run_join count/max, checksum of its materialized pairs"
+    from tests import torch_check as tc
+
+    torch.cuda.empty_cache()
+    if CONFIGS[name][2] == "fk":
+        want = tc.fk_join(rd, sd)
+        how = "independent torch FK gather (tests/torch_check.py)"
+    else:
+        want = tc.general_join(rd, sd)
+        how = "independent torch sort + searchsorted join (tests/torch_check.py)"
+    torch.cuda.empty_cache()
+    return want, how
+
+
 def impl_ours(args):
     import torch
 
@@ -240,7 +300,7 @@ def impl_ours(args):
     if ws > 1 or (os.environ.get("MPSM_BENCH_DIST") == "1" and "LOCAL_RANK" in os.environ):
         from paper_1207_0145_b200 import distributed
 
-        return distributed.bench_main(args, METRIC, CONFIGS, make_inputs, Clocks, run_reference_sample)
+        return distributed.bench_main(args, METRIC, Clocks)
 
     import paper_1207_0145_b200 as P
     from paper_1207_0145_b200 import _lib
@@ -257,18 +317,18 @@ def impl_ours(args):
     # resident device inputs
     rd = Relation(torch.from_numpy(r.keys).to(dev), torch.from_numpy(r.payloads).to(dev))
     sd = Relation(torch.from_numpy(s.keys).to(dev), torch.from_numpy(s.payloads).to(dev))
-    cfg = JoinConfig(threads=1, algorithm="p-mpsm", key_domain=dom)
+    cfg = JoinConfig(threads=args.threads, algorithm="p-mpsm", key_domain=dom)
 
     clocks = Clocks(local)
     clocks.start()  # sampling runs from before the warm-up; samples are kept for the timed region only
     for _ in range(args.warmup):
         res = P.run_join(rd, sd, cfg)
     torch.cuda.synchronize()
-    golden = GOLDEN.get(args.config)
     result = (res.match_count, res.aggregate_max, res.checksum)
-    parity = None if golden is None else (result == golden)
-    if golden is not None and not parity:
-        log(f"[bench] PARITY FAILURE {result} != {golden}")
+    want, how = expected_result(args.config, rd, sd)
+    parity = result == tuple(want)
+    if not parity:
+        log(f"[bench] PARITY FAILURE {result} != {want} ({how})")
 
     _lib.profile_enable(True)
     l0 = _lib.launch_count()
@@ -287,10 +347,12 @@ def impl_ours(args):
     clocks.mark(w0, time.time())
     launches = _lib.launch_count() - l0
     ms = ev0.elapsed_time(ev1) / args.steps
-    prof = {k: _lib.profile_read(k) for k in ("seg_scatter", "seg_count", "merge", "merge_partition")}
+    prof = {k: _lib.profile_read(k) for k in ("seg_scatter", "seg_count", "merge", "merge_partition",
+                                              "radix_histogram")}
     _lib.profile_enable(False)
     clk = clocks.stop()
     value = n_tot / (ms / 1e3)
+    timed_ok = (res.match_count, res.aggregate_max, res.checksum) == result
 
     # roofline of the dominant kernel, the radix scatter pass (seg::k_scatter):
     # algorithmic bytes per tuple = its reads + writes in the layout it runs:
@@ -311,27 +373,30 @@ def impl_ours(args):
     except OSError:
         pass
     peak = peaks.get("hbm_gbs", 6650.0)
-    # whole-join canonical bytes for context
-    canonical = (n_s * (8 + 32 * math.ceil(wbits / 8)) + n_r * (8 + 32 * math.ceil(wbits / 8))
-                 + 16 * (n_r + n_s))
-    step_gbs = canonical / (ms / 1e3) / 1e9
 
     # per-phase HBM roofline (the north star asks >= 60 % on the sort and
-    # merge-join phases): bytes the phase moves in this layout (count passes
-    # 8 B/tuple + scatter passes, merge reads every run once) and SURVEY
-    # 8(d)'s canonical bytes, over the phase's CUDA-event time
+    # merge-join phases) on the bytes each phase actually moves in this
+    # layout: count sweeps 8 B/tuple per pass + the scatter passes; the merge
+    # reads every run once (8 B packed records, 16 B pairs); cross-checked
+    # with ncu dram__bytes where a capture is committed (profiles/)
     n_pub, n_priv = max(n_r, n_s), min(n_r, n_s)
-    sort_b = (8 * passes + per_tuple) if packed else (8 * passes + 32 * passes)
-    canon_sort = 8 + 32 * math.ceil(wbits / 8)
+    sort_b = 8 * passes + per_tuple
     rec_b = 8 if packed else 16
     phase_roof = {}
-    for name, nb, cb in (("sort_public", n_pub * sort_b, n_pub * canon_sort),
-                         ("sort_private", n_priv * sort_b, n_priv * canon_sort),
-                         ("join", (n_r + n_s) * rec_b, 16 * (n_r + n_s))):
+    for name, nb in (("sort_public", n_pub * sort_b), ("sort_private", n_priv * sort_b),
+                     ("join", (n_r + n_s) * rec_b)):
         t = phase[name] / args.steps
         if t > 0:
-            phase_roof[name] = {"gbs": nb / t / 1e9, "frac": nb / t / 1e9 / peak,
-                                "canonical_gbs": cb / t / 1e9, "canonical_frac": cb / t / 1e9 / peak}
+            phase_roof[name] = {"bytes": nb, "ms": 1e3 * t, "gbs": nb / t / 1e9, "frac": nb / t / 1e9 / peak}
+    moved = sum(v["bytes"] for v in phase_roof.values())
+    step_roof = {"bytes": moved, "gbs": moved / (ms / 1e3) / 1e9, "frac": moved / (ms / 1e3) / 1e9 / peak,
+                 "floor_ms": 1e3 * moved / (peak * 1e9)}
+    mfile = os.path.join(ROOT, "profiles", "traffic_merge.json")
+    if "join" in phase_roof and packed and args.config == "cfg2" and os.path.exists(mfile):
+        with open(mfile) as f:
+            tj = json.load(f)
+        phase_roof["join"]["ncu_dram_bytes"] = tj.get("dram_bytes_per_launch")
+        phase_roof["join"]["ncu_source"] = "profiles/traffic_merge.json"
 
     e2e = None
     if not args.no_e2e:
@@ -358,11 +423,12 @@ def impl_ours(args):
                "input_path": "host-packed records (csrc/upload.cu)" if up else "column copies"}
         del rh, sh
 
+    del rd, sd
+    torch.cuda.empty_cache()
     cpu = None
     if not args.no_cpu_baseline:
         try:
-            v, kind, cores, sample, cres = run_reference_sample(reps=2)
-            cpu = {"value": v, "unit": "tuples/s", "cores": cores, "kind": kind, "sample": sample}
+            cpu = cpu_baseline(r, s, dom, reps=args.cpu_reps)
         except Exception as exc:
             cpu = {"value": None, "unit": "tuples/s", "cores": cpu_threads(), "kind": "reference",
                    "sample": f"failed: {exc!r}"}
@@ -382,16 +448,13 @@ def impl_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": "tuples/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u64", "data": "synthetic (FK generator SURVEY 8(d), PCG64 seed 0)",
-        "config": {"workload": f"{args.config}: |R|={n_r:,} |S|={n_s:,} "
-                               + ("FK equi-join" if CONFIGS[args.config][2] == "fk"
-                                  else "negatively correlated 80-20 skew join, 32-bit keys")
-                               + ", 16-B (u64,u64) tuples",
-                   "algorithm": "p-mpsm", "threads": 1, "key_domain": [dom.lower, dom.upper],
-                   "l2": f"inputs {16 * (n_r + n_s) / 1e9:.1f} GB >> 126 MB L2 (no flush needed)",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic (numpy PCG64 seed 0, SURVEY 8(d) generators)",
+        "config": config_of(args.config, dom),
+        "engine": {"impl": "paper_1207_0145_b200 run_join (libmpsm_b200.so, sm_100a)", "threads": args.threads,
                    "parallelism": "single GPU"},
         "result": {"match_count": result[0], "aggregate_max": result[1], "checksum": hex(result[2]),
-                   "matches_golden": parity},
+                   "expected": [want[0], want[1], hex(want[2])], "verified_by": how, "matches": parity,
+                   "timed_steps_match": timed_ok},
         "phase_ms": {k: 1e3 * v / args.steps for k, v in phase.items()},
         "roofline": {"bound": "hbm", "kernel": "seg::k_scatter (radix scatter pass)", "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
@@ -399,8 +462,8 @@ def impl_ours(args):
                      "algorithmic_bytes_per_tuple_per_sort": per_tuple,
                      "layout": "packed 8-B records" if packed else "(key, payload) pairs", "passes_per_sort": passes,
                      "launches": os_n, "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
-        "step_canonical_gbs": step_gbs,
         "phase_roofline": phase_roof,
+        "step_roofline": step_roof,
         "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
         "gpu_launches": launches,
         "clocks": clk,
@@ -417,7 +480,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--threads", type=int, default=1, help="logical workers T (JoinConfig.threads)")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()

@@ -51,8 +51,13 @@ extern "C" {
 #define MPSM_PAIR_PROBES 4   /* interpolation-search positions read            */
 #define MPSM_PAIR_END 5      /* upper bound of the private run's last key      */
 #define MPSM_PAIR_EXAMINED 6 /* distinct public positions the merge scan reads */
-#define MPSM_PAIR_EMITTED 7  /* pairs written (materialize)                    */
-#define MPSM_PAIR_FIELDS 8
+#define MPSM_PAIR_EMITTED 7  /* pairs written (materialize, at most the cap)   */
+#define MPSM_PAIR_FLAGS 8    /* MPSM_FLAG_* bits found by the merge            */
+#define MPSM_PAIR_FIELDS 9
+
+/* MPSM_PAIR_FLAGS bits */
+#define MPSM_FLAG_UNSORTED 1 /* a run the merge walked is not sorted ascending
+                                (the reference's Run invariant, core.py:153-154) */
 
 /* a sorted run or a relation chunk in device memory */
 typedef struct {
@@ -115,6 +120,18 @@ int mpsm_sort_packed(const uint64_t* in_keys, const uint64_t* in_pays, int64_t n
 int mpsm_radix_histogram(const uint64_t* keys, int64_t n, uint64_t lower, uint64_t span_m1, int shift,
                          int nbuckets, int64_t* d_counts, unsigned long long* d_bad, void* stream);
 
+/* ------------------------------------------------- boundary checks ----
+ * Replaces core.validate_relation (core.py:248-260) as used by
+ * engine._prepare (engine.py:181-190) to word its DomainError: d_report
+ * (2 words, initialised by the call) receives [0] the number of keys outside
+ * [lower, lower + span_m1] and [1] the index of the first one (UINT64_MAX if
+ * none).  Only called once a sort or histogram pass has flagged a bad key. */
+int mpsm_domain_report(const uint64_t* keys, int64_t n, uint64_t lower, uint64_t span_m1,
+                       unsigned long long* d_report, void* stream);
+/* Replaces the order check of core.Run (core.py:153-154) for device runs:
+ * *d_flag |= 1 if some keys[i] > keys[i + 1]. */
+int mpsm_check_sorted(const uint64_t* keys, int64_t n, unsigned int* d_flag, void* stream);
+
 /* --------------------------------------------------- partition scatter ----
  * Replaces _kernels.scatter_chunk (_kernels.py:262-284) / partition.scatter
  * (partition.py:233-276): each tuple goes to partition d_sp[(key-lower)>>shift]
@@ -161,8 +178,16 @@ int mpsm_interp_lower_bound(const uint64_t* keys, int64_t n, const uint64_t* d_t
  * 69-78, 217-218), so pairs are oriented (public, private) for the checksum
  * and materialized output.
  * mode MPSM_MODE_MATERIALIZE additionally writes matched pairs as
- * (r_pay, s_pay) rows into d_out (uint64[2*cap], row-major); call once with
- * d_out == NULL to obtain counts, then again with an output buffer.  */
+ * (r_pay, s_pay) rows into d_out (uint64[2*cap], row-major); storage stops
+ * at cap rows (pairs beyond it are counted, not written: the reference's
+ * merge_join_run, _kernels.py:382-390) and each pair record's
+ * MPSM_PAIR_EMITTED says how many of its pairs landed.  Call once with
+ * d_out == NULL to obtain counts, then again with an output buffer.
+ * Every adjacent pair of keys the merge walks (the whole private run and
+ * the public window) is checked for order; a violation sets
+ * MPSM_FLAG_UNSORTED in the pair's MPSM_PAIR_FLAGS (the caller raises
+ * InternalConsistencyError; the reference's Run rejects unsorted runs,
+ * core.py:153-154).  */
 int mpsm_join_workspace_bytes(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub,
                               size_t* bytes);
 int mpsm_join_pairs(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub, int swap, int mode,

@@ -19,15 +19,16 @@ LIB_PATH = os.environ.get("MPSM_LIB") or os.path.join(_HERE, "libmpsm_b200.so")
 MPSM_OK = 0
 ERR_DOMAIN, ERR_INTERNAL, ERR_CONFIG, ERR_CUDA, ERR_CAP, ERR_ARG, ERR_FORMAT, ERR_IO = -1, -2, -3, -4, -5, -6, -7, -8
 MODE_AGGREGATE_MAX, MODE_COUNT, MODE_MATERIALIZE = 0, 1, 2
-PAIR_COUNT, PAIR_BEST, PAIR_CHECKSUM, PAIR_START, PAIR_PROBES, PAIR_END, PAIR_EXAMINED, PAIR_EMITTED = range(8)
-PAIR_FIELDS = 8
+PAIR_COUNT, PAIR_BEST, PAIR_CHECKSUM, PAIR_START, PAIR_PROBES, PAIR_END, PAIR_EXAMINED, PAIR_EMITTED, PAIR_FLAGS = range(9)
+PAIR_FIELDS = 9
+FLAG_UNSORTED = 1
 
 # every symbol include/mpsm_b200.h declares (checked by tests/test_boundary.py)
 EXPORTS = (
     "mpsm_version", "mpsm_last_error", "mpsm_device_init", "mpsm_launch_count",
     "mpsm_profile_enable", "mpsm_profile_read",
     "mpsm_sort_workspace_bytes", "mpsm_sort_pass_count", "mpsm_sort_pairs", "mpsm_sort_packed",
-    "mpsm_radix_histogram",
+    "mpsm_radix_histogram", "mpsm_domain_report", "mpsm_check_sorted",
     "mpsm_scatter_workspace_bytes", "mpsm_scatter_chunk",
     "mpsm_interp_lower_bound",
     "mpsm_join_workspace_bytes", "mpsm_join_pairs", "mpsm_join_pairs_packed",
@@ -57,6 +58,8 @@ _SIGS = {
     "mpsm_sort_pairs": (_int, [_vp, _vp, _i64, _u64, _u64, _int, _vp, _vp, _vp, _vp, _vp, _sz, _vp, _vp]),
     "mpsm_sort_packed": (_int, [_vp, _vp, _i64, _u64, _u64, _int, _vp, _vp, _vp, _sz, _vp, _vp, _vp]),
     "mpsm_radix_histogram": (_int, [_vp, _i64, _u64, _u64, _int, _int, _vp, _vp, _vp]),
+    "mpsm_domain_report": (_int, [_vp, _i64, _u64, _u64, _vp, _vp]),
+    "mpsm_check_sorted": (_int, [_vp, _i64, _vp, _vp]),
     "mpsm_scatter_workspace_bytes": (_int, [_i64, _int, ctypes.POINTER(_sz)]),
     "mpsm_scatter_chunk": (_int, [_vp, _vp, _i64, _u64, _int, _vp, _int, _int, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "mpsm_interp_lower_bound": (_int, [_vp, _i64, _vp, _i64, _vp, _vp, _vp]),

@@ -1,11 +1,17 @@
-// histogram.cu -- private-input radix histogram with fused domain check.
+// histogram.cu -- private-input radix histogram with fused domain check, and
+// the small validation kernels of the boundary (domain report, run order).
 //
 // Replaces _kernels.radix_histogram (/root/reference/pkg/src/mpsm/_kernels.py
 // 247-259) behind partition.build_radix_histogram (partition.py:110-122):
 // counts[(key - lower) >> shift] += 1 over 2^B buckets.  One read of 8 B per
-// key.  Out-of-domain keys are reported through *d_bad and counted in the
-// clamped bucket (the same clamp the partition scatter applies), so a scatter
-// built on these counts never leaves its regions even for bad input.
+// key, 16-B vector loads; the counts go to shared-memory histograms, one
+// copy per warp pair (fewer collisions between warps), and lanes of a warp
+// that hit the same bucket add once (match.any aggregation: duplicate-heavy
+// keys cost one shared atomic per distinct bucket per warp instruction, not
+// 32 serialised ones).  Out-of-domain keys are reported through *d_bad and
+// counted in the clamped bucket (the same clamp the partition scatter
+// applies), so a scatter built on these counts never leaves its regions even
+// for bad input.
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -16,26 +22,62 @@
 
 namespace mpsm {
 
-constexpr int HIST_SMEM_MAX_BUCKETS = 1 << 14;
+constexpr int HIST_THREADS = 512;
+constexpr int HIST_COPIES = 4;  // shared histogram copies per CTA
+constexpr int HIST_SMEM_MAX_BUCKETS = 1 << 12;  // 4 copies x 4096 x 4 B = 64 KB
 
-__global__ void __launch_bounds__(512) k_radix_hist_smem(const uint64_t* __restrict__ keys, int64_t n, uint64_t lower,
-                                                         uint64_t span_m1, int shift, int nbuckets,
-                                                         unsigned long long* __restrict__ counts,
-                                                         unsigned long long* __restrict__ d_bad) {
+__device__ __forceinline__ void hist_add(uint32_t* h, uint64_t key, int64_t i, uint64_t lower, uint64_t span_m1,
+                                         int shift, int nbuckets, unsigned long long* d_bad, bool valid) {
+    const uint64_t nk = key - lower;
+    if (valid && nk > span_m1 && d_bad) atomicMin(d_bad, (unsigned long long)i);
+    uint64_t b64 = nk >> shift;
+    const uint32_t b = b64 >= (uint64_t)nbuckets ? (uint32_t)(nbuckets - 1) : (uint32_t)b64;
+    const unsigned act = __ballot_sync(0xffffffffu, valid);
+    if (!valid) return;
+    const unsigned peers = __match_any_sync(act, b);
+    if ((__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&h[b], (uint32_t)__popc(peers));
+}
+
+__global__ void __launch_bounds__(HIST_THREADS) k_radix_hist_smem(const uint64_t* __restrict__ keys, int64_t n,
+                                                                  uint64_t lower, uint64_t span_m1, int shift,
+                                                                  int nbuckets, unsigned long long* __restrict__ counts,
+                                                                  unsigned long long* __restrict__ d_bad) {
     extern __shared__ uint32_t sh[];
-    for (int i = threadIdx.x; i < nbuckets; i += blockDim.x) sh[i] = 0;
+    for (int i = threadIdx.x; i < HIST_COPIES * nbuckets; i += blockDim.x) sh[i] = 0;
     __syncthreads();
+    uint32_t* h = sh + ((threadIdx.x >> 5) % HIST_COPIES) * nbuckets;
+    // element pairs with 16-B loads from the first 16-B aligned element on
+    const int64_t head = (((uintptr_t)keys & 15) != 0) ? 1 : 0;
+    const int64_t npairs = (n - head) / 2;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        uint64_t nk = ld_stream(keys + i) - lower;
-        if (nk > span_m1 && d_bad) atomicMin(d_bad, (unsigned long long)i);
-        uint64_t b = nk >> shift;
-        if (b >= (uint64_t)nbuckets) b = nbuckets - 1;
-        atomicAdd(&sh[b], 1u);
+    const int64_t tid0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // the loop bound is warp-uniform so every lane reaches the warp collectives
+    const int64_t iters = (npairs + stride - 1) / stride;
+    for (int64_t it = 0; it < iters; ++it) {
+        const int64_t q = tid0 + it * stride;
+        const bool valid = q < npairs;
+        ulonglong2 v = make_ulonglong2(lower, lower);
+        if (valid) v = __ldcs(reinterpret_cast<const ulonglong2*>(keys + head) + q);
+        hist_add(h, v.x, head + 2 * q, lower, span_m1, shift, nbuckets, d_bad, valid);
+        hist_add(h, v.y, head + 2 * q + 1, lower, span_m1, shift, nbuckets, d_bad, valid);
+    }
+    // the unpaired head / tail element
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+        const int64_t tail = head + 2 * npairs;
+        const int lane = threadIdx.x;
+        const bool vh = lane == 0 && head == 1 && n > 0;
+        const bool vt = lane == 1 && tail < n;
+        const int64_t i = vh ? 0 : tail;
+        const bool valid = vh || vt;
+        hist_add(h, valid ? keys[i] : lower, i, lower, span_m1, shift, nbuckets, d_bad, valid);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < nbuckets; i += blockDim.x)
-        if (sh[i]) atomicAdd(&counts[i], (unsigned long long)sh[i]);
+    for (int i = threadIdx.x; i < nbuckets; i += blockDim.x) {
+        uint32_t c = 0;
+#pragma unroll
+        for (int k = 0; k < HIST_COPIES; ++k) c += sh[k * nbuckets + i];
+        if (c) atomicAdd(&counts[i], (unsigned long long)c);
+    }
 }
 
 __global__ void __launch_bounds__(512) k_radix_hist_global(const uint64_t* __restrict__ keys, int64_t n, uint64_t lower,
@@ -52,6 +94,38 @@ __global__ void __launch_bounds__(512) k_radix_hist_global(const uint64_t* __res
     }
 }
 
+// keys outside [lower, lower + span_m1]: report[0] += count, report[1] =
+// min index (the reference's ValidationReport, core.py:248-260)
+__global__ void __launch_bounds__(512) k_domain_report(const uint64_t* __restrict__ keys, int64_t n, uint64_t lower,
+                                                       uint64_t span_m1, unsigned long long* __restrict__ report) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    unsigned long long cnt = 0, first = ~0ull;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        if (ld_stream(keys + i) - lower > span_m1) {
+            ++cnt;
+            first = min(first, (unsigned long long)i);
+        }
+    }
+    cnt = warp_sum(cnt);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+    if ((threadIdx.x & 31) == 0 && cnt) {
+        atomicAdd(&report[0], cnt);
+        atomicMin(&report[1], first);
+    }
+}
+
+// *flag |= 1 if some keys[i] > keys[i + 1] (the reference's Run check,
+// core.py:153-154)
+__global__ void __launch_bounds__(512) k_check_sorted(const uint64_t* __restrict__ keys, int64_t n,
+                                                      unsigned int* __restrict__ flag) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    bool bad = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i + 1 < n; i += stride)
+        bad |= ld_stream(keys + i) > ld_stream(keys + i + 1);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
 }  // namespace mpsm
 
 using namespace mpsm;
@@ -61,19 +135,45 @@ extern "C" int mpsm_radix_histogram(const uint64_t* keys, int64_t n, uint64_t lo
     cudaStream_t st = (cudaStream_t)stream;
     if (n < 0 || nbuckets < 1 || shift < 0 || shift > 63) return MPSM_ERR_ARG;
     if (n == 0) return MPSM_OK;
-    int grid = (int)std::min<int64_t>(num_sms() * 4, (n + 511) / 512);
     ProfScope ps("radix_histogram", st);
     if (nbuckets <= HIST_SMEM_MAX_BUCKETS) {
-        size_t smem = sizeof(uint32_t) * nbuckets;
-        if (smem > 48 * 1024)
+        const size_t smem = sizeof(uint32_t) * HIST_COPIES * nbuckets;
+        static bool attr = false;
+        if (!attr) {
             MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_radix_hist_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                      (int)smem),
+                                                      (int)(sizeof(uint32_t) * HIST_COPIES * HIST_SMEM_MAX_BUCKETS)),
                                  "smem attr"));
-        k_radix_hist_smem<<<grid, 512, smem, st>>>(keys, n, lower, span_m1, shift, nbuckets,
-                                                   (unsigned long long*)d_counts, d_bad);
+            attr = true;
+        }
+        // one wave of resident CTAs (HBM-bound streaming read)
+        const int grid = (int)std::min<int64_t>((int64_t)num_sms() * 2, std::max<int64_t>(1, (n / 2 + 511) / 512));
+        k_radix_hist_smem<<<grid, HIST_THREADS, smem, st>>>(keys, n, lower, span_m1, shift, nbuckets,
+                                                            (unsigned long long*)d_counts, d_bad);
     } else {
+        const int grid = (int)std::min<int64_t>(num_sms() * 4, (n + 511) / 512);
         k_radix_hist_global<<<grid, 512, 0, st>>>(keys, n, lower, span_m1, shift, nbuckets,
                                                   (unsigned long long*)d_counts, d_bad);
     }
     return check_launch("k_radix_hist");
+}
+
+extern "C" int mpsm_domain_report(const uint64_t* keys, int64_t n, uint64_t lower, uint64_t span_m1,
+                                  unsigned long long* d_report, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n < 0 || !d_report) return MPSM_ERR_ARG;
+    const unsigned long long init[2] = {0ull, ~0ull};
+    MPSM_TRY(cuda_status(cudaMemcpyAsync(d_report, init, sizeof(init), cudaMemcpyHostToDevice, st), "h2d"));
+    if (n == 0) return MPSM_OK;
+    const int grid = (int)std::min<int64_t>(num_sms() * 4, (n + 511) / 512);
+    k_domain_report<<<grid, 512, 0, st>>>(keys, n, lower, span_m1, d_report);
+    return check_launch("k_domain_report");
+}
+
+extern "C" int mpsm_check_sorted(const uint64_t* keys, int64_t n, unsigned int* d_flag, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n < 0 || !d_flag) return MPSM_ERR_ARG;
+    if (n < 2) return MPSM_OK;
+    const int grid = (int)std::min<int64_t>(num_sms() * 4, (n + 511) / 512);
+    k_check_sorted<<<grid, 512, 0, st>>>(keys, n, d_flag);
+    return check_launch("k_check_sorted");
 }

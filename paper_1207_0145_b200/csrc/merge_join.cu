@@ -189,6 +189,7 @@ __global__ void k_windows(const mpsm_run_t* __restrict__ priv, int n_priv, const
     o[MPSM_PAIR_END] = (uint64_t)w.end;
     o[MPSM_PAIR_EXAMINED] = (uint64_t)examined;
     o[MPSM_PAIR_EMITTED] = 0;
+    o[MPSM_PAIR_FLAGS] = 0;
 }
 
 __global__ void __launch_bounds__(1024) k_tile_scan(PairWin* __restrict__ win, int npairs, int64_t* __restrict__ total) {
@@ -447,7 +448,8 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                                                                  const int64_t* __restrict__ total, int swap,
                                                                  uint64_t* __restrict__ out_pairs,
                                                                  int64_t* __restrict__ tile_cnt,
-                                                                 uint64_t* __restrict__ emit_out, PackInfo pi) {
+                                                                 uint64_t* __restrict__ emit_out, int64_t cap,
+                                                                 PackInfo pi) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     MergeSmem<PK>& sm = *reinterpret_cast<MergeSmem<PK>*>(smem_raw);
     const int tid = threadIdx.x;
@@ -485,6 +487,10 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
             count = best = csum = 0;
         }
         MJ_TS(1)
+        // MODE 0, thread 0: the public element before the tile, for the
+        // sortedness check of the tile boundary
+        uint64_t w_prev = 0;
+        if (MODE == 0 && tid == 0 && t.w0 > 0) w_prev = __ldg(t.wk + t.w0 - 1);
         mbar_wait(&sm.bar[buf], (par >> buf) & 1u);
         par ^= 1u << buf;
         MJ_TS(2)
@@ -547,10 +553,27 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                 int ri = lo, wj = k0 - lo;
                 KT rkc = ri < nR ? rk_w(ri) : 0;
                 KT wkc = wj < nW ? wk_w(wj) : 0;
-                bool dup = ri < nR && ri - 1 >= -hp && rkey(ri - 1) == rkc;
+                // the reference's Run invariant (core.py:153-154), checked on
+                // every adjacent pair the walk advances over: a run out of
+                // order (e.g. an unstable radix pass) flags the pair record
+                bool unsorted = false;
+                bool dup = false;
+                if (ri < nR && ri - 1 >= -hp) {
+                    const KT pk = rkey(ri - 1);
+                    dup = pk == rkc;
+                    unsorted = pk > rkc;
+                }
                 if (tid == 0) {
-                    if (hp == 2) dup = dup || rk_w(-2) == rk_w(-1);
-                    else if (hp == 1) rk_w(-1);
+                    if (hp == 2) {
+                        const KT a = rk_w(-2), b = rk_w(-1);
+                        dup = dup || a == b;
+                        unsorted = unsorted || a > b;
+                    } else if (hp == 1) {
+                        rk_w(-1);
+                    }
+                    // the W element before the tile (global memory, loaded
+                    // before the stage wait)
+                    if (t.w0 > 0 && nW > 0) unsorted = unsorted || nkey(w_prev) > wkey(0);
                 }
                 KT dmin = dup ? (KT)0 : (KT)1;  // 0 iff two neighbouring R keys are equal (one min per step)
                 for (int st = k0; st < k1; ++st) {
@@ -561,13 +584,21 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                     if (take_r && ri < nR) {
                         const KT nk = rk_w(ri);
                         dmin = min(dmin, (KT)(nk ^ rkc));
+                        unsorted = unsorted || nk < rkc;
                         rkc = nk;
                     }
-                    if (!take_r && wj < nW) wkc = wk_w(wj);
+                    if (!take_r && wj < nW) {
+                        const KT nw = wk_w(wj);
+                        unsorted = unsorted || nw < wkc;
+                        wkc = nw;
+                    }
                 }
                 dup = dmin == 0;
                 const int fl = (dup ? 1 : 0) | ((K32 && (wide & kmask)) ? 2 : 0);
                 if (fl) atomicOr(&sm.tdup[buf], fl);
+                if (__any_sync(0xffffffffu, unsorted) && (tid & 31) == 0)
+                    atomicOr((unsigned long long*)(out_pairs + (size_t)t.pair * MPSM_PAIR_FIELDS + MPSM_PAIR_FLAGS),
+                             (unsigned long long)MPSM_FLAG_UNSORTED);
             }
             __syncthreads();
             MJ_TS(4)
@@ -691,9 +722,13 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                 } else if (MODE == 1 || pass == 0) {
                     ++e;
                 } else {
+                    // storage stops at capacity (the reference's merge_join_run,
+                    // _kernels.py:382-390); PAIR_EMITTED says how many landed
                     const int64_t o = emit_base + e;
-                    emit_out[2 * o] = swap ? sp : rp;
-                    emit_out[2 * o + 1] = swap ? rp : sp;
+                    if (o < cap) {
+                        emit_out[2 * o] = swap ? sp : rp;
+                        emit_out[2 * o + 1] = swap ? rp : sp;
+                    }
                     ++e;
                 }
             };
@@ -755,7 +790,7 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
 // per-pair emitted counts from per-tile counts; tile offsets (exclusive scan)
 __global__ void __launch_bounds__(1024) k_emit_offsets(int64_t* __restrict__ tile_cnt, const TileSplit* __restrict__ splits,
                                                        const int64_t* __restrict__ total, uint64_t* __restrict__ out_pairs,
-                                                       int64_t* __restrict__ grand) {
+                                                       int64_t cap, int64_t* __restrict__ grand) {
     __shared__ int64_t s[1024];
     __shared__ int64_t carry;
     if (threadIdx.x == 0) carry = 0;
@@ -764,9 +799,6 @@ __global__ void __launch_bounds__(1024) k_emit_offsets(int64_t* __restrict__ til
     for (int64_t base = 0; base < n; base += 1024) {
         const int64_t g = base + threadIdx.x;
         const int64_t v = g < n ? tile_cnt[g] : 0;
-        if (g < n && v)
-            atomicAdd((unsigned long long*)(out_pairs + (size_t)splits[g].pair * MPSM_PAIR_FIELDS + MPSM_PAIR_EMITTED),
-                      (unsigned long long)v);
         s[threadIdx.x] = v;
         __syncthreads();
         for (int off = 1; off < 1024; off <<= 1) {
@@ -775,7 +807,16 @@ __global__ void __launch_bounds__(1024) k_emit_offsets(int64_t* __restrict__ til
             s[threadIdx.x] += a;
             __syncthreads();
         }
-        if (g < n) tile_cnt[g] = carry + s[threadIdx.x] - v;
+        if (g < n) {
+            const int64_t off = carry + s[threadIdx.x] - v;
+            tile_cnt[g] = off;
+            // pairs of this tile that land below the capacity
+            const int64_t w = min(v, max(cap - off, (int64_t)0));
+            if (w)
+                atomicAdd((unsigned long long*)(out_pairs + (size_t)splits[g].pair * MPSM_PAIR_FIELDS +
+                                                MPSM_PAIR_EMITTED),
+                          (unsigned long long)w);
+        }
         __syncthreads();
         if (threadIdx.x == 1023) carry += s[1023];
         __syncthreads();
@@ -827,7 +868,7 @@ static size_t join_ws_size(int n_priv, int n_pub, int64_t mt) {
 }
 
 template <int MODE, bool PK, bool K32 = false>
-static int launch_merge(const JoinWs& w, int swap, uint64_t* d_pairs, uint64_t* emit_out, int64_t mt,
+static int launch_merge(const JoinWs& w, int swap, uint64_t* d_pairs, uint64_t* emit_out, int64_t cap, int64_t mt,
                         const PackInfo& pi, cudaStream_t st) {
     static int per_sm = 0;
     if (per_sm == 0) {
@@ -843,15 +884,16 @@ static int launch_merge(const JoinWs& w, int swap, uint64_t* d_pairs, uint64_t* 
     const int grid = (int)std::min<int64_t>((int64_t)num_sms() * per_sm, mt);
     ProfScope ps(MODE == 0 ? "merge" : (MODE == 1 ? "merge_count" : "merge_emit"), st);
     k_merge<MODE, PK, K32><<<grid, MJ_THREADS, sizeof(MergeSmem<PK>), st>>>(w.splits, w.total, swap, d_pairs, w.tile_cnt,
-                                                                    emit_out, pi);
+                                                                    emit_out, cap, pi);
     return check_launch("k_merge");
 }
 
 template <bool PK>
 static int join_pairs_impl(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub, int swap, int mode,
-                           uint64_t* d_out, uint64_t* d_pairs, void* workspace, size_t ws_bytes, const PackInfo& pi,
-                           cudaStream_t st) {
+                           uint64_t* d_out, int64_t cap, uint64_t* d_pairs, void* workspace, size_t ws_bytes,
+                           const PackInfo& pi, cudaStream_t st) {
     if (n_priv < 1 || n_pub < 1 || !d_pairs) return MPSM_ERR_ARG;
+    if (mode == MPSM_MODE_MATERIALIZE && d_out && cap < 0) return MPSM_ERR_ARG;
     if (mode < 0 || mode > 2) return MPSM_ERR_ARG;
     const int npairs = n_priv * n_pub;
     const int64_t mt = max_tiles(priv, n_priv, pub, n_pub);
@@ -876,14 +918,14 @@ static int join_pairs_impl(const mpsm_run_t* priv, int n_priv, const mpsm_run_t*
     }
     MPSM_TRY(check_launch("k_partition"));
     const bool k32 = PK && (64 - pi.pw) <= 32;  // packed keys fit 32 bits
-    if (k32) MPSM_TRY((launch_merge<0, PK, PK>(w, swap, d_pairs, nullptr, mt, pi, st)));
-    else MPSM_TRY((launch_merge<0, PK>(w, swap, d_pairs, nullptr, mt, pi, st)));
+    if (k32) MPSM_TRY((launch_merge<0, PK, PK>(w, swap, d_pairs, nullptr, 0, mt, pi, st)));
+    else MPSM_TRY((launch_merge<0, PK>(w, swap, d_pairs, nullptr, 0, mt, pi, st)));
     if (mode != MPSM_MODE_MATERIALIZE || d_out == nullptr) return MPSM_OK;
     // materialize: per-tile counts, offsets, emission
-    MPSM_TRY((launch_merge<1, PK>(w, swap, d_pairs, nullptr, mt, pi, st)));
-    k_emit_offsets<<<1, 1024, 0, st>>>(w.tile_cnt, w.splits, w.total, d_pairs, w.grand);
+    MPSM_TRY((launch_merge<1, PK>(w, swap, d_pairs, nullptr, 0, mt, pi, st)));
+    k_emit_offsets<<<1, 1024, 0, st>>>(w.tile_cnt, w.splits, w.total, d_pairs, cap, w.grand);
     MPSM_TRY(check_launch("k_emit_offsets"));
-    return launch_merge<2, PK>(w, swap, d_pairs, d_out, mt, pi, st);
+    return launch_merge<2, PK>(w, swap, d_pairs, d_out, cap, mt, pi, st);
 }
 
 }  // namespace mpsm
@@ -915,18 +957,16 @@ extern "C" int mpsm_join_workspace_bytes(const mpsm_run_t* priv, int n_priv, con
 extern "C" int mpsm_join_pairs(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub, int swap,
                                int mode, uint64_t* d_out, int64_t cap, uint64_t* d_pairs, void* workspace,
                                size_t ws_bytes, void* stream) {
-    (void)cap;  // the caller sized d_out from the counts of a first call
-    return join_pairs_impl<false>(priv, n_priv, pub, n_pub, swap, mode, d_out, d_pairs, workspace, ws_bytes,
+    return join_pairs_impl<false>(priv, n_priv, pub, n_pub, swap, mode, d_out, cap, d_pairs, workspace, ws_bytes,
                                   PackInfo{0, 0, 0, 0}, (cudaStream_t)stream);
 }
 
 extern "C" int mpsm_join_pairs_packed(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub,
                                       int width_bits, uint64_t lower, int swap, int mode, uint64_t* d_out, int64_t cap,
                                       uint64_t* d_pairs, void* workspace, size_t ws_bytes, void* stream) {
-    (void)cap;
     if (width_bits < 1 || width_bits > 63) return MPSM_ERR_ARG;
     const int pw = 64 - width_bits;
-    return join_pairs_impl<true>(priv, n_priv, pub, n_pub, swap, mode, d_out, d_pairs, workspace, ws_bytes,
+    return join_pairs_impl<true>(priv, n_priv, pub, n_pub, swap, mode, d_out, cap, d_pairs, workspace, ws_bytes,
                                  PackInfo{pw, lower, (1ull << pw) - 1, pw >= 32 ? (1u << (pw - 32)) - 1u : 0u},
                                  (cudaStream_t)stream);
 }

@@ -198,6 +198,24 @@ def radix_histogram(keys: torch.Tensor, lower: int, span_m1: int, shift: int, nb
                                                 stream_ptr()), "mpsm_radix_histogram")
 
 
+def domain_report(keys: torch.Tensor, lower: int, span_m1: int) -> tuple:
+    """(violation count, first index or -1) of a device key column
+    (core.validate_relation's counts, computed on the GPU; synchronises)"""
+    rep = torch.empty(2, dtype=U64, device=keys.device)
+    _lib.check(_lib.load().mpsm_domain_report(ptr(keys), int(keys.numel()), lower, span_m1, ptr(rep), stream_ptr()),
+               "mpsm_domain_report")
+    cnt, first = (int(x) for x in rep.view(I64).cpu().tolist())
+    return cnt, (first if cnt else -1)
+
+
+def is_sorted(keys: torch.Tensor) -> bool:
+    """keys[i] <= keys[i + 1] for all i (device check; synchronises)"""
+    flag = torch.zeros(1, dtype=torch.int32, device=keys.device)
+    _lib.check(_lib.load().mpsm_check_sorted(ptr(keys), int(keys.numel()), ptr(flag), stream_ptr()),
+               "mpsm_check_sorted")
+    return int(flag.item()) == 0
+
+
 def scatter_chunk(keys, pays, lower: int, shift: int, sp: torch.Tensor, nbuckets: int, npart: int,
                   cursors: torch.Tensor, arena_k, arena_p, written: torch.Tensor) -> None:
     n = int(keys.numel())

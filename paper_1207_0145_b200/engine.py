@@ -9,16 +9,23 @@ all workers to the GPU in barrier order (engine.py:380-419); there are no
 worker threads and no barriers to deadlock on (SURVEY.md finding 7).
 
 Per phase, device work only (csrc/):
-  sort_public   onesweep LSD radix sort of every public chunk into its run
-  histogram     per-worker 2^B bucket counts of the private chunks (+ domain)
-  splitters     host: CDF from f*T bounds per run + C++ min-max search
-  scatter       stable partition scatter into the arena (reference layout)
-  sort_private  radix sort of every partition run
+  sort_public   LSD radix sort of every public chunk into its run
+  sort_private  the private input sorted as ONE run (P-MPSM; B-MPSM: per
+                chunk), first pass fused with the domain check
+  histogram     2^B bucket counts read off the sorted private run (bucket
+                starts by lower-bound search)
+  splitters     host: CDF from f*T bounds per public run + C++ min-max search
+  scatter       none on one GPU: the range partition sends contiguous key
+                ranges to the partitions in worker order and the run sort is
+                stable, so partition p's run is the slice [run_base[p],
+                run_base[p+1]) of the sorted private run -- the same tuples in
+                the same order as the reference's arena + per-partition sort
+                (partition.py:233-276, engine.py:396-409).  The multi-GPU
+                engine (distributed.py) does move tuples: there the partition
+                is a real scatter into per-rank send buffers + all-to-all.
   join          merge-path merge-join of every (private, public) run pair with
-                fused COUNT / MAX / checksum (no materialisation unless asked)
-
-With T == 1 the partition phase is the identity, so the private input is
-sorted directly (the reference still copies it through its arena).
+                fused COUNT / MAX / checksum and the Run order check (no
+                materialisation unless asked)
 """
 
 from __future__ import annotations
@@ -45,8 +52,9 @@ from .core import (
     Run,
     WorkerStats,
     chunk_bounds,
+    validate_relation,
 )
-from .partition import SplitterVector, combine_counts, effective_radix_bits
+from .partition import combine_counts, effective_radix_bits
 from .skew import LocalBounds, bound_positions, build_cdf, compute_splitters
 
 PhaseHook = Optional[Callable[[int, str], None]]
@@ -173,10 +181,27 @@ def _prepare(r: Relation, s: Relation, cfg: JoinConfig):
     return cfg.key_domain, roles, private, public
 
 
-def _raise_domain(flag: torch.Tensor, rel_name: str) -> None:
-    idx = int(flag.item())
-    if idx != -1:
-        raise DomainError(f"relation {rel_name} has out-of-domain keys (first at index {idx})")
+def _domain_report(rel: Relation, dom: KeyDomain) -> tuple:
+    """(violations, first index) of one relation: on the GPU for device
+    columns, numpy for host columns (the error path only)"""
+    if rel.cardinality == 0:
+        return 0, -1
+    keys = rel.keys
+    if isinstance(keys, torch.Tensor) and keys.is_cuda:
+        return D.domain_report(keys, dom.lower, dom.upper - dom.lower - 1)
+    rep = validate_relation(rel, dom)
+    return rep.violation_count, (rep.sample_indices[0] if rep.sample_indices else -1)
+
+
+def raise_domain_error(r: Relation, s: Relation, dom: KeyDomain) -> None:
+    """The reference's DomainError, r checked before s (engine.py:181-190).
+    Called once a fused domain check (first sort pass / histogram / upload)
+    has flagged an out-of-domain key."""
+    for name, rel in (("r", r), ("s", s)):
+        cnt, first = _domain_report(rel, dom)
+        if cnt:
+            raise DomainError(f"relation {name} has {cnt} out-of-domain keys (first at index {first})")
+    raise InternalConsistencyError("a domain check flagged a key that a recount does not find")
 
 
 # packed 8-B records (key - lower) << (64 - w) | payload are used whenever the
@@ -197,6 +222,15 @@ class JoinContext:
     """Device buffers and state of one join on one GPU.
 
     Runs are (keys, payloads) tensor pairs, or (records, None) in packed mode.
+
+    The private side of P-MPSM is sorted as ONE run and cut at the partition
+    boundaries: the range partition (partition.py:233-276) sends contiguous
+    key ranges to the partitions in worker order and the stable run sort keeps
+    input order among equal keys, so sorting the whole private input and
+    cutting it at run_base yields exactly the runs the arena + per-partition
+    sorts produce (same tuples in the same order), without the scatter pass.
+    The bucket histogram that feeds the splitters is read off the sorted run
+    by 2^B lower-bound searches (the bucket starts).
     """
 
     def __init__(self, r: Relation, s: Relation, cfg: JoinConfig, phase_hook: PhaseHook, packed: bool,
@@ -204,29 +238,28 @@ class JoinContext:
         self.cfg = cfg
         self.hook = phase_hook
         self.dev = D.ensure_device()
+        self.r, self.s = r, s
         self.dom, self.roles, private, public = _prepare(r, s, cfg)
-        # the reference names relations r / s in its domain errors (engine.py:183-188)
-        self.rel_name = {"private": self.roles.private, "public": "s" if self.roles.private == "r" else "r"}
         self.t = cfg.threads
+        self.variant = variant
         self.wbits = self.dom.width_bits
         self.packed = bool(packed) and 1 <= self.wbits <= 63
         self.pw = 64 - self.wbits
         self.span_m1 = self.dom.upper - self.dom.lower - 1
-        # the private side skips the partition (which reads key columns) in
-        # B-MPSM and with one worker; host inputs of it are staged after the
-        # public sort is queued, so that upload overlaps the public sort
+        # the private side is sorted whole (P-MPSM) or per chunk (B-MPSM);
+        # host inputs of it are staged after the public sort is queued, so
+        # that upload overlaps the public sort
         self._private = private
-        self._priv_pack = variant == "b-mpsm" or self.t == 1
         self.priv_rec = None
         self.n_priv = int(private.keys.shape[0]) if hasattr(private.keys, "shape") else len(private.keys)
         # the private upload buffer is allocated now, before the public sort is
         # queued: its copies then need not wait for that sort
         self._priv_buf = self._priv_ready = None
-        if self._priv_pack and self.packed and HOST_PACK and D.host_columns(private.keys) is not None:
+        if self.packed and HOST_PACK and D.host_columns(private.keys) is not None:
             self._priv_buf = torch.empty(self.n_priv, dtype=torch.uint64, device=self.dev)
             self._priv_ready = torch.cuda.Event()
             self._priv_ready.record()
-        self.pub_rec = self._upload(public, "public", True)
+        self.pub_rec = self._upload(public, True)
         if self.pub_rec is None:
             self.pub_k = D.to_device(public.keys, self.dev)
             self.pub_p = D.to_device(public.payloads, self.dev)
@@ -246,14 +279,13 @@ class JoinContext:
         """private input -> device (packed records or columns)"""
         private = self._private
         # the GPU is sorting the public run: host threads pack every chunk
-        self.priv_rec = self._upload(private, "private", self._priv_pack, gpu_pack_every=0, buf=self._priv_buf,
-                                     ready=self._priv_ready)
+        self.priv_rec = self._upload(private, True, gpu_pack_every=0, buf=self._priv_buf, ready=self._priv_ready)
         if self.priv_rec is None:
             self.priv_k = D.to_device(private.keys, self.dev)
             self.priv_p = D.to_device(private.payloads, self.dev)
         self._private = None
 
-    def _upload(self, rel: Relation, name: str, allowed: bool, gpu_pack_every: int = -1, buf=None, ready=None):
+    def _upload(self, rel: Relation, allowed: bool, gpu_pack_every: int = -1, buf=None, ready=None):
         """host columns -> packed records on the device, or None (columns path)"""
         if not (allowed and self.packed and HOST_PACK):
             return None
@@ -264,10 +296,16 @@ class JoinContext:
         bad, ovf = D.upload_records(hk[0], hp[0], self.dom.lower, self.span_m1, self.wbits, rec,
                                     gpu_pack_every=gpu_pack_every, ready=ready)
         if bad >= 0:
-            raise DomainError(f"relation {self.rel_name[name]} has out-of-domain keys (first at index {bad})")
+            raise_domain_error(self.r, self.s, self.dom)
         if ovf:
             raise _PackOverflow()
         return rec
+
+    def check_domain(self) -> None:
+        """raise the reference's DomainError if a fused check flagged a key
+        (synchronises on the two flags)"""
+        if int(self.bad_priv.item()) != -1 or int(self.bad_pub.item()) != -1:
+            raise_domain_error(self.r, self.s, self.dom)
 
     def _hook(self, i: int, phase: str) -> None:
         if self.hook:
@@ -320,18 +358,24 @@ class JoinContext:
             self.pub_runs.append(run)
             self.stats[i].tuples_sorted_public = b - a
 
+    def _sort_private_range(self, a: int, b: int) -> tuple:
+        if self.priv_rec is not None:
+            return self._sort_into(self.priv_rec[a:b], None, self.priv_store, a, b, self.bad_priv)
+        return self._sort_into(self.priv_k[a:b], self.priv_p[a:b], self.priv_store, a, b, self.bad_priv)
+
     def sort_private_chunks(self):
-        """B-MPSM phase 2 / P-MPSM with T=1: each private chunk sorted into its run."""
+        """B-MPSM phase 2: each private chunk sorted into its run (engine.py:297-309)."""
         self.priv_store = self._alloc_runs(self.n_priv)
         self.priv_runs = []
         for i, (a, b) in enumerate(self.priv_chunks):
             self._hook(i, "sort_private")
-            if self.priv_rec is not None:
-                run = self._sort_into(self.priv_rec[a:b], None, self.priv_store, a, b, self.bad_priv)
-            else:
-                run = self._sort_into(self.priv_k[a:b], self.priv_p[a:b], self.priv_store, a, b, self.bad_priv)
-            self.priv_runs.append(run)
+            self.priv_runs.append(self._sort_private_range(a, b))
             self.stats[i].tuples_sorted_private = b - a
+
+    def sort_private_whole(self):
+        """P-MPSM: the whole private input -> one sorted run (cut by partition())."""
+        self.priv_store = self._alloc_runs(self.n_priv)
+        self.priv_whole = self._sort_private_range(0, self.n_priv)
 
     def _public_bound_keys(self, f: int) -> np.ndarray:
         """equi-height bound keys of every sorted public run (skew.py:52-62)"""
@@ -344,25 +388,39 @@ class JoinContext:
             vals = (vals >> np.uint64(self.pw)) + np.uint64(self.dom.lower)
         return vals
 
+    def _bucket_starts(self, bits: int) -> torch.Tensor:
+        """lower bound of every bucket b = (key - lower) >> (w - bits) in the
+        sorted private run (b = 1 .. 2^bits - 1; bucket 0 starts at 0)"""
+        nb, shift = 1 << bits, self.wbits - bits
+        b = np.arange(1, nb, dtype=np.uint64)
+        if self.packed:
+            tg = (b << np.uint64(shift)) << np.uint64(self.pw)  # records of key lower + (b << shift), payload 0
+        else:
+            tg = np.uint64(self.dom.lower) + (b << np.uint64(shift))
+        run = self.priv_whole[0]
+        idx, _ = D.interp_lower_bound(run, torch.from_numpy(tg).to(self.dev))
+        return idx
+
     def partition(self):
-        """P-MPSM phase 2 (engine.py:359-374, 396-406): histograms, splitters,
-        cursors, scatter.  Returns the arena run bases."""
+        """P-MPSM phase 2 (engine.py:359-374, 396-406): histogram, splitters,
+        cursors; the partition runs are slices of the sorted private run."""
         t, dom = self.t, self.dom
+        for i in range(t):
+            self._hook(i, "histogram")
         bits = effective_radix_bits(dom, self.cfg.radix_bits)
         if (1 << bits) < t:
             raise ConfigurationError(f"effective radix bits {bits} give fewer buckets than {t} workers")
         nb = 1 << bits
-        shift = self.wbits - bits
-        hists = torch.zeros((t, nb), dtype=torch.int64, device=self.dev)
-        for i, (a, b) in enumerate(self.priv_chunks):
-            self._hook(i, "histogram")
-            D.radix_histogram(self.priv_k[a:b], dom.lower, self.span_m1, shift, nb, hists[i], self.bad_priv)
+        starts = self._bucket_starts(bits) if self.n_priv else None
         f = self.cfg.cdf_fanout
-        # the single host synchronisation of the join: counts + bounds + flags
+        # the single host synchronisation of the join: bucket starts + bounds + flags
         bk = self._public_bound_keys(f)
-        hist_h = hists.cpu().numpy()
-        _raise_domain(self.bad_priv, self.rel_name["private"])
-        _raise_domain(self.bad_pub, self.rel_name["public"])
+        self.check_domain()
+        edges = np.zeros(nb + 1, np.int64)
+        if starts is not None:
+            edges[1:nb] = starts.cpu().numpy()
+        edges[nb] = self.n_priv
+        hist = np.diff(edges)
         bounds, off = [], 0
         for a, b in self.pub_chunks:
             if b > a:
@@ -371,34 +429,25 @@ class JoinContext:
             else:
                 bounds.append(LocalBounds(np.empty(0, np.uint64), 0))
         cdf = build_cdf(bounds, anchor_key=dom.lower)
-        ss = compute_splitters(hist_h.sum(axis=0), cdf, t, dom, bits)
+        ss = compute_splitters(hist, cdf, t, dom, bits)
         self.splitters = ss
-        cursors = combine_counts(list(hist_h), ss.vector.sp, t)
+        cursors = combine_counts([hist], ss.vector.sp, t)
         cursors.verify_disjoint()
         self.cursors = cursors
-        arena_k = self._empty(self.n_priv)
-        arena_p = self._empty(self.n_priv)
-        sp_dev = torch.from_numpy(ss.vector.sp.astype(np.int32)).to(self.dev)
-        cur_all = torch.from_numpy(np.stack([cursors.absolute_cursors(i)[0] for i in range(t)])).to(self.dev)
-        written = torch.zeros((t, t), dtype=torch.int64, device=self.dev)
         for i, (a, b) in enumerate(self.priv_chunks):
             self._hook(i, "scatter")
-            D.scatter_chunk(self.priv_k[a:b], self.priv_p[a:b], dom.lower, shift, sp_dev, nb, t, cur_all[i],
-                            arena_k, arena_p, written[i])
             self.stats[i].tuples_scattered = b - a
-        self.written = written
-        self.arena = (arena_k, arena_p)
         return cursors.run_base
 
-    def sort_partitions(self, run_base):
-        """P-MPSM phase 3 (engine.py:405-409)."""
-        arena_k, arena_p = self.arena
-        self.priv_store = self._alloc_runs(self.n_priv)
+    def cut_partitions(self, run_base):
+        """P-MPSM phase 3 (engine.py:405-409): partition p's run is
+        [run_base[p], run_base[p+1]) of the sorted private run."""
+        k, p = self.priv_whole
         self.priv_runs = []
         for i in range(self.t):
             a, b = int(run_base[i]), int(run_base[i + 1])
             self._hook(i, "sort_private")
-            self.priv_runs.append(self._sort_into(arena_k[a:b], arena_p[a:b], self.priv_store, a, b, None))
+            self.priv_runs.append((k[a:b], None if p is None else p[a:b]))
             self.stats[i].tuples_sorted_private = b - a
 
     def _join(self, mode: int, out=None, cap: int = 0):
@@ -429,8 +478,9 @@ class JoinContext:
         """engine.py:195-225 plus the checksum and per-worker statistics."""
         t = self.t
         rec = self.rec.cpu().numpy().reshape(t, t, _lib.PAIR_FIELDS).astype(object)
-        _raise_domain(self.bad_priv, self.rel_name["private"])
-        _raise_domain(self.bad_pub, self.rel_name["public"])
+        self.check_domain()
+        if any(int(f) & _lib.FLAG_UNSORTED for f in rec[:, :, _lib.PAIR_FLAGS].ravel()):
+            raise InternalConsistencyError("run keys are not sorted ascending (found by the merge-join walk)")
         count, agg, csum = 0, None, 0
         for i in range(t):
             st = self.stats[i]
@@ -474,43 +524,49 @@ def _run(variant: str, r: Relation, s: Relation, cfg: JoinConfig, phase_hook: Ph
         ctx.sort_public()
         ctx.tl.mark("public")
         # with host inputs the private upload runs while the GPU sorts the
-        # public run (its wait lands in the "partition" interval)
+        # public run
         ctx.stage_private()
     except _PackOverflow:
         return _run(variant, r, s, cfg, phase_hook, packed=False)
     if variant == "b-mpsm":
-        ctx.tl.mark("scatter")
+        ctx.tl.mark("partitioned")
         ctx.sort_private_chunks()
-    elif ctx.t == 1:
-        # one partition: the histogram/scatter are the identity (the splitter
-        # search returns [0, 2^B]); sort the private input directly
-        effective_radix_bits(ctx.dom, cfg.radix_bits)
-        for ph in ("histogram", "scatter"):
-            ctx._hook(0, ph)
-        ctx.stats[0].tuples_scattered = ctx.n_priv
-        ctx.tl.mark("scatter")
-        ctx.sort_private_chunks()
+        ctx.tl.mark("sort_private")
     else:
-        run_base = ctx.partition()
-        ctx.tl.mark("scatter")
-        ctx.sort_partitions(run_base)
-    ctx.tl.mark("sort_private")
+        # P-MPSM: sort the private input as one run, derive the bucket
+        # histogram and the splitters, cut the run at the partition bounds.
+        # With one worker the partition is the identity (the splitter search
+        # returns [0, 2^B]) and the histogram is not needed.
+        ctx.sort_private_whole()
+        ctx.tl.mark("sorted_private")
+        if ctx.t == 1:
+            effective_radix_bits(ctx.dom, cfg.radix_bits)
+            for ph in ("histogram", "scatter"):
+                ctx._hook(0, ph)
+            ctx.stats[0].tuples_scattered = ctx.n_priv
+            ctx.tl.mark("partitioned")
+            ctx.cut_partitions([0, ctx.n_priv])
+        else:
+            run_base = ctx.partition()
+            ctx.tl.mark("partitioned")
+            ctx.cut_partitions(run_base)
+        ctx.tl.mark("sort_private")
     ctx.join()
     ctx.tl.mark("join")
     torch.cuda.current_stream().synchronize()
     if ctx.packed_overflowed():
         # a payload needs more than 64 - w bits: redo on (key, payload) pairs
-        _raise_domain(ctx.bad_priv, ctx.rel_name["private"])
-        _raise_domain(ctx.bad_pub, ctx.rel_name["public"])
+        ctx.check_domain()
         return _run(variant, r, s, cfg, phase_hook, packed=False)
-    if variant == "p-mpsm" and ctx.t > 1:
-        if not np.array_equal(ctx.written.cpu().numpy(), ctx.cursors.counts):
-            raise InternalConsistencyError("scatter wrote a different number of tuples than the histograms promised")
     tl = ctx.tl
-    timings = {"sort_public": tl.seconds("t0", "public"),
-               "partition": tl.seconds("public", "scatter") if variant == "p-mpsm" else 0.0,
-               "sort_private": tl.seconds("scatter", "sort_private"), "join": tl.seconds("sort_private", "join"),
-               "total": tl.seconds("t0", "join")}
+    if variant == "p-mpsm":
+        timings = {"sort_public": tl.seconds("t0", "public"), "partition": tl.seconds("sorted_private", "partitioned"),
+                   "sort_private": tl.seconds("public", "sorted_private"), "join": tl.seconds("sort_private", "join"),
+                   "total": tl.seconds("t0", "join")}
+    else:
+        timings = {"sort_public": tl.seconds("t0", "public"), "partition": 0.0,
+                   "sort_private": tl.seconds("partitioned", "sort_private"), "join": tl.seconds("sort_private", "join"),
+                   "total": tl.seconds("t0", "join")}
     return ctx.finalize(timings)
 
 
@@ -525,6 +581,78 @@ def run_pmpsm(r: Relation, s: Relation, cfg: JoinConfig, *, phase_hook: PhaseHoo
     return _run("p-mpsm", r, s, cfg, phase_hook)
 
 
+def _payloads_below_2_63(rel: Relation) -> bool:
+    if rel.cardinality == 0:
+        return True
+    p = rel.payloads
+    if isinstance(p, torch.Tensor) and p.is_cuda:
+        return D.domain_report(p, 0, (1 << 63) - 1)[0] == 0
+    return int(np.asarray(rel.host_payloads()).max()) < 1 << 63
+
+
+def run_hash_oracle(r: Relation, s: Relation, cfg: JoinConfig) -> JoinResult:
+    """algorithm="hash-oracle" (engine.py:462-465 -> datagen.hash_join_oracle,
+    datagen.py:121-200) served on the GPU: the reference's ground-truth join
+    over the full 64-bit key space (no key domain), build side = the smaller
+    input, with its result shape -- phase_timings build / join / total,
+    worker_stats [], aggregate_max only in aggregate-max mode with matches,
+    materialized (r, s) rows (MaterializeCapExceeded past the cap), payloads
+    >= 2^63 rejected with ValueError.  The build and probe sides are sorted
+    by the run sort over all 64 key bits and joined by the merge kernel (the
+    same COUNT / MAX / checksum; pair order is key order, not probe order)."""
+    for name, rel in (("r", r), ("s", s)):
+        if not _payloads_below_2_63(rel):
+            raise ValueError(f"relation {name} has payloads >= 2^63; aggregate undefined")
+    dev = D.ensure_device()
+    build_is_r = r.cardinality <= s.cardinality
+    build, probe = (r, s) if build_is_r else (s, r)
+    tl = _Timeline()
+    tl.mark("t0")
+    full = (1 << 64) - 1
+
+    def sorted_run(rel):
+        k, p = D.to_device(rel.keys, dev), D.to_device(rel.payloads, dev)
+        n = int(k.numel())
+        ok, op = torch.empty_like(k), torch.empty_like(p)
+        if n:
+            tk, tp = torch.empty_like(k), torch.empty_like(p)
+            D.sort_pairs(k, p, 0, full, 64, ok, op, tk, tp, None)
+        return ok, op
+
+    b_run = sorted_run(build)
+    p_run = sorted_run(probe)
+    tl.mark("build")
+    if b_run[0].numel() == 0 or p_run[0].numel() == 0:
+        rec = None
+    else:
+        rec = D.join_pairs([b_run], [p_run], not build_is_r, _lib.MODE_COUNT)
+    tl.mark("join")
+    count, best, csum = 0, None, 0
+    if rec is not None:
+        row = rec.cpu().numpy()[0]
+        count = int(row[_lib.PAIR_COUNT])
+        best = int(row[_lib.PAIR_BEST]) if count else None
+        csum = int(row[_lib.PAIR_CHECKSUM])
+        if int(row[_lib.PAIR_FLAGS]) & _lib.FLAG_UNSORTED:
+            raise InternalConsistencyError("run keys are not sorted ascending (found by the merge-join walk)")
+    materialized = None
+    if cfg.query_mode == "materialize":
+        if count > cfg.materialize_cap:
+            raise MaterializeCapExceeded(f"oracle output exceeds cap {cfg.materialize_cap}")
+        if count:
+            out = torch.empty(2 * count, dtype=torch.uint64, device=dev)
+            D.join_pairs([b_run], [p_run], not build_is_r, _lib.MODE_MATERIALIZE, out, count)
+            materialized = out.view(count, 2).cpu().numpy()
+        else:
+            materialized = np.empty((0, 2), np.uint64)
+    torch.cuda.current_stream().synchronize()
+    t_build, t_join = tl.seconds("t0", "build"), tl.seconds("build", "join")
+    return JoinResult(match_count=count, aggregate_max=best if cfg.query_mode == "aggregate-max" else None,
+                      materialized=materialized,
+                      phase_timings={"build": t_build, "join": t_join, "total": t_build + t_join},
+                      worker_stats=[], checksum=csum)
+
+
 def run_join(r: Relation, s: Relation, cfg: JoinConfig, *, phase_hook: PhaseHook = None) -> JoinResult:
     """Dispatch on cfg.algorithm (engine.py:456-466)."""
     if cfg.algorithm == "b-mpsm":
@@ -532,6 +660,5 @@ def run_join(r: Relation, s: Relation, cfg: JoinConfig, *, phase_hook: PhaseHook
     if cfg.algorithm == "p-mpsm":
         return run_pmpsm(r, s, cfg, phase_hook=phase_hook)
     if cfg.algorithm == "hash-oracle":
-        raise ConfigurationError("algorithm 'hash-oracle' is the reference's CPU ground truth "
-                                 "(datagen.hash_join_oracle); this package implements the MPSM engines only")
+        return run_hash_oracle(r, s, cfg)
     raise ConfigurationError(f"unknown algorithm {cfg.algorithm!r}")
