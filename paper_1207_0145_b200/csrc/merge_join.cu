@@ -57,6 +57,9 @@ namespace mpsm {
 #ifndef MPSM_MJ_P2_UNROLL  // match-phase loop unroll (independent W tuples in flight)
 #define MPSM_MJ_P2_UNROLL 2
 #endif
+#ifndef MPSM_MJ_ORDER_CHECK  // the Run order check in the walk (0: off, A/B timing only; 1: per array; 2: merged)
+#define MPSM_MJ_ORDER_CHECK 2
+#endif
 #define MPSM_PRAGMA(x) _Pragma(#x)
 #define MPSM_UNROLL(n) MPSM_PRAGMA(unroll n)
 constexpr int MJ_THREADS = MPSM_MJ_THREADS;
@@ -325,16 +328,17 @@ __global__ void k_split_fill(const mpsm_run_t* __restrict__ priv, int n_pub, con
 // inside the mapped allocation.
 template <bool PK>
 struct alignas(16) MergeStage {
-    uint64_t k[MJ_TILE + 8];
+    uint64_t k[MJ_TILE + 8];           // R span (<= 4 extra slots) + W span (<= 3 extra slots)
     uint64_t p[PK ? 2 : MJ_TILE + 8];  // payloads (SoA runs only)
     TileSplit t;                       // descriptor of the staged tile
-    int r0, w0, rp0, wp0, hp;          // where R tile element 0 / W element 0 sit in k[] (p[]); prior R tuples
+    int r0, w0, rp0, wp0, hp, whp;     // where R tile element 0 / W element 0 sit in k[] (p[]); prior R / W tuples
 };
 template <bool PK>
 struct MergeSmem {
     MergeStage<PK> st[2];
     uint16_t ub[MJ_TILE];  // MODE 0: per W tuple of the tile, R tuples <= its key (tile-relative)
     int tdup[2];           // MODE 0, per tile parity: some R key of the tile repeats
+    int wend[MJ_THREADS / 32], wlo[MJ_THREADS / 32];  // MODE 0: where each warp's walk ends / starts (R index)
     uint32_t kmask;        // PackInfo::kmask, read back with a volatile load (see k_merge)
     uint64_t bar[2];
     uint64_t red[3][MJ_THREADS / 32];
@@ -358,14 +362,17 @@ __device__ __forceinline__ Span span_of(const uint64_t* a, int64_t first, int n)
 // where tile t's elements sit in a stage
 struct TilePlace {
     Span rk, wk, rp, wp;
-    int hp;
+    int hp, whp;
 };
 template <bool PK>
 __device__ __forceinline__ TilePlace place_of(const TileSplit& t) {
     TilePlace q;
     q.hp = t.i0 >= 2 ? 2 : (int)t.i0;  // up to two prior R tuples
     q.rk = span_of(t.rk, t.i0 - q.hp, t.nR + q.hp);
-    q.wk = span_of(t.wk, t.w0, t.nW);
+    // the W key before the tile comes along (the order check of the tile
+    // boundary); its payload is never read
+    q.whp = (t.w0 > 0 && t.nW > 0) ? 1 : 0;
+    q.wk = span_of(t.wk, t.w0 - q.whp, t.nW + q.whp);
     if (!PK) {
         q.rp = span_of(t.rp, t.i0 - q.hp, t.nR + q.hp);
         q.wp = span_of(t.wp, t.w0, t.nW);
@@ -379,8 +386,9 @@ __device__ __forceinline__ void fetch_tile(MergeStage<PK>& st, uint64_t* bar, co
     st.t = t;
     // the placement, computed once here for every thread of the CTA
     st.hp = q.hp;
+    st.whp = q.whp;
     st.r0 = q.rk.off + q.hp;
-    st.w0 = (int)(q.rk.bytes / 8) + q.wk.off;
+    st.w0 = (int)(q.rk.bytes / 8) + q.wk.off + q.whp;
     if (!PK) {
         st.rp0 = q.rp.off + q.hp;
         st.wp0 = (int)(q.rp.bytes / 8) + q.wp.off;
@@ -487,10 +495,6 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
             count = best = csum = 0;
         }
         MJ_TS(1)
-        // MODE 0, thread 0: the public element before the tile, for the
-        // sortedness check of the tile boundary
-        uint64_t w_prev = 0;
-        if (MODE == 0 && tid == 0 && t.w0 > 0) w_prev = __ldg(t.wk + t.w0 - 1);
         mbar_wait(&sm.bar[buf], (par >> buf) & 1u);
         par ^= 1u << buf;
         MJ_TS(2)
@@ -563,6 +567,9 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                     dup = pk == rkc;
                     unsorted = pk > rkc;
                 }
+                // the W pair across the thread boundary (the one inside the
+                // walk ranges of two threads)
+                if (wj >= 1 && wj < nW) unsorted = unsorted || wkey(wj - 1) > wkc;
                 if (tid == 0) {
                     if (hp == 2) {
                         const KT a = rk_w(-2), b = rk_w(-1);
@@ -571,27 +578,47 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                     } else if (hp == 1) {
                         rk_w(-1);
                     }
-                    // the W element before the tile (global memory, loaded
-                    // before the stage wait)
-                    if (t.w0 > 0 && nW > 0) unsorted = unsorted || nkey(w_prev) > wkey(0);
+                    // the W element before the tile (staged with it)
+                    if (sm.st[buf].whp) unsorted = unsorted || wkey(-1) > wkey(0);
                 }
                 KT dmin = dup ? (KT)0 : (KT)1;  // 0 iff two neighbouring R keys are equal (one min per step)
+                // the keys the walk takes must not decrease: within a thread
+                // that covers every adjacent R pair and W pair it steps over
+                // (both arrays are taken in order); the pairs across thread
+                // and tile boundaries are checked above, and the threads'
+                // walks must meet (checked below), so every adjacent pair of
+                // the tile is compared
+                KT last = 0;
+                uint32_t down = 0;
                 for (int st = k0; st < k1; ++st) {
                     const bool take_r = ri < nR && (wj >= nW || rkc <= wkc);
+                    if (MPSM_MJ_ORDER_CHECK == 2) {
+                        const KT m = take_r ? rkc : wkc;
+                        down |= (uint32_t)(m < last);
+                        last = m;
+                    }
                     if (!take_r) sm.ub[wj] = (uint16_t)ri;
                     ri += take_r;
                     wj += !take_r;
                     if (take_r && ri < nR) {
                         const KT nk = rk_w(ri);
                         dmin = min(dmin, (KT)(nk ^ rkc));
-                        unsorted = unsorted || nk < rkc;
+                        if (MPSM_MJ_ORDER_CHECK == 1) unsorted = unsorted || nk < rkc;
                         rkc = nk;
                     }
                     if (!take_r && wj < nW) {
                         const KT nw = wk_w(wj);
-                        unsorted = unsorted || nw < wkc;
+                        if (MPSM_MJ_ORDER_CHECK == 1) unsorted = unsorted || nw < wkc;
                         wkc = nw;
                     }
+                }
+                unsorted = unsorted || down != 0;
+                // the walks meet: my end is the next thread's merge-path split
+                if (MPSM_MJ_ORDER_CHECK) {
+                    const int nlo = __shfl_down_sync(0xffffffffu, lo, 1);
+                    if ((tid & 31) != 31) unsorted = unsorted || nlo != ri;
+                    else sm.wend[tid >> 5] = ri;
+                    if ((tid & 31) == 0) sm.wlo[tid >> 5] = lo;
                 }
                 dup = dmin == 0;
                 const int fl = (dup ? 1 : 0) | ((K32 && (wide & kmask)) ? 2 : 0);
@@ -601,6 +628,10 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                              (unsigned long long)MPSM_FLAG_UNSORTED);
             }
             __syncthreads();
+            // the walks of consecutive warps meet
+            if (MPSM_MJ_ORDER_CHECK && tid < MJ_THREADS / 32 - 1 && sm.wend[tid] != sm.wlo[tid + 1])
+                atomicOr((unsigned long long*)(out_pairs + (size_t)t.pair * MPSM_PAIR_FIELDS + MPSM_PAIR_FLAGS),
+                         (unsigned long long)MPSM_FLAG_UNSORTED);
             MJ_TS(4)
             // phase 2 -- W tuples dealt round-robin (balanced, no merge
             // control flow): each matches the equal-key R group ending at
