@@ -65,6 +65,32 @@ namespace mpsm {
 constexpr int MJ_THREADS = MPSM_MJ_THREADS;
 constexpr int MJ_ITEMS = MPSM_MJ_ITEMS;  // odd: 64-bit smem accesses at stride ITEMS are conflict-free
 constexpr int MJ_TILE = MJ_THREADS * MJ_ITEMS;
+#ifndef MPSM_MJ_TABLE  // MODE 0 direct-address match path (0: always the merge walk)
+#define MPSM_MJ_TABLE 1
+#endif
+constexpr int MJ_TBL = 2048;  // table slots (a tile's R keys must span fewer)
+constexpr int MJ_TBL_TAGS = 32;  // 5-bit tile tags; the table is cleared when they run out
+static_assert(MJ_TILE + 3 < (1 << 11), "stage index + 1 fits the 11-bit field of a table entry");
+
+// Masked accumulation on the FMA pipe (the merge is bound by the ALU pipe:
+// LOP3 / SHF / IADD3 / SEL / ISETP share it, IMAD runs beside it).  m is 0
+// or 1: acc += h * m as a 64-bit add with carry through two IMADs.
+__device__ __forceinline__ uint64_t mad_mask64(uint64_t acc, uint64_t h, uint32_t m) {
+    uint32_t alo = (uint32_t)acc, ahi = (uint32_t)(acc >> 32);
+    asm("mad.lo.cc.u32 %0, %2, %4, %0;\n\tmadc.lo.u32 %1, %3, %4, %1;"
+        : "+r"(alo), "+r"(ahi)
+        : "r"((uint32_t)h), "r"((uint32_t)(h >> 32)), "r"(m));
+    return ((uint64_t)ahi << 32) | alo;
+}
+// (a + b) * m, 64-bit, on the FMA pipe
+__device__ __forceinline__ uint64_t add_mask64(uint64_t a, uint64_t b, uint32_t m) {
+    uint32_t lo, hi;
+    asm("mul.lo.u32 %0, %2, %6;\n\tmul.lo.u32 %1, %3, %6;\n\t"
+        "mad.lo.cc.u32 %0, %4, %6, %0;\n\tmadc.lo.u32 %1, %5, %6, %1;"
+        : "=r"(lo), "=r"(hi)
+        : "r"((uint32_t)b), "r"((uint32_t)(b >> 32)), "r"((uint32_t)a), "r"((uint32_t)(a >> 32)), "r"(m));
+    return ((uint64_t)hi << 32) | lo;
+}
 
 struct PackInfo {
     int pw;          // payload bits of a packed record (0: SoA runs)
@@ -336,7 +362,10 @@ struct alignas(16) MergeStage {
 template <bool PK>
 struct MergeSmem {
     MergeStage<PK> st[2];
-    uint16_t ub[MJ_TILE];  // MODE 0: per W tuple of the tile, R tuples <= its key (tile-relative)
+    union {
+        uint16_t ub[MJ_TILE];   // MODE 0 walk: per W tuple of the tile, R tuples <= its key (tile-relative)
+        uint16_t tbl[MJ_TBL];   // MODE 0 table: slot key - key(R[-hp]) -> tag << 11 | stage index + 1
+    };
     int tdup[2];           // MODE 0, per tile parity: some R key of the tile repeats
     int wend[MJ_THREADS / 32], wlo[MJ_THREADS / 32];  // MODE 0: where each warp's walk ends / starts (R index)
     uint32_t kmask;        // PackInfo::kmask, read back with a volatile load (see k_merge)
@@ -480,6 +509,7 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
         if (g + G < ntiles) t_nxt = splits[g + G];
     }
     using KT = typename std::conditional<K32, uint32_t, uint64_t>::type;
+    int tgen = MJ_TBL_TAGS;  // MODE 0 table: tag of the next table tile (MJ_TBL_TAGS: clear first)
     for (; g < ntiles; g += G) {
         MJ_TS(0)
         __syncthreads();  // stage buf^1 free, stage buf's descriptor visible
@@ -520,6 +550,209 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
         auto wkey = [&](int j) -> KT { return nkey(WK[j]); };
         auto rpay = [&](int i) -> uint64_t { return PK ? (RP[i] & pi.pmask) : RP[i]; };
         auto wpay = [&](int j) -> uint64_t { return PK ? (WP[j] & pi.pmask) : WP[j]; };
+        bool tile_done = false;
+#if MPSM_MJ_TABLE
+        // ---- MODE 0 direct-address match.  When the tile's R keys (with
+        // the staged prior tuples) span fewer than MJ_TBL key values, every
+        // R tuple is entered at slot key - key(R[-hp]) of a shared table and
+        // every W tuple looks its key up: a hit is the R tuple with that key
+        // (the last one written if the key repeats; the group is then walked
+        // in both directions).  No merge-path split and no merge walk inside
+        // the tile: per W tuple a load, a table probe, the compare and the
+        // aggregate, two W tuples per lane and step without branches (two
+        // independent hash chains for the scheduler).  Both passes deal
+        // warp-contiguous runs of the tile to the lanes, so every adjacent R
+        // and W pair of the tile (and the staged prior tuples) is compared
+        // through a lane shuffle: the Run order check of core.py:153-154.
+        // Tiles whose R keys spread wider (sparse R) take the merge walk.
+        if (MODE == 0) {
+            const int nRh = nR + hp;
+            // K32 keys are key << ksh | kmask: slot = (k - kb) >> ksh; the
+            // span limit keeps every in-tile key difference inside int32
+            const int ksh = K32 ? pi.pw - 32 : 0;
+            const uint64_t tlim64 = min((uint64_t)MJ_TBL << ksh, (uint64_t)0x7fffffff);
+            const KT tlim = (KT)tlim64;
+            const KT kb = nRh > 0 ? rkey(-hp) : (KT)0;
+            if (nRh > 0 && (KT)(rkey(nR - 1) - kb) < tlim) {
+                tile_done = true;
+                if (tgen >= MJ_TBL_TAGS) {  // tags used up (or the walk wrote ub over the table)
+                    for (int q = tid; q < MJ_TBL / 8; q += MJ_THREADS)
+                        reinterpret_cast<uint4*>(sm.tbl)[q] = make_uint4(0, 0, 0, 0);
+                    __syncthreads();
+                    tgen = 1;
+                }
+                const uint32_t tag = (uint32_t)tgen << 11;
+                const int lane = tid & 31, warp = tid >> 5;
+                constexpr int NWARP = MJ_THREADS / 32;
+                uint32_t bad = 0;
+                // insert: stage indices e = 0 .. nRh-1 (R index e - hp); the
+                // order check as the minimum of the in-tile key steps (int32:
+                // keys inside the span), keys outside it are out of order
+                // dense: every step is exactly one key (R keys consecutive, the
+                // FK case: a W key's R tuple is at stage index (k - kb) >> ksh
+                // without the table)
+                int32_t mind = 1;
+                uint32_t nondense = 0;
+                const uint32_t step1 = 1u << ksh;
+                {
+                    const int cw = (nRh + NWARP - 1) / NWARP;
+                    const int beg = min(warp * cw, nRh), end = min(beg + cw, nRh);
+                    uint32_t carry = beg > 0 ? (uint32_t)(rkey(beg - 1 - hp) - kb) : 0u;
+                    for (int e0 = beg; e0 < end; e0 += 32) {
+                        const int e = e0 + lane;
+                        const bool valid = e < end;
+                        const KT d = valid ? (KT)(rkey(e - hp) - kb) : (KT)0;
+                        const uint32_t d32 = (uint32_t)d;
+                        uint32_t prev = __shfl_up_sync(0xffffffffu, d32, 1);
+                        if (lane == 0) prev = carry;
+                        carry = __shfl_sync(0xffffffffu, d32, 31);
+                        if (valid) {
+                            bad |= (uint32_t)(d >= tlim);
+                            if (e > 0) {
+                                mind = min(mind, (int32_t)(d32 - prev));
+                                nondense |= (d32 - prev) ^ step1;
+                            }
+                            if (d < tlim) sm.tbl[d32 >> ksh] = (uint16_t)(tag | (uint32_t)(e + 1));
+                        }
+                    }
+                }
+                bad |= (uint32_t)(mind < 0);
+                {
+                    const uint32_t f = __reduce_or_sync(0xffffffffu, (mind == 0 ? 1u : 0u) | (nondense ? 4u : 0u));
+                    if (lane == 0 && f) atomicOr(&sm.tdup[buf], (int)f);
+                }
+                __syncthreads();
+                const int tflags = sm.tdup[buf];
+                const bool tdup = tflags & 1;
+                const bool dense = !(tflags & 5);
+                // probe: W indices j = 0 .. nW-1
+                uint64_t best_t = best, csum_t = 0;
+                uint32_t cnt_t = 0;
+                {
+                    const int cw = (nW + NWARP - 1) / NWARP;
+                    const int beg = min(warp * cw, nW), end = min(beg + cw, nW);
+                    const int whp = sm.st[buf].whp;
+                    KT carry = beg > 0 ? wkey(beg - 1) : (whp ? wkey(-1) : (KT)0);
+                    const bool has_prev0 = beg > 0 || whp;
+                    const uint64_t pmask = K32 ? (pi.pmask | 0xffffffffull) : pi.pmask;
+                    // the R tuple of a W tuple: its stage index + 1, or 0
+                    auto probe = [&](KT k, bool valid) -> int {
+                        const KT d = k - kb;
+                        if (!valid || d >= tlim) return 0;
+                        const uint32_t ent = sm.tbl[(uint32_t)d >> ksh];
+                        return (ent ^ tag) < (1u << 11) ? (int)(ent & 0x7ffu) : 0;
+                    };
+                    auto rpay_of = [&](uint64_t rv, int i) -> uint64_t { return PK ? (rv & pmask) : RP[i]; };
+                    auto wpay_of = [&](uint64_t wv, int j) -> uint64_t { return PK ? (wv & pmask) : WP[j]; };
+                    // dense tiles: the R tuple of key k is at stage index
+                    // (k - kb) >> ksh if that is below nRh
+                    const KT dlim = (KT)((uint64_t)nRh << ksh);
+                    auto dense_probe = [&](KT k, bool valid) -> int {
+                        const KT d = k - kb;
+                        return (valid && d < dlim) ? (int)((uint32_t)d >> ksh) + 1 : 0;
+                    };
+                    auto unique_probe = [&](auto SW, auto DENSE) {
+                        // unique R keys: two W tuples per lane and step, the
+                        // aggregate masked (IMADs) instead of branched; the W
+                        // loads past the end stay inside shared memory
+                        for (int j0 = beg; j0 < end; j0 += 64) {
+                            const int ja = j0 + lane, jb = ja + 32;
+                            const bool va = ja < end, vb = jb < end;
+                            const uint64_t wa = WK[ja], wb = WK[jb];
+                            const KT ka = nkey(wa), kb2 = nkey(wb);
+                            KT pa = __shfl_up_sync(0xffffffffu, ka, 1), pb = __shfl_up_sync(0xffffffffu, kb2, 1);
+                            const KT la = __shfl_sync(0xffffffffu, ka, 31);
+                            if (lane == 0) {
+                                pa = carry;
+                                pb = la;
+                            }
+                            carry = __shfl_sync(0xffffffffu, kb2, 31);
+                            bad |= (uint32_t)(va && (ja > beg || has_prev0) && pa > ka);
+                            bad |= (uint32_t)(vb && pb > kb2);
+                            // hit flags (0/1) and R stage indices (a miss reads R[-hp])
+                            uint32_t ma, mb;
+                            int ia, ib;
+                            if (decltype(DENSE)::value) {
+                                const KT da = ka - kb, db = kb2 - kb;
+                                ma = (va && da < dlim) ? 1u : 0u;
+                                mb = (vb && db < dlim) ? 1u : 0u;
+                                ia = (int)(ma * ((uint32_t)da >> ksh)) - hp;
+                                ib = (int)(mb * ((uint32_t)db >> ksh)) - hp;
+                            } else {
+                                const int ea = probe(ka, va), eb = probe(kb2, vb);
+                                ma = ea ? 1u : 0u;
+                                mb = eb ? 1u : 0u;
+                                ia = (ea ? ea : 1) - 1 - hp;
+                                ib = (eb ? eb : 1) - 1 - hp;
+                            }
+                            const uint64_t ra = RK[ia], rb = RK[ib];
+                            const uint64_t rpa = rpay_of(ra, ia), spa = PK ? (wa & pmask) : (va ? WP[ja] : 0);
+                            const uint64_t rpb = rpay_of(rb, ib), spb = PK ? (wb & pmask) : (vb ? WP[jb] : 0);
+                            const uint64_t ha = decltype(SW)::value ? pair_hash(spa, rpa) : pair_hash(rpa, spa);
+                            const uint64_t hb = decltype(SW)::value ? pair_hash(spb, rpb) : pair_hash(rpb, spb);
+                            const uint64_t sa = add_mask64(rpa, spa, ma), sb = add_mask64(rpb, spb, mb);
+                            if (sa > best_t) best_t = sa;
+                            if (sb > best_t) best_t = sb;
+                            csum_t = mad_mask64(mad_mask64(csum_t, ha, ma), hb, mb);
+                            cnt_t += ma + mb;
+                        }
+                    };
+                    if (dense) {
+                        if (swap) unique_probe(std::true_type{}, std::true_type{});
+                        else unique_probe(std::false_type{}, std::true_type{});
+                    } else if (!tdup) {
+                        if (swap) unique_probe(std::true_type{}, std::false_type{});
+                        else unique_probe(std::false_type{}, std::false_type{});
+                    } else {
+                        for (int j0 = beg; j0 < end; j0 += 32) {
+                            const int j = j0 + lane;
+                            const bool valid = j < end;
+                            const uint64_t wv = valid ? WK[j] : 0;
+                            const KT k = nkey(wv);
+                            KT prev = __shfl_up_sync(0xffffffffu, k, 1);
+                            if (lane == 0) prev = carry;
+                            carry = __shfl_sync(0xffffffffu, k, 31);
+                            bad |= (uint32_t)(valid && (j > beg || has_prev0) && prev > k);
+                            const int ent = probe(k, valid);
+                            if (!ent) continue;  // no R tuple with this key
+                            int i = ent - 1 - hp;
+                            const uint64_t sp = wpay_of(wv, j);
+                            auto acc = [&](uint64_t rp) {
+                                const uint64_t v = rp + sp;
+                                best_t = v > best_t ? v : best_t;
+                                csum_t += swap ? pair_hash(sp, rp) : pair_hash(rp, sp);
+                                ++cnt_t;
+                            };
+                            // repeated R keys: the whole equal-key group
+                            while (i + 1 < nR && rkey(i + 1) == k) ++i;
+                            for (;;) {
+                                acc(rpay_of(RK[i], i));
+                                if (--i < -hp) {  // the group reaches back before the stage
+                                    for (int64_t gi = t.i0 + i; gi >= 0; --gi) {
+                                        const uint64_t gv = t.rk[gi];
+                                        if (nkey(gv) != k) break;
+                                        acc(PK ? (gv & pmask) : t.rp[gi]);
+                                    }
+                                    break;
+                                }
+                                if (rkey(i) != k) break;
+                            }
+                        }
+                    }
+                }
+                count += cnt_t;
+                best = best_t;
+                csum += csum_t;
+                if (__any_sync(0xffffffffu, bad != 0) && lane == 0)
+                    atomicOr((unsigned long long*)(out_pairs + (size_t)t.pair * MPSM_PAIR_FIELDS + MPSM_PAIR_FLAGS),
+                             (unsigned long long)MPSM_FLAG_UNSORTED);
+                ++tgen;
+            } else {
+                tgen = MJ_TBL_TAGS;  // the walk writes ub over the table
+            }
+        }
+#endif
+        if (!tile_done) {
         const int L = nR + nW;
         const int k0 = min(tid * MJ_ITEMS, L);
         const int k1 = min(k0 + MJ_ITEMS, L);
@@ -812,6 +1045,7 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                 tile_cnt[g] = sum;
             }
         }
+        }  // !tile_done
         MJ_TS(5)
         buf ^= 1;
     }
