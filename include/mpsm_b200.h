@@ -275,8 +275,10 @@ int mpsm_pack_records(const uint64_t* d_keys, const uint64_t* d_pays, int64_t n,
  * (8 per host-packed tuple, 16 per tuple the GPU packs from mapped memory) */
 uint64_t mpsm_upload_bytes(int reset);
 /* sort packed records (key in the top width_bits bits) by key: every pass
- * moves 8 B (the mpsm_sort_packed passes after its packing pass).  in_rec
- * must differ from out_rec and tmp_rec.  Same workspace as mpsm_sort_pairs. */
+ * moves 8 B (the mpsm_sort_packed passes after its packing pass).  tmp_rec
+ * must differ from both; in_rec may equal out_rec (sort in place) when
+ * mpsm_sort_pass_count(width_bits) is even.  Same workspace as
+ * mpsm_sort_pairs. */
 int mpsm_sort_records(const uint64_t* in_rec, int64_t n, int width_bits, uint64_t* out_rec, uint64_t* tmp_rec,
                       void* workspace, size_t ws_bytes, void* stream);
 

@@ -92,6 +92,26 @@ __device__ __forceinline__ uint64_t add_mask64(uint64_t a, uint64_t b, uint32_t 
     return ((uint64_t)hi << 32) | lo;
 }
 
+#ifndef MPSM_MJ_FMA_SHR  // splitmix's 64-bit right shifts as IMAD.HI / IMAD (FMA pipe) in the probe loop
+#define MPSM_MJ_FMA_SHR 0
+#endif
+// z ^ (z >> k) with the shift on the FMA pipe: mul = 2^(32-k) (1 <= k <= 31)
+// from a register ptxas cannot fold, hi >> k = umulhi(hi, mul) and
+// (lo >> k) | (hi << (32-k)) = umulhi(lo, mul) + hi * mul
+__device__ __forceinline__ uint64_t xorshr_fma(uint64_t z, uint32_t mul) {
+    const uint32_t lo = (uint32_t)z, hi = (uint32_t)(z >> 32);
+    const uint32_t hs = __umulhi(hi, mul);
+    const uint32_t ls = __umulhi(lo, mul) + hi * mul;
+    return ((uint64_t)(hi ^ hs) << 32) | (lo ^ ls);
+}
+__device__ __forceinline__ uint64_t pair_hash_fma(uint64_t r_pay, uint64_t s_pay, uint32_t m30, uint32_t m27,
+                                                  uint32_t m31) {
+    uint64_t z = (r_pay ^ rotl64(s_pay, 17)) + 0x9E3779B97F4A7C15ull;
+    z = xorshr_fma(z, m30) * 0xBF58476D1CE4E5B9ull;
+    z = xorshr_fma(z, m27) * 0x94D049BB133111EBull;
+    return xorshr_fma(z, m31);
+}
+
 struct PackInfo {
     int pw;          // payload bits of a packed record (0: SoA runs)
     uint64_t lower;  // key domain lower bound (packed keys are key - lower)
@@ -369,6 +389,7 @@ struct MergeSmem {
     int tdup[2];           // MODE 0, per tile parity: some R key of the tile repeats
     int wend[MJ_THREADS / 32], wlo[MJ_THREADS / 32];  // MODE 0: where each warp's walk ends / starts (R index)
     uint32_t kmask;        // PackInfo::kmask, read back with a volatile load (see k_merge)
+    uint32_t shr_mul[3];   // 2^(32-30), 2^(32-27), 2^(32-31): the splitmix shifts as IMAD.HI (see mix64_fma)
     uint64_t bar[2];
     uint64_t red[3][MJ_THREADS / 32];
     int64_t warp_cnt[MJ_THREADS / 32];
@@ -505,6 +526,9 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         sm.tdup[0] = sm.tdup[1] = 0;
         sm.kmask = pi.kmask;
+        sm.shr_mul[0] = 1u << 2;
+        sm.shr_mul[1] = 1u << 5;
+        sm.shr_mul[2] = 1u << 1;
         fetch_tile<PK>(sm.st[0], &sm.bar[0], splits[g]);
         if (g + G < ntiles) t_nxt = splits[g + G];
     }
@@ -542,6 +566,15 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
         // register for an LDC per key)
         uint32_t kmask;
         asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(kmask) : "r"(smem_addr(&sm.kmask)));
+#if MPSM_MJ_FMA_SHR
+        uint32_t m30, m27, m31;  // opaque to ptxas, so the products stay IMADs
+        asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(m30) : "r"(smem_addr(&sm.shr_mul[0])));
+        asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(m27) : "r"(smem_addr(&sm.shr_mul[1])));
+        asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(m31) : "r"(smem_addr(&sm.shr_mul[2])));
+        auto hash2 = [&](uint64_t a, uint64_t b) -> uint64_t { return pair_hash_fma(a, b, m30, m27, m31); };
+#else
+        auto hash2 = [&](uint64_t a, uint64_t b) -> uint64_t { return pair_hash(a, b); };
+#endif
         auto nkey = [&](uint64_t v) -> KT {
             if (K32) return (KT)((uint32_t)(v >> 32) | kmask);
             return PK ? (KT)(v >> pi.pw) : (KT)v;
@@ -688,8 +721,8 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                             const uint64_t ra = RK[ia], rb = RK[ib];
                             const uint64_t rpa = rpay_of(ra, ia), spa = PK ? (wa & pmask) : (va ? WP[ja] : 0);
                             const uint64_t rpb = rpay_of(rb, ib), spb = PK ? (wb & pmask) : (vb ? WP[jb] : 0);
-                            const uint64_t ha = decltype(SW)::value ? pair_hash(spa, rpa) : pair_hash(rpa, spa);
-                            const uint64_t hb = decltype(SW)::value ? pair_hash(spb, rpb) : pair_hash(rpb, spb);
+                            const uint64_t ha = decltype(SW)::value ? hash2(spa, rpa) : hash2(rpa, spa);
+                            const uint64_t hb = decltype(SW)::value ? hash2(spb, rpb) : hash2(rpb, spb);
                             const uint64_t sa = add_mask64(rpa, spa, ma), sb = add_mask64(rpb, spb, mb);
                             if (sa > best_t) best_t = sa;
                             if (sb > best_t) best_t = sb;

@@ -1068,8 +1068,13 @@ extern "C" int mpsm_sort_records(const uint64_t* in_rec, int64_t n, int width_bi
     cudaStream_t st = (cudaStream_t)stream;
     if (n < 0 || width_bits < 1 || width_bits > 63) return MPSM_ERR_ARG;
     if (n == 0) return MPSM_OK;
-    if (in_rec == out_rec || in_rec == tmp_rec || out_rec == tmp_rec) {
-        set_error("mpsm_sort_records: in, out and tmp must be distinct");
+    const Plan plan = make_plan(width_bits);
+    const int pw = 64 - width_bits;
+    const int P = plan.npasses;
+    // in place (in == out) with an even number of passes: the first pass
+    // writes tmp, the last one lands back in the input buffer
+    if (in_rec == tmp_rec || out_rec == tmp_rec || (in_rec == out_rec && P % 2 != 0)) {
+        set_error("mpsm_sort_records: in, out and tmp must be distinct (in == out only for an even pass count)");
         return MPSM_ERR_ARG;
     }
     Ws ws;
@@ -1077,9 +1082,6 @@ extern "C" int mpsm_sort_records(const uint64_t* in_rec, int64_t n, int width_bi
         set_error("sort workspace too small");
         return MPSM_ERR_ARG;
     }
-    const Plan plan = make_plan(width_bits);
-    const int pw = 64 - width_bits;
-    const int P = plan.npasses;
     const uint64_t* src = in_rec;
     for (int i = 0; i < P; ++i) {
         uint64_t* dst = ((P - 1 - i) % 2 == 0) ? out_rec : tmp_rec;

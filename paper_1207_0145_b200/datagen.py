@@ -12,7 +12,7 @@ bit-identical relations:
 * ``gen_skewed_8020`` -- restates the reference generator
   (datagen.py:65-84): 80 % of the keys uniform in the hot 20 % tail of the
   domain (high or low end), the rest uniform in the remainder.  Config 4 uses
-  R = low, S = high.  tests/test_host_logic.py checks it reproduces the
+  R = low, S = high.  tests/test_oracle_golden.py checks the oracle's copy reproduces the
   reference's arrays bit for bit (fingerprints in tests/golden/golden.json).
 * ``gen_uniform`` / ``gen_location_skew`` -- datagen.py:58-62, 87-105.
 """
@@ -121,6 +121,51 @@ def generate(spec: GenSpec) -> Relation:
         return gen_skewed_8020(spec.cardinality, spec.key_domain, "low", spec.seed)
     base = gen_uniform(spec.cardinality, spec.key_domain, spec.seed)
     return gen_location_skew(base, spec.location_threads, spec.seed)
+
+
+def fk_range_device(n_r: int, n_s: int, r_range: tuple, s_range: tuple, seed: int, device) -> tuple:
+    """Positions [r_range) of R and [s_range) of S of a counter-based FK
+    workload generated on the GPU (any range of any size, independently):
+    R keys are a bijective Feistel permutation of [0, n_r) (cycle walking)
+    plus 1, S keys splitmix64(seed, pos) mod n_r plus 1, payloads splitmix64
+    masked to 32 bits.  -> (R, S) Relations with CUDA uint64 columns."""
+    import math
+
+    import torch
+
+    def mix(x):
+        x = x + (0x9E3779B97F4A7C15 - (1 << 64))  # int64 arithmetic wraps
+        x = (x ^ (x >> 30).bitwise_and((1 << 34) - 1)) * -4658895280553007687  # 0xBF58476D1CE4E5B9
+        x = (x ^ (x >> 27).bitwise_and((1 << 37) - 1)) * -7723592293110705685  # 0x94D049BB133111EB
+        return x ^ (x >> 31).bitwise_and((1 << 33) - 1)
+
+    half = max(1, math.ceil(math.log2(max(n_r, 2)) / 2))
+    mask = (1 << half) - 1
+
+    def feistel(x):
+        l, r_ = x >> half, x & mask
+        for rnd in range(4):
+            l, r_ = r_, l ^ (mix(r_ + (seed * 4 + rnd) * 0x1000193) & mask)
+        return (l << half) | r_
+
+    ra, rb = r_range
+    sa, sb = s_range
+    pos = torch.arange(ra, rb, dtype=torch.int64, device=device)
+    k = feistel(pos)
+    while True:
+        bad = k >= n_r
+        if not bool(bad.any()):
+            break
+        k = torch.where(bad, feistel(k), k)
+    r_keys = (k + 1).view(torch.uint64)
+    r_pays = (mix(pos + (2 * seed + 11) * (1 << 40)) & 0xFFFFFFFF).view(torch.uint64)
+    del pos, k
+    spos = torch.arange(sa, sb, dtype=torch.int64, device=device)
+    hs = mix(spos + (2 * seed + 1) * (1 << 41))
+    s_keys = ((hs & 0x7FFFFFFFFFFFFFFF) % n_r + 1).view(torch.uint64)
+    del hs
+    s_pays = (mix(spos + (2 * seed + 13) * (1 << 42)) & 0xFFFFFFFF).view(torch.uint64)
+    return Relation(r_keys, r_pays), Relation(s_keys, s_pays)
 
 
 def gen_fk_device(n_r: int, n_s: int, seed: int = 0, device=None, rank: int = 0, world: int = 1) -> tuple:

@@ -443,47 +443,12 @@ def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=Non
 
 # ------------------------------------------------------------------ bench
 def fk_shard_device(n_r: int, n_s: int, rank: int, world: int, seed: int, device) -> tuple:
-    """Position-shard `rank` of a world-wide FK workload generated on the GPU.
-
-    Counter-based so a rank builds only its shard: R keys are a bijective
-    Feistel permutation of [0, n_r) (cycle walking) plus 1, S keys
-    splitmix64(seed, pos) mod n_r plus 1, payloads splitmix64 masked to 32
-    bits.  (The numpy generator of datagen.gen_fk needs the whole permutation
-    and is used at N=1.)
-    """
+    """Position-shard `rank` of a world-wide FK workload generated on the GPU
+    (datagen.fk_range_device): a rank builds only its shard."""
     from .core import chunk_bounds
+    from .datagen import fk_range_device
 
-    def mix(x):
-        x = x + (0x9E3779B97F4A7C15 - (1 << 64))  # int64 arithmetic wraps
-        x = (x ^ (x >> 30).bitwise_and((1 << 34) - 1)) * -4658895280553007687  # 0xBF58476D1CE4E5B9
-        x = (x ^ (x >> 27).bitwise_and((1 << 37) - 1)) * -7723592293110705685  # 0x94D049BB133111EB
-        return x ^ (x >> 31).bitwise_and((1 << 33) - 1)
-
-    ra, rb = chunk_bounds(n_r, world)[rank]
-    sa, sb = chunk_bounds(n_s, world)[rank]
-    half = max(1, math.ceil(math.log2(max(n_r, 2)) / 2))
-    mask = (1 << half) - 1
-
-    def feistel(x):
-        l, r_ = x >> half, x & mask
-        for rnd in range(4):
-            l, r_ = r_, l ^ (mix(r_ + (seed * 4 + rnd) * 0x1000193) & mask)
-        return (l << half) | r_
-
-    pos = torch.arange(ra, rb, dtype=torch.int64, device=device)
-    k = feistel(pos)
-    while True:
-        bad = k >= n_r
-        if not bool(bad.any()):
-            break
-        k = torch.where(bad, feistel(k), k)
-    r_keys = (k + 1).view(torch.uint64)
-    r_pays = (mix(pos + (2 * seed + 11) * (1 << 40)) & 0xFFFFFFFF).view(torch.uint64)
-    spos = torch.arange(sa, sb, dtype=torch.int64, device=device)
-    hs = mix(spos + (2 * seed + 1) * (1 << 41))
-    s_keys = ((hs & 0x7FFFFFFFFFFFFFFF) % n_r + 1).view(torch.uint64)
-    s_pays = (mix(spos + (2 * seed + 13) * (1 << 42)) & 0xFFFFFFFF).view(torch.uint64)
-    return Relation(r_keys, r_pays), Relation(s_keys, s_pays)
+    return fk_range_device(n_r, n_s, chunk_bounds(n_r, world)[rank], chunk_bounds(n_s, world)[rank], seed, device)
 
 
 def bench_main(args, metric, configs, make_inputs, Clocks, run_reference_sample):

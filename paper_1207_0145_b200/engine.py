@@ -48,6 +48,7 @@ from .core import (
     JoinResult,
     KeyDomain,
     MaterializeCapExceeded,
+    PackedRelation,
     Relation,
     Run,
     WorkerStats,
@@ -184,7 +185,7 @@ def _prepare(r: Relation, s: Relation, cfg: JoinConfig):
 def _domain_report(rel: Relation, dom: KeyDomain) -> tuple:
     """(violations, first index) of one relation: on the GPU for device
     columns, numpy for host columns (the error path only)"""
-    if rel.cardinality == 0:
+    if rel.cardinality == 0 or isinstance(rel, PackedRelation):  # records were validated when packed
         return 0, -1
     keys = rel.keys
     if isinstance(keys, torch.Tensor) and keys.is_cuda:
@@ -244,6 +245,15 @@ class JoinContext:
         self.variant = variant
         self.wbits = self.dom.width_bits
         self.packed = bool(packed) and 1 <= self.wbits <= 63
+        for rel in (r, s):
+            if isinstance(rel, PackedRelation):
+                if rel.key_domain != self.dom:
+                    raise ConfigurationError("a PackedRelation's key domain must be the join's key domain")
+                if not self.packed:
+                    raise ConfigurationError("PackedRelation inputs need the packed record layout (MPSM_PACK=1)")
+        # record inputs sorted in place (even pass count: the last pass lands
+        # back in the input buffer)
+        self._inplace = _lib.load().mpsm_sort_pass_count(self.wbits) % 2 == 0
         self.pw = 64 - self.wbits
         self.span_m1 = self.dom.upper - self.dom.lower - 1
         # the private side is sorted whole (P-MPSM) or per chunk (B-MPSM);
@@ -251,11 +261,12 @@ class JoinContext:
         # that upload overlaps the public sort
         self._private = private
         self.priv_rec = None
-        self.n_priv = int(private.keys.shape[0]) if hasattr(private.keys, "shape") else len(private.keys)
+        self.n_priv = private.cardinality
         # the private upload buffer is allocated now, before the public sort is
         # queued: its copies then need not wait for that sort
         self._priv_buf = self._priv_ready = None
-        if self.packed and HOST_PACK and D.host_columns(private.keys) is not None:
+        if self.packed and HOST_PACK and not isinstance(private, PackedRelation) \
+                and D.host_columns(private.keys) is not None:
             self._priv_buf = torch.empty(self.n_priv, dtype=torch.uint64, device=self.dev)
             self._priv_ready = torch.cuda.Event()
             self._priv_ready.record()
@@ -287,6 +298,8 @@ class JoinContext:
 
     def _upload(self, rel: Relation, allowed: bool, gpu_pack_every: int = -1, buf=None, ready=None):
         """host columns -> packed records on the device, or None (columns path)"""
+        if isinstance(rel, PackedRelation):
+            return rel.records
         if not (allowed and self.packed and HOST_PACK):
             return None
         hk, hp = D.host_columns(rel.keys), D.host_columns(rel.payloads)
@@ -344,10 +357,17 @@ class JoinContext:
             D.sort_pairs(in_k, in_p, self.dom.lower, self.span_m1, self.wbits, ok, op, tmp[0][:n], tmp[1][:n], bad)
         return (ok, op)
 
+    def _store_for(self, rel, rec, n: int) -> tuple:
+        """where the runs of a side go: in place for consumed record inputs"""
+        if isinstance(rel, PackedRelation) and self._inplace:
+            return (rec, None)
+        return self._alloc_runs(n)
+
     def sort_public(self):
         """phase 1: every public chunk -> sorted run (engine.py:389-395)."""
         self._tmp(max((b - a for a, b in self.pub_chunks), default=0))
-        self.pub_store = self._alloc_runs(self.n_pub)
+        public = self.s if self.roles.private == "r" else self.r
+        self.pub_store = self._store_for(public, self.pub_rec, self.n_pub)
         self.pub_runs = []
         for i, (a, b) in enumerate(self.pub_chunks):
             self._hook(i, "sort_public")
@@ -363,9 +383,12 @@ class JoinContext:
             return self._sort_into(self.priv_rec[a:b], None, self.priv_store, a, b, self.bad_priv)
         return self._sort_into(self.priv_k[a:b], self.priv_p[a:b], self.priv_store, a, b, self.bad_priv)
 
+    def _private_rel(self):
+        return self.r if self.roles.private == "r" else self.s
+
     def sort_private_chunks(self):
         """B-MPSM phase 2: each private chunk sorted into its run (engine.py:297-309)."""
-        self.priv_store = self._alloc_runs(self.n_priv)
+        self.priv_store = self._store_for(self._private_rel(), self.priv_rec, self.n_priv)
         self.priv_runs = []
         for i, (a, b) in enumerate(self.priv_chunks):
             self._hook(i, "sort_private")
@@ -374,7 +397,7 @@ class JoinContext:
 
     def sort_private_whole(self):
         """P-MPSM: the whole private input -> one sorted run (cut by partition())."""
-        self.priv_store = self._alloc_runs(self.n_priv)
+        self.priv_store = self._store_for(self._private_rel(), self.priv_rec, self.n_priv)
         self.priv_whole = self._sort_private_range(0, self.n_priv)
 
     def _public_bound_keys(self, f: int) -> np.ndarray:
@@ -600,6 +623,8 @@ def run_hash_oracle(r: Relation, s: Relation, cfg: JoinConfig) -> JoinResult:
     >= 2^63 rejected with ValueError.  The build and probe sides are sorted
     by the run sort over all 64 key bits and joined by the merge kernel (the
     same COUNT / MAX / checksum; pair order is key order, not probe order)."""
+    if isinstance(r, PackedRelation) or isinstance(s, PackedRelation):
+        raise ConfigurationError("algorithm 'hash-oracle' joins Relations (keys and payloads), not PackedRelations")
     for name, rel in (("r", r), ("s", s)):
         if not _payloads_below_2_63(rel):
             raise ValueError(f"relation {name} has payloads >= 2^63; aggregate undefined")

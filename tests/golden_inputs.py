@@ -2,7 +2,7 @@
 
 The recipes mirror tests/golden/make_golden.py but depend only on numpy and
 this repo (the reference is not present on the GPU box).  Skewed inputs come
-from the product's restated generator; test_host_logic checks its arrays'
+from the product's restated generator; test_oracle_golden checks its arrays'
 fingerprints against the reference's.
 """
 

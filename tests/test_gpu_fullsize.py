@@ -1,24 +1,25 @@
-"""Parity at BASELINE.json's full sizes (opt-in: MPSM_FULLSIZE=1; minutes and up
-to ~120 GB of HBM).
+"""Parity at BASELINE.json's full sizes, every config (part of ``-m gpu``).
 
 The CPU oracle cannot join billions of tuples in test time, so at full size
-the GPU join is checked against an independent plain-PyTorch computation of
-the same three outputs on the same device (COUNT, MAX(r.payload + s.payload)
-and the splitmix64 checksum of SURVEY.md 8(a) a13), written with torch
-gathers / sorts / searchsorted -- none of this package's kernels:
+the GPU join is checked against the independent plain-PyTorch computation of
+the same three outputs in tests/torch_check.py (COUNT, MAX(r.payload +
+s.payload), the splitmix64 checksum of SURVEY.md 8(a) a13 -- torch gathers /
+sorts / searchsorted, none of this package's kernels), itself pinned to the
+CPU oracle by ``test_torch_checksum_matches_the_oracle_definition``:
 
-* FK configs (2 and 3 at multiplicity 16): R keys are a permutation, so the
-  match of every S tuple is lookup[s.key] (the oracle's FK gather, done on the
-  GPU); cfg2 also against the committed golden (the reference's count/max).
-* config 4 (negatively correlated skew, duplicates on both sides): R sorted by
-  torch.sort, every S tuple's equal-key R range by searchsorted, the pairs
-  enumerated with repeat_interleave.
-
-``tools/fullsize_parity.sh`` runs this module on the GPU box; its log is kept
-under profiles/.
+* config 2 (100M x 400M FK, numpy PCG64 seed 0): also the committed golden
+  (the reference's own count / max);
+* config 3 (|R| = 200M, |S| = 1x, 4x, 8x, 16x |R|, up to 3.4G tuples / 54 GB):
+  the counter-based FK generator on the device;
+* config 4 (400M x 1.6B, negatively correlated 80-20 skew, 32-bit keys,
+  duplicates on both sides; numpy generator of the reference's datagen);
+* config 5 (1.6B x 6.4B FK, 8G tuples): its 16-B columns (128 GB) plus runs
+  do not fit one B200, so the relations are generated chunk by chunk
+  straight into packed 8-B records (PackedRelation, 64 GB) and joined on one
+  GPU; the checker sees the same chunks.  The multi-GPU engine runs this
+  config sharded over 2-8 GPUs (distributed.py); the join result does not
+  depend on the GPU count.
 """
-
-import os
 
 import numpy as np
 import pytest
@@ -28,93 +29,26 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 if not torch.cuda.is_available():  # pragma: no cover - collected on CPU boxes too
     pytest.skip("needs a CUDA device", allow_module_level=True)
-if os.environ.get("MPSM_FULLSIZE") != "1":
-    pytest.skip("full BASELINE sizes: set MPSM_FULLSIZE=1 (minutes, up to ~120 GB of HBM)", allow_module_level=True)
 
 import paper_1207_0145_b200 as P  # noqa: E402
 from paper_1207_0145_b200 import datagen  # noqa: E402
-from paper_1207_0145_b200.core import JoinConfig, KeyDomain, Relation  # noqa: E402
+from paper_1207_0145_b200 import device as D  # noqa: E402
+from paper_1207_0145_b200.core import JoinConfig, KeyDomain, PackedRelation, Relation  # noqa: E402
+from tests import torch_check as tc  # noqa: E402
 
 DEV = torch.device("cuda", 0)
-M64 = (1 << 64) - 1
 
 
-def _s64(c: int) -> int:
-    return c - (1 << 64) if c >= 1 << 63 else c
-
-
-C0, C1, C2 = _s64(0x9E3779B97F4A7C15), _s64(0xBF58476D1CE4E5B9), _s64(0x94D049BB133111EB)
-
-
-def _lsr(z, k):
-    """logical right shift of int64 tensors"""
-    return torch.bitwise_and(torch.bitwise_right_shift(z, k), (1 << (64 - k)) - 1)
-
-
-def _pair_hash(rp, sp):
-    """splitmix64(r ^ rotl64(s, 17)) in wrapping int64 arithmetic"""
-    x = torch.bitwise_xor(rp, torch.bitwise_or(torch.bitwise_left_shift(sp, 17), _lsr(sp, 47)))
-    z = x + C0
-    z = torch.bitwise_xor(z, _lsr(z, 30)) * C1
-    z = torch.bitwise_xor(z, _lsr(z, 27)) * C2
-    return torch.bitwise_xor(z, _lsr(z, 31))
-
-
-class _Acc:
-    def __init__(self):
-        self.count, self.best, self.csum = 0, None, 0
-
-    def add(self, rp, sp):
-        if rp.numel() == 0:
-            return
-        self.count += int(rp.numel())
-        b = int((rp + sp).max().item())  # payloads < 2^32: the sum fits int64
-        self.best = b if self.best is None or b > self.best else self.best
-        self.csum = (self.csum + int(_pair_hash(rp, sp).sum().item())) & M64
-
-    def result(self):
-        return self.count, self.best, self.csum
-
-
-def _torch_fk(r, s, chunk=1 << 28):
-    rk, rp = r.keys.view(torch.int64), r.payloads.view(torch.int64)
-    lookup = torch.zeros(int(rk.max().item()) + 1, dtype=torch.int64, device=DEV)
-    lookup[rk] = rp
-    acc = _Acc()
-    sk, sp = s.keys.view(torch.int64), s.payloads.view(torch.int64)
-    for a in range(0, sk.numel(), chunk):
-        acc.add(lookup[sk[a:a + chunk]], sp[a:a + chunk])
-    return acc.result()
-
-
-def _torch_join(r, s, chunk=1 << 27):
-    """general equi-join (duplicates on both sides) by sort + searchsorted"""
-    rk, order = torch.sort(r.keys.view(torch.int64))
-    rp = r.payloads.view(torch.int64)[order]
-    del order
-    acc = _Acc()
-    sk_all, sp_all = s.keys.view(torch.int64), s.payloads.view(torch.int64)
-    for a in range(0, sk_all.numel(), chunk):
-        sk, sp = sk_all[a:a + chunk], sp_all[a:a + chunk]
-        lo = torch.searchsorted(rk, sk, right=False)
-        cnt = torch.searchsorted(rk, sk, right=True) - lo
-        hit = cnt > 0
-        lo, cnt, spm = lo[hit], cnt[hit], sp[hit]
-        if cnt.numel() == 0:
-            continue
-        total = int(cnt.sum().item())
-        start = torch.cumsum(cnt, 0) - cnt  # first pair of each S tuple
-        s_of = torch.repeat_interleave(torch.arange(cnt.numel(), device=DEV), cnt, output_size=total)
-        r_idx = lo[s_of] + (torch.arange(total, device=DEV) - start[s_of])
-        acc.add(rp[r_idx], spm[s_of])
-    return acc.result()
-
-
-def _ours(r, s, dom):
-    res = P.run_join(r, s, JoinConfig(threads=1, algorithm="p-mpsm", key_domain=dom))
-    out = (res.match_count, res.aggregate_max, res.checksum)
+@pytest.fixture(autouse=True)
+def _free_hbm():
     torch.cuda.empty_cache()
-    return out
+    yield
+    torch.cuda.empty_cache()
+
+
+def _ours(r, s, dom, threads=1):
+    res = P.run_join(r, s, JoinConfig(threads=threads, algorithm="p-mpsm", key_domain=dom))
+    return res.match_count, res.aggregate_max, res.checksum
 
 
 def _to_dev(rel):
@@ -127,15 +61,17 @@ def test_cfg2_full_size_vs_torch_and_golden():
     del r, s
     ours = _ours(rd, sd, dom)
     assert ours == (400_000_000, 8_589_753_492, 0xAA48801BE88FA31B)  # tests/golden/golden.json cfg2
-    assert ours == _torch_fk(rd, sd)
+    assert ours == tc.fk_join(rd, sd)
 
 
-def test_cfg3_multiplicity16_full_size_vs_torch():
-    # |R| = 200M, |S| = 3.2B (54 GB of input); counter-based generator on the device
-    r, s, dom = datagen.gen_fk_device(200_000_000, 3_200_000_000, seed=3, device=DEV)
+@pytest.mark.parametrize("mult", [1, 4, 8, 16])
+def test_cfg3_multiplicity_full_size_vs_torch(mult):
+    # |R| = 200M, |S| = mult x |R| (16: 3.2B, 54 GB of input); counter-based generator on the device
+    n_r = 200_000_000
+    r, s, dom = datagen.gen_fk_device(n_r, mult * n_r, seed=3, device=DEV)
     ours = _ours(r, s, dom)
-    want = _torch_fk(r, s)
-    assert want[0] == 3_200_000_000
+    want = tc.fk_join(r, s)
+    assert want[0] == mult * n_r
     assert ours == want
 
 
@@ -145,10 +81,73 @@ def test_cfg4_negcorr_skew_full_size_vs_torch():
     rd, sd = _to_dev(r), _to_dev(s)
     del r, s
     ours = _ours(rd, sd, dom)
-    want = _torch_join(rd, sd)
+    want = tc.general_join(rd, sd)
     # E[matches] = 0.35 |R||S| / (0.8 (2^32 - 1)) ~ 6.52e7
     assert 6.0e7 < want[0] < 7.0e7
     assert ours == want
+
+
+def _packed_fk(n_r, n_s, seed, chunk=1 << 28):
+    """cfg5-sized FK relations generated chunk-wise into packed records, with
+    the torch checker fed the same chunks: -> (R, S PackedRelations, dom, want)"""
+    dom = KeyDomain(1, n_r + 1)
+    w = dom.width_bits
+    span_m1 = dom.upper - dom.lower - 1
+    bad = D.new_bad_flag(DEV)
+    ovf = torch.zeros(1, dtype=torch.int32, device=DEV)
+    r_rec = torch.empty(n_r, dtype=torch.uint64, device=DEV)
+    lookup = torch.zeros(n_r + 1, dtype=torch.int64, device=DEV)
+    for a in range(0, n_r, chunk):
+        b = min(n_r, a + chunk)
+        r, _ = datagen.fk_range_device(n_r, n_s, (a, b), (0, 0), seed, DEV)
+        lookup[r.keys.view(torch.int64)] = r.payloads.view(torch.int64)
+        D.pack_records(r.keys, r.payloads, dom.lower, span_m1, w, r_rec[a:b], bad, ovf)
+        del r
+    s_rec = torch.empty(n_s, dtype=torch.uint64, device=DEV)
+    acc = tc.Acc()
+    for a in range(0, n_s, chunk):
+        b = min(n_s, a + chunk)
+        _, s = datagen.fk_range_device(n_r, n_s, (0, 0), (a, b), seed, DEV)
+        tc.fk_add(acc, lookup, s.keys, s.payloads)
+        D.pack_records(s.keys, s.payloads, dom.lower, span_m1, w, s_rec[a:b], bad, ovf)
+        del s
+    del lookup
+    assert int(bad.item()) == -1 and int(ovf.item()) == 0
+    return PackedRelation(r_rec, dom), PackedRelation(s_rec, dom), dom, acc.result()
+
+
+def test_cfg5_full_size_one_gpu_packed_vs_torch():
+    # BASELINE configs[4]: |R| = 1.6B, |S| = 6.4B (8G tuples); 64 GB of packed records
+    r, s, dom, want = _packed_fk(1_600_000_000, 6_400_000_000, seed=5)
+    assert want[0] == 6_400_000_000
+    ours = _ours(r, s, dom)
+    assert ours == want
+
+
+def test_packed_relation_matches_columns():
+    """PackedRelation inputs give the column path's results and statistics
+    (T = 1 and T = 3, both engines)"""
+    r, s, dom, want = _packed_fk(3_000_000, 12_000_000, seed=9, chunk=1 << 20)
+    pw = 64 - dom.width_bits
+
+    def unpack(rec):
+        v = rec.view(torch.int64)
+        return Relation((tc._lsr(v, pw) + dom.lower).view(torch.uint64), (v & ((1 << pw) - 1)).view(torch.uint64))
+
+    cols = (unpack(r.records), unpack(s.records))
+    for algo in ("p-mpsm", "b-mpsm"):
+        for t in (1, 3):
+            cfg = JoinConfig(threads=t, algorithm=algo, key_domain=dom)
+            a = P.run_join(*cols, cfg)
+            pr = PackedRelation(r.records.clone(), dom)
+            ps = PackedRelation(s.records.clone(), dom)
+            b = P.run_join(pr, ps, cfg)
+            assert (a.match_count, a.aggregate_max, a.checksum) == want
+            assert (b.match_count, b.aggregate_max, b.checksum) == want
+            def stats(res):
+                return [{k: v for k, v in vars(x).items() if not k.endswith("_seconds")} for x in res.worker_stats]
+
+            assert stats(a) == stats(b)
 
 
 def test_torch_checksum_matches_the_oracle_definition():
@@ -164,5 +163,5 @@ def test_torch_checksum_matches_the_oracle_definition():
     want = orc.join(rk, rp, sk, sp, threads=1, lower=1, upper=n + 1)
     r = Relation(torch.from_numpy(rk).to(DEV), torch.from_numpy(rp).to(DEV))
     s = Relation(torch.from_numpy(sk).to(DEV), torch.from_numpy(sp).to(DEV))
-    assert _torch_fk(r, s) == (want.match_count, want.aggregate_max, want.checksum)
-    assert _torch_join(r, s) == (want.match_count, want.aggregate_max, want.checksum)
+    assert tc.fk_join(r, s) == (want.match_count, want.aggregate_max, want.checksum)
+    assert tc.general_join(r, s) == (want.match_count, want.aggregate_max, want.checksum)
