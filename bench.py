@@ -481,6 +481,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--threads", type=int, default=1, help="logical workers T (JoinConfig.threads)")
+    ap.add_argument("--dist-config", default=None, choices=["cfg5", "cfg4", "cfg2"],
+                    help="multi-GPU workload (torchrun, N>1): cfg5 (default), cfg4, cfg2 per GPU")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -816,23 +816,31 @@ __global__ void k_probe_lane_order(int* bad) {
     }
 }
 
+// probed once per device (the merge-join's Run order check catches a pass
+// that came out unstable anyway: InternalConsistencyError, not a silent miss)
 static bool lane_ordered_atomics() {
-    static int state = -1;
-    if (state < 0) {
+    constexpr int MAXDEV = 64;
+    static std::atomic<int> state[MAXDEV];  // 0 unknown, 1 ordered, 2 not
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= MAXDEV) return false;
+    int s = state[dev].load();
+    if (s == 0) {
         int* d = nullptr;
         int bad = 1;
         if (cudaMalloc(&d, sizeof(int)) == cudaSuccess) {
             cudaMemset(d, 0, sizeof(int));
-            k_probe_lane_order<<<148, 256>>>(d);
+            k_probe_lane_order<<<num_sms(), 256>>>(d);
             cudaMemcpy(&bad, d, sizeof(int), cudaMemcpyDeviceToHost);
             cudaFree(d);
         }
-        state = (bad == 0 && cudaGetLastError() == cudaSuccess) ? 1 : 0;
+        s = (bad == 0 && cudaGetLastError() == cudaSuccess) ? 1 : 2;
         // MPSM_SEG_BALLOT_RANK=1 forces the ballot ranking (tests of the fallback)
         const char* force = getenv("MPSM_SEG_BALLOT_RANK");
-        if (force && force[0] == '1') state = 0;
+        if (force && force[0] == '1') s = 2;
+        state[dev].store(s);
     }
-    return state == 1;
+    return s == 1;
 }
 
 extern "C" int mpsm_dbg_lane_ordered() { return lane_ordered_atomics() ? 1 : 0; }

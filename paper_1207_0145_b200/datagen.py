@@ -168,6 +168,71 @@ def fk_range_device(n_r: int, n_s: int, r_range: tuple, s_range: tuple, seed: in
     return Relation(r_keys, r_pays), Relation(s_keys, s_pays)
 
 
+def fk_shard_chunked(n_r: int, n_s: int, rank: int, world: int, seed: int, device, chunk: int = 1 << 27) -> tuple:
+    """Position-shard `rank` of `world` of the counter-based FK workload
+    (fk_range_device), generated chunk by chunk into preallocated columns so
+    the generator's temporaries stay small (config 5: 6.4G S tuples)."""
+    import torch
+
+    from .core import chunk_bounds
+
+    (ra, rb), (sa, sb) = chunk_bounds(n_r, world)[rank], chunk_bounds(n_s, world)[rank]
+    cols = [torch.empty(n, dtype=torch.uint64, device=device) for n in (rb - ra, rb - ra, sb - sa, sb - sa)]
+    for a in range(ra, rb, chunk):
+        b = min(rb, a + chunk)
+        r, _ = fk_range_device(n_r, n_s, (a, b), (0, 0), seed, device)
+        cols[0][a - ra:b - ra].copy_(r.keys)
+        cols[1][a - ra:b - ra].copy_(r.payloads)
+    for a in range(sa, sb, chunk):
+        b = min(sb, a + chunk)
+        _, s = fk_range_device(n_r, n_s, (0, 0), (a, b), seed, device)
+        cols[2][a - sa:b - sa].copy_(s.keys)
+        cols[3][a - sa:b - sa].copy_(s.payloads)
+    return Relation(cols[0], cols[1]), Relation(cols[2], cols[3])
+
+
+def skewed_8020_range_device(n: int, dom: KeyDomain, direction: str, pos_range: tuple, seed: int, device,
+                             chunk: int = 1 << 27) -> Relation:
+    """Positions [pos_range) of an 80-20 skewed relation generated on the GPU
+    (counter-based, any range independently): the distribution of
+    gen_skewed_8020 / the reference's datagen.py:65-84 (80 % of the keys
+    uniform in the hot 20 % tail of the domain, high or low end, the rest
+    uniform in the remainder, payloads uniform 32-bit), not its numpy stream.
+    The multi-GPU bench builds config 4 shards with it."""
+    import torch
+
+    if direction not in ("high", "low"):
+        raise ConfigurationError("direction must be 'high' or 'low'")
+    M = 0x7FFFFFFFFFFFFFFF
+
+    def mix(x):
+        x = x + (0x9E3779B97F4A7C15 - (1 << 64))
+        x = (x ^ (x >> 30).bitwise_and((1 << 34) - 1)) * -4658895280553007687
+        x = (x ^ (x >> 27).bitwise_and((1 << 37) - 1)) * -7723592293110705685
+        return x ^ (x >> 31).bitwise_and((1 << 33) - 1)
+
+    w = dom.width
+    if direction == "high":
+        cut = dom.lower + (w * 4) // 5
+        hot_lo, hot_n, cold_lo, cold_n = cut, dom.upper - cut, dom.lower, cut - dom.lower
+    else:
+        edge = dom.lower + w - (w * 4) // 5
+        hot_lo, hot_n, cold_lo, cold_n = dom.lower, edge - dom.lower, edge, dom.upper - edge
+    a0, b0 = pos_range
+    keys = torch.empty(b0 - a0, dtype=torch.uint64, device=device)
+    pays = torch.empty(b0 - a0, dtype=torch.uint64, device=device)
+    for a in range(a0, b0, chunk):
+        b = min(b0, a + chunk)
+        pos = torch.arange(a, b, dtype=torch.int64, device=device)
+        u = mix(pos + (3 * seed + 1) * (1 << 40)) & M
+        hot = (u % 1000) < 800
+        v = mix(pos + (3 * seed + 2) * (1 << 41)) & M
+        k = torch.where(hot, hot_lo + v % hot_n, cold_lo + v % max(cold_n, 1))
+        keys[a - a0:b - a0].copy_(k.view(torch.uint64))
+        pays[a - a0:b - a0].copy_((mix(pos + (3 * seed + 3) * (1 << 42)) & 0xFFFFFFFF).view(torch.uint64))
+    return Relation(keys, pays)
+
+
 def gen_fk_device(n_r: int, n_s: int, seed: int = 0, device=None, rank: int = 0, world: int = 1) -> tuple:
     """FK workload generated on the GPU (counter-based; a rank builds only its
     position shard): -> (R, S, KeyDomain) with CUDA uint64 columns.  Not the

@@ -42,6 +42,7 @@ from . import device as D
 from .core import (
     ConfigurationError,
     DomainError,
+    InternalConsistencyError,
     JoinConfig,
     JoinResult,
     MaterializeCapExceeded,
@@ -69,7 +70,13 @@ class PeerRun:
         return self.n
 
 
-_IPC_BLOCKS: dict = {}  # (device index, handle bytes) -> mapped block base, open once per process
+# mappings of peer ranks' public runs: (device, peer) -> (handle bytes, base).
+# A peer names its public run by the cudaMalloc block holding it; it keeps
+# that block alive (CudaBackend's persistent public store) and only retires
+# it after the final collective of a join in which every importer has seen
+# the new handle -- an importer closes the old mapping the moment a peer's
+# handle changes, so no block is freed while mapped (CUDA IPC forbids that).
+_IPC_PEERS: dict = {}
 
 
 def ipc_share(t: torch.Tensor) -> tuple:
@@ -82,18 +89,34 @@ def ipc_share(t: torch.Tensor) -> tuple:
     return bytes(h), int(off.value), int(t.numel())
 
 
-def ipc_open(shared: tuple, device) -> PeerRun:
-    """map a peer's tensor into the current device (cached per block)"""
+def ipc_open(shared: tuple, device, peer: int = -1) -> PeerRun:
+    """map a peer's tensor into the current device; one mapping per peer,
+    replaced (old one closed) when the peer's block changes"""
     import ctypes
 
     handle, off, n = shared
-    key = (torch.cuda.current_device(), handle)
-    if key not in _IPC_BLOCKS:
+    key = (torch.cuda.current_device(), peer if peer >= 0 else handle)
+    cached = _IPC_PEERS.get(key)
+    if cached is None or cached[0] != handle:
+        if cached is not None:
+            _lib.check(_lib.load().mpsm_ipc_close_handle(ctypes.c_void_p(cached[1])), "mpsm_ipc_close_handle")
+            del _IPC_PEERS[key]
         p = ctypes.c_void_p()
         buf = (ctypes.c_char * 64).from_buffer_copy(handle)
         _lib.check(_lib.load().mpsm_ipc_open_handle(buf, ctypes.byref(p)), "mpsm_ipc_open_handle")
-        _IPC_BLOCKS[key] = int(p.value)
-    return PeerRun(_IPC_BLOCKS[key] + off, n, device)
+        _IPC_PEERS[key] = (handle, int(p.value))
+    return PeerRun(_IPC_PEERS[key][1] + off, n, device)
+
+
+def ipc_close_all() -> None:
+    """close every peer mapping of this process (after the last join of a
+    process group, before it is destroyed)"""
+    import ctypes
+
+    torch.cuda.synchronize()
+    for key, (_, base) in list(_IPC_PEERS.items()):
+        _lib.check(_lib.load().mpsm_ipc_close_handle(ctypes.c_void_p(base)), "mpsm_ipc_close_handle")
+        del _IPC_PEERS[key]
 
 
 class CudaBackend:
@@ -106,6 +129,41 @@ class CudaBackend:
         # where the all-to-all buffers live: the GPU (NCCL), or the host for a
         # CPU process group (gloo; tests run several ranks on one GPU)
         self.comm_device = comm_device if comm_device is not None else self.dev
+        # the public run lives in a grow-only store the backend owns: peers map
+        # its block (CUDA IPC), so it must outlive their mappings (see _IPC_PEERS)
+        self._pub = None
+        self._retired = []
+
+    def unpacked(self):
+        return type(self)(device=self.dev, packed=False, comm_device=self.comm_device)
+
+    def _public_out(self, n: int) -> torch.Tensor:
+        if self._pub is None or self._pub.numel() < n:
+            if self._pub is not None:
+                self._retired.append(self._pub)  # released after this join's last collective
+            self._pub = torch.empty(max(n, 1), dtype=torch.uint64, device=self.dev)
+        return self._pub[:n]
+
+    def release(self) -> None:
+        """after a join's final collective: every importer has switched to the
+        current public store, the retired ones can go"""
+        self._retired.clear()
+
+    def upload(self, rel):
+        """host columns of a packed join -> 8-B records on the device (half the
+        PCIe bytes, device.upload_records); None for device columns or pairs"""
+        if not (self.packed and HOST_PACK):
+            return None
+        hk, hp = D.host_columns(rel.keys), D.host_columns(rel.payloads)
+        if hk is None or hp is None:
+            return None
+        rec = self.empty(int(hk[0].shape[0]))
+        bad, ovf = D.upload_records(hk[0], hp[0], self.dom.lower, self.span_m1, self.wbits, rec)
+        if bad >= 0:
+            self.bad.fill_(bad)
+        if ovf:
+            self.overflow.fill_(1)
+        return rec
 
     def setup(self, dom):
         self.dom = dom
@@ -122,14 +180,18 @@ class CudaBackend:
     def empty(self, n: int) -> torch.Tensor:
         return torch.empty(n, dtype=torch.uint64, device=self.dev)
 
-    def sort(self, k, p):
+    def sort(self, k, p, public: bool = False):
         n = int(k.numel())
         if self.packed:
-            out, tmp = self.empty(n), self.empty(n)
-            D.sort_packed(k, p, self.dom.lower, self.span_m1, self.wbits, out, tmp, self.bad, self.overflow)
+            out = self._public_out(n) if public else self.empty(n)
+            D.sort_packed(k, p, self.dom.lower, self.span_m1, self.wbits, out, self.empty(n), self.bad, self.overflow)
             return (out, None)
-        ok, op, tk, tp = self.empty(n), self.empty(n), self.empty(n), self.empty(n)
-        D.sort_pairs(k, p, self.dom.lower, self.span_m1, self.wbits, ok, op, tk, tp, self.bad)
+        if public:  # pairs: keys and payloads in one store block
+            st = self._public_out(2 * n)
+            ok, op = st[:n], st[n:]
+        else:
+            ok, op = self.empty(n), self.empty(n)
+        D.sort_pairs(k, p, self.dom.lower, self.span_m1, self.wbits, ok, op, self.empty(n), self.empty(n), self.bad)
         return (ok, op)
 
     def histogram_async(self, keys, shift: int, nb: int) -> torch.Tensor:
@@ -170,10 +232,10 @@ class CudaBackend:
                             self.overflow)
         return rec
 
-    def sort_records(self, rec):
+    def sort_records(self, rec, public: bool = False):
         n = int(rec.numel())
-        out, tmp = self.empty(n), self.empty(n)
-        D.sort_records(rec, self.wbits, out, tmp)
+        out = self._public_out(n) if public else self.empty(n)
+        D.sort_records(rec, self.wbits, out, self.empty(n))
         return (out, None)
 
     def bad_index(self) -> int:
@@ -186,9 +248,9 @@ class CudaBackend:
         """CUDA IPC description of a run, for peer ranks (mpsm_ipc_get_handle)."""
         return [None if t is None else ((b"", 0, 0) if t.numel() == 0 else ipc_share(t)) for t in run]
 
-    def open(self, shared):
+    def open(self, shared, peer: int = -1):
         """a peer's run mapped into this rank's device (lazy NVLink peer access)"""
-        return tuple(None if s is None else (PeerRun(0, 0, self.dev) if s[2] == 0 else ipc_open(s, self.dev))
+        return tuple(None if s is None else (PeerRun(0, 0, self.dev) if s[2] == 0 else ipc_open(s, self.dev, peer))
                      for s in shared)
 
     def join(self, priv_runs, pub_runs, swap: bool, mode: int, out=None, cap: int = 0) -> torch.Tensor:
@@ -259,6 +321,71 @@ def _gather_obj(obj, group):
     return out
 
 
+class _Guard:
+    """Failure protocol between the collectives of one join.
+
+    A rank whose local work raises does not skip ahead: it enters the next
+    collective of the protocol with a failure flag (appended to the vector
+    every rank gathers there, or a one-word MAX all-reduce before the
+    variable-size all-to-all), and then every rank raises at that same point
+    -- the failing rank its own exception, the root cause, the others a
+    RuntimeError naming it (the reference prefers the root cause over the
+    broken-barrier noise of its worker threads, engine.py:440-453).  No rank
+    blocks on a peer that has already given up; a peer that dies outright is
+    caught by the process group's timeout (init_process_group(timeout=...))."""
+
+    def __init__(self, group, cdev):
+        self.group, self.cdev = group, cdev
+        self.err: Optional[BaseException] = None
+
+    def call(self, fn, *args, **kw):
+        if self.err is not None:
+            return None
+        try:
+            return fn(*args, **kw)
+        except Exception as exc:  # noqa: BLE001 - re-raised at the next collective
+            self.err = exc
+            return None
+
+    def _raise(self, flags) -> None:
+        bad = [int(i) for i in np.flatnonzero(np.asarray(flags))]
+        if bad:
+            if self.err is not None:
+                raise self.err
+            raise RuntimeError(f"distributed join: rank(s) {bad} failed before this collective "
+                               "(their own exception is the root cause)")
+        if self.err is not None:  # world of one, no collective
+            raise self.err
+
+    def gather(self, vec, length: int) -> np.ndarray:
+        """_gather_u64 of a fixed-length vector plus this rank's status -> [G, length]"""
+        v = np.zeros(length + 1, np.uint64)
+        if self.err is None and vec is not None:
+            v[:length] = np.asarray(vec, np.uint64)
+        v[length] = 0 if self.err is None else 1
+        allv = _gather_u64(v, self.group, self.cdev)
+        self._raise(allv[:, length])
+        return allv[:, :length]
+
+    def gather_obj(self, obj) -> list:
+        out = _gather_obj((self.err is not None, None if self.err is not None else obj), self.group)
+        self._raise([x[0] for x in out])
+        return [x[1] for x in out]
+
+    def check(self) -> None:
+        """a status-only collective (MAX all-reduce of one word)"""
+        if dist.get_world_size(self.group) == 1:
+            self._raise([0])
+            return
+        t = torch.tensor([0 if self.err is None else 1], dtype=torch.int64, device=self.cdev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        if int(t.item()):
+            if self.err is not None:
+                raise self.err
+            raise RuntimeError("distributed join: a peer rank failed before the all-to-all "
+                               "(its own exception is the root cause)")
+
+
 def _alltoall(be, k, p, send_counts, recv_counts, group):
     """all-to-all(v) of the private tuples; received in source-rank order."""
     n_recv = int(recv_counts.sum())
@@ -284,7 +411,8 @@ def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=Non
     """P-MPSM over the ranks of `group`; r and s are this rank's shards.
 
     Every rank returns the same JoinResult (worker i = rank i).  cfg.threads is
-    ignored: the worker count is the group size.
+    ignored: the worker count is the group size.  Local failures follow the
+    _Guard protocol (every rank raises at the same collective).
     """
     if cfg.algorithm != "p-mpsm":
         raise ConfigurationError("the distributed engine runs p-mpsm")
@@ -292,7 +420,6 @@ def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=Non
     me = dist.get_rank(group)
     be = backend or CudaBackend()
     dom = cfg.key_domain
-    be.setup(dom)
     t0 = time.perf_counter()
     trace = [] if (timings is not None and os.environ.get("MPSM_DIST_TRACE") == "1") else None
 
@@ -301,7 +428,9 @@ def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=Non
             trace.append((what, 1e3 * (time.perf_counter() - t0)))
 
     cdev = getattr(be, "comm_device", torch.device("cpu"))
-    sizes = _gather_u64([r.cardinality, s.cardinality], group, cdev).astype(np.int64)
+    gd = _Guard(group, cdev)
+    gd.call(be.setup, dom)
+    sizes = gd.gather([r.cardinality, s.cardinality], 2).astype(np.int64)
     _tr("sizes gathered")
     n_r, n_s = int(sizes[:, 0].sum()), int(sizes[:, 1].sum())
     roles = choose_roles(n_r, n_s, cfg.role_policy)
@@ -311,29 +440,34 @@ def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=Non
         raise ConfigurationError(f"effective radix bits {bits} give fewer buckets than {G} workers")
     nb = 1 << bits
     shift = dom.width_bits - bits
-    # host-resident public shards of a packed join cross PCIe as 8-B records
-    pub_rec = be.upload(public) if hasattr(be, "upload") else None
-    pk, pp = be.to_device(private.keys), be.to_device(private.payloads)
+    f = cfg.cdf_fanout
+    kb = f * G
     stats = [WorkerStats(i) for i in range(G)]
 
     # 1-2: private histogram (queued first: it needs only the private
     # shard), public run, bounds
-    h_dev = be.histogram_async(pk, shift, nb) if hasattr(be, "histogram_async") else None
-    if pub_rec is not None:
-        pub_run = be.sort_records(pub_rec)
-    else:
-        pub_run = be.sort(be.to_device(public.keys), be.to_device(public.payloads))
-    hist = h_dev.cpu().numpy() if h_dev is not None else be.histogram(pk, shift, nb)
-    f = cfg.cdf_fanout
-    bk = np.asarray(be.bound_keys(pub_run, f, G), np.uint64)
+    def local_public():
+        # host-resident public shards of a packed join cross PCIe as 8-B records
+        pub_rec = be.upload(public) if hasattr(be, "upload") else None
+        pk, pp = be.to_device(private.keys), be.to_device(private.payloads)
+        h_dev = be.histogram_async(pk, shift, nb) if hasattr(be, "histogram_async") else None
+        if pub_rec is not None:
+            pub_run = be.sort_records(pub_rec, public=True)
+        else:
+            pub_run = be.sort(be.to_device(public.keys), be.to_device(public.payloads), public=True)
+        hist = h_dev.cpu().numpy() if h_dev is not None else be.histogram(pk, shift, nb)
+        bk = np.asarray(be.bound_keys(pub_run, f, G), np.uint64)
+        # per rank: [hist (nb) | public cardinality | bad index | #bounds | f*G bounds]
+        vec = np.zeros(nb + 3 + kb, np.uint64)
+        vec[:nb] = np.asarray(hist, np.int64).view(np.uint64)
+        vec[nb:nb + 3] = np.array([int(public.cardinality), be.bad_index(), bk.shape[0]], np.int64).view(np.uint64)
+        vec[nb + 3:nb + 3 + bk.shape[0]] = bk
+        return pk, pp, pub_run, vec
+
+    loc = gd.call(local_public)
+    pk, pp, pub_run, vec = loc if loc is not None else (None, None, None, None)
     _tr("public sorted, hist + bounds on host")
-    # per rank: [hist (nb) | public cardinality | bad index | #bounds | f*G bounds]
-    kb = f * G
-    vec = np.zeros(nb + 3 + kb, np.uint64)
-    vec[:nb] = np.asarray(hist, np.int64).view(np.uint64)
-    vec[nb:nb + 3] = np.array([int(public.cardinality), be.bad_index(), bk.shape[0]], np.int64).view(np.uint64)
-    vec[nb + 3:nb + 3 + bk.shape[0]] = bk
-    allv = _gather_u64(vec, group, cdev)
+    allv = gd.gather(vec, nb + 3 + kb)
     info = []
     for v in allv:
         card, bad, nbk = (int(x) for x in v[nb:nb + 3].view(np.int64))
@@ -353,21 +487,39 @@ def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=Non
     send_starts = np.zeros(G, np.int64)
     np.cumsum(send_counts[:-1], out=send_starts[1:])
     _tr("splitters")
+
     # 4-5: scatter into send segments, one all-to-all
-    rec = be.partition_records(pk, pp, shift, ss.vector.sp, G) if hasattr(be, "partition_records") else None
-    if rec is None:
+    def local_partition():
+        rec = be.partition_records(pk, pp, shift, ss.vector.sp, G) if hasattr(be, "partition_records") else None
+        if rec is not None:
+            return rec, None, None
         sk, sp = be.partition(pk, pp, shift, ss.vector.sp, G, send_starts)
-    if rec is not None:  # packed join: one all-to-all of 8-B records
+        return None, sk, sp
+
+    part = gd.call(local_partition)
+    gd.check()
+    rec, sk, sp = part
+    packed_xchg = rec is not None
+    if packed_xchg:  # packed join: one all-to-all of 8-B records
         rr = _alltoall_one(be, rec, send_counts, recv_counts, group)
+        rk = rp = None
         n_recv_priv = int(rr.numel())
     else:
         rk, rp = _alltoall(be, sk, sp, send_counts, recv_counts, group)
+        rr = None
         n_recv_priv = int(rk.numel())
+    del pk, pp, rec, sk, sp
     t_part = time.perf_counter()
     _tr("partition + all-to-all issued")
-    # 6: private run
-    priv_run = be.sort_records(rr) if rec is not None else be.sort(rk, rp)
-    be.sync()
+
+    # 6: private run; this rank's public run named for the peers
+    def local_private():
+        run = be.sort_records(rr) if packed_xchg else be.sort(rk, rp)
+        be.sync()
+        return run, (be.share(pub_run) if G > 1 else None)
+
+    got = gd.call(local_private)
+    priv_run, my_share = got if got is not None else (None, None)
     t_sort = time.perf_counter()
     _tr("private sorted")
     # 7: join against every public run (remote ones through peer mappings)
@@ -377,24 +529,37 @@ def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=Non
     order = [(me + k) % G for k in range(G)]
     if G > 1:
         if isinstance(be, CudaBackend):  # IPC handles: fixed layout, one tensor gather
-            shared = [_dec_share(v) for v in _gather_u64(_enc_share(be.share(pub_run)), group, cdev)]
+            enc = _enc_share(my_share) if my_share is not None else None
+            shared = [_dec_share(v) for v in gd.gather(enc, 22)]
         else:
-            shared = _gather_obj(be.share(pub_run), group)
-        pub_runs = [pub_run if j == me else be.open(shared[j]) for j in order]
-    else:
-        pub_runs = [pub_run]
+            shared = gd.gather_obj(my_share)
     mode = {"aggregate-max": _lib.MODE_AGGREGATE_MAX, "count": _lib.MODE_COUNT,
             "materialize": _lib.MODE_COUNT}[cfg.query_mode]
-    rec_rot = np.asarray(be.records(be.join([priv_run], pub_runs, roles.swapped, mode))).reshape(G, _lib.PAIR_FIELDS)
-    rec_h = np.empty_like(rec_rot)
-    rec_h[order] = rec_rot  # back to public-run (rank) order
-    overflow = be.overflowed()
-    fin = np.concatenate([np.asarray(rec_h, np.uint64).ravel(), np.array([n_recv_priv, int(overflow)], np.uint64)])
-    gathered = [(v[:-2].reshape(G, _lib.PAIR_FIELDS), int(v[-2]), bool(v[-1])) for v in _gather_u64(fin, group, cdev)]
+
+    def local_join():
+        if G > 1:
+            pub_runs = [pub_run if j == me else be.open(shared[j], j) for j in order]
+        else:
+            pub_runs = [pub_run]
+        rec_rot = np.asarray(be.records(be.join([priv_run], pub_runs, roles.swapped, mode))).reshape(
+            G, _lib.PAIR_FIELDS)
+        rec_h = np.empty_like(rec_rot)
+        rec_h[order] = rec_rot  # back to public-run (rank) order
+        if any(int(x) & _lib.FLAG_UNSORTED for x in rec_h[:, _lib.PAIR_FLAGS]):
+            raise InternalConsistencyError("run keys are not sorted ascending (found by the merge-join walk)")
+        fin = np.concatenate([np.asarray(rec_h, np.uint64).ravel(),
+                              np.array([n_recv_priv, int(be.overflowed())], np.uint64)])
+        return pub_runs, rec_h, fin
+
+    got = gd.call(local_join)
+    pub_runs, rec_h, fin = got if got is not None else (None, None, None)
+    gathered = [(v[:-2].reshape(G, _lib.PAIR_FIELDS), int(v[-2]), bool(v[-1]))
+                for v in gd.gather(fin, G * _lib.PAIR_FIELDS + 2)]
     if any(g[2] for g in gathered):
         # a payload is wider than a packed record allows: redo on pairs
-        be2 = type(be)(packed=False, comm_device=be.comm_device) if isinstance(be, CudaBackend) else be.unpacked()
-        return run_join_distributed(r, s, cfg, group=group, backend=be2, timings=timings)
+        if hasattr(be, "release"):
+            be.release()
+        return run_join_distributed(r, s, cfg, group=group, backend=be.unpacked(), timings=timings)
     t_join = time.perf_counter()
     # 8: fold, as engine.finalize with worker i = rank i
     pub_sizes = [x[2] for x in info]
@@ -427,9 +592,11 @@ def run_join_distributed(r: Relation, s: Relation, cfg: JoinConfig, *, group=Non
         if count > cfg.materialize_cap:
             raise MaterializeCapExceeded(f"join produced {count} pairs, cap is {cfg.materialize_cap}")
         mine = int(sum(int(x) for x in rec_h.reshape(G, _lib.PAIR_FIELDS)[:, _lib.PAIR_COUNT]))
-        local = be.materialize([priv_run], pub_runs, roles.swapped, mine)
-        parts = _gather_obj(local, group)
+        local = gd.call(be.materialize, [priv_run], pub_runs, roles.swapped, mine)
+        parts = gd.gather_obj(local)
         materialized = np.concatenate(parts, axis=0) if parts else np.empty((0, 2), np.uint64)
+    if hasattr(be, "release"):
+        be.release()  # every importer is past its mapping step of this join
     tm = {"sort_public": t_pub - t0, "partition": t_part - t_pub, "sort_private": t_sort - t_part,
           "join": t_join - t_sort, "total": t_join - t0}
     if timings is not None:
@@ -451,22 +618,61 @@ def fk_shard_device(n_r: int, n_s: int, rank: int, world: int, seed: int, device
     return fk_range_device(n_r, n_s, chunk_bounds(n_r, world)[rank], chunk_bounds(n_s, world)[rank], seed, device)
 
 
-def bench_main(args, metric, configs, make_inputs, Clocks, run_reference_sample):
-    """bench.py under torchrun: every rank holds a cfg-sized shard (weak scaling)."""
-    from .core import KeyDomain
+# BASELINE.json configs the multi-GPU bench runs: (n_r, n_s, kind, scaling)
+DIST_CONFIGS = {
+    "cfg5": (1_600_000_000, 6_400_000_000, "fk", "strong"),   # configs[4]: whole-box scale-out
+    "cfg4": (400_000_000, 1_600_000_000, "negcorr", "strong"),  # configs[3] on 8 B200
+    "cfg2": (100_000_000, 400_000_000, "fk", "weak"),          # configs[1] per GPU (weak scaling)
+}
+
+
+def _dist_inputs(name: str, G: int, me: int, dev):
+    """this rank's position shards of a DIST_CONFIGS workload (counter-based,
+    generated on the device chunk by chunk) -> (R, S, KeyDomain, n_r, n_s)"""
+    from .core import KeyDomain, chunk_bounds
+    from .datagen import fk_shard_chunked, skewed_8020_range_device
+
+    n_r, n_s, kind, scaling = DIST_CONFIGS[name]
+    if scaling == "weak":
+        n_r, n_s = n_r * G, n_s * G
+    if kind == "fk":
+        r, s = fk_shard_chunked(n_r, n_s, me, G, 0, dev)
+        return r, s, KeyDomain(1, n_r + 1), n_r, n_s
+    dom = KeyDomain(1, 1 << 32)
+    r = skewed_8020_range_device(n_r, dom, "low", chunk_bounds(n_r, G)[me], 0, dev)
+    s = skewed_8020_range_device(n_s, dom, "high", chunk_bounds(n_s, G)[me], 1, dev)
+    return r, s, dom, n_r, n_s
+
+
+def bench_main(args, metric, Clocks):
+    """bench.py under torchrun: BASELINE configs[4] (cfg5, 1.6B x 6.4B, strong
+    scaling over the ranks) by default, --dist-config cfg4 / cfg2 (cfg2-sized
+    shards per GPU, weak scaling).  Every rank generates its position shards
+    on its GPU; the join result is checked (COUNT, MAX, checksum) against the
+    sharded torch checker (tests/torch_check.py) computed before the timed
+    region."""
+    import datetime
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    timeout = datetime.timedelta(seconds=int(os.environ.get("MPSM_DIST_TIMEOUT", "600")))
+    dist.init_process_group("nccl", device_id=dev, timeout=timeout)
     G, me = dist.get_world_size(), dist.get_rank()
-    n_r1, n_s1, _ = configs[args.config]
-    n_r, n_s = n_r1 * G, n_s1 * G
-    dom = KeyDomain(1, n_r + 1)
-    r, s = fk_shard_device(n_r, n_s, me, G, 0, torch.device("cuda", local))
+    name = getattr(args, "dist_config", None) or "cfg5"
+    n_r0, n_s0, kind, scaling = DIST_CONFIGS[name]
+    r, s, dom, n_r, n_s = _dist_inputs(name, G, me, dev)
+    # the expected result, before any join buffer exists (the checker
+    # rebuilds all of R on every rank)
+    from tests import torch_check as tc
+
+    want = tc.fk_join_dist(r, s, n_r) if kind == "fk" else tc.general_join_dist(r, s)
+    torch.cuda.empty_cache()
     cfg = JoinConfig(threads=G, key_domain=dom)
     be = CudaBackend()
     for _ in range(args.warmup):
         res = run_join_distributed(r, s, cfg, backend=be)
+    got = (res.match_count, res.aggregate_max, res.checksum)
     clocks = Clocks(local)
     clocks.start()
     dist.barrier()
@@ -488,9 +694,10 @@ def bench_main(args, metric, configs, make_inputs, Clocks, run_reference_sample)
     clk = clocks.stop()
     launches = _lib.launch_count() - l0
     sc_ms, sc_n = _lib.profile_read("seg_scatter")
+    mg_ms, _ = _lib.profile_read("merge")
     _lib.profile_enable(False)
     ms = float(ms.item())
-    ok = res.match_count == n_s
+    timed_ok = (res.match_count, res.aggregate_max, res.checksum) == got
 
     # roofline of the radix scatter on this rank: public sort (packing pass +
     # record passes) and the record sort of the received private tuples
@@ -498,7 +705,7 @@ def bench_main(args, metric, configs, make_inputs, Clocks, run_reference_sample)
     n_recv = res.worker_stats[me].tuples_sorted_private
     sc_bytes = args.steps * (s.cardinality * (24 + 16 * (passes - 1)) + n_recv * 16 * passes)
     achieved = sc_bytes / (sc_ms / 1e3) / 1e9 if sc_ms > 0 else None
-    peak = 6532.2
+    peak = 6548.2
     try:
         with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                "MEASURED_PEAKS.json")) as fh:
@@ -507,11 +714,19 @@ def bench_main(args, metric, configs, make_inputs, Clocks, run_reference_sample)
         pass
     roof = {"bound": "hbm", "kernel": "seg::k_scatter (radix scatter pass), rank 0", "achieved": achieved,
             "peak": peak, "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": None,
-            "launches": sc_n}
+            "launches": sc_n, "merge_ms_per_step_rank0": mg_ms / args.steps}
 
-    # end to end: every rank's shard from pinned host memory through the same call
+    # end to end: every rank's shard from pinned host memory through the same
+    # call, when the host has the RAM for all ranks' shards
     e2e = None
-    if not getattr(args, "no_e2e", False):
+    need = 16 * (r.cardinality + s.cardinality) * int(os.environ.get("LOCAL_WORLD_SIZE", G))
+    try:
+        import psutil
+
+        room = psutil.virtual_memory().available > 1.5 * need
+    except ImportError:
+        room = False
+    if not getattr(args, "no_e2e", False) and room:
         def pinned(t):  # device -> pinned host directly (no pageable copy: N ranks share the host RAM)
             h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
             h.copy_(t)
@@ -521,6 +736,7 @@ def bench_main(args, metric, configs, make_inputs, Clocks, run_reference_sample)
         sh = Relation(pinned(s.keys), pinned(s.payloads))
         k = max(1, min(args.steps, getattr(args, "e2e_steps", 3)))
         run_join_distributed(rh, sh, cfg, backend=be)
+        _lib.load().mpsm_upload_bytes(1)
         dist.barrier()
         torch.cuda.synchronize()
         e0.record()
@@ -530,26 +746,38 @@ def bench_main(args, metric, configs, make_inputs, Clocks, run_reference_sample)
         torch.cuda.synchronize()
         e_ms = torch.tensor([e0.elapsed_time(e1) / k], device="cuda")
         dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        up = torch.tensor([int(_lib.load().mpsm_upload_bytes(1)) // k], dtype=torch.int64, device="cuda")
+        dist.all_reduce(up, op=dist.ReduceOp.SUM)
         e_ms = float(e_ms.item())
+        up = int(up.item())
         e2e = {"value": (n_r + n_s) / (e_ms / 1e3), "unit": "tuples/s", "ms_per_step": e_ms, "steps": k,
-               "h2d_bytes_per_step": 8 * n_s + 16 * n_r, "d2h_bytes_per_step": 8 * _lib.PAIR_FIELDS * G * G,
-               "result_ok": (res_e.match_count, res_e.checksum) == (res.match_count, res.checksum),
-               "input_path": "pinned host shards; public side as packed 8-B records (upload_records), "
+               "h2d_bytes_per_step": up + 16 * (n_r if up else n_r + n_s),
+               "d2h_bytes_per_step": 8 * _lib.PAIR_FIELDS * G * G,
+               "result_ok": (res_e.match_count, res_e.aggregate_max, res_e.checksum) == got,
+               "input_path": "pinned host shards; public side as packed 8-B records (CudaBackend.upload), "
                              "private side as columns"}
         del rh, sh
+    elif not room:
+        e2e = {"value": None, "skipped": f"host RAM below 1.5 x the {need / 1e9:.0f} GB of pinned shards"}
     if me == 0:
         line = {
             "metric": metric, "value": (n_r + n_s) / (ms / 1e3), "unit": "tuples/s", "n_gpus": G,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-            "data": "synthetic (counter-based FK generator on device, seed 0)",
-            "config": {"workload": f"{args.config} per GPU: |R|={n_r:,} |S|={n_s:,} FK join over {G} GPUs",
-                       "algorithm": "p-mpsm", "threads": G, "parallelism": f"dp{G} (range-partitioned R, "
-                       "NCCL all-to-all, NVLink peer reads of S runs)",
+            "scaling": scaling, "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (counter-based generators on device, seed 0)",
+            "config": {"workload": f"{name}: |R|={n_r:,} |S|={n_s:,} "
+                                   + ("FK join" if kind == "fk" else "negatively correlated 80-20 skew join")
+                                   + f" sharded by position over {G} GPUs",
+                       "algorithm": "p-mpsm", "key_domain": [dom.lower, dom.upper],
                        "l2": "inputs >> L2 (no flush needed)"},
-            "result": {"match_count": res.match_count, "aggregate_max": res.aggregate_max,
-                       "checksum": hex(res.checksum), "fk_count_ok": ok},
+            "engine": {"impl": "paper_1207_0145_b200.distributed (NCCL all-to-all of R, NVLink peer reads of "
+                               "S runs)", "threads": G, "parallelism": f"dp{G}"},
+            "result": {"match_count": got[0], "aggregate_max": got[1], "checksum": hex(got[2]),
+                       "expected": [want[0], want[1], hex(want[2])],
+                       "verified_by": "sharded torch checker (tests/torch_check.py)", "matches": got == want,
+                       "timed_steps_match": timed_ok},
             "gpu_launches": launches, "clocks": clk, "e2e": e2e, "roofline": roof, "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)
+    ipc_close_all()
     dist.destroy_process_group()

@@ -35,7 +35,7 @@ class OracleBackend:
             return a.cpu()
         return torch.from_numpy(np.ascontiguousarray(a, np.uint64).copy())
 
-    def sort(self, k, p):
+    def sort(self, k, p, public=False):
         kk = k.numpy().copy()
         pp = p.numpy().copy()
         if orc.three_phase_sort(kk, pp, self.dom.lower, self.dom.width_bits) < 0:
@@ -74,7 +74,7 @@ class OracleBackend:
     def share(self, run):
         return (run[0].numpy().copy(), run[1].numpy().copy())
 
-    def open(self, shared):
+    def open(self, shared, peer=-1):
         return (torch.from_numpy(shared[0]), torch.from_numpy(shared[1]))
 
     def join(self, priv_runs, pub_runs, swap, mode, out=None, cap=0):

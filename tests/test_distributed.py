@@ -105,3 +105,62 @@ def test_counter_based_fk_shards_form_a_permutation():
     assert np.unique(sk).shape[0] > 0.9 * (1 - np.exp(-4)) * n_r
     pays = np.concatenate([p[0].payloads.numpy() for p in parts])
     assert pays.max() < (1 << 32) and np.unique(pays).shape[0] > 0.99 * n_r
+
+
+def _fault_worker(rank, world, port, where, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import datetime
+
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=60))
+    try:
+        from paper_1207_0145_b200.core import JoinConfig, KeyDomain, Relation, chunk_bounds
+        from paper_1207_0145_b200.distributed import run_join_distributed
+        from tests.dist_backend import OracleBackend
+        from tests.golden_inputs import dataset, make_inputs
+
+        class Faulty(OracleBackend):
+            def sort(self, k, p, public=False):
+                if where == "public" and public:
+                    raise ValueError("boom in the public sort")
+                if where == "private" and not public:
+                    raise ValueError("boom in the private sort")
+                return super().sort(k, p, public)
+
+            def partition(self, *a):
+                if where == "partition":
+                    raise ValueError("boom in the partition")
+                return super().partition(*a)
+
+        rk, rp, sk, sp, lo, up = make_inputs(dataset("fk_small"))
+        ra, rb = chunk_bounds(rk.shape[0], world)[rank]
+        sa, sb = chunk_bounds(sk.shape[0], world)[rank]
+        be = Faulty() if rank == 1 else OracleBackend()
+        try:
+            run_join_distributed(Relation(rk[ra:rb], rp[ra:rb]), Relation(sk[sa:sb], sp[sa:sb]),
+                                 JoinConfig(threads=world, key_domain=KeyDomain(lo, up)), backend=be)
+            q.put((rank, "ok", ""))
+        except Exception as exc:  # noqa: BLE001 - reported to the test
+            q.put((rank, type(exc).__name__, str(exc)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("where", ["public", "partition", "private"])
+def test_failing_rank_raises_everywhere_without_hanging(where):
+    """a rank whose local work raises enters the next collective with a
+    failure flag: it raises its own exception (the root cause), its peers a
+    RuntimeError naming it, and nobody blocks (engine.py:440-453)"""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fault_worker, args=(r, 2, port, where, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = dict((r, (kind, msg)) for r, kind, msg in (q.get(timeout=120) for _ in procs))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert results[1][0] == "ValueError" and "boom" in results[1][1]
+    kind, msg = results[0]
+    assert kind == "RuntimeError" and ("rank(s) [1]" in msg or "peer rank failed" in msg), (kind, msg)

@@ -102,7 +102,7 @@ print("OK" if bool((t == want).all()) else "MISMATCH")
     del big, x
 
 
-def _gloo_cuda_worker(rank, world, port, cases, packed, q):
+def _gloo_cuda_worker(rank, world, port, cases, packed, q, per_rank_device=False):
     import os as _os
 
     _os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -110,7 +110,7 @@ def _gloo_cuda_worker(rank, world, port, cases, packed, q):
     import torch as _t
     import torch.distributed as _dist
 
-    _t.cuda.set_device(0)
+    _t.cuda.set_device(rank if per_rank_device else 0)
     _dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_1207_0145_b200.core import JoinConfig as _JC, KeyDomain as _KD, Relation as _Rel, chunk_bounds
@@ -132,6 +132,9 @@ def _gloo_cuda_worker(rank, world, port, cases, packed, q):
                           w.tuples_sorted_private) for w in res.worker_stats]))
         q.put((rank, out))
     finally:
+        from paper_1207_0145_b200.distributed import ipc_close_all
+
+        ipc_close_all()
         _dist.destroy_process_group()
 
 
@@ -174,3 +177,33 @@ def test_cuda_backend_two_ranks_one_gpu_match_reference(golden, packed):
             stats = [(w["public_tuples_examined"], w["probe_tuples_examined"], w["s_runs_with_matches"],
                       w["tuples_sorted_private"]) for w in want["worker_stats"]]
             assert got[4] == stats, name
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs two GPUs: a peer run on another device")
+@pytest.mark.parametrize("packed", [True, False], ids=["packed", "pairs"])
+def test_merge_reads_public_run_on_another_gpu(golden, packed):
+    """Rank i on cuda:i: each rank's merge kernel TMA-loads the other rank's
+    public run from the other GPU's HBM through its CUDA-IPC mapping (NVLink
+    peer access) -- the multi-GPU data path, checked against the reference."""
+    import torch.multiprocessing as mp
+
+    from tests.test_distributed import CASES
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    with socket.socket() as sck:
+        sck.bind(("127.0.0.1", 0))
+        port = sck.getsockname()[1]
+    procs = [ctx.Process(target=_gloo_cuda_worker, args=(r, 2, port, CASES, packed, q, True)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert results[0] == results[1]
+    from tests.golden_inputs import reference_totals
+
+    for (name, mode, role), got in zip(CASES, results[0]):
+        count, mx, cs = reference_totals(name)
+        assert got[0] == count and got[2] == cs, name

@@ -83,13 +83,14 @@ def fk_join(r, s, chunk: int = 1 << 28):
     return acc.result()
 
 
-def general_join(r, s, chunk: int = 1 << 27):
-    """general equi-join (duplicates on both sides) by sort + searchsorted"""
-    dev = r.keys.device
-    rk, order = torch.sort(r.keys.view(torch.int64))
-    rp = r.payloads.view(torch.int64)[order]
+def _general_add(acc: Acc, r_keys, r_pays, s, chunk: int) -> None:
+    """every (R, S) pair with equal keys into acc: R sorted by torch.sort,
+    each S tuple's equal-key R range by searchsorted, the pairs enumerated
+    with repeat_interleave"""
+    dev = r_keys.device
+    rk, order = torch.sort(r_keys.view(torch.int64))
+    rp = r_pays.view(torch.int64)[order]
     del order
-    acc = Acc()
     sk_all, sp_all = s.keys.view(torch.int64), s.payloads.view(torch.int64)
     for a in range(0, sk_all.numel(), chunk):
         sk, sp = sk_all[a:a + chunk], sp_all[a:a + chunk]
@@ -104,4 +105,73 @@ def general_join(r, s, chunk: int = 1 << 27):
         s_of = torch.repeat_interleave(torch.arange(cnt.numel(), device=dev), cnt, output_size=total)
         r_idx = lo[s_of] + (torch.arange(total, device=dev) - start[s_of])
         acc.add(rp[r_idx], spm[s_of])
+
+
+def general_join(r, s, chunk: int = 1 << 27):
+    """general equi-join (duplicates on both sides) by sort + searchsorted"""
+    acc = Acc()
+    _general_add(acc, r.keys, r.payloads, s, chunk)
     return acc.result()
+
+
+# ------------------------------------------------ sharded (torch.distributed)
+def _reduce(acc: Acc, group, device):
+    """(count, max, checksum) over the ranks: sum / max / sum mod 2^64"""
+    import torch.distributed as dist
+
+    cs = acc.csum - (1 << 64) if acc.csum >= 1 << 63 else acc.csum
+    t = torch.tensor([acc.count, cs], dtype=torch.int64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    b = torch.tensor([-1 if acc.best is None else acc.best], dtype=torch.int64, device=device)
+    dist.all_reduce(b, op=dist.ReduceOp.MAX, group=group)
+    count, best = int(t[0].item()), int(b[0].item())
+    return count, (None if best < 0 else best), int(t[1].item()) & M64
+
+
+def _gather_padded(x, group, chunk: int):
+    """all_gather of this rank's x[c:c+chunk] for every chunk c, padded with
+    zeros (yields the gathered chunk tensors, [G * chunk] each)"""
+    import torch.distributed as dist
+
+    G = dist.get_world_size(group)
+    n = torch.tensor([x.numel()], dtype=torch.int64, device=x.device)
+    sizes = [torch.empty_like(n) for _ in range(G)]
+    dist.all_gather(sizes, n, group=group)
+    top = max(int(v.item()) for v in sizes)
+    for c in range(0, top, chunk):
+        piece = torch.zeros(chunk, dtype=torch.int64, device=x.device)
+        part = x.view(torch.int64)[c:c + chunk]
+        piece[:part.numel()] = part
+        outs = [torch.empty_like(piece) for _ in range(G)]
+        dist.all_gather(outs, piece, group=group)
+        yield outs, [max(0, min(chunk, int(v.item()) - c)) for v in sizes]
+
+
+def fk_join_dist(r, s, n_r: int, group=None, chunk: int = 1 << 26):
+    """FK join over position shards (every rank holds one R and one S shard):
+    the full lookup is rebuilt on every rank from gathered R chunks, each rank
+    gathers its S shard, the partials are reduced."""
+    dev = r.keys.device
+    lookup = torch.zeros(n_r + 1, dtype=torch.int64, device=dev)
+    for (ks, ns), (ps, _) in zip(_gather_padded(r.keys, group, chunk), _gather_padded(r.payloads, group, chunk)):
+        for k, p, m in zip(ks, ps, ns):
+            lookup[k[:m]] = p[:m]
+    acc = Acc()
+    fk_add(acc, lookup, s.keys, s.payloads)
+    del lookup
+    return _reduce(acc, group, dev)
+
+
+def general_join_dist(r, s, group=None, chunk: int = 1 << 26):
+    """general equi-join over position shards: every rank gathers all of R,
+    joins its S shard against it, the partials are reduced."""
+    ks, ps = [], []
+    for (kc, ns), (pc, _) in zip(_gather_padded(r.keys, group, chunk), _gather_padded(r.payloads, group, chunk)):
+        for k, p, m in zip(kc, pc, ns):
+            ks.append(k[:m].clone())
+            ps.append(p[:m].clone())
+    rk, rp = torch.cat(ks), torch.cat(ps)
+    del ks, ps
+    acc = Acc()
+    _general_add(acc, rk, rp, s, chunk)
+    return _reduce(acc, group, r.keys.device)
