@@ -91,6 +91,27 @@ struct Carve {
 };
 
 // ---------------------------------------------------------------- device
+// device-side bounds checks of the hot kernels' shared- and global-memory
+// indexing, compiled in only for the checked build (tools/checked_build.sh:
+// -DMPSM_DEBUG_CHECKS=1); a violation prints the site and traps
+#ifndef MPSM_DEBUG_CHECKS
+#define MPSM_DEBUG_CHECKS 0
+#endif
+#if MPSM_DEBUG_CHECKS
+#define MPSM_CHECK(cond)                                                                              \
+    do {                                                                                              \
+        if (!(cond)) {                                                                                \
+            printf("MPSM_CHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                 \
+            __trap();                                                                                 \
+        }                                                                                             \
+    } while (0)
+#else
+#define MPSM_CHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
+
 __device__ __forceinline__ uint64_t rotl64(uint64_t x, unsigned r) { return (x << r) | (x >> (64 - r)); }
 
 // splitmix64 finalizer

@@ -35,6 +35,7 @@ __device__ __forceinline__ void hist_add(uint32_t* h, uint64_t key, int64_t i, u
     const unsigned act = __ballot_sync(0xffffffffu, valid);
     if (!valid) return;
     const unsigned peers = __match_any_sync(act, b);
+    MPSM_CHECK(b < (uint32_t)nbuckets);
     if ((__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&h[b], (uint32_t)__popc(peers));
 }
 

@@ -443,6 +443,7 @@ __device__ __forceinline__ void fetch_tile(MergeStage<PK>& st, uint64_t* bar, co
         st.rp0 = q.rp.off + q.hp;
         st.wp0 = (int)(q.rp.bytes / 8) + q.wp.off;
     }
+    MPSM_CHECK(q.rk.bytes / 8 + q.wk.bytes / 8 <= MJ_TILE + 8);
     unsigned tx = q.rk.bytes + q.wk.bytes;
     if (!PK) tx += q.rp.bytes + q.wp.bytes;
     mbar_arrive_expect_tx(bar, tx);
@@ -645,7 +646,10 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                                 mind = min(mind, (int32_t)(d32 - prev));
                                 nondense |= (d32 - prev) ^ step1;
                             }
-                            if (d < tlim) sm.tbl[d32 >> ksh] = (uint16_t)(tag | (uint32_t)(e + 1));
+                            if (d < tlim) {
+                                MPSM_CHECK((d32 >> ksh) < (uint32_t)MJ_TBL);
+                                sm.tbl[d32 >> ksh] = (uint16_t)(tag | (uint32_t)(e + 1));
+                            }
                         }
                     }
                 }
@@ -718,6 +722,9 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                                 ia = (ea ? ea : 1) - 1 - hp;
                                 ib = (eb ? eb : 1) - 1 - hp;
                             }
+                            MPSM_CHECK(ia >= -hp && ia < nR && ib >= -hp && ib < nR);
+                            // the W loads past the end stay inside the CTA's shared memory
+                            MPSM_CHECK((const char*)(WK + jb + 1) <= (const char*)&sm + sizeof(MergeSmem<PK>));
                             const uint64_t ra = RK[ia], rb = RK[ib];
                             const uint64_t rpa = rpay_of(ra, ia), spa = PK ? (wa & pmask) : (va ? WP[ja] : 0);
                             const uint64_t rpb = rpay_of(rb, ib), spb = PK ? (wb & pmask) : (vb ? WP[jb] : 0);
@@ -863,6 +870,7 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                         down |= (uint32_t)(m < last);
                         last = m;
                     }
+                    MPSM_CHECK(take_r || wj < nW);
                     if (!take_r) sm.ub[wj] = (uint16_t)ri;
                     ri += take_r;
                     wj += !take_r;

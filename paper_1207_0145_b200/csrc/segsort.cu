@@ -494,6 +494,7 @@ __global__ void __launch_bounds__(THREADS, LCfg<LAYOUT>::BLOCKS) k_scatter(
         for (int k = 0; k < IT; ++k) {
             if (cnt == TL || 32 * k < lim) {
                 const uint32_t p = __byte_perm(hrow[dg[k]], 0, half) + rk[k];
+                MPSM_CHECK(p < (uint32_t)cnt);
                 sm.buf[b][0][p] = key[k];
                 if (LAYOUT == SS) sm.buf[b][1][p] = pay[k];
             }
@@ -507,6 +508,7 @@ __global__ void __launch_bounds__(THREADS, LCfg<LAYOUT>::BLOCKS) k_scatter(
             const uint64_t v = sm.buf[b][0][i];
             const int64_t o =
                 sm.gdelta[TABLE ? odig.lookup(v) : (LAYOUT == SS ? odig(v) : rec_digit<HI>(v, odig))] + i;
+            MPSM_CHECK(o >= 0 && o < sg.n);
             out_k[o] = v;
             if (LAYOUT == SS) out_p[o] = sm.buf[b][1][i];
         }
@@ -662,7 +664,9 @@ __global__ void __launch_bounds__(WsCfg<LAYOUT>::THREADS_ALL, 1) k_scatter_ws(
 #pragma unroll 4
             for (int i = wt; i < cnt; i += WS_WRITERS) {
                 const uint64_t v = sb[i];
-                out_k[gd[TABLE ? odig.lookup(v) : rec_digit<HI>(v, odig)] + i] = v;
+                const int64_t o = gd[TABLE ? odig.lookup(v) : rec_digit<HI>(v, odig)] + i;
+                MPSM_CHECK(o >= 0 && o < sg.n);
+                out_k[o] = v;
             }
             WS_TS(THREADS, t, 5)
             named_sync(BAR_WRITE, WS_WRITERS);  // buffer b read by every writer
@@ -770,6 +774,7 @@ __global__ void __launch_bounds__(WsCfg<LAYOUT>::THREADS_ALL, 1) k_scatter_ws(
             if (cnt == TL || 32 * k < lim) {
                 const uint32_t d = TABLE ? odig.lookup(key[k]) : rec_digit<HI>(key[k], odig);
                 const uint32_t p = __byte_perm(hrow[d], 0, half) + rk[k];
+                MPSM_CHECK(p < (uint32_t)cnt);
                 sm.buf[b][0][p] = key[k];
             }
         }
