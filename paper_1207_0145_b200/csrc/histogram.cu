@@ -4,11 +4,11 @@
 // Replaces _kernels.radix_histogram (/root/reference/pkg/src/mpsm/_kernels.py
 // 247-259) behind partition.build_radix_histogram (partition.py:110-122):
 // counts[(key - lower) >> shift] += 1 over 2^B buckets.  One read of 8 B per
-// key, 16-B vector loads; the counts go to shared-memory histograms, one
-// copy per warp pair (fewer collisions between warps), and lanes of a warp
-// that hit the same bucket add once (match.any aggregation: duplicate-heavy
-// keys cost one shared atomic per distinct bucket per warp instruction, not
-// 32 serialised ones).  Out-of-domain keys are reported through *d_bad and
+// key, 16-B vector loads; the counts go to shared-memory histograms, one copy
+// per group of warps (fewer collisions between warps), one shared atomic per
+// key (match.any aggregation per warp instruction measured 3.3x slower on
+// uniform keys: 0.77 vs 0.23 ms for 100M records).  Out-of-domain keys are
+// reported through *d_bad and
 // counted in the clamped bucket (the same clamp the partition scatter
 // applies), so a scatter built on these counts never leaves its regions even
 // for bad input.
@@ -32,11 +32,8 @@ __device__ __forceinline__ void hist_add(uint32_t* h, uint64_t key, int64_t i, u
     if (valid && nk > span_m1 && d_bad) atomicMin(d_bad, (unsigned long long)i);
     uint64_t b64 = nk >> shift;
     const uint32_t b = b64 >= (uint64_t)nbuckets ? (uint32_t)(nbuckets - 1) : (uint32_t)b64;
-    const unsigned act = __ballot_sync(0xffffffffu, valid);
-    if (!valid) return;
-    const unsigned peers = __match_any_sync(act, b);
     MPSM_CHECK(b < (uint32_t)nbuckets);
-    if ((__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(&h[b], (uint32_t)__popc(peers));
+    if (valid) atomicAdd(&h[b], 1u);
 }
 
 __global__ void __launch_bounds__(HIST_THREADS) k_radix_hist_smem(const uint64_t* __restrict__ keys, int64_t n,

@@ -628,29 +628,34 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                 int32_t mind = 1;
                 uint32_t nondense = 0;
                 const uint32_t step1 = 1u << ksh;
+                const int cw_r = (nRh + NWARP - 1) / NWARP;
+                const int beg_r = min(warp * cw_r, nRh), end_r = min(beg_r + cw_r, nRh);
+                // a span of exactly nRh - 1 keys is dense if the steps say so:
+                // then the pass only checks them (no table stores; R-heavy
+                // tiles, e.g. T > 1, read each R tuple once more and that is all)
+                const bool span_dense = (KT)(rkey(nR - 1) - kb) == (KT)((uint64_t)(nRh - 1) << ksh);
+                auto store = [&](int e, KT d) {
+                    bad |= (uint32_t)(d >= tlim);
+                    if (d < tlim) {
+                        MPSM_CHECK(((uint32_t)d >> ksh) < (uint32_t)MJ_TBL);
+                        sm.tbl[(uint32_t)d >> ksh] = (uint16_t)(tag | (uint32_t)(e + 1));
+                    }
+                };
                 {
-                    const int cw = (nRh + NWARP - 1) / NWARP;
-                    const int beg = min(warp * cw, nRh), end = min(beg + cw, nRh);
-                    uint32_t carry = beg > 0 ? (uint32_t)(rkey(beg - 1 - hp) - kb) : 0u;
-                    for (int e0 = beg; e0 < end; e0 += 32) {
+                    uint32_t carry = beg_r > 0 ? (uint32_t)(rkey(beg_r - 1 - hp) - kb) : 0u;
+                    for (int e0 = beg_r; e0 < end_r; e0 += 32) {
                         const int e = e0 + lane;
-                        const bool valid = e < end;
+                        const bool valid = e < end_r;
                         const KT d = valid ? (KT)(rkey(e - hp) - kb) : (KT)0;
                         const uint32_t d32 = (uint32_t)d;
                         uint32_t prev = __shfl_up_sync(0xffffffffu, d32, 1);
                         if (lane == 0) prev = carry;
                         carry = __shfl_sync(0xffffffffu, d32, 31);
-                        if (valid) {
-                            bad |= (uint32_t)(d >= tlim);
-                            if (e > 0) {
-                                mind = min(mind, (int32_t)(d32 - prev));
-                                nondense |= (d32 - prev) ^ step1;
-                            }
-                            if (d < tlim) {
-                                MPSM_CHECK((d32 >> ksh) < (uint32_t)MJ_TBL);
-                                sm.tbl[d32 >> ksh] = (uint16_t)(tag | (uint32_t)(e + 1));
-                            }
+                        if (valid && e > 0) {
+                            mind = min(mind, (int32_t)(d32 - prev));
+                            nondense |= (d32 - prev) ^ step1;
                         }
+                        if (valid && !span_dense) store(e, d);
                     }
                 }
                 bad |= (uint32_t)(mind < 0);
@@ -660,6 +665,10 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                 }
                 __syncthreads();
                 const int tflags = sm.tdup[buf];
+                if (span_dense && (tflags & 4)) {  // not dense after all: the table it is
+                    for (int e = beg_r + lane; e < end_r; e += 32) store(e, (KT)(rkey(e - hp) - kb));
+                    __syncthreads();
+                }
                 const bool tdup = tflags & 1;
                 const bool dense = !(tflags & 5);
                 // probe: W indices j = 0 .. nW-1

@@ -11,9 +11,11 @@ worker threads and no barriers to deadlock on (SURVEY.md finding 7).
 Per phase, device work only (csrc/):
   sort_public   LSD radix sort of every public chunk into its run
   sort_private  the private input sorted as ONE run (P-MPSM; B-MPSM: per
-                chunk), first pass fused with the domain check
-  histogram     2^B bucket counts read off the sorted private run (bucket
-                starts by lower-bound search)
+                chunk), first pass fused with the domain check; the host
+                computes the splitters meanwhile
+  histogram     2^B bucket counts of the private input (k_radix_hist, over
+                the packed records for host inputs), queued with the public
+                runs' bound keys ahead of the private sort
   splitters     host: CDF from f*T bounds per public run + C++ min-max search
   scatter       none on one GPU: the range partition sends contiguous key
                 ranges to the partitions in worker order and the run sort is
@@ -230,8 +232,9 @@ class JoinContext:
     input order among equal keys, so sorting the whole private input and
     cutting it at run_base yields exactly the runs the arena + per-partition
     sorts produce (same tuples in the same order), without the scatter pass.
-    The bucket histogram that feeds the splitters is read off the sorted run
-    by 2^B lower-bound searches (the bucket starts).
+    The bucket histogram that feeds the splitters is computed before the
+    private sort is queued and read back behind an event, so the host's
+    splitter search overlaps the sort.
     """
 
     def __init__(self, r: Relation, s: Relation, cfg: JoinConfig, phase_hook: PhaseHook, packed: bool,
@@ -400,33 +403,13 @@ class JoinContext:
         self.priv_store = self._store_for(self._private_rel(), self.priv_rec, self.n_priv)
         self.priv_whole = self._sort_private_range(0, self.n_priv)
 
-    def _public_bound_keys(self, f: int) -> np.ndarray:
-        """equi-height bound keys of every sorted public run (skew.py:52-62)"""
-        pos_list = [torch.from_numpy(bound_positions(b - a, f, self.t) + a) for a, b in self.pub_chunks if b > a]
-        if not pos_list:
-            return np.empty(0, np.uint64)
-        gather = torch.cat(pos_list).to(self.dev)
-        vals = self.pub_store[0].view(torch.int64)[gather].cpu().numpy().view(np.uint64)
-        if self.packed:
-            vals = (vals >> np.uint64(self.pw)) + np.uint64(self.dom.lower)
-        return vals
-
-    def _bucket_starts(self, bits: int) -> torch.Tensor:
-        """lower bound of every bucket b = (key - lower) >> (w - bits) in the
-        sorted private run (b = 1 .. 2^bits - 1; bucket 0 starts at 0)"""
-        nb, shift = 1 << bits, self.wbits - bits
-        b = np.arange(1, nb, dtype=np.uint64)
-        if self.packed:
-            tg = (b << np.uint64(shift)) << np.uint64(self.pw)  # records of key lower + (b << shift), payload 0
-        else:
-            tg = np.uint64(self.dom.lower) + (b << np.uint64(shift))
-        run = self.priv_whole[0]
-        idx, _ = D.interp_lower_bound(run, torch.from_numpy(tg).to(self.dev))
-        return idx
-
-    def partition(self):
-        """P-MPSM phase 2 (engine.py:359-374, 396-406): histogram, splitters,
-        cursors; the partition runs are slices of the sorted private run."""
+    def queue_histogram(self):
+        """P-MPSM, T > 1, before the private sort is queued: the 2^B bucket
+        histogram of the private input (partition.py:110-122; over the packed
+        records when the private side was uploaded as records) and the
+        equi-height bound keys of the public runs (skew.py:52-62), both copied
+        to pinned host memory behind one event -- the host computes the
+        splitters while the GPU sorts the private run."""
         t, dom = self.t, self.dom
         for i in range(t):
             self._hook(i, "histogram")
@@ -434,16 +417,37 @@ class JoinContext:
         if (1 << bits) < t:
             raise ConfigurationError(f"effective radix bits {bits} give fewer buckets than {t} workers")
         nb = 1 << bits
-        starts = self._bucket_starts(bits) if self.n_priv else None
         f = self.cfg.cdf_fanout
-        # the single host synchronisation of the join: bucket starts + bounds + flags
-        bk = self._public_bound_keys(f)
-        self.check_domain()
-        edges = np.zeros(nb + 1, np.int64)
-        if starts is not None:
-            edges[1:nb] = starts.cpu().numpy()
-        edges[nb] = self.n_priv
-        hist = np.diff(edges)
+        hist = torch.zeros(nb, dtype=torch.int64, device=self.dev)
+        if self.n_priv:
+            if self.priv_rec is not None:  # records: the bucket is the top bits of the record
+                D.radix_histogram(self.priv_rec, 0, (1 << 64) - 1, self.pw + self.wbits - bits, nb, hist, None)
+            else:
+                D.radix_histogram(self.priv_k, dom.lower, self.span_m1, self.wbits - bits, nb, hist, self.bad_priv)
+        pos_list = [torch.from_numpy(bound_positions(b - a, f, t) + a) for a, b in self.pub_chunks if b > a]
+        bk = self.pub_store[0].view(torch.int64)[torch.cat(pos_list).to(self.dev)] if pos_list else None
+        h_hist = torch.empty(nb, dtype=torch.int64, pin_memory=True)
+        h_hist.copy_(hist, non_blocking=True)
+        h_bk = None
+        if bk is not None:
+            h_bk = torch.empty(bk.numel(), dtype=torch.int64, pin_memory=True)
+            h_bk.copy_(bk, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._hist_pending = (ev, h_hist, h_bk, bits, hist, bk)
+
+    def partition(self):
+        """P-MPSM phase 2 (engine.py:359-374, 396-406) on the host, from the
+        queued histogram and bounds: splitters, cursors; the partition runs
+        are slices of the sorted private run (cut_partitions)."""
+        t, dom, f = self.t, self.dom, self.cfg.cdf_fanout
+        ev, h_hist, h_bk, bits, _, _ = self._hist_pending
+        ev.synchronize()  # the histogram and the bounds only, not the private sort behind them
+        hist = h_hist.numpy().copy()
+        bk = np.empty(0, np.uint64) if h_bk is None else h_bk.numpy().view(np.uint64).copy()
+        if self.packed:
+            bk = (bk >> np.uint64(self.pw)) + np.uint64(dom.lower)
+        self._hist_pending = None
         bounds, off = [], 0
         for a, b in self.pub_chunks:
             if b > a:
@@ -556,10 +560,14 @@ def _run(variant: str, r: Relation, s: Relation, cfg: JoinConfig, phase_hook: Ph
         ctx.sort_private_chunks()
         ctx.tl.mark("sort_private")
     else:
-        # P-MPSM: sort the private input as one run, derive the bucket
-        # histogram and the splitters, cut the run at the partition bounds.
-        # With one worker the partition is the identity (the splitter search
-        # returns [0, 2^B]) and the histogram is not needed.
+        # P-MPSM: histogram + public bounds queued, then the private input
+        # sorted as one run while the host computes the splitters from them;
+        # the run is cut at the partition bounds.  With one worker the
+        # partition is the identity (the splitter search returns [0, 2^B]) and
+        # the histogram is not needed.
+        if ctx.t > 1:
+            ctx.queue_histogram()
+        ctx.tl.mark("hist_queued")
         ctx.sort_private_whole()
         ctx.tl.mark("sorted_private")
         if ctx.t == 1:
@@ -583,9 +591,10 @@ def _run(variant: str, r: Relation, s: Relation, cfg: JoinConfig, phase_hook: Ph
         return _run(variant, r, s, cfg, phase_hook, packed=False)
     tl = ctx.tl
     if variant == "p-mpsm":
-        timings = {"sort_public": tl.seconds("t0", "public"), "partition": tl.seconds("sorted_private", "partitioned"),
-                   "sort_private": tl.seconds("public", "sorted_private"), "join": tl.seconds("sort_private", "join"),
-                   "total": tl.seconds("t0", "join")}
+        timings = {"sort_public": tl.seconds("t0", "public"),
+                   "partition": tl.seconds("public", "hist_queued") + tl.seconds("sorted_private", "partitioned"),
+                   "sort_private": tl.seconds("hist_queued", "sorted_private"),
+                   "join": tl.seconds("sort_private", "join"), "total": tl.seconds("t0", "join")}
     else:
         timings = {"sort_public": tl.seconds("t0", "public"), "partition": 0.0,
                    "sort_private": tl.seconds("partitioned", "sort_private"), "join": tl.seconds("sort_private", "join"),
