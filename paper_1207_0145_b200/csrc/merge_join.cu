@@ -82,6 +82,17 @@ __device__ __forceinline__ uint64_t mad_mask64(uint64_t acc, uint64_t h, uint32_
         : "r"((uint32_t)h), "r"((uint32_t)(h >> 32)), "r"(m));
     return ((uint64_t)ahi << 32) | alo;
 }
+// splitmix64(a ^ rotl64(b, 17)) for 32-bit a, b (the rotation is a shift),
+// the input's halves built explicitly: lo = a ^ (b << 17), hi = b >> 15
+__device__ __forceinline__ uint64_t pair_hash32(uint32_t a, uint32_t b) {
+    const uint32_t lo = a ^ (b << 17), hi = b >> 15;
+    return mix64(((uint64_t)hi << 32) | lo);
+}
+// best = max(best, v) with the compare on the ALU pipe and the moves
+// predicated (IMAD.MOV on the FMA pipe instead of two SELs)
+__device__ __forceinline__ void max_into(uint64_t& best, uint64_t v) {
+    asm("{\n\t.reg .pred p;\n\tsetp.gt.u64 p, %1, %0;\n\t@p mov.b64 %0, %1;\n\t}" : "+l"(best) : "l"(v));
+}
 // (a + b) * m, 64-bit, on the FMA pipe
 __device__ __forceinline__ uint64_t add_mask64(uint64_t a, uint64_t b, uint32_t m) {
     uint32_t lo, hi;
@@ -659,8 +670,20 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                     }
                 }
                 bad |= (uint32_t)(mind < 0);
+                // K32: does a record of the tile carry payload bits above bit
+                // 31 (in its high word, under kmask)?  If none does, the probe
+                // works on the low words (32-bit payloads: the hash input
+                // r ^ (s << 17) and the sum need no 64-bit payload math)
+                uint32_t wide = 0;
+                if (K32) {
+                    const uint32_t* hw = reinterpret_cast<const uint32_t*>(sm.st[buf].k);
+                    const int n_all = (int)((sm.st[buf].w0 + nW + 1) & ~1);  // every staged record (R span, W span)
+                    for (int q = tid; q < n_all; q += MJ_THREADS) wide |= hw[2 * q + 1];
+                    wide &= kmask;
+                }
                 {
-                    const uint32_t f = __reduce_or_sync(0xffffffffu, (mind == 0 ? 1u : 0u) | (nondense ? 4u : 0u));
+                    const uint32_t f = __reduce_or_sync(0xffffffffu, (mind == 0 ? 1u : 0u) | (nondense ? 4u : 0u) |
+                                                                         (wide ? 8u : 0u));
                     if (lane == 0 && f) atomicOr(&sm.tdup[buf], (int)f);
                 }
                 __syncthreads();
@@ -671,6 +694,7 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                 }
                 const bool tdup = tflags & 1;
                 const bool dense = !(tflags & 5);
+                const bool narrow = K32 && !(tflags & 8);
                 // probe: W indices j = 0 .. nW-1
                 uint64_t best_t = best, csum_t = 0;
                 uint32_t cnt_t = 0;
@@ -697,7 +721,7 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                         const KT d = k - kb;
                         return (valid && d < dlim) ? (int)((uint32_t)d >> ksh) + 1 : 0;
                     };
-                    auto unique_probe = [&](auto SW, auto DENSE) {
+                    auto unique_probe = [&](auto SW, auto DENSE, auto NARROW) {
                         // unique R keys: two W tuples per lane and step, the
                         // aggregate masked (IMADs) instead of branched; the W
                         // loads past the end stay inside shared memory
@@ -735,23 +759,40 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                             // the W loads past the end stay inside the CTA's shared memory
                             MPSM_CHECK((const char*)(WK + jb + 1) <= (const char*)&sm + sizeof(MergeSmem<PK>));
                             const uint64_t ra = RK[ia], rb = RK[ib];
-                            const uint64_t rpa = rpay_of(ra, ia), spa = PK ? (wa & pmask) : (va ? WP[ja] : 0);
-                            const uint64_t rpb = rpay_of(rb, ib), spb = PK ? (wb & pmask) : (vb ? WP[jb] : 0);
-                            const uint64_t ha = decltype(SW)::value ? hash2(spa, rpa) : hash2(rpa, spa);
-                            const uint64_t hb = decltype(SW)::value ? hash2(spb, rpb) : hash2(rpb, spb);
-                            const uint64_t sa = add_mask64(rpa, spa, ma), sb = add_mask64(rpb, spb, mb);
-                            if (sa > best_t) best_t = sa;
-                            if (sb > best_t) best_t = sb;
+                            uint64_t ha, hb, sa, sb;
+                            if (decltype(NARROW)::value) {
+                                // 32-bit payloads in the low words: rotl64(s, 17) is a shift
+                                const uint32_t rpa = (uint32_t)ra, spa = (uint32_t)wa;
+                                const uint32_t rpb = (uint32_t)rb, spb = (uint32_t)wb;
+                                ha = decltype(SW)::value ? pair_hash32(spa, rpa) : pair_hash32(rpa, spa);
+                                hb = decltype(SW)::value ? pair_hash32(spb, rpb) : pair_hash32(rpb, spb);
+                                sa = add_mask64(rpa, spa, ma);
+                                sb = add_mask64(rpb, spb, mb);
+                            } else {
+                                const uint64_t rpa = rpay_of(ra, ia), spa = PK ? (wa & pmask) : (va ? WP[ja] : 0);
+                                const uint64_t rpb = rpay_of(rb, ib), spb = PK ? (wb & pmask) : (vb ? WP[jb] : 0);
+                                ha = decltype(SW)::value ? hash2(spa, rpa) : hash2(rpa, spa);
+                                hb = decltype(SW)::value ? hash2(spb, rpb) : hash2(rpb, spb);
+                                sa = add_mask64(rpa, spa, ma);
+                                sb = add_mask64(rpb, spb, mb);
+                            }
+                            max_into(best_t, sa);
+                            max_into(best_t, sb);
                             csum_t = mad_mask64(mad_mask64(csum_t, ha, ma), hb, mb);
                             cnt_t += ma + mb;
                         }
                     };
-                    if (dense) {
-                        if (swap) unique_probe(std::true_type{}, std::true_type{});
-                        else unique_probe(std::false_type{}, std::true_type{});
+                    using T_ = std::true_type;
+                    using F_ = std::false_type;
+                    if (dense && narrow) {
+                        if (swap) unique_probe(T_{}, T_{}, std::integral_constant<bool, K32>{});
+                        else unique_probe(F_{}, T_{}, std::integral_constant<bool, K32>{});
+                    } else if (dense) {
+                        if (swap) unique_probe(T_{}, T_{}, F_{});
+                        else unique_probe(F_{}, T_{}, F_{});
                     } else if (!tdup) {
-                        if (swap) unique_probe(std::true_type{}, std::false_type{});
-                        else unique_probe(std::false_type{}, std::false_type{});
+                        if (swap) unique_probe(T_{}, F_{}, F_{});
+                        else unique_probe(F_{}, F_{}, F_{});
                     } else {
                         for (int j0 = beg; j0 < end; j0 += 32) {
                             const int j = j0 + lane;

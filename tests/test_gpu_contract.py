@@ -190,3 +190,33 @@ def test_threads_above_partition_scatter_limit():
     res = P.run_join(r, s, JoinConfig(threads=600, key_domain=dom))
     assert (res.match_count, res.aggregate_max, res.checksum) == want
     assert sum(w.tuples_sorted_private for w in res.worker_stats) == r.cardinality
+
+
+@pytest.mark.parametrize("pay_bits", [32, 33, 40])
+@pytest.mark.parametrize("dense", [True, False])
+def test_packed_payloads_above_32_bits(pay_bits, dense):
+    """packed records whose payloads use bits above 31 (kept in the record's
+    high word, w + pay_bits <= 64) take the merge's 64-bit payload path; every
+    other tile the 32-bit one -- both against the oracle (FK dense keys and
+    sparse keys)"""
+    rng = np.random.default_rng(pay_bits + 100 * dense)
+    w = 20
+    n_r, n_s = 200_000, 800_000
+    if dense:
+        rk = (rng.permutation(n_r) + 1).astype(np.uint64)
+        sk = rng.integers(1, n_r + 1, n_s, dtype=np.uint64)
+    else:
+        rk = rng.integers(1, 1 << w, n_r, dtype=np.uint64)
+        sk = rng.integers(1, 1 << w, n_s, dtype=np.uint64)
+    rp = rng.integers(0, 1 << 32, n_r, dtype=np.uint64)
+    sp = rng.integers(0, 1 << 32, n_s, dtype=np.uint64)
+    # a few payloads with high bits (one per ~1000 tuples: most tiles stay narrow)
+    hi = np.uint64((1 << pay_bits) - 1)
+    rp[::997] = rng.integers(0, 1 << 62, rp[::997].shape[0], dtype=np.uint64) & hi
+    sp[::1009] = rng.integers(0, 1 << 62, sp[::1009].shape[0], dtype=np.uint64) & hi
+    dom = KeyDomain(1, 1 << w)
+    want = orc.join(rk, rp, sk, sp, threads=1, lower=1, upper=1 << w)
+    for device in (True, False):
+        res = P.run_join(_rel(rk, rp, device), _rel(sk, sp, device), JoinConfig(threads=1, key_domain=dom))
+        assert (res.match_count, res.aggregate_max, res.checksum) == (want.match_count, want.aggregate_max,
+                                                                     want.checksum)
