@@ -282,6 +282,30 @@ uint64_t mpsm_upload_bytes(int reset);
 int mpsm_sort_records(const uint64_t* in_rec, int64_t n, int width_bits, uint64_t* out_rec, uint64_t* tmp_rec,
                       void* workspace, size_t ws_bytes, void* stream);
 
+/* ------------------------------------------------ segmented run sort ----
+ * nseg independent sorts in one launch sequence: elements [h_offsets[s],
+ * h_offsets[s+1]) form segment s and are sorted among themselves, in place
+ * of position (the T public chunks of a join -> T runs, engine.py:389-395;
+ * B-MPSM's private chunks, engine.py:297-309).  h_offsets: HOST int64
+ * [nseg + 1], 0 = h_offsets[0] <= ... <= h_offsets[nseg] = n, 1 <= nseg <=
+ * 1024.  Scatter tiles never straddle a segment; every pass is one count, one
+ * scan and one scatter launch for all segments.  Domain errors report the
+ * index in the whole array.  Workspace from
+ * mpsm_sort_segments_workspace_bytes; otherwise as the unsegmented calls
+ * (mpsm_sort_pairs_segments needs in_keys != out_keys). */
+int mpsm_sort_segments_workspace_bytes(int64_t n, int nseg, int width_bits, size_t* bytes);
+int mpsm_sort_pairs_segments(const uint64_t* in_keys, const uint64_t* in_pays, int64_t n, int nseg,
+                             const int64_t* h_offsets, uint64_t lower, uint64_t span_m1, int width_bits,
+                             uint64_t* out_keys, uint64_t* out_pays, uint64_t* tmp_keys, uint64_t* tmp_pays,
+                             void* workspace, size_t ws_bytes, unsigned long long* d_bad, void* stream);
+int mpsm_sort_packed_segments(const uint64_t* in_keys, const uint64_t* in_pays, int64_t n, int nseg,
+                              const int64_t* h_offsets, uint64_t lower, uint64_t span_m1, int width_bits,
+                              uint64_t* out_rec, uint64_t* tmp_rec, void* workspace, size_t ws_bytes,
+                              unsigned long long* d_bad, unsigned int* d_overflow, void* stream);
+int mpsm_sort_records_segments(const uint64_t* in_rec, int64_t n, int nseg, const int64_t* h_offsets,
+                               int width_bits, uint64_t* out_rec, uint64_t* tmp_rec, void* workspace,
+                               size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

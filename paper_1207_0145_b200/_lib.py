@@ -37,6 +37,8 @@ EXPORTS = (
     "mpsm_relfile_header", "mpsm_relfile_read", "mpsm_relfile_read_columns", "mpsm_relfile_write",
     "mpsm_deinterleave",
     "mpsm_upload_records", "mpsm_upload_bytes", "mpsm_sort_records", "mpsm_pack_records", "mpsm_partition_records",
+    "mpsm_sort_segments_workspace_bytes", "mpsm_sort_pairs_segments", "mpsm_sort_packed_segments",
+    "mpsm_sort_records_segments",
 )
 
 
@@ -81,6 +83,12 @@ _SIGS = {
     "mpsm_upload_records": (_int, [_vp, _vp, _i64, _u64, _u64, _int, _vp, _int, _int, _vp, _vp,
                                    ctypes.POINTER(_i64), ctypes.POINTER(_int)]),
     "mpsm_sort_records": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _sz, _vp]),
+    "mpsm_sort_segments_workspace_bytes": (_int, [_i64, _int, _int, ctypes.POINTER(_sz)]),
+    "mpsm_sort_pairs_segments": (_int, [_vp, _vp, _i64, _int, _vp, _u64, _u64, _int, _vp, _vp, _vp, _vp, _vp, _sz, _vp,
+                                        _vp]),
+    "mpsm_sort_packed_segments": (_int, [_vp, _vp, _i64, _int, _vp, _u64, _u64, _int, _vp, _vp, _vp, _sz, _vp, _vp,
+                                         _vp]),
+    "mpsm_sort_records_segments": (_int, [_vp, _i64, _int, _vp, _int, _vp, _vp, _vp, _sz, _vp]),
     "mpsm_upload_bytes": (_u64, [_int]),
     "mpsm_pack_records": (_int, [_vp, _vp, _i64, _u64, _u64, _int, _vp, _vp, _vp, _vp]),
     "mpsm_partition_records": (_int, [_vp, _vp, _i64, _u64, _u64, _int, _int, _vp, _int, _int, _vp, _vp, _sz, _vp,

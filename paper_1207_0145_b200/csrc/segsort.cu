@@ -33,6 +33,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 
@@ -118,11 +119,63 @@ struct Digit {
     }
 };
 
+// Tile geometry of one pass.  Single mode (nseg == 0): one sort over n
+// elements, count CTA g covers [g * seg_len, (g + 1) * seg_len), scatter tile
+// t starts at t * TL.  Multi mode (nseg > 0): nseg independent sorts of the
+// element ranges [off[s], off[s+1]) in one launch sequence (the T public
+// chunks of a join); scatter tiles never straddle a segment (tile t of
+// segment s starts at off[s] + (t - tb[s]) * TL), count CTA g covers the
+// tiles [tb[s] + (g - gb[s]) * tpc, ...) of its segment s.
 struct Segs {
     int64_t n;
-    int64_t seg_len;  // multiple of TILE
-    __device__ __forceinline__ int64_t begin(int g) const { return min((int64_t)g * seg_len, n); }
-    __device__ __forceinline__ int64_t end(int g) const { return min((int64_t)(g + 1) * seg_len, n); }
+    int64_t seg_len;  // single mode: multiple of the scatter tile
+    int nseg = 0;
+    const int64_t* off = nullptr;  // [nseg + 1] element offsets
+    const int64_t* tb = nullptr;   // [nseg + 1] first scatter tile of each segment
+    const int64_t* gb = nullptr;   // [nseg + 1] first count CTA of each segment
+    int64_t tpc = 0;               // scatter tiles per count CTA
+    __device__ __forceinline__ int seg_of(const int64_t* starts, int64_t x) const {  // last s with starts[s] <= x
+        int lo = 0, hi = nseg - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (starts[mid] <= x) lo = mid;
+            else hi = mid - 1;
+        }
+        return lo;
+    }
+    // count CTA g -> its element range [b, e) and first scatter tile
+    __device__ __forceinline__ void cta(int g, int64_t TL, int64_t& b, int64_t& e, int64_t& t0) const {
+        if (nseg == 0) {
+            b = min((int64_t)g * seg_len, n);
+            e = min((int64_t)(g + 1) * seg_len, n);
+            t0 = b / TL;
+            return;
+        }
+        if (g >= gb[nseg]) {  // launched for the bound, not needed
+            b = e = t0 = 0;
+            return;
+        }
+        const int s = seg_of(gb, g);
+        t0 = tb[s] + (int64_t)(g - gb[s]) * tpc;
+        const int64_t t1 = min(t0 + tpc, tb[s + 1]);
+        b = off[s] + (t0 - tb[s]) * TL;
+        e = min(off[s] + (t1 - tb[s]) * TL, off[s + 1]);
+        if (t0 >= t1) e = b;
+    }
+    // scatter tile t -> element start, count, count CTA
+    __device__ __forceinline__ void tile(int64_t t, int64_t TL, int64_t& start, int& cnt, int64_t& g) const {
+        if (nseg == 0) {
+            start = t * TL;
+            cnt = (int)min(TL, n - start);
+            g = t / (seg_len / TL);
+            return;
+        }
+        const int s = seg_of(tb, t);
+        start = off[s] + (t - tb[s]) * TL;
+        cnt = (int)min(TL, off[s + 1] - start);
+        g = gb[s] + (t - tb[s]) / tpc;
+    }
+    __device__ __forceinline__ int64_t ntiles(int64_t TL) const { return nseg == 0 ? (n + TL - 1) / TL : tb[nseg]; }
 };
 
 // ------------------------------------------------------------------ count
@@ -141,13 +194,14 @@ __global__ void __launch_bounds__(THREADS) k_count(const uint64_t* __restrict__ 
     h[1][tid] = 0;
     if (blockIdx.x == 0 && tid == 0 && ticket) *ticket = 0;  // the scatter's tile dispenser
     __syncthreads();
-    const int64_t b = sg.begin(blockIdx.x), e = sg.end(blockIdx.x);
+    int64_t b, e, tfirst;
+    sg.cta(blockIdx.x, STILE, b, e, tfirst);
     uint32_t run = 0;  // thread d: digit d's count in the tiles so far
     uint64_t v[ITEMS], w[ITEMS];
     // element u of a thread's chunk share: pairs of neighbours moved with
-    // 16-B loads when the input is 16-B aligned (chunks start at TILE
-    // multiples), else single elements
-    const bool vec = ((uintptr_t)in & 15) == 0;
+    // 16-B loads when the CTA's range is 16-B aligned (chunks are TILE apart),
+    // else single elements
+    const bool vec = ((uintptr_t)(in + b) & 15) == 0;
     auto pos = [&](int64_t c0, int u) -> int64_t {
         return vec ? c0 + 2 * ((u >> 1) * THREADS + tid) + (u & 1) : c0 + u * THREADS + tid;
     };
@@ -183,7 +237,7 @@ __global__ void __launch_bounds__(THREADS) k_count(const uint64_t* __restrict__ 
         for (int u = 0; u < ITEMS; ++u) v[u] = w[u];
         if (++c < CPT && c0 + TILE < e) continue;
         __syncthreads();  // h[k] complete; the next tile counts into h[k ^ 1]
-        if (tid < nbins) toffs[(size_t)((c0 - (c - 1) * TILE) / STILE) * MAX_BINS + tid] = run;
+        if (tid < nbins) toffs[(size_t)(tfirst + (c0 - (c - 1) * TILE - b) / STILE) * MAX_BINS + tid] = run;
         run += h[k][tid];
         h[k][tid] = 0;
         k ^= 1;
@@ -224,6 +278,68 @@ __global__ void __launch_bounds__(32 * SCAN_GROUPS) k_scan(const uint32_t* __res
     }
 }
 
+// multi-segment sorts: one CTA per sort segment s, thread d per digit.
+// base[g][d] = off[s] + (digit d's start inside segment s) + sum over the
+// segment's earlier count CTAs g' of counts[g'][d] -- the whole output offset
+// of the first digit-d tuple of count CTA g (the scatter adds the tile's
+// prefix and the in-tile rank)
+__global__ void __launch_bounds__(MAX_BINS) k_scan_mseg(const uint32_t* __restrict__ counts, Segs sg, int nbins,
+                                                        int64_t* __restrict__ base) {
+    __shared__ int64_t wsum[MAX_BINS / 32];
+    const int s = blockIdx.x, d = threadIdx.x, lane = d & 31, warp = d >> 5;
+    const int64_t g0 = sg.gb[s], g1 = sg.gb[s + 1];
+    const bool mine = d < nbins;
+    int64_t tot = 0;
+    for (int64_t g = g0; g < g1; ++g) tot += mine ? counts[(size_t)g * nbins + d] : 0;
+    int64_t incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int64_t run = sg.off[s] + incl - tot;
+    for (int w = 0; w < warp; ++w) run += wsum[w];
+    if (!mine) return;
+    for (int64_t g = g0; g < g1; ++g) {  // second read hits L2
+        const uint32_t c = counts[(size_t)g * nbins + d];
+        base[(size_t)g * nbins + d] = run;
+        run += c;
+    }
+}
+
+// multi-segment geometry of one pass (tile TL, tpc scatter tiles per count
+// CTA): tb / gb from off (one CTA, nseg <= MAX_SEGS); count CTAs past gb[nseg]
+// get empty ranges (Segs::cta)
+constexpr int MAX_SEGS = 1024;
+__global__ void __launch_bounds__(MAX_SEGS) k_seg_geom(const int64_t* __restrict__ off, int nseg, int64_t TL,
+                                                       int64_t tpc, int64_t* __restrict__ tb,
+                                                       int64_t* __restrict__ gb) {
+    __shared__ int64_t s_nt[MAX_SEGS], s_ng[MAX_SEGS];
+    const int s = threadIdx.x;
+    int64_t nt = 0, ng = 0;
+    if (s < nseg) {
+        nt = (off[s + 1] - off[s] + TL - 1) / TL;
+        ng = (nt + tpc - 1) / tpc;
+    }
+    s_nt[s] = nt;
+    s_ng[s] = ng;
+    __syncthreads();
+    for (int o = 1; o < MAX_SEGS; o <<= 1) {  // inclusive scans
+        const int64_t a = s >= o ? s_nt[s - o] : 0, b = s >= o ? s_ng[s - o] : 0;
+        __syncthreads();
+        s_nt[s] += a;
+        s_ng[s] += b;
+        __syncthreads();
+    }
+    if (s < nseg) {
+        tb[s + 1] = s_nt[s];
+        gb[s + 1] = s_ng[s];
+    }
+    if (s == 0) tb[0] = gb[0] = 0;
+}
+
 // ---------------------------------------------------------------- scatter
 // Shared memory of one scatter CTA.  The digit histogram of a tile keeps one
 // row per warp, two warps per 32-bit word (16-bit fields: a warp counts at
@@ -238,6 +354,8 @@ struct Smem {
     uint32_t toffs[NST][MAX_BINS];       // per buffer: the tile's segment-local digit prefixes
     uint32_t wtot[WARPS];                // digit-scan carries
     int64_t tile[NST];                   // per buffer: tile index
+    int64_t tstart[NST], tg[NST];        // per buffer: first element, count CTA (Segs::tile)
+    int tcnt[NST], toffk[NST], toffp[NST];  // per buffer: tuples, alignment slots of the key / payload copies
     uint64_t bar[NST];                   // bulk-copy completion, per buffer
 };
 static_assert(THREADS == MAX_BINS, "the digit scan gives each thread one digit");
@@ -326,9 +444,8 @@ __global__ void __launch_bounds__(THREADS, LCfg<LAYOUT>::BLOCKS) k_scatter(
     static_assert(32 * IT < 65536 && TL < 65536, "16-bit histogram fields");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt = lanemask_lt();
-    const int64_t T = (sg.n + TL - 1) / TL, tiles_per_seg = sg.seg_len / TL;
+    const int64_t T = sg.ntiles(TL);
     if ((int64_t)blockIdx.x >= T) return;
-    const int offk = (int)(((uintptr_t)in_k >> 3) & 1), offp = NARR == 2 ? (int)(((uintptr_t)in_p >> 3) & 1) : 0;
     const bool mine = tid < nbins;  // the digit this thread scans
     uint32_t* hrow = sm.hist[warp >> 1];
     const uint32_t inc = (warp & 1) ? 0x10000u : 1u;
@@ -336,8 +453,9 @@ __global__ void __launch_bounds__(THREADS, LCfg<LAYOUT>::BLOCKS) k_scatter(
     for (int i = tid; i < ROWS * MAX_BINS / 4; i += THREADS)
         reinterpret_cast<uint4*>(&sm.hist[0][0])[i] = make_uint4(0, 0, 0, 0);
     // start of my digit's output region: exclusive scan of the digit totals
-    int64_t dstart;
-    {
+    // (multi-segment sorts: the scan kernel folded it into base)
+    int64_t dstart = 0;
+    if (sg.nseg == 0) {
         const int64_t v = mine ? dtot[tid] : 0;
         int64_t incl = v;
 #pragma unroll
@@ -354,9 +472,17 @@ __global__ void __launch_bounds__(THREADS, LCfg<LAYOUT>::BLOCKS) k_scatter(
     // thread 0: one mbarrier phase brings tile t's tuples and its digit
     // prefixes into buffer bb
     auto fetch = [&](int bb, int64_t t) {
-        const int64_t t0 = t * TL;
-        const int cnt = (int)min((int64_t)TL, sg.n - t0);
+        int64_t t0, g;
+        int cnt;
+        sg.tile(t, TL, t0, cnt, g);
+        const int offk = (int)(((uintptr_t)(in_k + t0) >> 3) & 1);
+        const int offp = NARR == 2 ? (int)(((uintptr_t)(in_p + t0) >> 3) & 1) : 0;
         sm.tile[bb] = t;
+        sm.tstart[bb] = t0;
+        sm.tg[bb] = g;
+        sm.tcnt[bb] = cnt;
+        sm.toffk[bb] = offk;
+        sm.toffp[bb] = offp;
         unsigned bk = tile_plain(sm.buf[bb][0], in_k + t0, offk, cnt), bp = 0;
         if (NARR == 2) bp = tile_plain(sm.buf[bb][NARR - 1], in_p + t0, offp, cnt);
         const unsigned bo = MAX_BINS * 4;
@@ -400,12 +526,12 @@ __global__ void __launch_bounds__(THREADS, LCfg<LAYOUT>::BLOCKS) k_scatter(
             }
         }
         // my digit's segment base (L2-resident, G x 512); consumed after the rank
-        const int64_t sbase = mine ? base[(size_t)(t / tiles_per_seg) * nbins + tid] : 0;
+        const int64_t sbase = mine ? base[(size_t)sm.tg[b] * nbins + tid] : 0;
+        const int offk = sm.toffk[b], offp = sm.toffp[b];
+        const int cnt = sm.tcnt[b];
         mbar_wait(&sm.bar[b], (par >> b) & 1u);
         par ^= 1u << b;
         SEG_TS(1)
-        const int64_t t0 = t * TL;
-        const int cnt = (int)min((int64_t)TL, sg.n - t0);
         const int wb = warp * (32 * IT);
         const int lim = cnt - wb - lane;  // item k is valid iff 32 * k < lim
 
@@ -566,6 +692,8 @@ struct WsSmem {
     uint32_t toffs[WS_NB][MAX_BINS];
     uint32_t wtot[WARPS];
     int64_t tile[WS_NB];
+    int64_t tg[WS_NB];                     // per buffer: count CTA of the tile (Segs::tile)
+    int tcnt[WS_NB], toffk[WS_NB], toffp[WS_NB];  // per buffer: tuples, alignment slots
     uint64_t bar[WS_NB];
 };
 
@@ -589,16 +717,22 @@ __global__ void __launch_bounds__(WsCfg<LAYOUT>::THREADS_ALL, 1) k_scatter_ws(
     constexpr int IT = LCfg<LAYOUT>::ITEMS_L, TL = LCfg<LAYOUT>::TILE_L;
     static_assert(32 * IT < 65536 && TL < 65536, "16-bit histogram fields");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t T = (sg.n + TL - 1) / TL, tiles_per_seg = sg.seg_len / TL;
+    const int64_t T = sg.ntiles(TL);
     if ((int64_t)blockIdx.x >= T) return;
-    const int offk = (int)(((uintptr_t)in_k >> 3) & 1), offp = NARR == 2 ? (int)(((uintptr_t)in_p >> 3) & 1) : 0;
     const bool ranker = tid < THREADS;
     const bool mine = tid < nbins;
 
     auto fetch = [&](int bb, int64_t t) {
-        const int64_t t0 = t * TL;
-        const int cnt = (int)min((int64_t)TL, sg.n - t0);
+        int64_t t0, g;
+        int cnt;
+        sg.tile(t, TL, t0, cnt, g);
+        const int offk = (int)(((uintptr_t)(in_k + t0) >> 3) & 1);
+        const int offp = NARR == 2 ? (int)(((uintptr_t)(in_p + t0) >> 3) & 1) : 0;
         sm.tile[bb] = t;
+        sm.tg[bb] = g;
+        sm.tcnt[bb] = cnt;
+        sm.toffk[bb] = offk;
+        sm.toffp[bb] = offp;
         unsigned bk = tile_plain(sm.buf[bb][0], in_k + t0, offk, cnt), bp = 0;
         if (NARR == 2) bp = tile_plain(sm.buf[bb][NARR - 1], in_p + t0, offp, cnt);
         const unsigned bo = MAX_BINS * 4;
@@ -619,9 +753,9 @@ __global__ void __launch_bounds__(WsCfg<LAYOUT>::THREADS_ALL, 1) k_scatter_ws(
 
     for (int i = tid; i < ROWS * MAX_BINS / 4; i += WS_THREADS)
         reinterpret_cast<uint4*>(&sm.hist[0][0])[i] = make_uint4(0, 0, 0, 0);
-    int64_t dstart = 0;  // ranker d: start of digit d's output region
+    int64_t dstart = 0;  // ranker d: start of digit d's output region (multi-segment: in base)
     {
-        const int64_t v = mine ? dtot[tid] : 0;
+        const int64_t v = (mine && sg.nseg == 0) ? dtot[tid] : 0;
         int64_t incl = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -658,7 +792,7 @@ __global__ void __launch_bounds__(WsCfg<LAYOUT>::THREADS_ALL, 1) k_scatter_ws(
             if (tid == THREADS) g_seg_ts[t & ((1 << 22) - 1)][3] = w0;
 #endif
             WS_TS(THREADS, t, 4)
-            const int cnt = (int)min((int64_t)TL, sg.n - t * TL);
+            const int cnt = sm.tcnt[b];
             const uint64_t* sb = sm.buf[b][0];
             const int64_t* gd = sm.gdelta[b];
 #pragma unroll 4
@@ -699,8 +833,9 @@ __global__ void __launch_bounds__(WsCfg<LAYOUT>::THREADS_ALL, 1) k_scatter_ws(
         if (tid == 0) g_seg_ts[t & ((1 << 22) - 1)][0] = r0;
 #endif
         WS_TS(0, t, 1)
-        const int64_t sbase = mine ? base[(size_t)(t / tiles_per_seg) * nbins + tid] : 0;
-        const int cnt = (int)min((int64_t)TL, sg.n - t * TL);
+        const int64_t sbase = mine ? base[(size_t)sm.tg[b] * nbins + tid] : 0;
+        const int cnt = sm.tcnt[b];
+        const int offk = sm.toffk[b], offp = sm.toffp[b];
         const int wb = warp * (32 * IT);
         const int lim = cnt - wb - lane;
         uint64_t key[IT], pay[LAYOUT == SP ? IT : 1];
@@ -856,6 +991,8 @@ struct Ws {
     uint32_t* toffs;   // [tiles][MAX_BINS]
     int64_t* dtot;     // [MAX_BINS]
     unsigned int* ticket;
+    int64_t *off, *tb, *gb;  // multi-segment sorts: [nseg + 1] each
+    int nseg;
 };
 
 // one CTA per resident slot: the pair layouts (146 KB of shared memory) fit
@@ -884,22 +1021,47 @@ static Segs make_segs(int64_t n, int G, int tile = TILE) {
 
 static size_t ntiles(int64_t n) { return (size_t)((n + TILE - 1) / TILE); }
 
-static size_t ws_bytes(int64_t n) {
-    const int G = max_grid();
-    return align_up(sizeof(uint32_t) * (size_t)G * MAX_BINS) + align_up(sizeof(int64_t) * (size_t)G * MAX_BINS) +
-           align_up(sizeof(uint32_t) * ntiles(n) * MAX_BINS) + align_up(sizeof(int64_t) * MAX_BINS) +
-           align_up(sizeof(unsigned int));
+// multi-segment sorts: count CTAs (at most max_grid() + nseg) and scatter
+// tiles (at most one partial tile per segment more)
+static size_t ws_bytes(int64_t n, int nseg = 0) {
+    const size_t G = (size_t)max_grid() + nseg;
+    return align_up(sizeof(uint32_t) * G * MAX_BINS) + align_up(sizeof(int64_t) * G * MAX_BINS) +
+           align_up(sizeof(uint32_t) * (ntiles(n) + nseg) * MAX_BINS) + align_up(sizeof(int64_t) * MAX_BINS) +
+           align_up(sizeof(unsigned int)) + 3 * align_up(sizeof(int64_t) * (nseg + 1));
 }
 
-static bool carve(void* ws, size_t bytes, int64_t n, Ws* o) {
+static bool carve(void* ws, size_t bytes, int64_t n, Ws* o, int nseg = 0) {
     Carve c{(char*)ws, bytes};
-    const int G = max_grid();
-    o->counts = c.take<uint32_t>((size_t)G * MAX_BINS);
-    o->base = c.take<int64_t>((size_t)G * MAX_BINS);
-    o->toffs = c.take<uint32_t>(ntiles(n) * MAX_BINS);
+    const size_t G = (size_t)max_grid() + nseg;
+    o->counts = c.take<uint32_t>(G * MAX_BINS);
+    o->base = c.take<int64_t>(G * MAX_BINS);
+    o->toffs = c.take<uint32_t>((ntiles(n) + nseg) * MAX_BINS);
     o->dtot = c.take<int64_t>(MAX_BINS);
     o->ticket = c.take<unsigned int>(1);
+    o->off = c.take<int64_t>(nseg + 1);
+    o->tb = c.take<int64_t>(nseg + 1);
+    o->gb = c.take<int64_t>(nseg + 1);
+    o->nseg = nseg;
     return c.ok;
+}
+
+// the host offsets of a multi-segment sort -> ws.off, through a pinned
+// staging buffer (a pageable copy would wait for the stream)
+static int upload_offsets(const int64_t* h_off, int nseg, const Ws& ws, cudaStream_t st) {
+    static int64_t* stage = nullptr;
+    static size_t cap = 0;
+    static cudaEvent_t done = nullptr;
+    if (!done) MPSM_TRY(cuda_status(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "event"));
+    MPSM_TRY(cuda_status(cudaEventSynchronize(done), "event"));  // the previous copy has left the buffer
+    if (cap < (size_t)nseg + 1) {
+        if (stage) cudaFreeHost(stage);
+        cap = std::max<size_t>(nseg + 1, 1025);
+        MPSM_TRY(cuda_status(cudaMallocHost(&stage, sizeof(int64_t) * cap), "cudaMallocHost"));
+    }
+    std::copy(h_off, h_off + nseg + 1, stage);
+    MPSM_TRY(cuda_status(cudaMemcpyAsync(ws.off, stage, sizeof(int64_t) * (nseg + 1), cudaMemcpyHostToDevice, st),
+                         "h2d"));
+    return cuda_status(cudaEventRecord(done, st), "event");
 }
 
 template <int LAYOUT, bool HI, bool TABLE = false>
@@ -933,17 +1095,32 @@ static int pass(const uint64_t* in_k, const uint64_t* in_p, uint64_t* out_k, uin
                 uint64_t pk_lower, int pk_pw, unsigned int* overflow, cudaStream_t st) {
     // segments (count CTAs) are independent of the scatter grid: the tile
     // prefixes make every tile self-contained
+    constexpr int64_t TL = LCfg<LAYOUT>::TILE_L;
     const int G = std::min(grid_size<LAYOUT>(), max_grid());
-    const int GC = std::min(num_sms() * MPSM_SEG_COUNT_PER_SM, max_grid());
-    const Segs sg = make_segs(n, GC, LCfg<LAYOUT>::TILE_L);
+    int GC = std::min(num_sms() * MPSM_SEG_COUNT_PER_SM, max_grid());
+    Segs sg = make_segs(n, GC, (int)TL);
     const int nbins = 1 << bits;
+    if (ws.nseg > 0) {  // multi-segment: geometry of this pass's tiles on the device
+        const int64_t tpc = std::max<int64_t>(1, ((n + TL - 1) / TL + ws.nseg + GC - 1) / GC);
+        k_seg_geom<<<1, MAX_SEGS, 0, st>>>(ws.off, ws.nseg, TL, tpc, ws.tb, ws.gb);
+        MPSM_TRY(check_launch("k_seg_geom"));
+        sg.nseg = ws.nseg;
+        sg.off = ws.off;
+        sg.tb = ws.tb;
+        sg.gb = ws.gb;
+        sg.tpc = tpc;
+        GC += ws.nseg;  // a bound: the surplus count CTAs exit at once
+    }
     {
         ProfScope ps("seg_count", st);
         k_count<LCfg<LAYOUT>::TILE_L / TILE, TABLE><<<GC, THREADS, 0, st>>>(in_k, sg, count_dig, nbins, ws.counts,
                                                                              ws.toffs, ws.ticket, span_m1, d_bad);
     }
     MPSM_TRY(check_launch("k_count"));
-    k_scan<<<(nbins + 31) / 32, 32 * SCAN_GROUPS, 0, st>>>(ws.counts, GC, nbins, ws.base, ws.dtot);
+    if (ws.nseg > 0)
+        k_scan_mseg<<<ws.nseg, MAX_BINS, 0, st>>>(ws.counts, sg, nbins, ws.base);
+    else
+        k_scan<<<(nbins + 31) / 32, 32 * SCAN_GROUPS, 0, st>>>(ws.counts, GC, nbins, ws.base, ws.dtot);
     MPSM_TRY(check_launch("k_scan"));
     // digit of a staged value: records staged by the SP pass carry the key
     // above the payload bits
@@ -996,19 +1173,45 @@ extern "C" int mpsm_sort_workspace_bytes(int64_t n, int width_bits, size_t* byte
     return MPSM_OK;
 }
 
-extern "C" int mpsm_sort_pairs(const uint64_t* in_keys, const uint64_t* in_pays, int64_t n, uint64_t lower,
-                               uint64_t span_m1, int width_bits, uint64_t* out_keys, uint64_t* out_pays,
-                               uint64_t* tmp_keys, uint64_t* tmp_pays, void* workspace, size_t ws_bytes,
-                               unsigned long long* d_bad, void* stream) {
+namespace mpsm {
+namespace seg {
+// the workspace of a (multi-segment) sort, its segment offsets uploaded
+static int prepare(void* workspace, size_t bytes, int64_t n, int nseg, const int64_t* h_off, Ws* ws,
+                   cudaStream_t st) {
+    if (nseg < 0 || nseg > MAX_SEGS || (nseg > 0 && !h_off)) {
+        set_error("segment count must be 0 (one sort) or 1.." + std::to_string(MAX_SEGS));
+        return MPSM_ERR_ARG;
+    }
+    if (nseg > 0) {
+        if (h_off[0] != 0 || h_off[nseg] != n) {
+            set_error("segment offsets must run from 0 to n");
+            return MPSM_ERR_ARG;
+        }
+        for (int s = 0; s < nseg; ++s)
+            if (h_off[s + 1] < h_off[s]) {
+                set_error("segment offsets must not decrease");
+                return MPSM_ERR_ARG;
+            }
+    }
+    if (!carve(workspace, bytes, n, ws, nseg)) {
+        set_error("sort workspace too small");
+        return MPSM_ERR_ARG;
+    }
+    return nseg > 0 ? upload_offsets(h_off, nseg, *ws, st) : MPSM_OK;
+}
+}  // namespace seg
+}  // namespace mpsm
+
+static int sort_pairs_impl(const uint64_t* in_keys, const uint64_t* in_pays, int64_t n, int nseg, const int64_t* h_off,
+                           uint64_t lower, uint64_t span_m1, int width_bits, uint64_t* out_keys, uint64_t* out_pays,
+                           uint64_t* tmp_keys, uint64_t* tmp_pays, void* workspace, size_t ws_bytes,
+                           unsigned long long* d_bad, void* stream) {
     using namespace seg;
     cudaStream_t st = (cudaStream_t)stream;
     if (n < 0 || width_bits < 0 || width_bits > 64) return MPSM_ERR_ARG;
     if (n == 0) return MPSM_OK;
     Ws ws;
-    if (!carve(workspace, ws_bytes, n, &ws)) {
-        set_error("sort workspace too small");
-        return MPSM_ERR_ARG;
-    }
+    MPSM_TRY(prepare(workspace, ws_bytes, n, nseg, h_off, &ws, st));
     const Plan plan = make_plan(width_bits);
     if (plan.npasses == 0) {  // one-value domain: check it and copy
         const int G = max_grid();
@@ -1043,18 +1246,16 @@ extern "C" int mpsm_sort_pairs(const uint64_t* in_keys, const uint64_t* in_pays,
     return MPSM_OK;
 }
 
-extern "C" int mpsm_sort_packed(const uint64_t* in_keys, const uint64_t* in_pays, int64_t n, uint64_t lower,
-                                uint64_t span_m1, int width_bits, uint64_t* out_rec, uint64_t* tmp_rec, void* workspace,
-                                size_t ws_bytes, unsigned long long* d_bad, unsigned int* d_overflow, void* stream) {
+static int sort_packed_impl(const uint64_t* in_keys, const uint64_t* in_pays, int64_t n, int nseg,
+                            const int64_t* h_off, uint64_t lower, uint64_t span_m1, int width_bits, uint64_t* out_rec,
+                            uint64_t* tmp_rec, void* workspace, size_t ws_bytes, unsigned long long* d_bad,
+                            unsigned int* d_overflow, void* stream) {
     using namespace seg;
     cudaStream_t st = (cudaStream_t)stream;
     if (n < 0 || width_bits < 1 || width_bits > 63 || !d_overflow) return MPSM_ERR_ARG;
     if (n == 0) return MPSM_OK;
     Ws ws;
-    if (!carve(workspace, ws_bytes, n, &ws)) {
-        set_error("sort workspace too small");
-        return MPSM_ERR_ARG;
-    }
+    MPSM_TRY(prepare(workspace, ws_bytes, n, nseg, h_off, &ws, st));
     const Plan plan = make_plan(width_bits);
     const int pw = 64 - width_bits;
     const int P = plan.npasses;
@@ -1075,8 +1276,8 @@ extern "C" int mpsm_sort_packed(const uint64_t* in_keys, const uint64_t* in_pays
     return MPSM_OK;
 }
 
-extern "C" int mpsm_sort_records(const uint64_t* in_rec, int64_t n, int width_bits, uint64_t* out_rec,
-                                 uint64_t* tmp_rec, void* workspace, size_t ws_bytes, void* stream) {
+static int sort_records_impl(const uint64_t* in_rec, int64_t n, int nseg, const int64_t* h_off, int width_bits,
+                             uint64_t* out_rec, uint64_t* tmp_rec, void* workspace, size_t ws_bytes, void* stream) {
     using namespace seg;
     cudaStream_t st = (cudaStream_t)stream;
     if (n < 0 || width_bits < 1 || width_bits > 63) return MPSM_ERR_ARG;
@@ -1091,10 +1292,7 @@ extern "C" int mpsm_sort_records(const uint64_t* in_rec, int64_t n, int width_bi
         return MPSM_ERR_ARG;
     }
     Ws ws;
-    if (!carve(workspace, ws_bytes, n, &ws)) {
-        set_error("sort workspace too small");
-        return MPSM_ERR_ARG;
-    }
+    MPSM_TRY(prepare(workspace, ws_bytes, n, nseg, h_off, &ws, st));
     const uint64_t* src = in_rec;
     for (int i = 0; i < P; ++i) {
         uint64_t* dst = ((P - 1 - i) % 2 == 0) ? out_rec : tmp_rec;
@@ -1103,6 +1301,57 @@ extern "C" int mpsm_sort_records(const uint64_t* in_rec, int64_t n, int width_bi
         src = dst;
     }
     return MPSM_OK;
+}
+
+extern "C" int mpsm_sort_pairs(const uint64_t* in_keys, const uint64_t* in_pays, int64_t n, uint64_t lower,
+                               uint64_t span_m1, int width_bits, uint64_t* out_keys, uint64_t* out_pays,
+                               uint64_t* tmp_keys, uint64_t* tmp_pays, void* workspace, size_t ws_bytes,
+                               unsigned long long* d_bad, void* stream) {
+    return sort_pairs_impl(in_keys, in_pays, n, 0, nullptr, lower, span_m1, width_bits, out_keys, out_pays, tmp_keys,
+                           tmp_pays, workspace, ws_bytes, d_bad, stream);
+}
+
+extern "C" int mpsm_sort_packed(const uint64_t* in_keys, const uint64_t* in_pays, int64_t n, uint64_t lower,
+                                uint64_t span_m1, int width_bits, uint64_t* out_rec, uint64_t* tmp_rec, void* workspace,
+                                size_t ws_bytes, unsigned long long* d_bad, unsigned int* d_overflow, void* stream) {
+    return sort_packed_impl(in_keys, in_pays, n, 0, nullptr, lower, span_m1, width_bits, out_rec, tmp_rec, workspace,
+                            ws_bytes, d_bad, d_overflow, stream);
+}
+
+extern "C" int mpsm_sort_records(const uint64_t* in_rec, int64_t n, int width_bits, uint64_t* out_rec,
+                                 uint64_t* tmp_rec, void* workspace, size_t ws_bytes, void* stream) {
+    return sort_records_impl(in_rec, n, 0, nullptr, width_bits, out_rec, tmp_rec, workspace, ws_bytes, stream);
+}
+
+extern "C" int mpsm_sort_segments_workspace_bytes(int64_t n, int nseg, int width_bits, size_t* bytes) {
+    if (!bytes || n < 0 || nseg < 0 || nseg > seg::MAX_SEGS || width_bits < 0 || width_bits > 64) return MPSM_ERR_ARG;
+    *bytes = seg::ws_bytes(n, nseg);
+    return MPSM_OK;
+}
+
+extern "C" int mpsm_sort_pairs_segments(const uint64_t* in_keys, const uint64_t* in_pays, int64_t n, int nseg,
+                                        const int64_t* h_offsets, uint64_t lower, uint64_t span_m1, int width_bits,
+                                        uint64_t* out_keys, uint64_t* out_pays, uint64_t* tmp_keys, uint64_t* tmp_pays,
+                                        void* workspace, size_t ws_bytes, unsigned long long* d_bad, void* stream) {
+    if (nseg < 1 || in_keys == out_keys) return MPSM_ERR_ARG;
+    return sort_pairs_impl(in_keys, in_pays, n, nseg, h_offsets, lower, span_m1, width_bits, out_keys, out_pays,
+                           tmp_keys, tmp_pays, workspace, ws_bytes, d_bad, stream);
+}
+
+extern "C" int mpsm_sort_packed_segments(const uint64_t* in_keys, const uint64_t* in_pays, int64_t n, int nseg,
+                                         const int64_t* h_offsets, uint64_t lower, uint64_t span_m1, int width_bits,
+                                         uint64_t* out_rec, uint64_t* tmp_rec, void* workspace, size_t ws_bytes,
+                                         unsigned long long* d_bad, unsigned int* d_overflow, void* stream) {
+    if (nseg < 1) return MPSM_ERR_ARG;
+    return sort_packed_impl(in_keys, in_pays, n, nseg, h_offsets, lower, span_m1, width_bits, out_rec, tmp_rec,
+                            workspace, ws_bytes, d_bad, d_overflow, stream);
+}
+
+extern "C" int mpsm_sort_records_segments(const uint64_t* in_rec, int64_t n, int nseg, const int64_t* h_offsets,
+                                          int width_bits, uint64_t* out_rec, uint64_t* tmp_rec, void* workspace,
+                                          size_t ws_bytes, void* stream) {
+    if (nseg < 1) return MPSM_ERR_ARG;
+    return sort_records_impl(in_rec, n, nseg, h_offsets, width_bits, out_rec, tmp_rec, workspace, ws_bytes, stream);
 }
 
 extern "C" int mpsm_partition_records(const uint64_t* keys, const uint64_t* pays, int64_t n, uint64_t lower,

@@ -127,6 +127,56 @@ def sort_records(in_rec: torch.Tensor, width_bits: int, out_rec: torch.Tensor, t
                                    stream_ptr()), "mpsm_sort_records")
 
 
+def _seg_ws(dev, n: int, nseg: int, width_bits: int) -> torch.Tensor:
+    L = _lib.load()
+    sz = ctypes.c_size_t(0)
+    _lib.check(L.mpsm_sort_segments_workspace_bytes(n, nseg, width_bits, ctypes.byref(sz)), "sort workspace")
+    return workspace(dev).get(sz.value)
+
+
+def _offsets(offsets) -> np.ndarray:
+    return np.ascontiguousarray(offsets, dtype=np.int64)
+
+
+def sort_packed_segments(in_k, in_p, offsets, lower: int, span_m1: int, width_bits: int, out_rec, tmp_rec, bad,
+                         overflow) -> None:
+    """len(offsets) - 1 independent packed sorts of [offsets[s], offsets[s+1])
+    in one launch sequence (segment s -> run s, in place of position)"""
+    n = int(in_k.numel())
+    if n == 0:
+        return
+    off = _offsets(offsets)
+    ws = _seg_ws(in_k.device, n, off.shape[0] - 1, width_bits)
+    _lib.check(_lib.load().mpsm_sort_packed_segments(ptr(in_k), ptr(in_p), n, off.shape[0] - 1, off.ctypes.data, lower,
+                                                     span_m1, width_bits, ptr(out_rec), ptr(tmp_rec), ptr(ws),
+                                                     ws.numel(), ptr(bad), ptr(overflow), stream_ptr()),
+               "mpsm_sort_packed_segments")
+
+
+def sort_records_segments(in_rec, offsets, width_bits: int, out_rec, tmp_rec) -> None:
+    n = int(in_rec.numel())
+    if n == 0:
+        return
+    off = _offsets(offsets)
+    ws = _seg_ws(in_rec.device, n, off.shape[0] - 1, width_bits)
+    _lib.check(_lib.load().mpsm_sort_records_segments(ptr(in_rec), n, off.shape[0] - 1, off.ctypes.data, width_bits,
+                                                      ptr(out_rec), ptr(tmp_rec), ptr(ws), ws.numel(), stream_ptr()),
+               "mpsm_sort_records_segments")
+
+
+def sort_pairs_segments(in_k, in_p, offsets, lower: int, span_m1: int, width_bits: int, out_k, out_p, tmp_k, tmp_p,
+                        bad) -> None:
+    n = int(in_k.numel())
+    if n == 0:
+        return
+    off = _offsets(offsets)
+    ws = _seg_ws(in_k.device, n, off.shape[0] - 1, width_bits)
+    _lib.check(_lib.load().mpsm_sort_pairs_segments(ptr(in_k), ptr(in_p), n, off.shape[0] - 1, off.ctypes.data, lower,
+                                                    span_m1, width_bits, ptr(out_k), ptr(out_p), ptr(tmp_k),
+                                                    ptr(tmp_p), ptr(ws), ws.numel(), ptr(bad), stream_ptr()),
+               "mpsm_sort_pairs_segments")
+
+
 def pack_records(keys: torch.Tensor, pays: torch.Tensor, lower: int, span_m1: int, width_bits: int,
                  out_rec: torch.Tensor, bad: torch.Tensor, overflow: torch.Tensor) -> None:
     """device columns -> packed records; domain / payload-width flags on device"""

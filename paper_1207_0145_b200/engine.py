@@ -366,11 +366,38 @@ class JoinContext:
             return (rec, None)
         return self._alloc_runs(n)
 
+    def _sort_segments(self, chunks, rec, k, p, dst: tuple, bad) -> list:
+        """every chunk [a, b) sorted into dst[.][a:b] by ONE segmented sort
+        (mpsm_sort_*_segments: one count / scan / scatter launch per pass for
+        all chunks); returns the runs"""
+        n = chunks[-1][1] if chunks else 0
+        off = [a for a, _ in chunks] + [n]
+        tmp = self._tmp(n)
+        if n:
+            if rec is not None:
+                D.sort_records_segments(rec, off, self.wbits, dst[0], tmp[0][:n])
+            elif self.packed:
+                D.sort_packed_segments(k, p, off, self.dom.lower, self.span_m1, self.wbits, dst[0], tmp[0][:n], bad,
+                                       self.overflow)
+            else:
+                D.sort_pairs_segments(k, p, off, self.dom.lower, self.span_m1, self.wbits, dst[0], dst[1],
+                                      tmp[0][:n], tmp[1][:n], bad)
+        return [(dst[0][a:b], None if dst[1] is None else dst[1][a:b]) for a, b in chunks]
+
     def sort_public(self):
-        """phase 1: every public chunk -> sorted run (engine.py:389-395)."""
-        self._tmp(max((b - a for a, b in self.pub_chunks), default=0))
+        """phase 1: every public chunk -> sorted run (engine.py:389-395); T > 1
+        chunks in one segmented sort."""
         public = self.s if self.roles.private == "r" else self.r
         self.pub_store = self._store_for(public, self.pub_rec, self.n_pub)
+        if self.t > 1:
+            self._tmp(self.n_pub)
+            for i, (a, b) in enumerate(self.pub_chunks):
+                self._hook(i, "sort_public")
+                self.stats[i].tuples_sorted_public = b - a
+            k, p = (None, None) if self.pub_rec is not None else (self.pub_k, self.pub_p)
+            self.pub_runs = self._sort_segments(self.pub_chunks, self.pub_rec, k, p, self.pub_store, self.bad_pub)
+            return
+        self._tmp(max((b - a for a, b in self.pub_chunks), default=0))
         self.pub_runs = []
         for i, (a, b) in enumerate(self.pub_chunks):
             self._hook(i, "sort_public")
@@ -390,13 +417,17 @@ class JoinContext:
         return self.r if self.roles.private == "r" else self.s
 
     def sort_private_chunks(self):
-        """B-MPSM phase 2: each private chunk sorted into its run (engine.py:297-309)."""
+        """B-MPSM phase 2: each private chunk sorted into its run (engine.py:297-309),
+        all chunks in one segmented sort."""
         self.priv_store = self._store_for(self._private_rel(), self.priv_rec, self.n_priv)
-        self.priv_runs = []
         for i, (a, b) in enumerate(self.priv_chunks):
             self._hook(i, "sort_private")
-            self.priv_runs.append(self._sort_private_range(a, b))
             self.stats[i].tuples_sorted_private = b - a
+        if self.t == 1:
+            self.priv_runs = [self._sort_private_range(0, self.n_priv)]
+            return
+        k, p = (None, None) if self.priv_rec is not None else (self.priv_k, self.priv_p)
+        self.priv_runs = self._sort_segments(self.priv_chunks, self.priv_rec, k, p, self.priv_store, self.bad_priv)
 
     def sort_private_whole(self):
         """P-MPSM: the whole private input -> one sorted run (cut by partition())."""

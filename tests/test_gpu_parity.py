@@ -455,3 +455,45 @@ def test_payloads_above_32_bits_in_packed_records(frac_wide, pack_mode):
     for t in (1, 2):
         res = P.run_join(r, s, JoinConfig(threads=t, key_domain=dom))
         assert (res.match_count, res.aggregate_max, res.checksum) == want
+
+
+@pytest.mark.parametrize("layout", ["packed", "records", "pairs"])
+@pytest.mark.parametrize("sizes", [[5, 0, 8193, 1, 4095, 4097, 3], [100_003] * 7, [0, 0, 1], [12345]])
+def test_segmented_sort_sorts_every_segment(layout, sizes):
+    """mpsm_sort_*_segments: each segment sorted in place of position, stable
+    (odd segment offsets, empty and one-element segments, tile edges)"""
+    import torch
+
+    from paper_1207_0145_b200 import device as D
+
+    w = 23
+    rng = np.random.default_rng(sum(sizes) + len(sizes))
+    n = sum(sizes)
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    keys = rng.integers(0, 1 << w, n, dtype=np.uint64)
+    keys[::7] = keys[0]  # repeated keys: stability matters
+    pays = np.arange(n, dtype=np.uint64)
+    dk, dp = torch.from_numpy(keys).cuda(), torch.from_numpy(pays).cuda()
+    out, tmp = torch.empty_like(dk), torch.empty_like(dk)
+    bad = D.new_bad_flag(dk.device)
+    ovf = torch.zeros(1, dtype=torch.int32, device=dk.device)
+    pw = 64 - w
+    if layout == "packed":
+        D.sort_packed_segments(dk, dp, off, 0, (1 << w) - 1, w, out, tmp, bad, ovf)
+        got_k = (out.cpu().numpy() >> np.uint64(pw))
+        got_p = out.cpu().numpy() & np.uint64((1 << pw) - 1)
+    elif layout == "records":
+        rec = torch.from_numpy((keys << np.uint64(pw)) | pays).cuda()
+        D.sort_records_segments(rec, off, w, out, tmp)
+        got_k = (out.cpu().numpy() >> np.uint64(pw))
+        got_p = out.cpu().numpy() & np.uint64((1 << pw) - 1)
+    else:
+        op, tp = torch.empty_like(dp), torch.empty_like(dp)
+        D.sort_pairs_segments(dk, dp, off, 0, (1 << w) - 1, w, out, op, tmp, tp, bad)
+        got_k, got_p = out.cpu().numpy(), op.cpu().numpy()
+    assert int(bad.item()) == -1
+    for s in range(len(sizes)):
+        a, b = off[s], off[s + 1]
+        order = np.argsort(keys[a:b], kind="stable")
+        assert np.array_equal(got_k[a:b], keys[a:b][order]), s
+        assert np.array_equal(got_p[a:b], pays[a:b][order]), s
