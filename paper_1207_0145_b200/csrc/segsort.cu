@@ -16,11 +16,16 @@
 //            brings tile i+1 (tuples + digit prefixes) into shared memory with
 //            TMA bulk copies while tile i is ranked -- one shared atomicAdd
 //            per tuple into per-warp 16-bit histogram rows gives a stable
-//            rank (lane-ordered atomics, probed at start-up; warp-ballot
-//            fallback) -- scanned, staged in digit order in place and written
-//            out in coalesced runs.  No CTA waits for another (the decoupled
-//            look-back of the first design, kept for the partition scatter in
-//            partition_scatter.cu, held that kernel to ~35 % of HBM).
+//            rank (lane-ordered atomics, probed at start-up per device;
+//            warp-ballot fallback) -- scanned, staged in digit order in place
+//            and written out in coalesced runs.  No CTA waits for another
+//            (the decoupled look-back of the first design held its kernel to
+//            ~35 % of HBM; the partition scatter of the reference's arena,
+//            mpsm_scatter_chunk, is now this pass with the partition as digit
+//            and the worker's cursors as digit starts).
+//
+// One call sorts one array, or (multi-segment, Segs::nseg > 0) up to 1024
+// independent segments of it in the same launches -- the T runs of a join.
 //
 // Layouts: (key, payload) pairs throughout (SS); pairs in -> packed 8-B
 // records (key - lower) << pw | payload out (SP, first pass of a packed sort);
@@ -134,6 +139,9 @@ struct Segs {
     const int64_t* tb = nullptr;   // [nseg + 1] first scatter tile of each segment
     const int64_t* gb = nullptr;   // [nseg + 1] first count CTA of each segment
     int64_t tpc = 0;               // scatter tiles per count CTA
+    // single mode: explicit output start of each digit (the partition
+    // scatter's cursors) instead of the exclusive scan of the digit totals
+    const int64_t* dbase = nullptr;
     __device__ __forceinline__ int seg_of(const int64_t* starts, int64_t x) const {  // last s with starts[s] <= x
         int lo = 0, hi = nseg - 1;
         while (lo < hi) {
@@ -455,7 +463,9 @@ __global__ void __launch_bounds__(THREADS, LCfg<LAYOUT>::BLOCKS) k_scatter(
     // start of my digit's output region: exclusive scan of the digit totals
     // (multi-segment sorts: the scan kernel folded it into base)
     int64_t dstart = 0;
-    if (sg.nseg == 0) {
+    if (sg.dbase) {
+        dstart = mine ? sg.dbase[tid] : 0;
+    } else if (sg.nseg == 0) {
         const int64_t v = mine ? dtot[tid] : 0;
         int64_t incl = v;
 #pragma unroll
@@ -1092,13 +1102,15 @@ static int set_attr_ws() {
 template <int LAYOUT, bool TABLE = false>
 static int pass(const uint64_t* in_k, const uint64_t* in_p, uint64_t* out_k, uint64_t* out_p, int64_t n,
                 Digit count_dig, Digit dig, int bits, const Ws& ws, uint64_t span_m1, unsigned long long* d_bad,
-                uint64_t pk_lower, int pk_pw, unsigned int* overflow, cudaStream_t st) {
+                uint64_t pk_lower, int pk_pw, unsigned int* overflow, cudaStream_t st,
+                const int64_t* dbase = nullptr) {
     // segments (count CTAs) are independent of the scatter grid: the tile
     // prefixes make every tile self-contained
     constexpr int64_t TL = LCfg<LAYOUT>::TILE_L;
     const int G = std::min(grid_size<LAYOUT>(), max_grid());
     int GC = std::min(num_sms() * MPSM_SEG_COUNT_PER_SM, max_grid());
     Segs sg = make_segs(n, GC, (int)TL);
+    sg.dbase = dbase;
     const int nbins = 1 << bits;
     if (ws.nseg > 0) {  // multi-segment: geometry of this pass's tiles on the device
         const int64_t tpc = std::max<int64_t>(1, ((n + TL - 1) / TL + ws.nseg + GC - 1) / GC);
@@ -1131,7 +1143,7 @@ static int pass(const uint64_t* in_k, const uint64_t* in_p, uint64_t* out_k, uin
         ProfScope ps("seg_scatter", st);
         ProfScope ps2(LAYOUT == SS ? "seg_scatter_ss" : (LAYOUT == SP ? "seg_scatter_sp" : "seg_scatter_pp"), st);
         const bool lo = lane_ordered_atomics();
-        if constexpr (MPSM_SEG_WS && LAYOUT != SS) {
+        if constexpr (MPSM_SEG_WS && LAYOUT != SS && !TABLE) {
             MPSM_TRY(hi ? (set_attr_ws<LAYOUT, true, TABLE>()) : (set_attr_ws<LAYOUT, false, TABLE>()));
             const int GW = num_sms();
             if (hi)
@@ -1352,6 +1364,58 @@ extern "C" int mpsm_sort_records_segments(const uint64_t* in_rec, int64_t n, int
                                           size_t ws_bytes, void* stream) {
     if (nseg < 1) return MPSM_ERR_ARG;
     return sort_records_impl(in_rec, n, nseg, h_offsets, width_bits, out_rec, tmp_rec, workspace, ws_bytes, stream);
+}
+
+namespace mpsm {
+namespace seg {
+__global__ void k_add_written(const int64_t* __restrict__ dtot, int npart, int64_t* __restrict__ written) {
+    const int d = threadIdx.x;
+    if (d < npart) written[d] += dtot[d];
+}
+}  // namespace seg
+}  // namespace mpsm
+
+// ------------------------------------------------------------ partition scatter
+// The reference's scatter_chunk (_kernels.py:262-284) / partition.scatter
+// (partition.py:233-276): one stable radix pass over (key, payload) pairs
+// whose digit is the partition of the key's bucket (splitter table) and whose
+// digit regions start at the worker's cursors -- the arena layout of the
+// reference.  d_written += the tuples each partition received.
+extern "C" int mpsm_scatter_workspace_bytes(int64_t n, int npart, size_t* bytes) {
+    if (!bytes || n < 0 || npart < 1 || npart > seg::MAX_BINS) return MPSM_ERR_ARG;
+    *bytes = seg::ws_bytes(n);
+    return MPSM_OK;
+}
+
+extern "C" int mpsm_scatter_chunk(const uint64_t* keys, const uint64_t* pays, int64_t n, uint64_t lower, int shift,
+                                  const int32_t* d_sp, int nbuckets, int npart, const int64_t* d_cursors,
+                                  uint64_t* arena_keys, uint64_t* arena_pays, int64_t* d_written, void* workspace,
+                                  size_t ws_bytes, void* stream) {
+    using namespace seg;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n < 0 || npart < 1 || npart > MAX_BINS || nbuckets < 1 || shift < 0 || shift > 63 || !d_sp || !d_cursors) {
+        set_error("scatter: bad arguments (1 <= npart <= 512)");
+        return MPSM_ERR_ARG;
+    }
+    if (n == 0) return MPSM_OK;
+    Ws ws;
+    if (!carve(workspace, ws_bytes, n, &ws)) {
+        set_error("scatter workspace too small");
+        return MPSM_ERR_ARG;
+    }
+    int pbits = 0;
+    while ((1 << pbits) < npart) ++pbits;
+    const Digit dg{lower, shift, 0u, d_sp, nbuckets};
+    {
+        ProfScope ps("scatter", st);
+        MPSM_TRY((pass<SS, true>(keys, pays, arena_keys, arena_pays, n, dg, dg, pbits, ws, ~0ull, nullptr, 0, 0,
+                                 nullptr, st, d_cursors)));
+    }
+    if (d_written) {
+        k_add_written<<<1, MAX_BINS, 0, st>>>(ws.dtot, npart, d_written);
+        MPSM_TRY(check_launch("k_add_written"));
+    }
+    return MPSM_OK;
 }
 
 extern "C" int mpsm_partition_records(const uint64_t* keys, const uint64_t* pays, int64_t n, uint64_t lower,
