@@ -45,14 +45,19 @@
 
 namespace mpsm {
 
+// 256 threads x 23 = 5888-tuple tiles, 2 CTAs per SM: larger tiles amortise
+// the per-tile work (partition searches, staging, table setup) -- A/B on B200
+// (tools/merge_variants_run.py, merge + tile partition, FK 100M x 400M):
+// 128 x 15 (round 1) 1.68 ms, 256 x 15 1.62, 256 x 19 1.61, 256 x 23 1.57,
+// 256 x 27 (one CTA per SM) 1.97, 512 x 15 1.76, 64 x 15 1.99
 #ifndef MPSM_MJ_THREADS
-#define MPSM_MJ_THREADS 128
+#define MPSM_MJ_THREADS 256
 #endif
 #ifndef MPSM_MJ_ITEMS
-#define MPSM_MJ_ITEMS 15
+#define MPSM_MJ_ITEMS 23
 #endif
 #ifndef MPSM_MJ_BLOCKS
-#define MPSM_MJ_BLOCKS 6
+#define MPSM_MJ_BLOCKS 2
 #endif
 #ifndef MPSM_MJ_P2_UNROLL  // match-phase loop unroll (independent W tuples in flight)
 #define MPSM_MJ_P2_UNROLL 2
@@ -69,8 +74,12 @@ constexpr int MJ_TILE = MJ_THREADS * MJ_ITEMS;
 #define MPSM_MJ_TABLE 1
 #endif
 constexpr int MJ_TBL = 2048;  // table slots (a tile's R keys must span fewer)
-constexpr int MJ_TBL_TAGS = 32;  // 5-bit tile tags; the table is cleared when they run out
-static_assert(MJ_TILE + 3 < (1 << 11), "stage index + 1 fits the 11-bit field of a table entry");
+// a table entry (16 bits): tile tag << MJ_IDX_BITS | stage index + 1; the
+// table is cleared when the tags run out
+constexpr int MJ_IDX_BITS = (MJ_TILE + 3 < (1 << 11)) ? 11 : (MJ_TILE + 3 < (1 << 12)) ? 12 : 13;
+static_assert(MJ_TILE + 3 < (1 << MJ_IDX_BITS), "stage index + 1 fits the index field of a table entry");
+constexpr int MJ_TBL_TAGS = 1 << (16 - MJ_IDX_BITS);
+constexpr uint32_t MJ_IDX_MASK = (1u << MJ_IDX_BITS) - 1;
 
 // Masked accumulation on the FMA pipe (the merge is bound by the ALU pipe:
 // LOP3 / SHF / IADD3 / SEL / ISETP share it, IMAD runs beside it).  m is 0
@@ -395,7 +404,7 @@ struct MergeSmem {
     MergeStage<PK> st[2];
     union {
         uint16_t ub[MJ_TILE];   // MODE 0 walk: per W tuple of the tile, R tuples <= its key (tile-relative)
-        uint16_t tbl[MJ_TBL];   // MODE 0 table: slot key - key(R[-hp]) -> tag << 11 | stage index + 1
+        uint16_t tbl[MJ_TBL];   // MODE 0 table: slot key - key(R[-hp]) -> tag << MJ_IDX_BITS | stage index + 1
     };
     int tdup[2];           // MODE 0, per tile parity: some R key of the tile repeats
     int wend[MJ_THREADS / 32], wlo[MJ_THREADS / 32];  // MODE 0: where each warp's walk ends / starts (R index)
@@ -618,7 +627,13 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
             const uint64_t tlim64 = min((uint64_t)MJ_TBL << ksh, (uint64_t)0x7fffffff);
             const KT tlim = (KT)tlim64;
             const KT kb = nRh > 0 ? rkey(-hp) : (KT)0;
-            if (nRh > 0 && (KT)(rkey(nR - 1) - kb) < tlim) {
+            const KT span = nRh > 0 ? (KT)(rkey(nR - 1) - kb) : (KT)0;
+            // a span of exactly nRh - 1 keys is dense if the steps say so
+            // (checked below): then no table is needed, so R-heavy dense
+            // tiles (T > 1) of any span below 2^31 take this path too
+            const bool span_dense = nRh > 0 && span == (KT)((uint64_t)(nRh - 1) << ksh) && span <= (KT)0x7fffffff;
+            const bool table_ok = nRh > 0 && span < tlim;
+            if (table_ok || span_dense) {
                 tile_done = true;
                 if (tgen >= MJ_TBL_TAGS) {  // tags used up (or the walk wrote ub over the table)
                     for (int q = tid; q < MJ_TBL / 8; q += MJ_THREADS)
@@ -626,7 +641,7 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                     __syncthreads();
                     tgen = 1;
                 }
-                const uint32_t tag = (uint32_t)tgen << 11;
+                const uint32_t tag = (uint32_t)tgen << MJ_IDX_BITS;
                 const int lane = tid & 31, warp = tid >> 5;
                 constexpr int NWARP = MJ_THREADS / 32;
                 uint32_t bad = 0;
@@ -644,7 +659,6 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                 // a span of exactly nRh - 1 keys is dense if the steps say so:
                 // then the pass only checks them (no table stores; R-heavy
                 // tiles, e.g. T > 1, read each R tuple once more and that is all)
-                const bool span_dense = (KT)(rkey(nR - 1) - kb) == (KT)((uint64_t)(nRh - 1) << ksh);
                 auto store = [&](int e, KT d) {
                     bad |= (uint32_t)(d >= tlim);
                     if (d < tlim) {
@@ -688,6 +702,14 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                 }
                 __syncthreads();
                 const int tflags = sm.tdup[buf];
+                if (span_dense && (tflags & 4) && !table_ok) {
+                    // not dense after all and too wide for the table: the walk
+                    tile_done = false;
+                    if (__any_sync(0xffffffffu, bad != 0) && lane == 0)
+                        atomicOr((unsigned long long*)(out_pairs + (size_t)t.pair * MPSM_PAIR_FIELDS + MPSM_PAIR_FLAGS),
+                                 (unsigned long long)MPSM_FLAG_UNSORTED);
+                    tgen = MJ_TBL_TAGS;
+                } else {
                 if (span_dense && (tflags & 4)) {  // not dense after all: the table it is
                     for (int e = beg_r + lane; e < end_r; e += 32) store(e, (KT)(rkey(e - hp) - kb));
                     __syncthreads();
@@ -710,7 +732,7 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                         const KT d = k - kb;
                         if (!valid || d >= tlim) return 0;
                         const uint32_t ent = sm.tbl[(uint32_t)d >> ksh];
-                        return (ent ^ tag) < (1u << 11) ? (int)(ent & 0x7ffu) : 0;
+                        return (ent ^ tag) <= MJ_IDX_MASK ? (int)(ent & MJ_IDX_MASK) : 0;
                     };
                     auto rpay_of = [&](uint64_t rv, int i) -> uint64_t { return PK ? (rv & pmask) : RP[i]; };
                     auto wpay_of = [&](uint64_t wv, int j) -> uint64_t { return PK ? (wv & pmask) : WP[j]; };
@@ -837,6 +859,7 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                     atomicOr((unsigned long long*)(out_pairs + (size_t)t.pair * MPSM_PAIR_FIELDS + MPSM_PAIR_FLAGS),
                              (unsigned long long)MPSM_FLAG_UNSORTED);
                 ++tgen;
+                }  // dense or table
             } else {
                 tgen = MJ_TBL_TAGS;  // the walk writes ub over the table
             }

@@ -22,21 +22,31 @@ def srt(k, p):
     o, t = torch.empty_like(k), torch.empty_like(k)
     D.sort_packed(k, p, 1, n_r - 1, bits, o, t, None, ovf)
     return o
-R, S = srt(rk, rp), srt(sk, sp)
+T = int(os.environ.get("TJOIN", "1"))
+R = srt(rk, rp)
+if T == 1:
+    S = [srt(sk, sp)]
+    Rr = [R]
+else:  # T public chunks sorted separately, R cut into T key ranges (P-MPSM's runs)
+    cs = n_s // T
+    S = [srt(sk[i * cs:(i + 1) * cs].contiguous(), sp[i * cs:(i + 1) * cs].contiguous()) for i in range(T)]
+    cr = n_r // T
+    Rr = [R[i * cr:(i + 1) * cr] for i in range(T)]
 del rk, rp, sk, sp
 best = None
 for it in range(4):
     _lib.profile_enable(True)
-    rec = D.join_pairs_packed([R], [S], bits, 1, False, 0)
+    rec = D.join_pairs_packed(Rr, S, bits, 1, False, 0)
     torch.cuda.synchronize()
     ms, n = _lib.profile_read("merge")
     pm, _ = _lib.profile_read("merge_partition")
     best = (ms, pm) if best is None else min(best, (ms, pm))
-print(f"{os.environ['VNAME']:12s} merge {best[0]:.3f} ms  ({4e9/best[0]/1e6:.0f} GB/s packed)  partition {best[1]:.3f} ms"
-      f"  count={int(rec[0,0].item())}")
+print(f"{os.environ['VNAME']:12s} T={T} merge {best[0]:.3f} ms  ({4e9/best[0]/1e6:.0f} GB/s packed)  partition {best[1]:.3f} ms"
+      f"  count={int(rec[:, 0].sum().item())}")
 '''
 for lib in sorted(glob.glob(os.path.join(ROOT, "build", "variants", "*", "libmpsm_b200.so"))):
     name = os.path.basename(os.path.dirname(lib))
-    env = dict(os.environ, MPSM_LIB=lib, ROOT=ROOT, VNAME=name)
-    r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True, timeout=300)
-    print(r.stdout.strip() or (name + " FAILED " + r.stderr[-800:]), flush=True)
+    for tj in os.environ.get("TJOINS", "1").split(","):
+        env = dict(os.environ, MPSM_LIB=lib, ROOT=ROOT, VNAME=name, TJOIN=tj)
+        r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True, timeout=300)
+        print(r.stdout.strip() or (name + " FAILED " + r.stderr[-800:]), flush=True)
