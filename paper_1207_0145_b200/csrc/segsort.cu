@@ -190,8 +190,8 @@ struct Segs {
 // counts[g][d] for segment g, and for every tile t of the segment the
 // segment-local exclusive prefix toffs[t][d] (digit d's tuples in earlier
 // tiles of the segment); optional domain check (first pass)
-template <int CPT, bool TABLE = false>  // count chunks (TILE tuples) per scatter tile
-__global__ void __launch_bounds__(THREADS) k_count(const uint64_t* __restrict__ in, Segs sg, Digit dig, int nbins,
+template <int CPT, bool TABLE = false, bool MSEG = false>  // count chunks (TILE tuples) per scatter tile
+__global__ void __launch_bounds__(THREADS, 2) k_count(const uint64_t* __restrict__ in, Segs sg, Digit dig, int nbins,
                                                    uint32_t* __restrict__ counts, uint32_t* __restrict__ toffs,
                                                    unsigned int* __restrict__ ticket, uint64_t span_m1,
                                                    unsigned long long* __restrict__ d_bad) {
@@ -203,7 +203,13 @@ __global__ void __launch_bounds__(THREADS) k_count(const uint64_t* __restrict__ 
     if (blockIdx.x == 0 && tid == 0 && ticket) *ticket = 0;  // the scatter's tile dispenser
     __syncthreads();
     int64_t b, e, tfirst;
-    sg.cta(blockIdx.x, STILE, b, e, tfirst);
+    if (MSEG) {
+        sg.cta(blockIdx.x, STILE, b, e, tfirst);
+    } else {
+        b = min((int64_t)blockIdx.x * sg.seg_len, sg.n);
+        e = min((int64_t)(blockIdx.x + 1) * sg.seg_len, sg.n);
+        tfirst = b / STILE;
+    }
     uint32_t run = 0;  // thread d: digit d's count in the tiles so far
     uint64_t v[ITEMS], w[ITEMS];
     // element u of a thread's chunk share: pairs of neighbours moved with
@@ -245,7 +251,10 @@ __global__ void __launch_bounds__(THREADS) k_count(const uint64_t* __restrict__ 
         for (int u = 0; u < ITEMS; ++u) v[u] = w[u];
         if (++c < CPT && c0 + TILE < e) continue;
         __syncthreads();  // h[k] complete; the next tile counts into h[k ^ 1]
-        if (tid < nbins) toffs[(size_t)(tfirst + (c0 - (c - 1) * TILE - b) / STILE) * MAX_BINS + tid] = run;
+        if (tid < nbins) {
+            const int64_t ts = c0 - (c - 1) * TILE;  // this scatter tile's first element
+            toffs[(size_t)(MSEG ? tfirst + (ts - b) / STILE : ts / STILE) * MAX_BINS + tid] = run;
+        }
         run += h[k][tid];
         h[k][tid] = 0;
         k ^= 1;
@@ -1125,8 +1134,13 @@ static int pass(const uint64_t* in_k, const uint64_t* in_p, uint64_t* out_k, uin
     }
     {
         ProfScope ps("seg_count", st);
-        k_count<LCfg<LAYOUT>::TILE_L / TILE, TABLE><<<GC, THREADS, 0, st>>>(in_k, sg, count_dig, nbins, ws.counts,
-                                                                             ws.toffs, ws.ticket, span_m1, d_bad);
+        constexpr int CPT = LCfg<LAYOUT>::TILE_L / TILE;
+        if (ws.nseg > 0)
+            k_count<CPT, TABLE, true><<<GC, THREADS, 0, st>>>(in_k, sg, count_dig, nbins, ws.counts, ws.toffs,
+                                                               ws.ticket, span_m1, d_bad);
+        else
+            k_count<CPT, TABLE, false><<<GC, THREADS, 0, st>>>(in_k, sg, count_dig, nbins, ws.counts, ws.toffs,
+                                                                ws.ticket, span_m1, d_bad);
     }
     MPSM_TRY(check_launch("k_count"));
     if (ws.nseg > 0)
