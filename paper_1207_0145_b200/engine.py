@@ -319,9 +319,26 @@ class JoinContext:
 
     def check_domain(self) -> None:
         """raise the reference's DomainError if a fused check flagged a key
-        (synchronises on the two flags)"""
-        if int(self.bad_priv.item()) != -1 or int(self.bad_pub.item()) != -1:
+        (synchronises on the two flags unless fetch_status read them)"""
+        st = getattr(self, "_status", None)
+        flags = (st[1], st[2]) if st is not None else (int(self.bad_priv.item()), int(self.bad_pub.item()))
+        if flags != (-1, -1):
             raise_domain_error(self.r, self.s, self.dom)
+
+    def fetch_status(self) -> None:
+        """after the join is queued: the pair records and the three device
+        flags (domain, payload width) into pinned host memory, one stream
+        synchronisation for all of them"""
+        n = int(self.rec.numel())
+        h = torch.empty(n + 3, dtype=torch.int64, pin_memory=True)
+        h[:n].copy_(self.rec.view(torch.int64).view(-1), non_blocking=True)
+        h[n:n + 1].copy_(self.bad_priv, non_blocking=True)
+        h[n + 1:n + 2].copy_(self.bad_pub, non_blocking=True)
+        h[n + 2:n + 3].copy_(self.overflow.to(torch.int64), non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        v = h.numpy()
+        self._rec_host = v[:n].view(np.uint64)
+        self._status = (int(v[n + 2]), int(v[n]), int(v[n + 1]))  # overflow, bad_priv, bad_pub
 
     def _hook(self, i: int, phase: str) -> None:
         if self.hook:
@@ -530,12 +547,15 @@ class JoinContext:
         return out.view(total, 2).cpu().numpy()
 
     def packed_overflowed(self) -> bool:
-        return self.packed and int(self.overflow.item()) != 0
+        st = getattr(self, "_status", None)
+        ovf = st[0] if st is not None else int(self.overflow.item())
+        return self.packed and ovf != 0
 
     def finalize(self, timings: dict) -> JoinResult:
         """engine.py:195-225 plus the checksum and per-worker statistics."""
         t = self.t
-        rec = self.rec.cpu().numpy().reshape(t, t, _lib.PAIR_FIELDS).astype(object)
+        rec_h = self._rec_host if getattr(self, "_rec_host", None) is not None else self.rec.cpu().numpy()
+        rec = rec_h.reshape(t, t, _lib.PAIR_FIELDS).astype(object)
         self.check_domain()
         if any(int(f) & _lib.FLAG_UNSORTED for f in rec[:, :, _lib.PAIR_FLAGS].ravel()):
             raise InternalConsistencyError("run keys are not sorted ascending (found by the merge-join walk)")
@@ -615,7 +635,7 @@ def _run(variant: str, r: Relation, s: Relation, cfg: JoinConfig, phase_hook: Ph
         ctx.tl.mark("sort_private")
     ctx.join()
     ctx.tl.mark("join")
-    torch.cuda.current_stream().synchronize()
+    ctx.fetch_status()
     if ctx.packed_overflowed():
         # a payload needs more than 64 - w bits: redo on (key, payload) pairs
         ctx.check_domain()
