@@ -132,6 +132,41 @@ __device__ __forceinline__ uint64_t pair_hash_fma(uint64_t r_pay, uint64_t s_pay
     return xorshr_fma(z, m31);
 }
 
+// splitmix64(a ^ rotl64(b, 17)) of 32-bit a, b with a chosen share of the
+// work on the FMA pipe (the dense-run join is bound by the ALU pipe): FMA
+// bit 0 the input's shifts as IMAD / IMAD.HI, bit 1 the add of the golden
+// ratio as a mad chain, bits 2-4 the three xor-shifts as IMAD.HI (see
+// xorshr_fma).  K holds 2^17, 2^2, 2^5, 2^1 and 1 where ptxas cannot fold
+// them (read through volatile shared loads).
+struct FmaK {
+    uint32_t m17, m30, m27, m31, one;
+};
+__device__ __forceinline__ uint64_t xorshr_alu(uint64_t z, int k) { return z ^ (z >> k); }
+template <int FMA>
+__device__ __forceinline__ uint64_t pair_hash32_mix(uint32_t a, uint32_t b, const FmaK& K) {
+    uint32_t lo, hi;
+    if (FMA & 1) {
+        lo = a ^ (b * K.m17);
+        hi = __umulhi(b, K.m17);
+    } else {
+        lo = a ^ (b << 17);
+        hi = b >> 15;
+    }
+    uint64_t z;
+    if (FMA & 2) {
+        uint32_t zl, zh;
+        asm("mad.lo.cc.u32 %0, %2, %4, 0x7F4A7C15;\n\tmadc.lo.u32 %1, %3, %4, 0x9E3779B9;"
+            : "=r"(zl), "=r"(zh)
+            : "r"(lo), "r"(hi), "r"(K.one));
+        z = ((uint64_t)zh << 32) | zl;
+    } else {
+        z = (((uint64_t)hi << 32) | lo) + 0x9E3779B97F4A7C15ull;
+    }
+    z = ((FMA & 4) ? xorshr_fma(z, K.m30) : xorshr_alu(z, 30)) * 0xBF58476D1CE4E5B9ull;
+    z = ((FMA & 8) ? xorshr_fma(z, K.m27) : xorshr_alu(z, 27)) * 0x94D049BB133111EBull;
+    return (FMA & 16) ? xorshr_fma(z, K.m31) : xorshr_alu(z, 31);
+}
+
 struct PackInfo {
     int pw;          // payload bits of a packed record (0: SoA runs)
     uint64_t lower;  // key domain lower bound (packed keys are key - lower)
@@ -229,9 +264,12 @@ __global__ void k_interp_batch(const uint64_t* __restrict__ keys, int64_t n, con
     if (probes) probes[t] = pr;
 }
 
+// nondense (optional): per private run, nonzero unless the dense-run path
+// (k_dense_join) takes its pairs; those get no merge tiles
 template <bool PK>
 __global__ void k_windows(const mpsm_run_t* __restrict__ priv, int n_priv, const mpsm_run_t* __restrict__ pub,
-                          int n_pub, PairWin* __restrict__ win, uint64_t* __restrict__ out, PackInfo pi) {
+                          int n_pub, PairWin* __restrict__ win, uint64_t* __restrict__ out, PackInfo pi,
+                          const uint32_t* __restrict__ nondense) {
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n_priv * n_pub) return;
     const mpsm_run_t r = priv[p / n_pub];
@@ -247,7 +285,8 @@ __global__ void k_windows(const mpsm_run_t* __restrict__ priv, int n_priv, const
         examined = (w.end < s.n - 1 ? w.end : s.n - 1) - w.start + 1;
         if (examined < 0) examined = 0;
         const int64_t len = r.n + (w.end - w.start);
-        w.tiles = (w.end > w.start) ? (len + MJ_TILE - 1) / MJ_TILE : 0;
+        const bool merge = nondense == nullptr || nondense[p / n_pub] != 0;
+        w.tiles = (merge && w.end > w.start) ? (len + MJ_TILE - 1) / MJ_TILE : 0;
     }
     win[p] = w;
     o[MPSM_PAIR_COUNT] = 0;
@@ -1223,7 +1262,7 @@ struct JoinWs {
     int64_t* tile_cnt;
 };
 
-static bool carve_join(Carve c, int n_priv, int n_pub, int64_t mt, JoinWs* o) {
+static bool carve_join(Carve& c, int n_priv, int n_pub, int64_t mt, JoinWs* o) {
     o->d_priv = c.take<mpsm_run_t>(std::max(n_priv, 1));
     o->d_pub = c.take<mpsm_run_t>(std::max(n_pub, 1));
     o->win = c.take<PairWin>((size_t)std::max(n_priv * n_pub, 1));
@@ -1234,17 +1273,6 @@ static bool carve_join(Carve c, int n_priv, int n_pub, int64_t mt, JoinWs* o) {
     return c.ok;
 }
 
-static size_t join_ws_size(int n_priv, int n_pub, int64_t mt) {
-    Carve c{nullptr, (size_t)-1};
-    c.take<mpsm_run_t>(std::max(n_priv, 1));
-    c.take<mpsm_run_t>(std::max(n_pub, 1));
-    c.take<PairWin>((size_t)std::max(n_priv * n_pub, 1));
-    c.take<int64_t>(1);
-    c.take<int64_t>(1);
-    c.take<TileSplit>(mt);
-    c.take<int64_t>(mt);
-    return c.off;
-}
 
 template <int MODE, bool PK, bool K32 = false>
 static int launch_merge(const JoinWs& w, int swap, uint64_t* d_pairs, uint64_t* emit_out, int64_t cap, int64_t mt,
@@ -1267,6 +1295,678 @@ static int launch_merge(const JoinWs& w, int swap, uint64_t* d_pairs, uint64_t* 
     return check_launch("k_merge");
 }
 
+// ================================================================ dense private runs
+// MODE 0 over packed records when a private run is dense: its keys step by
+// exactly one (R[k+1] = R[k] + 1 -- the primary-key side of an FK join, or a
+// range partition of one).  Merging a sorted S window against such a run
+// needs no merge walk: the R tuple of public key k sits at index k - key(R[0]),
+// and every S tuple of the window [lb(key(R[0])), ub(key(R[n-1]))) has one.
+//   k_dense_check  one read of each private run: dense or not (a run out of
+//                  order is never dense; it takes the merge walk, which
+//                  flags it), and key(R[0])
+//   k_blk_bounds   each dense run cut into blocks of K tuples; per block b
+//                  and public run j the lower bound L(b, j) of the block's
+//                  first key inside the pair's window (b = 0: the window
+//                  start, b = nblk: its end)
+//   k_blk_count / k_scan_i64 / k_blk_tiles
+//                  tiles per block: ceil(S tuples of the block / DJ_TW)
+//   k_dense_join   persistent CTAs, one producer warp: per tile the R block
+//                  and the tile's share of the block's S pieces from ALL
+//                  public runs arrive by TMA (two stages, full/empty
+//                  mbarriers); 8 consumer warps take 64-tuple chunks: load,
+//                  index, gather the R tuple from shared memory, aggregate.
+// With T public runs the R block is staged once for all of them (the merge
+// path reads every R tuple once per (i, j) pair, T times), and the work per
+// tile is proportional to its S tuples.  The Run order check covers every
+// adjacent S pair of the windows: lane shuffles inside a piece, the staged
+// tuple before each piece, block bounds that must not decrease, and every S
+// key inside its block's key range.  Per-pair COUNT / MAX / checksum are
+// reduced per warp and piece into shared accumulators of the CTA's current
+// private run, flushed with one atomic per pair when the run changes.
+constexpr int DJ_WARPS = 8;  // consumer warps; one more warp produces
+constexpr int DJ_THREADS = 32 * (DJ_WARPS + 1);
+#ifndef MPSM_DJ_TW
+#define MPSM_DJ_TW 4096
+#endif
+constexpr int DJ_TW = MPSM_DJ_TW;  // S tuples per tile (at most)
+#ifndef MPSM_DJ_KMAX
+#define MPSM_DJ_KMAX 2048
+#endif
+constexpr int DJ_KMAX = MPSM_DJ_KMAX;  // R tuples per block (at most)
+#ifndef MPSM_DJ_STAGES
+#define MPSM_DJ_STAGES 2
+#endif
+constexpr int DJ_STAGES = MPSM_DJ_STAGES;
+constexpr int DJ_MAXRUNS = 64;     // runs per side on this path
+#ifndef MPSM_DJ_CHUNK
+#define MPSM_DJ_CHUNK 128
+#endif
+constexpr int DJ_CHUNK = MPSM_DJ_CHUNK;  // S tuples per warp step
+constexpr int DJ_U = DJ_CHUNK / 32;       // per lane
+#ifndef MPSM_DJ_FMA  // pair_hash32_mix's FMA-pipe share (bit 5: the checksum adds as mad chains)
+#define MPSM_DJ_FMA 5
+#endif
+
+struct DjTile {
+    int32_t e;  // block entry
+    int32_t q;  // which share of the entry's S tuples
+};
+
+struct alignas(16) DjStage {
+    uint64_t r[DJ_KMAX + 4];                             // R block (aligned superset)
+    uint64_t w[DJ_TW + 3 * DJ_MAXRUNS + 2 * DJ_CHUNK];  // pieces (aligned supersets + prior tuple) + over-read slack
+    int poff[DJ_MAXRUNS], pn[DJ_MAXRUNS], pj[DJ_MAXRUNS], phas[DJ_MAXRUNS];
+    int pcb[DJ_MAXRUNS + 1];  // exclusive chunk offsets of the pieces
+    int npieces, i, r0, nb;
+    uint64_t kblk;  // normalized key of the block's first R tuple
+};
+struct DjSmem {
+    DjStage st[DJ_STAGES];
+    uint64_t full[DJ_STAGES], empty[DJ_STAGES];
+    unsigned long long acc_cnt[DJ_MAXRUNS], acc_best[DJ_MAXRUNS], acc_csum[DJ_MAXRUNS];
+    mpsm_run_t priv[DJ_MAXRUNS];
+    int64_t blk_base[DJ_MAXRUNS + 1];
+    uint64_t kb[DJ_MAXRUNS];
+    uint32_t fmak[5];  // FmaK, read back through volatile loads
+};
+
+struct DjArgs {
+    const mpsm_run_t* priv;
+    const mpsm_run_t* pub;
+    int n_priv, n_pub;
+    int64_t K;                // R tuples per block
+    int64_t nent;             // block entries (nblk + 1 per private run)
+    uint32_t* nondense;       // per private run
+    uint64_t* kb;             // per private run: normalized key of R[0]
+    const int64_t* blk_base;  // per private run: its first entry (n_priv + 1)
+    const PairWin* win;
+    int64_t* L;       // [nent][n_pub] piece bounds
+    int64_t* tb;      // [nent + 1] first tile of each entry
+    int32_t* nsub;    // [nent] tiles of each entry
+    int64_t* part;    // per 1024 entries: tiles (k_blk_count), then their offsets
+    DjTile* tiles;
+    int64_t* ntiles;
+    uint64_t* out_pairs;
+    PackInfo pi;
+};
+
+__device__ __forceinline__ int dj_run_of(const int64_t* __restrict__ blk_base, int n_priv, int64_t e) {
+    int lo = 0, hi = n_priv - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (blk_base[mid] <= e) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+// per private run: nondense[i] = 1 unless every key steps by one; kb[i] =
+// normalized key of R[0].  Each warp checks 128 consecutive records per step
+// (four loads in flight per lane).
+__global__ void __launch_bounds__(256) k_dense_check(const mpsm_run_t* __restrict__ priv, int pw,
+                                                     uint32_t* __restrict__ nondense, uint64_t* __restrict__ kb) {
+    const int i = blockIdx.y;
+    const mpsm_run_t r = priv[i];
+    const int lane = threadIdx.x & 31;
+    if (r.n <= 0) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) nondense[i] = 1;
+        return;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) kb[i] = r.keys[0] >> pw;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    bool bad = false;
+    for (int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c * 128 < r.n - 1; c += nw) {
+        const int64_t k0 = c * 128;
+        uint64_t v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t k = k0 + u * 32 + lane;
+            v[u] = k < r.n ? ld_stream(r.keys + k) : 0;
+        }
+        const int64_t kn = k0 + 128;
+        const uint64_t tail = (lane == 31 && kn < r.n) ? r.keys[kn] : 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            uint64_t nx = __shfl_down_sync(0xffffffffu, v[u], 1);
+            const uint64_t first_next = __shfl_sync(0xffffffffu, v[u < 3 ? u + 1 : 3], 0);
+            if (lane == 31) nx = u < 3 ? first_next : tail;
+            const int64_t k = k0 + u * 32 + lane;
+            if (k + 1 < r.n) bad |= ((nx >> pw) - (v[u] >> pw)) != 1;
+        }
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&nondense[i], 1u);
+}
+
+__global__ void k_blk_bounds(DjArgs a) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= a.nent * a.n_pub) return;
+    const int64_t e = t / a.n_pub;
+    const int j = (int)(t - e * a.n_pub);
+    const int i = dj_run_of(a.blk_base, a.n_priv, e);
+    int64_t v = 0;
+    if (!a.nondense[i]) {
+        const int64_t b = e - a.blk_base[i];
+        const int64_t nblk = a.blk_base[i + 1] - a.blk_base[i] - 1;
+        const PairWin w = a.win[(int64_t)i * a.n_pub + j];
+        if (b == 0) {
+            v = w.start;
+        } else if (b >= nblk) {
+            v = w.end;
+        } else {
+            const uint64_t key = a.kb[i] + (uint64_t)(b * a.K);
+            const uint64_t* sk = a.pub[j].keys;
+            const int pw = a.pi.pw;
+            int64_t lo = w.start, hi = w.end;
+            while (lo < hi) {
+                const int64_t mid = lo + ((hi - lo) >> 1);
+                if ((sk[mid] >> pw) < key) lo = mid + 1;
+                else hi = mid;
+            }
+            v = lo;
+        }
+    }
+    a.L[t] = v;
+}
+
+// tiles per entry (local exclusive offsets per 1024 entries + their totals);
+// decreasing bounds (a public run out of order) flag the pair
+__global__ void __launch_bounds__(1024) k_blk_count(DjArgs a) {
+    __shared__ int64_t s[1024];
+    const int64_t e = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+    int64_t ns = 0;
+    if (e < a.nent) {
+        const int i = dj_run_of(a.blk_base, a.n_priv, e);
+        const int64_t b = e - a.blk_base[i];
+        const int64_t nblk = a.blk_base[i + 1] - a.blk_base[i] - 1;
+        if (!a.nondense[i] && b < nblk) {
+            const int64_t* L0 = a.L + e * a.n_pub;
+            const int64_t* L1 = L0 + a.n_pub;
+            int64_t c = 0;
+            for (int j = 0; j < a.n_pub; ++j) {
+                const int64_t d = L1[j] - L0[j];
+                if (d < 0)
+                    atomicOr((unsigned long long*)(a.out_pairs + ((size_t)i * a.n_pub + j) * MPSM_PAIR_FIELDS +
+                                                   MPSM_PAIR_FLAGS),
+                             (unsigned long long)MPSM_FLAG_UNSORTED);
+                else c += d;
+            }
+            ns = (c + DJ_TW - 1) / DJ_TW;
+        }
+        a.nsub[e] = (int32_t)ns;
+    }
+    s[threadIdx.x] = ns;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+        const int64_t u = threadIdx.x >= off ? s[threadIdx.x - off] : 0;
+        __syncthreads();
+        s[threadIdx.x] += u;
+        __syncthreads();
+    }
+    if (e < a.nent) a.tb[e] = s[threadIdx.x] - ns;
+    if (threadIdx.x == 1023) a.part[blockIdx.x] = s[1023];
+}
+
+// in-place exclusive scan of v[0, n) (one CTA), *total = the sum
+__global__ void __launch_bounds__(1024) k_scan_i64(int64_t* __restrict__ v, int64_t n, int64_t* __restrict__ total) {
+    __shared__ int64_t s[1024];
+    __shared__ int64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < n; base += 1024) {
+        const int64_t p = base + threadIdx.x;
+        const int64_t x = p < n ? v[p] : 0;
+        s[threadIdx.x] = x;
+        __syncthreads();
+        for (int off = 1; off < 1024; off <<= 1) {
+            const int64_t u = threadIdx.x >= off ? s[threadIdx.x - off] : 0;
+            __syncthreads();
+            s[threadIdx.x] += u;
+            __syncthreads();
+        }
+        if (p < n) v[p] = carry + s[threadIdx.x] - x;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry += s[1023];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void k_blk_tiles(DjArgs a) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= a.nent) return;
+    const int64_t base = a.tb[e] + a.part[e / 1024];
+    a.tb[e] = base;
+    if (e == a.nent - 1) a.tb[a.nent] = *a.ntiles;
+    const int32_t ns = a.nsub[e];
+    for (int32_t q = 0; q < ns; ++q) a.tiles[base + q] = DjTile{(int32_t)e, q};
+}
+
+template <bool K32, bool SW>
+__global__ void __launch_bounds__(DJ_THREADS, 2) k_dense_join(DjArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    DjSmem& sm = *reinterpret_cast<DjSmem*>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t ntiles = *a.ntiles;
+    const int64_t G = gridDim.x;
+    if ((int64_t)blockIdx.x >= ntiles) return;
+    const int n_pub = a.n_pub, n_priv = a.n_priv;
+    if (tid == 0) {
+        for (int q = 0; q < DJ_STAGES; ++q) {
+            mbar_init(&sm.full[q], 1);
+            mbar_init(&sm.empty[q], DJ_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int q = tid; q < DJ_MAXRUNS; q += DJ_THREADS) sm.acc_cnt[q] = sm.acc_best[q] = sm.acc_csum[q] = 0;
+    for (int q = tid; q < n_priv; q += DJ_THREADS) {
+        sm.priv[q] = a.priv[q];
+        sm.kb[q] = a.kb[q];
+    }
+    for (int q = tid; q <= n_priv; q += DJ_THREADS) sm.blk_base[q] = a.blk_base[q];
+    if (tid == 0) {
+        sm.fmak[0] = 1u << 17;
+        sm.fmak[1] = 1u << 2;
+        sm.fmak[2] = 1u << 5;
+        sm.fmak[3] = 1u << 1;
+        sm.fmak[4] = 1u;
+    }
+    __syncthreads();
+    const int pw = a.pi.pw;
+    if (warp == DJ_WARPS) {
+        // ---- producer.  Software-pipelined: the descriptor of tile k + 2
+        // and the bounds rows of tile k + 1 are in flight while tile k's
+        // pieces are placed and its copies issued.
+        const unsigned lt = lanemask_lt();
+        struct Rows {
+            DjTile t;
+            int64_t tb0, tb1, l0[2], l1[2];
+        };
+        auto load_rows = [&](const DjTile& t) {
+            Rows r;
+            r.t = t;
+            r.tb0 = a.tb[t.e];
+            r.tb1 = a.tb[t.e + 1];
+            const int64_t* L0 = a.L + (int64_t)t.e * n_pub;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = lane + 32 * h;
+                r.l0[h] = j < n_pub ? L0[j] : 0;
+                r.l1[h] = j < n_pub ? L0[n_pub + j] : 0;
+            }
+            return r;
+        };
+        Rows cur = load_rows(a.tiles[blockIdx.x]);
+        DjTile t_nxt = blockIdx.x + G < ntiles ? a.tiles[blockIdx.x + G] : DjTile{0, 0};
+        int it = 0;
+        for (int64_t g = blockIdx.x; g < ntiles; g += G, ++it) {
+            Rows nxt;
+            const bool more = g + G < ntiles;
+            if (more) nxt = load_rows(t_nxt);
+            if (g + 2 * G < ntiles) t_nxt = a.tiles[g + 2 * G];
+            const int s = it % DJ_STAGES;
+            DjStage& st = sm.st[s];
+            const DjTile t = cur.t;
+            const int i = dj_run_of(sm.blk_base, n_priv, t.e);
+            const int64_t b = t.e - sm.blk_base[i];
+            const mpsm_run_t R = sm.priv[i];
+            const int64_t r_first = b * a.K;
+            const int nb = (int)min(a.K, R.n - r_first);
+            const int64_t nsub = cur.tb1 - cur.tb0;
+            // public run j = lane + 32 h: its piece of the block, then this
+            // tile's share [c0, c1) of the block's pieces in run order
+            int64_t c[2], P[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                c[h] = max(cur.l1[h] - cur.l0[h], (int64_t)0);
+                P[h] = c[h];
+            }
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int64_t u0 = __shfl_up_sync(0xffffffffu, P[0], o), u1 = __shfl_up_sync(0xffffffffu, P[1], o);
+                if (lane >= o) {
+                    P[0] += u0;
+                    P[1] += u1;
+                }
+            }
+            P[1] += __shfl_sync(0xffffffffu, P[0], 31);
+            const int64_t total = __shfl_sync(0xffffffffu, P[1], 31);
+            const int64_t c0 = t.q * total / nsub, c1 = (t.q + 1) * total / nsub;
+            int n[2], hp[2], recs[2], chs[2];
+            Span sp[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t excl = P[h] - c[h];
+                const int64_t lo = max(excl, c0), hi = min(P[h], c1);
+                n[h] = hi > lo ? (int)(hi - lo) : 0;
+                const int64_t gs = cur.l0[h] + (lo - excl);
+                hp[h] = (n[h] > 0 && gs > 0) ? 1 : 0;
+                sp[h] = n[h] > 0 ? span_of(a.pub[lane + 32 * h].keys, gs - hp[h], n[h] + hp[h]) : Span{nullptr, 0, 0u};
+                recs[h] = (int)(sp[h].bytes / 8);
+                chs[h] = (n[h] + DJ_CHUNK - 1) / DJ_CHUNK;
+            }
+            const unsigned m0 = __ballot_sync(0xffffffffu, n[0] > 0), m1 = __ballot_sync(0xffffffffu, n[1] > 0);
+            const int slot0 = __popc(m0 & lt), slot1 = __popc(m0) + __popc(m1 & lt);
+            const int np = __popc(m0) + __popc(m1);
+            // stage positions and chunk offsets: exclusive scans in run order
+            int rp[2] = {recs[0], recs[1]}, cp[2] = {chs[0], chs[1]};
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int a0 = __shfl_up_sync(0xffffffffu, rp[0], o), a1 = __shfl_up_sync(0xffffffffu, rp[1], o);
+                const int b0 = __shfl_up_sync(0xffffffffu, cp[0], o), b1 = __shfl_up_sync(0xffffffffu, cp[1], o);
+                if (lane >= o) {
+                    rp[0] += a0;
+                    rp[1] += a1;
+                    cp[0] += b0;
+                    cp[1] += b1;
+                }
+            }
+            rp[1] += __shfl_sync(0xffffffffu, rp[0], 31);
+            cp[1] += __shfl_sync(0xffffffffu, cp[0], 31);
+            const int nchunks = __shfl_sync(0xffffffffu, cp[1], 31);
+            const Span rs = span_of(R.keys, r_first, nb);
+            unsigned tx = sp[0].bytes + sp[1].bytes;
+            tx = warp_sum(tx) + rs.bytes;
+            // the tile is placed; now wait for its stage
+            if (it >= DJ_STAGES) mbar_wait(&sm.empty[s], ((it / DJ_STAGES) - 1) & 1);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (n[h] > 0) {
+                    const int slot = h ? slot1 : slot0;
+                    const int pos = rp[h] - recs[h];
+                    MPSM_CHECK(slot < DJ_MAXRUNS && pos + recs[h] <= DJ_TW + 3 * DJ_MAXRUNS);
+                    st.poff[slot] = pos + sp[h].off + hp[h];
+                    st.pn[slot] = n[h];
+                    st.pj[slot] = lane + 32 * h;
+                    st.phas[slot] = hp[h];
+                    st.pcb[slot] = cp[h] - chs[h];
+                }
+            }
+            if (lane == 0) {
+                st.pcb[np] = nchunks;
+                st.npieces = np;
+                st.i = i;
+                st.nb = nb;
+                st.r0 = rs.off;
+                st.kblk = sm.kb[i] + (uint64_t)r_first;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive_expect_tx(&sm.full[s], tx);
+            __syncwarp();
+            if (lane == 0 && rs.bytes) bulk_load(st.r, rs.src, rs.bytes, &sm.full[s]);
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                if (n[h] > 0) bulk_load(st.w + (rp[h] - recs[h]), sp[h].src, sp[h].bytes, &sm.full[s]);
+            if (more) cur = nxt;
+        }
+        return;
+    }
+    // ---- consumers.  Per-lane COUNT / MAX / checksum of the warp's current
+    // pair stay in registers across chunks and tiles; they are reduced into
+    // the CTA's shared accumulators when the pair changes.
+    using KT = typename std::conditional<K32, uint32_t, uint64_t>::type;
+    const uint32_t kmask = a.pi.kmask;
+    const uint64_t pmask = a.pi.pmask;
+    const uint32_t pmask32 = (uint32_t)pmask;
+    auto nk = [&](uint64_t v) -> KT {
+        if (K32) return (KT)((uint32_t)(v >> 32) >> (pw - 32));
+        return (KT)(v >> pw);
+    };
+    int cur_i = -1, acc_j = -1;
+    uint64_t best = 0, csum = 0;
+    int64_t cnt = 0;  // warp-uniform
+    bool bad = false;
+    auto flush_regs = [&]() {
+        if (acc_j < 0) return;
+        const uint64_t cs = warp_sum(csum);
+        const uint64_t bs = warp_max_u64(best);
+        const bool anybad = __any_sync(0xffffffffu, bad);
+        if (lane == 0) {
+            if (cnt) {
+                atomicAdd(&sm.acc_cnt[acc_j], (unsigned long long)cnt);
+                atomicMax(&sm.acc_best[acc_j], (unsigned long long)bs);
+                atomicAdd(&sm.acc_csum[acc_j], (unsigned long long)cs);
+            }
+            if (anybad)
+                atomicOr((unsigned long long*)(a.out_pairs + ((size_t)cur_i * n_pub + acc_j) * MPSM_PAIR_FIELDS +
+                                               MPSM_PAIR_FLAGS),
+                         (unsigned long long)MPSM_FLAG_UNSORTED);
+        }
+        best = csum = 0;
+        cnt = 0;
+        bad = false;
+        acc_j = -1;
+    };
+    auto flush_runs = [&](int ci) {
+        named_bar_sync(1, DJ_WARPS * 32);
+        if (warp == 0) {
+            for (int j = lane; j < n_pub; j += 32) {
+                const unsigned long long cn = sm.acc_cnt[j];
+                if (cn) {
+                    uint64_t* o = a.out_pairs + ((size_t)ci * n_pub + j) * MPSM_PAIR_FIELDS;
+                    atomicAdd((unsigned long long*)(o + MPSM_PAIR_COUNT), cn);
+                    atomicMax((unsigned long long*)(o + MPSM_PAIR_BEST), sm.acc_best[j]);
+                    atomicAdd((unsigned long long*)(o + MPSM_PAIR_CHECKSUM), sm.acc_csum[j]);
+                }
+                sm.acc_cnt[j] = sm.acc_best[j] = sm.acc_csum[j] = 0;
+            }
+        }
+        named_bar_sync(1, DJ_WARPS * 32);
+    };
+    // hash + sum of one matched pair of low words / full payloads
+    FmaK fk;
+    {
+        uint32_t* kp = &fk.m17;
+        for (int q = 0; q < 5; ++q)
+            asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(kp[q]) : "r"(smem_addr(&sm.fmak[q])));
+    }
+    auto agg32 = [&](uint32_t rp, uint32_t sp, uint64_t& h, uint64_t& sum) {
+        h = SW ? pair_hash32_mix<MPSM_DJ_FMA>(sp, rp, fk) : pair_hash32_mix<MPSM_DJ_FMA>(rp, sp, fk);
+        sum = (uint64_t)rp + sp;
+    };
+    auto agg64 = [&](uint64_t rp, uint64_t sp, uint64_t& h, uint64_t& sum) {
+        h = SW ? pair_hash(sp, rp) : pair_hash(rp, sp);
+        sum = rp + sp;
+    };
+    int it = 0;
+    for (int64_t g = blockIdx.x; g < ntiles; g += G, ++it) {
+        const int s = it % DJ_STAGES;
+        mbar_wait(&sm.full[s], (it / DJ_STAGES) & 1);
+        const DjStage& st = sm.st[s];
+        const int i = st.i;
+        if (i != cur_i) {
+            flush_regs();
+            if (cur_i >= 0) flush_runs(cur_i);
+            cur_i = i;
+        }
+        const int C = st.pcb[st.npieces];
+        const int cb = warp * C / DJ_WARPS, ce = (warp + 1) * C / DJ_WARPS;
+        const uint64_t* RB = st.r + st.r0;
+        const uint64_t* W = st.w;
+        const KT kblk = (KT)st.kblk;
+        const KT nbk = (KT)st.nb, nbm1 = nbk - 1;
+        int c = cb;
+        int p = 0;
+        if (c < ce)
+            while (st.pcb[p + 1] <= c) ++p;
+        while (c < ce) {
+            // the warp's chunks of piece p
+            const int off = st.poff[p], n = st.pn[p], pc = st.pcb[p], pe = min(st.pcb[p + 1], ce);
+            const int j = st.pj[p];
+            if (j != acc_j) {
+                flush_regs();
+                acc_j = j;
+            }
+            int k0 = (c - pc) * DJ_CHUNK;
+            // key of the tuple before the chunk (the staged prior of the
+            // piece, or the previous chunk's last)
+            KT carry = (k0 > 0 || st.phas[p]) ? nk(W[off + k0 - 1]) : (KT)0;
+            for (; c < pe; ++c, k0 += DJ_CHUNK) {
+                // DJ_U tuples per lane: element u of lane l is k0 + 32 u + l
+                const int rem = n - k0;
+                uint64_t wv[DJ_U], rv[DJ_U];
+                KT kk[DJ_U], dd[DJ_U];
+#pragma unroll
+                for (int u = 0; u < DJ_U; ++u) {
+                    wv[u] = W[off + k0 + 32 * u + lane];
+                    kk[u] = nk(wv[u]);
+                    dd[u] = kk[u] - kblk;
+                }
+                MPSM_CHECK(off + k0 + DJ_CHUNK - 32 + lane < DJ_TW + 3 * DJ_MAXRUNS + 2 * DJ_CHUNK);
+#pragma unroll
+                for (int u = 0; u < DJ_U; ++u) rv[u] = RB[min(dd[u], nbm1)];
+                // the order check: each key against the one before it
+                KT pk[DJ_U];
+#pragma unroll
+                for (int u = 0; u < DJ_U; ++u) {
+                    pk[u] = __shfl_up_sync(0xffffffffu, kk[u], 1);
+                    const KT last = u ? __shfl_sync(0xffffffffu, kk[u - 1], 31) : carry;
+                    if (lane == 0) pk[u] = last;
+                }
+                carry = __shfl_sync(0xffffffffu, kk[DJ_U - 1], 31);
+                bool wide = false;
+                if (K32 && kmask != 0) {
+                    uint32_t hiw = 0;
+#pragma unroll
+                    for (int u = 0; u < DJ_U; ++u) hiw |= (uint32_t)(wv[u] >> 32) | (uint32_t)(rv[u] >> 32);
+                    wide = __any_sync(0xffffffffu, (hiw & kmask) != 0);
+                }
+                uint64_t hh[DJ_U], ss[DJ_U];
+                if (!wide) {
+#pragma unroll
+                    for (int u = 0; u < DJ_U; ++u)
+                        agg32((uint32_t)rv[u] & pmask32, (uint32_t)wv[u] & pmask32, hh[u], ss[u]);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < DJ_U; ++u) agg64(rv[u] & pmask, wv[u] & pmask, hh[u], ss[u]);
+                }
+                if (rem >= DJ_CHUNK) {
+                    // a full chunk: every tuple matches (a key outside the
+                    // block or a step down is a run out of order: flagged)
+#pragma unroll
+                    for (int u = 0; u < DJ_U; ++u) {
+                        bad |= (pk[u] > kk[u]) | (dd[u] > nbm1);
+                        max_into(best, ss[u]);
+                        if (MPSM_DJ_FMA & 32) csum = mad_mask64(csum, hh[u], fk.one);
+                        else csum += hh[u];
+                    }
+                    cnt += DJ_CHUNK;
+                } else {
+#pragma unroll
+                    for (int u = 0; u < DJ_U; ++u) {
+                        const bool v = lane + 32 * u < rem;
+                        bad |= v && (pk[u] > kk[u] || dd[u] > nbm1);
+                        const uint32_t m = v ? 1u : 0u;
+                        max_into(best, ss[u] * m);
+                        csum = mad_mask64(csum, hh[u], m);
+                    }
+                    cnt += rem;
+                }
+            }
+            if (c < ce) ++p;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[s]);
+    }
+    flush_regs();
+    if (cur_i >= 0) flush_runs(cur_i);
+}
+
+static bool dj_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("MPSM_DENSE_JOIN");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
+// host plan of the dense-run path: block size, entries, tile bound
+struct DjPlan {
+    bool on = false;
+    int64_t K = 0, nent = 0, maxt = 0, nparts = 0;
+    std::vector<int64_t> blk_base;
+};
+static DjPlan dj_plan(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub) {
+    DjPlan p;
+    if (!dj_enabled() || n_priv < 1 || n_pub < 1 || n_priv > DJ_MAXRUNS || n_pub > DJ_MAXRUNS) return p;
+    int64_t nr = 0, ns = 0;
+    for (int i = 0; i < n_priv; ++i) nr += priv[i].n;
+    for (int j = 0; j < n_pub; ++j) ns += pub[j].n;
+    // blocks of about 0.8 DJ_TW S tuples when S spreads like R (one tile)
+    const double k = ns > 0 ? 0.8 * DJ_TW * (double)nr / (double)ns : (double)DJ_KMAX;
+    p.K = std::min<int64_t>(DJ_KMAX, std::max<int64_t>(64, (int64_t)std::min(k, (double)DJ_KMAX) & ~(int64_t)15));
+    p.blk_base.resize(n_priv + 1);
+    int64_t e = 0;
+    for (int i = 0; i < n_priv; ++i) {
+        p.blk_base[i] = e;
+        e += (std::max<int64_t>(priv[i].n, 0) + p.K - 1) / p.K + 1;
+    }
+    p.blk_base[n_priv] = e;
+    p.nent = e;
+    p.nparts = (e + 1023) / 1024;
+    // a tile per entry plus one per DJ_TW S tuples of the windows (each
+    // private run's windows hold at most all of S)
+    p.maxt = e + ((int64_t)n_priv * ns + DJ_TW - 1) / DJ_TW + 1;
+    p.on = p.maxt < (int64_t)INT32_MAX && e < (int64_t)INT32_MAX;
+    return p;
+}
+
+struct DjWs {
+    uint32_t* nondense;
+    uint64_t* kb;
+    int64_t* blk_base;
+    int64_t* L;
+    int64_t* tb;
+    int32_t* nsub;
+    int64_t* part;
+    DjTile* tiles;
+    int64_t* ntiles;
+};
+static bool carve_dj(Carve& c, int n_priv, int n_pub, const DjPlan& p, DjWs* o) {
+    o->nondense = c.take<uint32_t>(n_priv);
+    o->kb = c.take<uint64_t>(n_priv);
+    o->blk_base = c.take<int64_t>(n_priv + 1);
+    o->L = c.take<int64_t>((size_t)p.nent * n_pub);
+    o->tb = c.take<int64_t>(p.nent + 1);
+    o->nsub = c.take<int32_t>(p.nent);
+    o->part = c.take<int64_t>(p.nparts + 1);
+    o->tiles = c.take<DjTile>(p.maxt);
+    o->ntiles = c.take<int64_t>(1);
+    return c.ok;
+}
+
+static size_t join_ws_size(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub) {
+    const int64_t mt = max_tiles(priv, n_priv, pub, n_pub);
+    Carve c{nullptr, (size_t)-1};
+    JoinWs w;
+    carve_join(c, n_priv, n_pub, mt, &w);
+    const DjPlan dp = dj_plan(priv, n_priv, pub, n_pub);
+    if (dp.on) {
+        DjWs d;
+        carve_dj(c, n_priv, n_pub, dp, &d);
+    }
+    return c.off;
+}
+
+template <bool K32>
+static int launch_dense(const DjArgs& a, int swap, cudaStream_t st) {
+    static int attr = 0;
+    if (!attr) {
+        MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_dense_join<K32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)sizeof(DjSmem)),
+                             "smem attr"));
+        MPSM_TRY(cuda_status(cudaFuncSetAttribute(k_dense_join<K32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)sizeof(DjSmem)),
+                             "smem attr"));
+        attr = 1;
+    }
+    const int grid = num_sms() * 2;
+    ProfScope ps("dense_join", st);
+    if (swap) k_dense_join<K32, true><<<grid, DJ_THREADS, sizeof(DjSmem), st>>>(a);
+    else k_dense_join<K32, false><<<grid, DJ_THREADS, sizeof(DjSmem), st>>>(a);
+    return check_launch("k_dense_join");
+}
+
 template <bool PK>
 static int join_pairs_impl(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub, int swap, int mode,
                            uint64_t* d_out, int64_t cap, uint64_t* d_pairs, void* workspace, size_t ws_bytes,
@@ -1277,14 +1977,52 @@ static int join_pairs_impl(const mpsm_run_t* priv, int n_priv, const mpsm_run_t*
     const int npairs = n_priv * n_pub;
     const int64_t mt = max_tiles(priv, n_priv, pub, n_pub);
     JoinWs w;
-    if (!carve_join(Carve{(char*)workspace, ws_bytes}, n_priv, n_pub, mt, &w)) {
+    Carve cv{(char*)workspace, ws_bytes};
+    if (!carve_join(cv, n_priv, n_pub, mt, &w)) {
         set_error("join workspace too small");
         return MPSM_ERR_ARG;
     }
+    // the dense-run path: aggregates over packed records (the materialize
+    // modes walk the merge tiles of every pair)
+    DjPlan dp = dj_plan(priv, n_priv, pub, n_pub);
+    DjWs dw{};
+    const bool dense = PK && dp.on && (mode != MPSM_MODE_MATERIALIZE || d_out == nullptr) &&
+                       carve_dj(cv, n_priv, n_pub, dp, &dw);
     MPSM_TRY(cuda_status(cudaMemcpyAsync(w.d_priv, priv, sizeof(mpsm_run_t) * n_priv, cudaMemcpyHostToDevice, st), "h2d"));
     MPSM_TRY(cuda_status(cudaMemcpyAsync(w.d_pub, pub, sizeof(mpsm_run_t) * n_pub, cudaMemcpyHostToDevice, st), "h2d"));
-    k_windows<PK><<<(npairs + 127) / 128, 128, 0, st>>>(w.d_priv, n_priv, w.d_pub, n_pub, w.win, d_pairs, pi);
+    DjArgs da{};
+    if (dense) {
+        MPSM_TRY(cuda_status(cudaMemcpyAsync(dw.blk_base, dp.blk_base.data(), sizeof(int64_t) * (n_priv + 1),
+                                             cudaMemcpyHostToDevice, st),
+                             "h2d"));
+        MPSM_TRY(cuda_status(cudaMemsetAsync(dw.nondense, 0, sizeof(uint32_t) * n_priv, st), "memset"));
+        da = DjArgs{w.d_priv, w.d_pub, n_priv,   n_pub,   dp.K,      dp.nent,   dw.nondense, dw.kb,     dw.blk_base,
+                    w.win,    dw.L,    dw.tb,    dw.nsub, dw.part,   dw.tiles,  dw.ntiles,   d_pairs,   pi};
+        ProfScope ps("dense_check", st);
+        const dim3 grid((unsigned)std::max(1, num_sms() * 4 / n_priv), (unsigned)n_priv);
+        k_dense_check<<<grid, 256, 0, st>>>(w.d_priv, pi.pw, dw.nondense, dw.kb);
+        MPSM_TRY(check_launch("k_dense_check"));
+    }
+    k_windows<PK><<<(npairs + 127) / 128, 128, 0, st>>>(w.d_priv, n_priv, w.d_pub, n_pub, w.win, d_pairs, pi,
+                                                        dense ? dw.nondense : nullptr);
     MPSM_TRY(check_launch("k_windows"));
+    if (dense) {
+        {
+            ProfScope ps("dense_tiles", st);
+            const int64_t nb = dp.nent * n_pub;
+            k_blk_bounds<<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(da);
+            MPSM_TRY(check_launch("k_blk_bounds"));
+            k_blk_count<<<(unsigned)dp.nparts, 1024, 0, st>>>(da);
+            MPSM_TRY(check_launch("k_blk_count"));
+            k_scan_i64<<<1, 1024, 0, st>>>(dw.part, dp.nparts, dw.ntiles);
+            MPSM_TRY(check_launch("k_scan_i64"));
+            k_blk_tiles<<<(unsigned)((dp.nent + 255) / 256), 256, 0, st>>>(da);
+            MPSM_TRY(check_launch("k_blk_tiles"));
+        }
+        const bool k32d = (64 - pi.pw) <= 32;
+        if (k32d) MPSM_TRY(launch_dense<true>(da, swap, st));
+        else MPSM_TRY(launch_dense<false>(da, swap, st));
+    }
     k_tile_scan<<<1, 1024, 0, st>>>(w.win, npairs, w.total);
     MPSM_TRY(check_launch("k_tile_scan"));
     {
@@ -1329,7 +2067,7 @@ extern "C" int mpsm_dbg_mj_ts(long long* host, int ntiles) {
 extern "C" int mpsm_join_workspace_bytes(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub,
                                          size_t* bytes) {
     if (!bytes || n_priv < 0 || n_pub < 0) return MPSM_ERR_ARG;
-    *bytes = join_ws_size(n_priv, n_pub, max_tiles(priv, n_priv, pub, n_pub));
+    *bytes = join_ws_size(priv, n_priv, pub, n_pub);
     return MPSM_OK;
 }
 

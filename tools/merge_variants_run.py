@@ -38,14 +38,17 @@ for it in range(4):
     _lib.profile_enable(True)
     rec = D.join_pairs_packed(Rr, S, bits, 1, False, 0)
     torch.cuda.synchronize()
-    ms, n = _lib.profile_read("merge")
-    pm, _ = _lib.profile_read("merge_partition")
-    best = (ms, pm) if best is None else min(best, (ms, pm))
-print(f"{os.environ['VNAME']:12s} T={T} merge {best[0]:.3f} ms  ({4e9/best[0]/1e6:.0f} GB/s packed)  partition {best[1]:.3f} ms"
-      f"  count={int(rec[:, 0].sum().item())}")
+    names = ("merge", "merge_partition", "dense_check", "dense_tiles", "dense_join")
+    ms = tuple(_lib.profile_read(k)[0] for k in names)
+    best = ms if best is None or sum(ms) < sum(best) else best
+print(f"{os.environ['VNAME']:12s} T={T} " + "  ".join(f"{k} {v:.3f}" for k, v in zip(names, best)) +
+      f"  total {sum(best):.3f} ms  count={int(rec[:, 0].sum().item())}")
 '''
-for lib in sorted(glob.glob(os.path.join(ROOT, "build", "variants", "*", "libmpsm_b200.so"))):
-    name = os.path.basename(os.path.dirname(lib))
+libs = sorted(glob.glob(os.path.join(ROOT, "build", "variants", "*", "libmpsm_b200.so")))
+if os.environ.get("INTREE"):
+    libs = [os.path.join(ROOT, "paper_1207_0145_b200", "libmpsm_b200.so")]
+for lib in libs:
+    name = os.environ.get("INTREE") or os.path.basename(os.path.dirname(lib))
     for tj in os.environ.get("TJOINS", "1").split(","):
         env = dict(os.environ, MPSM_LIB=lib, ROOT=ROOT, VNAME=name, TJOIN=tj)
         r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True, timeout=300)

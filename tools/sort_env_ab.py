@@ -34,15 +34,15 @@ for it in range(5):
     D.sort_packed(keys, pays, 0, (1 << bits) - 1, bits, ok, tk, None, ovf)
     b.record(); torch.cuda.synchronize()
     res.append((a.elapsed_time(b), _lib.profile_read("seg_scatter"), _lib.profile_read("seg_count"),
-                _lib.profile_read("seg_scatter_sp"), _lib.profile_read("seg_scatter_pp")))
+                _lib.profile_read("seg_scatter_sp"), _lib.profile_read("seg_scatter_pp"), _lib.profile_read("seg_hist_all")))
 v = ok.view(torch.int64)
 k = torch.bitwise_right_shift(v, 64 - bits) & ((1 << bits) - 1)
 srt = bool((k[1:] >= k[:-1]).all())
 w = torch.arange(1, n + 1, device=dev, dtype=torch.int64)
 fp = (int(v.sum().item()) & (2**64 - 1), int((v * w).sum().item()) & (2**64 - 1))
-ms, sc, cn, sp, pp = min(res)
+ms, sc, cn, sp, pp, ha = min(res)
 print(f"{os.environ['VAR']}={os.environ[os.environ['VAR']]} total {ms:7.3f} ms  scatter {sc[0]:6.3f}/{sc[1]}"
-      f"  count {cn[0]:6.3f}/{cn[1]}  sp {sp[0]:6.3f}  pp {pp[0]:6.3f}/{pp[1]}  sorted={srt} fp={fp[0]:016x}:{fp[1]:016x}",
+      f"  count {cn[0]:6.3f}/{cn[1]}  hist_all {ha[0]:6.3f}  sp {sp[0]:6.3f}  pp {pp[0]:6.3f}/{pp[1]}  sorted={srt} fp={fp[0]:016x}:{fp[1]:016x}",
       flush=True)
 '''
 for v in vals:
