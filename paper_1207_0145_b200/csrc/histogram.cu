@@ -50,14 +50,25 @@ __global__ void __launch_bounds__(HIST_THREADS) k_radix_hist_smem(const uint64_t
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t tid0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     // the loop bound is warp-uniform so every lane reaches the warp collectives
-    const int64_t iters = (npairs + stride - 1) / stride;
+    // four pairs per thread and step in flight
+    constexpr int U = 4;
+    const int64_t iters = (npairs + U * stride - 1) / (U * stride);
     for (int64_t it = 0; it < iters; ++it) {
-        const int64_t q = tid0 + it * stride;
-        const bool valid = q < npairs;
-        ulonglong2 v = make_ulonglong2(lower, lower);
-        if (valid) v = __ldcs(reinterpret_cast<const ulonglong2*>(keys + head) + q);
-        hist_add(h, v.x, head + 2 * q, lower, span_m1, shift, nbuckets, d_bad, valid);
-        hist_add(h, v.y, head + 2 * q + 1, lower, span_m1, shift, nbuckets, d_bad, valid);
+        ulonglong2 v[U];
+        bool valid[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t q = tid0 + (it * U + u) * stride;
+            valid[u] = q < npairs;
+            v[u] = make_ulonglong2(lower, lower);
+            if (valid[u]) v[u] = __ldcs(reinterpret_cast<const ulonglong2*>(keys + head) + q);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t q = tid0 + (it * U + u) * stride;
+            hist_add(h, v[u].x, head + 2 * q, lower, span_m1, shift, nbuckets, d_bad, valid[u]);
+            hist_add(h, v[u].y, head + 2 * q + 1, lower, span_m1, shift, nbuckets, d_bad, valid[u]);
+        }
     }
     // the unpaired head / tail element
     if (blockIdx.x == 0 && threadIdx.x < 32) {

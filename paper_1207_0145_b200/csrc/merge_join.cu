@@ -1401,8 +1401,10 @@ __device__ __forceinline__ int dj_run_of(const int64_t* __restrict__ blk_base, i
 }
 
 // per private run: nondense[i] = 1 unless every key steps by one; kb[i] =
-// normalized key of R[0].  Each warp checks 128 consecutive records per step
-// (four loads in flight per lane).
+// normalized key of R[0].  Each warp checks 256 consecutive records per
+// step: four 16-B loads in flight per lane (record pairs), neighbours across
+// lanes by shuffles.  A run not 16-B aligned is checked from its second
+// record on, the first against it separately.
 __global__ void __launch_bounds__(256) k_dense_check(const mpsm_run_t* __restrict__ priv, int pw,
                                                      uint32_t* __restrict__ nondense, uint64_t* __restrict__ kb) {
     const int i = blockIdx.y;
@@ -1412,51 +1414,112 @@ __global__ void __launch_bounds__(256) k_dense_check(const mpsm_run_t* __restric
         if (blockIdx.x == 0 && threadIdx.x == 0) nondense[i] = 1;
         return;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) kb[i] = r.keys[0] >> pw;
-    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int64_t head = ((uintptr_t)r.keys & 15) ? 1 : 0;
     bool bad = false;
-    for (int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c * 128 < r.n - 1; c += nw) {
-        const int64_t k0 = c * 128;
-        uint64_t v[4];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        kb[i] = r.keys[0] >> pw;
+        if (head && r.n > 1) bad = ((r.keys[1] >> pw) - (r.keys[0] >> pw)) != 1;
+    }
+    const uint64_t* base = r.keys + head;
+    const int64_t n = r.n - head;  // records from the aligned one on
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c * 256 < n - 1; c += nw) {
+        const int64_t k0 = c * 256;
+        ulonglong2 v[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const int64_t k = k0 + u * 32 + lane;
-            v[u] = k < r.n ? ld_stream(r.keys + k) : 0;
+            const int64_t k = k0 + 64 * u + 2 * lane;
+            if (k + 1 < n) {
+                v[u] = __ldcs(reinterpret_cast<const ulonglong2*>(base + k));
+            } else {
+                v[u].x = k < n ? base[k] : 0;
+                v[u].y = 0;
+            }
         }
-        const int64_t kn = k0 + 128;
-        const uint64_t tail = (lane == 31 && kn < r.n) ? r.keys[kn] : 0;
+        const int64_t kn = k0 + 256;
+        const uint64_t tail = (lane == 31 && kn < n) ? base[kn] : 0;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            uint64_t nx = __shfl_down_sync(0xffffffffu, v[u], 1);
-            const uint64_t first_next = __shfl_sync(0xffffffffu, v[u < 3 ? u + 1 : 3], 0);
+            const int64_t k = k0 + 64 * u + 2 * lane;
+            uint64_t nx = __shfl_down_sync(0xffffffffu, v[u].x, 1);
+            const uint64_t first_next = __shfl_sync(0xffffffffu, v[u < 3 ? u + 1 : 3].x, 0);
             if (lane == 31) nx = u < 3 ? first_next : tail;
-            const int64_t k = k0 + u * 32 + lane;
-            if (k + 1 < r.n) bad |= ((nx >> pw) - (v[u] >> pw)) != 1;
+            if (k + 1 < n) bad |= ((v[u].y >> pw) - (v[u].x >> pw)) != 1;
+            if (k + 2 < n) bad |= ((nx >> pw) - (v[u].y >> pw)) != 1;
         }
     }
     if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(&nondense[i], 1u);
 }
 
+// two levels (as the merge partition): COARSE places the bound of every
+// DJ_COARSE-th block (and the run's end) by a search over the whole window,
+// the fine pass each other bound inside its coarse bracket
+constexpr int DJ_COARSE = 32;
+template <bool COARSE>
 __global__ void k_blk_bounds(DjArgs a) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= a.nent * a.n_pub) return;
     const int64_t e = t / a.n_pub;
     const int j = (int)(t - e * a.n_pub);
     const int i = dj_run_of(a.blk_base, a.n_priv, e);
+    const int64_t b = e - a.blk_base[i];
+    const int64_t nblk = a.blk_base[i + 1] - a.blk_base[i] - 1;
+    const bool coarse_entry = b % DJ_COARSE == 0 || b >= nblk;
+    if (COARSE != coarse_entry) return;
     int64_t v = 0;
     if (!a.nondense[i]) {
-        const int64_t b = e - a.blk_base[i];
-        const int64_t nblk = a.blk_base[i + 1] - a.blk_base[i] - 1;
         const PairWin w = a.win[(int64_t)i * a.n_pub + j];
         if (b == 0) {
             v = w.start;
         } else if (b >= nblk) {
             v = w.end;
+        } else if (!COARSE) {
+            // inside the bracket of the coarse bounds around b
+            const uint64_t key = a.kb[i] + (uint64_t)(b * a.K);
+            const uint64_t* sk = a.pub[j].keys;
+            const int pw = a.pi.pw;
+            const int64_t b0 = b - b % DJ_COARSE, b1 = min(b0 + DJ_COARSE, nblk);
+            int64_t lo = a.L[(a.blk_base[i] + b0) * a.n_pub + j], hi = a.L[(a.blk_base[i] + b1) * a.n_pub + j];
+            hi = max(hi, lo);
+            while (lo < hi) {
+                const int64_t mid = lo + ((hi - lo) >> 1);
+                if ((sk[mid] >> pw) < key) lo = mid + 1;
+                else hi = mid;
+            }
+            v = lo;
         } else {
             const uint64_t key = a.kb[i] + (uint64_t)(b * a.K);
             const uint64_t* sk = a.pub[j].keys;
             const int pw = a.pi.pw;
+            // lower bound of key in [start, end): interpolation steps
+            // alternating with halvings (a few probes on spread keys, at
+            // most twice the binary search's on any)
             int64_t lo = w.start, hi = w.end;
+            bool interp = true;
+            while (hi - lo > 16) {
+                int64_t mid;
+                if (interp) {
+                    const uint64_t klo = sk[lo] >> pw, khi = sk[hi - 1] >> pw;
+                    if (key <= klo) {
+                        hi = lo;
+                        break;
+                    }
+                    if (key > khi) {
+                        lo = hi;
+                        break;
+                    }
+                    const double f = (double)(key - klo) / (double)(khi - klo);
+                    mid = lo + (int64_t)(f * (double)(hi - 1 - lo));
+                    mid = min(max(mid, lo), hi - 1);
+                } else {
+                    mid = lo + ((hi - lo) >> 1);
+                }
+                const int64_t w0 = hi - lo;
+                if ((sk[mid] >> pw) < key) lo = mid + 1;
+                else hi = mid;
+                // keep interpolating while it more than halves the window
+                interp = !interp || 2 * (hi - lo) < w0;
+            }
             while (lo < hi) {
                 const int64_t mid = lo + ((hi - lo) >> 1);
                 if ((sk[mid] >> pw) < key) lo = mid + 1;
@@ -1717,8 +1780,16 @@ __global__ void __launch_bounds__(DJ_THREADS, 2) k_dense_join(DjArgs a) {
     bool bad = false;
     auto flush_regs = [&]() {
         if (acc_j < 0) return;
-        const uint64_t cs = warp_sum(csum);
-        const uint64_t bs = warp_max_u64(best);
+        // warp reductions as REDUX: the 64-bit sum from four 16-bit slices,
+        // the 64-bit max as the max high word, then the max low word under it
+        const uint32_t lo = (uint32_t)csum, hi = (uint32_t)(csum >> 32);
+        const uint64_t cs = (uint64_t)__reduce_add_sync(0xffffffffu, lo & 0xffffu) +
+                            ((uint64_t)__reduce_add_sync(0xffffffffu, lo >> 16) << 16) +
+                            ((uint64_t)__reduce_add_sync(0xffffffffu, hi & 0xffffu) << 32) +
+                            ((uint64_t)__reduce_add_sync(0xffffffffu, hi >> 16) << 48);
+        const uint32_t bh = __reduce_max_sync(0xffffffffu, (uint32_t)(best >> 32));
+        const uint32_t bl = __reduce_max_sync(0xffffffffu, (uint32_t)(best >> 32) == bh ? (uint32_t)best : 0u);
+        const uint64_t bs = ((uint64_t)bh << 32) | bl;
         const bool anybad = __any_sync(0xffffffffu, bad);
         if (lane == 0) {
             if (cnt) {
@@ -1892,8 +1963,14 @@ static DjPlan dj_plan(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub,
     int64_t nr = 0, ns = 0;
     for (int i = 0; i < n_priv; ++i) nr += priv[i].n;
     for (int j = 0; j < n_pub; ++j) ns += pub[j].n;
-    // blocks of about 0.8 DJ_TW S tuples when S spreads like R (one tile)
-    const double k = ns > 0 ? 0.8 * DJ_TW * (double)nr / (double)ns : (double)DJ_KMAX;
+    // the largest blocks: fewer bound searches, full tiles (a block's S
+    // tuples split into tiles of DJ_TW), larger pieces per public run
+    // (A/B, FK 100M x 400M: K = 819 / 1024 / 2048 -> join 1.57 / 1.63 / 1.46
+    // ms at T = 1, 2.47 / 2.51 / 2.07 ms at T = 16)
+    double k = DJ_KMAX;
+    if (const char* ev = getenv("MPSM_DJ_K")) k = atof(ev);
+    (void)nr;
+    (void)ns;
     p.K = std::min<int64_t>(DJ_KMAX, std::max<int64_t>(64, (int64_t)std::min(k, (double)DJ_KMAX) & ~(int64_t)15));
     p.blk_base.resize(n_priv + 1);
     int64_t e = 0;
@@ -2010,10 +2087,18 @@ static int join_pairs_impl(const mpsm_run_t* priv, int n_priv, const mpsm_run_t*
         {
             ProfScope ps("dense_tiles", st);
             const int64_t nb = dp.nent * n_pub;
-            k_blk_bounds<<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(da);
-            MPSM_TRY(check_launch("k_blk_bounds"));
-            k_blk_count<<<(unsigned)dp.nparts, 1024, 0, st>>>(da);
-            MPSM_TRY(check_launch("k_blk_count"));
+            {
+                ProfScope ps1("dense_bounds", st);
+                k_blk_bounds<true><<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(da);
+                MPSM_TRY(check_launch("k_blk_bounds"));
+                k_blk_bounds<false><<<(unsigned)((nb + 255) / 256), 256, 0, st>>>(da);
+                MPSM_TRY(check_launch("k_blk_bounds"));
+            }
+            {
+                ProfScope ps2("dense_count", st);
+                k_blk_count<<<(unsigned)dp.nparts, 1024, 0, st>>>(da);
+                MPSM_TRY(check_launch("k_blk_count"));
+            }
             k_scan_i64<<<1, 1024, 0, st>>>(dw.part, dp.nparts, dw.ntiles);
             MPSM_TRY(check_launch("k_scan_i64"));
             k_blk_tiles<<<(unsigned)((dp.nent + 255) / 256), 256, 0, st>>>(da);

@@ -186,6 +186,31 @@ struct Segs {
     __device__ __forceinline__ int64_t ntiles(int64_t TL) const { return nseg == 0 ? (n + TL - 1) / TL : tb[nseg]; }
 };
 
+// Segs::tile for one thread that asks for increasing tiles (the tile
+// fetcher of a scatter CTA): the current segment's geometry stays in
+// registers, so a fetch costs no dependent loads unless the segment changes
+struct SegCursor {
+    int s = -1;
+    int64_t tb0 = 0, tb1 = 0, off0 = 0, off1 = 0, gb0 = 0;
+    __device__ __forceinline__ void tile(const Segs& sg, int64_t t, int64_t TL, int64_t& start, int& cnt, int64_t& g) {
+        if (sg.nseg == 0) {
+            sg.tile(t, TL, start, cnt, g);
+            return;
+        }
+        if (s < 0 || t < tb0 || t >= tb1) {
+            s = (s >= 0 && t >= tb1 && t < sg.tb[s + 2 <= sg.nseg ? s + 2 : sg.nseg]) ? s + 1 : sg.seg_of(sg.tb, t);
+            tb0 = sg.tb[s];
+            tb1 = sg.tb[s + 1];
+            off0 = sg.off[s];
+            off1 = sg.off[s + 1];
+            gb0 = sg.gb[s];
+        }
+        start = off0 + (t - tb0) * TL;
+        cnt = (int)min(TL, off1 - start);
+        g = gb0 + (t - tb0) / sg.tpc;
+    }
+};
+
 // ------------------------------------------------------------------ count
 // counts[g][d] for segment g, and for every tile t of the segment the
 // segment-local exclusive prefix toffs[t][d] (digit d's tuples in earlier
@@ -307,6 +332,7 @@ __global__ void __launch_bounds__(MAX_BINS) k_scan_mseg(const uint32_t* __restri
     const int64_t g0 = sg.gb[s], g1 = sg.gb[s + 1];
     const bool mine = d < nbins;
     int64_t tot = 0;
+#pragma unroll 16
     for (int64_t g = g0; g < g1; ++g) tot += mine ? counts[(size_t)g * nbins + d] : 0;
     int64_t incl = tot;
 #pragma unroll
@@ -319,6 +345,7 @@ __global__ void __launch_bounds__(MAX_BINS) k_scan_mseg(const uint32_t* __restri
     int64_t run = sg.off[s] + incl - tot;
     for (int w = 0; w < warp; ++w) run += wsum[w];
     if (!mine) return;
+#pragma unroll 16
     for (int64_t g = g0; g < g1; ++g) {  // second read hits L2
         const uint32_t c = counts[(size_t)g * nbins + d];
         base[(size_t)g * nbins + d] = run;
@@ -490,10 +517,11 @@ __global__ void __launch_bounds__(THREADS, LCfg<LAYOUT>::BLOCKS) k_scatter(
 
     // thread 0: one mbarrier phase brings tile t's tuples and its digit
     // prefixes into buffer bb
+    SegCursor cur;  // the fetching thread's
     auto fetch = [&](int bb, int64_t t) {
         int64_t t0, g;
         int cnt;
-        sg.tile(t, TL, t0, cnt, g);
+        cur.tile(sg, t, TL, t0, cnt, g);
         const int offk = (int)(((uintptr_t)(in_k + t0) >> 3) & 1);
         const int offp = NARR == 2 ? (int)(((uintptr_t)(in_p + t0) >> 3) & 1) : 0;
         sm.tile[bb] = t;
@@ -741,10 +769,11 @@ __global__ void __launch_bounds__(WsCfg<LAYOUT>::THREADS_ALL, 1) k_scatter_ws(
     const bool ranker = tid < THREADS;
     const bool mine = tid < nbins;
 
+    SegCursor cur;  // the fetching thread's
     auto fetch = [&](int bb, int64_t t) {
         int64_t t0, g;
         int cnt;
-        sg.tile(t, TL, t0, cnt, g);
+        cur.tile(sg, t, TL, t0, cnt, g);
         const int offk = (int)(((uintptr_t)(in_k + t0) >> 3) & 1);
         const int offp = NARR == 2 ? (int)(((uintptr_t)(in_p + t0) >> 3) & 1) : 0;
         sm.tile[bb] = t;

@@ -216,6 +216,26 @@ PACK_RECORDS = os.environ.get("MPSM_PACK", "1") != "0"
 # MPSM_HOST_PACK=0 copies the columns instead.
 HOST_PACK = os.environ.get("MPSM_HOST_PACK", "1") != "0"
 
+# device copies of the public runs' equi-height bound positions, per (device,
+# chunk layout, fanout, workers): a host -> device copy from pageable memory
+# would wait for the public sort queued before it
+_BOUND_POS: dict = {}
+
+
+def _bound_positions_device(chunks, f: int, t: int, dev) -> Optional[torch.Tensor]:
+    key = (str(dev), tuple(chunks), f, t)
+    pos = _BOUND_POS.get(key)
+    if pos is None:
+        parts = [bound_positions(b - a, f, t) + a for a, b in chunks if b > a]
+        if not parts:
+            return None
+        host = torch.from_numpy(np.concatenate(parts).astype(np.int64)).pin_memory()
+        pos = host.to(dev, non_blocking=True)
+        if len(_BOUND_POS) > 64:
+            _BOUND_POS.clear()
+        _BOUND_POS[key] = pos
+    return pos
+
 
 class _PackOverflow(Exception):
     """a payload does not fit the packed record: rerun on (key, payload) pairs"""
@@ -472,8 +492,8 @@ class JoinContext:
                 D.radix_histogram(self.priv_rec, 0, (1 << 64) - 1, self.pw + self.wbits - bits, nb, hist, None)
             else:
                 D.radix_histogram(self.priv_k, dom.lower, self.span_m1, self.wbits - bits, nb, hist, self.bad_priv)
-        pos_list = [torch.from_numpy(bound_positions(b - a, f, t) + a) for a, b in self.pub_chunks if b > a]
-        bk = self.pub_store[0].view(torch.int64)[torch.cat(pos_list).to(self.dev)] if pos_list else None
+        pos = _bound_positions_device(self.pub_chunks, f, t, self.dev)
+        bk = self.pub_store[0].view(torch.int64)[pos] if pos is not None else None
         h_hist = torch.empty(nb, dtype=torch.int64, pin_memory=True)
         h_hist.copy_(hist, non_blocking=True)
         h_bk = None

@@ -13,12 +13,13 @@ import paper_1207_0145_b200 as P  # noqa: E402
 from paper_1207_0145_b200.core import JoinConfig, KeyDomain, Relation  # noqa: E402
 
 n_r = int(sys.argv[1]) if len(sys.argv) > 1 else 100_000_000
+threads = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 dev = torch.device("cuda", 0)
 r = Relation((torch.randperm(n_r, device=dev) + 1).view(torch.uint64),
              torch.randint(0, 1 << 32, (n_r,), device=dev).view(torch.uint64))
 s = Relation(torch.randint(1, n_r + 1, (4 * n_r,), device=dev).view(torch.uint64),
              torch.randint(0, 1 << 32, (4 * n_r,), device=dev).view(torch.uint64))
-cfg = JoinConfig(key_domain=KeyDomain(1, n_r + 1))
+cfg = JoinConfig(threads=threads, key_domain=KeyDomain(1, n_r + 1))
 for _ in range(3):
     P.run_join(r, s, cfg)
 torch.cuda.synchronize()
@@ -37,3 +38,4 @@ for _ in range(5):
     P.run_join(r, s, cfg)
 pr.disable()
 pstats.Stats(pr).sort_stats("tottime").print_stats(18)
+pstats.Stats(pr).sort_stats("cumulative").print_stats(25)
