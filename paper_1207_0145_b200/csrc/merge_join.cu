@@ -1851,7 +1851,7 @@ __global__ void __launch_bounds__(DJ_THREADS, 2) k_dense_join(DjArgs a) {
         }
         const int C = st.pcb[st.npieces];
         const int cb = warp * C / DJ_WARPS, ce = (warp + 1) * C / DJ_WARPS;
-        const uint64_t* RB = st.r + st.r0;
+        const uint32_t rb_addr = smem_addr(st.r + st.r0);
         const uint64_t* W = st.w;
         const KT kblk = (KT)st.kblk;
         const KT nbk = (KT)st.nb, nbm1 = nbk - 1;
@@ -1868,32 +1868,28 @@ __global__ void __launch_bounds__(DJ_THREADS, 2) k_dense_join(DjArgs a) {
                 acc_j = j;
             }
             int k0 = (c - pc) * DJ_CHUNK;
-            // key of the tuple before the chunk (the staged prior of the
-            // piece, or the previous chunk's last)
-            KT carry = (k0 > 0 || st.phas[p]) ? nk(W[off + k0 - 1]) : (KT)0;
+            const bool has = st.phas[p] != 0;
             for (; c < pe; ++c, k0 += DJ_CHUNK) {
                 // DJ_U tuples per lane: element u of lane l is k0 + 32 u + l
                 const int rem = n - k0;
                 uint64_t wv[DJ_U], rv[DJ_U];
-                KT kk[DJ_U], dd[DJ_U];
+                KT kk[DJ_U], dd[DJ_U], pk[DJ_U];
 #pragma unroll
                 for (int u = 0; u < DJ_U; ++u) {
                     wv[u] = W[off + k0 + 32 * u + lane];
                     kk[u] = nk(wv[u]);
                     dd[u] = kk[u] - kblk;
+                    // the order check: each key against the one before it,
+                    // read from the stage (the piece's first tuple has its
+                    // staged prior, or none: W[off - 1] is then ignored)
+                    pk[u] = nk(W[off + k0 + 32 * u + lane - 1]);
                 }
+                if (lane == 0 && k0 == 0 && !has) pk[0] = 0;
                 MPSM_CHECK(off + k0 + DJ_CHUNK - 32 + lane < DJ_TW + 3 * DJ_MAXRUNS + 2 * DJ_CHUNK);
+                // R gathers through a 32-bit shared address (one IMAD each)
 #pragma unroll
-                for (int u = 0; u < DJ_U; ++u) rv[u] = RB[min(dd[u], nbm1)];
-                // the order check: each key against the one before it
-                KT pk[DJ_U];
-#pragma unroll
-                for (int u = 0; u < DJ_U; ++u) {
-                    pk[u] = __shfl_up_sync(0xffffffffu, kk[u], 1);
-                    const KT last = u ? __shfl_sync(0xffffffffu, kk[u - 1], 31) : carry;
-                    if (lane == 0) pk[u] = last;
-                }
-                carry = __shfl_sync(0xffffffffu, kk[DJ_U - 1], 31);
+                for (int u = 0; u < DJ_U; ++u)
+                    asm("ld.shared.u64 %0, [%1];" : "=l"(rv[u]) : "r"(rb_addr + 8u * (uint32_t)min(dd[u], nbm1)));
                 bool wide = false;
                 if (K32 && kmask != 0) {
                     uint32_t hiw = 0;
@@ -1903,9 +1899,11 @@ __global__ void __launch_bounds__(DJ_THREADS, 2) k_dense_join(DjArgs a) {
                 }
                 uint64_t hh[DJ_U], ss[DJ_U];
                 if (!wide) {
+                    // K32 (pw >= 32): the low word is the whole payload
 #pragma unroll
                     for (int u = 0; u < DJ_U; ++u)
-                        agg32((uint32_t)rv[u] & pmask32, (uint32_t)wv[u] & pmask32, hh[u], ss[u]);
+                        agg32(K32 ? (uint32_t)rv[u] : (uint32_t)rv[u] & pmask32,
+                              K32 ? (uint32_t)wv[u] : (uint32_t)wv[u] & pmask32, hh[u], ss[u]);
                 } else {
 #pragma unroll
                     for (int u = 0; u < DJ_U; ++u) agg64(rv[u] & pmask, wv[u] & pmask, hh[u], ss[u]);
