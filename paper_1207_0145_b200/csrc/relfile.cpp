@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "../../include/mpsm_b200.h"
+#include "hostcpu.h"
 
 namespace mpsm {
 void set_error(const std::string& msg);
@@ -71,7 +72,7 @@ bool pwrite_all(int fd, const char* src, size_t bytes, off_t off) {
 // returns false on an I/O error
 template <class F>
 bool parallel_ranges(uint64_t n, int threads, F fn) {
-    if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+    if (threads <= 0) threads = mpsm::usable_cores();
     const uint64_t per = std::max<uint64_t>((uint64_t)1 << 20, (n + threads - 1) / threads);
     std::vector<std::thread> pool;
     std::vector<char> ok;
@@ -143,7 +144,7 @@ extern "C" int mpsm_relfile_read(const char* path, uint64_t n, void* dst, int th
         return MPSM_ERR_IO;
     }
     const size_t bytes = (size_t)n * 16;
-    if (threads <= 0) threads = (int)std::max(1u, std::thread::hardware_concurrency());
+    if (threads <= 0) threads = mpsm::usable_cores();
     const size_t chunk = std::max<size_t>((size_t)64 << 20, (bytes + threads - 1) / threads);
     std::vector<std::thread> pool;
     std::vector<char> ok((bytes + chunk - 1) / chunk + 1, 1);

@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "hostcpu.h"
 
 namespace mpsm {
 
@@ -114,7 +115,7 @@ struct Uploader {
             // the copy is host-memory-bandwidth bound: 3/4 of the cores pack
             // (measured best on the 16-core GPU box: 12 -> 113 ms, 16 -> 121 ms
             // for cfg2's 500M tuples)
-            threads = e ? atoi(e) : (int)std::max(1u, std::thread::hardware_concurrency() * 3 / 4);
+            threads = e ? atoi(e) : std::max(1, usable_cores() * 3 / 4);
         }
         nslots = 2 * threads;
         slot.resize(nslots);
