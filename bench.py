@@ -347,7 +347,8 @@ def impl_ours(args):
     clocks.mark(w0, time.time())
     launches = _lib.launch_count() - l0
     ms = ev0.elapsed_time(ev1) / args.steps
-    prof = {k: _lib.profile_read(k) for k in ("seg_scatter", "seg_count", "merge", "merge_partition",
+    prof = {k: _lib.profile_read(k) for k in ("seg_scatter", "seg_scatter_sp", "seg_scatter_pp", "seg_count", "merge",
+                                              "merge_partition", "dense_check", "dense_tiles", "dense_join",
                                               "radix_histogram")}
     _lib.profile_enable(False)
     clk = clocks.stop()

@@ -163,16 +163,32 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// MPSM_MBAR_SUSPEND_NS > 0: try_wait with a suspend-time hint -- a waiting
+// warp sleeps until the phase completes (or the hint runs out) instead of
+// spinning through issue slots its SM sub-partition's working warps need
+#ifndef MPSM_MBAR_SUSPEND_NS
+#define MPSM_MBAR_SUSPEND_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
     unsigned done;
     do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(smem_addr(bar)), "r"(parity)
-            : "memory");
+        if (MPSM_MBAR_SUSPEND_NS > 0) {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(done)
+                : "r"(smem_addr(bar)), "r"(parity), "n"(MPSM_MBAR_SUSPEND_NS)
+                : "memory");
+        } else {
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(done)
+                : "r"(smem_addr(bar)), "r"(parity)
+                : "memory");
+        }
     } while (!done);
 }
 

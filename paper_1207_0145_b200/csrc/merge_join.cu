@@ -102,6 +102,20 @@ __device__ __forceinline__ uint64_t pair_hash32(uint32_t a, uint32_t b) {
 __device__ __forceinline__ void max_into(uint64_t& best, uint64_t v) {
     asm("{\n\t.reg .pred p;\n\tsetp.gt.u64 p, %1, %0;\n\t@p mov.b64 %0, %1;\n\t}" : "+l"(best) : "l"(v));
 }
+// MAX(r + s) of 32-bit payloads without 64-bit compares: the sums split by
+// the carry of the 32-bit add into two 32-bit maxima (b1: sums >= 2^32, h1
+// set once one occurred) -- an IADD3 with carry-out and predicated VIMNMX
+__device__ __forceinline__ void max33(uint32_t r, uint32_t s, uint32_t& b0, uint32_t& b1, uint32_t& h1) {
+    asm("{\n\t.reg .pred p;\n\t.reg .u32 t, c;\n\t"
+        "add.cc.u32 t, %3, %4;\n\t"
+        "addc.u32 c, 0, 0;\n\t"
+        "setp.ne.u32 p, c, 0;\n\t"
+        "@p max.u32 %1, %1, t;\n\t"
+        "@!p max.u32 %0, %0, t;\n\t"
+        "@p mov.u32 %2, 1;\n\t}"
+        : "+r"(b0), "+r"(b1), "+r"(h1)
+        : "r"(r), "r"(s));
+}
 // (a + b) * m, 64-bit, on the FMA pipe
 __device__ __forceinline__ uint64_t add_mask64(uint64_t a, uint64_t b, uint32_t m) {
     uint32_t lo, hi;
@@ -1323,8 +1337,18 @@ static int launch_merge(const JoinWs& w, int swap, uint64_t* d_pairs, uint64_t* 
 // key inside its block's key range.  Per-pair COUNT / MAX / checksum are
 // reduced per warp and piece into shared accumulators of the CTA's current
 // private run, flushed with one atomic per pair when the run changes.
-constexpr int DJ_WARPS = 8;  // consumer warps; one more warp produces
-constexpr int DJ_THREADS = 32 * (DJ_WARPS + 1);
+#ifndef MPSM_DJ_WARPS
+#define MPSM_DJ_WARPS 8
+#endif
+#ifndef MPSM_DJ_CTAS  // resident CTAs per SM
+#define MPSM_DJ_CTAS 2
+#endif
+constexpr int DJ_WARPS = MPSM_DJ_WARPS;  // consumer warps; DJ_NPROD more warps produce
+#ifndef MPSM_DJ_PRODUCERS  // producer warps, each placing every NPROD-th tile of the CTA
+#define MPSM_DJ_PRODUCERS 1
+#endif
+constexpr int DJ_NPROD = MPSM_DJ_PRODUCERS;
+constexpr int DJ_THREADS = 32 * (DJ_WARPS + DJ_NPROD);
 #ifndef MPSM_DJ_TW
 #define MPSM_DJ_TW 4096
 #endif
@@ -1343,6 +1367,16 @@ constexpr int DJ_MAXRUNS = 64;     // runs per side on this path
 #endif
 constexpr int DJ_CHUNK = MPSM_DJ_CHUNK;  // S tuples per warp step
 constexpr int DJ_U = DJ_CHUNK / 32;       // per lane
+#ifndef MPSM_DJ_CONSEC  // consumer lanes own 4 consecutive S tuples (16-B loads, in-lane order check)
+#define MPSM_DJ_CONSEC 1
+#endif
+static_assert(!MPSM_DJ_CONSEC || DJ_U == 4, "the consecutive consumer layout moves 4 tuples per lane");
+#ifndef MPSM_DJ_DYN  // consumer warps take a tile's chunks from a shared counter (else a static split)
+#define MPSM_DJ_DYN 0
+#endif
+#ifndef MPSM_DJ_GRAB  // chunks per take
+#define MPSM_DJ_GRAB 1
+#endif
 #ifndef MPSM_DJ_FMA  // pair_hash32_mix's FMA-pipe share (bit 5: the checksum adds as mad chains)
 #define MPSM_DJ_FMA 5
 #endif
@@ -1358,6 +1392,7 @@ struct alignas(16) DjStage {
     int poff[DJ_MAXRUNS], pn[DJ_MAXRUNS], pj[DJ_MAXRUNS], phas[DJ_MAXRUNS];
     int pcb[DJ_MAXRUNS + 1];  // exclusive chunk offsets of the pieces
     int npieces, i, r0, nb;
+    int next;       // MPSM_DJ_DYN: the next chunk a consumer warp takes
     uint64_t kblk;  // normalized key of the block's first R tuple
 };
 struct DjSmem {
@@ -1604,8 +1639,18 @@ __global__ void k_blk_tiles(DjArgs a) {
     for (int32_t q = 0; q < ns; ++q) a.tiles[base + q] = DjTile{(int32_t)e, q};
 }
 
+#ifdef MPSM_DBG_TIMING
+__device__ long long g_dj_ts[1 << 20][8];
+#define DJ_TS(who, gg, i) \
+    if (lane == 0 && (who) && (gg) < (1 << 20)) g_dj_ts[gg][i] = clock64();
+extern "C" int mpsm_dbg_dj_ts(long long* host, int ntiles) {
+    return cuda_status(cudaMemcpyFromSymbol(host, g_dj_ts, sizeof(long long) * 8 * (size_t)ntiles), "dbg");
+}
+#else
+#define DJ_TS(who, gg, i)
+#endif
 template <bool K32, bool SW>
-__global__ void __launch_bounds__(DJ_THREADS, 2) k_dense_join(DjArgs a) {
+__global__ void __launch_bounds__(DJ_THREADS, MPSM_DJ_CTAS) k_dense_join(DjArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     DjSmem& sm = *reinterpret_cast<DjSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1635,7 +1680,7 @@ __global__ void __launch_bounds__(DJ_THREADS, 2) k_dense_join(DjArgs a) {
     }
     __syncthreads();
     const int pw = a.pi.pw;
-    if (warp == DJ_WARPS) {
+    if (warp >= DJ_WARPS) {
         // ---- producer.  Software-pipelined: the descriptor of tile k + 2
         // and the bounds rows of tile k + 1 are in flight while tile k's
         // pieces are placed and its copies issued.
@@ -1658,14 +1703,21 @@ __global__ void __launch_bounds__(DJ_THREADS, 2) k_dense_join(DjArgs a) {
             }
             return r;
         };
-        Rows cur = load_rows(a.tiles[blockIdx.x]);
-        DjTile t_nxt = blockIdx.x + G < ntiles ? a.tiles[blockIdx.x + G] : DjTile{0, 0};
-        int it = 0;
-        for (int64_t g = blockIdx.x; g < ntiles; g += G, ++it) {
+        // producer pw places the CTA's tiles it = pw, pw + NPROD, ... (the
+        // placement is a chain of shuffles and dependent loads; with one
+        // producer it bounded the tile rate)
+        const int pw = warp - DJ_WARPS;
+        const int64_t GS = G * DJ_NPROD;
+        const int64_t g0 = blockIdx.x + (int64_t)pw * G;
+        if (g0 >= ntiles) return;
+        Rows cur = load_rows(a.tiles[g0]);
+        DjTile t_nxt = g0 + GS < ntiles ? a.tiles[g0 + GS] : DjTile{0, 0};
+        int it = pw;
+        for (int64_t g = g0; g < ntiles; g += GS, it += DJ_NPROD) {
             Rows nxt;
-            const bool more = g + G < ntiles;
+            const bool more = g + GS < ntiles;
             if (more) nxt = load_rows(t_nxt);
-            if (g + 2 * G < ntiles) t_nxt = a.tiles[g + 2 * G];
+            if (g + 2 * GS < ntiles) t_nxt = a.tiles[g + 2 * GS];
             const int s = it % DJ_STAGES;
             DjStage& st = sm.st[s];
             const DjTile t = cur.t;
@@ -1705,7 +1757,11 @@ __global__ void __launch_bounds__(DJ_THREADS, 2) k_dense_join(DjArgs a) {
                 hp[h] = (n[h] > 0 && gs > 0) ? 1 : 0;
                 sp[h] = n[h] > 0 ? span_of(a.pub[lane + 32 * h].keys, gs - hp[h], n[h] + hp[h]) : Span{nullptr, 0, 0u};
                 recs[h] = (int)(sp[h].bytes / 8);
-                chs[h] = (n[h] + DJ_CHUNK - 1) / DJ_CHUNK;
+                // CONSEC: a piece is consumed from the even stage slot at or
+                // below its first tuple (lead = 1 puts the tuple before it,
+                // prior or alignment slack, in front)
+                const int lead = MPSM_DJ_CONSEC ? ((sp[h].off + hp[h]) & 1) : 0;
+                chs[h] = n[h] > 0 ? (n[h] + lead + DJ_CHUNK - 1) / DJ_CHUNK : 0;
             }
             const unsigned m0 = __ballot_sync(0xffffffffu, n[0] > 0), m1 = __ballot_sync(0xffffffffu, n[1] > 0);
             const int slot0 = __popc(m0 & lt), slot1 = __popc(m0) + __popc(m1 & lt);
@@ -1730,7 +1786,9 @@ __global__ void __launch_bounds__(DJ_THREADS, 2) k_dense_join(DjArgs a) {
             unsigned tx = sp[0].bytes + sp[1].bytes;
             tx = warp_sum(tx) + rs.bytes;
             // the tile is placed; now wait for its stage
+            DJ_TS(true, g, 0)
             if (it >= DJ_STAGES) mbar_wait(&sm.empty[s], ((it / DJ_STAGES) - 1) & 1);
+            DJ_TS(true, g, 1)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 if (n[h] > 0) {
@@ -1747,6 +1805,7 @@ __global__ void __launch_bounds__(DJ_THREADS, 2) k_dense_join(DjArgs a) {
             if (lane == 0) {
                 st.pcb[np] = nchunks;
                 st.npieces = np;
+                st.next = 0;
                 st.i = i;
                 st.nb = nb;
                 st.r0 = rs.off;
@@ -1759,6 +1818,7 @@ __global__ void __launch_bounds__(DJ_THREADS, 2) k_dense_join(DjArgs a) {
 #pragma unroll
             for (int h = 0; h < 2; ++h)
                 if (n[h] > 0) bulk_load(st.w + (rp[h] - recs[h]), sp[h].src, sp[h].bytes, &sm.full[s]);
+            DJ_TS(true, g, 2)
             if (more) cur = nxt;
         }
         return;
@@ -1778,8 +1838,14 @@ __global__ void __launch_bounds__(DJ_THREADS, 2) k_dense_join(DjArgs a) {
     uint64_t best = 0, csum = 0;
     int64_t cnt = 0;  // warp-uniform
     bool bad = false;
+    uint32_t b0 = 0, b1 = 0, h1 = 0;  // max33 classes of the warp's current pair
     auto flush_regs = [&]() {
         if (acc_j < 0) return;
+        {
+            const uint64_t cb = h1 ? ((1ull << 32) | b1) : (uint64_t)b0;
+            if (cb > best) best = cb;
+            b0 = b1 = h1 = 0;
+        }
         // warp reductions as REDUX: the 64-bit sum from four 16-bit slices,
         // the 64-bit max as the max high word, then the max low word under it
         const uint32_t lo = (uint32_t)csum, hi = (uint32_t)(csum >> 32);
@@ -1841,7 +1907,9 @@ __global__ void __launch_bounds__(DJ_THREADS, 2) k_dense_join(DjArgs a) {
     int it = 0;
     for (int64_t g = blockIdx.x; g < ntiles; g += G, ++it) {
         const int s = it % DJ_STAGES;
+        DJ_TS(warp == 0, g, 3)
         mbar_wait(&sm.full[s], (it / DJ_STAGES) & 1);
+        DJ_TS(warp == 0, g, 4)
         const DjStage& st = sm.st[s];
         const int i = st.i;
         if (i != cur_i) {
@@ -1850,13 +1918,31 @@ __global__ void __launch_bounds__(DJ_THREADS, 2) k_dense_join(DjArgs a) {
             cur_i = i;
         }
         const int C = st.pcb[st.npieces];
-        const int cb = warp * C / DJ_WARPS, ce = (warp + 1) * C / DJ_WARPS;
         const uint32_t rb_addr = smem_addr(st.r + st.r0);
         const uint64_t* W = st.w;
         const KT kblk = (KT)st.kblk;
         const KT nbk = (KT)st.nb, nbm1 = nbk - 1;
-        int c = cb;
         int p = 0;
+        // the warp's chunks [cb, ce): with MPSM_DJ_DYN taken MPSM_DJ_GRAB at a
+        // time from the stage's counter until the tile is used up (the stage
+        // is released when its slowest warp is done: a static split left
+        // warps idle behind the slowest, tools/dj_timing.py), else one
+        // static share
+        for (int take = 0;; ++take) {
+        int cb, ce;
+        if (MPSM_DJ_DYN) {
+            int q = 0;
+            if (lane == 0) q = atomicAdd(&sm.st[s].next, MPSM_DJ_GRAB);
+            q = __shfl_sync(0xffffffffu, q, 0);
+            if (q >= C) break;
+            cb = q;
+            ce = min(q + MPSM_DJ_GRAB, C);
+        } else {
+            if (take > 0) break;
+            cb = warp * C / DJ_WARPS;
+            ce = (warp + 1) * C / DJ_WARPS;
+        }
+        int c = cb;
         if (c < ce)
             while (st.pcb[p + 1] <= c) ++p;
         while (c < ce) {
@@ -1869,6 +1955,98 @@ __global__ void __launch_bounds__(DJ_THREADS, 2) k_dense_join(DjArgs a) {
             }
             int k0 = (c - pc) * DJ_CHUNK;
             const bool has = st.phas[p] != 0;
+#if MPSM_DJ_CONSEC
+            // lane l owns the 4 consecutive stage slots base + k0 + 4l + u of
+            // the piece seen from the even slot base <= off (lead = 1: slot
+            // base is the tuple before the piece -- its prior, or with no
+            // prior (the run's first tuple) alignment slack, never aggregated)
+            const int lead = off & 1, base = off - lead, nv = n + lead;
+            const int lo_ok = lead - (has ? 1 : 0);  // pairs (v - 1, v) with v - 1 >= lo_ok are run neighbours
+            // key before the warp's first tuple here (0: nothing to check)
+            KT carry = 0;
+            if (k0 > 0) carry = nk(W[base + k0 - 1]);
+            else if (lead == 0 && has) carry = nk(W[base - 1]);
+            for (; c < pe; ++c, k0 += DJ_CHUNK) {
+                const int rem = nv - k0;
+                const uint64_t* wq = W + base + k0 + 4 * lane;
+                const ulonglong2 q0 = *reinterpret_cast<const ulonglong2*>(wq);
+                const ulonglong2 q1 = *reinterpret_cast<const ulonglong2*>(wq + 2);
+                const uint64_t wv[4] = {q0.x, q0.y, q1.x, q1.y};
+                uint64_t rv[4];
+                KT kk[4], dd[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    kk[u] = nk(wv[u]);
+                    dd[u] = kk[u] - kblk;
+                }
+                MPSM_CHECK(base + k0 + DJ_CHUNK <= DJ_TW + 3 * DJ_MAXRUNS + 2 * DJ_CHUNK);
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    asm("ld.shared.u64 %0, [%1];" : "=l"(rv[u]) : "r"(rb_addr + 8u * (uint32_t)min(dd[u], nbm1)));
+                KT prv = __shfl_up_sync(0xffffffffu, kk[3], 1);
+                if (lane == 0) prv = carry;
+                carry = __shfl_sync(0xffffffffu, kk[3], 31);
+                bool wide = false;
+                if (K32 && kmask != 0) {
+                    uint32_t hiw = 0;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) hiw |= (uint32_t)(wv[u] >> 32) | (uint32_t)(rv[u] >> 32);
+                    wide = __any_sync(0xffffffffu, (hiw & kmask) != 0);
+                }
+                const bool full = rem >= DJ_CHUNK && (k0 > 0 || lead == 0);
+                if (!wide) {
+                    uint32_t r32[4], s32[4];
+                    uint64_t hh[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        r32[u] = K32 ? (uint32_t)rv[u] : (uint32_t)rv[u] & pmask32;
+                        s32[u] = K32 ? (uint32_t)wv[u] : (uint32_t)wv[u] & pmask32;
+                        hh[u] = SW ? pair_hash32_mix<MPSM_DJ_FMA>(s32[u], r32[u], fk)
+                                   : pair_hash32_mix<MPSM_DJ_FMA>(r32[u], s32[u], fk);
+                    }
+                    if (full) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            max33(r32[u], s32[u], b0, b1, h1);
+                            if (MPSM_DJ_FMA & 32) csum = mad_mask64(csum, hh[u], fk.one);
+                            else csum += hh[u];
+                        }
+                    } else {
+                        const int v0 = k0 + 4 * lane;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const uint32_t m = (v0 + u >= lead && v0 + u < nv) ? 1u : 0u;
+                            max33(r32[u] * m, s32[u] * m, b0, b1, h1);
+                            csum = mad_mask64(csum, hh[u], m);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        uint64_t h, sm_;
+                        agg64(rv[u] & pmask, wv[u] & pmask, h, sm_);
+                        const int v = k0 + 4 * lane + u;
+                        const uint32_t mu = (full || (v >= lead && v < nv)) ? 1u : 0u;
+                        max_into(best, sm_ * mu);
+                        csum = mad_mask64(csum, h, mu);
+                    }
+                }
+                if (full) {
+                    bad |= (prv > kk[0]) | (kk[0] > kk[1]) | (kk[1] > kk[2]) | (kk[2] > kk[3]);
+                    cnt += DJ_CHUNK;
+                } else {
+                    const int v0 = k0 + 4 * lane;
+                    KT pv = prv;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int v = v0 + u;
+                        bad |= (v < nv && v - 1 >= lo_ok) && pv > kk[u];
+                        pv = kk[u];
+                    }
+                    cnt += max(0, min(nv, k0 + DJ_CHUNK) - max(k0, lead));
+                }
+            }
+#else
             for (; c < pe; ++c, k0 += DJ_CHUNK) {
                 // DJ_U tuples per lane: element u of lane l is k0 + 32 u + l
                 const int rem = n - k0;
@@ -1931,9 +2109,13 @@ __global__ void __launch_bounds__(DJ_THREADS, 2) k_dense_join(DjArgs a) {
                     cnt += rem;
                 }
             }
+#endif
             if (c < ce) ++p;
         }
+        }
         __syncwarp();
+        DJ_TS(warp == 0, g, 5)
+        DJ_TS(warp == DJ_WARPS - 1, g, 6)
         if (lane == 0) mbar_arrive(&sm.empty[s]);
     }
     flush_regs();
@@ -2035,7 +2217,7 @@ static int launch_dense(const DjArgs& a, int swap, cudaStream_t st) {
                              "smem attr"));
         attr = 1;
     }
-    const int grid = num_sms() * 2;
+    const int grid = num_sms() * MPSM_DJ_CTAS;
     ProfScope ps("dense_join", st);
     if (swap) k_dense_join<K32, true><<<grid, DJ_THREADS, sizeof(DjSmem), st>>>(a);
     else k_dense_join<K32, false><<<grid, DJ_THREADS, sizeof(DjSmem), st>>>(a);

@@ -758,6 +758,16 @@ def run_hash_oracle(r: Relation, s: Relation, cfg: JoinConfig) -> JoinResult:
                       worker_stats=[], checksum=csum)
 
 
+def hash_join_oracle(r: Relation, s: Relation, query_mode: str = "aggregate-max",
+                     cap: Optional[int] = None) -> JoinResult:
+    """The reference's ground-truth join as a function (datagen.py:121-200):
+    build on the smaller input, result shape of run_hash_oracle; cap None =
+    no materialize cap."""
+    cfg = JoinConfig(algorithm="hash-oracle", query_mode=query_mode,
+                     materialize_cap=(1 << 62) if cap is None else int(cap))
+    return run_hash_oracle(r, s, cfg)
+
+
 def run_join(r: Relation, s: Relation, cfg: JoinConfig, *, phase_hook: PhaseHook = None) -> JoinResult:
     """Dispatch on cfg.algorithm (engine.py:456-466)."""
     if cfg.algorithm == "b-mpsm":

@@ -240,9 +240,10 @@ def test_histogram_and_scatter_kats():
     scatter(A, 0, cur, sp, dom, arena)
     scatter(B, 1, cur, sp, dom, arena)
     r0, r1 = arena.run_view(0), arena.run_view(1)
-    assert r0.keys.cpu().tolist() == [13, 1, 9, 5, 2, 6, 11]  # exact reference layout
-    assert r0.payloads.cpu().tolist() == [0, 1, 2, 4, 10, 12, 15]
-    assert r1.keys.cpu().tolist() == [27, 30, 19, 17, 22, 31, 25]
+    assert r0.keys.tolist() == [13, 1, 9, 5, 2, 6, 11]  # exact reference layout (host view, as the reference's)
+    assert r0.payloads.tolist() == [0, 1, 2, 4, 10, 12, 15]
+    assert r1.keys.tolist() == [27, 30, 19, 17, 22, 31, 25]
+    assert arena.device_keys.cpu().tolist() == [13, 1, 9, 5, 2, 6, 11, 27, 30, 19, 17, 22, 31, 25]
     from paper_1207_0145_b200.core import InternalConsistencyError
 
     hc = [build_radix_histogram(C, dom, 2)]

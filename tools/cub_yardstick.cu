@@ -35,5 +35,21 @@ int main(int argc, char** argv) {
         float ms; cudaEventElapsedTime(&ms, a, b);
         printf("cub SortPairs n=%zu bits=%d: %.3f ms  (%.1f Gpairs/s)\n", n, bits, ms, n / ms / 1e6);
     }
+    // keys only: 8-B records, the layout of our record passes
+    {
+        cub::DoubleBuffer<uint64_t> kk(k0, k1);
+        size_t t2 = 0;
+        cub::DeviceRadixSort::SortKeys(nullptr, t2, kk, n, 0, bits);
+        void* tt; cudaMalloc(&tt, t2);
+        for (int it = 0; it < 4; ++it) {
+            fill<<<4096, 256>>>(kk.Current(), p0, n, (bits == 64) ? ~0ull : ((1ull << bits) - 1));
+            cudaEventRecord(a);
+            cub::DeviceRadixSort::SortKeys(tt, t2, kk, n, 0, bits);
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float ms; cudaEventElapsedTime(&ms, a, b);
+            printf("cub SortKeys u64 n=%zu bits=%d: %.3f ms  (%.1f Gkeys/s)\n", n, bits, ms, n / ms / 1e6);
+        }
+    }
     return 0;
 }
