@@ -215,16 +215,22 @@ struct SegCursor {
 // counts[g][d] for segment g, and for every tile t of the segment the
 // segment-local exclusive prefix toffs[t][d] (digit d's tuples in earlier
 // tiles of the segment); optional domain check (first pass)
+#ifndef MPSM_SEG_COUNT_TPS  // one-chunk scatter tiles (SP / SS passes) whose prefixes one barrier flushes
+#define MPSM_SEG_COUNT_TPS 1
+#endif
 template <int CPT, bool TABLE = false, bool MSEG = false>  // count chunks (TILE tuples) per scatter tile
 __global__ void __launch_bounds__(THREADS, 2) k_count(const uint64_t* __restrict__ in, Segs sg, Digit dig, int nbins,
                                                    uint32_t* __restrict__ counts, uint32_t* __restrict__ toffs,
                                                    unsigned int* __restrict__ ticket, uint64_t span_m1,
                                                    unsigned long long* __restrict__ d_bad) {
     constexpr int STILE = CPT * TILE;
-    __shared__ uint32_t h[2][MAX_BINS];  // scatter tile k counts into h[k & 1]
+    // TPS scatter tiles are counted per barrier (each into its own row);
+    // flush group g counts into h[g & 1], so one barrier per group suffices
+    constexpr int TPS = CPT == 1 ? MPSM_SEG_COUNT_TPS : 1;
+    __shared__ uint32_t h[2][TPS][MAX_BINS];
     const int tid = threadIdx.x;
-    h[0][tid] = 0;
-    h[1][tid] = 0;
+#pragma unroll
+    for (int j = 0; j < TPS; ++j) h[0][j][tid] = h[1][j][tid] = 0;
     if (blockIdx.x == 0 && tid == 0 && ticket) *ticket = 0;  // the scatter's tile dispenser
     __syncthreads();
     int64_t b, e, tfirst;
@@ -261,7 +267,8 @@ __global__ void __launch_bounds__(THREADS, 2) k_count(const uint64_t* __restrict
         }
     };
     if (b < e) load(v, b);
-    int k = 0, c = 0;
+    int k = 0, c = 0, q = 0;  // buffer, chunk within the tile, tile within the flush group
+    int64_t ts[TPS];          // first element of each tile of the group
     for (int64_t c0 = b; c0 < e; c0 += TILE) {
         if (c0 + TILE < e) load(w, c0 + TILE);  // next chunk in flight during this one
 #pragma unroll
@@ -269,21 +276,28 @@ __global__ void __launch_bounds__(THREADS, 2) k_count(const uint64_t* __restrict
             const int64_t i = pos(c0, u);
             if (i < e) {
                 if (d_bad && v[u] - dig.lower > span_m1) atomicMin(d_bad, (unsigned long long)i);
-                atomicAdd(&h[k][TABLE ? dig.lookup(v[u]) : dig(v[u])], 1u);
+                atomicAdd(&h[k][TPS == 1 ? 0 : q][TABLE ? dig.lookup(v[u]) : dig(v[u])], 1u);
             }
         }
 #pragma unroll
         for (int u = 0; u < ITEMS; ++u) v[u] = w[u];
-        if (++c < CPT && c0 + TILE < e) continue;
-        __syncthreads();  // h[k] complete; the next tile counts into h[k ^ 1]
-        if (tid < nbins) {
-            const int64_t ts = c0 - (c - 1) * TILE;  // this scatter tile's first element
-            toffs[(size_t)(MSEG ? tfirst + (ts - b) / STILE : ts / STILE) * MAX_BINS + tid] = run;
-        }
-        run += h[k][tid];
-        h[k][tid] = 0;
-        k ^= 1;
+        const bool last = c0 + TILE >= e;
+        if (++c < CPT && !last) continue;
+        ts[TPS == 1 ? 0 : q] = c0 - (c - 1) * TILE;  // this scatter tile's first element
         c = 0;
+        if (++q < TPS && !last) continue;
+        __syncthreads();  // h[k] complete; the next group counts into h[k ^ 1]
+#pragma unroll
+        for (int j = 0; j < TPS; ++j) {
+            if (j < q) {
+                if (tid < nbins)
+                    toffs[(size_t)(MSEG ? tfirst + (ts[j] - b) / STILE : ts[j] / STILE) * MAX_BINS + tid] = run;
+                run += h[k][j][tid];
+                h[k][j][tid] = 0;
+            }
+        }
+        k ^= 1;
+        q = 0;
     }
     if (tid < nbins) counts[(size_t)blockIdx.x * nbins + tid] = run;
 }
