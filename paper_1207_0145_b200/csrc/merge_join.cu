@@ -2122,6 +2122,254 @@ __global__ void __launch_bounds__(DJ_THREADS, MPSM_DJ_CTAS) k_dense_join(DjArgs 
     if (cur_i >= 0) flush_runs(cur_i);
 }
 
+// ---------------------------------------------------------------------------
+// One dense private run against one public run (T = 1, the FK join): warps
+// stream the S window straight from HBM -- each warp a contiguous range of
+// 128-tuple steps, lane l the 4 consecutive records 4l..4l+3 of a step (two
+// 16-B loads, the next step's in flight while this one is hashed) -- and
+// gather every tuple's R record from global memory at index key - key(R[0]).
+// S is sorted, so a step's R records are a few consecutive lines (L1 hits
+// after the first; R is read from HBM once).  No staging, tiles or
+// barriers.  Run order check: every adjacent S pair of the window and the
+// pair before it (in-lane, one shuffle across lanes, the step before through
+// a carried key).  Selected when the pair is the only one (n_priv = n_pub =
+// 1): the tiled k_dense_join stages one R block for T public runs.
+constexpr int DF_THREADS = 256;
+#ifndef MPSM_DF_MINB  // resident CTAs per SM the register budget is cut for
+#define MPSM_DF_MINB 4
+#endif
+// measured (FK 100M x 400M, dense_join): S loads one step ahead in
+// registers, 64 registers / 4 CTAs per SM 1.05 ms; two steps ahead 1.08-1.10;
+// a per-warp cp.async ring of 4-5 steps 1.21-1.33; the R gather issued one
+// step ahead 1.20-1.60 (spills or fewer warps); 96 registers / 3 CTAs 1.32.
+// Bounds (MPSM_DBG_DF_NO_GATHER / _NO_HASH): the S stream alone 0.56 ms
+// (5.7 TB/s), + gather 0.80, + hash 0.90
+#ifndef MPSM_DF_DEPTH  // steps of S loads in flight ahead of the one hashed (1 or 2)
+#define MPSM_DF_DEPTH 1
+#endif
+template <bool K32, bool SW>
+__global__ void __launch_bounds__(DF_THREADS, MPSM_DF_MINB) k_dense_flat(const mpsm_run_t* __restrict__ priv,
+                                                           const mpsm_run_t* __restrict__ pub,
+                                                           const PairWin* __restrict__ win,
+                                                           const uint32_t* __restrict__ nondense,
+                                                           const uint64_t* __restrict__ kbp, PackInfo pi,
+                                                           uint64_t* __restrict__ out_pairs) {
+    __shared__ unsigned long long s_cnt, s_best, s_csum;
+    __shared__ unsigned s_bad;
+    __shared__ uint32_t s_fmak[5];
+    const int tid = threadIdx.x, lane = tid & 31;
+    if (tid == 0) {
+        s_cnt = s_best = s_csum = 0;
+        s_bad = 0;
+        s_fmak[0] = 1u << 17;
+        s_fmak[1] = 1u << 2;
+        s_fmak[2] = 1u << 5;
+        s_fmak[3] = 1u << 1;
+        s_fmak[4] = 1u;
+    }
+    __syncthreads();
+    if (nondense[0]) return;
+    const PairWin w = win[0];
+    if (w.end <= w.start) return;
+    using KT = typename std::conditional<K32, uint32_t, uint64_t>::type;
+    const mpsm_run_t R = priv[0], S = pub[0];
+    const uint64_t* __restrict__ sk = S.keys;
+    const uint64_t* __restrict__ rk = R.keys;
+    const int pw = pi.pw;
+    const uint32_t kmask = pi.kmask;
+    const uint64_t pmask = pi.pmask;
+    const uint32_t pmask32 = (uint32_t)pmask;
+    auto nk = [&](uint64_t v) -> KT {
+        if (K32) return (KT)((uint32_t)(v >> 32) >> (pw - 32));
+        return (KT)(v >> pw);
+    };
+    const KT kb = (KT)kbp[0];
+    const KT nrm1 = (KT)(R.n - 1);
+    FmaK fk;
+    {
+        uint32_t* kp = &fk.m17;
+        for (int q = 0; q < 5; ++q)
+            asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(kp[q]) : "r"(smem_addr(&s_fmak[q])));
+    }
+    // step grid from the 16-B aligned index at or below the window start
+    const int64_t n = S.n;
+    const int al = (int)(((uintptr_t)sk >> 3) & 1);
+    const int64_t b0 = w.start - ((w.start + al) & 1);
+    const int64_t nsteps = (w.end - b0 + 127) >> 7;
+    const int64_t gw = ((int64_t)blockIdx.x * DF_THREADS + tid) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * DF_THREADS) >> 5;
+    const int64_t s0 = nsteps * gw / nw, s1 = nsteps * (gw + 1) / nw;
+    const int64_t lo_chk = w.start > 1 ? w.start : 1;  // pairs (v - 1, v) checked for v >= lo_chk
+    auto load4 = [&](int64_t e0, uint64_t* x) {
+        if (e0 >= 0 && e0 + 3 < n) {
+            const ulonglong2 a = __ldcs(reinterpret_cast<const ulonglong2*>(sk + e0));
+            const ulonglong2 b = __ldcs(reinterpret_cast<const ulonglong2*>(sk + e0 + 2));
+            x[0] = a.x;
+            x[1] = a.y;
+            x[2] = b.x;
+            x[3] = b.y;
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) x[u] = (e0 + u >= 0 && e0 + u < n) ? sk[e0 + u] : 0;
+        }
+    };
+    uint64_t best = 0, csum = 0;
+    uint32_t b0m = 0, b1m = 0, h1 = 0;
+    int64_t cnt = 0;  // warp-uniform
+    bool bad = false;
+    KT carry = 0;
+    if (s0 < s1) {
+        const int64_t first = b0 + (s0 << 7);
+        if (first - 1 >= 0) carry = nk(sk[first - 1]);
+    }
+    uint64_t nx[4], nx2[4];
+    if (s0 < s1) load4(b0 + (s0 << 7) + 4 * lane, nx);
+    if (MPSM_DF_DEPTH > 1 && s0 + 1 < s1) load4(b0 + ((s0 + 1) << 7) + 4 * lane, nx2);
+    for (int64_t st = s0; st < s1; ++st) {
+        const int64_t base = b0 + (st << 7);
+        uint64_t wv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) wv[u] = nx[u];
+        if (MPSM_DF_DEPTH > 1) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) nx[u] = nx2[u];
+            if (st + 2 < s1) load4(base + 256 + 4 * lane, nx2);
+        } else if (st + 1 < s1) {
+            load4(base + 128 + 4 * lane, nx);
+        }
+        KT kk[4];
+        uint64_t rv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            kk[u] = nk(wv[u]);
+            const KT d = kk[u] - kb;
+#ifdef MPSM_DBG_DF_NO_GATHER
+            rv[u] = wv[u] ^ (uint64_t)d;
+#else
+            rv[u] = __ldg(rk + (d < nrm1 ? d : nrm1));
+#endif
+        }
+        KT prv = __shfl_up_sync(0xffffffffu, kk[3], 1);
+        if (lane == 0) prv = carry;
+        carry = __shfl_sync(0xffffffffu, kk[3], 31);
+        bool wide = false;
+        if (K32 && kmask != 0) {
+            uint32_t hiw = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) hiw |= (uint32_t)(wv[u] >> 32) | (uint32_t)(rv[u] >> 32);
+            wide = __any_sync(0xffffffffu, (hiw & kmask) != 0);
+        }
+        const bool full = base >= lo_chk && base + 128 <= w.end;
+        const int64_t v0 = base + 4 * lane;
+        if (!wide) {
+            uint32_t r32[4], s32[4];
+            uint64_t hh[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                r32[u] = K32 ? (uint32_t)rv[u] : (uint32_t)rv[u] & pmask32;
+                s32[u] = K32 ? (uint32_t)wv[u] : (uint32_t)wv[u] & pmask32;
+#ifdef MPSM_DBG_DF_NO_HASH
+                hh[u] = (uint64_t)r32[u] * s32[u];
+#else
+                hh[u] = SW ? pair_hash32_mix<MPSM_DJ_FMA>(s32[u], r32[u], fk)
+                           : pair_hash32_mix<MPSM_DJ_FMA>(r32[u], s32[u], fk);
+#endif
+            }
+            if (full) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    max33(r32[u], s32[u], b0m, b1m, h1);
+                    if (MPSM_DJ_FMA & 32) csum = mad_mask64(csum, hh[u], fk.one);
+                    else csum += hh[u];
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t m = (v0 + u >= w.start && v0 + u < w.end) ? 1u : 0u;
+                    max33(r32[u] * m, s32[u] * m, b0m, b1m, h1);
+                    csum = mad_mask64(csum, hh[u], m);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint64_t rp = rv[u] & pmask, sp = wv[u] & pmask;
+                const uint64_t h = SW ? pair_hash(sp, rp) : pair_hash(rp, sp);
+                const uint32_t m = (full || (v0 + u >= w.start && v0 + u < w.end)) ? 1u : 0u;
+                max_into(best, (rp + sp) * m);
+                csum = mad_mask64(csum, h, m);
+            }
+        }
+        if (full) {
+            bad |= (prv > kk[0]) | (kk[0] > kk[1]) | (kk[1] > kk[2]) | (kk[2] > kk[3]);
+            cnt += 128;
+        } else {
+            KT pv = prv;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t v = v0 + u;
+                bad |= (v >= lo_chk && v < w.end) && pv > kk[u];
+                pv = kk[u];
+            }
+            cnt += max((int64_t)0, min(w.end, base + 128) - max(w.start, base));
+        }
+    }
+    {
+        const uint64_t cb = h1 ? ((1ull << 32) | b1m) : (uint64_t)b0m;
+        if (cb > best) best = cb;
+    }
+    const uint32_t lo = (uint32_t)csum, hi = (uint32_t)(csum >> 32);
+    const uint64_t cs = (uint64_t)__reduce_add_sync(0xffffffffu, lo & 0xffffu) +
+                        ((uint64_t)__reduce_add_sync(0xffffffffu, lo >> 16) << 16) +
+                        ((uint64_t)__reduce_add_sync(0xffffffffu, hi & 0xffffu) << 32) +
+                        ((uint64_t)__reduce_add_sync(0xffffffffu, hi >> 16) << 48);
+    const uint32_t bh = __reduce_max_sync(0xffffffffu, (uint32_t)(best >> 32));
+    const uint32_t bl = __reduce_max_sync(0xffffffffu, (uint32_t)(best >> 32) == bh ? (uint32_t)best : 0u);
+    const bool anybad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+        if (cnt) {
+            atomicAdd(&s_cnt, (unsigned long long)cnt);
+            atomicMax(&s_best, (unsigned long long)(((uint64_t)bh << 32) | bl));
+            atomicAdd(&s_csum, (unsigned long long)cs);
+        }
+        if (anybad) atomicOr(&s_bad, 1u);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        if (s_cnt) {
+            atomicAdd((unsigned long long*)(out_pairs + MPSM_PAIR_COUNT), s_cnt);
+            atomicMax((unsigned long long*)(out_pairs + MPSM_PAIR_BEST), s_best);
+            atomicAdd((unsigned long long*)(out_pairs + MPSM_PAIR_CHECKSUM), s_csum);
+        }
+        if (s_bad) atomicOr((unsigned long long*)(out_pairs + MPSM_PAIR_FLAGS), (unsigned long long)MPSM_FLAG_UNSORTED);
+    }
+}
+
+template <bool K32>
+static int launch_dense_flat(const mpsm_run_t* d_priv, const mpsm_run_t* d_pub, const PairWin* win,
+                             const uint32_t* nondense, const uint64_t* kb, const PackInfo& pi, uint64_t* d_pairs,
+                             int swap, cudaStream_t st) {
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dense_flat<K32, false>, DF_THREADS, 0);
+        if (per_sm < 1) per_sm = 1;
+    }
+    const int grid = num_sms() * per_sm;
+    ProfScope ps("dense_join", st);
+    if (swap) k_dense_flat<K32, true><<<grid, DF_THREADS, 0, st>>>(d_priv, d_pub, win, nondense, kb, pi, d_pairs);
+    else k_dense_flat<K32, false><<<grid, DF_THREADS, 0, st>>>(d_priv, d_pub, win, nondense, kb, pi, d_pairs);
+    return check_launch("k_dense_flat");
+}
+
+static bool df_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("MPSM_DENSE_FLAT");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
 static bool dj_enabled() {
     static int on = -1;
     if (on < 0) {
@@ -2263,7 +2511,13 @@ static int join_pairs_impl(const mpsm_run_t* priv, int n_priv, const mpsm_run_t*
     k_windows<PK><<<(npairs + 127) / 128, 128, 0, st>>>(w.d_priv, n_priv, w.d_pub, n_pub, w.win, d_pairs, pi,
                                                         dense ? dw.nondense : nullptr);
     MPSM_TRY(check_launch("k_windows"));
-    if (dense) {
+    if (dense && n_priv == 1 && n_pub == 1 && df_enabled()) {
+        // one pair: the flat kernel streams it (no tile plan)
+        if ((64 - pi.pw) <= 32)
+            MPSM_TRY(launch_dense_flat<true>(w.d_priv, w.d_pub, w.win, dw.nondense, dw.kb, pi, d_pairs, swap, st));
+        else
+            MPSM_TRY(launch_dense_flat<false>(w.d_priv, w.d_pub, w.win, dw.nondense, dw.kb, pi, d_pairs, swap, st));
+    } else if (dense) {
         {
             ProfScope ps("dense_tiles", st);
             const int64_t nb = dp.nent * n_pub;
