@@ -2123,32 +2123,343 @@ __global__ void __launch_bounds__(DJ_THREADS, MPSM_DJ_CTAS) k_dense_join(DjArgs 
 }
 
 // ---------------------------------------------------------------------------
-// One dense private run against one public run (T = 1, the FK join): warps
-// stream the S window straight from HBM -- each warp a contiguous range of
-// 128-tuple steps, lane l the 4 consecutive records 4l..4l+3 of a step (two
-// 16-B loads, the next step's in flight while this one is hashed) -- and
-// gather every tuple's R record from global memory at index key - key(R[0]).
-// S is sorted, so a step's R records are a few consecutive lines (L1 hits
-// after the first; R is read from HBM once).  No staging, tiles or
-// barriers.  Run order check: every adjacent S pair of the window and the
-// pair before it (in-lane, one shuffle across lanes, the step before through
-// a carried key).  Selected when the pair is the only one (n_priv = n_pub =
-// 1): the tiled k_dense_join stages one R block for T public runs.
+// Dense private runs against public runs, streamed (the FK join at any T):
+// every (private run i, public run j) pair whose run i is dense contributes
+// the 128-tuple steps of its S window; the steps of all pairs (private-run
+// major) are dealt to warps in chunks of DF_CHUNK consecutive steps, chunk k
+// to warp k mod W, so the warps sweep the step sequence together and run i's
+// records stay in L2 while its T pairs are streamed.  In a step lane l owns
+// the 4 consecutive S records 4l..4l+3 (two 16-B loads, the next step's in
+// flight while this one is hashed) and gathers each tuple's R record from
+// global memory at index key - key(R_i[0]) (S is sorted: a step's R records
+// are a few consecutive lines).  No staging, tiles or barriers.  Run order
+// check: every adjacent S pair of each window and the pair before it
+// (in-lane, one shuffle across lanes, the step before through a carried key
+// or one load at a chunk / pair start).  Per-warp COUNT / MAX / checksum go
+// to the pair's record with atomics when the warp's pair changes.
+//   k_df_plan    per pair: first step index (scan) and aligned window start
+//   k_dense_flat the stream
 constexpr int DF_THREADS = 256;
 #ifndef MPSM_DF_MINB  // resident CTAs per SM the register budget is cut for
-#define MPSM_DF_MINB 4
+#define MPSM_DF_MINB 3
 #endif
-// measured (FK 100M x 400M, dense_join): S loads one step ahead in
-// registers, 64 registers / 4 CTAs per SM 1.05 ms; two steps ahead 1.08-1.10;
-// a per-warp cp.async ring of 4-5 steps 1.21-1.33; the R gather issued one
-// step ahead 1.20-1.60 (spills or fewer warps); 96 registers / 3 CTAs 1.32.
-// Bounds (MPSM_DBG_DF_NO_GATHER / _NO_HASH): the S stream alone 0.56 ms
-// (5.7 TB/s), + gather 0.80, + hash 0.90
-#ifndef MPSM_DF_DEPTH  // steps of S loads in flight ahead of the one hashed (1 or 2)
-#define MPSM_DF_DEPTH 1
+#ifndef MPSM_DF_CHUNK  // consecutive steps a warp takes at a time
+#define MPSM_DF_CHUNK 64
 #endif
+constexpr int DF_MAXPAIRS = 4096;
+
+struct DfArgs {
+    const mpsm_run_t* priv;
+    const mpsm_run_t* pub;
+    const PairWin* win;
+    const uint32_t* nondense;
+    const uint64_t* kb;
+    int n_priv, n_pub;
+    int64_t* pstep;  // [npairs + 1] first step of each pair (exclusive scan)
+    int64_t* pb0;    // [npairs] 16-B aligned index at or below the window start
+    uint64_t* out_pairs;
+    PackInfo pi;
+};
+
+__global__ void __launch_bounds__(1024) k_df_plan(DfArgs a) {
+    __shared__ int64_t part[32];
+    const int np = a.n_priv * a.n_pub;
+    constexpr int PER = DF_MAXPAIRS / 1024;
+    int64_t v[PER];
+    int64_t tot = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int p = threadIdx.x * PER + q;
+        int64_t st = 0;
+        if (p < np) {
+            const PairWin w = a.win[p];
+            const int i = p / a.n_pub, j = p - i * a.n_pub;
+            if (!a.nondense[i] && w.end > w.start) {
+                const int al = (int)(((uintptr_t)a.pub[j].keys >> 3) & 1);
+                const int64_t b0 = w.start - ((w.start + al) & 1);
+                a.pb0[p] = b0;
+                st = (w.end - b0 + 127) >> 7;
+            } else {
+                a.pb0[p] = 0;
+            }
+        }
+        v[q] = st;
+        tot += st;
+    }
+    // exclusive scan of the per-thread totals
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int64_t incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+    }
+    if (lane == 31) part[wid] = incl;
+    __syncthreads();
+    int64_t run = incl - tot;
+    for (int q = 0; q < wid; ++q) run += part[q];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int p = threadIdx.x * PER + q;
+        if (p < np) a.pstep[p] = run;
+        run += v[q];
+    }
+    if (threadIdx.x == 1023) a.pstep[np] = run;
+}
+
 template <bool K32, bool SW>
-__global__ void __launch_bounds__(DF_THREADS, MPSM_DF_MINB) k_dense_flat(const mpsm_run_t* __restrict__ priv,
+__global__ void __launch_bounds__(DF_THREADS, MPSM_DF_MINB) k_dense_flat(DfArgs a) {
+    __shared__ uint32_t s_fmak[5];
+    const int tid = threadIdx.x, lane = tid & 31;
+    if (tid == 0) {
+        s_fmak[0] = 1u << 17;
+        s_fmak[1] = 1u << 2;
+        s_fmak[2] = 1u << 5;
+        s_fmak[3] = 1u << 1;
+        s_fmak[4] = 1u;
+    }
+    __syncthreads();
+    using KT = typename std::conditional<K32, uint32_t, uint64_t>::type;
+    const int np = a.n_priv * a.n_pub;
+    const int64_t total = a.pstep[np];
+    const int pw = a.pi.pw;
+    const uint32_t kmask = a.pi.kmask;
+    const uint64_t pmask = a.pi.pmask;
+    const uint32_t pmask32 = (uint32_t)pmask;
+    auto nk = [&](uint64_t v) -> KT {
+        if (K32) return (KT)((uint32_t)(v >> 32) >> (pw - 32));
+        return (KT)(v >> pw);
+    };
+    FmaK fk;
+    {
+        uint32_t* kp = &fk.m17;
+        for (int q = 0; q < 5; ++q)
+            asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(kp[q]) : "r"(smem_addr(&s_fmak[q])));
+    }
+    const int64_t gw = ((int64_t)blockIdx.x * DF_THREADS + tid) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * DF_THREADS) >> 5;
+    const int64_t nchunks = (total + MPSM_DF_CHUNK - 1) / MPSM_DF_CHUNK;
+
+    // the warp's current pair and its parameters
+    int p = -1;
+    int64_t p_first = 0, p_end = 0;  // the pair's steps [p_first, p_end)
+    const uint64_t* sk = nullptr;
+    const uint64_t* rk = nullptr;
+    int64_t sn = 0, b0 = 0, wstart = 0, wend = 0, lo_chk = 0;
+    KT kb = 0, nrm1 = 0;
+    // per-warp aggregates of pair p
+    uint64_t best = 0, csum = 0;
+    uint32_t b0m = 0, b1m = 0, h1 = 0;
+    int64_t cnt = 0;  // warp-uniform
+    bool bad = false;
+    auto flush = [&]() {
+        if (p < 0) return;
+        const uint64_t cb = h1 ? ((1ull << 32) | b1m) : (uint64_t)b0m;
+        if (cb > best) best = cb;
+        const uint32_t lo = (uint32_t)csum, hi = (uint32_t)(csum >> 32);
+        const uint64_t cs = (uint64_t)__reduce_add_sync(0xffffffffu, lo & 0xffffu) +
+                            ((uint64_t)__reduce_add_sync(0xffffffffu, lo >> 16) << 16) +
+                            ((uint64_t)__reduce_add_sync(0xffffffffu, hi & 0xffffu) << 32) +
+                            ((uint64_t)__reduce_add_sync(0xffffffffu, hi >> 16) << 48);
+        const uint32_t bh = __reduce_max_sync(0xffffffffu, (uint32_t)(best >> 32));
+        const uint32_t bl = __reduce_max_sync(0xffffffffu, (uint32_t)(best >> 32) == bh ? (uint32_t)best : 0u);
+        const bool anybad = __any_sync(0xffffffffu, bad);
+        if (lane == 0) {
+            uint64_t* o = a.out_pairs + (size_t)p * MPSM_PAIR_FIELDS;
+            if (cnt) {
+                atomicAdd((unsigned long long*)(o + MPSM_PAIR_COUNT), (unsigned long long)cnt);
+                atomicMax((unsigned long long*)(o + MPSM_PAIR_BEST), (unsigned long long)(((uint64_t)bh << 32) | bl));
+                atomicAdd((unsigned long long*)(o + MPSM_PAIR_CHECKSUM), (unsigned long long)cs);
+            }
+            if (anybad) atomicOr((unsigned long long*)(o + MPSM_PAIR_FLAGS), (unsigned long long)MPSM_FLAG_UNSORTED);
+        }
+        best = csum = 0;
+        b0m = b1m = h1 = 0;
+        cnt = 0;
+        bad = false;
+    };
+    auto enter = [&](int q) {  // make pair q current
+        flush();
+        p = q;
+        p_first = a.pstep[q];
+        p_end = a.pstep[q + 1];
+        const int i = q / a.n_pub, j = q - i * a.n_pub;
+        const mpsm_run_t S = a.pub[j], R = a.priv[i];
+        sk = S.keys;
+        sn = S.n;
+        rk = R.keys;
+        nrm1 = (KT)(R.n - 1);
+        kb = (KT)a.kb[i];
+        b0 = a.pb0[q];
+        const PairWin w = a.win[q];
+        wstart = w.start;
+        wend = w.end;
+        lo_chk = wstart > 1 ? wstart : 1;
+    };
+    auto load4 = [&](int64_t e0, uint64_t* x) {
+        if (e0 >= 0 && e0 + 3 < sn) {
+            const ulonglong2 u0 = __ldcs(reinterpret_cast<const ulonglong2*>(sk + e0));
+            const ulonglong2 u1 = __ldcs(reinterpret_cast<const ulonglong2*>(sk + e0 + 2));
+            x[0] = u0.x;
+            x[1] = u0.y;
+            x[2] = u1.x;
+            x[3] = u1.y;
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) x[u] = (e0 + u >= 0 && e0 + u < sn) ? sk[e0 + u] : 0;
+        }
+    };
+    uint64_t nx[4] = {0, 0, 0, 0};
+    int64_t pre_step = -1;  // the step whose S nx holds (prefetched across chunks), else -1
+    for (int64_t ch = gw; ch < nchunks; ch += nw) {
+        const int64_t c0 = ch * MPSM_DF_CHUNK, c1 = min(c0 + MPSM_DF_CHUNK, total);
+        // the pair holding step c0 (pairs are visited in increasing order)
+        if (p < 0 || c0 >= p_end) {
+            int lo = p < 0 ? 0 : p, hi = np - 1;
+            while (lo < hi) {  // last q with pstep[q] <= c0
+                const int mid = (lo + hi + 1) >> 1;
+                if (a.pstep[mid] <= c0) lo = mid;
+                else hi = mid - 1;
+            }
+            while (a.pstep[lo + 1] <= c0) ++lo;  // skip pairs without steps
+            if (lo != p) enter(lo);
+        }
+        int64_t st = c0;
+        while (st < c1) {
+            if (st >= p_end) {  // the chunk runs into the next pair(s)
+                int q = p + 1;
+                while (a.pstep[q + 1] <= st) ++q;
+                enter(q);
+            }
+            const int64_t se = min(c1, p_end);  // this chunk's steps of pair p
+            // key before the first step here (0: nothing to check)
+            int64_t base = b0 + ((st - p_first) << 7);
+            KT carry = (base - 1 >= 0) ? nk(sk[base - 1]) : (KT)0;
+            if (st != pre_step) load4(base + 4 * lane, nx);  // not prefetched
+            pre_step = -1;
+            for (; st < se; ++st, base += 128) {
+                uint64_t wv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) wv[u] = nx[u];
+                if (st + 1 < se) {
+                    load4(base + 128 + 4 * lane, nx);
+                } else if (st + 1 == c1) {
+                    // the warp's next chunk, when it continues this pair:
+                    // its first step's S in flight during this step
+                    const int64_t nc = c0 + nw * MPSM_DF_CHUNK;
+                    if (nc < p_end) {
+                        load4(b0 + ((nc - p_first) << 7) + 4 * lane, nx);
+                        pre_step = nc;
+                    }
+                }
+                KT kk[4];
+                uint64_t rv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    kk[u] = nk(wv[u]);
+                    const KT d = kk[u] - kb;
+#ifdef MPSM_DBG_DF_NO_GATHER
+                    rv[u] = wv[u] ^ (uint64_t)d;
+#else
+                    rv[u] = __ldg(rk + (d < nrm1 ? d : nrm1));
+#endif
+                }
+                KT prv = __shfl_up_sync(0xffffffffu, kk[3], 1);
+                if (lane == 0) prv = carry;
+                carry = __shfl_sync(0xffffffffu, kk[3], 31);
+                bool wide = false;
+                if (K32 && kmask != 0) {
+                    uint32_t hiw = 0;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) hiw |= (uint32_t)(wv[u] >> 32) | (uint32_t)(rv[u] >> 32);
+                    wide = __any_sync(0xffffffffu, (hiw & kmask) != 0);
+                }
+                const bool full = base >= lo_chk && base + 128 <= wend;
+                const int64_t v0 = base + 4 * lane;
+                if (!wide) {
+                    uint32_t r32[4], s32[4];
+                    uint64_t hh[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        r32[u] = K32 ? (uint32_t)rv[u] : (uint32_t)rv[u] & pmask32;
+                        s32[u] = K32 ? (uint32_t)wv[u] : (uint32_t)wv[u] & pmask32;
+#ifdef MPSM_DBG_DF_NO_HASH
+                        hh[u] = (uint64_t)r32[u] * s32[u];
+#else
+                        hh[u] = SW ? pair_hash32_mix<MPSM_DJ_FMA>(s32[u], r32[u], fk)
+                                   : pair_hash32_mix<MPSM_DJ_FMA>(r32[u], s32[u], fk);
+#endif
+                    }
+                    if (full) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            max33(r32[u], s32[u], b0m, b1m, h1);
+                            if (MPSM_DJ_FMA & 32) csum = mad_mask64(csum, hh[u], fk.one);
+                            else csum += hh[u];
+                        }
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const uint32_t m = (v0 + u >= wstart && v0 + u < wend) ? 1u : 0u;
+                            max33(r32[u] * m, s32[u] * m, b0m, b1m, h1);
+                            csum = mad_mask64(csum, hh[u], m);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const uint64_t rp = rv[u] & pmask, sp = wv[u] & pmask;
+                        const uint64_t h = SW ? pair_hash(sp, rp) : pair_hash(rp, sp);
+                        const uint32_t m = (full || (v0 + u >= wstart && v0 + u < wend)) ? 1u : 0u;
+                        max_into(best, (rp + sp) * m);
+                        csum = mad_mask64(csum, h, m);
+                    }
+                }
+                if (full) {
+                    bad |= (prv > kk[0]) | (kk[0] > kk[1]) | (kk[1] > kk[2]) | (kk[2] > kk[3]);
+                    cnt += 128;
+                } else {
+                    KT pv = prv;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int64_t v = v0 + u;
+                        bad |= (v >= lo_chk && v < wend) && pv > kk[u];
+                        pv = kk[u];
+                    }
+                    cnt += max((int64_t)0, min(wend, base + 128) - max(wstart, base));
+                }
+            }
+        }
+    }
+    flush();
+}
+
+template <bool K32>
+static int launch_dense_flat(const DfArgs& a, int swap, cudaStream_t st) {
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dense_flat<K32, false>, DF_THREADS, 0);
+        if (per_sm < 1) per_sm = 1;
+    }
+    const int grid = num_sms() * per_sm;
+    ProfScope ps("dense_join", st);
+    k_df_plan<<<1, 1024, 0, st>>>(a);
+    MPSM_TRY(check_launch("k_df_plan"));
+    if (swap) k_dense_flat<K32, true><<<grid, DF_THREADS, 0, st>>>(a);
+    else k_dense_flat<K32, false><<<grid, DF_THREADS, 0, st>>>(a);
+    return check_launch("k_dense_flat");
+}
+
+// One pair (T = 1): each warp streams one contiguous range of steps (no
+// chunk dealing or pair lookup; S prefetched one step ahead in registers).
+// Measured (FK 100M x 400M): 1.05 ms vs 1.12-1.15 for the dealt-chunk kernel
+// on the same pair; S loads two steps ahead 1.08-1.10, a per-warp cp.async
+// ring 1.21-1.33, the R gather issued one step ahead 1.20-1.60 (spills or
+// fewer warps).  Bounds: the S stream alone 0.56 ms (5.7 TB/s), + the R
+// gather 0.80, + the hash 0.90 (MPSM_DBG_DF_NO_GATHER / _NO_HASH in the
+// dealt kernel).
+template <bool K32, bool SW>
+__global__ void __launch_bounds__(DF_THREADS, 4) k_dense_flat1(const mpsm_run_t* __restrict__ priv,
                                                            const mpsm_run_t* __restrict__ pub,
                                                            const PairWin* __restrict__ win,
                                                            const uint32_t* __restrict__ nondense,
@@ -2222,32 +2533,21 @@ __global__ void __launch_bounds__(DF_THREADS, MPSM_DF_MINB) k_dense_flat(const m
         const int64_t first = b0 + (s0 << 7);
         if (first - 1 >= 0) carry = nk(sk[first - 1]);
     }
-    uint64_t nx[4], nx2[4];
+    uint64_t nx[4];
     if (s0 < s1) load4(b0 + (s0 << 7) + 4 * lane, nx);
-    if (MPSM_DF_DEPTH > 1 && s0 + 1 < s1) load4(b0 + ((s0 + 1) << 7) + 4 * lane, nx2);
     for (int64_t st = s0; st < s1; ++st) {
         const int64_t base = b0 + (st << 7);
         uint64_t wv[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) wv[u] = nx[u];
-        if (MPSM_DF_DEPTH > 1) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) nx[u] = nx2[u];
-            if (st + 2 < s1) load4(base + 256 + 4 * lane, nx2);
-        } else if (st + 1 < s1) {
-            load4(base + 128 + 4 * lane, nx);
-        }
+        if (st + 1 < s1) load4(base + 128 + 4 * lane, nx);
         KT kk[4];
         uint64_t rv[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             kk[u] = nk(wv[u]);
             const KT d = kk[u] - kb;
-#ifdef MPSM_DBG_DF_NO_GATHER
-            rv[u] = wv[u] ^ (uint64_t)d;
-#else
             rv[u] = __ldg(rk + (d < nrm1 ? d : nrm1));
-#endif
         }
         KT prv = __shfl_up_sync(0xffffffffu, kk[3], 1);
         if (lane == 0) prv = carry;
@@ -2268,12 +2568,8 @@ __global__ void __launch_bounds__(DF_THREADS, MPSM_DF_MINB) k_dense_flat(const m
             for (int u = 0; u < 4; ++u) {
                 r32[u] = K32 ? (uint32_t)rv[u] : (uint32_t)rv[u] & pmask32;
                 s32[u] = K32 ? (uint32_t)wv[u] : (uint32_t)wv[u] & pmask32;
-#ifdef MPSM_DBG_DF_NO_HASH
-                hh[u] = (uint64_t)r32[u] * s32[u];
-#else
                 hh[u] = SW ? pair_hash32_mix<MPSM_DJ_FMA>(s32[u], r32[u], fk)
                            : pair_hash32_mix<MPSM_DJ_FMA>(r32[u], s32[u], fk);
-#endif
             }
             if (full) {
 #pragma unroll
@@ -2346,19 +2642,19 @@ __global__ void __launch_bounds__(DF_THREADS, MPSM_DF_MINB) k_dense_flat(const m
 }
 
 template <bool K32>
-static int launch_dense_flat(const mpsm_run_t* d_priv, const mpsm_run_t* d_pub, const PairWin* win,
+static int launch_dense_flat1(const mpsm_run_t* d_priv, const mpsm_run_t* d_pub, const PairWin* win,
                              const uint32_t* nondense, const uint64_t* kb, const PackInfo& pi, uint64_t* d_pairs,
                              int swap, cudaStream_t st) {
     static int per_sm = 0;
     if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dense_flat<K32, false>, DF_THREADS, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dense_flat1<K32, false>, DF_THREADS, 0);
         if (per_sm < 1) per_sm = 1;
     }
     const int grid = num_sms() * per_sm;
     ProfScope ps("dense_join", st);
-    if (swap) k_dense_flat<K32, true><<<grid, DF_THREADS, 0, st>>>(d_priv, d_pub, win, nondense, kb, pi, d_pairs);
-    else k_dense_flat<K32, false><<<grid, DF_THREADS, 0, st>>>(d_priv, d_pub, win, nondense, kb, pi, d_pairs);
-    return check_launch("k_dense_flat");
+    if (swap) k_dense_flat1<K32, true><<<grid, DF_THREADS, 0, st>>>(d_priv, d_pub, win, nondense, kb, pi, d_pairs);
+    else k_dense_flat1<K32, false><<<grid, DF_THREADS, 0, st>>>(d_priv, d_pub, win, nondense, kb, pi, d_pairs);
+    return check_launch("k_dense_flat1");
 }
 
 static bool df_enabled() {
@@ -2426,6 +2722,8 @@ struct DjWs {
     int64_t* part;
     DjTile* tiles;
     int64_t* ntiles;
+    int64_t* pstep;  // streamed path: [npairs + 1]
+    int64_t* pb0;    // streamed path: [npairs]
 };
 static bool carve_dj(Carve& c, int n_priv, int n_pub, const DjPlan& p, DjWs* o) {
     o->nondense = c.take<uint32_t>(n_priv);
@@ -2437,6 +2735,8 @@ static bool carve_dj(Carve& c, int n_priv, int n_pub, const DjPlan& p, DjWs* o) 
     o->part = c.take<int64_t>(p.nparts + 1);
     o->tiles = c.take<DjTile>(p.maxt);
     o->ntiles = c.take<int64_t>(1);
+    o->pstep = c.take<int64_t>((size_t)n_priv * n_pub + 1);
+    o->pb0 = c.take<int64_t>((size_t)n_priv * n_pub);
     return c.ok;
 }
 
@@ -2511,12 +2811,18 @@ static int join_pairs_impl(const mpsm_run_t* priv, int n_priv, const mpsm_run_t*
     k_windows<PK><<<(npairs + 127) / 128, 128, 0, st>>>(w.d_priv, n_priv, w.d_pub, n_pub, w.win, d_pairs, pi,
                                                         dense ? dw.nondense : nullptr);
     MPSM_TRY(check_launch("k_windows"));
-    if (dense && n_priv == 1 && n_pub == 1 && df_enabled()) {
-        // one pair: the flat kernel streams it (no tile plan)
-        if ((64 - pi.pw) <= 32)
-            MPSM_TRY(launch_dense_flat<true>(w.d_priv, w.d_pub, w.win, dw.nondense, dw.kb, pi, d_pairs, swap, st));
-        else
-            MPSM_TRY(launch_dense_flat<false>(w.d_priv, w.d_pub, w.win, dw.nondense, dw.kb, pi, d_pairs, swap, st));
+    if (dense && df_enabled() && npairs <= DF_MAXPAIRS) {
+        // the streamed path (no tile plan)
+        const DfArgs fa{w.d_priv, w.d_pub, w.win, dw.nondense, dw.kb, n_priv, n_pub, dw.pstep, dw.pb0, d_pairs, pi};
+        const bool k32f = (64 - pi.pw) <= 32;
+        if (npairs == 1) {
+            if (k32f) MPSM_TRY(launch_dense_flat1<true>(w.d_priv, w.d_pub, w.win, dw.nondense, dw.kb, pi, d_pairs, swap, st));
+            else MPSM_TRY(launch_dense_flat1<false>(w.d_priv, w.d_pub, w.win, dw.nondense, dw.kb, pi, d_pairs, swap, st));
+        } else if (k32f) {
+            MPSM_TRY(launch_dense_flat<true>(fa, swap, st));
+        } else {
+            MPSM_TRY(launch_dense_flat<false>(fa, swap, st));
+        }
     } else if (dense) {
         {
             ProfScope ps("dense_tiles", st);
