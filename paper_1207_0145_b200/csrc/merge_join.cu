@@ -2657,13 +2657,11 @@ static int launch_dense_flat1(const mpsm_run_t* d_priv, const mpsm_run_t* d_pub,
     return check_launch("k_dense_flat1");
 }
 
+// MPSM_DENSE_FLAT=0 selects the staged k_dense_join instead (read per call:
+// the tests run both paths in one process)
 static bool df_enabled() {
-    static int on = -1;
-    if (on < 0) {
-        const char* e = getenv("MPSM_DENSE_FLAT");
-        on = (e && e[0] == '0') ? 0 : 1;
-    }
-    return on == 1;
+    const char* e = getenv("MPSM_DENSE_FLAT");
+    return !(e && e[0] == '0');
 }
 
 static bool dj_enabled() {

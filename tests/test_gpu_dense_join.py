@@ -1,4 +1,5 @@
-"""GPU parity of the dense-run join path (k_dense_join, csrc/merge_join.cu):
+"""GPU parity of the dense-run join paths (k_dense_flat / k_dense_flat1 and
+k_dense_join, csrc/merge_join.cu):
 private runs whose keys step by one take it, every other run the merge walk.
 Per (private run, public run) pair the record must equal the reference's
 interpolation search plus merge_join_run (_kernels.py:287-408) on the same
@@ -19,6 +20,17 @@ from paper_1207_0145_b200 import device as D  # noqa: E402
 from oracle import oracle as orc  # noqa: E402
 
 DEV = torch.device("cuda", 0)
+
+
+@pytest.fixture(autouse=True, params=["streamed", "staged"])
+def dense_path(request, monkeypatch):
+    """every case through both dense kernels: the streamed k_dense_flat[1]
+    (default) and the staged k_dense_join (MPSM_DENSE_FLAT=0)"""
+    if request.param == "staged":
+        monkeypatch.setenv("MPSM_DENSE_FLAT", "0")
+    else:
+        monkeypatch.delenv("MPSM_DENSE_FLAT", raising=False)
+    return request.param
 
 
 def _pack(keys, pays, lower, w):
