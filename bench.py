@@ -392,12 +392,20 @@ def impl_ours(args):
     moved = sum(v["bytes"] for v in phase_roof.values())
     step_roof = {"bytes": moved, "gbs": moved / (ms / 1e3) / 1e9, "frac": moved / (ms / 1e3) / 1e9 / peak,
                  "floor_ms": 1e3 * moved / (peak * 1e9)}
-    mfile = os.path.join(ROOT, "profiles", "traffic_merge.json")
-    if "join" in phase_roof and packed and args.config == "cfg2" and os.path.exists(mfile):
+    # the join kernel alone (the dense-run stream on FK inputs, else the
+    # merge): the bytes it moves over its summed CUDA-event time
+    jk = "dense_join" if prof["dense_join"][0] > 0 else "merge"
+    jms = prof[jk][0] / args.steps
+    if "join" in phase_roof and jms > 0:
+        nb = (n_r + n_s) * rec_b
+        phase_roof["join_kernel"] = {"kernel": "k_dense_flat1 / k_dense_flat" if jk == "dense_join" else "k_merge",
+                                     "bytes": nb, "ms": jms, "gbs": nb / jms / 1e6, "frac": nb / jms / 1e6 / peak}
+    mfile = os.path.join(ROOT, "profiles", "traffic_join.json")
+    if "join_kernel" in phase_roof and jk == "dense_join" and packed and args.config == "cfg2" and os.path.exists(mfile):
         with open(mfile) as f:
             tj = json.load(f)
-        phase_roof["join"]["ncu_dram_bytes"] = tj.get("dram_bytes_per_launch")
-        phase_roof["join"]["ncu_source"] = "profiles/traffic_merge.json"
+        phase_roof["join_kernel"]["ncu_dram_bytes"] = tj.get("dram_bytes_per_launch")
+        phase_roof["join_kernel"]["ncu_source"] = "profiles/traffic_join.json"
 
     e2e = None
     if not args.no_e2e:
