@@ -693,9 +693,11 @@ __global__ void __launch_bounds__(THREADS, LCfg<LAYOUT>::BLOCKS) k_scatter(
 #pragma unroll 4
         for (int i = tid; i < cnt; i += THREADS) {
             const uint64_t v = sm.buf[b][0][i];
-            const int64_t o =
-                sm.gdelta[TABLE ? odig.lookup(v) : (LAYOUT == SS ? odig(v) : rec_digit<HI>(v, odig))] + i;
-            MPSM_CHECK(o >= 0 && o < sg.n);
+            const uint32_t od = TABLE ? odig.lookup(v) : (LAYOUT == SS ? odig(v) : rec_digit<HI>(v, odig));
+            const int64_t o = sm.gdelta[od] + i;
+            // explicit digit starts (the arena scatter): inside the digit's
+            // own region of the caller's output; else inside the n outputs
+            MPSM_CHECK(o >= 0 && (sg.dbase ? (o >= sg.dbase[od] && o < sg.dbase[od] + dtot[od]) : o < sg.n));
             out_k[o] = v;
             if (LAYOUT == SS) out_p[o] = sm.buf[b][1][i];
         }
