@@ -152,3 +152,41 @@ def test_partition_host_kats():
     with pytest.raises(InternalConsistencyError):
         PrefixCursors(np.array([[0], [3]]), np.array([[4], [3]]), np.array([7]), np.array([0, 7])).verify_disjoint()
     assert SplitterVector.from_bucket_bounds([0, 1, 4], 4).sp.tolist() == [0, 1, 1, 1]
+
+
+# the reference's operator layer (mpsm._kernels, _kernels.py:217-408) as the
+# package exposes it over the C ABI: same names and parameter lists
+_REF_KERNEL_SIGNATURES = {
+    "radix_histogram": ["keys", "lower", "shift", "counts"],
+    "scatter_chunk": ["keys", "pays", "lower", "shift", "sp", "cursors", "ends", "out_keys", "out_pays"],
+    "interp_lower_bound": ["keys", "target"],
+    "merge_join_run": ["r_keys", "r_pays", "s_keys", "s_pays", "s_start", "collect", "out_r", "out_s"],
+    "three_phase_sort": ["keys", "pays", "lo", "hi", "lower", "width_bits"],
+    "warmup": [],
+}
+
+
+def test_operator_layer_signatures():
+    import inspect
+
+    from paper_1207_0145_b200 import _kernels as K
+
+    for name, params in _REF_KERNEL_SIGNATURES.items():
+        assert list(inspect.signature(getattr(K, name)).parameters) == params, name
+    assert K._EMPTY_U64.dtype == np.uint64 and K._EMPTY_U64.size == 0
+    assert P.hash_join_oracle is not None  # datagen.hash_join_oracle's name at the top level, as the reference's
+
+
+def test_reference_suite_staging(tmp_path):
+    """oracle.ref_suite stages the reference's tests with the alias conftest
+    (needs /root/reference: this container; the GPU box runs the staged copy)"""
+    from oracle import ref_suite
+
+    src = "/root/reference/pkg/tests"
+    if not os.path.isdir(src):
+        pytest.skip("the reference is not present here")
+    conf = ref_suite.CONFTEST
+    assert 'sys.modules["mpsm"] = P' in conf and 'sys.modules["mpsm._kernels"] = K' in conf
+    assert ref_suite.prepare(src)
+    assert os.path.exists(os.path.join(ref_suite.DST, "conftest.py"))
+    assert len([f for f in os.listdir(ref_suite.DST) if f.startswith("test_")]) >= 5
