@@ -989,6 +989,11 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                 // the tile is compared
                 KT last = 0;
                 uint32_t down = 0;
+                // the shared address of ub[0] in a register: through the
+                // array ptxas rebuilt the shared window base (S2R CgaCtaId,
+                // LEA) at every store of the walk
+                uint32_t ub_base;  // opaque to ptxas (a volatile mov): kept, not rematerialised
+                asm volatile("mov.u32 %0, %1;" : "=r"(ub_base) : "r"(smem_addr(&sm.ub[0])));
                 for (int st = k0; st < k1; ++st) {
                     const bool take_r = ri < nR && (wj >= nW || rkc <= wkc);
                     if (MPSM_MJ_ORDER_CHECK == 2) {
@@ -997,7 +1002,7 @@ __global__ void __launch_bounds__(MJ_THREADS, PK ? MPSM_MJ_BLOCKS : 2) k_merge(c
                         last = m;
                     }
                     MPSM_CHECK(take_r || wj < nW);
-                    if (!take_r) sm.ub[wj] = (uint16_t)ri;
+                    if (!take_r) asm volatile("st.shared.u16 [%0], %1;" ::"r"(ub_base + 2u * (uint32_t)wj), "h"((unsigned short)ri) : "memory");
                     ri += take_r;
                     wj += !take_r;
                     if (take_r && ri < nR) {
@@ -1458,7 +1463,16 @@ __global__ void __launch_bounds__(256) k_dense_check(const mpsm_run_t* __restric
     const uint64_t* base = r.keys + head;
     const int64_t n = r.n - head;  // records from the aligned one on
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    int iter = 0;
     for (int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c * 256 < n - 1; c += nw) {
+        // a run found not dense: the rest need not be read (the skewed and
+        // sparse runs of cfg4 stop after their first chunks); the flag other
+        // warps raised is polled every 8th chunk
+        if (__any_sync(0xffffffffu, bad)) {
+            if (lane == 0) atomicOr(&nondense[i], 1u);
+            break;
+        }
+        if ((++iter & 7) == 0 && *(volatile const uint32_t*)&nondense[i]) break;
         const int64_t k0 = c * 256;
         ulonglong2 v[4];
 #pragma unroll
