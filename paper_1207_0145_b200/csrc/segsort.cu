@@ -269,14 +269,27 @@ __global__ void __launch_bounds__(THREADS, 2) k_count(const uint64_t* __restrict
     if (b < e) load(v, b);
     int k = 0, c = 0, q = 0;  // buffer, chunk within the tile, tile within the flush group
     int64_t ts[TPS];          // first element of each tile of the group
+    // the histograms' shared address in a register (through the array ptxas
+    // re-reads the CTA's shared window base, S2UR CgaCtaId, per atomic)
+    uint32_t hbase;
+    asm volatile("mov.u32 %0, %1;" : "=r"(hbase) : "r"(smem_addr(&h[0][0][0])));
+    auto bump = [&](uint32_t row, uint32_t d) {
+        asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(hbase + 4u * (row * MAX_BINS + d)) : "memory");
+    };
     for (int64_t c0 = b; c0 < e; c0 += TILE) {
         if (c0 + TILE < e) load(w, c0 + TILE);  // next chunk in flight during this one
+        const uint32_t row = (uint32_t)(k * TPS + (TPS == 1 ? 0 : q));
+        if (c0 + TILE <= e && !d_bad) {  // a whole chunk, no domain check: no per-item guards
 #pragma unroll
-        for (int u = 0; u < ITEMS; ++u) {
-            const int64_t i = pos(c0, u);
-            if (i < e) {
-                if (d_bad && v[u] - dig.lower > span_m1) atomicMin(d_bad, (unsigned long long)i);
-                atomicAdd(&h[k][TPS == 1 ? 0 : q][TABLE ? dig.lookup(v[u]) : dig(v[u])], 1u);
+            for (int u = 0; u < ITEMS; ++u) bump(row, TABLE ? dig.lookup(v[u]) : dig(v[u]));
+        } else {
+#pragma unroll
+            for (int u = 0; u < ITEMS; ++u) {
+                const int64_t i = pos(c0, u);
+                if (i < e) {
+                    if (d_bad && v[u] - dig.lower > span_m1) atomicMin(d_bad, (unsigned long long)i);
+                    bump(row, TABLE ? dig.lookup(v[u]) : dig(v[u]));
+                }
             }
         }
 #pragma unroll
