@@ -117,6 +117,18 @@ def test_fk_vs_oracle_gather(n_r, n_s, seed):
                                                                               s.payloads, 1)
 
 
+@pytest.mark.parametrize("threads,algorithm", [(2, "p-mpsm"), (16, "p-mpsm"), (64, "p-mpsm"), (100, "p-mpsm"),
+                                                (7, "b-mpsm"), (64, "b-mpsm")])
+def test_fk_many_workers_vs_oracle_gather(threads, algorithm):
+    """T x T dense pairs through the streamed join (k_dense_flat up to 64 x 64
+    = 4096 pairs; beyond 64 runs a side the merge walk), both variants"""
+    r, s, dom = P.gen_fk(2_000_000, 8_000_000, 11)
+    res = P.run_join(r, s, JoinConfig(threads=threads, algorithm=algorithm, key_domain=dom))
+    assert (res.match_count, res.aggregate_max, res.checksum) == orc.fk_gather(r.keys, r.payloads, s.keys,
+                                                                              s.payloads, 1)
+    assert len(res.worker_stats) == threads
+
+
 def test_negcorr_skew_vs_oracle(pack_mode):
     dom = KeyDomain(1, 1 << 32)
     r, s = P.gen_negcorr(400_000, 1_600_000, dom, seed=0)
