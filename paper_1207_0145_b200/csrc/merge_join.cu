@@ -2547,83 +2547,113 @@ __global__ void __launch_bounds__(DF_THREADS, 4) k_dense_flat1(const mpsm_run_t*
         const int64_t first = b0 + (s0 << 7);
         if (first - 1 >= 0) carry = nk(sk[first - 1]);
     }
-    uint64_t nx[4];
-    if (s0 < s1) load4(b0 + (s0 << 7) + 4 * lane, nx);
-    for (int64_t st = s0; st < s1; ++st) {
-        const int64_t base = b0 + (st << 7);
-        uint64_t wv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) wv[u] = nx[u];
-        if (st + 1 < s1) load4(base + 128 + 4 * lane, nx);
-        KT kk[4];
-        uint64_t rv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            kk[u] = nk(wv[u]);
-            const KT d = kk[u] - kb;
-            rv[u] = __ldg(rk + (d < nrm1 ? d : nrm1));
+    // a warp whose steps all lie inside the window (every warp but the
+    // first and the last) runs the lean loop: no bounds or window masks, S
+    // through a running pointer
+    const bool interior = s0 < s1 && b0 + (s0 << 7) >= lo_chk && b0 + (s1 << 7) <= w.end;
+    auto run = [&](auto lean_tag) {
+        constexpr bool LEAN = decltype(lean_tag)::value;
+        const uint64_t* sq = sk + b0 + (s0 << 7) + 4 * lane;  // LEAN: this lane's records of the current step
+        uint64_t nx[4];
+        auto ld16 = [&](const uint64_t* q, uint64_t* x) {
+            const ulonglong2 a0 = __ldcs(reinterpret_cast<const ulonglong2*>(q));
+            const ulonglong2 a1 = __ldcs(reinterpret_cast<const ulonglong2*>(q + 2));
+            x[0] = a0.x;
+            x[1] = a0.y;
+            x[2] = a1.x;
+            x[3] = a1.y;
+        };
+        if (s0 < s1) {
+            if (LEAN) ld16(sq, nx);
+            else load4(b0 + (s0 << 7) + 4 * lane, nx);
         }
-        KT prv = __shfl_up_sync(0xffffffffu, kk[3], 1);
-        if (lane == 0) prv = carry;
-        carry = __shfl_sync(0xffffffffu, kk[3], 31);
-        bool wide = false;
-        if (K32 && kmask != 0) {
-            uint32_t hiw = 0;
+        for (int64_t st = s0; st < s1; ++st) {
+            const int64_t base = b0 + (st << 7);
+            uint64_t wv[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) hiw |= (uint32_t)(wv[u] >> 32) | (uint32_t)(rv[u] >> 32);
-            wide = __any_sync(0xffffffffu, (hiw & kmask) != 0);
-        }
-        const bool full = base >= lo_chk && base + 128 <= w.end;
-        const int64_t v0 = base + 4 * lane;
-        if (!wide) {
-            uint32_t r32[4], s32[4];
-            uint64_t hh[4];
+            for (int u = 0; u < 4; ++u) wv[u] = nx[u];
+            if (st + 1 < s1) {
+                if (LEAN) {
+                    sq += 128;
+                    ld16(sq, nx);
+                } else {
+                    load4(base + 128 + 4 * lane, nx);
+                }
+            }
+            KT kk[4];
+            uint64_t rv[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                r32[u] = K32 ? (uint32_t)rv[u] : (uint32_t)rv[u] & pmask32;
-                s32[u] = K32 ? (uint32_t)wv[u] : (uint32_t)wv[u] & pmask32;
-                hh[u] = SW ? pair_hash32_mix<MPSM_DJ_FMA>(s32[u], r32[u], fk)
-                           : pair_hash32_mix<MPSM_DJ_FMA>(r32[u], s32[u], fk);
+                kk[u] = nk(wv[u]);
+                const KT d = kk[u] - kb;
+                rv[u] = __ldg(rk + (d < nrm1 ? d : nrm1));
             }
-            if (full) {
+            KT prv = __shfl_up_sync(0xffffffffu, kk[3], 1);
+            if (lane == 0) prv = carry;
+            carry = __shfl_sync(0xffffffffu, kk[3], 31);
+            bool wide = false;
+            if (K32 && kmask != 0) {
+                uint32_t hiw = 0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) hiw |= (uint32_t)(wv[u] >> 32) | (uint32_t)(rv[u] >> 32);
+                wide = __any_sync(0xffffffffu, (hiw & kmask) != 0);
+            }
+            const bool full = LEAN || (base >= lo_chk && base + 128 <= w.end);
+            if (!wide) {
+                uint32_t r32[4], s32[4];
+                uint64_t hh[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    max33(r32[u], s32[u], b0m, b1m, h1);
-                    if (MPSM_DJ_FMA & 32) csum = mad_mask64(csum, hh[u], fk.one);
-                    else csum += hh[u];
+                    r32[u] = K32 ? (uint32_t)rv[u] : (uint32_t)rv[u] & pmask32;
+                    s32[u] = K32 ? (uint32_t)wv[u] : (uint32_t)wv[u] & pmask32;
+                    hh[u] = SW ? pair_hash32_mix<MPSM_DJ_FMA>(s32[u], r32[u], fk)
+                               : pair_hash32_mix<MPSM_DJ_FMA>(r32[u], s32[u], fk);
+                }
+                if (full) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        max33(r32[u], s32[u], b0m, b1m, h1);
+                        if (MPSM_DJ_FMA & 32) csum = mad_mask64(csum, hh[u], fk.one);
+                        else csum += hh[u];
+                    }
+                } else {
+                    const int64_t v0 = base + 4 * lane;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const uint32_t m = (v0 + u >= w.start && v0 + u < w.end) ? 1u : 0u;
+                        max33(r32[u] * m, s32[u] * m, b0m, b1m, h1);
+                        csum = mad_mask64(csum, hh[u], m);
+                    }
                 }
             } else {
+                const int64_t v0 = base + 4 * lane;
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const uint32_t m = (v0 + u >= w.start && v0 + u < w.end) ? 1u : 0u;
-                    max33(r32[u] * m, s32[u] * m, b0m, b1m, h1);
-                    csum = mad_mask64(csum, hh[u], m);
+                    const uint64_t rp = rv[u] & pmask, sp = wv[u] & pmask;
+                    const uint64_t h = SW ? pair_hash(sp, rp) : pair_hash(rp, sp);
+                    const uint32_t m = (full || (v0 + u >= w.start && v0 + u < w.end)) ? 1u : 0u;
+                    max_into(best, (rp + sp) * m);
+                    csum = mad_mask64(csum, h, m);
                 }
             }
-        } else {
+            if (full) {
+                bad |= (prv > kk[0]) | (kk[0] > kk[1]) | (kk[1] > kk[2]) | (kk[2] > kk[3]);
+                cnt += 128;
+            } else {
+                const int64_t v0 = base + 4 * lane;
+                KT pv = prv;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint64_t rp = rv[u] & pmask, sp = wv[u] & pmask;
-                const uint64_t h = SW ? pair_hash(sp, rp) : pair_hash(rp, sp);
-                const uint32_t m = (full || (v0 + u >= w.start && v0 + u < w.end)) ? 1u : 0u;
-                max_into(best, (rp + sp) * m);
-                csum = mad_mask64(csum, h, m);
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t v = v0 + u;
+                    bad |= (v >= lo_chk && v < w.end) && pv > kk[u];
+                    pv = kk[u];
+                }
+                cnt += max((int64_t)0, min(w.end, base + 128) - max(w.start, base));
             }
         }
-        if (full) {
-            bad |= (prv > kk[0]) | (kk[0] > kk[1]) | (kk[1] > kk[2]) | (kk[2] > kk[3]);
-            cnt += 128;
-        } else {
-            KT pv = prv;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int64_t v = v0 + u;
-                bad |= (v >= lo_chk && v < w.end) && pv > kk[u];
-                pv = kk[u];
-            }
-            cnt += max((int64_t)0, min(w.end, base + 128) - max(w.start, base));
-        }
-    }
+    };
+    if (interior) run(std::true_type{});
+    else run(std::false_type{});
     {
         const uint64_t cb = h1 ? ((1ull << 32) | b1m) : (uint64_t)b0m;
         if (cb > best) best = cb;
