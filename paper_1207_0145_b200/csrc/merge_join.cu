@@ -2351,98 +2351,122 @@ __global__ void __launch_bounds__(DF_THREADS, MPSM_DF_MINB) k_dense_flat(DfArgs 
             KT carry = (base - 1 >= 0) ? nk(sk[base - 1]) : (KT)0;
             if (st != pre_step) load4(base + 4 * lane, nx);  // not prefetched
             pre_step = -1;
-            for (; st < se; ++st, base += 128) {
-                uint64_t wv[4];
+            // a segment inside the window (all but a pair's first and last
+            // few steps) runs lean: no bounds, masks or 64-bit index math
+            const bool inside = base >= lo_chk && b0 + ((se - p_first) << 7) <= wend;
+            auto segment = [&](auto lean_tag) {
+                constexpr bool LEAN = decltype(lean_tag)::value;
+                const uint64_t* sq = sk + base + 4 * lane;
+                auto ld16 = [&](const uint64_t* q, uint64_t* x) {
+                    const ulonglong2 a0 = __ldcs(reinterpret_cast<const ulonglong2*>(q));
+                    const ulonglong2 a1 = __ldcs(reinterpret_cast<const ulonglong2*>(q + 2));
+                    x[0] = a0.x;
+                    x[1] = a0.y;
+                    x[2] = a1.x;
+                    x[3] = a1.y;
+                };
+                for (; st < se; ++st, base += 128) {
+                    uint64_t wv[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) wv[u] = nx[u];
-                if (st + 1 < se) {
-                    load4(base + 128 + 4 * lane, nx);
-                } else if (st + 1 == c1) {
-                    // the warp's next chunk, when it continues this pair:
-                    // its first step's S in flight during this step
-                    const int64_t nc = c0 + nw * MPSM_DF_CHUNK;
-                    if (nc < p_end) {
-                        load4(b0 + ((nc - p_first) << 7) + 4 * lane, nx);
-                        pre_step = nc;
+                    for (int u = 0; u < 4; ++u) wv[u] = nx[u];
+                    if (st + 1 < se) {
+                        if (LEAN) {
+                            sq += 128;
+                            ld16(sq, nx);
+                        } else {
+                            load4(base + 128 + 4 * lane, nx);
+                        }
+                    } else if (st + 1 == c1) {
+                        // the warp's next chunk, when it continues this pair:
+                        // its first step's S in flight during this step
+                        const int64_t nc = c0 + nw * MPSM_DF_CHUNK;
+                        if (nc < p_end) {
+                            load4(b0 + ((nc - p_first) << 7) + 4 * lane, nx);
+                            pre_step = nc;
+                        }
                     }
-                }
-                KT kk[4];
-                uint64_t rv[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    kk[u] = nk(wv[u]);
-                    const KT d = kk[u] - kb;
-#ifdef MPSM_DBG_DF_NO_GATHER
-                    rv[u] = wv[u] ^ (uint64_t)d;
-#else
-                    rv[u] = __ldg(rk + (d < nrm1 ? d : nrm1));
-#endif
-                }
-                KT prv = __shfl_up_sync(0xffffffffu, kk[3], 1);
-                if (lane == 0) prv = carry;
-                carry = __shfl_sync(0xffffffffu, kk[3], 31);
-                bool wide = false;
-                if (K32 && kmask != 0) {
-                    uint32_t hiw = 0;
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) hiw |= (uint32_t)(wv[u] >> 32) | (uint32_t)(rv[u] >> 32);
-                    wide = __any_sync(0xffffffffu, (hiw & kmask) != 0);
-                }
-                const bool full = base >= lo_chk && base + 128 <= wend;
-                const int64_t v0 = base + 4 * lane;
-                if (!wide) {
-                    uint32_t r32[4], s32[4];
-                    uint64_t hh[4];
+                    KT kk[4];
+                    uint64_t rv[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        r32[u] = K32 ? (uint32_t)rv[u] : (uint32_t)rv[u] & pmask32;
-                        s32[u] = K32 ? (uint32_t)wv[u] : (uint32_t)wv[u] & pmask32;
-#ifdef MPSM_DBG_DF_NO_HASH
-                        hh[u] = (uint64_t)r32[u] * s32[u];
+                        kk[u] = nk(wv[u]);
+                        const KT d = kk[u] - kb;
+#ifdef MPSM_DBG_DF_NO_GATHER
+                        rv[u] = wv[u] ^ (uint64_t)d;
 #else
-                        hh[u] = SW ? pair_hash32_mix<MPSM_DJ_FMA>(s32[u], r32[u], fk)
-                                   : pair_hash32_mix<MPSM_DJ_FMA>(r32[u], s32[u], fk);
+                        rv[u] = __ldg(rk + (d < nrm1 ? d : nrm1));
 #endif
                     }
-                    if (full) {
+                    KT prv = __shfl_up_sync(0xffffffffu, kk[3], 1);
+                    if (lane == 0) prv = carry;
+                    carry = __shfl_sync(0xffffffffu, kk[3], 31);
+                    bool wide = false;
+                    if (K32 && kmask != 0) {
+                        uint32_t hiw = 0;
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) hiw |= (uint32_t)(wv[u] >> 32) | (uint32_t)(rv[u] >> 32);
+                        wide = __any_sync(0xffffffffu, (hiw & kmask) != 0);
+                    }
+                    const bool full = LEAN || (base >= lo_chk && base + 128 <= wend);
+                    if (!wide) {
+                        uint32_t r32[4], s32[4];
+                        uint64_t hh[4];
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
-                            max33(r32[u], s32[u], b0m, b1m, h1);
-                            if (MPSM_DJ_FMA & 32) csum = mad_mask64(csum, hh[u], fk.one);
-                            else csum += hh[u];
+                            r32[u] = K32 ? (uint32_t)rv[u] : (uint32_t)rv[u] & pmask32;
+                            s32[u] = K32 ? (uint32_t)wv[u] : (uint32_t)wv[u] & pmask32;
+#ifdef MPSM_DBG_DF_NO_HASH
+                            hh[u] = (uint64_t)r32[u] * s32[u];
+#else
+                            hh[u] = SW ? pair_hash32_mix<MPSM_DJ_FMA>(s32[u], r32[u], fk)
+                                       : pair_hash32_mix<MPSM_DJ_FMA>(r32[u], s32[u], fk);
+#endif
+                        }
+                        if (full) {
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                max33(r32[u], s32[u], b0m, b1m, h1);
+                                if (MPSM_DJ_FMA & 32) csum = mad_mask64(csum, hh[u], fk.one);
+                                else csum += hh[u];
+                            }
+                        } else {
+                            const int64_t v0 = base + 4 * lane;
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const uint32_t m = (v0 + u >= wstart && v0 + u < wend) ? 1u : 0u;
+                                max33(r32[u] * m, s32[u] * m, b0m, b1m, h1);
+                                csum = mad_mask64(csum, hh[u], m);
+                            }
                         }
                     } else {
+                        const int64_t v0 = base + 4 * lane;
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
-                            const uint32_t m = (v0 + u >= wstart && v0 + u < wend) ? 1u : 0u;
-                            max33(r32[u] * m, s32[u] * m, b0m, b1m, h1);
-                            csum = mad_mask64(csum, hh[u], m);
+                            const uint64_t rp = rv[u] & pmask, sp = wv[u] & pmask;
+                            const uint64_t h = SW ? pair_hash(sp, rp) : pair_hash(rp, sp);
+                            const uint32_t m = (full || (v0 + u >= wstart && v0 + u < wend)) ? 1u : 0u;
+                            max_into(best, (rp + sp) * m);
+                            csum = mad_mask64(csum, h, m);
                         }
                     }
-                } else {
+                    if (full) {
+                        bad |= (prv > kk[0]) | (kk[0] > kk[1]) | (kk[1] > kk[2]) | (kk[2] > kk[3]);
+                        cnt += 128;
+                    } else {
+                        const int64_t v0 = base + 4 * lane;
+                        KT pv = prv;
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const uint64_t rp = rv[u] & pmask, sp = wv[u] & pmask;
-                        const uint64_t h = SW ? pair_hash(sp, rp) : pair_hash(rp, sp);
-                        const uint32_t m = (full || (v0 + u >= wstart && v0 + u < wend)) ? 1u : 0u;
-                        max_into(best, (rp + sp) * m);
-                        csum = mad_mask64(csum, h, m);
+                        for (int u = 0; u < 4; ++u) {
+                            const int64_t v = v0 + u;
+                            bad |= (v >= lo_chk && v < wend) && pv > kk[u];
+                            pv = kk[u];
+                        }
+                        cnt += max((int64_t)0, min(wend, base + 128) - max(wstart, base));
                     }
                 }
-                if (full) {
-                    bad |= (prv > kk[0]) | (kk[0] > kk[1]) | (kk[1] > kk[2]) | (kk[2] > kk[3]);
-                    cnt += 128;
-                } else {
-                    KT pv = prv;
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int64_t v = v0 + u;
-                        bad |= (v >= lo_chk && v < wend) && pv > kk[u];
-                        pv = kk[u];
-                    }
-                    cnt += max((int64_t)0, min(wend, base + 128) - max(wstart, base));
-                }
-            }
+            };
+            if (inside) segment(std::true_type{});
+            else segment(std::false_type{});
         }
     }
     flush();
