@@ -279,9 +279,18 @@ __global__ void __launch_bounds__(THREADS, 2) k_count(const uint64_t* __restrict
     for (int64_t c0 = b; c0 < e; c0 += TILE) {
         if (c0 + TILE < e) load(w, c0 + TILE);  // next chunk in flight during this one
         const uint32_t row = (uint32_t)(k * TPS + (TPS == 1 ? 0 : q));
-        if (c0 + TILE <= e && !d_bad) {  // a whole chunk, no domain check: no per-item guards
+        if (c0 + TILE <= e) {  // a whole chunk: no per-item index guards
+            uint64_t viol = 0;  // first pass: any key outside the domain (rare: then the exact index below)
 #pragma unroll
-            for (int u = 0; u < ITEMS; ++u) bump(row, TABLE ? dig.lookup(v[u]) : dig(v[u]));
+            for (int u = 0; u < ITEMS; ++u) {
+                if (d_bad) viol |= (uint64_t)(v[u] - dig.lower > span_m1);
+                bump(row, TABLE ? dig.lookup(v[u]) : dig(v[u]));
+            }
+            if (viol) {
+#pragma unroll
+                for (int u = 0; u < ITEMS; ++u)
+                    if (v[u] - dig.lower > span_m1) atomicMin(d_bad, (unsigned long long)pos(c0, u));
+            }
         } else {
 #pragma unroll
             for (int u = 0; u < ITEMS; ++u) {
