@@ -3,7 +3,9 @@ pair layouts, both engines, several worker counts and role policies) against
 the CPU oracle on seeded inputs -- match count, MAX, checksum and every
 worker statistic bit-exact.  Sizes straddle the kernels' tile edges (4096 /
 8192-tuple sort tiles, 1920-element merge tiles) and key distributions cover
-unique keys, heavy duplicates on both sides, skew and pre-sorted inputs."""
+unique keys, heavy duplicates on both sides, skew, pre-sorted inputs and
+dense private sides with foreign keys (the streamed dense join; with one key
+doubled and one missing, the merge walk)."""
 
 import numpy as np
 import pytest
@@ -53,7 +55,7 @@ for _i in range(int(os.environ.get("MPSM_RANDOM_CASES", "96"))):
         n_r=int(_rng.choice([0, 1, 4095, 8193, 20_000, 150_001])),
         n_s=int(_rng.choice([1, 1919, 1921, 4096, 60_000, 400_003])),
         width=int(_rng.choice([1, 6, 13, 20, 27, 32, 40])),
-        kind=str(_rng.choice(["uniform", "dups", "skew", "sorted"])),
+        kind=str(_rng.choice(["uniform", "dups", "skew", "sorted", "fk", "fk", "fkhole"])),
         threads=int(_rng.choice([1, 2, 3, 8])),
         algorithm=str(_rng.choice(["p-mpsm", "b-mpsm"])),
         role=str(_rng.choice(["auto", "r-private", "s-private"])),
@@ -71,8 +73,20 @@ def test_random_join_matches_oracle(case, monkeypatch):
     rng = np.random.default_rng(case["seed"])
     lower = int(rng.integers(0, 1 << 20))
     span = 1 << case["width"]
-    rk = _keys(rng, case["n_r"], lower, span, case["kind"])
-    sk = _keys(rng, case["n_s"], lower, span, case["kind"])
+    if case["kind"] in ("fk", "fkhole") and 2 <= case["n_r"] <= span:
+        # a dense private side (consecutive keys: the streamed dense join)
+        # and foreign keys around it; fkhole: one key doubled and one missing
+        # (not dense: the merge walk)
+        start = int(rng.integers(0, span - case["n_r"] + 1))
+        rk = (rng.permutation(case["n_r"]).astype(np.uint64) + np.uint64(start + lower)).astype(np.uint64)
+        if case["kind"] == "fkhole":
+            rk[rk == np.uint64(start + lower + 1)] = np.uint64(start + lower)
+        lo_s, hi_s = max(0, start - 8), min(span, start + case["n_r"] + 8)
+        sk = (rng.integers(lo_s, hi_s, case["n_s"], dtype=np.uint64) + np.uint64(lower)).astype(np.uint64)
+    else:
+        kind = "uniform" if case["kind"] in ("fk", "fkhole") else case["kind"]
+        rk = _keys(rng, case["n_r"], lower, span, kind)
+        sk = _keys(rng, case["n_s"], lower, span, kind)
     hi = np.iinfo(np.uint64).max if case["wide"] else (1 << 32) - 1
     rp = rng.integers(0, hi, case["n_r"], dtype=np.uint64, endpoint=True)
     sp = rng.integers(0, hi, case["n_s"], dtype=np.uint64, endpoint=True)
