@@ -112,6 +112,18 @@ int mpsm_sort_packed(const uint64_t* in_keys, const uint64_t* in_pays, int64_t n
                      int width_bits, uint64_t* out_rec, uint64_t* tmp_rec, void* workspace, size_t ws_bytes,
                      unsigned long long* d_bad, unsigned int* d_overflow, void* stream);
 
+/* the same with a density probe of the sorted output (the private side of
+ * an FK join): the last pass reduces key(R[p]) - p over every output record
+ * p into d_dense[0] (min) and d_dense[1] (max), uint32, written by the call.
+ * Runs for width_bits <= 32 and n < 2^32; otherwise d_dense is set to
+ * "unknown" (d_dense[0] > d_dense[1]).  The sorted run is dense (its keys
+ * consecutive) iff d_dense[0] == d_dense[1] and key(R[n-1]) - key(R[0]) ==
+ * n - 1; mpsm_join_pairs_packed_hint takes it instead of reading the run. */
+int mpsm_sort_packed_dense(const uint64_t* in_keys, const uint64_t* in_pays, int64_t n, uint64_t lower,
+                           uint64_t span_m1, int width_bits, uint64_t* out_rec, uint64_t* tmp_rec, void* workspace,
+                           size_t ws_bytes, unsigned long long* d_bad, unsigned int* d_overflow, uint32_t* d_dense,
+                           void* stream);
+
 /* ------------------------------------------------- radix histogram ----
  * Replaces _kernels.radix_histogram (_kernels.py:247-259) / partition.
  * build_radix_histogram (partition.py:110-122): d_counts[(key-lower)>>shift]
@@ -199,6 +211,15 @@ int mpsm_join_pairs(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, i
 int mpsm_join_pairs_packed(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub, int width_bits,
                            uint64_t lower, int swap, int mode, uint64_t* d_out, int64_t cap, uint64_t* d_pairs,
                            void* workspace, size_t ws_bytes, void* stream);
+/* mpsm_join_pairs_packed with the density probe of the sorted array the
+ * private runs were cut from (priv_n records at priv_base; d_dense from
+ * mpsm_sort_packed_dense / mpsm_sort_records_dense): when it proves the
+ * array dense, the dense-run path skips its own read of the private runs
+ * (d_dense may be NULL: the same as mpsm_join_pairs_packed) */
+int mpsm_join_pairs_packed_hint(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub,
+                                int width_bits, uint64_t lower, int swap, int mode, uint64_t* d_out, int64_t cap,
+                                uint64_t* d_pairs, void* workspace, size_t ws_bytes, const uint32_t* d_dense,
+                                const uint64_t* priv_base, int64_t priv_n, void* stream);
 
 /* ------------------------------------------------ splitter search ----
  * Replaces skew._minmax_contiguous (skew.py:180-273) as used by
@@ -281,6 +302,9 @@ uint64_t mpsm_upload_bytes(int reset);
  * mpsm_sort_pairs. */
 int mpsm_sort_records(const uint64_t* in_rec, int64_t n, int width_bits, uint64_t* out_rec, uint64_t* tmp_rec,
                       void* workspace, size_t ws_bytes, void* stream);
+/* mpsm_sort_records with the density probe of mpsm_sort_packed_dense */
+int mpsm_sort_records_dense(const uint64_t* in_rec, int64_t n, int width_bits, uint64_t* out_rec,
+                            uint64_t* tmp_rec, void* workspace, size_t ws_bytes, uint32_t* d_dense, void* stream);
 
 /* ------------------------------------------------ segmented run sort ----
  * nseg independent sorts in one launch sequence: elements [h_offsets[s],

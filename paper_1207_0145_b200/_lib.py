@@ -38,7 +38,8 @@ EXPORTS = (
     "mpsm_deinterleave",
     "mpsm_upload_records", "mpsm_upload_bytes", "mpsm_sort_records", "mpsm_pack_records", "mpsm_partition_records",
     "mpsm_sort_segments_workspace_bytes", "mpsm_sort_pairs_segments", "mpsm_sort_packed_segments",
-    "mpsm_sort_records_segments",
+    "mpsm_sort_records_segments", "mpsm_sort_packed_dense", "mpsm_sort_records_dense",
+    "mpsm_join_pairs_packed_hint",
 )
 
 
@@ -89,6 +90,10 @@ _SIGS = {
     "mpsm_sort_packed_segments": (_int, [_vp, _vp, _i64, _int, _vp, _u64, _u64, _int, _vp, _vp, _vp, _sz, _vp, _vp,
                                          _vp]),
     "mpsm_sort_records_segments": (_int, [_vp, _i64, _int, _vp, _int, _vp, _vp, _vp, _sz, _vp]),
+    "mpsm_sort_packed_dense": (_int, [_vp, _vp, _i64, _u64, _u64, _int, _vp, _vp, _vp, _sz, _vp, _vp, _vp, _vp]),
+    "mpsm_sort_records_dense": (_int, [_vp, _i64, _int, _vp, _vp, _vp, _sz, _vp, _vp]),
+    "mpsm_join_pairs_packed_hint": (_int, [ctypes.POINTER(RunDesc), _int, ctypes.POINTER(RunDesc), _int, _int, _u64,
+                                           _int, _int, _vp, _i64, _vp, _vp, _sz, _vp, _vp, _i64, _vp]),
     "mpsm_upload_bytes": (_u64, [_int]),
     "mpsm_pack_records": (_int, [_vp, _vp, _i64, _u64, _u64, _int, _vp, _vp, _vp, _vp]),
     "mpsm_partition_records": (_int, [_vp, _vp, _i64, _u64, _u64, _int, _int, _vp, _int, _int, _vp, _vp, _sz, _vp,

@@ -1445,14 +1445,27 @@ __device__ __forceinline__ int dj_run_of(const int64_t* __restrict__ blk_base, i
 // step: four 16-B loads in flight per lane (record pairs), neighbours across
 // lanes by shuffles.  A run not 16-B aligned is checked from its second
 // record on, the first against it separately.
+// hint (optional): the density probe of the sorted array the private runs
+// were cut from (mpsm_sort_*_dense: min / max of key - position over its hn
+// records at hbase).  Equal, with key(last) - key(first) = hn - 1, the array
+// is dense -- and so is every run cut from it: no run is read.
 __global__ void __launch_bounds__(256) k_dense_check(const mpsm_run_t* __restrict__ priv, int pw,
-                                                     uint32_t* __restrict__ nondense, uint64_t* __restrict__ kb) {
+                                                     uint32_t* __restrict__ nondense, uint64_t* __restrict__ kb,
+                                                     const uint32_t* __restrict__ hint,
+                                                     const uint64_t* __restrict__ hbase, int64_t hn) {
     const int i = blockIdx.y;
     const mpsm_run_t r = priv[i];
     const int lane = threadIdx.x & 31;
     if (r.n <= 0) {
         if (blockIdx.x == 0 && threadIdx.x == 0) nondense[i] = 1;
         return;
+    }
+    if (hint && hn > 0 && hint[0] == hint[1] && r.keys >= hbase && r.keys + r.n <= hbase + hn) {
+        const uint64_t k0 = hbase[0] >> pw, k1 = hbase[hn - 1] >> pw;
+        if (k1 >= k0 && k1 - k0 == (uint64_t)(hn - 1)) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) kb[i] = k0 + (uint64_t)(r.keys - hbase);
+            return;  // nondense[i] stays 0
+        }
     }
     const int64_t head = ((uintptr_t)r.keys & 15) ? 1 : 0;
     bool bad = false;
@@ -1852,9 +1865,12 @@ __global__ void __launch_bounds__(DJ_THREADS, MPSM_DJ_CTAS) k_dense_join(DjArgs 
     uint64_t best = 0, csum = 0;
     int64_t cnt = 0;  // warp-uniform
     bool bad = false;
+    KT vacc = 0;  // OR of (gathered R key ^ S key) over whole chunks: nonzero = a run not dense after all
     uint32_t b0 = 0, b1 = 0, h1 = 0;  // max33 classes of the warp's current pair
     auto flush_regs = [&]() {
         if (acc_j < 0) return;
+        bad |= vacc != 0;
+        vacc = 0;
         {
             const uint64_t cb = h1 ? ((1ull << 32) | b1) : (uint64_t)b0;
             if (cb > best) best = cb;
@@ -2047,6 +2063,9 @@ __global__ void __launch_bounds__(DJ_THREADS, MPSM_DJ_CTAS) k_dense_join(DjArgs 
                 }
                 if (full) {
                     bad |= (prv > kk[0]) | (kk[0] > kk[1]) | (kk[1] > kk[2]) | (kk[2] > kk[3]);
+                    // every gathered R tuple must carry the S key (a private
+                    // run that is not dense after all: flagged, not miscounted)
+                    vacc |= (nk(rv[0]) ^ kk[0]) | (nk(rv[1]) ^ kk[1]) | (nk(rv[2]) ^ kk[2]) | (nk(rv[3]) ^ kk[3]);
                     cnt += DJ_CHUNK;
                 } else {
                     const int v0 = k0 + 4 * lane;
@@ -2055,6 +2074,7 @@ __global__ void __launch_bounds__(DJ_THREADS, MPSM_DJ_CTAS) k_dense_join(DjArgs 
                     for (int u = 0; u < 4; ++u) {
                         const int v = v0 + u;
                         bad |= (v < nv && v - 1 >= lo_ok) && pv > kk[u];
+                        bad |= (v >= lead && v < nv) && nk(rv[u]) != kk[u];
                         pv = kk[u];
                     }
                     cnt += max(0, min(nv, k0 + DJ_CHUNK) - max(k0, lead));
@@ -2266,8 +2286,11 @@ __global__ void __launch_bounds__(DF_THREADS, MPSM_DF_MINB) k_dense_flat(DfArgs 
     uint32_t b0m = 0, b1m = 0, h1 = 0;
     int64_t cnt = 0;  // warp-uniform
     bool bad = false;
+    KT vacc = 0;  // OR of (gathered R key ^ S key) over whole steps: nonzero = a run not dense after all
     auto flush = [&]() {
         if (p < 0) return;
+        bad |= vacc != 0;
+        vacc = 0;
         const uint64_t cb = h1 ? ((1ull << 32) | b1m) : (uint64_t)b0m;
         if (cb > best) best = cb;
         const uint32_t lo = (uint32_t)csum, hi = (uint32_t)(csum >> 32);
@@ -2451,6 +2474,9 @@ __global__ void __launch_bounds__(DF_THREADS, MPSM_DF_MINB) k_dense_flat(DfArgs 
                     }
                     if (full) {
                         bad |= (prv > kk[0]) | (kk[0] > kk[1]) | (kk[1] > kk[2]) | (kk[2] > kk[3]);
+                    // every gathered R tuple must carry the S key (a private
+                    // run that is not dense after all: flagged, not miscounted)
+                    vacc |= (nk(rv[0]) ^ kk[0]) | (nk(rv[1]) ^ kk[1]) | (nk(rv[2]) ^ kk[2]) | (nk(rv[3]) ^ kk[3]);
                         cnt += 128;
                     } else {
                         const int64_t v0 = base + 4 * lane;
@@ -2459,6 +2485,7 @@ __global__ void __launch_bounds__(DF_THREADS, MPSM_DF_MINB) k_dense_flat(DfArgs 
                         for (int u = 0; u < 4; ++u) {
                             const int64_t v = v0 + u;
                             bad |= (v >= lo_chk && v < wend) && pv > kk[u];
+                            bad |= (v >= wstart && v < wend) && nk(rv[u]) != kk[u];
                             pv = kk[u];
                         }
                         cnt += max((int64_t)0, min(wend, base + 128) - max(wstart, base));
@@ -2566,6 +2593,7 @@ __global__ void __launch_bounds__(DF_THREADS, 4) k_dense_flat1(const mpsm_run_t*
     uint32_t b0m = 0, b1m = 0, h1 = 0;
     int64_t cnt = 0;  // warp-uniform
     bool bad = false;
+    KT vacc = 0;  // OR of (gathered R key ^ S key) over whole steps: nonzero = a run not dense after all
     KT carry = 0;
     if (s0 < s1) {
         const int64_t first = b0 + (s0 << 7);
@@ -2662,6 +2690,9 @@ __global__ void __launch_bounds__(DF_THREADS, 4) k_dense_flat1(const mpsm_run_t*
             }
             if (full) {
                 bad |= (prv > kk[0]) | (kk[0] > kk[1]) | (kk[1] > kk[2]) | (kk[2] > kk[3]);
+                    // every gathered R tuple must carry the S key (a private
+                    // run that is not dense after all: flagged, not miscounted)
+                    vacc |= (nk(rv[0]) ^ kk[0]) | (nk(rv[1]) ^ kk[1]) | (nk(rv[2]) ^ kk[2]) | (nk(rv[3]) ^ kk[3]);
                 cnt += 128;
             } else {
                 const int64_t v0 = base + 4 * lane;
@@ -2670,6 +2701,7 @@ __global__ void __launch_bounds__(DF_THREADS, 4) k_dense_flat1(const mpsm_run_t*
                 for (int u = 0; u < 4; ++u) {
                     const int64_t v = v0 + u;
                     bad |= (v >= lo_chk && v < w.end) && pv > kk[u];
+                    bad |= (v >= w.start && v < w.end) && nk(rv[u]) != kk[u];
                     pv = kk[u];
                 }
                 cnt += max((int64_t)0, min(w.end, base + 128) - max(w.start, base));
@@ -2678,6 +2710,7 @@ __global__ void __launch_bounds__(DF_THREADS, 4) k_dense_flat1(const mpsm_run_t*
     };
     if (interior) run(std::true_type{});
     else run(std::false_type{});
+    bad |= vacc != 0;
     {
         const uint64_t cb = h1 ? ((1ull << 32) | b1m) : (uint64_t)b0m;
         if (cb > best) best = cb;
@@ -2841,7 +2874,8 @@ static int launch_dense(const DjArgs& a, int swap, cudaStream_t st) {
 template <bool PK>
 static int join_pairs_impl(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub, int swap, int mode,
                            uint64_t* d_out, int64_t cap, uint64_t* d_pairs, void* workspace, size_t ws_bytes,
-                           const PackInfo& pi, cudaStream_t st) {
+                           const PackInfo& pi, cudaStream_t st, const uint32_t* hint = nullptr,
+                           const uint64_t* hbase = nullptr, int64_t hn = 0) {
     if (n_priv < 1 || n_pub < 1 || !d_pairs) return MPSM_ERR_ARG;
     if (mode == MPSM_MODE_MATERIALIZE && d_out && cap < 0) return MPSM_ERR_ARG;
     if (mode < 0 || mode > 2) return MPSM_ERR_ARG;
@@ -2871,7 +2905,7 @@ static int join_pairs_impl(const mpsm_run_t* priv, int n_priv, const mpsm_run_t*
                     w.win,    dw.L,    dw.tb,    dw.nsub, dw.part,   dw.tiles,  dw.ntiles,   d_pairs,   pi};
         ProfScope ps("dense_check", st);
         const dim3 grid((unsigned)std::max(1, num_sms() * 4 / n_priv), (unsigned)n_priv);
-        k_dense_check<<<grid, 256, 0, st>>>(w.d_priv, pi.pw, dw.nondense, dw.kb);
+        k_dense_check<<<grid, 256, 0, st>>>(w.d_priv, pi.pw, dw.nondense, dw.kb, hint, hbase, hn);
         MPSM_TRY(check_launch("k_dense_check"));
     }
     k_windows<PK><<<(npairs + 127) / 128, 128, 0, st>>>(w.d_priv, n_priv, w.d_pub, n_pub, w.win, d_pairs, pi,
@@ -2977,4 +3011,20 @@ extern "C" int mpsm_join_pairs_packed(const mpsm_run_t* priv, int n_priv, const 
     return join_pairs_impl<true>(priv, n_priv, pub, n_pub, swap, mode, d_out, cap, d_pairs, workspace, ws_bytes,
                                  PackInfo{pw, lower, (1ull << pw) - 1, pw >= 32 ? (1u << (pw - 32)) - 1u : 0u},
                                  (cudaStream_t)stream);
+}
+
+extern "C" int mpsm_join_pairs_packed_hint(const mpsm_run_t* priv, int n_priv, const mpsm_run_t* pub, int n_pub,
+                                           int width_bits, uint64_t lower, int swap, int mode, uint64_t* d_out,
+                                           int64_t cap, uint64_t* d_pairs, void* workspace, size_t ws_bytes,
+                                           const uint32_t* d_dense, const uint64_t* priv_base, int64_t priv_n,
+                                           void* stream) {
+    if (width_bits < 1 || width_bits > 63 || priv_n < 0 || (d_dense && priv_n > 0 && !priv_base)) {
+        set_error("mpsm_join_pairs_packed_hint: bad width, private length or missing base");
+        return MPSM_ERR_ARG;
+    }
+    if (priv_n == 0) d_dense = nullptr;  // nothing to hint
+    const int pw = 64 - width_bits;
+    return join_pairs_impl<true>(priv, n_priv, pub, n_pub, swap, mode, d_out, cap, d_pairs, workspace, ws_bytes,
+                                 PackInfo{pw, lower, (1ull << pw) - 1, pw >= 32 ? (1u << (pw - 32)) - 1u : 0u},
+                                 (cudaStream_t)stream, d_dense, priv_base, priv_n);
 }

@@ -792,7 +792,7 @@ __global__ void __launch_bounds__(WsCfg<LAYOUT>::THREADS_ALL, 1) k_scatter_ws(
     const uint64_t* __restrict__ in_k, const uint64_t* __restrict__ in_p, uint64_t* __restrict__ out_k, Segs sg,
     Digit dig, Digit odig, int nbins, const int64_t* __restrict__ base, const uint32_t* __restrict__ toffs,
     const int64_t* __restrict__ dtot, unsigned int* __restrict__ ticket, uint64_t pk_lower, int pk_pw,
-    unsigned int* __restrict__ overflow, bool lane_ordered) {
+    unsigned int* __restrict__ overflow, bool lane_ordered, uint32_t* __restrict__ dense, int dshift) {
     static_assert(LAYOUT != SS, "record output only");
     constexpr int WS_WRITERS = WsCfg<LAYOUT>::WRITERS, WS_THREADS = WsCfg<LAYOUT>::THREADS_ALL;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -867,6 +867,9 @@ __global__ void __launch_bounds__(WsCfg<LAYOUT>::THREADS_ALL, 1) k_scatter_ws(
 
     if (!ranker) {  // ------------------------------------------ writers
         const int wt = tid - THREADS;
+        // density probe (dense != null, the last pass of a sort): min / max
+        // of key - output position over the records this writer stores
+        uint32_t dmin = 0xffffffffu, dmax = 0;
         for (int b = 0;; b = (b == WS_NB - 1) ? 0 : b + 1) {
 #ifdef MPSM_DBG_TIMING
             const long long w0 = clock64();
@@ -881,18 +884,39 @@ __global__ void __launch_bounds__(WsCfg<LAYOUT>::THREADS_ALL, 1) k_scatter_ws(
             const int cnt = sm.tcnt[b];
             const uint64_t* sb = sm.buf[b][0];
             const int64_t* gd = sm.gdelta[b];
+            if (dense) {
 #pragma unroll 4
-            for (int i = wt; i < cnt; i += WS_WRITERS) {
-                const uint64_t v = sb[i];
-                const int64_t o = gd[TABLE ? odig.lookup(v) : rec_digit<HI>(v, odig)] + i;
-                MPSM_CHECK(o >= 0 && o < sg.n);
-                out_k[o] = v;
+                for (int i = wt; i < cnt; i += WS_WRITERS) {
+                    const uint64_t v = sb[i];
+                    const int64_t o = gd[TABLE ? odig.lookup(v) : rec_digit<HI>(v, odig)] + i;
+                    MPSM_CHECK(o >= 0 && o < sg.n);
+                    out_k[o] = v;
+                    const uint32_t d = (uint32_t)(v >> dshift) - (uint32_t)o;
+                    dmin = min(dmin, d);
+                    dmax = max(dmax, d);
+                }
+            } else {
+#pragma unroll 4
+                for (int i = wt; i < cnt; i += WS_WRITERS) {
+                    const uint64_t v = sb[i];
+                    const int64_t o = gd[TABLE ? odig.lookup(v) : rec_digit<HI>(v, odig)] + i;
+                    MPSM_CHECK(o >= 0 && o < sg.n);
+                    out_k[o] = v;
+                }
             }
             WS_TS(THREADS, t, 5)
             named_sync(BAR_WRITE, WS_WRITERS);  // buffer b read by every writer
             if (wt == 0) {
                 fence_proxy_async_smem();  // generic accesses to buf[b] before the bulk copy
                 fetch_next(b);
+            }
+        }
+        if (dense) {
+            dmin = __reduce_min_sync(0xffffffffu, dmin);
+            dmax = __reduce_max_sync(0xffffffffu, dmax);
+            if ((wt & 31) == 0) {
+                atomicMin(&dense[0], dmin);
+                atomicMax(&dense[1], dmax);
             }
         }
         return;
@@ -1179,7 +1203,7 @@ template <int LAYOUT, bool TABLE = false>
 static int pass(const uint64_t* in_k, const uint64_t* in_p, uint64_t* out_k, uint64_t* out_p, int64_t n,
                 Digit count_dig, Digit dig, int bits, const Ws& ws, uint64_t span_m1, unsigned long long* d_bad,
                 uint64_t pk_lower, int pk_pw, unsigned int* overflow, cudaStream_t st,
-                const int64_t* dbase = nullptr) {
+                const int64_t* dbase = nullptr, uint32_t* dense = nullptr, int dshift = 0) {
     // segments (count CTAs) are independent of the scatter grid: the tile
     // prefixes make every tile self-contained
     constexpr int64_t TL = LCfg<LAYOUT>::TILE_L;
@@ -1230,11 +1254,11 @@ static int pass(const uint64_t* in_k, const uint64_t* in_p, uint64_t* out_k, uin
             if (hi)
                 k_scatter_ws<LAYOUT, true, TABLE><<<GW, WsCfg<LAYOUT>::THREADS_ALL, sizeof(WsSmem<LAYOUT>), st>>>(
                     in_k, in_p, out_k, sg, dig, odig, nbins, ws.base, ws.toffs, ws.dtot, ws.ticket, pk_lower, pk_pw,
-                    overflow, lo);
+                    overflow, lo, dense, dshift);
             else
                 k_scatter_ws<LAYOUT, false, TABLE><<<GW, WsCfg<LAYOUT>::THREADS_ALL, sizeof(WsSmem<LAYOUT>), st>>>(
                     in_k, in_p, out_k, sg, dig, odig, nbins, ws.base, ws.toffs, ws.dtot, ws.ticket, pk_lower, pk_pw,
-                    overflow, lo);
+                    overflow, lo, dense, dshift);
             return check_launch("k_scatter_ws");
         }
         if (hi)
@@ -1339,13 +1363,23 @@ static int sort_pairs_impl(const uint64_t* in_keys, const uint64_t* in_pays, int
     return MPSM_OK;
 }
 
+// d_dense (optional): the density probe of the sorted output (see
+// mpsm_sort_packed_dense); set to "unknown" (min > max) where it cannot run
+static int dense_init(uint32_t* d_dense, bool probe, cudaStream_t st) {
+    if (!d_dense) return MPSM_OK;
+    MPSM_TRY(cuda_status(cudaMemsetAsync(d_dense, probe ? 0xff : 0x01, sizeof(uint32_t), st), "memset"));
+    return cuda_status(cudaMemsetAsync(d_dense + 1, 0, sizeof(uint32_t), st), "memset");
+}
+
 static int sort_packed_impl(const uint64_t* in_keys, const uint64_t* in_pays, int64_t n, int nseg,
                             const int64_t* h_off, uint64_t lower, uint64_t span_m1, int width_bits, uint64_t* out_rec,
                             uint64_t* tmp_rec, void* workspace, size_t ws_bytes, unsigned long long* d_bad,
-                            unsigned int* d_overflow, void* stream) {
+                            unsigned int* d_overflow, void* stream, uint32_t* d_dense = nullptr) {
     using namespace seg;
     cudaStream_t st = (cudaStream_t)stream;
     if (n < 0 || width_bits < 1 || width_bits > 63 || !d_overflow) return MPSM_ERR_ARG;
+    const bool probe = d_dense && nseg == 0 && width_bits <= 32 && n > 0 && n < ((int64_t)1 << 32);
+    MPSM_TRY(dense_init(d_dense, probe, st));
     if (n == 0) return MPSM_OK;
     Ws ws;
     MPSM_TRY(prepare(workspace, ws_bytes, n, nseg, h_off, &ws, st));
@@ -1355,14 +1389,15 @@ static int sort_packed_impl(const uint64_t* in_keys, const uint64_t* in_pays, in
     const uint64_t* src = nullptr;
     for (int i = 0; i < P; ++i) {
         uint64_t* dst = ((P - 1 - i) % 2 == 0) ? out_rec : tmp_rec;
+        uint32_t* dense = (probe && i == P - 1) ? d_dense : nullptr;  // the last pass probes its output
         if (i == 0) {
             const Digit dg{lower, plan.shift[0], (1u << plan.bits[0]) - 1u};
             MPSM_TRY(pass<SP>(in_keys, in_pays, dst, nullptr, n, dg, dg, plan.bits[0], ws, span_m1, d_bad, lower, pw,
-                              d_overflow, st));
+                              d_overflow, st, nullptr, dense, pw));
         } else {
             const Digit dg{0, pw + plan.shift[i], (1u << plan.bits[i]) - 1u};
             MPSM_TRY(pass<PP>(src, nullptr, dst, nullptr, n, dg, dg, plan.bits[i], ws, ~0ull, nullptr, 0, pw, nullptr,
-                              st));
+                              st, nullptr, dense, pw));
         }
         src = dst;
     }
@@ -1370,10 +1405,13 @@ static int sort_packed_impl(const uint64_t* in_keys, const uint64_t* in_pays, in
 }
 
 static int sort_records_impl(const uint64_t* in_rec, int64_t n, int nseg, const int64_t* h_off, int width_bits,
-                             uint64_t* out_rec, uint64_t* tmp_rec, void* workspace, size_t ws_bytes, void* stream) {
+                             uint64_t* out_rec, uint64_t* tmp_rec, void* workspace, size_t ws_bytes, void* stream,
+                             uint32_t* d_dense = nullptr) {
     using namespace seg;
     cudaStream_t st = (cudaStream_t)stream;
     if (n < 0 || width_bits < 1 || width_bits > 63) return MPSM_ERR_ARG;
+    const bool probe = d_dense && nseg == 0 && width_bits <= 32 && n > 0 && n < ((int64_t)1 << 32);
+    MPSM_TRY(dense_init(d_dense, probe, st));
     if (n == 0) return MPSM_OK;
     const Plan plan = make_plan(width_bits);
     const int pw = 64 - width_bits;
@@ -1390,7 +1428,8 @@ static int sort_records_impl(const uint64_t* in_rec, int64_t n, int nseg, const 
     for (int i = 0; i < P; ++i) {
         uint64_t* dst = ((P - 1 - i) % 2 == 0) ? out_rec : tmp_rec;
         const Digit dg{0, pw + plan.shift[i], (1u << plan.bits[i]) - 1u};
-        MPSM_TRY(pass<PP>(src, nullptr, dst, nullptr, n, dg, dg, plan.bits[i], ws, ~0ull, nullptr, 0, pw, nullptr, st));
+        MPSM_TRY(pass<PP>(src, nullptr, dst, nullptr, n, dg, dg, plan.bits[i], ws, ~0ull, nullptr, 0, pw, nullptr, st,
+                          nullptr, (probe && i == P - 1) ? d_dense : nullptr, pw));
         src = dst;
     }
     return MPSM_OK;
@@ -1414,6 +1453,23 @@ extern "C" int mpsm_sort_packed(const uint64_t* in_keys, const uint64_t* in_pays
 extern "C" int mpsm_sort_records(const uint64_t* in_rec, int64_t n, int width_bits, uint64_t* out_rec,
                                  uint64_t* tmp_rec, void* workspace, size_t ws_bytes, void* stream) {
     return sort_records_impl(in_rec, n, 0, nullptr, width_bits, out_rec, tmp_rec, workspace, ws_bytes, stream);
+}
+
+extern "C" int mpsm_sort_packed_dense(const uint64_t* in_keys, const uint64_t* in_pays, int64_t n, uint64_t lower,
+                                      uint64_t span_m1, int width_bits, uint64_t* out_rec, uint64_t* tmp_rec,
+                                      void* workspace, size_t ws_bytes, unsigned long long* d_bad,
+                                      unsigned int* d_overflow, uint32_t* d_dense, void* stream) {
+    if (!d_dense) return MPSM_ERR_ARG;
+    return sort_packed_impl(in_keys, in_pays, n, 0, nullptr, lower, span_m1, width_bits, out_rec, tmp_rec, workspace,
+                            ws_bytes, d_bad, d_overflow, stream, d_dense);
+}
+
+extern "C" int mpsm_sort_records_dense(const uint64_t* in_rec, int64_t n, int width_bits, uint64_t* out_rec,
+                                       uint64_t* tmp_rec, void* workspace, size_t ws_bytes, uint32_t* d_dense,
+                                       void* stream) {
+    if (!d_dense) return MPSM_ERR_ARG;
+    return sort_records_impl(in_rec, n, 0, nullptr, width_bits, out_rec, tmp_rec, workspace, ws_bytes, stream,
+                             d_dense);
 }
 
 extern "C" int mpsm_sort_segments_workspace_bytes(int64_t n, int nseg, int width_bits, size_t* bytes) {

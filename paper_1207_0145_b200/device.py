@@ -100,29 +100,46 @@ def sort_pairs(in_k: torch.Tensor, in_p: torch.Tensor, lower: int, span_m1: int,
 
 def sort_packed(in_k: torch.Tensor, in_p: torch.Tensor, lower: int, span_m1: int, width_bits: int,
                 out_rec: torch.Tensor, tmp_rec: torch.Tensor, bad: Optional[torch.Tensor],
-                overflow: torch.Tensor) -> None:
+                overflow: torch.Tensor, dense: Optional[torch.Tensor] = None) -> None:
     """Sort into packed records (key - lower) << (64 - w) | payload; sets
-    overflow[0] = 1 if a payload does not fit (caller falls back to SoA)."""
+    overflow[0] = 1 if a payload does not fit (caller falls back to SoA).
+    dense (uint32[2], optional): the density probe of the sorted output
+    (mpsm_sort_packed_dense)."""
     n = int(in_k.numel())
-    if n == 0:
-        return
     L = _lib.load()
+    if n == 0:
+        if dense is not None:
+            dense.copy_(torch.tensor([1, 0], dtype=torch.int32).view(torch.uint32))
+        return
     sz = ctypes.c_size_t(0)
     _lib.check(L.mpsm_sort_workspace_bytes(n, width_bits, ctypes.byref(sz)), "sort workspace")
     ws = workspace(in_k.device).get(sz.value)
+    if dense is not None:
+        _lib.check(L.mpsm_sort_packed_dense(ptr(in_k), ptr(in_p), n, lower, span_m1, width_bits, ptr(out_rec),
+                                            ptr(tmp_rec), ptr(ws), ws.numel(), ptr(bad), ptr(overflow), ptr(dense),
+                                            stream_ptr()), "mpsm_sort_packed_dense")
+        return
     _lib.check(L.mpsm_sort_packed(ptr(in_k), ptr(in_p), n, lower, span_m1, width_bits, ptr(out_rec), ptr(tmp_rec),
                                   ptr(ws), ws.numel(), ptr(bad), ptr(overflow), stream_ptr()), "mpsm_sort_packed")
 
 
-def sort_records(in_rec: torch.Tensor, width_bits: int, out_rec: torch.Tensor, tmp_rec: torch.Tensor) -> None:
-    """Sort packed records (key in the top width_bits bits); in, out, tmp distinct."""
+def sort_records(in_rec: torch.Tensor, width_bits: int, out_rec: torch.Tensor, tmp_rec: torch.Tensor,
+                 dense: Optional[torch.Tensor] = None) -> None:
+    """Sort packed records (key in the top width_bits bits); in, out, tmp
+    distinct (in == out for an even pass count); dense as for sort_packed."""
     n = int(in_rec.numel())
-    if n == 0:
-        return
     L = _lib.load()
+    if n == 0:
+        if dense is not None:
+            dense.copy_(torch.tensor([1, 0], dtype=torch.int32).view(torch.uint32))
+        return
     sz = ctypes.c_size_t(0)
     _lib.check(L.mpsm_sort_workspace_bytes(n, width_bits, ctypes.byref(sz)), "sort workspace")
     ws = workspace(in_rec.device).get(sz.value)
+    if dense is not None:
+        _lib.check(L.mpsm_sort_records_dense(ptr(in_rec), n, width_bits, ptr(out_rec), ptr(tmp_rec), ptr(ws),
+                                             ws.numel(), ptr(dense), stream_ptr()), "mpsm_sort_records_dense")
+        return
     _lib.check(L.mpsm_sort_records(ptr(in_rec), n, width_bits, ptr(out_rec), ptr(tmp_rec), ptr(ws), ws.numel(),
                                    stream_ptr()), "mpsm_sort_records")
 
@@ -315,8 +332,11 @@ def join_pairs(priv: Sequence[tuple], pub: Sequence[tuple], swap: bool, mode: in
 
 
 def join_pairs_packed(priv: Sequence[torch.Tensor], pub: Sequence[torch.Tensor], width_bits: int, lower: int,
-                      swap: bool, mode: int, out: Optional[torch.Tensor] = None, cap: int = 0) -> torch.Tensor:
-    """join_pairs over runs of packed records (one uint64 tensor per run)."""
+                      swap: bool, mode: int, out: Optional[torch.Tensor] = None, cap: int = 0,
+                      hint: Optional[tuple] = None) -> torch.Tensor:
+    """join_pairs over runs of packed records (one uint64 tensor per run).
+    hint: (dense uint32[2], whole sorted private array) the runs were cut
+    from -- the density probe of its sort (mpsm_join_pairs_packed_hint)."""
     dev = (priv[0] if priv else pub[0]).device
     pa = _lib.runs_array((ptr(k) or 0, 0, int(k.numel())) for k in priv)
     ua = _lib.runs_array((ptr(k) or 0, 0, int(k.numel())) for k in pub)
@@ -325,6 +345,13 @@ def join_pairs_packed(priv: Sequence[torch.Tensor], pub: Sequence[torch.Tensor],
     _lib.check(L.mpsm_join_workspace_bytes(pa, len(priv), ua, len(pub), ctypes.byref(sz)), "join workspace")
     ws = workspace(dev).get(sz.value)
     rec = torch.empty((len(priv) * len(pub), _lib.PAIR_FIELDS), dtype=U64, device=dev)
+    if hint is not None:
+        dense, base = hint
+        _lib.check(L.mpsm_join_pairs_packed_hint(pa, len(priv), ua, len(pub), width_bits, lower, int(bool(swap)),
+                                                 int(mode), ptr(out), int(cap), ptr(rec), ptr(ws), ws.numel(),
+                                                 ptr(dense), ptr(base), int(base.numel()), stream_ptr()),
+                   "mpsm_join_pairs_packed_hint")
+        return rec
     _lib.check(L.mpsm_join_pairs_packed(pa, len(priv), ua, len(pub), width_bits, lower, int(bool(swap)), int(mode),
                                         ptr(out), int(cap), ptr(rec), ptr(ws), ws.numel(), stream_ptr()),
                "mpsm_join_pairs_packed")

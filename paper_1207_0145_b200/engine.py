@@ -376,21 +376,20 @@ class JoinContext:
     def _alloc_runs(self, n: int) -> tuple:
         return (self._empty(n), None) if self.packed else (self._empty(n), self._empty(n))
 
-    def _sort_into(self, in_k, in_p, dst: tuple, a: int, b: int, bad) -> tuple:
+    def _sort_into(self, in_k, in_p, dst: tuple, a: int, b: int, bad, dense=None) -> tuple:
         """sort in_k/in_p (length b-a; in_p None: in_k holds packed records)
-        into dst[.][a:b]; returns the run"""
+        into dst[.][a:b]; returns the run.  dense: the sort's density probe
+        of its output (packed layouts)"""
         n = b - a
         tmp = self._tmp(n)
         if in_p is None:
             out = dst[0][a:b]
-            if n:
-                D.sort_records(in_k, self.wbits, out, tmp[0][:n])
+            D.sort_records(in_k, self.wbits, out, tmp[0][:n], dense)
             return (out, None)
         if self.packed:
             out = dst[0][a:b]
-            if n:
-                D.sort_packed(in_k, in_p, self.dom.lower, self.span_m1, self.wbits, out, tmp[0][:n], bad,
-                              self.overflow)
+            D.sort_packed(in_k, in_p, self.dom.lower, self.span_m1, self.wbits, out, tmp[0][:n], bad,
+                          self.overflow, dense)
             return (out, None)
         ok, op = dst[0][a:b], dst[1][a:b]
         if n:
@@ -445,10 +444,10 @@ class JoinContext:
             self.pub_runs.append(run)
             self.stats[i].tuples_sorted_public = b - a
 
-    def _sort_private_range(self, a: int, b: int) -> tuple:
+    def _sort_private_range(self, a: int, b: int, dense=None) -> tuple:
         if self.priv_rec is not None:
-            return self._sort_into(self.priv_rec[a:b], None, self.priv_store, a, b, self.bad_priv)
-        return self._sort_into(self.priv_k[a:b], self.priv_p[a:b], self.priv_store, a, b, self.bad_priv)
+            return self._sort_into(self.priv_rec[a:b], None, self.priv_store, a, b, self.bad_priv, dense)
+        return self._sort_into(self.priv_k[a:b], self.priv_p[a:b], self.priv_store, a, b, self.bad_priv, dense)
 
     def _private_rel(self):
         return self.r if self.roles.private == "r" else self.s
@@ -467,9 +466,12 @@ class JoinContext:
         self.priv_runs = self._sort_segments(self.priv_chunks, self.priv_rec, k, p, self.priv_store, self.bad_priv)
 
     def sort_private_whole(self):
-        """P-MPSM: the whole private input -> one sorted run (cut by partition())."""
+        """P-MPSM: the whole private input -> one sorted run (cut by partition()).
+        Packed: the sort also reports whether its output is dense (consecutive
+        keys, the FK case), which the join then need not read R to decide."""
         self.priv_store = self._store_for(self._private_rel(), self.priv_rec, self.n_priv)
-        self.priv_whole = self._sort_private_range(0, self.n_priv)
+        self.priv_dense = torch.empty(2, dtype=torch.uint32, device=self.dev) if self.packed else None
+        self.priv_whole = self._sort_private_range(0, self.n_priv, self.priv_dense)
 
     def queue_histogram(self):
         """P-MPSM, T > 1, before the private sort is queued: the 2^B bucket
@@ -547,8 +549,10 @@ class JoinContext:
 
     def _join(self, mode: int, out=None, cap: int = 0):
         if self.packed:
+            dense = getattr(self, "priv_dense", None)
+            hint = (dense, self.priv_whole[0]) if dense is not None and self.n_priv > 0 else None
             return D.join_pairs_packed([r[0] for r in self.priv_runs], [r[0] for r in self.pub_runs], self.wbits,
-                                       self.dom.lower, self.roles.swapped, mode, out, cap)
+                                       self.dom.lower, self.roles.swapped, mode, out, cap, hint)
         return D.join_pairs(self.priv_runs, self.pub_runs, self.roles.swapped, mode, out, cap)
 
     def join(self):

@@ -134,8 +134,11 @@ def test_engine_raises_on_unsorted_run(monkeypatch):
     r, s, dom = P.gen_fk(200_000, 800_000, seed=4)
     real = D.sort_records
 
-    def broken(in_rec, width_bits, out_rec, tmp_rec):
-        real(in_rec, width_bits, out_rec, tmp_rec)
+    def broken(in_rec, width_bits, out_rec, tmp_rec, dense=None):
+        # the density probe (if asked for) describes the sort's own output;
+        # the swap below happens after it -- the dense join's check of every
+        # gathered R key must still catch the corrupted private run
+        real(in_rec, width_bits, out_rec, tmp_rec, dense)
         n = out_rec.numel()
         if n > 1000:
             o = out_rec.view(torch.int64)
