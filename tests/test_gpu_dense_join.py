@@ -171,3 +171,49 @@ def test_dense_path_flags_unsorted_public_run():
     flags = rec[:, _lib.PAIR_FLAGS].astype(np.int64)
     assert flags.reshape(2, 2)[:, 1].any() and (flags & _lib.FLAG_UNSORTED).any()
     assert not flags.reshape(2, 2)[:, 0].any()
+
+
+@pytest.mark.parametrize("kind", ["dense", "hole", "dup", "random"])
+def test_sort_density_probe_and_join_hint(kind):
+    """mpsm_sort_packed_dense reports min/max of key - position over its
+    output (equal iff the sorted run is dense); the join with that hint gives
+    the same records as without it, and a private run changed after its sort
+    is flagged by the dense join's key check, never miscounted"""
+    rng = np.random.default_rng(5)
+    n_r, n_s, lower, w = 50_000, 200_000, 1, 27
+    rk = np.arange(lower, lower + n_r, dtype=np.uint64)
+    if kind == "hole":
+        rk[123] = rk[124]  # one key doubled, one missing
+    elif kind == "dup":
+        rk[-1] = rk[-2]
+    elif kind == "random":
+        rk = rng.integers(lower, lower + 4 * n_r, n_r, dtype=np.uint64)
+    rk = rk[rng.permutation(n_r)]
+    rp = rng.integers(0, 1 << 32, n_r, dtype=np.uint64)
+    sk = rng.integers(lower, lower + n_r, n_s, dtype=np.uint64)
+    sp = rng.integers(0, 1 << 32, n_s, dtype=np.uint64)
+
+    def sorted_records(k, p, dense=None):
+        out, tmp = (torch.empty(k.shape[0], dtype=torch.uint64, device=DEV) for _ in range(2))
+        ovf = torch.zeros(1, dtype=torch.int32, device=DEV)
+        D.sort_packed(_dev(k), _dev(p), lower, (1 << w) - 1, w, out, tmp, None, ovf, dense)
+        return out
+
+    dense = torch.empty(2, dtype=torch.uint32, device=DEV)
+    R = sorted_records(rk, rp, dense)
+    S = sorted_records(sk, sp)
+    d = dense.cpu().numpy()
+    assert (d[0] == d[1]) == (kind == "dense"), (kind, d)
+    if kind == "dense":
+        assert int(d[0]) == 0  # key(R[0]) - lower
+    plain = D.join_pairs_packed([R], [S], w, lower, False, _lib.MODE_COUNT)
+    hinted = D.join_pairs_packed([R], [S], w, lower, False, _lib.MODE_COUNT, hint=(dense, R))
+    assert torch.equal(plain, hinted)
+    assert int(hinted[0, _lib.PAIR_FLAGS].item()) == 0
+    if kind == "dense":
+        o = R.view(torch.int64)
+        a = o[1000].clone()
+        o[1000] = o[2000]
+        o[2000] = a  # after the sort: the probe still says dense
+        bad = D.join_pairs_packed([R], [S], w, lower, False, _lib.MODE_COUNT, hint=(dense, R))
+        assert int(bad[0, _lib.PAIR_FLAGS].item()) & _lib.FLAG_UNSORTED
