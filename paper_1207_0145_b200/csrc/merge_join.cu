@@ -1865,12 +1865,9 @@ __global__ void __launch_bounds__(DJ_THREADS, MPSM_DJ_CTAS) k_dense_join(DjArgs 
     uint64_t best = 0, csum = 0;
     int64_t cnt = 0;  // warp-uniform
     bool bad = false;
-    KT vacc = 0;  // OR of (gathered R key ^ S key) over whole chunks: nonzero = a run not dense after all
     uint32_t b0 = 0, b1 = 0, h1 = 0;  // max33 classes of the warp's current pair
     auto flush_regs = [&]() {
         if (acc_j < 0) return;
-        bad |= vacc != 0;
-        vacc = 0;
         {
             const uint64_t cb = h1 ? ((1ull << 32) | b1) : (uint64_t)b0;
             if (cb > best) best = cb;
@@ -2065,7 +2062,7 @@ __global__ void __launch_bounds__(DJ_THREADS, MPSM_DJ_CTAS) k_dense_join(DjArgs 
                     bad |= (prv > kk[0]) | (kk[0] > kk[1]) | (kk[1] > kk[2]) | (kk[2] > kk[3]);
                     // every gathered R tuple must carry the S key (a private
                     // run that is not dense after all: flagged, not miscounted)
-                    vacc |= (nk(rv[0]) ^ kk[0]) | (nk(rv[1]) ^ kk[1]) | (nk(rv[2]) ^ kk[2]) | (nk(rv[3]) ^ kk[3]);
+                    bad |= (nk(rv[0]) != kk[0]) | (nk(rv[1]) != kk[1]) | (nk(rv[2]) != kk[2]) | (nk(rv[3]) != kk[3]);
                     cnt += DJ_CHUNK;
                 } else {
                     const int v0 = k0 + 4 * lane;
@@ -2286,11 +2283,8 @@ __global__ void __launch_bounds__(DF_THREADS, MPSM_DF_MINB) k_dense_flat(DfArgs 
     uint32_t b0m = 0, b1m = 0, h1 = 0;
     int64_t cnt = 0;  // warp-uniform
     bool bad = false;
-    KT vacc = 0;  // OR of (gathered R key ^ S key) over whole steps: nonzero = a run not dense after all
     auto flush = [&]() {
         if (p < 0) return;
-        bad |= vacc != 0;
-        vacc = 0;
         const uint64_t cb = h1 ? ((1ull << 32) | b1m) : (uint64_t)b0m;
         if (cb > best) best = cb;
         const uint32_t lo = (uint32_t)csum, hi = (uint32_t)(csum >> 32);
@@ -2476,7 +2470,7 @@ __global__ void __launch_bounds__(DF_THREADS, MPSM_DF_MINB) k_dense_flat(DfArgs 
                         bad |= (prv > kk[0]) | (kk[0] > kk[1]) | (kk[1] > kk[2]) | (kk[2] > kk[3]);
                     // every gathered R tuple must carry the S key (a private
                     // run that is not dense after all: flagged, not miscounted)
-                    vacc |= (nk(rv[0]) ^ kk[0]) | (nk(rv[1]) ^ kk[1]) | (nk(rv[2]) ^ kk[2]) | (nk(rv[3]) ^ kk[3]);
+                    bad |= (nk(rv[0]) != kk[0]) | (nk(rv[1]) != kk[1]) | (nk(rv[2]) != kk[2]) | (nk(rv[3]) != kk[3]);
                         cnt += 128;
                     } else {
                         const int64_t v0 = base + 4 * lane;
@@ -2593,7 +2587,6 @@ __global__ void __launch_bounds__(DF_THREADS, 4) k_dense_flat1(const mpsm_run_t*
     uint32_t b0m = 0, b1m = 0, h1 = 0;
     int64_t cnt = 0;  // warp-uniform
     bool bad = false;
-    KT vacc = 0;  // OR of (gathered R key ^ S key) over whole steps: nonzero = a run not dense after all
     KT carry = 0;
     if (s0 < s1) {
         const int64_t first = b0 + (s0 << 7);
@@ -2692,7 +2685,7 @@ __global__ void __launch_bounds__(DF_THREADS, 4) k_dense_flat1(const mpsm_run_t*
                 bad |= (prv > kk[0]) | (kk[0] > kk[1]) | (kk[1] > kk[2]) | (kk[2] > kk[3]);
                     // every gathered R tuple must carry the S key (a private
                     // run that is not dense after all: flagged, not miscounted)
-                    vacc |= (nk(rv[0]) ^ kk[0]) | (nk(rv[1]) ^ kk[1]) | (nk(rv[2]) ^ kk[2]) | (nk(rv[3]) ^ kk[3]);
+                    bad |= (nk(rv[0]) != kk[0]) | (nk(rv[1]) != kk[1]) | (nk(rv[2]) != kk[2]) | (nk(rv[3]) != kk[3]);
                 cnt += 128;
             } else {
                 const int64_t v0 = base + 4 * lane;
@@ -2710,7 +2703,6 @@ __global__ void __launch_bounds__(DF_THREADS, 4) k_dense_flat1(const mpsm_run_t*
     };
     if (interior) run(std::true_type{});
     else run(std::false_type{});
-    bad |= vacc != 0;
     {
         const uint64_t cb = h1 ? ((1ull << 32) | b1m) : (uint64_t)b0m;
         if (cb > best) best = cb;
