@@ -74,6 +74,14 @@ const char* mpsm_last_error(void);
 int mpsm_device_init(int device);
 /* number of kernels this library launched (process-wide counter) */
 uint64_t mpsm_launch_count(void);
+/* copy words_a uint64 from src_a then words_b from src_b (device memory) to
+ * host_dst, which must be pinned host memory (cudaHostAlloc / torch
+ * pin_memory), by a kernel on `stream` -- a join's pair records and flags
+ * without a copy-engine hand-off (meant for small results: every word
+ * crosses PCIe as a posted write).  Synchronise the stream before reading
+ * host_dst. */
+int mpsm_fetch_small(void* host_dst, const void* src_a, int64_t words_a, const void* src_b, int64_t words_b,
+                     void* stream);
 /* per-kernel CUDA-event timing: enable (and reset) / read the summed device
  * time and launch count of one kernel family ("seg_scatter", "seg_count",
  * "seg_scatter_sp", "seg_scatter_pp", "merge", "merge_partition", ...) */

@@ -39,7 +39,7 @@ EXPORTS = (
     "mpsm_upload_records", "mpsm_upload_bytes", "mpsm_sort_records", "mpsm_pack_records", "mpsm_partition_records",
     "mpsm_sort_segments_workspace_bytes", "mpsm_sort_pairs_segments", "mpsm_sort_packed_segments",
     "mpsm_sort_records_segments", "mpsm_sort_packed_dense", "mpsm_sort_records_dense",
-    "mpsm_join_pairs_packed_hint",
+    "mpsm_join_pairs_packed_hint", "mpsm_fetch_small",
 )
 
 
@@ -54,6 +54,7 @@ _SIGS = {
     "mpsm_last_error": (ctypes.c_char_p, []),
     "mpsm_device_init": (_int, [_int]),
     "mpsm_launch_count": (_u64, []),
+    "mpsm_fetch_small": (_int, [_vp, _vp, _i64, _vp, _i64, _vp]),
     "mpsm_profile_enable": (_int, [_int]),
     "mpsm_profile_read": (_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_u64)]),
     "mpsm_sort_workspace_bytes": (_int, [_i64, _int, ctypes.POINTER(_sz)]),

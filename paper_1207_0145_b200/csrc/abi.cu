@@ -1,6 +1,7 @@
 // abi.cu -- library-level entry points of the C ABI (include/mpsm_b200.h):
 // version, error reporting, device selection, launch accounting, CUDA IPC.
 
+#include <algorithm>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -93,6 +94,40 @@ extern "C" int mpsm_version(void) { return 1; }
 extern "C" const char* mpsm_last_error(void) { return g_last_error.c_str(); }
 
 extern "C" uint64_t mpsm_launch_count(void) { return launch_counter().load(); }
+
+namespace mpsm {
+// a join's small results (pair records, flags) straight into pinned host
+// memory: a kernel right behind the join's last kernel, where a device ->
+// host copy starts ~12-14 us after it (copy-engine hand-off)
+__global__ void __launch_bounds__(256) k_fetch(uint64_t* __restrict__ dst, const uint64_t* __restrict__ a, int64_t na,
+                                               const uint64_t* __restrict__ b, int64_t nb) {
+    const int64_t step = (int64_t)gridDim.x * blockDim.x, t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t i = t; i < na; i += step) dst[i] = a[i];
+    for (int64_t i = t; i < nb; i += step) dst[na + i] = b[i];
+}
+}  // namespace mpsm
+
+extern "C" int mpsm_fetch_small(void* host_dst, const void* src_a, int64_t words_a, const void* src_b, int64_t words_b,
+                                void* stream) {
+    if (!host_dst || words_a < 0 || words_b < 0 || (words_a && !src_a) || (words_b && !src_b)) {
+        set_error("mpsm_fetch_small: null pointer or negative size");
+        return MPSM_ERR_ARG;
+    }
+    // pinned host memory is device-accessible at its host address (unified
+    // addressing); anything else is refused rather than faulting
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, host_dst) != cudaSuccess || at.type != cudaMemoryTypeHost ||
+        at.devicePointer == nullptr) {
+        cudaGetLastError();
+        set_error("mpsm_fetch_small: destination is not pinned host memory");
+        return MPSM_ERR_ARG;
+    }
+    if (words_a + words_b == 0) return MPSM_OK;
+    const int grid = (int)std::min<int64_t>(1024, (words_a + words_b + 255) / 256);
+    k_fetch<<<grid, 256, 0, (cudaStream_t)stream>>>((uint64_t*)at.devicePointer, (const uint64_t*)src_a, words_a,
+                                                (const uint64_t*)src_b, words_b);
+    return check_launch("k_fetch");
+}
 
 extern "C" int mpsm_device_init(int device) {
     MPSM_TRY(cuda_status(cudaSetDevice(device), "cudaSetDevice"));

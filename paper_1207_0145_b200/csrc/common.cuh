@@ -2,6 +2,8 @@
 #pragma once
 
 #include <cuda_runtime.h>
+
+#include <cstring>
 #include <stdint.h>
 
 #include <atomic>
@@ -228,6 +230,96 @@ __device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
         v = w > v ? w : v;
     }
     return v;
+}
+
+// ------------------------------------------------------------ small puts
+// Host -> device copies of a few hundred bytes (run descriptors, plan arrays,
+// flag resets) issued as the parameters of a one-CTA kernel: behind a kernel
+// it starts ~1 us after it, where a copy-engine transfer or memset starts
+// ~8-10 us after it (torch.profiler timeline of a cfg2 join) -- and a copy
+// from pageable memory needs no staging.  Batches that do not fit fall back
+// to cudaMemcpyAsync / cudaMemsetAsync.
+struct PutBatch {
+    static constexpr int WORDS = 640;  // 2.5 KB of data: well inside the 4 KB parameter space
+    static constexpr int ITEMS = 6;
+    uint32_t data[WORDS];
+    uint32_t* dst[ITEMS];
+    int off[ITEMS];
+    int nw[ITEMS];
+    int n = 0;
+    int used = 0;
+};
+
+// the launch carries only the words in use: a 2.5 KB parameter block starts
+// ~7 us after the kernel before it, a 100-B one ~2.5 us (same timeline)
+template <int WORDS>
+struct PutParams {
+    uint32_t data[WORDS];
+    uint32_t* dst[PutBatch::ITEMS];
+    int off[PutBatch::ITEMS];
+    int nw[PutBatch::ITEMS];
+    int n;
+};
+
+template <int WORDS>
+__global__ void __launch_bounds__(256) k_put(const PutParams<WORDS> b) {
+    for (int i = 0; i < b.n; ++i)
+        for (int w = threadIdx.x; w < b.nw[i]; w += blockDim.x) b.dst[i][w] = b.data[b.off[i] + w];
+}
+
+template <int WORDS>
+inline void put_launch(const PutBatch& b, cudaStream_t st) {
+    PutParams<WORDS> p;
+    std::memcpy(p.data, b.data, sizeof(uint32_t) * b.used);
+    for (int i = 0; i < b.n; ++i) {
+        p.dst[i] = b.dst[i];
+        p.off[i] = b.off[i];
+        p.nw[i] = b.nw[i];
+    }
+    p.n = b.n;
+    static bool carve = [] {
+        // the same shared-memory carveout as the sort kernels it runs between
+        // (no L1 / shared reconfiguration of the SMs around it)
+        cudaFuncSetAttribute(k_put<WORDS>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        return true;
+    }();
+    (void)carve;
+    k_put<WORDS><<<1, 256, 0, st>>>(p);
+}
+
+// queue `bytes` (a multiple of 4) from host memory for dst; src == nullptr:
+// zeros; v != 0: fill every word with v.  false: no room (caller copies)
+inline bool put_add(PutBatch& b, void* dst, const void* src, size_t bytes, uint32_t v = 0) {
+    const int nw = (int)(bytes / 4);
+    if (bytes % 4 || b.n == PutBatch::ITEMS || b.used + nw > PutBatch::WORDS) return false;
+    if (src) std::memcpy(b.data + b.used, src, bytes);
+    else
+        for (int w = 0; w < nw; ++w) b.data[b.used + w] = v;
+    b.dst[b.n] = (uint32_t*)dst;
+    b.off[b.n] = b.used;
+    b.nw[b.n] = nw;
+    ++b.n;
+    b.used += nw;
+    return true;
+}
+
+inline int put_flush(PutBatch& b, cudaStream_t st) {
+    if (b.n == 0) return 0;
+    if (b.used <= 32) put_launch<32>(b, st);
+    else if (b.used <= 160) put_launch<160>(b, st);
+    else put_launch<PutBatch::WORDS>(b, st);
+    b.n = b.used = 0;
+    return check_launch("k_put");
+}
+
+// copy (or with src == nullptr zero / fill) through the batch, or directly
+// when it is full
+inline int put_or_copy(PutBatch& b, void* dst, const void* src, size_t bytes, cudaStream_t st, uint32_t v = 0) {
+    if (bytes == 0 || put_add(b, dst, src, bytes, v)) return 0;
+    if (src) return cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st), "h2d");
+    if (v == 0 || v == 0xffffffffu || v == 0x01010101u)
+        return cuda_status(cudaMemsetAsync(dst, (int)(v & 0xff), bytes, st), "memset");
+    return -1;
 }
 
 }  // namespace mpsm

@@ -2885,14 +2885,18 @@ static int join_pairs_impl(const mpsm_run_t* priv, int n_priv, const mpsm_run_t*
     DjWs dw{};
     const bool dense = PK && dp.on && (mode != MPSM_MODE_MATERIALIZE || d_out == nullptr) &&
                        carve_dj(cv, n_priv, n_pub, dp, &dw);
-    MPSM_TRY(cuda_status(cudaMemcpyAsync(w.d_priv, priv, sizeof(mpsm_run_t) * n_priv, cudaMemcpyHostToDevice, st), "h2d"));
-    MPSM_TRY(cuda_status(cudaMemcpyAsync(w.d_pub, pub, sizeof(mpsm_run_t) * n_pub, cudaMemcpyHostToDevice, st), "h2d"));
+    // the run descriptors (and the dense plan's block bases and flags) as
+    // one small-put kernel when they fit its parameters
+    PutBatch pb;
+    MPSM_TRY(put_or_copy(pb, w.d_priv, priv, sizeof(mpsm_run_t) * n_priv, st));
+    MPSM_TRY(put_or_copy(pb, w.d_pub, pub, sizeof(mpsm_run_t) * n_pub, st));
     DjArgs da{};
     if (dense) {
-        MPSM_TRY(cuda_status(cudaMemcpyAsync(dw.blk_base, dp.blk_base.data(), sizeof(int64_t) * (n_priv + 1),
-                                             cudaMemcpyHostToDevice, st),
-                             "h2d"));
-        MPSM_TRY(cuda_status(cudaMemsetAsync(dw.nondense, 0, sizeof(uint32_t) * n_priv, st), "memset"));
+        MPSM_TRY(put_or_copy(pb, dw.blk_base, dp.blk_base.data(), sizeof(int64_t) * (n_priv + 1), st));
+        MPSM_TRY(put_or_copy(pb, dw.nondense, nullptr, sizeof(uint32_t) * n_priv, st));
+    }
+    MPSM_TRY(put_flush(pb, st));
+    if (dense) {
         da = DjArgs{w.d_priv, w.d_pub, n_priv,   n_pub,   dp.K,      dp.nent,   dw.nondense, dw.kb,     dw.blk_base,
                     w.win,    dw.L,    dw.tb,    dw.nsub, dw.part,   dw.tiles,  dw.ntiles,   d_pairs,   pi};
         ProfScope ps("dense_check", st);

@@ -1367,8 +1367,10 @@ static int sort_pairs_impl(const uint64_t* in_keys, const uint64_t* in_pays, int
 // mpsm_sort_packed_dense); set to "unknown" (min > max) where it cannot run
 static int dense_init(uint32_t* d_dense, bool probe, cudaStream_t st) {
     if (!d_dense) return MPSM_OK;
-    MPSM_TRY(cuda_status(cudaMemsetAsync(d_dense, probe ? 0xff : 0x01, sizeof(uint32_t), st), "memset"));
-    return cuda_status(cudaMemsetAsync(d_dense + 1, 0, sizeof(uint32_t), st), "memset");
+    const uint32_t init[2] = {probe ? 0xffffffffu : 0x01010101u, 0u};
+    PutBatch pb;  // a kernel, not two memsets: see PutBatch
+    MPSM_TRY(put_or_copy(pb, d_dense, init, sizeof(init), st));
+    return put_flush(pb, st);
 }
 
 static int sort_packed_impl(const uint64_t* in_keys, const uint64_t* in_pays, int64_t n, int nseg,

@@ -24,8 +24,15 @@ _init_lock = threading.Lock()
 _inited = {}
 
 
+_READY: dict = {}  # device index -> torch.device, once initialised
+
+
 def ensure_device(device: Optional[torch.device] = None) -> torch.device:
     """Select the CUDA device and verify it is a B200 (sm_100).  Raises if none."""
+    if device is None and _READY:  # per-join fast path: the current device, already initialised
+        d = _READY.get(torch.cuda.current_device())
+        if d is not None:
+            return d
     if not torch.cuda.is_available():
         raise RuntimeError("paper_1207_0145_b200 needs a CUDA device (B200); none is visible and there is no CPU path")
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
@@ -39,6 +46,7 @@ def ensure_device(device: Optional[torch.device] = None) -> torch.device:
             if rc < 0:
                 _lib.check(rc, "mpsm_device_init")
             _inited[dev.index] = rc
+            _READY[dev.index] = dev
     return dev
 
 
@@ -76,9 +84,42 @@ def workspace(device: torch.device) -> Workspace:
     return _ws[device.index]
 
 
+_WS_BYTES: dict = {}
+
+
+def _sort_ws_bytes(n: int, width_bits: int) -> int:
+    """mpsm_sort_workspace_bytes, memoised (a per-join ctypes round trip)"""
+    key = (n, width_bits)
+    v = _WS_BYTES.get(key)
+    if v is None:
+        sz = ctypes.c_size_t(0)
+        _lib.check(_lib.load().mpsm_sort_workspace_bytes(n, width_bits, ctypes.byref(sz)), "sort workspace")
+        v = int(sz.value)
+        if len(_WS_BYTES) > 256:
+            _WS_BYTES.clear()
+        _WS_BYTES[key] = v
+    return v
+
+
 def new_bad_flag(device: torch.device) -> torch.Tensor:
     """int64[1] = -1 (all ones == UINT64_MAX: no out-of-domain key seen)."""
     return torch.full((1,), -1, dtype=I64, device=device)
+
+
+_FLAGS_INIT = None
+
+
+def new_join_flags(device: torch.device) -> torch.Tensor:
+    """int64[3] = (-1, -1, 0): the public and private sides' out-of-domain
+    flags (as new_bad_flag) and the payload-overflow flag (an int32 in the low
+    half of the last word), set by one copy from a pinned template -- the
+    per-join flags without a kernel launch each."""
+    global _FLAGS_INIT
+    if _FLAGS_INIT is None:
+        _FLAGS_INIT = torch.tensor([-1, -1, 0], dtype=I64).pin_memory()
+    f = torch.empty(3, dtype=I64, device=device)
+    f.copy_(_FLAGS_INIT, non_blocking=True)
+    return f
 
 
 # ---------------------------------------------------------------- operators
@@ -111,9 +152,7 @@ def sort_packed(in_k: torch.Tensor, in_p: torch.Tensor, lower: int, span_m1: int
         if dense is not None:
             dense.copy_(torch.tensor([1, 0], dtype=torch.int32).view(torch.uint32))
         return
-    sz = ctypes.c_size_t(0)
-    _lib.check(L.mpsm_sort_workspace_bytes(n, width_bits, ctypes.byref(sz)), "sort workspace")
-    ws = workspace(in_k.device).get(sz.value)
+    ws = workspace(in_k.device).get(_sort_ws_bytes(n, width_bits))
     if dense is not None:
         _lib.check(L.mpsm_sort_packed_dense(ptr(in_k), ptr(in_p), n, lower, span_m1, width_bits, ptr(out_rec),
                                             ptr(tmp_rec), ptr(ws), ws.numel(), ptr(bad), ptr(overflow), ptr(dense),
@@ -133,9 +172,7 @@ def sort_records(in_rec: torch.Tensor, width_bits: int, out_rec: torch.Tensor, t
         if dense is not None:
             dense.copy_(torch.tensor([1, 0], dtype=torch.int32).view(torch.uint32))
         return
-    sz = ctypes.c_size_t(0)
-    _lib.check(L.mpsm_sort_workspace_bytes(n, width_bits, ctypes.byref(sz)), "sort workspace")
-    ws = workspace(in_rec.device).get(sz.value)
+    ws = workspace(in_rec.device).get(_sort_ws_bytes(n, width_bits))
     if dense is not None:
         _lib.check(L.mpsm_sort_records_dense(ptr(in_rec), n, width_bits, ptr(out_rec), ptr(tmp_rec), ptr(ws),
                                              ws.numel(), ptr(dense), stream_ptr()), "mpsm_sort_records_dense")

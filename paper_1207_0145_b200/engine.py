@@ -33,6 +33,7 @@ Per phase, device work only (csrc/):
 from __future__ import annotations
 
 import os
+import threading
 import time
 from dataclasses import dataclass
 from typing import Callable, Optional
@@ -163,14 +164,32 @@ def merge_join(r_run: Run, s_run: Run, s_start: int, emit: Callable[[int, int], 
 
 # ----------------------------------------------------------------- engine
 
+_EV_POOL = threading.local()  # per thread and device: timing events reused join after join
+
+
 class _Timeline:
-    """CUDA events at phase boundaries (engine.py:421-432 keys)."""
+    """CUDA events at phase boundaries (engine.py:421-432 keys).  The events
+    come from a per-thread pool (creating one costs as much host time as a
+    kernel launch, and a join's first launch waits behind it); a join reads
+    its timings before it returns, so the next join of the thread may reuse
+    them."""
 
     def __init__(self):
         self.ev = {}
+        pools = getattr(_EV_POOL, "pools", None)
+        if pools is None:
+            pools = _EV_POOL.pools = {}
+        dev = torch.cuda.current_device()
+        self.pool = pools.setdefault(dev, [])
+        self.used = 0
 
     def mark(self, name: str) -> None:
-        e = torch.cuda.Event(enable_timing=True)
+        if self.used < len(self.pool):
+            e = self.pool[self.used]
+        else:
+            e = torch.cuda.Event(enable_timing=True)
+            self.pool.append(e)
+        self.used += 1
         e.record()
         self.ev[name] = e
 
@@ -237,6 +256,33 @@ def _bound_positions_device(chunks, f: int, t: int, dev) -> Optional[torch.Tenso
     return pos
 
 
+_PASSES: dict = {}
+
+
+def _pass_count(width_bits: int) -> int:
+    v = _PASSES.get(width_bits)
+    if v is None:
+        v = _PASSES[width_bits] = int(_lib.load().mpsm_sort_pass_count(width_bits))
+    return v
+
+
+_STATUS_BUF: dict = {}
+
+
+def _pinned_status(n: int) -> torch.Tensor:
+    """pinned int64[n] for fetch_status, reused across joins (read back and
+    copied out before the next join of the thread can write it)"""
+
+    key = threading.get_ident()
+    h = _STATUS_BUF.get(key)
+    if h is None or h.numel() < n:
+        h = torch.empty(max(n, 64), dtype=torch.int64, pin_memory=True)
+        if len(_STATUS_BUF) > 64:
+            _STATUS_BUF.clear()
+        _STATUS_BUF[key] = h
+    return h[:n]
+
+
 class _PackOverflow(Exception):
     """a payload does not fit the packed record: rerun on (key, payload) pairs"""
 
@@ -276,7 +322,7 @@ class JoinContext:
                     raise ConfigurationError("PackedRelation inputs need the packed record layout (MPSM_PACK=1)")
         # record inputs sorted in place (even pass count: the last pass lands
         # back in the input buffer)
-        self._inplace = _lib.load().mpsm_sort_pass_count(self.wbits) % 2 == 0
+        self._inplace = _pass_count(self.wbits) % 2 == 0
         self.pw = 64 - self.wbits
         self.span_m1 = self.dom.upper - self.dom.lower - 1
         # the private side is sorted whole (P-MPSM) or per chunk (B-MPSM);
@@ -303,9 +349,11 @@ class JoinContext:
         self.pub_chunks = chunk_bounds(self.n_pub, self.t)
         self.priv_chunks = chunk_bounds(self.n_priv, self.t)
         self.stats = [WorkerStats(i) for i in range(self.t)]
-        self.bad_pub = D.new_bad_flag(self.dev)
-        self.bad_priv = D.new_bad_flag(self.dev)
-        self.overflow = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        # the two sides' domain flags and the payload-overflow flag in one
+        # int64[3] (one copy; fetch_status reads them back with one copy)
+        self.flags = D.new_join_flags(self.dev)
+        self.bad_pub, self.bad_priv = self.flags[0:1], self.flags[1:2]
+        self.overflow = self.flags[2:3].view(torch.int32)[0:1]
         self.tmp = []
         self.tl = _Timeline()
 
@@ -350,15 +398,15 @@ class JoinContext:
         flags (domain, payload width) into pinned host memory, one stream
         synchronisation for all of them"""
         n = int(self.rec.numel())
-        h = torch.empty(n + 3, dtype=torch.int64, pin_memory=True)
-        h[:n].copy_(self.rec.view(torch.int64).view(-1), non_blocking=True)
-        h[n:n + 1].copy_(self.bad_priv, non_blocking=True)
-        h[n + 1:n + 2].copy_(self.bad_pub, non_blocking=True)
-        h[n + 2:n + 3].copy_(self.overflow.to(torch.int64), non_blocking=True)
+        h = _pinned_status(n + 3)
+        # one kernel writes both into the pinned buffer (mpsm_fetch_small):
+        # bad_pub, bad_priv, overflow (low half) after the pair records
+        _lib.check(_lib.load().mpsm_fetch_small(h.data_ptr(), self.rec.data_ptr(), n, self.flags.data_ptr(), 3,
+                                                D.stream_ptr()), "mpsm_fetch_small")
         torch.cuda.current_stream().synchronize()
         v = h.numpy()
-        self._rec_host = v[:n].view(np.uint64)
-        self._status = (int(v[n + 2]), int(v[n]), int(v[n + 1]))  # overflow, bad_priv, bad_pub
+        self._rec_host = v[:n].view(np.uint64).copy()
+        self._status = (int(v[n + 2]) & 0xFFFFFFFF, int(v[n + 1]), int(v[n]))  # overflow, bad_priv, bad_pub
 
     def _hook(self, i: int, phase: str) -> None:
         if self.hook:
