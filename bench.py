@@ -238,6 +238,8 @@ def impl_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
+    if ws > 1:
+        return impl_reference_dist(args, ws)
     t_gen = time.perf_counter()
     r, s, dom = make_inputs(args.config)
     log(f"[bench-ref] generated {args.config} in {time.perf_counter() - t_gen:.1f}s")
@@ -262,6 +264,55 @@ def impl_reference(args):
                    "matches_golden": None if golden is None else tuple(res) == golden[:2]},
         "cpu_baseline": dict(ref.describe(f"{args.steps} timed joins after {args.warmup} warm-up joins"),
                              value=val, unit="tuples/s"),
+        "e2e": {"value": val, "unit": "tuples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def impl_reference_dist(args, ws: int):
+    """--impl reference under torchrun (N > 1): our arm runs a DIST_CONFIGS
+    workload (cfg5 by default) that no single host holds or finishes in
+    minutes, so the reference joins a bounded sample of it -- the same
+    generator family at 100M x 400M tuples (cfg5 / 16, cfg4 / 4, one GPU's
+    share of weak-scaled cfg2) -- one join per step on rank 0's host cores;
+    `config` is our arm's, the sample is named in cpu_baseline.sample."""
+    from paper_1207_0145_b200 import datagen
+    from paper_1207_0145_b200.core import KeyDomain
+    from paper_1207_0145_b200.distributed import dist_workload
+
+    name = args.dist_config or "cfg5"
+    config, _, n_r, n_s, kind, scaling = dist_workload(name, ws)
+    sn_r, sn_s = 100_000_000, 400_000_000
+    if os.environ.get("MPSM_BENCH_REF_SAMPLE"):  # "n_r,n_s": a smaller sample (CPU tests of this arm)
+        sn_r, sn_s = (int(v) for v in os.environ["MPSM_BENCH_REF_SAMPLE"].split(","))
+    t_gen = time.perf_counter()
+    if kind == "fk":
+        r, s, dom = datagen.gen_fk(sn_r, sn_s, 0)
+    else:
+        dom = KeyDomain(1, 1 << 32)
+        r, s = datagen.gen_negcorr(sn_r, sn_s, dom, 0)
+    log(f"[bench-ref] generated the {name} sample in {time.perf_counter() - t_gen:.1f}s")
+    ref = ReferenceCPU(r, s, dom)
+    res = None
+    for _ in range(args.warmup):
+        _, res = ref.step()
+    times = []
+    for _ in range(args.steps):
+        dt, res = ref.step()
+        times.append(dt)
+    total = sum(times)
+    val = args.steps * ref.n / total
+    sample = (f"a bounded sample of the workload: the same generator at |R|={sn_r:,} |S|={sn_s:,} "
+              f"(1/{n_r // sn_r} of {name}'s {n_r + n_s:,} tuples, key domain [{dom.lower}, {dom.upper})), "
+              f"p-mpsm run_join, threads={ref.t}, {args.steps} timed joins after {args.warmup} warm-up joins")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "tuples/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": scaling, "vs_baseline": None, "dtype": "u64", "data": "synthetic (numpy PCG64 seed 0)",
+        "config": config,
+        "engine": {"impl": f"reference run_join ({ref.kind}, CPU)", "threads": ref.t},
+        "result": {"match_count": res[0], "aggregate_max": res[1], "of": "the sample"},
+        "cpu_baseline": {"kind": ref.kind, "cores": ref.t, "sample": sample, "value": val, "unit": "tuples/s"},
         "e2e": {"value": val, "unit": "tuples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

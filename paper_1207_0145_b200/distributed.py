@@ -626,6 +626,24 @@ DIST_CONFIGS = {
 }
 
 
+def dist_workload(name: str, G: int) -> tuple:
+    """(config dict, KeyDomain, n_r, n_s, kind, scaling) of a DIST_CONFIGS
+    workload over G GPUs -- the description both bench arms print (ours and
+    the --impl reference arm's bounded sample of the same workload)."""
+    from .core import KeyDomain
+
+    n_r, n_s, kind, scaling = DIST_CONFIGS[name]
+    if scaling == "weak":
+        n_r, n_s = n_r * G, n_s * G
+    dom = KeyDomain(1, n_r + 1) if kind == "fk" else KeyDomain(1, 1 << 32)
+    config = {"workload": f"{name}: |R|={n_r:,} |S|={n_s:,} "
+                          + ("FK join" if kind == "fk" else "negatively correlated 80-20 skew join")
+                          + f" sharded by position over {G} GPUs",
+              "algorithm": "p-mpsm", "key_domain": [dom.lower, dom.upper],
+              "l2": "inputs >> L2 (no flush needed)"}
+    return config, dom, n_r, n_s, kind, scaling
+
+
 def _dist_inputs(name: str, G: int, me: int, dev):
     """this rank's position shards of a DIST_CONFIGS workload (counter-based,
     generated on the device chunk by chunk) -> (R, S, KeyDomain, n_r, n_s)"""
@@ -765,11 +783,7 @@ def bench_main(args, metric, Clocks):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (counter-based generators on device, seed 0)",
-            "config": {"workload": f"{name}: |R|={n_r:,} |S|={n_s:,} "
-                                   + ("FK join" if kind == "fk" else "negatively correlated 80-20 skew join")
-                                   + f" sharded by position over {G} GPUs",
-                       "algorithm": "p-mpsm", "key_domain": [dom.lower, dom.upper],
-                       "l2": "inputs >> L2 (no flush needed)"},
+            "config": dist_workload(name, G)[0],
             "engine": {"impl": "paper_1207_0145_b200.distributed (NCCL all-to-all of R, NVLink peer reads of "
                                "S runs)", "threads": G, "parallelism": f"dp{G}"},
             "result": {"match_count": got[0], "aggregate_max": got[1], "checksum": hex(got[2]),

@@ -190,3 +190,31 @@ def test_reference_suite_staging(tmp_path):
     assert ref_suite.prepare(src)
     assert os.path.exists(os.path.join(ref_suite.DST, "conftest.py"))
     assert len([f for f in os.listdir(ref_suite.DST) if f.startswith("test_")]) >= 5
+
+
+def test_reference_arm_under_torchrun_prints_the_distributed_config():
+    """bench.py --impl reference with WORLD_SIZE > 1: rank 0 alone joins a
+    bounded sample of the distributed workload on the host and prints the
+    distributed arm's `config`; the other ranks exit 0 without output."""
+    import json
+    import subprocess
+    import sys
+
+    from paper_1207_0145_b200.distributed import dist_workload
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if not (os.path.isdir(os.path.join(root, "oracle", "_ref", "mpsm")) or
+            os.path.exists(os.path.join(root, "oracle", "liboracle.so"))):
+        pytest.skip("neither the reference install nor the oracle is built")
+    cmd = [sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "2", "--steps", "1",
+           "--warmup", "1"]
+    base = dict(os.environ, WORLD_SIZE="2", LOCAL_RANK="0", MPSM_BENCH_REF_SAMPLE="20000,80000")
+    out0 = subprocess.run(cmd, env=dict(base, RANK="0"), capture_output=True, text=True, timeout=600)
+    assert out0.returncode == 0, out0.stderr[-2000:]
+    line = json.loads([x for x in out0.stdout.splitlines() if x.startswith("{")][-1])
+    config, _, n_r, n_s, _, scaling = dist_workload("cfg5", 2)
+    assert line["impl"] == "reference" and line["config"] == config and line["scaling"] == scaling
+    assert line["n_gpus"] == 2 and line["result"]["match_count"] == 80000
+    assert "bounded sample" in line["cpu_baseline"]["sample"] and line["e2e"]["h2d_bytes_per_step"] == 0
+    out1 = subprocess.run(cmd, env=dict(base, RANK="1", LOCAL_RANK="1"), capture_output=True, text=True, timeout=600)
+    assert out1.returncode == 0 and not [x for x in out1.stdout.splitlines() if x.startswith("{")]
