@@ -6,6 +6,8 @@
 
 #include <sched.h>
 
+#include <cstdlib>
+
 #include <thread>
 
 namespace mpsm {
@@ -20,6 +22,16 @@ inline int usable_cores() {
         if (n <= 0) n = 1;
     }
     return n;
+}
+
+// cores per process when a launcher runs one process per GPU on this node
+// (torchrun exports LOCAL_WORLD_SIZE): the ranks share the host's cores
+inline int usable_cores_per_rank() {
+    int n = usable_cores();
+    const char* e = getenv("LOCAL_WORLD_SIZE");
+    const int lws = e ? atoi(e) : 1;
+    if (lws > 1) n = (n + lws - 1) / lws;
+    return n < 1 ? 1 : n;
 }
 
 }  // namespace mpsm

@@ -114,8 +114,8 @@ struct Uploader {
             // leave the issuing thread a core
             // the copy is host-memory-bandwidth bound: 3/4 of the cores pack
             // (measured best on the 16-core GPU box: 12 -> 113 ms, 16 -> 121 ms
-            // for cfg2's 500M tuples)
-            threads = e ? atoi(e) : std::max(1, usable_cores() * 3 / 4);
+            // for cfg2's 500M tuples); one process per GPU: a rank's share of the cores
+            threads = e ? atoi(e) : std::max(1, usable_cores_per_rank() * 3 / 4);
         }
         nslots = 2 * threads;
         slot.resize(nslots);
