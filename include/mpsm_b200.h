@@ -289,7 +289,10 @@ int mpsm_deinterleave(const uint64_t* d_records, int64_t n, uint64_t* d_keys, ui
  * buffers have been read.  The copies start after the work queued on
  * `stream` before `ready_event` (a cudaEvent_t recorded when d_rec was
  * allocated; NULL: after all work queued on `stream` so far), so work queued
- * later overlaps the upload.  Not thread-safe (one uploader per process). */
+ * later overlaps the upload.  threads <= 0: MPSM_UPLOAD_THREADS, else 3/4 of
+ * the cores this process may run on, divided by LOCAL_WORLD_SIZE when a
+ * launcher runs one process per GPU.  Not thread-safe (one uploader per
+ * process). */
 int mpsm_upload_records(const uint64_t* h_keys, const uint64_t* h_pays, int64_t n, uint64_t lower,
                         uint64_t span_m1, int width_bits, uint64_t* d_rec, int threads, int gpu_pack_every,
                         void* stream, void* ready_event, int64_t* bad_index, int* overflow);
